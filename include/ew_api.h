@@ -1,0 +1,295 @@
+/* ew_api.h — C ABI of libelaskit_b200.so, the B200 build of ElasWave's
+ * per-step data-parallel recovery path.
+ *
+ * The reference (proj/include/elaskit) is a C++ library with no FFI layer;
+ * its C++ headers stay the primary API (the include/elaskit headers, implemented in
+ * the same .so).  This header is what a foreign caller (ctypes, cgo, JNI) or
+ * a C++ executor binds: plain pointers and sizes, integer status codes, no
+ * exceptions and no torch types.  Each planning entry point names the
+ * reference function it wraps; the device entry points execute what the
+ * reference only models (SURVEY §2 "Modelled transfer" table).
+ *
+ * Conventions
+ *   - Every function returns EW_OK (0) or an ew_status; ew_last_error() gives
+ *     the message.  Status codes map 1:1 onto the reference's exception types
+ *     (elaskit/device.hpp rethrows them).
+ *   - Device pointers are caller-owned and live on the CUDA device current on
+ *     the calling thread.  ew_stream_t is a cudaStream_t (NULL = default).
+ *   - Device calls are asynchronous on the given stream unless stated.
+ */
+#ifndef EW_API_H
+#define EW_API_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st* ew_stream_t;
+
+enum ew_status {
+  EW_OK = 0,
+  EW_ERR_INVALID_ARGUMENT = 1,   /* std::invalid_argument            */
+  EW_ERR_COVERAGE_MISMATCH = 2,  /* elaskit::CoverageMismatch        */
+  EW_ERR_MISSING_BACKUP = 3,     /* elaskit::MissingBackup           */
+  EW_ERR_NO_SURVIVORS = 4,       /* elaskit::NoSurvivors             */
+  EW_ERR_DIMENSION_MISMATCH = 5, /* elaskit::DimensionMismatch       */
+  EW_ERR_MISMATCHED_DP = 6,      /* elaskit::MismatchedDpDegree      */
+  EW_ERR_DISCONNECTED = 7,       /* elaskit::DisconnectedGroup       */
+  EW_ERR_OUT_OF_RANGE = 8,       /* std::out_of_range                */
+  EW_ERR_CAPACITY = 9,           /* output buffer too small          */
+  EW_ERR_CUDA = 10,
+  EW_ERR_NCCL = 11,
+  EW_ERR_INTERNAL = 12
+};
+
+const char* ew_last_error(void);
+const char* ew_version(void);
+
+/* ------------------------------------------------------------------------
+ * Layouts — PartitionLayout (reference param_fabric.hpp:27-33)
+ * ---------------------------------------------------------------------- */
+typedef struct ew_layout ew_layout;
+
+typedef struct ew_interval {
+  int64_t lo, hi; /* half-open */
+} ew_interval;
+
+/* One interval of a rank's packed shard buffer (elaskit/b200.hpp Segment). */
+typedef struct ew_segment {
+  int64_t global_lo, length, local_off;
+} ew_segment;
+
+/* Interleaved ZeRO over `ranks` (ZeroLayout::shard, migration.cpp:73-77,
+ * composed per SURVEY §8(a) A4). */
+int ew_layout_interleaved(const int64_t* layer_bytes, int n_layers, const int* ranks,
+                          int n_ranks, ew_layout** out);
+/* contiguous_layout (param_fabric.cpp:36-49) */
+int ew_layout_contiguous(const int* ranks, int n_ranks, int64_t total, ew_layout** out);
+/* Arbitrary layout: rank ranks[i] gets counts[i] consecutive entries of ivs. */
+int ew_layout_from_intervals(const int* ranks, const int* counts, int n_ranks,
+                             const ew_interval* ivs, int64_t total, ew_layout** out);
+void ew_layout_free(ew_layout* layout);
+int64_t ew_layout_total_bytes(const ew_layout* layout);
+int ew_layout_num_ranks(const ew_layout* layout);
+int ew_layout_ranks(const ew_layout* layout, int* out, int cap);
+int64_t ew_layout_shard_bytes(const ew_layout* layout, int rank);
+int64_t ew_layout_num_segments(const ew_layout* layout, int rank);
+int ew_layout_segments(const ew_layout* layout, int rank, ew_segment* out, int64_t cap);
+/* PartitionLayout::validate (param_fabric.cpp:14-34) */
+int ew_layout_validate(const ew_layout* layout);
+/* PartitionLayout::owner_of (param_fabric.cpp:7-12); -1 if uncovered */
+int ew_layout_owner_of(const ew_layout* layout, int64_t byte);
+
+/* integrity_check (param_fabric.cpp:66-80).  *recoverable = 0/1; the failed
+ * ranks whose holder also failed are written to missing_ranks. */
+int ew_integrity_check(const int* ring_members, int n_ring, const ew_layout* layout,
+                       const int* failed, int n_failed, int* recoverable, int* missing_ranks,
+                       int missing_cap, int* n_missing);
+
+/* ------------------------------------------------------------------------
+ * Transfer plans — overlap_matrix (param_fabric.cpp:82-121)
+ * ---------------------------------------------------------------------- */
+typedef struct ew_plan ew_plan;
+
+enum { EW_MEDIUM_D2D = 0, EW_MEDIUM_H2D_D2D = 1 };
+
+typedef struct ew_transfer_entry {
+  int32_t src_rank, dst_rank;
+  int64_t lo, hi;
+  int32_t medium, reserved;
+} ew_transfer_entry;
+
+/* n_ring == 0 passes ring = nullptr, like the reference default argument. */
+int ew_overlap_matrix(const ew_layout* src, const ew_layout* dst, const int* failed,
+                      int n_failed, const int* ring_members, int n_ring, ew_plan** out);
+void ew_plan_free(ew_plan* plan);
+int64_t ew_plan_num_entries(const ew_plan* plan);
+int64_t ew_plan_total_bytes_moved(const ew_plan* plan);
+int ew_plan_entries(const ew_plan* plan, ew_transfer_entry* out, int64_t cap);
+/* plan_to_json (param_fabric.cpp:123-134), compact dump, NUL-terminated. */
+int ew_plan_to_json(const ew_plan* plan, char* buf, int64_t cap, int64_t* needed);
+
+enum { EW_ROLE_OLD = 0, EW_ROLE_REPLICA = 1, EW_ROLE_NEW = 2 };
+
+typedef struct ew_copy_desc {
+  int32_t src_role, src_rank, dst_role, dst_rank;
+  int64_t src_off, dst_off, bytes;
+} ew_copy_desc;
+
+/* Lower a plan to the copies GPU `exec_rank` issues (b200.hpp reshard_copies).
+ * push != 0: copies sourced on exec_rank; push == 0: copies landing there.
+ * Writes min(n, cap) descriptors and *n_out = n (EW_ERR_CAPACITY if n > cap). */
+int ew_reshard_copies(const ew_plan* plan, const ew_layout* src, const ew_layout* dst,
+                      const int* failed, int n_failed, const int* ring_members, int n_ring,
+                      int exec_rank, int push, ew_copy_desc* out, int64_t cap, int64_t* n_out);
+
+/* ------------------------------------------------------------------------
+ * Host planners of the other hot-path modules
+ * ---------------------------------------------------------------------- */
+/* reshard_microbatches (dataflow.cpp:52-69): out arrays hold n_survivors. */
+int ew_reshard_microbatches(const int* old_per_slot_mbs, int n_old, int num_microbatches,
+                            const int* survivors, int n_survivors, int* out_slots,
+                            int* out_per_slot_mbs);
+/* weighted_grad_average (dataflow.cpp:71-83), fp64, grads row-major [n][dim] */
+int ew_weighted_grad_average(const double* weights, const double* grads, int n, int64_t dim,
+                             double* out);
+/* philox4x64 (rng.cpp:25-36) and draw (rng.cpp:38-53) */
+int ew_philox4x64(const uint64_t counter[4], const uint64_t key[2], uint64_t out[4]);
+int ew_draw(uint64_t seed, uint64_t sample_id, uint32_t layer_id, uint32_t op_index, int n,
+            double* out);
+
+/* plan_edit (communicator.cpp:54-105).  Groups are given as flat member
+ * lists; topo[i] 0 = Mesh, 1 = Ring; ids are NUL-terminated strings.  Links
+ * are (lo,hi) pairs.  Outputs are truncated at their caps (EW_ERR_CAPACITY). */
+int ew_plan_edit(int n_groups, const char* const* ids, const int* topo, const int* n_members,
+                 const int* members, int event_kind, const int* targets, int n_targets,
+                 const int* pool_links, int n_pool, int* add_links, int add_cap, int* n_add,
+                 int* remove_links, int remove_cap, int* n_remove, int* touched_groups,
+                 int* n_touched);
+
+/* ------------------------------------------------------------------------
+ * Device memory and peer mappings (B200 "links": CUDA IPC over NVSwitch)
+ * ---------------------------------------------------------------------- */
+int ew_device_count(int* n);
+int ew_set_device(int device);
+int ew_alloc(int64_t bytes, void** out); /* cudaMalloc, 256-B aligned, current device */
+int ew_free(void* ptr);
+int ew_memset_async(void* ptr, int value, int64_t bytes, ew_stream_t stream);
+int ew_memcpy_async(void* dst, const void* src, int64_t bytes, ew_stream_t stream);
+int ew_stream_sync(ew_stream_t stream);
+int ew_device_sync(void);
+/* 64-byte cudaIpcMemHandle of the allocation holding ptr + ptr's offset. */
+int ew_ipc_get_handle(const void* ptr, void* handle64, int64_t* offset);
+int ew_ipc_open(const void* handle64, int64_t offset, void** out);
+int ew_ipc_close(void* ptr);
+
+/* ------------------------------------------------------------------------
+ * (a) Snapshot + per-block checksum, verification
+ *
+ * Checksum spec (builder-defined; the reference has none — parity unpinned,
+ * see oracle/ew_oracle.c): the flat byte space is cut into blocks of
+ * block_bytes (power of two, 4 KiB..1 MiB).  For global little-endian u64
+ * word i (bytes [8i, 8i+8)) with the bytes a buffer does not hold read as 0,
+ *     s0(b) = sum w_i,  s1(b) = sum (i+1) * w_i   (mod 2^64)
+ * over the words of block b.  A "row" is (segment, block) and carries the
+ * partial sums of the bytes of that segment inside that block; rows of all
+ * ranks add up (mod 2^64) to the block sums of the whole space, for any
+ * layout — reshard verification needs no re-read of the source.
+ * ---------------------------------------------------------------------- */
+typedef struct ew_shardmap ew_shardmap;
+
+/* segs: ascending global order, local_off tiling [0, total) back to back. */
+int ew_shardmap_create(const ew_segment* segs, int64_t n_segs, int64_t block_bytes,
+                       ew_shardmap** out);
+void ew_shardmap_free(ew_shardmap* map);
+int64_t ew_shardmap_bytes(const ew_shardmap* map);
+int64_t ew_shardmap_num_rows(const ew_shardmap* map);
+int ew_shardmap_row_blocks(const ew_shardmap* map, int64_t* out_block_ids, int64_t cap);
+
+/* snap <- live (whole packed buffer) fused with row checksums of live.
+ * live/snap 16-byte aligned; row_sums: device uint64[2 * num_rows]. */
+int ew_snapshot(const ew_shardmap* map, const void* live, void* snap, uint64_t* row_sums,
+                ew_stream_t stream);
+int ew_checksum(const ew_shardmap* map, const void* buf, uint64_t* row_sums,
+                ew_stream_t stream);
+/* Recompute rows of buf and compare with expected.  *bad_count (device
+ * uint32, zeroed by the call) receives the number of mismatching rows, whose
+ * indices go to bad_rows[0..bad_cap) when bad_rows != NULL. */
+int ew_verify(const ew_shardmap* map, const void* buf, const uint64_t* expected_row_sums,
+              uint32_t* bad_count, int64_t* bad_rows, int64_t bad_cap, ew_stream_t stream);
+/* block_sums[2*b .. 2*b+1] += row sums of the rows in global block b. */
+int ew_rows_to_blocks(const ew_shardmap* map, const uint64_t* row_sums, uint64_t* block_sums,
+                      int64_t n_blocks, ew_stream_t stream);
+/* Synthetic model state: global word i = splitmix64(seed ^ i), placed by the
+ * segment map (any rank can regenerate any interval). */
+int ew_fill_synthetic(const ew_shardmap* map, void* buf, uint64_t seed, ew_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * (b) Reshard executor — peer-pointer copies over NVLink/NVSwitch
+ * ---------------------------------------------------------------------- */
+typedef struct ew_copy_program ew_copy_program;
+
+/* Resolve descriptors against buf_table[role * table_ranks + rank] (local or
+ * IPC-mapped peer pointers; NULL where absent) and upload the program to the
+ * current device.  Copies whose destination is not on exec_rank are "remote". */
+int ew_copy_program_create(const ew_copy_desc* descs, int64_t n, void* const* buf_table,
+                           int table_ranks, int exec_rank, ew_copy_program** out);
+/* Program from already-resolved pointers (src, dst, bytes, is_remote). */
+int ew_copy_program_create_raw(const void* const* srcs, void* const* dsts, const int64_t* bytes,
+                               const int* is_remote, int64_t n, ew_copy_program** out);
+void ew_copy_program_free(ew_copy_program* prog);
+int ew_copy_program_stats(const ew_copy_program* prog, int64_t* n_copies, int64_t* remote_bytes,
+                          int64_t* local_bytes);
+/* One launch: remote copies on the first CTAs, local copies on the rest.
+ * n_ctas / remote_ctas == 0 pick defaults (all SMs; CTAs split by bytes). */
+int ew_copy_program_launch(const ew_copy_program* prog, int n_ctas, int remote_ctas,
+                           ew_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * (c) Philox-4x64-10 dropout masks keyed by global sample id
+ * ---------------------------------------------------------------------- */
+/* bits[s][k/32] bit (k%32) = 1 iff element k of sample sample_lo+s is KEPT
+ * (reference rule sim.cpp:926-928: dropped iff u < keep_probability); rows
+ * are ceil(n_elems/32) words, trailing bits 0. */
+int ew_philox_dropout_mask(uint64_t seed, int64_t sample_lo, int64_t n_samples,
+                           uint32_t layer_id, uint32_t op_index, int64_t n_elems,
+                           double keep_probability, uint32_t* bits, ew_stream_t stream);
+/* out[s][k] = draw({seed, sample_lo+s, layer, op}, n_elems)[k] */
+int ew_philox_uniforms(uint64_t seed, int64_t sample_lo, int64_t n_samples, uint32_t layer_id,
+                       uint32_t op_index, int64_t n_elems, double* out, ew_stream_t stream);
+/* raw words of blocks block_lo .. block_lo+n_blocks-1 of one stream */
+int ew_philox_words(uint64_t seed, uint64_t sample_id, uint32_t layer_id, uint32_t op_index,
+                    uint64_t block_lo, int64_t n_blocks, uint64_t* out, ew_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * (d) Gradient-scale-preserving weighted reduce
+ *
+ * Each contribution unit u (a micro-batch or per-sample gradient, fp32 on
+ * device) is scaled by its weight in fp64 and rounded to int64 fixed point
+ * with frac_bits fractional bits; integer sums are exact and associative, so
+ * the result does not depend on how units are split across ranks.
+ * ---------------------------------------------------------------------- */
+/* max_u,i |w_u * g_u[i]| into *out_max (device double; written, not max-ed). */
+int ew_weighted_absmax(const float* const* units, const double* weights, int n_units,
+                       int64_t n_elems, double* out_max, ew_stream_t stream);
+/* Largest frac_bits with total_units * absmax * 2^frac_bits < 2^62. */
+int ew_fixed_point_bits(double global_absmax, int64_t total_units, int* frac_bits);
+/* acc[i] (+)= sum_u rint(w_u * g_u[i] * 2^frac_bits) */
+int ew_weighted_fold(const float* const* units, const double* weights, int n_units,
+                     int64_t n_elems, int frac_bits, int64_t* acc, int accumulate,
+                     ew_stream_t stream);
+int ew_fixed_to_float(const int64_t* acc, int64_t n, int frac_bits, float* out,
+                      ew_stream_t stream);
+int ew_fixed_to_double(const int64_t* acc, int64_t n, int frac_bits, double* out,
+                       ew_stream_t stream);
+
+/* NCCL communicator of the DP group (the B200 "dynamic communicator"). */
+typedef struct ew_comm ew_comm;
+int ew_comm_unique_id(void* id128);
+int ew_comm_init(const void* id128, int nranks, int rank, ew_comm** out);
+/* ncclCommShrink: every non-excluded rank calls this; abort != 0 uses
+ * NCCL_SHRINK_ABORT (a member died mid-operation). */
+int ew_comm_shrink(ew_comm* parent, const int* exclude_ranks, int n_exclude, int abort,
+                   ew_comm** out);
+int ew_comm_rank(const ew_comm* comm, int* rank, int* nranks);
+int ew_comm_destroy(ew_comm* comm);
+/* In-place sums over the communicator. */
+int ew_allreduce_i64(ew_comm* comm, int64_t* buf, int64_t n, ew_stream_t stream);
+int ew_allreduce_u64(ew_comm* comm, uint64_t* buf, int64_t n, ew_stream_t stream);
+int ew_allreduce_max_f64(ew_comm* comm, double* buf, int64_t n, ew_stream_t stream);
+/* Full (d): absmax pre-pass -> NCCL max -> fold -> NCCL int64 sum -> fp32.
+ * total_units is the global unit count; ws_acc holds n_elems int64,
+ * ws_max one double; *frac_bits_out (host) receives the scale used.  This
+ * call synchronises the stream once to read the global max. */
+int ew_weighted_reduce(ew_comm* comm, const float* const* units, const double* weights,
+                       int n_units, int64_t total_units, int64_t n_elems, int64_t* ws_acc,
+                       double* ws_max, float* out, int* frac_bits_out, ew_stream_t stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* EW_API_H */

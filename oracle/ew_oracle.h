@@ -1,0 +1,41 @@
+/* ORACLE — CPU restatement of the per-step DP recovery path (test
+ * infrastructure only; see ew_oracle.c for the rules of use). */
+#ifndef EW_ORACLE_H
+#define EW_ORACLE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+void ew_oracle_philox4x64(const uint64_t counter[4], const uint64_t key[2], uint64_t out[4]);
+void ew_oracle_draw(uint64_t seed, uint64_t sample, uint32_t layer, uint32_t op, int64_t n,
+                    double* out);
+void ew_oracle_dropout_mask(uint64_t seed, int64_t sample_lo, int64_t n_samples, uint32_t layer,
+                            uint32_t op, int64_t n_elems, double keep, uint32_t* bits);
+
+uint64_t ew_oracle_splitmix64(uint64_t x);
+int64_t ew_oracle_num_rows(const int64_t* segs, int64_t n_segs, int64_t block_bytes);
+int64_t ew_oracle_row_sums(const int64_t* segs, int64_t n_segs, int64_t block_bytes,
+                           const uint8_t* buf, uint64_t* out);
+void ew_oracle_block_sums_synthetic(uint64_t seed, int64_t total_bytes, int64_t block_bytes,
+                                    uint64_t* out);
+void ew_oracle_fill_synthetic(const int64_t* segs, int64_t n_segs, uint64_t seed, uint8_t* buf);
+
+int64_t ew_oracle_interleaved(const int64_t* layer_bytes, int n_layers, const int* ranks_sorted,
+                              int n_ranks, int* out_counts, int64_t* out_ivs);
+int64_t ew_oracle_overlap(const int* s_ranks, const int* s_counts, int s_n, const int64_t* s_ivs,
+                          const int* d_ranks, const int* d_counts, int d_n, const int64_t* d_ivs,
+                          const int* failed, int n_failed, const int* ring, int n_ring,
+                          int64_t* out, int64_t cap);
+
+int ew_oracle_fixed_point_bits(double absmax, int64_t total_units);
+void ew_oracle_weighted_fixed(const double* w, const float* g, int n_units, int64_t dim,
+                              int frac_bits, int64_t* acc);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

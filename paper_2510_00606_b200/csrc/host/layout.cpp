@@ -1,0 +1,169 @@
+// Interleaved-ZeRO layout composer and TransferPlan lowering (host side).
+#include <algorithm>
+#include <map>
+#include <string>
+
+#include "elaskit/b200.hpp"
+
+namespace elaskit::b200 {
+
+PartitionLayout interleaved_layout(const ZeroLayout& z, const std::vector<int>& ranks) {
+  if (z.kind != ZeroKind::Interleaved)
+    throw std::invalid_argument("interleaved_layout needs ZeroKind::Interleaved");
+  if (ranks.empty()) throw std::invalid_argument("interleaved_layout needs at least one rank");
+  std::vector<int> order(ranks);
+  std::sort(order.begin(), order.end());
+  if (std::adjacent_find(order.begin(), order.end()) != order.end())
+    throw std::invalid_argument("interleaved_layout: duplicate rank");
+
+  ZeroLayout over = z;
+  over.dp_degree = static_cast<int>(order.size());
+  PartitionLayout out;
+  out.total_bytes = over.total_bytes();
+  for (const int r : order) out.ranges[r];
+  std::int64_t base = 0;
+  for (std::size_t l = 0; l < over.layer_bytes.size(); ++l) {
+    if (over.layer_bytes[l] < 0) throw std::invalid_argument("negative layer size");
+    for (std::size_t j = 0; j < order.size(); ++j) {
+      const ByteInterval s = over.shard(static_cast<int>(l), static_cast<int>(j));
+      if (s.size() > 0) out.ranges[order[j]].push_back({base + s.lo, base + s.hi});
+    }
+    base += over.layer_bytes[l];
+  }
+  return out;
+}
+
+std::vector<Segment> shard_segments(const PartitionLayout& layout, int rank) {
+  std::vector<Segment> segs;
+  const auto it = layout.ranges.find(rank);
+  if (it == layout.ranges.end()) return segs;
+  std::int64_t local = 0;
+  segs.reserve(it->second.size());
+  for (const ByteInterval& iv : it->second) {
+    segs.push_back({iv.lo, iv.size(), local});
+    local += iv.size();
+  }
+  return segs;
+}
+
+std::int64_t shard_bytes(const PartitionLayout& layout, int rank) {
+  std::int64_t n = 0;
+  const auto it = layout.ranges.find(rank);
+  if (it != layout.ranges.end())
+    for (const ByteInterval& iv : it->second) n += iv.size();
+  return n;
+}
+
+namespace {
+
+// Local offset of global byte range [lo, hi) inside `rank`'s packed buffer;
+// the range must sit inside one of the rank's intervals.
+class LocalIndex {
+ public:
+  explicit LocalIndex(const PartitionLayout& layout) {
+    for (const auto& [rank, ivs] : layout.ranges) {
+      auto& v = index_[rank];
+      std::int64_t local = 0;
+      for (const ByteInterval& iv : ivs) {
+        v.push_back({iv.lo, iv.hi, local});
+        local += iv.size();
+      }
+    }
+  }
+
+  std::int64_t offset(int rank, std::int64_t lo, std::int64_t hi) const {
+    const auto it = index_.find(rank);
+    if (it != index_.end()) {
+      const auto& v = it->second;
+      auto pos = std::upper_bound(v.begin(), v.end(), lo,
+                                  [](std::int64_t x, const Row& r) { return x < r.lo; });
+      if (pos != v.begin()) {
+        const Row& r = *(pos - 1);
+        if (lo >= r.lo && hi <= r.hi) return r.local + (lo - r.lo);
+      }
+    }
+    throw CoverageMismatch("bytes [" + std::to_string(lo) + "," + std::to_string(hi) +
+                           ") are not held by rank " + std::to_string(rank));
+  }
+
+ private:
+  struct Row {
+    std::int64_t lo, hi, local;
+  };
+  std::map<int, std::vector<Row>> index_;
+};
+
+// Owner of [lo,hi) under `layout` (the range lies inside one interval).
+int owner_of_range(const PartitionLayout& layout, std::int64_t lo) {
+  for (const auto& [rank, ivs] : layout.ranges) {
+    auto pos = std::upper_bound(ivs.begin(), ivs.end(), lo,
+                                [](std::int64_t x, const ByteInterval& iv) { return x < iv.lo; });
+    if (pos != ivs.begin() && lo < (pos - 1)->hi) return rank;
+  }
+  return -1;
+}
+
+}  // namespace
+
+std::vector<CopyDesc> reshard_copies(const TransferPlan& plan, const PartitionLayout& src,
+                                     const PartitionLayout& dst, const std::set<int>& failed,
+                                     const SnapshotRing* ring, int exec_rank, bool push) {
+  const LocalIndex old_index(src);
+  const LocalIndex new_index(dst);
+  std::vector<CopyDesc> out;
+
+  for (const TransferEntry& e : plan.entries) {
+    const bool from_replica = e.medium == Medium::H2D_D2D;
+    const bool mine = push ? (e.src_rank == exec_rank) : (e.dst_rank == exec_rank);
+    if (!mine) continue;
+    CopyDesc c;
+    c.src_rank = e.src_rank;
+    c.dst_rank = e.dst_rank;
+    c.dst_role = BufRole::New;
+    c.bytes = e.iv.size();
+    c.dst_off = new_index.offset(e.dst_rank, e.iv.lo, e.iv.hi);
+    if (from_replica) {
+      // the holder's replica is packed like the dead owner's old shard
+      const int owner = owner_of_range(src, e.iv.lo);
+      if (owner < 0 || !failed.contains(owner) || ring == nullptr ||
+          ring->backed_up_by(owner) != e.src_rank)
+        throw CoverageMismatch("h2d_d2d entry at byte " + std::to_string(e.iv.lo) +
+                               " does not come from a failed owner's ring holder");
+      c.src_role = BufRole::Replica;
+      c.src_off = old_index.offset(owner, e.iv.lo, e.iv.hi);
+    } else {
+      c.src_role = BufRole::Old;
+      c.src_off = old_index.offset(e.src_rank, e.iv.lo, e.iv.hi);
+    }
+    out.push_back(c);
+  }
+
+  // retained bytes: exec_rank keeps ownership but its packing may change
+  const auto a = src.ranges.find(exec_rank);
+  const auto b = dst.ranges.find(exec_rank);
+  if (a != src.ranges.end() && b != dst.ranges.end() && !failed.contains(exec_rank)) {
+    std::size_t i = 0, j = 0;
+    const auto& x = a->second;
+    const auto& y = b->second;
+    while (i < x.size() && j < y.size()) {
+      const std::int64_t lo = std::max(x[i].lo, y[j].lo);
+      const std::int64_t hi = std::min(x[i].hi, y[j].hi);
+      if (lo < hi) {
+        CopyDesc c;
+        c.src_role = BufRole::Old;
+        c.src_rank = exec_rank;
+        c.dst_role = BufRole::New;
+        c.dst_rank = exec_rank;
+        c.src_off = old_index.offset(exec_rank, lo, hi);
+        c.dst_off = new_index.offset(exec_rank, lo, hi);
+        c.bytes = hi - lo;
+        out.push_back(c);
+      }
+      if (x[i].hi <= y[j].hi) ++i;
+      else ++j;
+    }
+  }
+  return out;
+}
+
+}  // namespace elaskit::b200

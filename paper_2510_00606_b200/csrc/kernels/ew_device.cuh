@@ -1,0 +1,135 @@
+// Internal device-side helpers for libelaskit_b200 (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "ew_api.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ < 1000)
+#error "libelaskit_b200 kernels target sm_100a (B200) only"
+#endif
+
+namespace ew {
+
+// ---- error plumbing (defined in runtime.cu) ----
+int set_error(int status, const std::string& msg);
+int cuda_status(cudaError_t e, const char* what);
+
+#define EW_CUDA_TRY(expr)                                      \
+  do {                                                         \
+    cudaError_t _e = (expr);                                   \
+    if (_e != cudaSuccess) return ::ew::cuda_status(_e, #expr); \
+  } while (0)
+
+// SM count of the current device (cached per device).
+int num_sms();
+
+// ---- segment map on device ----
+struct DevSeg {
+  int64_t global_lo;
+  int64_t length;
+  int64_t local_off;
+  int64_t row_base;  // first row of this segment
+};
+
+struct ShardMapView {
+  const DevSeg* segs;
+  int64_t n_segs;
+  int64_t n_rows;
+  int64_t total_bytes;  // packed local buffer size
+  int block_shift;      // log2(block_bytes)
+};
+
+// ---- 128-bit memory helpers ----
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ uint4 ld_plain(const void* p) {
+  uint4 v;
+  asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(p));
+  return v;
+}
+
+__device__ __forceinline__ void st_plain(void* p, const uint4& v) {
+  asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint64_t lo64(const uint4& v) {
+  return (static_cast<uint64_t>(v.y) << 32) | v.x;
+}
+__device__ __forceinline__ uint64_t hi64(const uint4& v) {
+  return (static_cast<uint64_t>(v.w) << 32) | v.z;
+}
+
+__host__ __device__ __forceinline__ int64_t floor_div(int64_t a, int64_t b) {
+  int64_t q = a / b;
+  return (a % b != 0 && ((a < 0) != (b < 0))) ? q - 1 : q;
+}
+
+__host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ULL;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+
+// Row r -> segment index (binary search over row_base).
+__device__ __forceinline__ int64_t seg_of_row(const ShardMapView& m, int64_t r) {
+  int64_t lo = 0, hi = m.n_segs - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (m.segs[mid].row_base <= r) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+struct RowGeom {
+  int64_t local_lo;  // first local byte of the row
+  int64_t len;       // bytes
+  int64_t delta;     // global = local + delta
+  int64_t block;     // global block id
+};
+
+__device__ __forceinline__ RowGeom row_geom(const ShardMapView& m, int64_t r) {
+  const DevSeg s = m.segs[seg_of_row(m, r)];
+  const int64_t b = (s.global_lo >> m.block_shift) + (r - s.row_base);
+  const int64_t g_lo = max(s.global_lo, b << m.block_shift);
+  const int64_t g_hi = min(s.global_lo + s.length, (b + 1) << m.block_shift);
+  RowGeom g;
+  g.delta = s.global_lo - s.local_off;
+  g.local_lo = g_lo - g.delta;
+  g.len = g_hi - g_lo;
+  g.block = b;
+  return g;
+}
+
+}  // namespace ew
+
+// Opaque handle bodies shared between translation units.
+struct ew_shardmap {
+  int device = -1;
+  int64_t n_segs = 0;
+  int64_t n_rows = 0;
+  int64_t total_bytes = 0;
+  int64_t block_bytes = 0;
+  int block_shift = 0;
+  ew::DevSeg* d_segs = nullptr;      // device copy
+  std::vector<ew::DevSeg> h_segs;    // host copy (row -> block queries)
+  ew::ShardMapView view() const {
+    return ew::ShardMapView{d_segs, n_segs, n_rows, total_bytes, block_shift};
+  }
+};

@@ -1,0 +1,370 @@
+// (a) Per-step snapshot with fused per-block checksum, and verification.
+//
+// Replaces the reference's *modelled* snapshot (SnapshotTimeline /
+// snapshot_overhead_s, param_fabric.hpp:86-96; Simulation::snapshot_delta,
+// sim.cpp:861-880) with the byte-moving operation: one HBM pass copies a
+// rank's packed shard live -> snapshot while checksumming it, a second pass
+// re-reads the snapshot and compares.  Both are HBM-bound streaming kernels:
+// 128-bit non-allocating loads, one 64 KiB checksum row per CTA iteration,
+// persistent grid of SMs x resident CTAs.
+//
+// Checksum spec (ew_api.h, oracle/ew_oracle.c ew_oracle_row_sums): per global
+// block b, s0 = sum w_i and s1 = sum (i+1) w_i (mod 2^64) over the global
+// little-endian u64 words w_i, bytes the buffer does not hold read as zero.
+//
+// Per local 8-byte word W at local byte x (8-aligned) the global position is
+// g = x + delta, q = floor(g/8), sh = g mod 8 (uniform per row).  W feeds
+// word q with A = W << 8sh and word q+1 with B = W >> (64-8sh) (sh > 0), so
+// with C = A + B:  s0 += C,  s1 += (q+1) C + B.  Bytes outside the row are
+// masked before the split, hence every nonzero contribution lands in the
+// row's own block.  Per thread the word indices are q_t + 512 i (+1 for the
+// odd word), so s1 needs only additions: sum i*D_i = n*T1 - T2 with the
+// running sums T1 += D_i, T2 += T1 (D_i = C_even + C_odd of iteration i).
+#include <algorithm>
+#include <vector>
+
+#include "ew_device.cuh"
+
+namespace ew {
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kUnroll = 8;
+
+__device__ __forceinline__ uint64_t byte_mask(int64_t x, int64_t a, int64_t e) {
+  // bytes of the 8-byte word at local x that fall in [a, e)
+  const int64_t lo = min(max(a - x, (int64_t)0), (int64_t)8);
+  const int64_t hi = min(max(e - x, (int64_t)0), (int64_t)8);
+  if (hi <= lo) return 0;
+  const uint64_t upper = (hi == 8) ? ~0ULL : ((1ULL << (8 * hi)) - 1);
+  return upper & (~0ULL << (8 * lo));
+}
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+enum class Mode { kSnapshot, kChecksum, kVerify };
+
+template <Mode M>
+__global__ void __launch_bounds__(kThreads) row_kernel(ShardMapView map,
+                                                       const uint8_t* __restrict__ src,
+                                                       uint8_t* __restrict__ dst,
+                                                       uint64_t* __restrict__ row_sums,
+                                                       const uint64_t* __restrict__ expected,
+                                                       uint32_t* __restrict__ bad_count,
+                                                       int64_t* __restrict__ bad_rows,
+                                                       int64_t bad_cap) {
+  __shared__ uint64_t red0[kThreads / 32];
+  __shared__ uint64_t red1[kThreads / 32];
+  const int tid = threadIdx.x;
+
+  for (int64_t r = blockIdx.x; r < map.n_rows; r += gridDim.x) {
+    const RowGeom g = row_geom(map, r);
+    const int64_t a = g.local_lo;
+    const int64_t e = g.local_lo + g.len;
+    const int64_t v_lo = a >> 4;
+    const int64_t nvec = ((e + 15) >> 4) - v_lo;
+    const int sh = static_cast<int>(g.delta & 7);  // delta >= 0 for packed shards
+    const int64_t q_t = floor_div(16 * (v_lo + tid) + g.delta, 8);
+
+    uint64_t t1 = 0, t2 = 0, odd = 0, bsum = 0;
+    const int64_t iters = (nvec + kThreads - 1) / kThreads;
+    const int64_t n_exec = (iters + kUnroll - 1) / kUnroll * kUnroll;
+
+    for (int64_t it = 0; it < iters; it += kUnroll) {
+      uint4 val[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t idx = tid + (it + u) * kThreads;
+        if (idx < nvec) val[u] = ld_stream(src + 16 * (v_lo + idx));
+        else val[u] = make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int64_t idx = tid + (it + u) * kThreads;
+        const int64_t x = 16 * (v_lo + idx);
+        if (M == Mode::kSnapshot && idx < nvec && x >= a) {
+          // each 16-byte vector is copied by the row that holds its first byte
+          if (x + 16 <= map.total_bytes) {
+            st_plain(dst + x, val[u]);
+          } else {
+            const uint8_t* b = reinterpret_cast<const uint8_t*>(&val[u]);
+            for (int k = 0; k < 16 && x + k < map.total_bytes; ++k) dst[x + k] = b[k];
+          }
+        }
+        uint64_t w0 = lo64(val[u]);
+        uint64_t w1 = hi64(val[u]);
+        if (x < a || x + 16 > e) {
+          w0 &= byte_mask(x, a, e);
+          w1 &= byte_mask(x + 8, a, e);
+        }
+        uint64_t c0 = w0, c1 = w1, b0 = 0, b1 = 0;
+        if (sh != 0) {
+          b0 = w0 >> (64 - 8 * sh);
+          b1 = w1 >> (64 - 8 * sh);
+          c0 = (w0 << (8 * sh)) + b0;
+          c1 = (w1 << (8 * sh)) + b1;
+        }
+        t1 += c0 + c1;
+        t2 += t1;
+        odd += c1;
+        bsum += b0 + b1;
+      }
+    }
+    uint64_t s0 = t1;
+    uint64_t s1 = static_cast<uint64_t>(q_t + 1) * t1 +
+                  512ULL * (static_cast<uint64_t>(n_exec) * t1 - t2) + odd + bsum;
+
+    s0 = warp_sum_u64(s0);
+    s1 = warp_sum_u64(s1);
+    if ((tid & 31) == 0) {
+      red0[tid >> 5] = s0;
+      red1[tid >> 5] = s1;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      uint64_t x0 = 0, x1 = 0;
+#pragma unroll
+      for (int w = 0; w < kThreads / 32; ++w) {
+        x0 += red0[w];
+        x1 += red1[w];
+      }
+      if (M == Mode::kVerify) {
+        if (x0 != expected[2 * r] || x1 != expected[2 * r + 1]) {
+          const uint32_t slot = atomicAdd(bad_count, 1u);
+          if (bad_rows != nullptr && static_cast<int64_t>(slot) < bad_cap) bad_rows[slot] = r;
+        }
+      } else {
+        row_sums[2 * r] = x0;
+        row_sums[2 * r + 1] = x1;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void rows_to_blocks_kernel(ShardMapView map, const uint64_t* __restrict__ rows,
+                                      unsigned long long* __restrict__ blocks, int64_t n_blocks) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < map.n_rows;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    const RowGeom g = row_geom(map, r);
+    if (g.block < 0 || g.block >= n_blocks) continue;
+    atomicAdd(&blocks[2 * g.block], static_cast<unsigned long long>(rows[2 * r]));
+    atomicAdd(&blocks[2 * g.block + 1], static_cast<unsigned long long>(rows[2 * r + 1]));
+  }
+}
+
+// Segment holding local byte x (binary search over local_off).
+__device__ __forceinline__ int64_t seg_of_local(const ShardMapView& m, int64_t x) {
+  int64_t lo = 0, hi = m.n_segs - 1;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi + 1) >> 1;
+    if (m.segs[mid].local_off <= x) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ uint8_t synth_byte(uint64_t seed, int64_t g) {
+  return static_cast<uint8_t>(splitmix64(seed ^ static_cast<uint64_t>(g >> 3)) >> (8 * (g & 7)));
+}
+
+__global__ void fill_kernel(ShardMapView map, uint8_t* __restrict__ buf, uint64_t seed) {
+  const int64_t nvec = (map.total_bytes + 15) >> 4;
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < nvec;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t x = 16 * v;
+    const DevSeg s = map.segs[seg_of_local(map, x)];
+    const bool inside = x + 16 <= s.local_off + s.length && x + 16 <= map.total_bytes;
+    if (inside) {
+      const int64_t g = x + (s.global_lo - s.local_off);
+      const int64_t q = g >> 3;
+      const int sh = static_cast<int>(g & 7);
+      const uint64_t w0 = splitmix64(seed ^ static_cast<uint64_t>(q));
+      const uint64_t w1 = splitmix64(seed ^ static_cast<uint64_t>(q + 1));
+      uint64_t lo, hi;
+      if (sh == 0) {
+        lo = w0;
+        hi = w1;
+      } else {
+        const uint64_t w2 = splitmix64(seed ^ static_cast<uint64_t>(q + 2));
+        lo = (w0 >> (8 * sh)) | (w1 << (64 - 8 * sh));
+        hi = (w1 >> (8 * sh)) | (w2 << (64 - 8 * sh));
+      }
+      st_plain(buf + x, make_uint4(static_cast<uint32_t>(lo), static_cast<uint32_t>(lo >> 32),
+                                   static_cast<uint32_t>(hi), static_cast<uint32_t>(hi >> 32)));
+    } else {
+      for (int k = 0; k < 16 && x + k < map.total_bytes; ++k) {
+        const DevSeg t = map.segs[seg_of_local(map, x + k)];
+        buf[x + k] = synth_byte(seed, x + k + (t.global_lo - t.local_off));
+      }
+    }
+  }
+}
+
+int row_grid(const void* kernel, int64_t n_rows) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
+  if (per_sm < 1) per_sm = 1;
+  const int64_t full = static_cast<int64_t>(num_sms()) * per_sm;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_rows, full)));
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+}  // namespace ew
+
+using namespace ew;
+
+extern "C" {
+
+int ew_shardmap_create(const ew_segment* segs, int64_t n_segs, int64_t block_bytes,
+                       ew_shardmap** out) {
+  if (out == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (n_segs < 0 || (n_segs > 0 && segs == nullptr))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "bad segment list");
+  if (block_bytes < 4096 || block_bytes > (1 << 20) || (block_bytes & (block_bytes - 1)))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "block_bytes must be a power of two in [4 KiB, 1 MiB]");
+  int shift = 0;
+  while ((int64_t{1} << shift) < block_bytes) ++shift;
+
+  auto* m = new ew_shardmap();
+  m->block_bytes = block_bytes;
+  m->block_shift = shift;
+  int64_t local = 0, prev_hi = INT64_MIN, rows = 0;
+  for (int64_t k = 0; k < n_segs; ++k) {
+    const ew_segment& s = segs[k];
+    if (s.length < 0 || s.global_lo < 0 || s.local_off != local || s.global_lo < prev_hi ||
+        s.global_lo < s.local_off) {
+      delete m;
+      return set_error(EW_ERR_COVERAGE_MISMATCH,
+                       "segments must be ascending, disjoint and packed back to back (segment " +
+                           std::to_string(k) + ")");
+    }
+    DevSeg d{s.global_lo, s.length, s.local_off, rows};
+    if (s.length > 0) rows += ((s.global_lo + s.length - 1) >> shift) - (s.global_lo >> shift) + 1;
+    m->h_segs.push_back(d);
+    local += s.length;
+    prev_hi = s.global_lo + s.length;
+  }
+  // drop empty segments from the device table (they own no rows)
+  std::vector<DevSeg> dev;
+  for (const DevSeg& d : m->h_segs)
+    if (d.length > 0) dev.push_back(d);
+  m->h_segs = dev;
+  m->n_segs = static_cast<int64_t>(dev.size());
+  m->n_rows = rows;
+  m->total_bytes = local;
+  cudaError_t e = cudaGetDevice(&m->device);
+  if (e == cudaSuccess && !dev.empty()) {
+    e = cudaMalloc(&m->d_segs, dev.size() * sizeof(DevSeg));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(m->d_segs, dev.data(), dev.size() * sizeof(DevSeg), cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    if (m->d_segs) cudaFree(m->d_segs);
+    delete m;
+    return cuda_status(e, "ew_shardmap_create");
+  }
+  *out = m;
+  return EW_OK;
+}
+
+void ew_shardmap_free(ew_shardmap* map) {
+  if (map == nullptr) return;
+  if (map->d_segs) cudaFree(map->d_segs);
+  delete map;
+}
+
+int64_t ew_shardmap_bytes(const ew_shardmap* map) { return map ? map->total_bytes : -1; }
+int64_t ew_shardmap_num_rows(const ew_shardmap* map) { return map ? map->n_rows : -1; }
+
+int ew_shardmap_row_blocks(const ew_shardmap* map, int64_t* out, int64_t cap) {
+  if (map == nullptr || (out == nullptr && cap > 0))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "bad arguments");
+  if (cap < map->n_rows) return set_error(EW_ERR_CAPACITY, "row block buffer too small");
+  int64_t r = 0;
+  for (const DevSeg& s : map->h_segs) {
+    const int64_t b0 = s.global_lo >> map->block_shift;
+    const int64_t b1 = (s.global_lo + s.length - 1) >> map->block_shift;
+    for (int64_t b = b0; b <= b1; ++b) out[r++] = b;
+  }
+  return EW_OK;
+}
+
+int ew_snapshot(const ew_shardmap* map, const void* live, void* snap, uint64_t* row_sums,
+                ew_stream_t stream) {
+  if (map == nullptr || row_sums == nullptr || (map->total_bytes > 0 && (!live || !snap)))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_snapshot: NULL argument");
+  if (!aligned16(live) || !aligned16(snap))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_snapshot: live/snap must be 16-byte aligned");
+  if (map->n_rows == 0) return EW_OK;
+  auto k = row_kernel<Mode::kSnapshot>;
+  k<<<row_grid((const void*)k, map->n_rows), kThreads, 0, (cudaStream_t)stream>>>(
+      map->view(), static_cast<const uint8_t*>(live), static_cast<uint8_t*>(snap), row_sums,
+      nullptr, nullptr, nullptr, 0);
+  EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}
+
+int ew_checksum(const ew_shardmap* map, const void* buf, uint64_t* row_sums,
+                ew_stream_t stream) {
+  if (map == nullptr || row_sums == nullptr || (map->total_bytes > 0 && !buf))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_checksum: NULL argument");
+  if (!aligned16(buf)) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_checksum: buf must be 16-byte aligned");
+  if (map->n_rows == 0) return EW_OK;
+  auto k = row_kernel<Mode::kChecksum>;
+  k<<<row_grid((const void*)k, map->n_rows), kThreads, 0, (cudaStream_t)stream>>>(
+      map->view(), static_cast<const uint8_t*>(buf), nullptr, row_sums, nullptr, nullptr, nullptr,
+      0);
+  EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}
+
+int ew_verify(const ew_shardmap* map, const void* buf, const uint64_t* expected,
+              uint32_t* bad_count, int64_t* bad_rows, int64_t bad_cap, ew_stream_t stream) {
+  if (map == nullptr || expected == nullptr || bad_count == nullptr ||
+      (map->total_bytes > 0 && !buf))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_verify: NULL argument");
+  if (!aligned16(buf)) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_verify: buf must be 16-byte aligned");
+  EW_CUDA_TRY(cudaMemsetAsync(bad_count, 0, sizeof(uint32_t), (cudaStream_t)stream));
+  if (map->n_rows == 0) return EW_OK;
+  auto k = row_kernel<Mode::kVerify>;
+  k<<<row_grid((const void*)k, map->n_rows), kThreads, 0, (cudaStream_t)stream>>>(
+      map->view(), static_cast<const uint8_t*>(buf), nullptr, nullptr, expected, bad_count,
+      bad_rows, bad_cap);
+  EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}
+
+int ew_rows_to_blocks(const ew_shardmap* map, const uint64_t* row_sums, uint64_t* block_sums,
+                      int64_t n_blocks, ew_stream_t stream) {
+  if (map == nullptr || row_sums == nullptr || block_sums == nullptr)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_rows_to_blocks: NULL argument");
+  if (map->n_rows == 0) return EW_OK;
+  const int grid = static_cast<int>(std::min<int64_t>((map->n_rows + 255) / 256, 4 * num_sms()));
+  rows_to_blocks_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      map->view(), row_sums, reinterpret_cast<unsigned long long*>(block_sums), n_blocks);
+  EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}
+
+int ew_fill_synthetic(const ew_shardmap* map, void* buf, uint64_t seed, ew_stream_t stream) {
+  if (map == nullptr || (map->total_bytes > 0 && buf == nullptr))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fill_synthetic: NULL argument");
+  if (!aligned16(buf)) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fill_synthetic: buf must be 16-byte aligned");
+  if (map->total_bytes == 0) return EW_OK;
+  const int64_t nvec = (map->total_bytes + 15) >> 4;
+  const int grid = static_cast<int>(std::min<int64_t>((nvec + 255) / 256, 8 * num_sms()));
+  fill_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(map->view(), static_cast<uint8_t*>(buf),
+                                                      seed);
+  EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}
+
+}  // extern "C"

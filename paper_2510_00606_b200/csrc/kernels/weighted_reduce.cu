@@ -1,0 +1,212 @@
+// (d) Gradient-scale-preserving weighted reduce across reshaped micro-batches.
+//
+// Reference: weighted_grad_average (dataflow.cpp:71-83) is an fp64 left fold
+// acc[i] += w_j * g_j[i] whose result depends on the fold order; the toy step
+// gets split invariance only by walking samples in one canonical order
+// (sim.cpp:901-953, test_dataflow.cpp:97-122).  On B200 the fold crosses GPUs
+// through NCCL, whose summation order changes with world size, so the device
+// path quantises each contribution unit once to int64 fixed point:
+//     q_u[i] = rint(w_u * (double)g_u[i] * 2^F)
+// and sums integers (exact, associative).  Any split of the same units over
+// any number of ranks yields bit-identical sums; F comes from a global absmax
+// pre-pass (an NCCL max, itself split-invariant).  Error vs the fp64
+// reference: <= U * 2^-(F+1) from rounding, plus one fp32 rounding of output.
+// The fold kernel is HBM-bound: 4 bytes per unit-element in, 8 bytes out.
+#include <algorithm>
+#include <cmath>
+
+#include "ew_device.cuh"
+
+namespace ew {
+namespace {
+
+constexpr int kMaxUnits = 16;
+
+struct Units {
+  const float* p[kMaxUnits];
+  double w[kMaxUnits];
+  int n;
+};
+
+__global__ void __launch_bounds__(256) absmax_kernel(Units u, int64_t n,
+                                                     unsigned long long* out_bits) {
+  double m = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    for (int k = 0; k < u.n; ++k) {
+      const double v = fabs(u.w[k] * static_cast<double>(u.p[k][i]));
+      m = (v > m || v != v) ? v : m;  // NaN propagates
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double x = __shfl_down_sync(0xffffffffu, m, o);
+    m = (x > m || x != x) ? x : m;
+  }
+  __shared__ double red[8];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) m = (red[k] > m || red[k] != red[k]) ? red[k] : m;
+    // non-negative doubles (and +NaN) order like their bit patterns
+    atomicMax(out_bits, static_cast<unsigned long long>(__double_as_longlong(m)));
+  }
+}
+
+template <bool kAccumulate>
+__global__ void __launch_bounds__(256) fold_kernel(Units u, int64_t n, double scale,
+                                                   long long* __restrict__ acc) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n4 = n / 4;
+  bool vec_ok = (reinterpret_cast<uintptr_t>(acc) & 15) == 0;
+  for (int k = 0; k < u.n; ++k) vec_ok = vec_ok && ((reinterpret_cast<uintptr_t>(u.p[k]) & 15) == 0);
+  if (vec_ok) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+      long long s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+      for (int k = 0; k < u.n; ++k) {
+        const float4 g = __ldg(reinterpret_cast<const float4*>(u.p[k]) + i);
+        const double w = u.w[k];
+        s0 += __double2ll_rn((w * static_cast<double>(g.x)) * scale);
+        s1 += __double2ll_rn((w * static_cast<double>(g.y)) * scale);
+        s2 += __double2ll_rn((w * static_cast<double>(g.z)) * scale);
+        s3 += __double2ll_rn((w * static_cast<double>(g.w)) * scale);
+      }
+      longlong2* dst = reinterpret_cast<longlong2*>(acc + 4 * i);
+      if (kAccumulate) {
+        const longlong2 a = dst[0], b = dst[1];
+        s0 += a.x;
+        s1 += a.y;
+        s2 += b.x;
+        s3 += b.y;
+      }
+      dst[0] = make_longlong2(s0, s1);
+      dst[1] = make_longlong2(s2, s3);
+    }
+  }
+  const int64_t start = vec_ok ? 4 * n4 : 0;
+  for (int64_t i = start + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    long long s = kAccumulate ? acc[i] : 0;
+    for (int k = 0; k < u.n; ++k)
+      s += __double2ll_rn((u.w[k] * static_cast<double>(u.p[k][i])) * scale);
+    acc[i] = s;
+  }
+}
+
+template <typename T>
+__global__ void dequant_kernel(const long long* __restrict__ acc, int64_t n, double inv_scale,
+                               T* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = static_cast<T>(static_cast<double>(acc[i]) * inv_scale);
+}
+
+int grid_for(int64_t work) {
+  const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, cap)));
+}
+
+int pack_units(const float* const* units, const double* weights, int n_units, int offset,
+               Units& u) {
+  u.n = std::min(kMaxUnits, n_units - offset);
+  for (int k = 0; k < u.n; ++k) {
+    if (units[offset + k] == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL unit pointer");
+    u.p[k] = units[offset + k];
+    u.w[k] = weights[offset + k];
+  }
+  for (int k = u.n; k < kMaxUnits; ++k) {
+    u.p[k] = nullptr;
+    u.w[k] = 0.0;
+  }
+  return EW_OK;
+}
+
+}  // namespace
+}  // namespace ew
+
+using namespace ew;
+
+extern "C" {
+
+int ew_weighted_absmax(const float* const* units, const double* weights, int n_units,
+                       int64_t n_elems, double* out_max, ew_stream_t stream) {
+  if (out_max == nullptr || n_units < 0 || n_elems < 0 || (n_units > 0 && (!units || !weights)))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_weighted_absmax: bad arguments");
+  EW_CUDA_TRY(cudaMemsetAsync(out_max, 0, sizeof(double), (cudaStream_t)stream));
+  for (int off = 0; off < n_units && n_elems > 0; off += kMaxUnits) {
+    Units u;
+    if (int st = pack_units(units, weights, n_units, off, u)) return st;
+    absmax_kernel<<<grid_for(n_elems), 256, 0, (cudaStream_t)stream>>>(
+        u, n_elems, reinterpret_cast<unsigned long long*>(out_max));
+    EW_CUDA_TRY(cudaGetLastError());
+  }
+  return EW_OK;
+}
+
+int ew_fixed_point_bits(double global_absmax, int64_t total_units, int* frac_bits) {
+  if (frac_bits == nullptr || total_units < 1)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fixed_point_bits: bad arguments");
+  if (!std::isfinite(global_absmax) || global_absmax < 0)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "gradient contains inf/nan");
+  if (global_absmax == 0.0) {
+    *frac_bits = 0;
+    return EW_OK;
+  }
+  int e = 0;
+  std::frexp(global_absmax, &e);  // absmax < 2^e
+  int cu = 0;
+  while ((int64_t{1} << cu) < total_units) ++cu;  // total_units <= 2^cu
+  *frac_bits = std::min(1000, 62 - e - cu);       // U * absmax * 2^F < 2^62
+  return EW_OK;
+}
+
+int ew_weighted_fold(const float* const* units, const double* weights, int n_units,
+                     int64_t n_elems, int frac_bits, int64_t* acc, int accumulate,
+                     ew_stream_t stream) {
+  if (acc == nullptr || n_units < 0 || n_elems < 0 || (n_units > 0 && (!units || !weights)))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_weighted_fold: bad arguments");
+  if (frac_bits > 1000 || frac_bits < -1000)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_weighted_fold: frac_bits out of range");
+  if (n_elems == 0) return EW_OK;
+  const double scale = std::ldexp(1.0, frac_bits);
+  if (n_units == 0) {
+    if (!accumulate)
+      EW_CUDA_TRY(cudaMemsetAsync(acc, 0, n_elems * sizeof(int64_t), (cudaStream_t)stream));
+    return EW_OK;
+  }
+  for (int off = 0; off < n_units; off += kMaxUnits) {
+    Units u;
+    if (int st = pack_units(units, weights, n_units, off, u)) return st;
+    const int grid = grid_for((n_elems + 3) / 4);
+    long long* a = reinterpret_cast<long long*>(acc);
+    if (accumulate || off > 0)
+      fold_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a);
+    else
+      fold_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a);
+    EW_CUDA_TRY(cudaGetLastError());
+  }
+  return EW_OK;
+}
+
+int ew_fixed_to_float(const int64_t* acc, int64_t n, int frac_bits, float* out,
+                      ew_stream_t stream) {
+  if ((n > 0 && (!acc || !out)) || n < 0)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fixed_to_float: bad arguments");
+  if (n == 0) return EW_OK;
+  dequant_kernel<float><<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const long long*>(acc), n, std::ldexp(1.0, -frac_bits), out);
+  EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}
+
+int ew_fixed_to_double(const int64_t* acc, int64_t n, int frac_bits, double* out,
+                       ew_stream_t stream) {
+  if ((n > 0 && (!acc || !out)) || n < 0)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fixed_to_double: bad arguments");
+  if (n == 0) return EW_OK;
+  dequant_kernel<double><<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+      reinterpret_cast<const long long*>(acc), n, std::ldexp(1.0, -frac_bits), out);
+  EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}
+
+}  // extern "C"
