@@ -1,0 +1,589 @@
+#!/usr/bin/env python3
+"""Benchmark of the B200 per-step DP recovery path (BASELINE.json metric:
+"snapshot+verify GB/s per GPU; reshard MTTR (ms) 8->7 B200 at 7B ZeRO state").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (driver, N > 1)
+
+One STEP = one per-step snapshot of this GPU's ZeRO shard with its fused
+per-block checksum, followed by verification of the snapshot (two kernels).
+Workload (config B): Llama-2 7B ZeRO state, bf16 params + fp32 master/m/v =
+14 B/param, interleaved over DP=8; each GPU owns one rank's 11.79 GB shard
+(weak scaling: per-GPU work is fixed as N grows).  `value` counts algorithmic
+HBM bytes, 2S (copy) + S (verify re-read) per step per GPU, summed over GPUs.
+
+Also measured in the same run (extra keys):
+  reshard   N -> N-1 live remap of the same 7B-per-GPU state over NVLink peer
+            pointers (N >= 2; the 8 -> 7 headline at N = 8, dropping rank 3),
+            with the MTTR breakdown (plan, peer mapping, NCCL shrink, copy).
+  philox    config E dropout masks for the busiest rank after DP 8 -> 5.
+  reduce    config E weighted fixed-point fold (+ NCCL int64 sum when N > 1).
+--impl reference times the CPU path on the host cores (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "snapshot+verify GB/s per GPU; reshard MTTR (ms) 8→7 B200 at 7B ZeRO state"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse_args():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    p.add_argument("--block-bytes", type=int, default=65536)
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--reshard-reps", type=int, default=10)
+    p.add_argument("--reduce-elems", type=int, default=1 << 30)
+    p.add_argument("--cpu-sample-bytes", type=int, default=1 << 30)
+    p.add_argument("--skip", default="", help="comma list of: e2e,reshard,philox,reduce,cpu")
+    p.add_argument("--json-out", default="")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ helpers ---
+
+def measured_peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return float(d.get("hbm_gbs", FALLBACK_HBM_GBS)), "measured"
+    return FALLBACK_HBM_GBS, "fallback"
+
+
+def profiled_traffic(kernel: str):
+    """dram read+write bytes per launch from the committed ncu capture."""
+    f = ROOT / "profiles" / "traffic.json"
+    if f.exists():
+        return json.loads(f.read_text()).get(kernel)
+    return None
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.out = None
+
+    def start(self):
+        try:
+            self.out = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-i", str(self.idx), "-lms", "100"], stdout=self.out, stderr=subprocess.DEVNULL)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.15)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.out.flush()
+        rows = []
+        for line in Path(self.out.name).read_text().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                rows.append({"sm": float(parts[1]), "max": float(parts[2]),
+                             "reasons": {"hw_slowdown": parts[5], "hw_thermal_slowdown": parts[6],
+                                         "sw_thermal_slowdown": parts[7], "sw_power_cap": parts[8]}})
+            except ValueError:
+                continue
+        os.unlink(self.out.name)
+        if not rows:
+            return None
+        reasons = sorted({k for r in rows for k, v in r["reasons"].items() if v == "Active"})
+        return {"sm_mhz": statistics.median(r["sm"] for r in rows),
+                "sm_max_mhz": max(r["max"] for r in rows), "reasons": reasons,
+                "samples": len(rows)}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+
+
+def max_over_ranks(values, world):
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(values, dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def gpu_index(local):
+    vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if vis:
+        ids = [x for x in vis.split(",") if x.strip()]
+        if local < len(ids) and ids[local].strip().isdigit():
+            return int(ids[local])
+    return local
+
+
+# ------------------------------------------------------------- (a) b200 arm ---
+
+def run_snapshot(args, rank, world, local, out):
+    import torch
+    from paper_2510_00606_b200 import configs, device as dev, fabric
+
+    cfg = configs.llama2_7b()
+    layout = fabric.interleaved_layout(cfg.layer_bytes, range(cfg.dp))
+    shard_rank = rank % cfg.dp
+    segs = layout.segments(shard_rank)
+    S = layout.shard_bytes(shard_rank)
+    m = dev.ShardMap(segs, args.block_bytes)
+    live = dev.empty_bytes(S)
+    snap = dev.empty_bytes(S)
+    rows = m.new_row_sums()
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dev.fill_synthetic(m, live, seed=0)
+    stream = torch.cuda.current_stream()
+
+    for _ in range(args.warmup):
+        dev.snapshot(m, live, snap, rows)
+        dev.verify(m, snap, rows, bad)
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0, "warm-up verification failed"
+    assert torch.equal(snap[:S], live[:S]), "snapshot differs from live state"
+
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+           torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    clocks = ClockSampler(gpu_index(local))
+    clocks.start()
+    time.sleep(0.3)
+    barrier(world)
+    start.record(stream)
+    for k in range(K):
+        ev[k][0].record(stream)
+        dev.snapshot(m, live, snap, rows)
+        ev[k][1].record(stream)
+        dev.verify(m, snap, rows, bad)
+        ev[k][2].record(stream)
+    end.record(stream)
+    barrier(world)
+    clk = clocks.stop()
+    assert int(bad.item()) == 0, "verification failed in the timed region"
+    t_total = start.elapsed_time(end) / 1e3
+    t_snap = sum(a.elapsed_time(b) for a, b, _ in ev) / K / 1e3
+    t_ver = sum(b.elapsed_time(c) for _, b, c in ev) / K / 1e3
+    t_total, t_snap, t_ver = max_over_ranks([t_total, t_snap, t_ver], world)
+    step = t_total / K
+    bytes_step = 3 * S
+    peak, peak_kind = measured_peaks()
+    achieved = 2 * S / t_snap / 1e9
+    out.update({
+        "metric": METRIC, "value": round(world * bytes_step / step / 1e9, 2), "unit": "GB/s",
+        "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": round(step * 1e3, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (word i = splitmix64(seed ^ i))",
+        "config": {"workload": "llama2-7b ZeRO interleaved DP=8, one rank's shard per GPU: "
+                               "snapshot (copy + per-block checksum) then verify",
+                   "shard_bytes": S, "block_bytes": args.block_bytes,
+                   "bytes_per_step_per_gpu": bytes_step,
+                   "bytes_counted": "HBM read+write: 2S snapshot + S verify",
+                   "l2": "inputs 11.8 GB/GPU >> 126 MB L2; no flush needed",
+                   "parallelism": f"dp{world} (independent shards)"},
+        "per_gpu_gbs": round(bytes_step / step / 1e9, 2),
+        "state_gbs_per_gpu": round(S / step / 1e9, 2),
+        "kernels": {"ew_snapshot_ms": round(t_snap * 1e3, 4), "ew_verify_ms": round(t_ver * 1e3, 4),
+                    "ew_verify_gbs": round(S / t_ver / 1e9, 1)},
+        "roofline": {"kernel": "ew_snapshot (row_kernel<kSnapshot>)", "bound": "hbm",
+                     "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "frac_of_8tbs_spec": round(achieved / 8000.0, 4),
+                     "traffic": profiled_traffic("snapshot_7b")},
+        "clocks": clk, "gpu_launches": 2 * K,
+    })
+    return m, live, snap, rows, bad, S, segs
+
+
+def run_e2e(args, rank, world, out, m, live, snap, rows, bad, S):
+    """Same step through the public API with the shard in pinned HOST memory:
+    H2D of the live shard, snapshot + verify, D2H of checksum rows + verdict."""
+    import torch
+    from paper_2510_00606_b200 import device as dev
+
+    host_live = torch.empty(live.numel(), dtype=torch.uint8, pin_memory=True)
+    host_live.copy_(live)
+    host_rows = torch.empty(rows.numel(), dtype=torch.int64, pin_memory=True)
+    host_bad = torch.empty(1, dtype=torch.int32, pin_memory=True)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        live.copy_(host_live, non_blocking=True)
+        dev.snapshot(m, live, snap, rows)
+        dev.verify(m, snap, rows, bad)
+        host_rows.copy_(rows, non_blocking=True)
+        host_bad.copy_(bad, non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    K = args.e2e_steps
+    barrier(world)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    s.record(stream)
+    for _ in range(K):
+        step()
+    e.record(stream)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    assert int(host_bad.item()) == 0
+    t = max_over_ranks([max(s.elapsed_time(e) / 1e3, wall)], world)[0] / K
+    out["e2e"] = {"value": round(world * 3 * S / t / 1e9, 2), "unit": "GB/s",
+                  "h2d_bytes_per_step": int(live.numel()),
+                  "d2h_bytes_per_step": int(rows.numel() * 8 + 4),
+                  "ms_per_step": round(t * 1e3, 3),
+                  "path": "pinned host shard -> H2D -> ew_snapshot -> ew_verify -> D2H rows+verdict"}
+    del host_live
+
+
+def run_cpu_baseline(args, out, segs, S):
+    """Oracle port (the reference has no snapshot/checksum) on the host cores."""
+    import numpy as np
+    from oracle.ew_oracle import load_oracle
+
+    orc = load_oracle()
+    sample = min(S, args.cpu_sample_bytes)
+    sub, local = [], 0
+    for s in segs:
+        if local >= sample:
+            break
+        n = min(int(s["length"]), sample - local)
+        sub.append({"global_lo": int(s["global_lo"]), "length": n, "local_off": local})
+        local += n
+    threads = os.cpu_count() or 1
+    live = orc.fill_synthetic(sub, local, 0)
+    snap = np.empty_like(live)
+    snap.fill(0)
+    orc.snapshot_mt(sub, args.block_bytes, live, snap, threads)  # warm
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        sums = orc.snapshot_mt(sub, args.block_bytes, live, snap, threads)
+        bad = orc.verify_mt(sub, args.block_bytes, snap, sums, threads)
+        reps += 1
+        if time.perf_counter() - t0 > 10.0 or reps >= 50:
+            break
+    dt = (time.perf_counter() - t0) / reps
+    assert bad == 0
+    out["cpu_baseline"] = {"value": round(3 * local / dt / 1e9, 3), "unit": "GB/s",
+                           "cores": threads, "kind": "port",
+                           "sample": f"first {local} bytes of the 7B rank-3 shard, {reps} reps "
+                                     "(memcpy + word-wise checksum, then verify re-read)"}
+    return out["cpu_baseline"]
+
+
+# ------------------------------------------------------------ (b) reshard ---
+
+def run_reshard(args, rank, world, out):
+    import torch
+    import torch.distributed as dist
+    from paper_2510_00606_b200 import configs, device as dev, fabric
+    from paper_2510_00606_b200.reshard import ReshardExecutor, ReshardPlan, shard_map
+
+    base = configs.llama2_7b()
+    # 7B-per-GPU state over `world` ranks (exactly config B at world = 8)
+    lb = base.layer_bytes if world == 8 else [x * world // 8 for x in base.layer_bytes]
+    drop = min(3, world - 1)
+    old = list(range(world))
+    new = [r for r in old if r != drop]
+
+    t0 = time.perf_counter()
+    rp = ReshardPlan.build(lb, old, new)
+    ex = ReshardExecutor(rp, rank, push=True)
+    t_plan = time.perf_counter() - t0
+    bufs = ex.allocate()
+    if bufs.old is not None:
+        dev.fill_synthetic(shard_map(rp.src, rank), bufs.old, 0)
+    if bufs.replica is not None:
+        dev.fill_synthetic(shard_map(rp.src, rp.replica_of(rank)), bufs.replica, 0)
+    if bufs.new is not None:
+        bufs.new.zero_()
+
+    # communicator repair: host edit plan + ncclCommShrink of the DP communicator
+    uid = [dev.Communicator.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = dev.Communicator.init(uid[0], world, rank)
+    barrier(world)
+    t0 = time.perf_counter()
+    pool = {(a, b) for a in old for b in old if a < b}
+    edit = fabric.plan_edit([fabric.CommGroup("dp-stage-1", old)], fabric.FAIL_STOP, [drop], pool)
+    shrunk = comm.shrink([drop]) if rank != drop else None
+    torch.cuda.synchronize()
+    t_comm = time.perf_counter() - t0
+
+    barrier(world)
+    t0 = time.perf_counter()
+    ex.bind(bufs)
+    t_bind = time.perf_counter() - t0
+    stream = torch.cuda.current_stream()
+    for _ in range(2):
+        ex.launch()
+    barrier(world)
+    reps = args.reshard_reps
+    times = []
+    for _ in range(reps):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        s.record(stream)
+        ex.launch()
+        e.record(stream)
+        barrier(world)
+        times.append(s.elapsed_time(e) / 1e3)
+    t_copy = max_over_ranks([sum(times) / reps, min(times)], world)
+
+    # verification without re-reading the source: block sums of the target
+    # shards (added over ranks) == block sums of the source shards
+    block = args.block_bytes
+    nblocks = (sum(lb) + block - 1) // block
+    before = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+    after = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+    if rank in rp.old_ranks:
+        mo = shard_map(rp.src, rank, block)
+        rows = mo.new_row_sums()
+        src_buf = bufs.old
+        if rank == drop:  # the dead rank's bytes as its ring holder keeps them
+            src_buf = bufs.old
+        dev.checksum(mo, src_buf, rows)
+        dev.rows_to_blocks(mo, rows, before)
+    if bufs.new is not None:
+        mn = shard_map(rp.dst, rank, block)
+        rows = mn.new_row_sums()
+        dev.checksum(mn, bufs.new, rows)
+        dev.rows_to_blocks(mn, rows, after)
+    dist.all_reduce(before)
+    dist.all_reduce(after)
+    verified = bool(torch.equal(before, after))
+    traffic = rp.traffic()
+    bott = traffic["bottleneck_bytes"]
+    nvl_gbs = bott / t_copy[0] / 1e9 if bott else None
+    out["reshard"] = {
+        "change": f"{world}->{world - 1} (drop rank {drop})", "verified_by_checksums": verified,
+        "state_bytes": int(sum(lb)), "per_gpu_shard_bytes": int(rp.src.shard_bytes(0)),
+        "total_bytes_moved": traffic["total_bytes_moved"], "nvlink_bytes": traffic["nvlink_bytes"],
+        "bottleneck_gpu_bytes": bott, "plan_entries": len(rp.plan),
+        "copy_ms": round(t_copy[0] * 1e3, 3), "copy_ms_best": round(t_copy[1] * 1e3, 3),
+        "bottleneck_nvlink_gbs": round(nvl_gbs, 1) if nvl_gbs else None,
+        "nvlink_frac_of_900": round(nvl_gbs / 900.0, 4) if nvl_gbs else None,
+        "nvlink_frac_of_770_measured": round(nvl_gbs / 770.0, 4) if nvl_gbs else None,
+        "mttr_ms": {"plan": round(t_plan * 1e3, 3), "comm_edit_and_nccl_shrink": round(t_comm * 1e3, 3),
+                    "peer_map": round(t_bind * 1e3, 3), "copy": round(t_copy[0] * 1e3, 3)},
+        "edit_plan": {"links_removed": len(edit.links_to_remove), "links_added": len(edit.links_to_add)},
+    }
+    out["reshard"]["mttr_ms"]["total"] = round(sum(out["reshard"]["mttr_ms"].values()), 3)
+    ex.close()
+    if shrunk is not None:
+        shrunk.destroy()
+    comm.destroy()
+    del bufs
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------- (c) and (d) ---
+
+def run_philox(args, rank, world, out):
+    import torch
+    from paper_2510_00606_b200 import device as dev, fabric
+
+    slots, sizes = fabric.reshard_microbatches([4] * 8, 32, [0, 1, 2, 3, 4])
+    per_rank = [32 * s for s in sizes]               # [224, 224, 192, 192, 192]
+    r = rank % 5
+    lo = sum(per_rank[:r])
+    n, K = per_rank[r], 4096 * 4096
+    bits = torch.empty((n, K // 32), dtype=torch.int32, device="cuda")
+    dev.dropout_mask(0, lo, n, 1, 0, K, 0.5, bits)
+    torch.cuda.synchronize()
+    reps = 3
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(world)
+    s.record()
+    for _ in range(reps):
+        dev.dropout_mask(0, lo, n, 1, 0, K, 0.5, bits)
+    e.record()
+    barrier(world)
+    t = max_over_ranks([s.elapsed_time(e) / 1e3 / reps], world)[0]
+    out["philox"] = {"workload": f"config E: {n} samples x 4096x4096 elements (rank {r} of DP5), keep 0.5",
+                     "ms": round(t * 1e3, 3), "gelem_per_s": round(n * K / t / 1e9, 1),
+                     "gblocks_per_s": round(n * K / 4 / t / 1e9, 2),
+                     "bound": "INT-ALU (20 64x64->128 multiplies per Philox block)"}
+    del bits
+    torch.cuda.empty_cache()
+
+
+def run_reduce(args, rank, world, out):
+    import torch
+    import torch.distributed as dist
+    from paper_2510_00606_b200 import device as dev
+
+    n = args.reduce_elems
+    g = torch.empty(n, dtype=torch.float32, device="cuda").normal_(0, 1e-3)
+    acc = torch.empty(n, dtype=torch.int64, device="cuda")
+    res = torch.empty(n, dtype=torch.float32, device="cuda")
+    w = [(7 if rank < 2 else 6) / 32]
+    amax = dev.weighted_absmax([g], w)
+    if world > 1:
+        dist.all_reduce(amax, op=dist.ReduceOp.MAX)
+    f = dev.fixed_point_bits(amax.item(), max(world, 1))
+    dev.weighted_fold([g], w, f, acc)
+    torch.cuda.synchronize()
+    s, m1, m2, e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    barrier(world)
+    s.record()
+    dev.weighted_fold([g], w, f, acc)
+    m1.record()
+    if world > 1:
+        dist.all_reduce(acc)  # ncclInt64 sum: exact, order-free
+    m2.record()
+    dev.fixed_to_float(acc, f, res)
+    e.record()
+    barrier(world)
+    t_fold, t_ar, t_deq = max_over_ranks([s.elapsed_time(m1) / 1e3, m1.elapsed_time(m2) / 1e3,
+                                          m2.elapsed_time(e) / 1e3], world)
+    out["reduce"] = {"elements": n, "frac_bits": f, "fold_ms": round(t_fold * 1e3, 3),
+                     "fold_gbs": round(12 * n / t_fold / 1e9, 1),
+                     "allreduce_int64_ms": round(t_ar * 1e3, 3) if world > 1 else None,
+                     "dequant_ms": round(t_deq * 1e3, 3)}
+    del g, acc, res
+    torch.cuda.empty_cache()
+
+
+# ------------------------------------------------------------------- arms ---
+
+def bench_b200(args):
+    import torch
+    rank, world, local = dist_setup(args)
+    skip = set(filter(None, args.skip.split(",")))
+    out = {}
+    m, live, snap, rows, bad, S, segs = run_snapshot(args, rank, world, local, out)
+    if "e2e" not in skip:
+        run_e2e(args, rank, world, out, m, live, snap, rows, bad, S)
+    del live, snap
+    torch.cuda.empty_cache()
+    if world == 1 and rank == 0 and "cpu" not in skip:
+        run_cpu_baseline(args, out, segs, S)
+    if world > 1 and "reshard" not in skip:
+        run_reshard(args, rank, world, out)
+    if "philox" not in skip:
+        run_philox(args, rank, world, out)
+    if "reduce" not in skip:
+        run_reduce(args, rank, world, out)
+    if rank == 0:
+        line = json.dumps(out)
+        print(line, flush=True)
+        if args.json_out:
+            Path(args.json_out).write_text(line + "\n")
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def bench_reference(args):
+    """CPU path on the host cores, rank 0 only (other ranks exit 0)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle.ew_oracle import load_oracle, load_reference
+    from paper_2510_00606_b200 import configs, fabric
+
+    cfg = configs.llama2_7b()
+    layout = fabric.interleaved_layout(cfg.layer_bytes, range(cfg.dp))
+    segs = layout.segments(3)
+    S = layout.shard_bytes(3)
+    out = {}
+    cb = run_cpu_baseline(argparse.Namespace(cpu_sample_bytes=args.cpu_sample_bytes,
+                                             block_bytes=args.block_bytes), out, segs, S)
+    res = {"metric": METRIC, "value": cb["value"], "unit": "GB/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "impl": "reference",
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+           "data": "synthetic (word i = splitmix64(seed ^ i))",
+           "config": {"workload": "llama2-7b ZeRO interleaved DP=8, one rank's shard: snapshot "
+                                  "(copy + per-block checksum) then verify, bounded sample on host "
+                                  "cores", "bytes_counted": "2S + S per step",
+                      "block_bytes": args.block_bytes},
+           "cpu_baseline": cb,
+           "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    ref = load_reference()
+    if ref is not None:
+        extra = {}
+        for name, c in (("per-layer", cfg), ("per-tensor", configs.llama2_7b_per_tensor())):
+            src = ref.interleaved(c.layer_bytes, range(8))
+            dst = ref.interleaved(c.layer_bytes, [0, 1, 2, 4, 5, 6, 7])
+            secs = []
+            for _ in range(5):
+                _, _, s = ref.overlap_matrix(src, dst, c.total_bytes, [3], list(range(8)))
+                secs.append(s)
+            extra[f"overlap_matrix_8to7_{name}_ms"] = round(min(secs) * 1e3, 3)
+        t0 = time.perf_counter()
+        ref.draw(0, 0, 1, 0, 4_000_000)
+        extra["draw_muniform_per_s_1thread"] = round(4.0 / (time.perf_counter() - t0), 1)
+        g = np.random.default_rng(5).normal(size=(5, 4_194_304))
+        t0 = time.perf_counter()
+        ref.weighted_grad_average(np.full(5, 0.2), g)
+        dt = time.perf_counter() - t0
+        extra["weighted_grad_average_gbs_1thread"] = round(5 * 4_194_304 * 8 / dt / 1e9, 2)
+        res["reference_cpu"] = extra
+        res["cpu_baseline"]["reference_planner"] = "oracle/_ref (unmodified reference sources)"
+    print(json.dumps(res), flush=True)
+    if args.json_out:
+        Path(args.json_out).write_text(json.dumps(res) + "\n")
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_b200(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -264,3 +264,117 @@ void ew_oracle_weighted_fixed(const double* w, const float* g, int n_units, int6
     acc[i] = s;
   }
 }
+
+/* ---------------- multi-threaded CPU baseline (bench.py cpu_baseline) ----
+ * Same definitions as above, organised for speed on host cores: each thread
+ * takes whole checksum rows; a row whose global/local shift is a multiple of
+ * 8 is checksummed word-wise (interior words straight from memory), other
+ * rows fall back to the byte-serial definition.  Used only as the reported
+ * CPU baseline ("port": the reference has no snapshot/checksum code). */
+#include <pthread.h>
+
+typedef struct {
+  int64_t local_lo, len, delta, block;
+} row_geom;
+
+static int64_t build_rows(const int64_t* segs, int64_t n_segs, int64_t block, row_geom** out) {
+  int64_t n = ew_oracle_num_rows(segs, n_segs, block), r = 0;
+  row_geom* rows = (row_geom*)malloc(sizeof(row_geom) * (size_t)(n > 0 ? n : 1));
+  for (int64_t k = 0; k < n_segs; ++k) {
+    const int64_t glo = segs[3 * k], len = segs[3 * k + 1], loff = segs[3 * k + 2];
+    if (len <= 0) continue;
+    for (int64_t b = glo / block; b <= (glo + len - 1) / block; ++b, ++r) {
+      const int64_t lo = glo > b * block ? glo : b * block;
+      const int64_t hi = (glo + len) < (b + 1) * block ? (glo + len) : (b + 1) * block;
+      rows[r].local_lo = lo - glo + loff;
+      rows[r].len = hi - lo;
+      rows[r].delta = glo - loff;
+      rows[r].block = b;
+    }
+  }
+  *out = rows;
+  return n;
+}
+
+static void row_checksum(const row_geom* g, const uint8_t* buf, uint64_t* s0o, uint64_t* s1o) {
+  const int64_t glo = g->local_lo + g->delta, ghi = glo + g->len;
+  uint64_t s0 = 0, s1 = 0;
+  int64_t i = glo / 8;
+  const int64_t i_end = (ghi - 1) / 8;
+  for (; i <= i_end; ++i) {
+    uint64_t w = 0;
+    if ((g->delta & 7) == 0 && 8 * i >= glo && 8 * i + 8 <= ghi) {
+      memcpy(&w, buf + (8 * i - g->delta), 8);
+    } else {
+      for (int j = 0; j < 8; ++j) {
+        const int64_t x = 8 * i + j;
+        if (x >= glo && x < ghi) w |= (uint64_t)buf[x - g->delta] << (8 * j);
+      }
+    }
+    s0 += w;
+    s1 += (uint64_t)(i + 1) * w;
+  }
+  *s0o = s0;
+  *s1o = s1;
+}
+
+typedef struct {
+  const row_geom* rows;
+  int64_t lo, hi;
+  const uint8_t* src;
+  uint8_t* dst;
+  uint64_t* sums;
+  const uint64_t* expected;
+  int64_t bad;
+} mt_job;
+
+static void* mt_worker(void* p) {
+  mt_job* j = (mt_job*)p;
+  for (int64_t r = j->lo; r < j->hi; ++r) {
+    const row_geom* g = &j->rows[r];
+    if (j->dst) memcpy(j->dst + g->local_lo, j->src + g->local_lo, (size_t)g->len);
+    uint64_t s0, s1;
+    row_checksum(g, j->src, &s0, &s1);
+    if (j->expected) {
+      if (s0 != j->expected[2 * r] || s1 != j->expected[2 * r + 1]) ++j->bad;
+    } else {
+      j->sums[2 * r] = s0;
+      j->sums[2 * r + 1] = s1;
+    }
+  }
+  return NULL;
+}
+
+static int64_t run_mt(const int64_t* segs, int64_t n_segs, int64_t block, const uint8_t* src,
+                      uint8_t* dst, uint64_t* sums, const uint64_t* expected, int threads) {
+  row_geom* rows;
+  const int64_t n = build_rows(segs, n_segs, block, &rows);
+  if (threads < 1) threads = 1;
+  pthread_t* th = (pthread_t*)malloc(sizeof(pthread_t) * (size_t)threads);
+  mt_job* jobs = (mt_job*)malloc(sizeof(mt_job) * (size_t)threads);
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (mt_job){rows, n * t / threads, n * (t + 1) / threads, src, dst, sums, expected, 0};
+    pthread_create(&th[t], NULL, mt_worker, &jobs[t]);
+  }
+  int64_t bad = 0;
+  for (int t = 0; t < threads; ++t) {
+    pthread_join(th[t], NULL);
+    bad += jobs[t].bad;
+  }
+  free(th);
+  free(jobs);
+  free(rows);
+  return bad;
+}
+
+/* snap <- live + row sums of live; returns 0 */
+int64_t ew_oracle_snapshot_mt(const int64_t* segs, int64_t n_segs, int64_t block,
+                              const uint8_t* live, uint8_t* snap, uint64_t* sums, int threads) {
+  return run_mt(segs, n_segs, block, live, snap, sums, NULL, threads);
+}
+
+/* number of rows of buf whose sums differ from expected */
+int64_t ew_oracle_verify_mt(const int64_t* segs, int64_t n_segs, int64_t block,
+                            const uint8_t* buf, const uint64_t* expected, int threads) {
+  return run_mt(segs, n_segs, block, buf, NULL, NULL, expected, threads);
+}

@@ -30,6 +30,11 @@ int64_t ew_oracle_overlap(const int* s_ranks, const int* s_counts, int s_n, cons
                           const int* failed, int n_failed, const int* ring, int n_ring,
                           int64_t* out, int64_t cap);
 
+int64_t ew_oracle_snapshot_mt(const int64_t* segs, int64_t n_segs, int64_t block,
+                              const uint8_t* live, uint8_t* snap, uint64_t* sums, int threads);
+int64_t ew_oracle_verify_mt(const int64_t* segs, int64_t n_segs, int64_t block,
+                            const uint8_t* buf, const uint64_t* expected, int threads);
+
 int ew_oracle_fixed_point_bits(double absmax, int64_t total_units);
 void ew_oracle_weighted_fixed(const double* w, const float* g, int n_units, int64_t dim,
                               int frac_bits, int64_t* acc);

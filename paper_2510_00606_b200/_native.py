@@ -1,0 +1,204 @@
+"""ctypes binding of libelaskit_b200.so (include/ew_api.h).
+
+This is the Python side of the drop-in boundary: every call goes through the
+C ABI of the in-tree shared library.  There is no Python or CPU fallback for
+any device operation — if the library is missing the import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libelaskit_b200.so"
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `make -C {_PKG / 'csrc'}` "
+        "(or __graft_entry__.build()); there is no fallback implementation")
+
+lib = C.CDLL(str(LIB_PATH), mode=os.RTLD_NOW | os.RTLD_GLOBAL)
+
+# ---------------------------------------------------------------- errors ---
+
+class ElaskitError(RuntimeError):
+    """Base of the errors mapped from ew_status codes."""
+
+
+class CoverageMismatch(ElaskitError):
+    """elaskit::CoverageMismatch (param_fabric.hpp:14)."""
+
+
+class MissingBackup(ElaskitError):
+    """elaskit::MissingBackup (rng.hpp:31)."""
+
+
+class NoSurvivors(ElaskitError):
+    """elaskit::NoSurvivors (dataflow.hpp:10)."""
+
+
+class DimensionMismatch(ElaskitError):
+    """elaskit::DimensionMismatch (dataflow.hpp:13)."""
+
+
+class MismatchedDpDegree(ElaskitError):
+    """elaskit::MismatchedDpDegree (migration.hpp:16)."""
+
+
+class DisconnectedGroup(ElaskitError):
+    """elaskit::DisconnectedGroup (communicator.hpp:13)."""
+
+
+class CapacityError(ElaskitError):
+    pass
+
+
+class CudaError(ElaskitError):
+    pass
+
+
+class NcclError(ElaskitError):
+    pass
+
+
+class InvalidArgument(ElaskitError, ValueError):
+    """std::invalid_argument."""
+
+
+class OutOfRange(ElaskitError, IndexError):
+    """std::out_of_range."""
+
+
+_STATUS = {
+    1: InvalidArgument, 2: CoverageMismatch, 3: MissingBackup, 4: NoSurvivors,
+    5: DimensionMismatch, 6: MismatchedDpDegree, 7: DisconnectedGroup, 8: OutOfRange,
+    9: CapacityError, 10: CudaError, 11: NcclError, 12: ElaskitError,
+}
+
+lib.ew_last_error.restype = C.c_char_p
+lib.ew_version.restype = C.c_char_p
+
+
+def check(status: int) -> None:
+    if status != 0:
+        msg = lib.ew_last_error().decode(errors="replace")
+        raise _STATUS.get(status, ElaskitError)(msg)
+
+
+# ------------------------------------------------------------- signatures ---
+
+i32, i64, u32, u64, f64 = C.c_int, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
+vp = C.c_void_p
+P = C.POINTER
+
+
+class Segment(C.Structure):
+    _fields_ = [("global_lo", i64), ("length", i64), ("local_off", i64)]
+
+
+class Interval(C.Structure):
+    _fields_ = [("lo", i64), ("hi", i64)]
+
+
+class TransferEntry(C.Structure):
+    _fields_ = [("src_rank", C.c_int32), ("dst_rank", C.c_int32), ("lo", i64), ("hi", i64),
+                ("medium", C.c_int32), ("reserved", C.c_int32)]
+
+
+class CopyDesc(C.Structure):
+    _fields_ = [("src_role", C.c_int32), ("src_rank", C.c_int32), ("dst_role", C.c_int32),
+                ("dst_rank", C.c_int32), ("src_off", i64), ("dst_off", i64), ("bytes", i64)]
+
+
+def _sig(name, restype, *argtypes):
+    f = getattr(lib, name)
+    f.restype = restype
+    f.argtypes = list(argtypes)
+
+
+_sig("ew_layout_interleaved", i32, P(i64), i32, P(i32), i32, P(vp))
+_sig("ew_layout_contiguous", i32, P(i32), i32, i64, P(vp))
+_sig("ew_layout_from_intervals", i32, P(i32), P(i32), i32, P(Interval), i64, P(vp))
+_sig("ew_layout_free", None, vp)
+_sig("ew_layout_total_bytes", i64, vp)
+_sig("ew_layout_num_ranks", i32, vp)
+_sig("ew_layout_ranks", i32, vp, P(i32), i32)
+_sig("ew_layout_shard_bytes", i64, vp, i32)
+_sig("ew_layout_num_segments", i64, vp, i32)
+_sig("ew_layout_segments", i32, vp, i32, P(Segment), i64)
+_sig("ew_layout_validate", i32, vp)
+_sig("ew_layout_owner_of", i32, vp, i64)
+_sig("ew_integrity_check", i32, P(i32), i32, vp, P(i32), i32, P(i32), P(i32), i32, P(i32))
+_sig("ew_overlap_matrix", i32, vp, vp, P(i32), i32, P(i32), i32, P(vp))
+_sig("ew_plan_free", None, vp)
+_sig("ew_plan_num_entries", i64, vp)
+_sig("ew_plan_total_bytes_moved", i64, vp)
+_sig("ew_plan_entries", i32, vp, P(TransferEntry), i64)
+_sig("ew_plan_to_json", i32, vp, C.c_char_p, i64, P(i64))
+_sig("ew_reshard_copies", i32, vp, vp, vp, P(i32), i32, P(i32), i32, i32, i32, P(CopyDesc), i64,
+     P(i64))
+_sig("ew_reshard_microbatches", i32, P(i32), i32, i32, P(i32), i32, P(i32), P(i32))
+_sig("ew_weighted_grad_average", i32, P(f64), P(f64), i32, i64, P(f64))
+_sig("ew_philox4x64", i32, P(u64), P(u64), P(u64))
+_sig("ew_draw", i32, u64, u64, u32, u32, i32, P(f64))
+_sig("ew_plan_edit", i32, i32, P(C.c_char_p), P(i32), P(i32), P(i32), i32, P(i32), i32, P(i32),
+     i32, P(i32), i32, P(i32), P(i32), i32, P(i32), P(i32), P(i32))
+
+_sig("ew_device_count", i32, P(i32))
+_sig("ew_set_device", i32, i32)
+_sig("ew_alloc", i32, i64, P(vp))
+_sig("ew_free", i32, vp)
+_sig("ew_memset_async", i32, vp, i32, i64, vp)
+_sig("ew_memcpy_async", i32, vp, vp, i64, vp)
+_sig("ew_stream_sync", i32, vp)
+_sig("ew_device_sync", i32)
+_sig("ew_ipc_get_handle", i32, vp, C.c_char_p, P(i64))
+_sig("ew_ipc_open", i32, C.c_char_p, i64, P(vp))
+_sig("ew_ipc_close", i32, vp)
+
+_sig("ew_shardmap_create", i32, P(Segment), i64, i64, P(vp))
+_sig("ew_shardmap_free", None, vp)
+_sig("ew_shardmap_bytes", i64, vp)
+_sig("ew_shardmap_num_rows", i64, vp)
+_sig("ew_shardmap_row_blocks", i32, vp, P(i64), i64)
+_sig("ew_snapshot", i32, vp, vp, vp, vp, vp)
+_sig("ew_checksum", i32, vp, vp, vp, vp)
+_sig("ew_verify", i32, vp, vp, vp, vp, vp, i64, vp)
+_sig("ew_rows_to_blocks", i32, vp, vp, vp, i64, vp)
+_sig("ew_fill_synthetic", i32, vp, vp, u64, vp)
+
+_sig("ew_copy_program_create", i32, P(CopyDesc), i64, P(vp), i32, i32, P(vp))
+_sig("ew_copy_program_create_raw", i32, P(vp), P(vp), P(i64), P(i32), i64, P(vp))
+_sig("ew_copy_program_free", None, vp)
+_sig("ew_copy_program_stats", i32, vp, P(i64), P(i64), P(i64))
+_sig("ew_copy_program_launch", i32, vp, i32, i32, vp)
+
+_sig("ew_philox_dropout_mask", i32, u64, i64, i64, u32, u32, i64, f64, vp, vp)
+_sig("ew_philox_uniforms", i32, u64, i64, i64, u32, u32, i64, vp, vp)
+_sig("ew_philox_words", i32, u64, u64, u32, u32, u64, i64, vp, vp)
+
+_sig("ew_weighted_absmax", i32, P(vp), P(f64), i32, i64, vp, vp)
+_sig("ew_fixed_point_bits", i32, f64, i64, P(i32))
+_sig("ew_weighted_fold", i32, P(vp), P(f64), i32, i64, i32, vp, i32, vp)
+_sig("ew_fixed_to_float", i32, vp, i64, i32, vp, vp)
+_sig("ew_fixed_to_double", i32, vp, i64, i32, vp, vp)
+
+_sig("ew_comm_unique_id", i32, C.c_char_p)
+_sig("ew_comm_init", i32, C.c_char_p, i32, i32, P(vp))
+_sig("ew_comm_shrink", i32, vp, P(i32), i32, i32, P(vp))
+_sig("ew_comm_rank", i32, vp, P(i32), P(i32))
+_sig("ew_comm_destroy", i32, vp)
+_sig("ew_allreduce_i64", i32, vp, vp, i64, vp)
+_sig("ew_allreduce_u64", i32, vp, vp, i64, vp)
+_sig("ew_allreduce_max_f64", i32, vp, vp, i64, vp)
+_sig("ew_weighted_reduce", i32, vp, P(vp), P(f64), i32, i64, i64, vp, vp, vp, P(i32), vp)
+
+def int_array(values) -> C.Array:
+    values = list(values)
+    return (i32 * max(1, len(values)))(*values)
+
+
+def i64_array(values) -> C.Array:
+    values = list(values)
+    return (i64 * max(1, len(values)))(*values)

@@ -233,10 +233,10 @@ int ew_comm_shrink(ew_comm* parent, const int* exclude_ranks, int n_exclude, int
   if (parent == nullptr || out == nullptr || n_exclude < 0 || (n_exclude > 0 && !exclude_ranks))
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_comm_shrink: bad arguments");
   *out = nullptr;
-  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
   auto* c = new ew_comm();
+  // config = NULL: the shrunk communicator inherits the parent's configuration
   const ncclResult_t r =
-      ncclCommShrink(parent->nccl, const_cast<int*>(exclude_ranks), n_exclude, &c->nccl, &cfg,
+      ncclCommShrink(parent->nccl, const_cast<int*>(exclude_ranks), n_exclude, &c->nccl, nullptr,
                      abort ? NCCL_SHRINK_ABORT : NCCL_SHRINK_DEFAULT);
   if (r != ncclSuccess) {
     delete c;

@@ -1,0 +1,336 @@
+"""Device side of the recovery path: thin wrappers over the sm_100a kernels.
+
+Torch is used only as the device-memory/stream plumbing: buffers are torch
+tensors whose raw pointers are handed to libelaskit_b200.so, kernels are
+enqueued on torch's current CUDA stream.  Every op here executes in the CUDA
+library; none has a CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import _native as N
+from ._native import check, lib
+from .fabric import COPY_DTYPE, SEGMENT_DTYPE
+
+DEFAULT_BLOCK_BYTES = 64 * 1024
+
+
+def _stream(stream: Optional[torch.cuda.Stream] = None) -> C.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t: Optional[torch.Tensor]) -> C.c_void_p:
+    if t is None:
+        return C.c_void_p(None)
+    if not t.is_cuda:
+        raise ValueError("device op needs a CUDA tensor")
+    if not t.is_contiguous():
+        raise ValueError("device op needs a contiguous tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+def device_count() -> int:
+    n = C.c_int()
+    check(lib.ew_device_count(C.byref(n)))
+    return n.value
+
+
+def empty_bytes(nbytes: int, device=None) -> torch.Tensor:
+    """16-byte aligned (caching allocator: 512 B) uint8 buffer, padded to 16."""
+    return torch.empty(max(16, (int(nbytes) + 15) // 16 * 16), dtype=torch.uint8,
+                       device=device or "cuda")
+
+
+# ---------------------------------------------------------------- (a) ---
+
+class ShardMap:
+    """Packed shard buffer geometry + checksum rows, resident on the device
+    (ew_shardmap)."""
+
+    def __init__(self, segments: np.ndarray, block_bytes: int = DEFAULT_BLOCK_BYTES):
+        segs = np.ascontiguousarray(segments, dtype=SEGMENT_DTYPE)
+        self.segments = segs
+        self.block_bytes = int(block_bytes)
+        h = C.c_void_p()
+        check(lib.ew_shardmap_create(segs.ctypes.data_as(C.POINTER(N.Segment)), len(segs),
+                                     self.block_bytes, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.ew_shardmap_free(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def nbytes(self) -> int:
+        return lib.ew_shardmap_bytes(self._h)
+
+    @property
+    def num_rows(self) -> int:
+        return lib.ew_shardmap_num_rows(self._h)
+
+    def row_blocks(self) -> np.ndarray:
+        out = np.zeros(max(1, self.num_rows), dtype=np.int64)
+        check(lib.ew_shardmap_row_blocks(self._h, out.ctypes.data_as(C.POINTER(C.c_int64)),
+                                         self.num_rows))
+        return out[:self.num_rows]
+
+    def new_row_sums(self, device=None) -> torch.Tensor:
+        return torch.zeros(2 * max(1, self.num_rows), dtype=torch.int64, device=device or "cuda")
+
+
+def snapshot(m: ShardMap, live: torch.Tensor, snap: torch.Tensor, row_sums: torch.Tensor,
+             stream=None) -> None:
+    """snap <- live fused with the per-block checksum rows of live."""
+    _check_buf(m, live)
+    _check_buf(m, snap)
+    check(lib.ew_snapshot(m.handle, _ptr(live), _ptr(snap), _ptr(row_sums), _stream(stream)))
+
+
+def checksum(m: ShardMap, buf: torch.Tensor, row_sums: torch.Tensor, stream=None) -> None:
+    _check_buf(m, buf)
+    check(lib.ew_checksum(m.handle, _ptr(buf), _ptr(row_sums), _stream(stream)))
+
+
+def verify(m: ShardMap, buf: torch.Tensor, expected: torch.Tensor, bad_count: torch.Tensor,
+           bad_rows: Optional[torch.Tensor] = None, stream=None) -> None:
+    """bad_count (device int32[1]) <- number of rows whose checksum differs."""
+    _check_buf(m, buf)
+    cap = 0 if bad_rows is None else bad_rows.numel()
+    check(lib.ew_verify(m.handle, _ptr(buf), _ptr(expected), _ptr(bad_count), _ptr(bad_rows), cap,
+                        _stream(stream)))
+
+
+def rows_to_blocks(m: ShardMap, row_sums: torch.Tensor, block_sums: torch.Tensor,
+                   stream=None) -> None:
+    check(lib.ew_rows_to_blocks(m.handle, _ptr(row_sums), _ptr(block_sums),
+                                block_sums.numel() // 2, _stream(stream)))
+
+
+def fill_synthetic(m: ShardMap, buf: torch.Tensor, seed: int, stream=None) -> None:
+    _check_buf(m, buf)
+    check(lib.ew_fill_synthetic(m.handle, _ptr(buf), int(seed), _stream(stream)))
+
+
+def _check_buf(m: ShardMap, buf: torch.Tensor) -> None:
+    if buf.numel() * buf.element_size() < m.nbytes:
+        raise ValueError(f"buffer holds {buf.numel() * buf.element_size()} bytes, "
+                         f"shard needs {m.nbytes}")
+
+
+# ---------------------------------------------------------------- (b) ---
+
+class CopyProgram:
+    """A GPU's reshard copies, resolved to pointers and resident on the device."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+
+    @classmethod
+    def from_descs(cls, descs: np.ndarray, buf_table: Dict[Tuple[int, int], int],
+                   table_ranks: int, exec_rank: int) -> "CopyProgram":
+        d = np.ascontiguousarray(descs, dtype=COPY_DTYPE)
+        table = (C.c_void_p * (3 * table_ranks))()
+        for (role, rank), ptr in buf_table.items():
+            table[role * table_ranks + rank] = ptr
+        h = C.c_void_p()
+        check(lib.ew_copy_program_create(d.ctypes.data_as(C.POINTER(N.CopyDesc)), len(d), table,
+                                         table_ranks, exec_rank, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def from_pointers(cls, srcs: Sequence[int], dsts: Sequence[int], nbytes: Sequence[int],
+                      remote: Sequence[bool]) -> "CopyProgram":
+        n = len(nbytes)
+        s = (C.c_void_p * max(1, n))(*srcs)
+        d = (C.c_void_p * max(1, n))(*dsts)
+        b = N.i64_array(nbytes)
+        r = N.int_array([1 if x else 0 for x in remote])
+        h = C.c_void_p()
+        check(lib.ew_copy_program_create_raw(s, d, b, r, n, C.byref(h)))
+        return cls(h)
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.ew_copy_program_free(self._h)
+            self._h = None
+
+    def stats(self) -> Tuple[int, int, int]:
+        n, r, l = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.ew_copy_program_stats(self._h, C.byref(n), C.byref(r), C.byref(l)))
+        return n.value, r.value, l.value
+
+    def launch(self, n_ctas: int = 0, remote_ctas: int = 0, stream=None) -> None:
+        check(lib.ew_copy_program_launch(self._h, n_ctas, remote_ctas, _stream(stream)))
+
+
+def ipc_handle(t: torch.Tensor) -> Tuple[bytes, int]:
+    h = C.create_string_buffer(64)
+    off = C.c_int64()
+    check(lib.ew_ipc_get_handle(_ptr(t), h, C.byref(off)))
+    return h.raw, off.value
+
+
+def ipc_open(handle: bytes, offset: int) -> int:
+    p = C.c_void_p()
+    check(lib.ew_ipc_open(handle, offset, C.byref(p)))
+    return p.value
+
+
+def ipc_close(ptr: int) -> None:
+    check(lib.ew_ipc_close(C.c_void_p(ptr)))
+
+
+# ---------------------------------------------------------------- (c) ---
+
+def mask_words(n_elems: int) -> int:
+    return (int(n_elems) + 31) // 32
+
+
+def dropout_mask(seed: int, sample_lo: int, n_samples: int, layer_id: int, op_index: int,
+                 n_elems: int, keep_probability: float, out: Optional[torch.Tensor] = None,
+                 stream=None) -> torch.Tensor:
+    """Packed keep-bits [n_samples, ceil(n_elems/32)] int32 (bit = element kept)."""
+    if out is None:
+        out = torch.empty((n_samples, mask_words(n_elems)), dtype=torch.int32, device="cuda")
+    check(lib.ew_philox_dropout_mask(seed, sample_lo, n_samples, layer_id, op_index, n_elems,
+                                     float(keep_probability), _ptr(out), _stream(stream)))
+    return out
+
+
+def philox_uniforms(seed: int, sample_lo: int, n_samples: int, layer_id: int, op_index: int,
+                    n_elems: int, stream=None) -> torch.Tensor:
+    out = torch.empty((n_samples, n_elems), dtype=torch.float64, device="cuda")
+    check(lib.ew_philox_uniforms(seed, sample_lo, n_samples, layer_id, op_index, n_elems,
+                                 _ptr(out), _stream(stream)))
+    return out
+
+
+def philox_words(seed: int, sample_id: int, layer_id: int, op_index: int, block_lo: int,
+                 n_blocks: int, stream=None) -> torch.Tensor:
+    out = torch.empty((n_blocks, 4), dtype=torch.int64, device="cuda")
+    check(lib.ew_philox_words(seed, sample_id, layer_id, op_index, block_lo, n_blocks, _ptr(out),
+                              _stream(stream)))
+    return out
+
+
+# ---------------------------------------------------------------- (d) ---
+
+def _units(units: Sequence[torch.Tensor], weights: Sequence[float]):
+    if len(units) != len(weights):
+        raise ValueError("one weight per unit")
+    n = None
+    for u in units:
+        if u.dtype != torch.float32:
+            raise ValueError("units must be float32")
+        n = u.numel() if n is None else n
+        if u.numel() != n:
+            raise N.DimensionMismatch(f"gradient vectors differ in length: {u.numel()} vs {n}")
+    ptrs = (C.c_void_p * max(1, len(units)))(*[u.data_ptr() for u in units])
+    w = (C.c_double * max(1, len(weights)))(*[float(x) for x in weights])
+    return ptrs, w, (n or 0)
+
+
+def weighted_absmax(units, weights, out: Optional[torch.Tensor] = None, stream=None):
+    ptrs, w, n = _units(units, weights)
+    if out is None:
+        out = torch.empty(1, dtype=torch.float64, device="cuda")
+    check(lib.ew_weighted_absmax(ptrs, w, len(units), n, _ptr(out), _stream(stream)))
+    return out
+
+
+def fixed_point_bits(global_absmax: float, total_units: int) -> int:
+    f = C.c_int()
+    check(lib.ew_fixed_point_bits(float(global_absmax), int(total_units), C.byref(f)))
+    return f.value
+
+
+def weighted_fold(units, weights, frac_bits: int, acc: torch.Tensor, accumulate: bool = False,
+                  stream=None) -> torch.Tensor:
+    ptrs, w, n = _units(units, weights)
+    if acc.dtype != torch.int64 or acc.numel() < n:
+        raise ValueError("acc must be int64 with one slot per element")
+    check(lib.ew_weighted_fold(ptrs, w, len(units), n, int(frac_bits), _ptr(acc),
+                               int(accumulate), _stream(stream)))
+    return acc
+
+
+def fixed_to_float(acc: torch.Tensor, frac_bits: int, out: Optional[torch.Tensor] = None,
+                   stream=None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(acc.numel(), dtype=torch.float32, device=acc.device)
+    check(lib.ew_fixed_to_float(_ptr(acc), acc.numel(), int(frac_bits), _ptr(out),
+                                _stream(stream)))
+    return out
+
+
+def fixed_to_double(acc: torch.Tensor, frac_bits: int, out: Optional[torch.Tensor] = None,
+                    stream=None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(acc.numel(), dtype=torch.float64, device=acc.device)
+    check(lib.ew_fixed_to_double(_ptr(acc), acc.numel(), int(frac_bits), _ptr(out),
+                                 _stream(stream)))
+    return out
+
+
+class Communicator:
+    """NCCL communicator of the DP group (ew_comm), shrinkable in place."""
+
+    def __init__(self, handle: C.c_void_p):
+        self._h = handle
+        r, n = C.c_int(), C.c_int()
+        check(lib.ew_comm_rank(self._h, C.byref(r), C.byref(n)))
+        self.rank, self.size = r.value, n.value
+
+    @staticmethod
+    def unique_id() -> bytes:
+        b = C.create_string_buffer(128)
+        check(lib.ew_comm_unique_id(b))
+        return b.raw
+
+    @classmethod
+    def init(cls, uid: bytes, nranks: int, rank: int) -> "Communicator":
+        h = C.c_void_p()
+        check(lib.ew_comm_init(uid, nranks, rank, C.byref(h)))
+        return cls(h)
+
+    def shrink(self, exclude: Sequence[int], abort: bool = False) -> Optional["Communicator"]:
+        """ncclCommShrink; returns None on an excluded rank."""
+        h = C.c_void_p()
+        check(lib.ew_comm_shrink(self._h, N.int_array(exclude), len(exclude), int(abort),
+                                 C.byref(h)))
+        return Communicator(h) if h.value else None
+
+    def destroy(self) -> None:
+        if self._h is not None and self._h.value:
+            check(lib.ew_comm_destroy(self._h))
+            self._h = None
+
+    def allreduce_i64(self, t: torch.Tensor, stream=None) -> None:
+        check(lib.ew_allreduce_i64(self._h, _ptr(t), t.numel(), _stream(stream)))
+
+    def allreduce_u64(self, t: torch.Tensor, stream=None) -> None:
+        check(lib.ew_allreduce_u64(self._h, _ptr(t), t.numel(), _stream(stream)))
+
+    def allreduce_max_f64(self, t: torch.Tensor, stream=None) -> None:
+        check(lib.ew_allreduce_max_f64(self._h, _ptr(t), t.numel(), _stream(stream)))
+
+    def weighted_reduce(self, units, weights, total_units: int, out: torch.Tensor,
+                        ws_acc: torch.Tensor, ws_max: torch.Tensor, stream=None) -> int:
+        """Full (d) path; returns the fixed-point fraction bits used."""
+        ptrs, w, n = _units(units, weights)
+        f = C.c_int()
+        check(lib.ew_weighted_reduce(self._h, ptrs, w, len(units), int(total_units), n,
+                                     _ptr(ws_acc), _ptr(ws_max), _ptr(out), C.byref(f),
+                                     _stream(stream)))
+        return f.value

@@ -1,0 +1,205 @@
+"""Interleaved-ZeRO live remap across GPUs.
+
+One process per GPU.  Every rank runs the same host planning (integrity
+check -> overlap_matrix -> lowering to its copy program, all C++), peers
+exchange CUDA IPC handles of their shard buffers over torch.distributed
+(plumbing only), and each GPU then executes its program in ONE kernel launch:
+remote copies are 128-bit stores into peer HBM over NVLink/NVSwitch, local
+copies (retained bytes, ring-holder self lanes) stream through local HBM.
+No NCCL on this path — the exchange is the plan.
+
+`emulate_on_one_gpu` runs the same programs for all ranks on a single GPU
+(rank buffers side by side) so the N-rank lowering can be checked where fewer
+GPUs than ranks exist.
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+import torch
+
+from . import device as dev
+from .fabric import (ROLE_NEW, ROLE_OLD, ROLE_REPLICA, PartitionLayout, SnapshotRing,
+                     TransferPlan, integrity_check, interleaved_layout, overlap_matrix,
+                     reshard_copies)
+from ._native import CoverageMismatch
+
+
+@dataclass
+class ReshardPlan:
+    """Host-side plan of one membership change, identical on every rank."""
+
+    layer_bytes: List[int]
+    old_ranks: List[int]
+    new_ranks: List[int]
+    failed: List[int]
+    src: PartitionLayout
+    dst: PartitionLayout
+    ring: SnapshotRing
+    plan: TransferPlan
+    plan_seconds: float
+
+    @classmethod
+    def build(cls, layer_bytes: Sequence[int], old_ranks: Sequence[int],
+              new_ranks: Sequence[int]) -> "ReshardPlan":
+        t0 = time.perf_counter()
+        old_ranks, new_ranks = sorted(old_ranks), sorted(new_ranks)
+        failed = sorted(set(old_ranks) - set(new_ranks))
+        src = interleaved_layout(layer_bytes, old_ranks)
+        dst = interleaved_layout(layer_bytes, new_ranks)
+        ring = SnapshotRing(list(old_ranks))
+        rep = integrity_check(ring, src, failed)
+        if not rep.recoverable:
+            raise CoverageMismatch(
+                f"ranks {sorted(rep.missing)} lost together with their ring holders")
+        plan = overlap_matrix(src, dst, failed, ring)
+        return cls(list(layer_bytes), old_ranks, new_ranks, failed, src, dst, ring, plan,
+                   time.perf_counter() - t0)
+
+    def copies(self, exec_rank: int, push: bool = True) -> np.ndarray:
+        return reshard_copies(self.plan, self.src, self.dst, self.failed, self.ring, exec_rank,
+                              push)
+
+    def replica_of(self, holder: int) -> Optional[int]:
+        """Rank whose old shard `holder` keeps (SnapshotRing::backs_up)."""
+        if holder not in self.old_ranks or len(self.old_ranks) < 2:
+            return None
+        return self.ring.backs_up(holder)
+
+    def traffic(self) -> Dict[str, object]:
+        """Per-rank NVLink egress/ingress and local bytes of the plan (+ retained)."""
+        ranks = sorted(set(self.old_ranks) | set(self.new_ranks))
+        egress = {r: 0 for r in ranks}
+        ingress = {r: 0 for r in ranks}
+        local = {r: 0 for r in ranks}
+        for e in self.plan.entries:
+            n = int(e["hi"] - e["lo"])
+            s, d = int(e["src_rank"]), int(e["dst_rank"])
+            if s == d:
+                local[s] += n
+            else:
+                egress[s] += n
+                ingress[d] += n
+        for r in ranks:
+            if r in self.failed:
+                continue
+            for c in self.copies(r, push=True):
+                if c["src_rank"] == c["dst_rank"] == r and c["src_role"] == ROLE_OLD:
+                    local[r] += int(c["bytes"])
+        bottleneck = max(max(egress.values()), max(ingress.values()))
+        return {"egress": egress, "ingress": ingress, "local": local,
+                "nvlink_bytes": sum(egress.values()), "bottleneck_bytes": bottleneck,
+                "total_bytes_moved": int(self.plan.total_bytes_moved)}
+
+
+@dataclass
+class RankBuffers:
+    old: Optional[torch.Tensor]
+    replica: Optional[torch.Tensor]
+    new: Optional[torch.Tensor]
+
+
+def shard_map(layout: PartitionLayout, rank: int, block_bytes: int = dev.DEFAULT_BLOCK_BYTES):
+    return dev.ShardMap(layout.segments(rank), block_bytes)
+
+
+class ReshardExecutor:
+    """Multi-process executor: one instance per rank/GPU."""
+
+    def __init__(self, rp: ReshardPlan, rank: int, push: bool = True):
+        self.rp = rp
+        self.rank = rank
+        self.push = push
+        self.program: Optional[dev.CopyProgram] = None
+        self._opened: List[int] = []
+
+    def allocate(self) -> RankBuffers:
+        rp, r = self.rp, self.rank
+        old = dev.empty_bytes(rp.src.shard_bytes(r)) if r in rp.old_ranks else None
+        rep_of = rp.replica_of(r)
+        replica = (dev.empty_bytes(rp.src.shard_bytes(rep_of))
+                   if rep_of is not None and rep_of in rp.failed else None)
+        new = dev.empty_bytes(rp.dst.shard_bytes(r)) if r in rp.new_ranks else None
+        return RankBuffers(old, replica, new)
+
+    def bind(self, bufs: RankBuffers, group=None) -> None:
+        """Exchange IPC handles with every rank and build this GPU's program."""
+        import torch.distributed as dist
+
+        mine = {}
+        for role, t in ((ROLE_OLD, bufs.old), (ROLE_REPLICA, bufs.replica), (ROLE_NEW, bufs.new)):
+            if t is not None:
+                mine[role] = dev.ipc_handle(t)
+        world = dist.get_world_size(group)
+        gathered: List[Dict[int, Tuple[bytes, int]]] = [None] * world  # type: ignore
+        dist.all_gather_object(gathered, (self.rank, mine), group=group)
+        table: Dict[Tuple[int, int], int] = {}
+        local = {ROLE_OLD: bufs.old, ROLE_REPLICA: bufs.replica, ROLE_NEW: bufs.new}
+        for role, t in local.items():
+            if t is not None:
+                table[(role, self.rank)] = t.data_ptr()
+        descs = self.rp.copies(self.rank, self.push)
+        needed = set()
+        for c in descs:
+            for role, rank in ((int(c["src_role"]), int(c["src_rank"])),
+                               (int(c["dst_role"]), int(c["dst_rank"]))):
+                if rank != self.rank:
+                    needed.add((role, rank))
+        for peer_rank, handles in gathered:
+            for role, (h, off) in handles.items():
+                if (role, peer_rank) in needed:
+                    p = dev.ipc_open(h, off)
+                    self._opened.append(p)
+                    table[(role, peer_rank)] = p
+        n_table = max(max(self.rp.old_ranks + self.rp.new_ranks) + 1, world)
+        self.program = dev.CopyProgram.from_descs(descs, table, n_table, self.rank)
+
+    def launch(self, n_ctas: int = 0, remote_ctas: int = 0, stream=None) -> None:
+        if self.program is not None:
+            self.program.launch(n_ctas, remote_ctas, stream)
+
+    def close(self) -> None:
+        self.program = None
+        for p in self._opened:
+            dev.ipc_close(p)
+        self._opened = []
+
+
+def emulate_on_one_gpu(rp: ReshardPlan, seed: int, push: bool = True,
+                       block_bytes: int = dev.DEFAULT_BLOCK_BYTES):
+    """Run every rank's program on the current GPU; returns (new buffers,
+    expected buffers) keyed by rank for comparison."""
+    bufs: Dict[int, RankBuffers] = {}
+    for r in sorted(set(rp.old_ranks) | set(rp.new_ranks)):
+        ex = ReshardExecutor(rp, r, push)
+        bufs[r] = ex.allocate()
+        if bufs[r].old is not None and r not in rp.failed:
+            dev.fill_synthetic(shard_map(rp.src, r, block_bytes), bufs[r].old, seed)
+        if bufs[r].replica is not None:
+            dev.fill_synthetic(shard_map(rp.src, rp.replica_of(r), block_bytes), bufs[r].replica,
+                               seed)
+        if bufs[r].new is not None:
+            bufs[r].new.fill_(0xA5)
+    table = {}
+    for r, b in bufs.items():
+        for role, t in ((ROLE_OLD, b.old), (ROLE_REPLICA, b.replica), (ROLE_NEW, b.new)):
+            if t is not None:
+                table[(role, r)] = t.data_ptr()
+    n_table = max(bufs) + 1
+    progs = []
+    for r in bufs:
+        if r in rp.failed:
+            continue
+        progs.append(dev.CopyProgram.from_descs(rp.copies(r, push), table, n_table, r))
+    for p in progs:
+        p.launch()
+    torch.cuda.synchronize()
+    expected = {}
+    for r in rp.new_ranks:
+        e = dev.empty_bytes(rp.dst.shard_bytes(r))
+        dev.fill_synthetic(shard_map(rp.dst, r, block_bytes), e, seed)
+        expected[r] = e
+    return {r: bufs[r].new for r in rp.new_ranks}, expected
