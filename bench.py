@@ -350,6 +350,8 @@ def run_reshard(args, rank, world, out):
     uid = [dev.Communicator.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = dev.Communicator.init(uid[0], world, rank)
+    warm = torch.zeros(1024, dtype=torch.int64, device="cuda")
+    comm.allreduce_i64(warm)  # a training job's DP communicator is warm
     barrier(world)
     t0 = time.perf_counter()
     pool = {(a, b) for a in old for b in old if a < b}

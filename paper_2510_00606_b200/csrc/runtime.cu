@@ -234,9 +234,13 @@ int ew_comm_shrink(ew_comm* parent, const int* exclude_ranks, int n_exclude, int
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_comm_shrink: bad arguments");
   *out = nullptr;
   auto* c = new ew_comm();
-  // config = NULL: the shrunk communicator inherits the parent's configuration
+  // A planned departure reuses the parent's buffers and connections
+  // (shrinkShare), so only the membership edit is paid; after a crash
+  // (abort) nothing of the parent can be trusted and it is rebuilt.
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  cfg.shrinkShare = abort ? 0 : 1;
   const ncclResult_t r =
-      ncclCommShrink(parent->nccl, const_cast<int*>(exclude_ranks), n_exclude, &c->nccl, nullptr,
+      ncclCommShrink(parent->nccl, const_cast<int*>(exclude_ranks), n_exclude, &c->nccl, &cfg,
                      abort ? NCCL_SHRINK_ABORT : NCCL_SHRINK_DEFAULT);
   if (r != ncclSuccess) {
     delete c;

@@ -1,0 +1,121 @@
+"""N > 1 GPUs, one process per GPU (the deployment shape): the reshard
+executor over CUDA-IPC peer pointers, the NCCL communicator shrink, and the
+world-size determinism of the weighted reduce.  Skipped with < 2 GPUs; run on
+a 2- or 4-GPU box with `gpurun --gpus N`."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, result_dir):
+    import torch.distributed as dist
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from paper_2510_00606_b200 import configs, device as dev
+    from paper_2510_00606_b200.reshard import ReshardExecutor, ReshardPlan, shard_map
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(rank)
+    dist.init_process_group("nccl", rank=rank, world_size=world,
+                            device_id=torch.device("cuda", rank))
+    report = {}
+    try:
+        # (b) reshard world -> world-1 of a scaled 7B state, every drop position
+        cfg = configs.scaled(configs.llama2_7b_per_tensor(), 2e-3)
+        for drop in range(world):
+            old = list(range(world))
+            new = [r for r in old if r != drop]
+            rp = ReshardPlan.build(cfg.layer_bytes, old, new)
+            for push in (True, False):
+                ex = ReshardExecutor(rp, rank, push=push)
+                bufs = ex.allocate()
+                if bufs.old is not None:
+                    dev.fill_synthetic(shard_map(rp.src, rank), bufs.old, 99)
+                if bufs.replica is not None:
+                    dev.fill_synthetic(shard_map(rp.src, rp.replica_of(rank)), bufs.replica, 99)
+                if bufs.new is not None:
+                    bufs.new.fill_(0xA5)
+                dist.barrier()
+                ex.bind(bufs)
+                dist.barrier()
+                torch.cuda.synchronize()
+                dist.barrier()
+                ex.launch()
+                torch.cuda.synchronize()
+                dist.barrier()
+                ok = True
+                if bufs.new is not None:
+                    exp = dev.empty_bytes(rp.dst.shard_bytes(rank))
+                    dev.fill_synthetic(shard_map(rp.dst, rank), exp, 99)
+                    n = rp.dst.shard_bytes(rank)
+                    ok = bool(torch.equal(bufs.new[:n], exp[:n]))
+                report[f"reshard drop{drop} push={push}"] = ok
+                ex.close()
+                dist.barrier()
+        # NCCL communicator: init, shrink without the last rank, reduce
+        uid = [dev.Communicator.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = dev.Communicator.init(uid[0], world, rank)
+        n_units, dim = 12, 100_003
+        rng = np.random.default_rng(21)
+        g = rng.normal(0, 1e-3, size=(n_units, dim)).astype(np.float32)
+        g[3, 5] = 1e2
+        w = rng.random(n_units) / n_units
+        # units split over the ranks of the shrunk communicator
+        survivors = list(range(world - 1)) if world > 2 else list(range(world))
+        shrunk = comm.shrink([world - 1]) if world > 2 and rank != world - 1 else (comm if world <= 2 else None)
+        if shrunk is not None:
+            k = len(survivors)
+            mine = [u for u in range(n_units) if u % k == shrunk.rank]
+            units = [torch.from_numpy(g[u]).cuda() for u in mine]
+            out = torch.empty(dim, dtype=torch.float32, device="cuda")
+            acc = torch.empty(dim, dtype=torch.int64, device="cuda")
+            mx = torch.empty(1, dtype=torch.float64, device="cuda")
+            f = shrunk.weighted_reduce(units, [w[u] for u in mine], n_units, out, acc, mx)
+            torch.cuda.synchronize()
+            # single-GPU fold of all units, same scale
+            all_units = [torch.from_numpy(x).cuda() for x in g]
+            acc1 = torch.empty(dim, dtype=torch.int64, device="cuda")
+            dev.weighted_fold(all_units, w, f, acc1)
+            single = dev.fixed_to_float(acc1, f)
+            report["reduce bit-identical to 1-GPU fold"] = bool(torch.equal(out, single))
+            report["shrunk size"] = shrunk.size
+        if world > 2 and shrunk is not None:
+            shrunk.destroy()
+        comm.destroy()
+    except Exception as e:  # report, do not hang the other ranks
+        report["error"] = repr(e)
+    import json
+    Path(result_dir, f"rank{rank}.json").write_text(json.dumps(report))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_multi_gpu_reshard_comm_reduce(world, tmp_path):
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs")
+    import json
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    for r in range(world):
+        rep = json.loads((tmp_path / f"rank{r}.json").read_text())
+        assert "error" not in rep, rep
+        for k, v in rep.items():
+            if k.startswith("reshard") or k.startswith("reduce"):
+                assert v is True, (r, k)
+        if "shrunk size" in rep:
+            assert rep["shrunk size"] == (world - 1 if world > 2 else world)
