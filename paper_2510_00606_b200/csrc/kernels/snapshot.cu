@@ -31,10 +31,10 @@ namespace {
 constexpr int kThreads = 256;
 constexpr int kUnroll = 8;
 
-__device__ __forceinline__ uint64_t byte_mask(int64_t x, int64_t a, int64_t e) {
-  // bytes of the 8-byte word at local x that fall in [a, e)
-  const int64_t lo = min(max(a - x, (int64_t)0), (int64_t)8);
-  const int64_t hi = min(max(e - x, (int64_t)0), (int64_t)8);
+__device__ __forceinline__ uint64_t byte_mask(int x, int a, int e) {
+  // bytes of the 8-byte word at row-relative x that fall in [a, e)
+  const int lo = min(max(a - x, 0), 8);
+  const int hi = min(max(e - x, 0), 8);
   if (hi <= lo) return 0;
   const uint64_t upper = (hi == 8) ? ~0ULL : ((1ULL << (8 * hi)) - 1);
   return upper & (~0ULL << (8 * lo));
@@ -48,15 +48,76 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 
 enum class Mode { kSnapshot, kChecksum, kVerify };
 
+// One 16-byte vector of a row: optional copy, edge masking, checksum terms.
+// `idx` is the vector index inside the row, `i` the thread's iteration.
+template <Mode M, bool kShift>
+__device__ __forceinline__ void row_vector(const uint4& v, int idx, int nvec, int head, int end,
+                                           int sh, bool copy_first, int pidx, int partial,
+                                           uint4* __restrict__ dvec, uint64_t& t1, uint64_t& t2,
+                                           uint64_t& odd, uint64_t& bsum) {
+  const bool edge = (idx == 0) | (idx == nvec - 1);
+  if (M == Mode::kSnapshot && idx < nvec) {
+    // each 16-byte vector is copied by the row that holds its first byte
+    if (idx > 0 || copy_first) {
+      if (idx != pidx) {
+        st_plain(dvec + idx, v);
+      } else {  // the buffer ends inside this vector: copy its valid bytes only
+        const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
+        uint8_t* d = reinterpret_cast<uint8_t*>(dvec + idx);
+        for (int k = 0; k < partial; ++k) d[k] = b[k];
+      }
+    }
+  }
+  uint64_t w0 = lo64(v);
+  uint64_t w1 = hi64(v);
+  if (edge) {  // row-relative byte coordinates: the row is [head, end)
+    w0 &= byte_mask(16 * idx, head, end);
+    w1 &= byte_mask(16 * idx + 8, head, end);
+  }
+  uint64_t c0 = w0, c1 = w1, b0 = 0, b1 = 0;
+  if (kShift) {
+    b0 = w0 >> (64 - 8 * sh);
+    b1 = w1 >> (64 - 8 * sh);
+    c0 = (w0 << (8 * sh)) + b0;
+    c1 = (w1 << (8 * sh)) + b1;
+    bsum += b0 + b1;
+  }
+  t1 += c0 + c1;
+  t2 += t1;
+  odd += c1;
+}
+
+template <Mode M, bool kShift>
+__device__ __forceinline__ void row_body(const uint4* __restrict__ svec, uint4* __restrict__ dvec,
+                                         int nvec, int head, int end, int sh, bool copy_first,
+                                         int pidx, int partial, int& n_exec, uint64_t& t1, uint64_t& t2,
+                                         uint64_t& odd, uint64_t& bsum) {
+  const int tid = threadIdx.x;
+  const int iters = (nvec + kThreads - 1) / kThreads;
+  n_exec = (iters + kUnroll - 1) / kUnroll * kUnroll;
+  for (int it = 0; it < iters; it += kUnroll) {
+    uint4 val[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int idx = tid + (it + u) * kThreads;
+      val[u] = idx < nvec ? ld_stream(svec + idx) : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u)
+      row_vector<M, kShift>(val[u], tid + (it + u) * kThreads, nvec, head, end, sh, copy_first,
+                            pidx, partial, dvec, t1, t2, odd, bsum);
+  }
+}
+
 template <Mode M>
-__global__ void __launch_bounds__(kThreads) row_kernel(ShardMapView map,
-                                                       const uint8_t* __restrict__ src,
-                                                       uint8_t* __restrict__ dst,
-                                                       uint64_t* __restrict__ row_sums,
-                                                       const uint64_t* __restrict__ expected,
-                                                       uint32_t* __restrict__ bad_count,
-                                                       int64_t* __restrict__ bad_rows,
-                                                       int64_t bad_cap) {
+__global__ void __launch_bounds__(kThreads, 4) row_kernel(ShardMapView map,
+                                                          const uint8_t* __restrict__ src,
+                                                          uint8_t* __restrict__ dst,
+                                                          uint64_t* __restrict__ row_sums,
+                                                          const uint64_t* __restrict__ expected,
+                                                          uint32_t* __restrict__ bad_count,
+                                                          int64_t* __restrict__ bad_rows,
+                                                          int64_t bad_cap) {
   __shared__ uint64_t red0[kThreads / 32];
   __shared__ uint64_t red1[kThreads / 32];
   const int tid = threadIdx.x;
@@ -66,57 +127,33 @@ __global__ void __launch_bounds__(kThreads) row_kernel(ShardMapView map,
     const int64_t a = g.local_lo;
     const int64_t e = g.local_lo + g.len;
     const int64_t v_lo = a >> 4;
-    const int64_t nvec = ((e + 15) >> 4) - v_lo;
+    // row-local 32-bit geometry (a row is at most one checksum block)
+    const int nvec = static_cast<int>(((e + 15) >> 4) - v_lo);
+    const int head = static_cast<int>(a & 15);
+    const int end = head + static_cast<int>(g.len);
     const int sh = static_cast<int>(g.delta & 7);  // delta >= 0 for packed shards
+    const bool copy_first = head == 0;
+    // the buffer's last vector may be partial: copy only its valid bytes
+    const int partial = static_cast<int>(map.total_bytes & 15);
+    const int64_t last_vec = (map.total_bytes - 1) >> 4;
+    const int pidx = (partial && last_vec >= v_lo && last_vec < v_lo + nvec)
+                         ? static_cast<int>(last_vec - v_lo) : -1;
     const int64_t q_t = floor_div(16 * (v_lo + tid) + g.delta, 8);
+    const uint4* svec = reinterpret_cast<const uint4*>(src) + v_lo;
+    uint4* dvec = (M == Mode::kSnapshot) ? reinterpret_cast<uint4*>(dst) + v_lo : nullptr;
 
     uint64_t t1 = 0, t2 = 0, odd = 0, bsum = 0;
-    const int64_t iters = (nvec + kThreads - 1) / kThreads;
-    const int64_t n_exec = (iters + kUnroll - 1) / kUnroll * kUnroll;
-
-    for (int64_t it = 0; it < iters; it += kUnroll) {
-      uint4 val[kUnroll];
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t idx = tid + (it + u) * kThreads;
-        if (idx < nvec) val[u] = ld_stream(src + 16 * (v_lo + idx));
-        else val[u] = make_uint4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const int64_t idx = tid + (it + u) * kThreads;
-        const int64_t x = 16 * (v_lo + idx);
-        if (M == Mode::kSnapshot && idx < nvec && x >= a) {
-          // each 16-byte vector is copied by the row that holds its first byte
-          if (x + 16 <= map.total_bytes) {
-            st_plain(dst + x, val[u]);
-          } else {
-            const uint8_t* b = reinterpret_cast<const uint8_t*>(&val[u]);
-            for (int k = 0; k < 16 && x + k < map.total_bytes; ++k) dst[x + k] = b[k];
-          }
-        }
-        uint64_t w0 = lo64(val[u]);
-        uint64_t w1 = hi64(val[u]);
-        if (x < a || x + 16 > e) {
-          w0 &= byte_mask(x, a, e);
-          w1 &= byte_mask(x + 8, a, e);
-        }
-        uint64_t c0 = w0, c1 = w1, b0 = 0, b1 = 0;
-        if (sh != 0) {
-          b0 = w0 >> (64 - 8 * sh);
-          b1 = w1 >> (64 - 8 * sh);
-          c0 = (w0 << (8 * sh)) + b0;
-          c1 = (w1 << (8 * sh)) + b1;
-        }
-        t1 += c0 + c1;
-        t2 += t1;
-        odd += c1;
-        bsum += b0 + b1;
-      }
-    }
+    int n_exec = 0;
+    if (sh == 0)
+      row_body<M, false>(svec, dvec, nvec, head, end, sh, copy_first, pidx, partial, n_exec, t1,
+                         t2, odd, bsum);
+    else
+      row_body<M, true>(svec, dvec, nvec, head, end, sh, copy_first, pidx, partial, n_exec, t1,
+                        t2, odd, bsum);
     uint64_t s0 = t1;
     uint64_t s1 = static_cast<uint64_t>(q_t + 1) * t1 +
-                  512ULL * (static_cast<uint64_t>(n_exec) * t1 - t2) + odd + bsum;
+                  static_cast<uint64_t>(2 * kThreads) *
+                      (static_cast<uint64_t>(n_exec) * t1 - t2) + odd + bsum;
 
     s0 = warp_sum_u64(s0);
     s1 = warp_sum_u64(s1);
