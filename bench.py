@@ -336,7 +336,7 @@ def run_reshard(args, rank, world, out):
 
     t0 = time.perf_counter()
     rp = ReshardPlan.build(lb, old, new)
-    ex = ReshardExecutor(rp, rank, push=True)
+    ex = ReshardExecutor(rp, rank, push=False)  # receivers pull over NVLink
     t_plan = time.perf_counter() - t0
     bufs = ex.allocate()
     if bufs.old is not None:

@@ -1,18 +1,26 @@
 // (b) Reshard executor: the planner's TransferPlan lowered to copies and run
-// as one kernel over NVLink/NVSwitch peer pointers plus local HBM.
+// over NVLink/NVSwitch peer pointers plus local HBM.
 //
 // The reference only *times* a remap (remap_time, sim.cpp:452-483: max lane
-// bytes / 25 GB/s).  Here each GPU runs one launch over its copy program
-// (b200.hpp reshard_copies): the first CTAs stream the remote copies (push:
-// 128-bit stores into IPC-mapped peer buffers), the remaining CTAs do the
-// local ones (retained bytes that change packed position, ring-holder
-// self-lanes).  Copies are byte-granular and src/dst may be mutually
-// misaligned: destination vectors are always 16-byte aligned
-// stores; a misaligned source is realigned in registers from two aligned
-// 16-byte loads (neighbour lane's vector via warp shuffle); head/tail bytes
-// use byte stores so adjacent copies from other GPUs never race on a vector.
-// Work is cut into 64 KiB destination-aligned chunks (no two chunks share a
-// 16-byte destination vector).
+// bytes / 25 GB/s).  Here each GPU executes its copy program (b200.hpp
+// reshard_copies) in one launch: remote copies are 128-bit stores into
+// IPC-mapped peer HBM (push) — or bulk loads from it (pull) — and local copies
+// move retained bytes to their new packed position and the ring holder's
+// self lanes.  The first CTAs take remote copies (NVLink-bound), the rest the
+// local ones (HBM-bound).
+//
+// Each CTA is warp-specialised around a shared-memory ring:
+//   producer (one elected lane): cp.async.bulk global -> shared of the
+//     16-byte-aligned source window of each piece, completing on a per-stage
+//     mbarrier — the Tensor Memory Accelerator keeps ~kStages x 16 KiB in
+//     flight per CTA with no register traffic;
+//   consumers (4 warps): read the stage, realign it to the destination when
+//     source and destination are not congruent mod 16 (byte-granular plans,
+//     SURVEY fact 9), write 16-byte vectors, and byte-store the partial
+//     vectors at copy ends so adjacent copies from other GPUs never race on a
+//     vector; then release the stage on its "empty" mbarrier.
+// Pieces are <= 16 KiB and cut at 16 KiB-aligned destination addresses, so
+// no two pieces share a destination vector.
 #include <algorithm>
 #include <vector>
 
@@ -21,35 +29,102 @@
 namespace ew {
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int64_t kChunk = 64 * 1024;
+constexpr int kConsumerWarps = 4;
+constexpr int kThreads = 32 * (kConsumerWarps + 1);
+constexpr int kStages = 6;
+constexpr int kPiece = 16 * 1024;          // destination bytes per piece
+// aligned source window of a piece (<= kPiece + 30) plus the realigning
+// reader's 32-byte overhang
+constexpr int kStageBytes = kPiece + 64;
+constexpr int kSmem = kStages * kStageBytes;
 
 struct CopyItem {
   const uint8_t* src;
   uint8_t* dst;
   int64_t bytes;
-  int64_t chunk_base;  // first chunk id of this item within its class
+  int64_t piece_base;  // first piece id of this item within its class
 };
 
-__host__ __device__ __forceinline__ int64_t chunks_of(const uint8_t* dst, int64_t bytes) {
+__host__ __device__ __forceinline__ int64_t pieces_of(const uint8_t* dst, int64_t bytes) {
   if (bytes <= 0) return 0;
   const uint64_t d = reinterpret_cast<uintptr_t>(dst);
-  return static_cast<int64_t>((d + bytes - 1) / kChunk - d / kChunk + 1);
+  return static_cast<int64_t>((d + bytes - 1) / kPiece - d / kPiece + 1);
 }
 
-__device__ __forceinline__ int64_t item_of_chunk(const CopyItem* items, int64_t n, int64_t c) {
+__device__ __forceinline__ int64_t item_of_piece(const CopyItem* items, int64_t n, int64_t p) {
   int64_t lo = 0, hi = n - 1;
   while (lo < hi) {
     const int64_t mid = (lo + hi + 1) >> 1;
-    if (items[mid].chunk_base <= c) lo = mid;
+    if (items[mid].piece_base <= p) lo = mid;
     else hi = mid - 1;
   }
   return lo;
 }
 
+struct Piece {
+  const uint8_t* src;  // first source byte
+  uint8_t* dst;        // first destination byte
+  int32_t bytes;
+};
+
+__device__ __forceinline__ Piece piece_at(const CopyItem* list, int64_t n_items, int64_t p) {
+  const CopyItem it = list[item_of_piece(list, n_items, p)];
+  const uint64_t d = reinterpret_cast<uintptr_t>(it.dst);
+  const uint64_t cut = (d / kPiece + static_cast<uint64_t>(p - it.piece_base)) * kPiece;
+  const uint64_t lo = max(d, cut);
+  const uint64_t hi = min(d + static_cast<uint64_t>(it.bytes), cut + kPiece);
+  return Piece{it.src + (lo - d), it.dst + (lo - d), static_cast<int32_t>(hi - lo)};
+}
+
+// ---- shared-memory / async-proxy primitives
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "EW_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra EW_WAIT;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load(void* smem, const void* gmem, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(const uint8_t* p) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(smem_u32(p)));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t pick(const uint32_t (&x)[8], int i) {
-  // i is warp-uniform; unrolled select keeps x in registers
-  uint32_t r = x[0];
+  uint32_t r = x[0];  // i is uniform per piece; the select chain stays in registers
 #pragma unroll
   for (int k = 1; k < 8; ++k) r = (i == k) ? x[k] : r;
   return r;
@@ -68,80 +143,89 @@ __device__ __forceinline__ uint4 realign(const uint4& a, const uint4& b, int off
   return o;
 }
 
-// CTA-cooperative copy of n bytes src -> dst (any alignment).
-__device__ __forceinline__ void copy_range(const uint8_t* __restrict__ s, uint8_t* __restrict__ d,
-                                           int64_t n) {
-  const int tid = threadIdx.x;
-  const int64_t head = min(n, static_cast<int64_t>((16 - (reinterpret_cast<uintptr_t>(d) & 15)) & 15));
-  const int64_t nv = (n - head) >> 4;
-  const int64_t tail = (n - head) & 15;
-  if (tid < head) d[tid] = s[tid];
-  if (tid >= 32 && tid < 32 + tail) {
-    const int64_t k = head + 16 * nv + (tid - 32);
-    d[k] = s[k];
+// Consumers write one staged piece.  `stage` holds the source window that
+// starts at floor16(pc.src); destination byte x lives at stage[x - dst + r].
+__device__ __forceinline__ void write_piece(const uint8_t* stage, const Piece& pc, int ctid) {
+  constexpr int kC = 32 * kConsumerWarps;
+  const int r = static_cast<int>(reinterpret_cast<uintptr_t>(pc.src) & 15);
+  const int head = min(pc.bytes, static_cast<int32_t>((16 - (reinterpret_cast<uintptr_t>(pc.dst) & 15)) & 15));
+  const int nv = (pc.bytes - head) >> 4;
+  const int tail = (pc.bytes - head) & 15;
+  if (ctid < head) pc.dst[ctid] = stage[r + ctid];
+  if (ctid >= 32 && ctid < 32 + tail) {
+    const int k = head + 16 * nv + (ctid - 32);
+    pc.dst[k] = stage[r + k];
   }
-  if (nv == 0) return;
-  const uint8_t* sb = s + head;
-  uint8_t* db = d + head;
-  const int off = static_cast<int>(reinterpret_cast<uintptr_t>(sb) & 15);
-
+  uint8_t* db = pc.dst + head;
+  const int off = (r + head) & 15;          // uniform per piece
+  const uint8_t* sb = stage + ((r + head) & ~15);
   if (off == 0) {
-    constexpr int U = 4;
-    for (int64_t j0 = tid; j0 < nv; j0 += kThreads * U) {
-      uint4 v[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j = j0 + u * kThreads;
-        if (j < nv) v[u] = ld_stream(sb + 16 * j);
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int64_t j = j0 + u * kThreads;
-        if (j < nv) st_plain(db + 16 * j, v[u]);
+#pragma unroll 4
+    for (int j = ctid; j < nv; j += kC) st_plain(db + 16 * j, lds128(sb + 16 * j));
+  } else {
+#pragma unroll 4
+    for (int j = ctid; j < nv; j += kC)
+      st_plain(db + 16 * j, realign(lds128(sb + 16 * j), lds128(sb + 16 * j + 16), off));
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) staged_copy_kernel(const CopyItem* __restrict__ items,
+                                                               int64_t n_remote,
+                                                               int64_t remote_pieces,
+                                                               int64_t n_local,
+                                                               int64_t local_pieces,
+                                                               int remote_ctas) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[kStages];
+  __shared__ __align__(8) uint64_t empty[kStages];
+
+  const bool remote = static_cast<int>(blockIdx.x) < remote_ctas;
+  const CopyItem* list = remote ? items : items + n_remote;
+  const int64_t n_items = remote ? n_remote : n_local;
+  const int64_t n_pieces = remote ? remote_pieces : local_pieces;
+  const int64_t first = remote ? blockIdx.x : blockIdx.x - remote_ctas;
+  const int64_t step = remote ? remote_ctas : static_cast<int64_t>(gridDim.x) - remote_ctas;
+  if (n_items == 0 || step <= 0 || first >= n_pieces) return;  // uniform per CTA
+  const int64_t mine = (n_pieces - first + step - 1) / step;
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {  // producer
+    if (lane == 0) {
+      for (int64_t k = 0; k < mine; ++k) {
+        const int s = static_cast<int>(k % kStages);
+        if (k >= kStages) {
+          mbar_wait(&empty[s], static_cast<uint32_t>(((k / kStages) - 1) & 1));
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        const Piece pc = piece_at(list, n_items, first + k * step);
+        const uintptr_t s0 = reinterpret_cast<uintptr_t>(pc.src) & ~uintptr_t{15};
+        const uintptr_t s1 = (reinterpret_cast<uintptr_t>(pc.src) + pc.bytes + 15) & ~uintptr_t{15};
+        const uint32_t n = static_cast<uint32_t>(s1 - s0);
+        mbar_expect_tx(&full[s], n);
+        tma_load(ring + s * kStageBytes, reinterpret_cast<const void*>(s0), n, &full[s]);
       }
     }
     return;
   }
 
-  // misaligned source: lane l of a warp handles destination vector 32*g + l
-  const uint8_t* sa = sb - off;  // aligned
-  const int lane = tid & 31;
-  const int warp = tid >> 5;
-  constexpr int kWarps = kThreads / 32;
-  const int64_t groups = (nv + 31) >> 5;
-  for (int64_t g = warp; g < groups; g += kWarps) {
-    const int64_t j = 32 * g + lane;
-    uint4 a = make_uint4(0, 0, 0, 0), b = make_uint4(0, 0, 0, 0);
-    if (j <= nv) a = ld_stream(sa + 16 * j);
-    if (lane == 31 && j + 1 <= nv) b = ld_stream(sa + 16 * (j + 1));
-    uint4 nb;
-    nb.x = __shfl_down_sync(0xffffffffu, a.x, 1);
-    nb.y = __shfl_down_sync(0xffffffffu, a.y, 1);
-    nb.z = __shfl_down_sync(0xffffffffu, a.z, 1);
-    nb.w = __shfl_down_sync(0xffffffffu, a.w, 1);
-    if (lane != 31) b = nb;
-    if (j < nv) st_plain(db + 16 * j, realign(a, b, off));
-  }
-}
-
-__global__ void __launch_bounds__(kThreads) copy_kernel(const CopyItem* __restrict__ items,
-                                                        int64_t n_remote, int64_t remote_chunks,
-                                                        int64_t n_local, int64_t local_chunks,
-                                                        int remote_ctas) {
-  const bool remote = static_cast<int>(blockIdx.x) < remote_ctas;
-  const CopyItem* list = remote ? items : items + n_remote;
-  const int64_t n_items = remote ? n_remote : n_local;
-  const int64_t n_chunks = remote ? remote_chunks : local_chunks;
-  const int64_t first = remote ? blockIdx.x : blockIdx.x - remote_ctas;
-  const int64_t step = remote ? remote_ctas : static_cast<int64_t>(gridDim.x) - remote_ctas;
-  if (n_items == 0 || step <= 0) return;
-  for (int64_t c = first; c < n_chunks; c += step) {
-    const CopyItem it = list[item_of_chunk(list, n_items, c)];
-    const uint64_t d = reinterpret_cast<uintptr_t>(it.dst);
-    const uint64_t cb = (d / kChunk + (c - it.chunk_base)) * kChunk;
-    const uint64_t lo = max(d, cb);
-    const uint64_t hi = min(d + static_cast<uint64_t>(it.bytes), cb + kChunk);
-    copy_range(it.src + (lo - d), it.dst + (lo - d), static_cast<int64_t>(hi - lo));
+  const int ctid = threadIdx.x - 32;  // consumer thread id
+  for (int64_t k = 0; k < mine; ++k) {
+    const int s = static_cast<int>(k % kStages);
+    mbar_wait(&full[s], static_cast<uint32_t>((k / kStages) & 1));
+    const Piece pc = piece_at(list, n_items, first + k * step);
+    write_piece(ring + s * kStageBytes, pc, ctid);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
 }
 
@@ -152,9 +236,8 @@ using namespace ew;
 
 struct ew_copy_program {
   int device = -1;
-  int64_t n_remote = 0, n_local = 0;
-  int64_t remote_chunks = 0, local_chunks = 0;
-  int64_t remote_bytes = 0, local_bytes = 0;
+  int64_t n_remote = 0, n_local = 0, remote_pieces = 0, local_pieces = 0;
+  int64_t remote_bytes = 0, local_bytes = 0, copies = 0;
   CopyItem* d_items = nullptr;
 };
 
@@ -165,20 +248,21 @@ int build_program(std::vector<CopyItem> remote, std::vector<CopyItem> local,
   auto* p = new ew_copy_program();
   int64_t base = 0;
   for (CopyItem& it : remote) {
-    it.chunk_base = base;
-    base += chunks_of(it.dst, it.bytes);
+    it.piece_base = base;
+    base += pieces_of(it.dst, it.bytes);
     p->remote_bytes += it.bytes;
   }
-  p->remote_chunks = base;
+  p->remote_pieces = base;
   base = 0;
   for (CopyItem& it : local) {
-    it.chunk_base = base;
-    base += chunks_of(it.dst, it.bytes);
+    it.piece_base = base;
+    base += pieces_of(it.dst, it.bytes);
     p->local_bytes += it.bytes;
   }
-  p->local_chunks = base;
+  p->local_pieces = base;
   p->n_remote = static_cast<int64_t>(remote.size());
   p->n_local = static_cast<int64_t>(local.size());
+  p->copies = p->n_remote + p->n_local;
   std::vector<CopyItem> all(remote);
   all.insert(all.end(), local.begin(), local.end());
   cudaError_t e = cudaGetDevice(&p->device);
@@ -188,6 +272,9 @@ int build_program(std::vector<CopyItem> remote, std::vector<CopyItem> local,
       e = cudaMemcpy(p->d_items, all.data(), all.size() * sizeof(CopyItem),
                      cudaMemcpyHostToDevice);
   }
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(staged_copy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSmem);
   if (e != cudaSuccess) {
     if (p->d_items) cudaFree(p->d_items);
     delete p;
@@ -221,8 +308,9 @@ int ew_copy_program_create(const ew_copy_desc* descs, int64_t n, void* const* bu
     if (src == nullptr || dst == nullptr)
       return set_error(EW_ERR_INVALID_ARGUMENT,
                        "copy descriptor " + std::to_string(i) + " refers to an unmapped buffer");
-    CopyItem it{src + c.src_off, dst + c.dst_off, c.bytes, 0};
-    (c.dst_rank != exec_rank ? remote : local).push_back(it);
+    // remote = the copy crosses NVLink (the other end is not exec_rank)
+    const bool crosses = c.dst_rank != exec_rank || c.src_rank != exec_rank;
+    (crosses ? remote : local).push_back({src + c.src_off, dst + c.dst_off, c.bytes, 0});
   }
   return build_program(std::move(remote), std::move(local), out);
 }
@@ -251,7 +339,7 @@ void ew_copy_program_free(ew_copy_program* prog) {
 int ew_copy_program_stats(const ew_copy_program* prog, int64_t* n_copies, int64_t* remote_bytes,
                           int64_t* local_bytes) {
   if (prog == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL program");
-  if (n_copies) *n_copies = prog->n_remote + prog->n_local;
+  if (n_copies) *n_copies = prog->copies;
   if (remote_bytes) *remote_bytes = prog->remote_bytes;
   if (local_bytes) *local_bytes = prog->local_bytes;
   return EW_OK;
@@ -260,24 +348,14 @@ int ew_copy_program_stats(const ew_copy_program* prog, int64_t* n_copies, int64_
 int ew_copy_program_launch(const ew_copy_program* prog, int n_ctas, int remote_ctas,
                            ew_stream_t stream) {
   if (prog == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL program");
-  if (prog->remote_chunks + prog->local_chunks == 0) return EW_OK;
+  if (prog->remote_pieces + prog->local_pieces == 0) return EW_OK;
   const int sms = num_sms();
-  if (n_ctas <= 0) n_ctas = 4 * sms;
-  if (prog->remote_chunks == 0) remote_ctas = 0;
-  else if (prog->local_chunks == 0) remote_ctas = n_ctas;
-  else if (remote_ctas <= 0) {
-    // NVLink-bound remote stream vs HBM-bound local stream (2 bytes of HBM
-    // traffic per local byte): give each class CTAs in proportion to its time
-    const double t_remote = static_cast<double>(prog->remote_bytes) / 750.0;
-    const double t_local = 2.0 * static_cast<double>(prog->local_bytes) / 6000.0;
-    remote_ctas = static_cast<int>(n_ctas * t_remote / (t_remote + t_local) + 0.5);
-    remote_ctas = std::max(sms / 2, std::min(remote_ctas, n_ctas - sms / 2));
-  }
-  remote_ctas = std::max(0, std::min(remote_ctas, n_ctas));
-  if (remote_ctas == n_ctas && prog->local_chunks > 0) n_ctas += sms;
-  if (remote_ctas == 0 && prog->remote_chunks > 0) remote_ctas = std::min(n_ctas, sms);
-  copy_kernel<<<n_ctas, kThreads, 0, (cudaStream_t)stream>>>(
-      prog->d_items, prog->n_remote, prog->remote_chunks, prog->n_local, prog->local_chunks,
+  if (n_ctas <= 0) n_ctas = 2 * sms;  // two 96 KiB rings per SM
+  if (prog->remote_pieces == 0) remote_ctas = 0;
+  else if (prog->local_pieces == 0) remote_ctas = n_ctas;
+  else if (remote_ctas <= 0 || remote_ctas >= n_ctas) remote_ctas = std::max(1, n_ctas / 4);
+  staged_copy_kernel<<<n_ctas, kThreads, kSmem, (cudaStream_t)stream>>>(
+      prog->d_items, prog->n_remote, prog->remote_pieces, prog->n_local, prog->local_pieces,
       remote_ctas);
   EW_CUDA_TRY(cudaGetLastError());
   return EW_OK;

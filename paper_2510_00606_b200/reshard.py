@@ -109,7 +109,10 @@ def shard_map(layout: PartitionLayout, rank: int, block_bytes: int = dev.DEFAULT
 class ReshardExecutor:
     """Multi-process executor: one instance per rank/GPU."""
 
-    def __init__(self, rp: ReshardPlan, rank: int, push: bool = True):
+    def __init__(self, rp: ReshardPlan, rank: int, push: bool = False):
+        # pull is the default: each receiver's TMA ring keeps ~100 KB of peer
+        # loads in flight per SM, which saturates NVLink better than posted
+        # stores from the (hot-spotted) ring holder (profiles/r01_reshard_*)
         self.rp = rp
         self.rank = rank
         self.push = push

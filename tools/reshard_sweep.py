@@ -89,8 +89,8 @@ def main():
         if bufs.replica is not None:
             dev.fill_synthetic(shard_map(rp.src, rp.replica_of(rank)), bufs.replica, 0)
         ex.bind(bufs)
-        for n_ctas, rem in ((0, 0), (592, 148), (592, 296), (592, 444), (1184, 296), (1184, 592),
-                            (1184, 888), (296, 148)):
+        for n_ctas, rem in ((0, 0), (148, 37), (148, 74), (296, 37), (296, 74), (296, 111),
+                            (296, 148), (444, 74), (444, 148)):
             t = timed(lambda: ex.launch(n_ctas, rem))
             emit({"test": f"reshard {world}->{world-1} drop {drop}", "push": push, "ctas": n_ctas,
                   "remote_ctas": rem, "ms": round(t * 1e3, 3),
