@@ -61,26 +61,43 @@ __global__ void __launch_bounds__(256) fold_kernel(Units u, int64_t n, double sc
   bool vec_ok = (reinterpret_cast<uintptr_t>(acc) & 15) == 0;
   for (int k = 0; k < u.n; ++k) vec_ok = vec_ok && ((reinterpret_cast<uintptr_t>(u.p[k]) & 15) == 0);
   if (vec_ok) {
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
-      long long s0 = 0, s1 = 0, s2 = 0, s3 = 0;
+    // kDepth independent float4 groups per thread keep enough loads in flight
+    constexpr int kDepth = 4;
+    for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n4;
+         i0 += kDepth * stride) {
+      long long s[kDepth][4] = {};
       for (int k = 0; k < u.n; ++k) {
-        const float4 g = __ldg(reinterpret_cast<const float4*>(u.p[k]) + i);
+        const float4* src = reinterpret_cast<const float4*>(u.p[k]);
         const double w = u.w[k];
-        s0 += __double2ll_rn((w * static_cast<double>(g.x)) * scale);
-        s1 += __double2ll_rn((w * static_cast<double>(g.y)) * scale);
-        s2 += __double2ll_rn((w * static_cast<double>(g.z)) * scale);
-        s3 += __double2ll_rn((w * static_cast<double>(g.w)) * scale);
+        float4 g[kDepth];
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) {
+          const int64_t i = i0 + d * stride;
+          g[d] = i < n4 ? __ldcs(src + i) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d) {
+          s[d][0] += __double2ll_rn((w * static_cast<double>(g[d].x)) * scale);
+          s[d][1] += __double2ll_rn((w * static_cast<double>(g[d].y)) * scale);
+          s[d][2] += __double2ll_rn((w * static_cast<double>(g[d].z)) * scale);
+          s[d][3] += __double2ll_rn((w * static_cast<double>(g[d].w)) * scale);
+        }
       }
-      longlong2* dst = reinterpret_cast<longlong2*>(acc + 4 * i);
-      if (kAccumulate) {
-        const longlong2 a = dst[0], b = dst[1];
-        s0 += a.x;
-        s1 += a.y;
-        s2 += b.x;
-        s3 += b.y;
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) {
+        const int64_t i = i0 + d * stride;
+        if (i >= n4) break;
+        longlong2* dst = reinterpret_cast<longlong2*>(acc + 4 * i);
+        if (kAccumulate) {
+          const longlong2 a = dst[0], b = dst[1];
+          s[d][0] += a.x;
+          s[d][1] += a.y;
+          s[d][2] += b.x;
+          s[d][3] += b.y;
+        }
+        __stcs(dst, make_longlong2(s[d][0], s[d][1]));
+        __stcs(dst + 1, make_longlong2(s[d][2], s[d][3]));
       }
-      dst[0] = make_longlong2(s0, s1);
-      dst[1] = make_longlong2(s2, s3);
     }
   }
   const int64_t start = vec_ok ? 4 * n4 : 0;
