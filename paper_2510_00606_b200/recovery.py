@@ -1,0 +1,157 @@
+"""Measured DP recovery on B200: the data-parallel slice of the reference's
+Simulation::recover_elaswave (sim.cpp:597-722), executed instead of modelled.
+
+Per step the group keeps a same-GPU snapshot of every rank's ZeRO shard with
+checksum rows (kernel (a)).  On a membership change (FailStop / ScaleIn /
+ScaleOut) each surviving rank runs, in the reference's order:
+
+  comm repair   plan_edit on the DP mesh (communicator.cpp:54-105), then the
+                edit applied: ncclCommShrink of the DP communicator
+  dataflow      reshard_microbatches (dataflow.cpp:52-69) -> new weights
+  remap         integrity_check + overlap_matrix on the interleaved layouts,
+                lowering to this GPU's copy program, CUDA-IPC peer mapping,
+                one copy launch (kernel (b)), verification of every moved
+                byte by checksum conservation (no source re-read)
+
+and reports an MttrEvent with the reference's fields (sim.hpp:31-45) filled
+with measured seconds (`mttr_csv` row format of sim.cpp:1119-1132).
+"""
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional, Sequence
+
+import torch
+import torch.distributed as dist
+
+from . import device as dev
+from .fabric import FAIL_STOP, SCALE_IN, SCALE_OUT, CommGroup, plan_edit, reshard_microbatches
+from .reshard import ReshardExecutor, ReshardPlan, shard_map
+
+KIND_NAMES = {FAIL_STOP: "fail_stop", SCALE_IN: "scale_in", SCALE_OUT: "scale_out"}
+
+
+@dataclass
+class MttrEvent:
+    """Reference MttrEvent (sim.hpp:31-45) with measured phases."""
+
+    step: int = 0
+    t_event_s: float = 0.0
+    kind: str = "fail_stop"
+    detect_s: float = 0.0          # detection is outside this library (agent)
+    comm_repair_s: float = 0.0     # plan_edit + ncclCommShrink
+    remap_s: float = 0.0           # plan + peer map + copy + verify
+    migration_stall_s: float = 0.0  # no layer migration on the DP path
+    other_s: float = 0.0           # micro-batch reshape + bookkeeping
+    lost_work_s: float = 0.0
+    phases: Dict[str, float] = field(default_factory=dict)
+    verified: bool = False
+
+    def total_s(self) -> float:
+        return (self.detect_s + self.comm_repair_s + self.remap_s + self.migration_stall_s +
+                self.other_s)
+
+    def csv_row(self, index: int) -> str:
+        """One line of the reference's mttr.csv (sim.cpp:1119-1132)."""
+        f = lambda x: f"{x:.9g}"
+        return ",".join([str(index), str(self.step), f(self.t_event_s), self.kind, f(self.detect_s),
+                         f(self.comm_repair_s), f(self.remap_s), f(self.migration_stall_s),
+                         f(self.other_s), f(self.lost_work_s), f(self.total_s())])
+
+
+MTTR_CSV_HEADER = ("event,step,t_event_s,kind,detect_s,comm_repair_s,remap_s,migration_stall_s,"
+                   "other_s,lost_work_s,total_s")
+
+
+class DpGroup:
+    """One rank's view of an interleaved-ZeRO DP group (one process per GPU)."""
+
+    def __init__(self, layer_bytes: Sequence[int], members: Sequence[int], rank: int,
+                 comm: Optional[dev.Communicator], per_slot_mbs: int = 4,
+                 num_microbatches: int = 32, block_bytes: int = dev.DEFAULT_BLOCK_BYTES):
+        self.layer_bytes = list(layer_bytes)
+        self.members = sorted(members)
+        self.rank = rank
+        self.comm = comm
+        self.block_bytes = block_bytes
+        self.mb_sizes = [per_slot_mbs] * len(self.members)
+        self.num_microbatches = num_microbatches
+        self.links = {(a, b) for i, a in enumerate(self.members) for b in self.members[i + 1:]}
+
+    def recover(self, departed: Sequence[int], bufs, push: bool = False, step: int = 0,
+                kind: int = FAIL_STOP, group=None) -> MttrEvent:
+        """Run the DP recovery for `departed` on this (surviving) rank.
+        `bufs` are this rank's RankBuffers for the change (old/replica filled)."""
+        ev = MttrEvent(step=step, kind=KIND_NAMES.get(kind, "fail_stop"))
+        t0 = time.perf_counter()
+        # comm repair: edit plan, then the NCCL communicator shrink
+        edit = plan_edit([CommGroup("dp", self.members)], kind, list(departed), self.links)
+        for l in edit.links_to_remove:
+            self.links.discard(l)
+        self.links |= edit.links_to_add
+        new_comm = self.comm.shrink(list(departed)) if self.comm is not None else None
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        ev.comm_repair_s = t1 - t0
+        ev.phases["plan_edit_links_removed"] = len(edit.links_to_remove)
+
+        # dataflow: global batch conserved over the survivors
+        survivors = [m for m in self.members if m not in set(departed)]
+        old_idx = {m: i for i, m in enumerate(self.members)}
+        _, sizes = reshard_microbatches(self.mb_sizes, self.num_microbatches,
+                                        [old_idx[m] for m in survivors])
+        t2 = time.perf_counter()
+        ev.other_s = t2 - t1
+
+        # remap: plan -> program -> peer map -> copy -> verify
+        rp = ReshardPlan.build(self.layer_bytes, self.members, survivors)
+        ex = ReshardExecutor(rp, self.rank, push=push)
+        t3 = time.perf_counter()
+        ex.bind(bufs, group=group)
+        t4 = time.perf_counter()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        dist.barrier(group=group)
+        s.record()
+        ex.launch()
+        e.record()
+        torch.cuda.synchronize()
+        dist.barrier(group=group)
+        t5 = time.perf_counter()
+        ev.verified = self.verify_conservation(rp, bufs, group)
+        t6 = time.perf_counter()
+        ev.remap_s = t6 - t2
+        ev.phases.update(plan_s=t3 - t2, peer_map_s=t4 - t3, copy_s=s.elapsed_time(e) / 1e3,
+                         copy_wall_s=t5 - t4, verify_s=t6 - t5)
+        ex.close()
+        # commit the new membership
+        self.members = survivors
+        self.mb_sizes = sizes
+        self.comm = new_comm
+        return ev
+
+    def verify_conservation(self, rp: ReshardPlan, bufs, group=None) -> bool:
+        """Block sums of all NEW shards == block sums of all OLD shards."""
+        block = self.block_bytes
+        nblocks = (sum(self.layer_bytes) + block - 1) // block
+        before = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+        after = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+        if bufs.old is not None and self.rank in rp.old_ranks and self.rank not in rp.failed:
+            m = shard_map(rp.src, self.rank, block)
+            rows = m.new_row_sums()
+            dev.checksum(m, bufs.old, rows)
+            dev.rows_to_blocks(m, rows, before)
+        if bufs.replica is not None:  # the dead rank's bytes as its ring holder keeps them
+            owner = rp.replica_of(self.rank)
+            m = shard_map(rp.src, owner, block)
+            rows = m.new_row_sums()
+            dev.checksum(m, bufs.replica, rows)
+            dev.rows_to_blocks(m, rows, before)
+        if bufs.new is not None:
+            m = shard_map(rp.dst, self.rank, block)
+            rows = m.new_row_sums()
+            dev.checksum(m, bufs.new, rows)
+            dev.rows_to_blocks(m, rows, after)
+        dist.all_reduce(before, group=group)
+        dist.all_reduce(after, group=group)
+        return bool(torch.equal(before, after))

@@ -66,18 +66,40 @@ def _worker(rank, world, port, result_dir):
                 report[f"reshard drop{drop} push={push}"] = ok
                 ex.close()
                 dist.barrier()
-        # NCCL communicator: init, shrink without the last rank, reduce
+        # full DP recovery of the last rank (recovery.DpGroup): plan_edit +
+        # ncclCommShrink, reshape, remap, checksum verification
+        from paper_2510_00606_b200.recovery import DpGroup
         uid = [dev.Communicator.unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         comm = dev.Communicator.init(uid[0], world, rank)
+        comm.allreduce_i64(torch.zeros(8, dtype=torch.int64, device="cuda"))
+        drop = world - 1
+        survivors = [r for r in range(world) if r != drop]
+        grp = dist.new_group(survivors)
+        rp = ReshardPlan.build(cfg.layer_bytes, range(world), survivors)
+        shrunk = None
+        if rank != drop:
+            ex = ReshardExecutor(rp, rank)
+            bufs = ex.allocate()
+            dev.fill_synthetic(shard_map(rp.src, rank), bufs.old, 5)
+            if bufs.replica is not None:
+                dev.fill_synthetic(shard_map(rp.src, rp.replica_of(rank)), bufs.replica, 5)
+            group = DpGroup(cfg.layer_bytes, range(world), rank, comm)
+            ev = group.recover([drop], bufs, group=grp)
+            report["recovery verified by checksums"] = ev.verified
+            report["recovery mttr row"] = ev.csv_row(0)
+            shrunk = group.comm
+            exp = dev.empty_bytes(rp.dst.shard_bytes(rank))
+            dev.fill_synthetic(shard_map(rp.dst, rank), exp, 5)
+            n = rp.dst.shard_bytes(rank)
+            report["recovery bytes"] = bool(torch.equal(bufs.new[:n], exp[:n]))
+        dist.barrier()
         n_units, dim = 12, 100_003
         rng = np.random.default_rng(21)
         g = rng.normal(0, 1e-3, size=(n_units, dim)).astype(np.float32)
         g[3, 5] = 1e2
         w = rng.random(n_units) / n_units
         # units split over the ranks of the shrunk communicator
-        survivors = list(range(world - 1)) if world > 2 else list(range(world))
-        shrunk = comm.shrink([world - 1]) if world > 2 and rank != world - 1 else (comm if world <= 2 else None)
         if shrunk is not None:
             k = len(survivors)
             mine = [u for u in range(n_units) if u % k == shrunk.rank]
@@ -94,7 +116,6 @@ def _worker(rank, world, port, result_dir):
             single = dev.fixed_to_float(acc1, f)
             report["reduce bit-identical to 1-GPU fold"] = bool(torch.equal(out, single))
             report["shrunk size"] = shrunk.size
-        if world > 2 and shrunk is not None:
             shrunk.destroy()
         comm.destroy()
     except Exception as e:  # report, do not hang the other ranks
@@ -115,7 +136,8 @@ def test_multi_gpu_reshard_comm_reduce(world, tmp_path):
         rep = json.loads((tmp_path / f"rank{r}.json").read_text())
         assert "error" not in rep, rep
         for k, v in rep.items():
-            if k.startswith("reshard") or k.startswith("reduce"):
+            if isinstance(v, bool):
                 assert v is True, (r, k)
-        if "shrunk size" in rep:
-            assert rep["shrunk size"] == (world - 1 if world > 2 else world)
+        if r != world - 1:
+            assert rep["shrunk size"] == world - 1
+            assert rep["recovery verified by checksums"] is True
