@@ -288,6 +288,32 @@ int ew_weighted_reduce(ew_comm* comm, const float* const* units, const double* w
                        int n_units, int64_t total_units, int64_t n_elems, int64_t* ws_acc,
                        double* ws_max, float* out, int* frac_bits_out, ew_stream_t stream);
 
+/* (d) fused with its collective over NVLink peer memory (no NCCL): the same
+ * quantised int64 sums, bit-identical to ew_weighted_reduce.  unit_ptrs lists
+ * EVERY rank's units (IPC-mapped peer pointers or local ones), out_ptrs every
+ * rank's fp32 output buffer; all 16-byte aligned.  Call reduce_scatter on all
+ * ranks, make sure every rank finished it (a host barrier), then all_gather;
+ * the caller also barriers before the units are read. */
+typedef struct ew_peer_fold ew_peer_fold;
+int ew_peer_fold_create(int world, int rank, int64_t n_elems, const float* const* unit_ptrs,
+                        const double* unit_weights, int n_units, float* const* out_ptrs,
+                        ew_peer_fold** out);
+int ew_peer_fold_reduce_scatter(ew_peer_fold* fold, int frac_bits, ew_stream_t stream);
+int ew_peer_fold_all_gather(ew_peer_fold* fold, ew_stream_t stream);
+void ew_peer_fold_free(ew_peer_fold* fold);
+
+/* Stream-ordered barrier across the GPUs of a group over peer memory.
+ * flag_ptrs[r] is rank r's zero-initialised uint64[world] array (IPC-mapped
+ * on the other ranks).  Every rank enqueues wait() the same number of times;
+ * a rank that never arrives makes the others give up after timeout_s and
+ * report it through timed_out() (no hang). */
+typedef struct ew_peer_barrier ew_peer_barrier;
+int ew_peer_barrier_create(int world, int rank, unsigned long long* const* flag_ptrs,
+                           ew_peer_barrier** out);
+int ew_peer_barrier_wait(ew_peer_barrier* barrier, double timeout_s, ew_stream_t stream);
+int ew_peer_barrier_timed_out(ew_peer_barrier* barrier, int* timed_out);
+void ew_peer_barrier_free(ew_peer_barrier* barrier);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -1,0 +1,273 @@
+// (d) Weighted reduce fused with its collective over NVLink peer memory.
+//
+// Same arithmetic as ew_weighted_fold + NCCL int64 all-reduce (each unit
+// quantised once, q = rint(w*g*2^F), exact int64 sums -> bit-identical for
+// every world size and split), but the collective is the kernel itself:
+//   reduce-scatter: GPU r reads element chunk r of EVERY unit of every rank
+//     straight from peer HBM (CUDA IPC mappings over NVSwitch), sums the
+//     quantised terms in registers and writes its fp32 output chunk;
+//   all-gather: GPU r pulls the other ranks' output chunks (staged-copy path).
+// NVLink bytes per GPU: (N-1)/N * n * (4 B per unit + 4 B), versus 2 *
+// (N-1)/N * n * 8 B for the int64 NCCL all-reduce, and no int64 accumulator
+// array in HBM.  The communicator edit for a departed rank is dropping its
+// pointers (no NCCL communicator to shrink).
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "ew_device.cuh"
+
+namespace ew {
+namespace {
+
+struct PeerUnit {
+  const float* p;
+  double w;
+};
+
+// Rank `rank`'s chunk of float4 groups: [lo4, hi4); the last rank also owns
+// the scalar tail [4*n4, n).
+__global__ void __launch_bounds__(256) peer_fold_kernel(const PeerUnit* __restrict__ units,
+                                                        int n_units, int64_t lo4, int64_t hi4,
+                                                        int64_t tail_lo, int64_t n, double scale,
+                                                        double inv_scale, float* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  constexpr int kDepth = 2;
+  for (int64_t i0 = lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < hi4;
+       i0 += kDepth * stride) {
+    long long s[kDepth][4] = {};
+    for (int k = 0; k < n_units; ++k) {
+      const float4* src = reinterpret_cast<const float4*>(units[k].p);
+      const double w = units[k].w;
+      float4 g[kDepth];
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) {
+        const int64_t i = i0 + d * stride;
+        g[d] = i < hi4 ? src[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) {
+        s[d][0] += __double2ll_rn((w * static_cast<double>(g[d].x)) * scale);
+        s[d][1] += __double2ll_rn((w * static_cast<double>(g[d].y)) * scale);
+        s[d][2] += __double2ll_rn((w * static_cast<double>(g[d].z)) * scale);
+        s[d][3] += __double2ll_rn((w * static_cast<double>(g[d].w)) * scale);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d) {
+      const int64_t i = i0 + d * stride;
+      if (i >= hi4) break;
+      reinterpret_cast<float4*>(out)[i] =
+          make_float4(static_cast<float>(static_cast<double>(s[d][0]) * inv_scale),
+                      static_cast<float>(static_cast<double>(s[d][1]) * inv_scale),
+                      static_cast<float>(static_cast<double>(s[d][2]) * inv_scale),
+                      static_cast<float>(static_cast<double>(s[d][3]) * inv_scale));
+    }
+  }
+  for (int64_t i = tail_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    long long acc = 0;
+    for (int k = 0; k < n_units; ++k)
+      acc += __double2ll_rn((units[k].w * static_cast<double>(units[k].p[i])) * scale);
+    out[i] = static_cast<float>(static_cast<double>(acc) * inv_scale);
+  }
+}
+
+// Device-side barrier across GPUs over peer memory: thread p stores `epoch`
+// into slot [rank] of rank p's flag array (system-scope release), then waits
+// until slot [p] of this rank's array reaches `epoch` (system-scope acquire).
+// A bounded spin: after ~timeout_cycles the wait gives up and raises *err, so
+// a missing peer surfaces as an error instead of a hung GPU.
+__global__ void peer_barrier_kernel(unsigned long long* const* __restrict__ flags, int rank,
+                                    int world, unsigned long long epoch, long long timeout_cycles,
+                                    int* __restrict__ err) {
+  const int p = threadIdx.x;
+  if (p >= world) return;
+  __threadfence_system();
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(flags[p] + rank), "l"(epoch)
+               : "memory");
+  const unsigned long long* mine = flags[rank] + p;
+  const long long start = clock64();
+  for (;;) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(mine) : "memory");
+    if (v >= epoch) break;
+    if (clock64() - start > timeout_cycles) {
+      atomicExch(err, 1);
+      break;
+    }
+    __nanosleep(200);
+  }
+}
+
+}  // namespace
+}  // namespace ew
+
+using namespace ew;
+
+struct ew_peer_barrier {
+  int world = 0, rank = 0;
+  unsigned long long epoch = 0;
+  unsigned long long** d_flags = nullptr;
+  int* d_err = nullptr;
+};
+
+extern "C" {
+
+int ew_peer_barrier_create(int world, int rank, unsigned long long* const* flag_ptrs,
+                           ew_peer_barrier** out) {
+  if (out == nullptr || world < 1 || world > 1024 || rank < 0 || rank >= world || !flag_ptrs)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_peer_barrier_create: bad arguments");
+  for (int r = 0; r < world; ++r)
+    if (flag_ptrs[r] == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL flag array");
+  auto* b = new ew_peer_barrier();
+  b->world = world;
+  b->rank = rank;
+  cudaError_t e = cudaMalloc(&b->d_flags, world * sizeof(unsigned long long*));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(b->d_flags, flag_ptrs, world * sizeof(unsigned long long*), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMalloc(&b->d_err, sizeof(int));
+  if (e == cudaSuccess) e = cudaMemset(b->d_err, 0, sizeof(int));
+  if (e != cudaSuccess) {
+    if (b->d_flags) cudaFree(b->d_flags);
+    if (b->d_err) cudaFree(b->d_err);
+    delete b;
+    return cuda_status(e, "ew_peer_barrier_create");
+  }
+  *out = b;
+  return EW_OK;
+}
+
+int ew_peer_barrier_wait(ew_peer_barrier* b, double timeout_s, ew_stream_t stream) {
+  if (b == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL barrier");
+  ++b->epoch;
+  const long long cycles = static_cast<long long>(timeout_s * 2.0e9);  // <= 2 GHz SM clock
+  peer_barrier_kernel<<<1, 32 * ((b->world + 31) / 32), 0, (cudaStream_t)stream>>>(
+      b->d_flags, b->rank, b->world, b->epoch, cycles, b->d_err);
+  EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}
+
+int ew_peer_barrier_timed_out(ew_peer_barrier* b, int* timed_out) {
+  if (b == nullptr || timed_out == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+  EW_CUDA_TRY(cudaMemcpy(timed_out, b->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  return EW_OK;
+}
+
+void ew_peer_barrier_free(ew_peer_barrier* b) {
+  if (b == nullptr) return;
+  if (b->d_flags) cudaFree(b->d_flags);
+  if (b->d_err) cudaFree(b->d_err);
+  delete b;
+}
+
+}  // extern "C"
+
+struct ew_peer_fold {
+  int world = 0, rank = 0, n_units = 0;
+  int64_t n = 0, lo4 = 0, hi4 = 0, tail_lo = 0, tail_hi = 0;
+  PeerUnit* d_units = nullptr;
+  float* out = nullptr;
+  ew_copy_program* gather = nullptr;
+};
+
+extern "C" {
+
+int ew_peer_fold_create(int world, int rank, int64_t n_elems, const float* const* unit_ptrs,
+                        const double* unit_weights, int n_units, float* const* out_ptrs,
+                        ew_peer_fold** out) {
+  if (out == nullptr || world < 1 || rank < 0 || rank >= world || n_elems < 0 || n_units < 0 ||
+      (n_units > 0 && (!unit_ptrs || !unit_weights)) || out_ptrs == nullptr)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_peer_fold_create: bad arguments");
+  *out = nullptr;
+  for (int k = 0; k < n_units; ++k)
+    if (unit_ptrs[k] == nullptr || (reinterpret_cast<uintptr_t>(unit_ptrs[k]) & 15))
+      return set_error(EW_ERR_INVALID_ARGUMENT, "unit pointers must be non-null and 16-byte aligned");
+  for (int r = 0; r < world; ++r)
+    if (out_ptrs[r] == nullptr || (reinterpret_cast<uintptr_t>(out_ptrs[r]) & 15))
+      return set_error(EW_ERR_INVALID_ARGUMENT, "output pointers must be non-null and 16-byte aligned");
+  auto* f = new ew_peer_fold();
+  f->world = world;
+  f->rank = rank;
+  f->n = n_elems;
+  f->n_units = n_units;
+  f->out = out_ptrs[rank];
+  const int64_t n4 = n_elems / 4;
+  auto lo_of = [&](int r) { return n4 * r / world; };
+  f->lo4 = lo_of(rank);
+  f->hi4 = lo_of(rank + 1);
+  f->tail_lo = (rank == world - 1) ? 4 * n4 : n_elems;  // last rank owns the scalar tail
+  std::vector<PeerUnit> units(static_cast<std::size_t>(n_units));
+  for (int k = 0; k < n_units; ++k) units[k] = PeerUnit{unit_ptrs[k], unit_weights[k]};
+  cudaError_t e = cudaSuccess;
+  if (n_units > 0) {
+    e = cudaMalloc(&f->d_units, units.size() * sizeof(PeerUnit));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(f->d_units, units.data(), units.size() * sizeof(PeerUnit),
+                     cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    if (f->d_units) cudaFree(f->d_units);
+    delete f;
+    return cuda_status(e, "ew_peer_fold_create");
+  }
+  // all-gather program: pull every other rank's chunk from its output buffer
+  std::vector<const void*> srcs;
+  std::vector<void*> dsts;
+  std::vector<int64_t> bytes;
+  std::vector<int> remote;
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) continue;
+    const int64_t lo = 4 * lo_of(r);
+    const int64_t hi = (r == world - 1) ? n_elems : 4 * lo_of(r + 1);
+    if (hi <= lo) continue;
+    srcs.push_back(out_ptrs[r] + lo);
+    dsts.push_back(out_ptrs[rank] + lo);
+    bytes.push_back((hi - lo) * 4);
+    remote.push_back(1);
+  }
+  if (!bytes.empty()) {
+    if (int st = ew_copy_program_create_raw(srcs.data(), dsts.data(), bytes.data(), remote.data(),
+                                            static_cast<int64_t>(bytes.size()), &f->gather)) {
+      if (f->d_units) cudaFree(f->d_units);
+      delete f;
+      return st;
+    }
+  }
+  *out = f;
+  return EW_OK;
+}
+
+int ew_peer_fold_reduce_scatter(ew_peer_fold* f, int frac_bits, ew_stream_t stream) {
+  if (f == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL peer fold");
+  if (frac_bits > 1000 || frac_bits < -1000)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "frac_bits out of range");
+  const int64_t work = std::max<int64_t>(f->hi4 - f->lo4, f->n - f->tail_lo);
+  if (work <= 0) return EW_OK;
+  if (f->n_units == 0) {
+    EW_CUDA_TRY(cudaMemsetAsync(f->out + 4 * f->lo4, 0, (f->hi4 - f->lo4) * 16, (cudaStream_t)stream));
+    if (f->n > f->tail_lo)
+      EW_CUDA_TRY(cudaMemsetAsync(f->out + f->tail_lo, 0, (f->n - f->tail_lo) * 4, (cudaStream_t)stream));
+    return EW_OK;
+  }
+  const int grid = static_cast<int>(std::min<int64_t>((work + 255) / 256, 8 * num_sms()));
+  peer_fold_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      f->d_units, f->n_units, f->lo4, f->hi4, f->tail_lo, f->n, std::ldexp(1.0, frac_bits),
+      std::ldexp(1.0, -frac_bits), f->out);
+  EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}
+
+int ew_peer_fold_all_gather(ew_peer_fold* f, ew_stream_t stream) {
+  if (f == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL peer fold");
+  if (f->gather == nullptr) return EW_OK;
+  return ew_copy_program_launch(f->gather, 0, 0, stream);
+}
+
+void ew_peer_fold_free(ew_peer_fold* f) {
+  if (f == nullptr) return;
+  if (f->d_units) cudaFree(f->d_units);
+  if (f->gather) ew_copy_program_free(f->gather);
+  delete f;
+}
+
+}  // extern "C"

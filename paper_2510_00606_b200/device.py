@@ -283,6 +283,125 @@ def fixed_to_double(acc: torch.Tensor, frac_bits: int, out: Optional[torch.Tenso
     return out
 
 
+class PeerFold:
+    """(d) fused with its collective over NVLink peer memory (ew_peer_fold).
+
+    Built from EVERY rank's unit pointers/weights and output buffers (peer
+    pointers IPC-mapped by the caller).  reduce_scatter -> host barrier ->
+    all_gather leaves the full reduced fp32 vector in this rank's output."""
+
+    def __init__(self, world: int, rank: int, n_elems: int, unit_ptrs: Sequence[int],
+                 weights: Sequence[float], out_ptrs: Sequence[int]):
+        u = (C.c_void_p * max(1, len(unit_ptrs)))(*unit_ptrs)
+        w = (C.c_double * max(1, len(weights)))(*[float(x) for x in weights])
+        o = (C.c_void_p * max(1, len(out_ptrs)))(*out_ptrs)
+        h = C.c_void_p()
+        check(lib.ew_peer_fold_create(world, rank, int(n_elems), u, w, len(unit_ptrs), o,
+                                      C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.ew_peer_fold_free(self._h)
+            self._h = None
+
+    def reduce_scatter(self, frac_bits: int, stream=None) -> None:
+        check(lib.ew_peer_fold_reduce_scatter(self._h, int(frac_bits), _stream(stream)))
+
+    def all_gather(self, stream=None) -> None:
+        check(lib.ew_peer_fold_all_gather(self._h, _stream(stream)))
+
+    def run(self, frac_bits: int, barrier: "PeerBarrier", stream=None) -> None:
+        """barrier -> reduce-scatter -> barrier -> all-gather, all enqueued on
+        one stream (no host synchronisation; device-timed)."""
+        barrier.wait(stream)
+        self.reduce_scatter(frac_bits, stream)
+        barrier.wait(stream)
+        self.all_gather(stream)
+
+
+class PeerBarrier:
+    """Stream-ordered cross-GPU barrier over peer memory (ew_peer_barrier)."""
+
+    def __init__(self, group=None, timeout_s: float = 30.0):
+        import torch.distributed as dist
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.timeout_s = timeout_s
+        self.flags = torch.zeros(max(2, self.world), dtype=torch.int64, device="cuda")
+        handles = [None] * self.world
+        dist.all_gather_object(handles, ipc_handle(self.flags), group=group)
+        self._opened = []
+        ptrs = []
+        for r, (h, off) in enumerate(handles):
+            if r == self.rank:
+                ptrs.append(self.flags.data_ptr())
+            else:
+                p = ipc_open(h, off)
+                self._opened.append(p)
+                ptrs.append(p)
+        torch.cuda.synchronize()
+        dist.barrier(group=group)  # every flag array is zero before first use
+        arr = (C.c_void_p * self.world)(*ptrs)
+        h = C.c_void_p()
+        check(lib.ew_peer_barrier_create(self.world, self.rank, arr, C.byref(h)))
+        self._h = h
+
+    def wait(self, stream=None) -> None:
+        check(lib.ew_peer_barrier_wait(self._h, self.timeout_s, _stream(stream)))
+
+    def timed_out(self) -> bool:
+        t = C.c_int()
+        check(lib.ew_peer_barrier_timed_out(self._h, C.byref(t)))
+        return bool(t.value)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value:
+            lib.ew_peer_barrier_free(self._h)
+            self._h = None
+        for p in self._opened:
+            ipc_close(p)
+        self._opened = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def peer_weighted_reduce_setup(units: Sequence[torch.Tensor], weights: Sequence[float],
+                               out: torch.Tensor, group=None):
+    """Exchange IPC handles of every rank's units and output buffer (over
+    torch.distributed, plumbing only) and build this rank's PeerFold.
+    Returns (fold, total_units, opened_peer_pointers)."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    mine = {"units": [ipc_handle(u) for u in units], "w": [float(x) for x in weights],
+            "out": ipc_handle(out), "n": out.numel()}
+    allv = [None] * world
+    dist.all_gather_object(allv, mine, group=group)
+    opened, unit_ptrs, wts, out_ptrs = [], [], [], []
+    for r, d in enumerate(allv):
+        if d["n"] != out.numel():
+            raise N.DimensionMismatch("ranks disagree on the gradient length")
+        if r == rank:
+            unit_ptrs += [u.data_ptr() for u in units]
+            out_ptrs.append(out.data_ptr())
+        else:
+            for h, off in d["units"]:
+                p = ipc_open(h, off)
+                opened.append(p)
+                unit_ptrs.append(p)
+            p = ipc_open(*d["out"])
+            opened.append(p)
+            out_ptrs.append(p)
+        wts += d["w"]
+    fold = PeerFold(world, rank, out.numel(), unit_ptrs, wts, out_ptrs)
+    return fold, len(unit_ptrs), opened
+
+
 class Communicator:
     """NCCL communicator of the DP group (ew_comm), shrinkable in place."""
 

@@ -118,6 +118,42 @@ def _worker(rank, world, port, result_dir):
             report["shrunk size"] = shrunk.size
             shrunk.destroy()
         comm.destroy()
+        # the same reduce fused with its collective over peer memory (no NCCL)
+        dist.barrier()
+        mine = [u for u in range(n_units) if u % world == rank]
+        units = [torch.from_numpy(g[u]).cuda() for u in mine]
+        out = torch.empty(dim, dtype=torch.float32, device="cuda")
+        fold, total, opened = dev.peer_weighted_reduce_setup(units, [w[u] for u in mine], out)
+        amax = dev.weighted_absmax(units, [w[u] for u in mine]) if units else \
+            torch.zeros(1, dtype=torch.float64, device="cuda")
+        dist.all_reduce(amax, op=dist.ReduceOp.MAX)
+        f = dev.fixed_point_bits(amax.item(), total)
+        dist.barrier()
+        fold.reduce_scatter(f)
+        torch.cuda.synchronize()
+        dist.barrier()
+        fold.all_gather()
+        torch.cuda.synchronize()
+        dist.barrier()
+        all_units = [torch.from_numpy(x).cuda() for x in g]
+        acc1 = torch.empty(dim, dtype=torch.int64, device="cuda")
+        dev.weighted_fold(all_units, w, f, acc1)
+        single = dev.fixed_to_float(acc1, f)
+        report["peer reduce bit-identical to 1-GPU fold"] = bool(torch.equal(out, single))
+        # stream-ordered version: device-side barriers between the phases
+        bar = dev.PeerBarrier()
+        out.fill_(-1.0)
+        for _ in range(3):
+            fold.run(f, bar)
+        bar.wait()  # nobody leaves while a peer may still read its chunk
+        torch.cuda.synchronize()
+        report["device barrier ok"] = not bar.timed_out()
+        report["peer reduce (device barriers) bit-identical"] = bool(torch.equal(out, single))
+        dist.barrier()
+        bar.close()
+        del fold
+        for p in opened:
+            dev.ipc_close(p)
     except Exception as e:  # report, do not hang the other ranks
         report["error"] = repr(e)
     import json
