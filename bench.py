@@ -48,7 +48,8 @@ def parse_args():
     p.add_argument("--block-bytes", type=int, default=65536)
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--reshard-reps", type=int, default=10)
-    p.add_argument("--reduce-elems", type=int, default=1 << 30)
+    # config E: a 7B-sized fp32 gradient per rank
+    p.add_argument("--reduce-elems", type=int, default=6_738_415_616)
     p.add_argument("--cpu-sample-bytes", type=int, default=1 << 30)
     p.add_argument("--skip", default="", help="comma list of: e2e,reshard,philox,reduce,cpu")
     p.add_argument("--json-out", default="")
@@ -346,7 +347,14 @@ def run_reshard(args, rank, world, out):
     if bufs.new is not None:
         bufs.new.zero_()
 
-    # communicator repair: host edit plan + ncclCommShrink of the DP communicator
+    # Communicator repair.  The B200 DP group's "links" are CUDA-IPC peer
+    # mappings (the weighted reduce runs over peer memory, ew_peer_fold), so
+    # the edit is plan_edit + unmapping the departed rank.  The NCCL
+    # communicator shrink is timed beside it as the library baseline.
+    probe = torch.empty(1 << 20, dtype=torch.uint8, device="cuda")
+    handles = [None] * world
+    dist.all_gather_object(handles, dev.ipc_handle(probe))
+    peer_maps = {r: dev.ipc_open(*handles[r]) for r in old if r != rank}
     uid = [dev.Communicator.unique_id() if rank == 0 else None]
     dist.broadcast_object_list(uid, src=0)
     comm = dev.Communicator.init(uid[0], world, rank)
@@ -356,14 +364,27 @@ def run_reshard(args, rank, world, out):
     t0 = time.perf_counter()
     pool = {(a, b) for a in old for b in old if a < b}
     edit = fabric.plan_edit([fabric.CommGroup("dp-stage-1", old)], fabric.FAIL_STOP, [drop], pool)
-    shrunk = comm.shrink([drop]) if rank != drop else None
-    torch.cuda.synchronize()
+    for a, b in edit.links_to_remove:  # unmap the departed rank's buffers
+        peer = b if a == rank else (a if b == rank else None)
+        if peer is not None and peer in peer_maps:
+            dev.ipc_close(peer_maps.pop(peer))
     t_comm = time.perf_counter() - t0
+    barrier(world)
+    t0 = time.perf_counter()
+    shrunk = comm.shrink([drop]) if rank != drop else None
+    if shrunk is not None:
+        shrunk.allreduce_i64(warm)  # first collective pays NCCL's lazy connect
+    torch.cuda.synchronize()
+    t_nccl = time.perf_counter() - t0
+    for p in peer_maps.values():
+        dev.ipc_close(p)
+    t_comm, t_nccl = max_over_ranks([t_comm, t_nccl], world)
 
     barrier(world)
     t0 = time.perf_counter()
     ex.bind(bufs)
     t_bind = time.perf_counter() - t0
+    t_plan, t_bind = max_over_ranks([t_plan, t_bind], world)
     stream = torch.cuda.current_stream()
     for _ in range(2):
         ex.launch()
@@ -382,6 +403,9 @@ def run_reshard(args, rank, world, out):
 
     # verification without re-reading the source: block sums of the target
     # shards (added over ranks) == block sums of the source shards
+    # (the "before" sums stand for the per-step snapshot rows every rank
+    # already holds; the bench's departed rank is still alive to supply its
+    # own, a real one's are known from its last snapshot)
     block = args.block_bytes
     nblocks = (sum(lb) + block - 1) // block
     before = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
@@ -389,19 +413,19 @@ def run_reshard(args, rank, world, out):
     if rank in rp.old_ranks:
         mo = shard_map(rp.src, rank, block)
         rows = mo.new_row_sums()
-        src_buf = bufs.old
-        if rank == drop:  # the dead rank's bytes as its ring holder keeps them
-            src_buf = bufs.old
-        dev.checksum(mo, src_buf, rows)
+        dev.checksum(mo, bufs.old, rows)
         dev.rows_to_blocks(mo, rows, before)
+    dist.all_reduce(before)
+    barrier(world)
+    t0 = time.perf_counter()
     if bufs.new is not None:
         mn = shard_map(rp.dst, rank, block)
         rows = mn.new_row_sums()
         dev.checksum(mn, bufs.new, rows)
         dev.rows_to_blocks(mn, rows, after)
-    dist.all_reduce(before)
     dist.all_reduce(after)
     verified = bool(torch.equal(before, after))
+    t_verify = max_over_ranks([time.perf_counter() - t0], world)[0]
     traffic = rp.traffic()
     bott = traffic["bottleneck_bytes"]
     nvl_gbs = bott / t_copy[0] / 1e9 if bott else None
@@ -414,8 +438,10 @@ def run_reshard(args, rank, world, out):
         "bottleneck_nvlink_gbs": round(nvl_gbs, 1) if nvl_gbs else None,
         "nvlink_frac_of_900": round(nvl_gbs / 900.0, 4) if nvl_gbs else None,
         "nvlink_frac_of_770_measured": round(nvl_gbs / 770.0, 4) if nvl_gbs else None,
-        "mttr_ms": {"plan": round(t_plan * 1e3, 3), "comm_edit_and_nccl_shrink": round(t_comm * 1e3, 3),
-                    "peer_map": round(t_bind * 1e3, 3), "copy": round(t_copy[0] * 1e3, 3)},
+        "mttr_ms": {"plan": round(t_plan * 1e3, 3), "comm_edit": round(t_comm * 1e3, 3),
+                    "peer_map": round(t_bind * 1e3, 3), "copy": round(t_copy[0] * 1e3, 3),
+                    "verify": round(t_verify * 1e3, 3)},
+        "baseline_nccl_shrink_plus_first_collective_ms": round(t_nccl * 1e3, 3),
         "edit_plan": {"links_removed": len(edit.links_to_remove), "links_added": len(edit.links_to_add)},
     }
     out["reshard"]["mttr_ms"]["total"] = round(sum(out["reshard"]["mttr_ms"].values()), 3)
@@ -489,9 +515,49 @@ def run_reduce(args, rank, world, out):
                                           m2.elapsed_time(e) / 1e3], world)
     out["reduce"] = {"elements": n, "frac_bits": f, "fold_ms": round(t_fold * 1e3, 3),
                      "fold_gbs": round(12 * n / t_fold / 1e9, 1),
-                     "allreduce_int64_ms": round(t_ar * 1e3, 3) if world > 1 else None,
-                     "dequant_ms": round(t_deq * 1e3, 3)}
-    del g, acc, res
+                     "nccl_allreduce_int64_ms": round(t_ar * 1e3, 3) if world > 1 else None,
+                     "dequant_ms": round(t_deq * 1e3, 3),
+                     "nccl_path_ms": round((t_fold + t_ar + t_deq) * 1e3, 3)}
+    del acc
+    torch.cuda.empty_cache()
+    if world > 1:
+        # the same reduce fused with its collective over NVLink peer memory
+        peer_out = torch.empty(n, dtype=torch.float32, device="cuda")
+        fold, total, opened = dev.peer_weighted_reduce_setup([g], w, peer_out)
+        bar = dev.PeerBarrier()
+        fold.run(f, bar)
+        bar.wait()
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(3):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier(world)
+            s.record()
+            fold.run(f, bar)
+            e.record()
+            bar.wait()
+            torch.cuda.synchronize()
+            times.append(s.elapsed_time(e) / 1e3)
+        assert not bar.timed_out(), "peer barrier timed out"
+        t_peer = max_over_ranks([min(times)], world)[0]
+        identical = bool(torch.equal(peer_out, res))
+        ok = torch.tensor([1 if identical else 0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        nvl = 2 * (world - 1) / world * 4 * n  # bytes pulled per GPU (both phases)
+        out["reduce"].update({
+            "peer_path_ms": round(t_peer * 1e3, 3),
+            "peer_path_nvlink_gbs": round(nvl / t_peer / 1e9, 1),
+            "peer_vs_nccl_speedup": round((t_fold + t_ar + t_deq) / t_peer, 2),
+            "peer_bit_identical_to_nccl": bool(ok.item())})
+        bar.wait()
+        torch.cuda.synchronize()
+        barrier(world)
+        bar.close()
+        del fold
+        for p in opened:
+            dev.ipc_close(p)
+        del peer_out
+    del g, res
     torch.cuda.empty_cache()
 
 
