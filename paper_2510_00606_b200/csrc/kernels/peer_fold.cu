@@ -215,8 +215,10 @@ int ew_peer_fold_create(int world, int rank, int64_t n_elems, const float* const
   std::vector<void*> dsts;
   std::vector<int64_t> bytes;
   std::vector<int> remote;
-  for (int r = 0; r < world; ++r) {
-    if (r == rank) continue;
+  // ring order (rank+1, rank+2, ...): CTAs work through the items in order,
+  // so at any moment each peer's chunk is being read by one puller
+  for (int step = 1; step < world; ++step) {
+    const int r = (rank + step) % world;
     const int64_t lo = 4 * lo_of(r);
     const int64_t hi = (r == world - 1) ? n_elems : 4 * lo_of(r + 1);
     if (hi <= lo) continue;

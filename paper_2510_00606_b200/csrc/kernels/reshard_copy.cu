@@ -294,7 +294,19 @@ int ew_copy_program_create(const ew_copy_desc* descs, int64_t n, void* const* bu
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_copy_program_create: bad arguments");
   *out = nullptr;
   std::vector<CopyItem> remote, local;
-  for (int64_t i = 0; i < n; ++i) {
+  // Remote copies in ring order of their peer (exec+1, exec+2, ...): CTAs
+  // sweep items in order, so the receivers of a pull (or the targets of a
+  // push) start on different peers instead of all hitting the same one.
+  std::vector<int64_t> order(static_cast<std::size_t>(std::max<int64_t>(n, 0)));
+  for (int64_t i = 0; i < n; ++i) order[static_cast<std::size_t>(i)] = i;
+  auto peer_of = [&](const ew_copy_desc& c) {
+    const int p = (c.src_rank != exec_rank) ? c.src_rank : c.dst_rank;
+    return (p - exec_rank + table_ranks) % table_ranks;
+  };
+  std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
+    return peer_of(descs[a]) < peer_of(descs[b]);
+  });
+  for (const int64_t i : order) {
     const ew_copy_desc& c = descs[i];
     if (c.bytes < 0 || c.src_role < 0 || c.src_role > 2 || c.dst_role < 0 || c.dst_role > 2 ||
         c.src_rank < 0 || c.src_rank >= table_ranks || c.dst_rank < 0 ||
