@@ -12,8 +12,10 @@
 #include <set>
 #include <vector>
 
+#include "elaskit/dataflow.hpp"
 #include "elaskit/migration.hpp"
 #include "elaskit/param_fabric.hpp"
+#include "elaskit/rng.hpp"
 
 namespace elaskit::b200 {
 
@@ -64,5 +66,12 @@ struct CopyDesc {
 std::vector<CopyDesc> reshard_copies(const TransferPlan& plan, const PartitionLayout& src,
                                      const PartitionLayout& dst, const std::set<int>& failed,
                                      const SnapshotRing* ring, int exec_rank, bool push);
+
+// Sample offsets of micro-batch 0 whose owning slot changes between two
+// assignments — the SampleReassignment list recover_elaswave derives before
+// reshard_rng (reference: sim.cpp:694-715; offsets beyond the smaller
+// per-micro-batch total are ignored, as there).
+std::vector<SampleReassignment> sample_reassignments(const MicrobatchAssignment& old_mb,
+                                                     const MicrobatchAssignment& new_mb);
 
 }  // namespace elaskit::b200

@@ -133,6 +133,17 @@ int ew_reshard_copies(const ew_plan* plan, const ew_layout* src, const ew_layout
 int ew_reshard_microbatches(const int* old_per_slot_mbs, int n_old, int num_microbatches,
                             const int* survivors, int n_survivors, int* out_slots,
                             int* out_per_slot_mbs);
+/* SampleReassignment derivation of recover_elaswave (sim.cpp:694-715) between
+ * two assignments: rows {sample_offset, old_slot, new_slot}. */
+int ew_sample_reassignments(const int* old_slots, const int* old_mbs, int n_old,
+                            const int* new_slots, const int* new_mbs, int n_new, int64_t* rows,
+                            int64_t cap, int64_t* n_out);
+/* plan_zero_migration (migration.cpp:87-154): kind 0 = Contiguous,
+ * 1 = Interleaved; rows {src, dst, cross_stage, lo, hi, round};
+ * totals {cross, intra, total}. */
+int ew_plan_zero_migration(int kind, int dp_degree, const int64_t* layer_bytes, int n_layers,
+                           int layer_idx, int dst_dp_degree, int64_t* rows, int64_t cap,
+                           int64_t* n_out, int64_t* totals);
 /* weighted_grad_average (dataflow.cpp:71-83), fp64, grads row-major [n][dim] */
 int ew_weighted_grad_average(const double* weights, const double* grads, int n, int64_t dim,
                              double* out);

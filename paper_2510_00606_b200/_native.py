@@ -140,6 +140,8 @@ _sig("ew_reshard_copies", i32, vp, vp, vp, P(i32), i32, P(i32), i32, i32, i32, P
      P(i64))
 _sig("ew_reshard_microbatches", i32, P(i32), i32, i32, P(i32), i32, P(i32), P(i32))
 _sig("ew_weighted_grad_average", i32, P(f64), P(f64), i32, i64, P(f64))
+_sig("ew_sample_reassignments", i32, P(i32), P(i32), i32, P(i32), P(i32), i32, P(i64), i64, P(i64))
+_sig("ew_plan_zero_migration", i32, i32, i32, P(i64), i32, i32, i32, P(i64), i64, P(i64), P(i64))
 _sig("ew_philox4x64", i32, P(u64), P(u64), P(u64))
 _sig("ew_draw", i32, u64, u64, u32, u32, i32, P(f64))
 _sig("ew_plan_edit", i32, i32, P(C.c_char_p), P(i32), P(i32), P(i32), i32, P(i32), i32, P(i32),

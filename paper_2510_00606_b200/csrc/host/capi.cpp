@@ -279,6 +279,57 @@ int ew_reshard_microbatches(const int* old_per_slot_mbs, int n_old, int num_micr
   });
 }
 
+int ew_sample_reassignments(const int* old_slots, const int* old_mbs, int n_old,
+                            const int* new_slots, const int* new_mbs, int n_new, int64_t* rows,
+                            int64_t cap, int64_t* n_out) {
+  return guarded([&]() -> int {
+    if (n_old < 0 || n_new < 0 || n_out == nullptr)
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_sample_reassignments: bad arguments");
+    elaskit::MicrobatchAssignment a, b;
+    a.slots.assign(old_slots, old_slots + n_old);
+    a.per_slot_mbs.assign(old_mbs, old_mbs + n_old);
+    b.slots.assign(new_slots, new_slots + n_new);
+    b.per_slot_mbs.assign(new_mbs, new_mbs + n_new);
+    const auto r = elaskit::b200::sample_reassignments(a, b);
+    *n_out = static_cast<int64_t>(r.size());
+    for (int64_t i = 0; i < std::min<int64_t>(cap, *n_out); ++i) {
+      rows[3 * i] = r[static_cast<std::size_t>(i)].sample_id;
+      rows[3 * i + 1] = r[static_cast<std::size_t>(i)].old_slot;
+      rows[3 * i + 2] = r[static_cast<std::size_t>(i)].new_slot;
+    }
+    return *n_out > cap ? set_error(EW_ERR_CAPACITY, "row buffer too small") : EW_OK;
+  });
+}
+
+int ew_plan_zero_migration(int kind, int dp_degree, const int64_t* layer_bytes, int n_layers,
+                           int layer_idx, int dst_dp_degree, int64_t* rows, int64_t cap,
+                           int64_t* n_out, int64_t* totals) {
+  return guarded([&]() -> int {
+    if (n_layers < 0 || n_out == nullptr || totals == nullptr)
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_plan_zero_migration: bad arguments");
+    elaskit::ZeroLayout z;
+    z.kind = kind ? elaskit::ZeroKind::Interleaved : elaskit::ZeroKind::Contiguous;
+    z.dp_degree = dp_degree;
+    z.layer_bytes.assign(layer_bytes, layer_bytes + n_layers);
+    const auto p = elaskit::plan_zero_migration(layer_idx, z, dst_dp_degree);
+    *n_out = static_cast<int64_t>(p.transfers.size());
+    totals[0] = p.cross_bytes;
+    totals[1] = p.intra_bytes;
+    totals[2] = p.total_bytes;
+    for (int64_t i = 0; i < std::min<int64_t>(cap, *n_out); ++i) {
+      const auto& t = p.transfers[static_cast<std::size_t>(i)];
+      int64_t* row = rows + 6 * i;
+      row[0] = t.src_rank;
+      row[1] = t.dst_rank;
+      row[2] = t.cross_stage ? 1 : 0;
+      row[3] = t.iv.lo;
+      row[4] = t.iv.hi;
+      row[5] = t.round;
+    }
+    return *n_out > cap ? set_error(EW_ERR_CAPACITY, "row buffer too small") : EW_OK;
+  });
+}
+
 int ew_weighted_grad_average(const double* weights, const double* grads, int n, int64_t dim,
                              double* out) {
   return guarded([&]() -> int {

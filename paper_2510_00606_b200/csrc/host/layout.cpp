@@ -166,4 +166,26 @@ std::vector<CopyDesc> reshard_copies(const TransferPlan& plan, const PartitionLa
   return out;
 }
 
+std::vector<SampleReassignment> sample_reassignments(const MicrobatchAssignment& old_mb,
+                                                     const MicrobatchAssignment& new_mb) {
+  const auto slot_at = [](const MicrobatchAssignment& a,
+                          const std::vector<std::pair<std::int64_t, std::int64_t>>& ranges,
+                          std::int64_t off) {
+    for (std::size_t i = 0; i < ranges.size(); ++i)
+      if (off >= ranges[i].first && off < ranges[i].second) return a.slots[i];
+    return -1;
+  };
+  const auto old_ranges = old_mb.sample_ranges(0, 0);
+  const auto new_ranges = new_mb.sample_ranges(0, 0);
+  const int total = std::min(old_mb.samples_per_microbatch(), new_mb.samples_per_microbatch());
+  std::vector<SampleReassignment> out;
+  for (int off = 0; off < total; ++off) {
+    const int from = slot_at(old_mb, old_ranges, off);
+    const int to = slot_at(new_mb, new_ranges, off);
+    if (from != to && from >= 0 && to >= 0)
+      out.push_back({static_cast<std::int64_t>(off), from, to});
+  }
+  return out;
+}
+
 }  // namespace elaskit::b200

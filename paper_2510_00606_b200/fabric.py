@@ -237,6 +237,32 @@ def sample_ranges(per_slot_mbs: Sequence[int], step_base: int, mb: int) -> List[
     return out
 
 
+def sample_reassignments(old_slots: Sequence[int], old_mbs: Sequence[int],
+                         new_slots: Sequence[int], new_mbs: Sequence[int]) -> List[Tuple[int, int, int]]:
+    """SampleReassignment derivation (reference sim.cpp:694-715)."""
+    cap = max(1, sum(old_mbs))
+    rows = np.zeros(3 * cap, dtype=np.int64)
+    n = C.c_int64()
+    check(lib.ew_sample_reassignments(N.int_array(old_slots), N.int_array(old_mbs), len(old_slots),
+                                      N.int_array(new_slots), N.int_array(new_mbs), len(new_slots),
+                                      rows.ctypes.data_as(C.POINTER(C.c_int64)), cap, C.byref(n)))
+    return [tuple(int(x) for x in rows[3 * i:3 * i + 3]) for i in range(n.value)]
+
+
+def plan_zero_migration(interleaved: bool, dp_degree: int, layer_bytes: Sequence[int],
+                        layer_idx: int, dst_dp_degree: int):
+    """Reference migration.cpp:87-154 -> (rows {src,dst,cross,lo,hi,round}, totals)."""
+    cap = 4 * max(1, dp_degree) ** 2 + 64
+    rows = np.zeros(6 * cap, dtype=np.int64)
+    tot = np.zeros(3, dtype=np.int64)
+    n = C.c_int64()
+    check(lib.ew_plan_zero_migration(int(interleaved), dp_degree, N.i64_array(layer_bytes),
+                                     len(layer_bytes), layer_idx, dst_dp_degree,
+                                     rows.ctypes.data_as(C.POINTER(C.c_int64)), cap, C.byref(n),
+                                     tot.ctypes.data_as(C.POINTER(C.c_int64))))
+    return rows[:6 * n.value].reshape(-1, 6), tot
+
+
 def weighted_grad_average(weights: Sequence[float], grads: np.ndarray) -> np.ndarray:
     """Reference dataflow.cpp:71-83 (fp64 left fold, host)."""
     g = np.ascontiguousarray(grads, dtype=np.float64)

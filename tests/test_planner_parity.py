@@ -237,3 +237,51 @@ def test_plan_edit_worked_cases():
     pool = {(0, 1), (1, 2), (2, 3), (3, 4), (0, 4)}
     p = fabric.plan_edit([ring], fabric.FAIL_STOP, [2], pool)
     assert p.links_to_remove == {(1, 2), (2, 3)} and p.links_to_add == {(1, 3)}
+
+
+# --------------------------------------------------------------- migration ---
+
+def test_plan_zero_migration_matches_reference(reference):
+    rng = random.Random(31)
+    for trial in range(300):
+        d = rng.choice([1, 2, 3, 4, 5, 7, 8])
+        layers = [rng.randint(0, 3000) for _ in range(rng.randint(1, 6))]
+        layer = rng.randrange(len(layers))
+        interleaved = rng.random() < 0.5
+        dst_d = d if rng.random() < 0.9 else d + 1
+        st, want, want_tot = reference.plan_zero_migration(interleaved, d, layers, layer, dst_d)
+        if st:
+            with pytest.raises(fabric.MismatchedDpDegree):
+                fabric.plan_zero_migration(interleaved, d, layers, layer, dst_d)
+            continue
+        rows, tot = fabric.plan_zero_migration(interleaved, d, layers, layer, dst_d)
+        assert rows.tolist() == want.tolist(), trial
+        assert tot.tolist() == want_tot.tolist()
+
+
+def _reassign_restated(old_slots, old_mbs, new_slots, new_mbs):
+    """sim.cpp:694-715, restated: offsets of micro-batch 0 whose slot changes."""
+    def slot_at(slots, mbs, off):
+        lo = 0
+        for s, m in zip(slots, mbs):
+            if lo <= off < lo + m:
+                return s
+            lo += m
+        return -1
+    out = []
+    for off in range(min(sum(old_mbs), sum(new_mbs))):
+        a, b = slot_at(old_slots, old_mbs, off), slot_at(new_slots, new_mbs, off)
+        if a != b and a >= 0 and b >= 0:
+            out.append((off, a, b))
+    return out
+
+
+def test_sample_reassignments_match_restatement():
+    rng = np.random.default_rng(7)
+    for _ in range(300):
+        n = int(rng.integers(1, 9))
+        mbs = int(rng.integers(1, 6))
+        survivors = sorted({int(s) for s in rng.integers(0, n + 2, size=int(rng.integers(1, n + 2)))})
+        slots, sizes = fabric.reshard_microbatches([mbs] * n, 4, survivors)
+        got = fabric.sample_reassignments(list(range(n)), [mbs] * n, slots, sizes)
+        assert got == _reassign_restated(list(range(n)), [mbs] * n, slots, sizes)
