@@ -453,6 +453,52 @@ def run_reshard(args, rank, world, out):
     torch.cuda.empty_cache()
 
 
+def run_replica(args, rank, world, out):
+    """Ring replica refresh: every holder pulls its ring
+    successor's per-step snapshot over NVLink and verifies it by checksum."""
+    import torch
+    from paper_2510_00606_b200 import configs, device as dev, fabric
+    from paper_2510_00606_b200.recovery import RingReplica
+    from paper_2510_00606_b200.reshard import shard_map
+
+    base = configs.llama2_7b()
+    lb = base.layer_bytes if world == 8 else [x * world // 8 for x in base.layer_bytes]
+    layout = fabric.interleaved_layout(lb, range(world))
+    m = shard_map(layout, rank, args.block_bytes)
+    snap = dev.empty_bytes(layout.shard_bytes(rank))
+    dev.fill_synthetic(m, snap, 11)
+    rows = m.new_row_sums()
+    dev.checksum(m, snap, rows)
+    owner = fabric.SnapshotRing(list(range(world))).backs_up(rank)
+    replica = dev.empty_bytes(layout.shard_bytes(owner))
+    rr = RingReplica(layout, list(range(world)), rank, replica, snap, rows, args.block_bytes)
+    barrier(world)
+    rr.refresh()
+    barrier(world)
+    times = []
+    for _ in range(3):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier(world)
+        s.record()
+        rr.refresh()
+        e.record()
+        barrier(world)
+        times.append(s.elapsed_time(e) / 1e3)
+    bad = int(rr.bad.item())
+    ok = torch.tensor([1 if bad == 0 else 0], device="cuda")
+    import torch.distributed as dist
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    t = max_over_ranks([min(times)], world)[0]
+    nbytes = layout.shard_bytes(owner)
+    out["replica"] = {"what": "holder pulls its ring successor's snapshot shard + rows, re-checksums",
+                      "shard_bytes": int(nbytes), "ms": round(t * 1e3, 3),
+                      "nvlink_gbs": round(nbytes / t / 1e9, 1), "verified": bool(ok.item())}
+    barrier(world)
+    rr.close()
+    del snap, replica
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------------------------- (c) and (d) ---
 
 def run_philox(args, rank, world, out):
@@ -577,6 +623,8 @@ def bench_b200(args):
         run_cpu_baseline(args, out, segs, S)
     if world > 1 and "reshard" not in skip:
         run_reshard(args, rank, world, out)
+    if world > 1 and "replica" not in skip:
+        run_replica(args, rank, world, out)
     if "philox" not in skip:
         run_philox(args, rank, world, out)
     if "reduce" not in skip:
