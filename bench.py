@@ -453,6 +453,58 @@ def run_reshard(args, rank, world, out):
     torch.cuda.empty_cache()
 
 
+def run_stage_move(args, rank, world, out):
+    """Cross-stage ZeRO layer move (PAPER Fig. 10): the 7B
+    model split over two pipeline stages of DP = world/2; stage 0's tail
+    layer (2.83 GB of optimizer state) moves to stage 1, interleaved ZeRO
+    (D j->j sends, in place) vs default contiguous ZeRO (re-cut both stages)."""
+    import torch
+    from paper_2510_00606_b200 import configs, device as dev
+    from paper_2510_00606_b200.reshard import ReshardExecutor, ReshardPlan, shard_map
+
+    lb = configs.llama2_7b().layer_bytes
+    s_layers, t_layers = lb[:17], lb[17:]
+    d = world // 2
+    src_gpus, dst_gpus = list(range(d)), list(range(d, 2 * d))
+    res = {"dp_per_stage": d, "layer_bytes": int(s_layers[-1])}
+    for kind, contiguous in (("interleaved", False), ("contiguous", True)):
+        rp = ReshardPlan.for_stage_move(s_layers, t_layers, src_gpus, dst_gpus, contiguous)
+        ex = ReshardExecutor(rp, rank, push=False)
+        bufs = ex.allocate(in_place=True)
+        dev.fill_synthetic(shard_map(rp.src, rank), bufs.old, 3)
+        barrier(world)
+        ex.bind(bufs)
+        ex.launch()
+        barrier(world)
+        n = rp.dst.shard_bytes(rank)
+        exp = dev.empty_bytes(n)
+        dev.fill_synthetic(shard_map(rp.dst, rank), exp, 3)
+        ok = torch.tensor([1 if torch.equal(bufs.new[:n], exp[:n]) else 0], device="cuda")
+        del exp
+        import torch.distributed as dist
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        times = []
+        for _ in range(3):
+            dev.fill_synthetic(shard_map(rp.src, rank), bufs.old, 3)  # restore the source
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier(world)
+            s.record()
+            ex.launch()
+            e.record()
+            barrier(world)
+            times.append(s.elapsed_time(e) / 1e3)
+        t = max_over_ranks([min(times)], world)[0]
+        tr = rp.traffic()
+        res[kind] = {"ms": round(t * 1e3, 3), "bytes_moved": tr["total_bytes_moved"],
+                     "bottleneck_link_bytes": tr["bottleneck_bytes"], "verified": bool(ok.item())}
+        ex.close()
+        del bufs
+        torch.cuda.empty_cache()
+        barrier(world)
+    res["interleaved_speedup"] = round(res["contiguous"]["ms"] / res["interleaved"]["ms"], 2)
+    out["stage_move"] = res
+
+
 def run_replica(args, rank, world, out):
     """Ring replica refresh: every holder pulls its ring
     successor's per-step snapshot over NVLink and verifies it by checksum."""
@@ -625,6 +677,8 @@ def bench_b200(args):
         run_reshard(args, rank, world, out)
     if world > 1 and "replica" not in skip:
         run_replica(args, rank, world, out)
+    if world > 1 and world % 2 == 0 and "stage" not in skip:
+        run_stage_move(args, rank, world, out)
     if "philox" not in skip:
         run_philox(args, rank, world, out)
     if "reduce" not in skip:

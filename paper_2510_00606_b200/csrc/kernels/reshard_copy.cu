@@ -320,6 +320,8 @@ int ew_copy_program_create(const ew_copy_desc* descs, int64_t n, void* const* bu
     if (src == nullptr || dst == nullptr)
       return set_error(EW_ERR_INVALID_ARGUMENT,
                        "copy descriptor " + std::to_string(i) + " refers to an unmapped buffer");
+    // in-place reshards alias OLD and NEW: retained bytes already in place
+    if (src + c.src_off == dst + c.dst_off) continue;
     // remote = the copy crosses NVLink (the other end is not exec_rank)
     const bool crosses = c.dst_rank != exec_rank || c.src_rank != exec_rank;
     (crosses ? remote : local).push_back({src + c.src_off, dst + c.dst_off, c.bytes, 0});

@@ -59,13 +59,77 @@ class ReshardPlan:
         return cls(list(layer_bytes), old_ranks, new_ranks, failed, src, dst, ring, plan,
                    time.perf_counter() - t0)
 
+    @classmethod
+    def for_stage_move(cls, src_stage_layers: Sequence[int], dst_stage_layers: Sequence[int],
+                       src_gpus: Sequence[int], dst_gpus: Sequence[int],
+                       contiguous: bool = False) -> "ReshardPlan":
+        """Cross-stage interleaved-ZeRO layer move (SURVEY §8(f) #2,
+        reference plan_zero_migration, migration.cpp:87-154): the source
+        stage's TAIL layer moves to the HEAD of the destination stage (equal
+        DP degree).  Both stages' state is laid out in one combined flat space
+        [src layers w/o the mover | mover | dst layers], so the layer keeps its
+        bytes and only changes owner: overlap_matrix then yields exactly the D
+        rank-j -> rank-j sends of plan_zero_migration, and the lowering adds
+        the local repacking of both stages' retained bytes.  Ranks are GPU ids
+        (src_gpus[j] / dst_gpus[j] hold DP rank j of each stage).
+
+        contiguous=True lays each stage out as default ZeRO instead (rank j of
+        a stage owns the j-th equal cut of the stage's flat array), the
+        baseline of the paper's Fig. 10 comparison; both stages are re-cut to
+        balance, so this moves more bytes than the reference's count for the
+        contiguous kind (which only re-cuts the source stage)."""
+        t0 = time.perf_counter()
+        src_gpus, dst_gpus = list(src_gpus), list(dst_gpus)
+        if len(src_gpus) != len(dst_gpus):
+            from ._native import MismatchedDpDegree
+            raise MismatchedDpDegree("stages of unequal DP degree: route through overlap_matrix")
+        if set(src_gpus) & set(dst_gpus):
+            raise ValueError("source and destination stages must use distinct GPUs")
+        d = len(src_gpus)
+        keep, mover = list(src_stage_layers[:-1]), int(src_stage_layers[-1])
+        layers = keep + [mover] + list(dst_stage_layers)
+
+        def owners(stage_of_layer):
+            ranges = {g: [] for g in src_gpus + dst_gpus}
+            off = 0
+            for li, sz in enumerate(layers):
+                gpus = src_gpus if stage_of_layer(li) == 0 else dst_gpus
+                for j, g in enumerate(gpus):
+                    lo, hi = off + sz * j // d, off + sz * (j + 1) // d
+                    if hi > lo:
+                        ranges[g].append((lo, hi))
+                off += sz
+            return PartitionLayout.from_ranges(ranges, sum(layers))
+
+        def contiguous_owners(split):
+            ranges = {g: [] for g in src_gpus + dst_gpus}
+            total = sum(layers)
+            for lo0, hi0, gpus in ((0, split, src_gpus), (split, total, dst_gpus)):
+                size = hi0 - lo0
+                for j, g in enumerate(gpus):
+                    lo, hi = lo0 + size * j // d, lo0 + size * (j + 1) // d
+                    if hi > lo:
+                        ranges[g].append((lo, hi))
+            return PartitionLayout.from_ranges(ranges, total)
+
+        n_keep = len(keep)
+        if contiguous:
+            src = contiguous_owners(sum(keep) + mover)
+            dst = contiguous_owners(sum(keep))
+        else:
+            src = owners(lambda li: 0 if li <= n_keep else 1)   # mover still on the source stage
+            dst = owners(lambda li: 0 if li < n_keep else 1)    # mover now on the destination
+        plan = overlap_matrix(src, dst)
+        all_gpus = sorted(src_gpus + dst_gpus)
+        return cls(layers, all_gpus, all_gpus, [], src, dst, None, plan, time.perf_counter() - t0)
+
     def copies(self, exec_rank: int, push: bool = True) -> np.ndarray:
         return reshard_copies(self.plan, self.src, self.dst, self.failed, self.ring, exec_rank,
                               push)
 
     def replica_of(self, holder: int) -> Optional[int]:
         """Rank whose old shard `holder` keeps (SnapshotRing::backs_up)."""
-        if holder not in self.old_ranks or len(self.old_ranks) < 2:
+        if self.ring is None or holder not in self.old_ranks or len(self.old_ranks) < 2:
             return None
         return self.ring.backs_up(holder)
 
@@ -119,13 +183,34 @@ class ReshardExecutor:
         self.program: Optional[dev.CopyProgram] = None
         self._opened: List[int] = []
 
-    def allocate(self) -> RankBuffers:
+    def allocate(self, in_place: bool = False) -> RankBuffers:
+        """Buffers of this rank.  in_place=True aliases NEW and OLD inside one
+        allocation when that is provably safe — every retained byte keeps
+        its address (one common shift s: OLD = buf[s:], NEW = buf[:]) and no
+        incoming byte lands on the OLD range — so retained bytes are not
+        copied at all (the program skips self-copies).  This is the case for
+        cross-stage layer moves (the source stage drops its tail, the
+        destination stage grows at its head); otherwise separate buffers."""
         rp, r = self.rp, self.rank
-        old = dev.empty_bytes(rp.src.shard_bytes(r)) if r in rp.old_ranks else None
         rep_of = rp.replica_of(r)
         replica = (dev.empty_bytes(rp.src.shard_bytes(rep_of))
                    if rep_of is not None and rep_of in rp.failed else None)
-        new = dev.empty_bytes(rp.dst.shard_bytes(r)) if r in rp.new_ranks else None
+        n_old = rp.src.shard_bytes(r) if r in rp.old_ranks else 0
+        n_new = rp.dst.shard_bytes(r) if r in rp.new_ranks else 0
+        if in_place and n_old and n_new:
+            pulls = rp.copies(r, push=False)
+            kept = pulls[(pulls["src_rank"] == r) & (pulls["src_role"] == ROLE_OLD)]
+            shifts = set((kept["dst_off"] - kept["src_off"]).tolist())
+            if len(shifts) == 1 and min(shifts) >= 0:
+                s = shifts.pop()
+                incoming = pulls[~((pulls["src_rank"] == r) & (pulls["src_role"] == ROLE_OLD))]
+                lo, hi = incoming["dst_off"], incoming["dst_off"] + incoming["bytes"]
+                overlaps = bool(((lo < s + n_old) & (hi > s)).any()) if len(incoming) else False
+                if not overlaps and s % 16 == 0:
+                    buf = dev.empty_bytes(max(n_new, s + n_old))
+                    return RankBuffers(buf[s:s + ((n_old + 15) // 16) * 16], replica, buf)
+        old = dev.empty_bytes(n_old) if r in rp.old_ranks else None
+        new = dev.empty_bytes(n_new) if r in rp.new_ranks else None
         return RankBuffers(old, replica, new)
 
     def bind(self, bufs: RankBuffers, group=None) -> None:

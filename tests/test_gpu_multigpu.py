@@ -66,6 +66,46 @@ def _worker(rank, world, port, result_dir):
                 report[f"reshard drop{drop} push={push}"] = ok
                 ex.close()
                 dist.barrier()
+        # cross-stage layer move (interleaved in place, and contiguous)
+        d = world // 2
+        for contiguous in (False, True):
+            sm = ReshardPlan.for_stage_move(cfg.layer_bytes[:40], cfg.layer_bytes[40:80],
+                                            range(d), range(d, 2 * d), contiguous)
+            ex = ReshardExecutor(sm, rank)
+            bufs = ex.allocate(in_place=True)
+            dev.fill_synthetic(shard_map(sm.src, rank), bufs.old, 8)
+            dist.barrier()
+            ex.bind(bufs)
+            ex.launch()
+            torch.cuda.synchronize()
+            dist.barrier()
+            n = sm.dst.shard_bytes(rank)
+            exp = dev.empty_bytes(n)
+            dev.fill_synthetic(shard_map(sm.dst, rank), exp, 8)
+            report[f"stage move contiguous={contiguous}"] = bool(torch.equal(bufs.new[:n], exp[:n]))
+            ex.close()
+            dist.barrier()
+        # ring replica refresh: pull the successor's snapshot, verify by rows
+        from paper_2510_00606_b200.recovery import RingReplica
+        lay = ReshardPlan.build(cfg.layer_bytes, range(world), range(world)).src
+        m = shard_map(lay, rank)
+        snap = dev.empty_bytes(lay.shard_bytes(rank))
+        dev.fill_synthetic(m, snap, 13)
+        rows = m.new_row_sums()
+        dev.checksum(m, snap, rows)
+        owner = (rank + 1) % world
+        replica = dev.empty_bytes(lay.shard_bytes(owner))
+        rr = RingReplica(lay, list(range(world)), rank, replica, snap, rows)
+        dist.barrier()
+        rr.refresh()
+        torch.cuda.synchronize()
+        exp = dev.empty_bytes(lay.shard_bytes(owner))
+        dev.fill_synthetic(shard_map(lay, owner), exp, 13)
+        report["replica verified"] = int(rr.bad.item()) == 0
+        report["replica bytes"] = bool(torch.equal(replica[:lay.shard_bytes(owner)],
+                                                   exp[:lay.shard_bytes(owner)]))
+        dist.barrier()
+        rr.close()
         # full DP recovery of the last rank (recovery.DpGroup): plan_edit +
         # ncclCommShrink, reshape, remap, checksum verification
         from paper_2510_00606_b200.recovery import DpGroup

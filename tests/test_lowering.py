@@ -69,6 +69,30 @@ def test_lowering_reconstructs_target_bytes(name, cfg, old, new, push, oracle):
         assert (written[r] == 1).all(), "every target byte written exactly once"
 
 
+@pytest.mark.parametrize("d", [1, 2, 3, 4])
+@pytest.mark.parametrize("push", [True, False], ids=["push", "pull"])
+def test_stage_move_is_plan_zero_migration(d, push, oracle):
+    """Cross-stage interleaved move of the source stage's tail layer: the
+    NVLink entries are exactly plan_zero_migration's D j->j sends, and the
+    lowered programs rebuild both stages' target shards byte for byte."""
+    rng = np.random.default_rng(d)
+    src_layers = [int(x) for x in rng.integers(1000, 5000, size=4)]
+    dst_layers = [int(x) for x in rng.integers(1000, 5000, size=3)]
+    src_gpus, dst_gpus = list(range(d)), list(range(d, 2 * d))
+    rp = ReshardPlan.for_stage_move(src_layers, dst_layers, src_gpus, dst_gpus)
+    rows, tot = fabric.plan_zero_migration(True, d, src_layers, len(src_layers) - 1, d)
+    e = rp.plan.entries
+    got = sorted((int(a), int(b), int(lo), int(hi)) for a, b, lo, hi in
+                 zip(e["src_rank"], e["dst_rank"], e["lo"], e["hi"]))
+    want = sorted((src_gpus[int(r[0])], dst_gpus[int(r[1])], int(r[3]), int(r[4])) for r in rows)
+    assert got == want and rp.plan.total_bytes_moved == int(tot[2])
+    bufs, written = _host_execute(rp, oracle, push)
+    for r in rp.new_ranks:
+        want_buf = oracle.fill_synthetic(rp.dst.segments(r), rp.dst.shard_bytes(r), SEED)
+        assert np.array_equal(bufs[(ROLE_NEW, r)], want_buf)
+        assert (written[r] == 1).all()
+
+
 def test_traffic_matches_reference_probe_numbers():
     # SURVEY Appendix A: 7B 8->7 drop r3, bottleneck r2 egress 10.107 GB
     rp = ReshardPlan.build(configs.llama2_7b().layer_bytes, range(8), [0, 1, 2, 4, 5, 6, 7])
