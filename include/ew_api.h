@@ -201,7 +201,8 @@ int64_t ew_shardmap_num_rows(const ew_shardmap* map);
 int ew_shardmap_row_blocks(const ew_shardmap* map, int64_t* out_block_ids, int64_t cap);
 
 /* snap <- live (whole packed buffer) fused with row checksums of live.
- * live/snap 16-byte aligned; row_sums: device uint64[2 * num_rows]. */
+ * live/snap 32-byte aligned (256-bit accesses; ew_checksum / ew_verify
+ * likewise); row_sums: device uint64[2 * num_rows]. */
 int ew_snapshot(const ew_shardmap* map, const void* live, void* snap, uint64_t* row_sums,
                 ew_stream_t stream);
 int ew_checksum(const ew_shardmap* map, const void* buf, uint64_t* row_sums,

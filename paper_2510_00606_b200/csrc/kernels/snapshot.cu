@@ -29,7 +29,7 @@ namespace ew {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kUnroll = 8;
+constexpr int kUnroll = 4;  // 4 x 32 B in flight per thread
 
 __device__ __forceinline__ uint64_t byte_mask(int x, int a, int e) {
   // bytes of the 8-byte word at row-relative x that fall in [a, e)
@@ -48,59 +48,62 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 
 enum class Mode { kSnapshot, kChecksum, kVerify };
 
-// One 16-byte vector of a row: optional copy, edge masking, checksum terms.
-// `idx` is the vector index inside the row, `i` the thread's iteration.
+// One 32-byte vector (four local words) of a row: optional copy, edge
+// masking, checksum terms.  `idx` is the vector index inside the row.
 template <Mode M, bool kShift>
-__device__ __forceinline__ void row_vector(const uint4& v, int idx, int nvec, int head, int end,
+__device__ __forceinline__ void row_vector(const Vec32& v, int idx, int nvec, int head, int end,
                                            int sh, bool copy_first, int pidx, int partial,
-                                           uint4* __restrict__ dvec, uint64_t& t1, uint64_t& t2,
+                                           uint8_t* __restrict__ dvec, uint64_t& t1, uint64_t& t2,
                                            uint64_t& odd, uint64_t& bsum) {
-  const bool edge = (idx == 0) | (idx == nvec - 1);
   if (M == Mode::kSnapshot && idx < nvec) {
-    // each 16-byte vector is copied by the row that holds its first byte
+    // each 32-byte vector is copied by the row that holds its first byte
     if (idx > 0 || copy_first) {
       if (idx != pidx) {
-        st_plain(dvec + idx, v);
+        st_stream32(dvec + 32 * idx, v);
       } else {  // the buffer ends inside this vector: copy its valid bytes only
-        const uint8_t* b = reinterpret_cast<const uint8_t*>(&v);
-        uint8_t* d = reinterpret_cast<uint8_t*>(dvec + idx);
-        for (int k = 0; k < partial; ++k) d[k] = b[k];
+        uint8_t* d = dvec + 32 * idx;
+#pragma unroll
+        for (int k = 0; k < 32; ++k)  // register extraction keeps v out of local memory
+          if (k < partial) d[k] = static_cast<uint8_t>(v.w[k >> 3] >> (8 * (k & 7)));
       }
     }
   }
-  uint64_t w0 = lo64(v);
-  uint64_t w1 = hi64(v);
-  if (edge) {  // row-relative byte coordinates: the row is [head, end)
-    w0 &= byte_mask(16 * idx, head, end);
-    w1 &= byte_mask(16 * idx + 8, head, end);
+  uint64_t w[4] = {v.w[0], v.w[1], v.w[2], v.w[3]};
+  if ((idx == 0) | (idx == nvec - 1)) {  // row-relative byte coordinates: the row is [head, end)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) w[k] &= byte_mask(32 * idx + 8 * k, head, end);
   }
-  uint64_t c0 = w0, c1 = w1, b0 = 0, b1 = 0;
-  if (kShift) {
-    b0 = w0 >> (64 - 8 * sh);
-    b1 = w1 >> (64 - 8 * sh);
-    c0 = (w0 << (8 * sh)) + b0;
-    c1 = (w1 << (8 * sh)) + b1;
-    bsum += b0 + b1;
+  uint64_t c[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    c[k] = w[k];
+    if (kShift) {
+      const uint64_t b = w[k] >> (64 - 8 * sh);
+      c[k] = (w[k] << (8 * sh)) + b;
+      bsum += b;
+    }
   }
-  t1 += c0 + c1;
+  const uint64_t c23 = c[2] + c[3];
+  t1 += (c[0] + c[1]) + c23;
   t2 += t1;
-  odd += c1;
+  odd += c[1] + c23 + c23 + c[3];  // 1*c1 + 2*c2 + 3*c3
 }
 
 template <Mode M, bool kShift>
-__device__ __forceinline__ void row_body(const uint4* __restrict__ svec, uint4* __restrict__ dvec,
+__device__ __forceinline__ void row_body(const uint8_t* __restrict__ svec, uint8_t* __restrict__ dvec,
                                          int nvec, int head, int end, int sh, bool copy_first,
-                                         int pidx, int partial, int& n_exec, uint64_t& t1, uint64_t& t2,
-                                         uint64_t& odd, uint64_t& bsum) {
+                                         int pidx, int partial, int& n_exec, uint64_t& t1,
+                                         uint64_t& t2, uint64_t& odd, uint64_t& bsum) {
   const int tid = threadIdx.x;
   const int iters = (nvec + kThreads - 1) / kThreads;
   n_exec = (iters + kUnroll - 1) / kUnroll * kUnroll;
   for (int it = 0; it < iters; it += kUnroll) {
-    uint4 val[kUnroll];
+    Vec32 val[kUnroll];
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u) {
       const int idx = tid + (it + u) * kThreads;
-      val[u] = idx < nvec ? ld_stream(svec + idx) : make_uint4(0, 0, 0, 0);
+      if (idx < nvec) val[u] = ld_stream32(svec + 32 * idx);
+      else val[u] = Vec32{{0, 0, 0, 0}};
     }
 #pragma unroll
     for (int u = 0; u < kUnroll; ++u)
@@ -126,21 +129,22 @@ __global__ void __launch_bounds__(kThreads, 4) row_kernel(ShardMapView map,
     const RowGeom g = row_geom(map, r);
     const int64_t a = g.local_lo;
     const int64_t e = g.local_lo + g.len;
-    const int64_t v_lo = a >> 4;
+    const int64_t v_lo = a >> 5;
     // row-local 32-bit geometry (a row is at most one checksum block)
-    const int nvec = static_cast<int>(((e + 15) >> 4) - v_lo);
-    const int head = static_cast<int>(a & 15);
+    const int nvec = static_cast<int>(((e + 31) >> 5) - v_lo);
+    const int head = static_cast<int>(a & 31);
     const int end = head + static_cast<int>(g.len);
     const int sh = static_cast<int>(g.delta & 7);  // delta >= 0 for packed shards
     const bool copy_first = head == 0;
     // the buffer's last vector may be partial: copy only its valid bytes
-    const int partial = static_cast<int>(map.total_bytes & 15);
-    const int64_t last_vec = (map.total_bytes - 1) >> 4;
+    const int partial = static_cast<int>(map.total_bytes & 31);
+    const int64_t last_vec = (map.total_bytes - 1) >> 5;
     const int pidx = (partial && last_vec >= v_lo && last_vec < v_lo + nvec)
                          ? static_cast<int>(last_vec - v_lo) : -1;
-    const int64_t q_t = floor_div(16 * (v_lo + tid) + g.delta, 8);
-    const uint4* svec = reinterpret_cast<const uint4*>(src) + v_lo;
-    uint4* dvec = (M == Mode::kSnapshot) ? reinterpret_cast<uint4*>(dst) + v_lo : nullptr;
+    // global word index of this thread's first word
+    const int64_t q_t = floor_div(32 * (v_lo + tid) + g.delta, 8);
+    const uint8_t* svec = src + 32 * v_lo;
+    uint8_t* dvec = (M == Mode::kSnapshot) ? dst + 32 * v_lo : nullptr;
 
     uint64_t t1 = 0, t2 = 0, odd = 0, bsum = 0;
     int n_exec = 0;
@@ -150,9 +154,10 @@ __global__ void __launch_bounds__(kThreads, 4) row_kernel(ShardMapView map,
     else
       row_body<M, true>(svec, dvec, nvec, head, end, sh, copy_first, pidx, partial, n_exec, t1,
                         t2, odd, bsum);
+    // words of iteration i start at q_t + 4*kThreads*i: sum_i i*D_i = n*T1 - T2
     uint64_t s0 = t1;
     uint64_t s1 = static_cast<uint64_t>(q_t + 1) * t1 +
-                  static_cast<uint64_t>(2 * kThreads) *
+                  static_cast<uint64_t>(4 * kThreads) *
                       (static_cast<uint64_t>(n_exec) * t1 - t2) + odd + bsum;
 
     s0 = warp_sum_u64(s0);
@@ -251,6 +256,7 @@ int row_grid(const void* kernel, int64_t n_rows) {
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
 
 }  // namespace
 }  // namespace ew
@@ -338,8 +344,8 @@ int ew_snapshot(const ew_shardmap* map, const void* live, void* snap, uint64_t* 
                 ew_stream_t stream) {
   if (map == nullptr || row_sums == nullptr || (map->total_bytes > 0 && (!live || !snap)))
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_snapshot: NULL argument");
-  if (!aligned16(live) || !aligned16(snap))
-    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_snapshot: live/snap must be 16-byte aligned");
+  if (!aligned32(live) || !aligned32(snap))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_snapshot: live/snap must be 32-byte aligned");
   if (map->n_rows == 0) return EW_OK;
   auto k = row_kernel<Mode::kSnapshot>;
   k<<<row_grid((const void*)k, map->n_rows), kThreads, 0, (cudaStream_t)stream>>>(
@@ -353,7 +359,7 @@ int ew_checksum(const ew_shardmap* map, const void* buf, uint64_t* row_sums,
                 ew_stream_t stream) {
   if (map == nullptr || row_sums == nullptr || (map->total_bytes > 0 && !buf))
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_checksum: NULL argument");
-  if (!aligned16(buf)) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_checksum: buf must be 16-byte aligned");
+  if (!aligned32(buf)) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_checksum: buf must be 32-byte aligned");
   if (map->n_rows == 0) return EW_OK;
   auto k = row_kernel<Mode::kChecksum>;
   k<<<row_grid((const void*)k, map->n_rows), kThreads, 0, (cudaStream_t)stream>>>(
@@ -368,7 +374,7 @@ int ew_verify(const ew_shardmap* map, const void* buf, const uint64_t* expected,
   if (map == nullptr || expected == nullptr || bad_count == nullptr ||
       (map->total_bytes > 0 && !buf))
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_verify: NULL argument");
-  if (!aligned16(buf)) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_verify: buf must be 16-byte aligned");
+  if (!aligned32(buf)) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_verify: buf must be 32-byte aligned");
   EW_CUDA_TRY(cudaMemsetAsync(bad_count, 0, sizeof(uint32_t), (cudaStream_t)stream));
   if (map->n_rows == 0) return EW_OK;
   auto k = row_kernel<Mode::kVerify>;
