@@ -21,6 +21,8 @@
 // odd word), so s1 needs only additions: sum i*D_i = n*T1 - T2 with the
 // running sums T1 += D_i, T2 += T1 (D_i = C_even + C_odd of iteration i).
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 #include "ew_device.cuh"
@@ -258,6 +260,223 @@ int row_grid(const void* kernel, int64_t n_rows) {
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
 
+// ------------------------------------------------------------------------
+// TMA-fed variant: the load pipeline never drains at row boundaries.
+//
+// Warp 0 (one lane) streams 16 KiB pieces of this CTA's rows into a ring of
+// shared-memory stages with cp.async.bulk (mbarrier complete_tx); four
+// consumer warps checksum each stage from shared memory (16-byte units,
+// conflict-free), the first consumer lane writes the snapshot copy of the
+// stage back with one bulk shared->global store, and the stage is released
+// once both the consumers and the store engine have read it.  Row sums are
+// reduced among the consumers only (named barrier 1), so the producer keeps
+// loading the next row meanwhile.  Checksum arithmetic is the same as
+// row_kernel (unit k of a row's 32-byte-aligned window holds global words
+// q_t + 256*i, i = the thread's iteration).
+constexpr int kTmaConsumers = 4;                  // warps
+constexpr int kTmaThreads = 32 * (kTmaConsumers + 1);
+constexpr int kTmaStages = 4;
+constexpr int kTmaPiece = 16 * 1024;              // bytes per stage
+constexpr int kTmaSmem = kTmaStages * kTmaPiece;  // 64 KiB -> 3 CTAs per SM
+constexpr int kTmaUnitsPerThread = kTmaPiece / 16 / (32 * kTmaConsumers);  // 8
+
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(32 * kTmaConsumers) : "memory");
+}
+
+struct TmaRow {
+  int64_t w0;      // first local byte of the 32-byte-aligned window
+  int head, end;   // the row inside the window: [head, end)
+  int n_pieces;
+  int64_t window_bytes;
+};
+
+__device__ __forceinline__ TmaRow tma_row(const ShardMapView& m, int64_t r, RowGeom& g) {
+  g = row_geom(m, r);
+  TmaRow t;
+  t.w0 = g.local_lo & ~int64_t{31};
+  t.head = static_cast<int>(g.local_lo - t.w0);
+  t.end = t.head + static_cast<int>(g.len);
+  t.window_bytes = ((g.local_lo + g.len + 31) & ~int64_t{31}) - t.w0;
+  t.n_pieces = static_cast<int>((t.window_bytes + kTmaPiece - 1) / kTmaPiece);
+  return t;
+}
+
+template <Mode M>
+__global__ void __launch_bounds__(kTmaThreads) tma_row_kernel(ShardMapView map,
+                                                              const uint8_t* __restrict__ src,
+                                                              uint8_t* __restrict__ dst,
+                                                              uint64_t* __restrict__ row_sums,
+                                                              const uint64_t* __restrict__ expected,
+                                                              uint32_t* __restrict__ bad_count,
+                                                              int64_t* __restrict__ bad_rows,
+                                                              int64_t bad_cap) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[kTmaStages];
+  __shared__ __align__(8) uint64_t empty[kTmaStages];
+  __shared__ uint64_t red0[kTmaConsumers], red1[kTmaConsumers];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kTmaStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kTmaConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == 0) {  // producer
+    if (lane != 0) return;
+    int64_t k = 0;
+    for (int64_t r = blockIdx.x; r < map.n_rows; r += gridDim.x) {
+      RowGeom g;
+      const TmaRow t = tma_row(map, r, g);
+      for (int p = 0; p < t.n_pieces; ++p, ++k) {
+        const int s = static_cast<int>(k % kTmaStages);
+        if (k >= kTmaStages) {
+          mbar_wait(&empty[s], static_cast<uint32_t>(((k / kTmaStages) - 1) & 1));
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+        const int64_t off = static_cast<int64_t>(p) * kTmaPiece;
+        const uint32_t n =
+            static_cast<uint32_t>(min(static_cast<int64_t>(kTmaPiece), t.window_bytes - off));
+        mbar_expect_tx(&full[s], n);
+        tma_load(ring + s * kTmaPiece, src + t.w0 + off, n, &full[s]);
+      }
+    }
+    return;
+  }
+
+  const int ctid = threadIdx.x - 32;
+  const int cwarp = warp - 1;
+  const int64_t last_vec_byte = (map.total_bytes - 1) & ~int64_t{31};  // start of the last 32-B vector
+  const int partial = static_cast<int>(map.total_bytes & 31);
+  int64_t k = 0;
+  for (int64_t r = blockIdx.x; r < map.n_rows; r += gridDim.x) {
+    RowGeom g;
+    const TmaRow t = tma_row(map, r, g);
+    const int sh = static_cast<int>(g.delta & 7);
+    const int64_t q_t = floor_div(t.w0 + 16 * ctid + g.delta, 8);
+    uint64_t t1 = 0, t2 = 0, odd = 0, bsum = 0;
+    for (int p = 0; p < t.n_pieces; ++p, ++k) {
+      const int s = static_cast<int>(k % kTmaStages);
+      mbar_wait(&full[s], static_cast<uint32_t>((k / kTmaStages) & 1));
+      const uint8_t* stage = ring + s * kTmaPiece;
+      const int base = p * kTmaPiece;  // window byte of the stage's first byte
+      const int n = static_cast<int>(min(static_cast<int64_t>(kTmaPiece), t.window_bytes - base));
+      if (M == Mode::kSnapshot && ctid == 0) {
+        // store the 32-byte vectors this row owns (the row holding a
+        // vector's first byte copies it); the buffer's partial last vector
+        // goes through byte stores below
+        int lo = (p == 0 && t.head != 0) ? 32 : 0;
+        int hi = n;
+        const int64_t last_in_window = last_vec_byte - t.w0 - base;
+        if (partial && last_in_window >= 0 && last_in_window < n) hi = static_cast<int>(last_in_window);
+        if (hi > lo) {
+          tma_store(dst + t.w0 + base + lo, stage + lo, static_cast<uint32_t>(hi - lo));
+          bulk_commit();
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kTmaUnitsPerThread; ++u) {
+        const int x = 16 * (ctid + u * 32 * kTmaConsumers);  // byte in the stage
+        const int wx = base + x;                             // byte in the window
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (x < n) v = lds128(stage + x);
+        uint64_t w0 = lo64(v), w1 = hi64(v);
+        if (wx < t.head || wx + 16 > t.end) {
+          w0 &= byte_mask(wx, t.head, t.end);
+          w1 &= byte_mask(wx + 8, t.head, t.end);
+        }
+        uint64_t c0 = w0, c1 = w1;
+        if (sh != 0) {
+          const uint64_t b0 = w0 >> (64 - 8 * sh), b1 = w1 >> (64 - 8 * sh);
+          c0 = (w0 << (8 * sh)) + b0;
+          c1 = (w1 << (8 * sh)) + b1;
+          bsum += b0 + b1;
+        }
+        t1 += c0 + c1;
+        t2 += t1;
+        odd += c1;
+      }
+      if (M == Mode::kSnapshot && partial) {
+        const int64_t last_in_window = last_vec_byte - t.w0 - base;
+        if (last_in_window >= 0 && last_in_window < n && ctid < partial &&
+            (last_in_window > 0 || p > 0 || t.head == 0))
+          dst[t.w0 + base + last_in_window + ctid] = stage[last_in_window + ctid];
+      }
+      if (M == Mode::kSnapshot && ctid == 0) bulk_wait_read<0>();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    const int64_t n_exec = static_cast<int64_t>(t.n_pieces) * kTmaUnitsPerThread;
+    uint64_t s0 = t1;
+    uint64_t s1 = static_cast<uint64_t>(q_t + 1) * t1 +
+                  static_cast<uint64_t>(2 * 32 * kTmaConsumers) *
+                      (static_cast<uint64_t>(n_exec) * t1 - t2) + odd + bsum;
+    s0 = warp_sum_u64(s0);
+    s1 = warp_sum_u64(s1);
+    if (lane == 0) {
+      red0[cwarp] = s0;
+      red1[cwarp] = s1;
+    }
+    consumer_sync();
+    if (ctid == 0) {
+      uint64_t x0 = 0, x1 = 0;
+#pragma unroll
+      for (int w = 0; w < kTmaConsumers; ++w) {
+        x0 += red0[w];
+        x1 += red1[w];
+      }
+      if (M == Mode::kVerify) {
+        if (x0 != expected[2 * r] || x1 != expected[2 * r + 1]) {
+          const uint32_t slot = atomicAdd(bad_count, 1u);
+          if (bad_rows != nullptr && static_cast<int64_t>(slot) < bad_cap) bad_rows[slot] = r;
+        }
+      } else {
+        row_sums[2 * r] = x0;
+        row_sums[2 * r + 1] = x1;
+      }
+    }
+    consumer_sync();
+  }
+  if (M == Mode::kSnapshot && ctid == 0) bulk_wait_all();
+}
+
+// EW_ROW_KERNEL=reg selects the register-streaming row_kernel (A/B runs).
+bool use_tma_rows() {
+  static const bool tma = [] {
+    const char* e = getenv("EW_ROW_KERNEL");
+    return !(e && std::string(e) == "reg");
+  }();
+  return tma;
+}
+
+template <Mode M>
+int launch_rows(const ShardMapView& v, const uint8_t* src, uint8_t* dst, uint64_t* rows,
+                const uint64_t* expected, uint32_t* bad, int64_t* bad_rows, int64_t cap,
+                cudaStream_t stream) {
+  if (use_tma_rows()) {
+    auto k = tma_row_kernel<M>;
+    static bool attr = false;
+    if (!attr) {
+      EW_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+      attr = true;
+    }
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTmaThreads, kTmaSmem);
+    const int64_t grid = std::min<int64_t>(v.n_rows, static_cast<int64_t>(num_sms()) * std::max(1, per_sm));
+    k<<<static_cast<int>(grid), kTmaThreads, kTmaSmem, stream>>>(v, src, dst, rows, expected, bad,
+                                                                  bad_rows, cap);
+  } else {
+    auto k = row_kernel<M>;
+    k<<<row_grid((const void*)k, v.n_rows), kThreads, 0, stream>>>(v, src, dst, rows, expected,
+                                                                    bad, bad_rows, cap);
+  }
+  EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}
+
 }  // namespace
 }  // namespace ew
 
@@ -347,12 +566,9 @@ int ew_snapshot(const ew_shardmap* map, const void* live, void* snap, uint64_t* 
   if (!aligned32(live) || !aligned32(snap))
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_snapshot: live/snap must be 32-byte aligned");
   if (map->n_rows == 0) return EW_OK;
-  auto k = row_kernel<Mode::kSnapshot>;
-  k<<<row_grid((const void*)k, map->n_rows), kThreads, 0, (cudaStream_t)stream>>>(
-      map->view(), static_cast<const uint8_t*>(live), static_cast<uint8_t*>(snap), row_sums,
-      nullptr, nullptr, nullptr, 0);
-  EW_CUDA_TRY(cudaGetLastError());
-  return EW_OK;
+  return launch_rows<Mode::kSnapshot>(map->view(), static_cast<const uint8_t*>(live),
+                                      static_cast<uint8_t*>(snap), row_sums, nullptr, nullptr,
+                                      nullptr, 0, (cudaStream_t)stream);
 }
 
 int ew_checksum(const ew_shardmap* map, const void* buf, uint64_t* row_sums,
@@ -361,12 +577,9 @@ int ew_checksum(const ew_shardmap* map, const void* buf, uint64_t* row_sums,
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_checksum: NULL argument");
   if (!aligned32(buf)) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_checksum: buf must be 32-byte aligned");
   if (map->n_rows == 0) return EW_OK;
-  auto k = row_kernel<Mode::kChecksum>;
-  k<<<row_grid((const void*)k, map->n_rows), kThreads, 0, (cudaStream_t)stream>>>(
-      map->view(), static_cast<const uint8_t*>(buf), nullptr, row_sums, nullptr, nullptr, nullptr,
-      0);
-  EW_CUDA_TRY(cudaGetLastError());
-  return EW_OK;
+  return launch_rows<Mode::kChecksum>(map->view(), static_cast<const uint8_t*>(buf), nullptr,
+                                      row_sums, nullptr, nullptr, nullptr, 0,
+                                      (cudaStream_t)stream);
 }
 
 int ew_verify(const ew_shardmap* map, const void* buf, const uint64_t* expected,
@@ -377,12 +590,9 @@ int ew_verify(const ew_shardmap* map, const void* buf, const uint64_t* expected,
   if (!aligned32(buf)) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_verify: buf must be 32-byte aligned");
   EW_CUDA_TRY(cudaMemsetAsync(bad_count, 0, sizeof(uint32_t), (cudaStream_t)stream));
   if (map->n_rows == 0) return EW_OK;
-  auto k = row_kernel<Mode::kVerify>;
-  k<<<row_grid((const void*)k, map->n_rows), kThreads, 0, (cudaStream_t)stream>>>(
-      map->view(), static_cast<const uint8_t*>(buf), nullptr, nullptr, expected, bad_count,
-      bad_rows, bad_cap);
-  EW_CUDA_TRY(cudaGetLastError());
-  return EW_OK;
+  return launch_rows<Mode::kVerify>(map->view(), static_cast<const uint8_t*>(buf), nullptr,
+                                    nullptr, expected, bad_count, bad_rows, bad_cap,
+                                    (cudaStream_t)stream);
 }
 
 int ew_rows_to_blocks(const ew_shardmap* map, const uint64_t* row_sums, uint64_t* block_sums,
