@@ -176,10 +176,26 @@ __global__ void __launch_bounds__(kThreads) staged_copy_kernel(const CopyItem* _
     const int s = static_cast<int>(k % kStages);
     mbar_wait(&full[s], static_cast<uint32_t>((k / kStages) & 1));
     const Piece pc = piece_at(list, n_items, first + k * step);
-    write_piece(ring + s * kStageBytes, pc, ctid);
+    const uint8_t* stage = ring + s * kStageBytes;
+    const bool aligned =
+        ((reinterpret_cast<uintptr_t>(pc.src) | reinterpret_cast<uintptr_t>(pc.dst)) & 15) == 0;
+    if (aligned && pc.bytes >= 16) {
+      // 16-byte-congruent piece: one bulk shared->global store of the body
+      // (no register traffic); the <16-byte tail by byte stores
+      const int body = pc.bytes & ~15;
+      if (ctid == 0) {
+        tma_store(pc.dst, stage, static_cast<uint32_t>(body));
+        bulk_commit();
+      }
+      if (ctid >= 32 && ctid < 32 + (pc.bytes - body)) pc.dst[body + ctid - 32] = stage[body + ctid - 32];
+      if (ctid == 0) bulk_wait_read<0>();  // the stage may be reused once read
+    } else {
+      write_piece(stage, pc, ctid);
+    }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
+  if (ctid == 0) bulk_wait_all();  // bulk stores complete before the kernel retires
 }
 
 }  // namespace
