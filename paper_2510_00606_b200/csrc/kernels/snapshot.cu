@@ -458,11 +458,8 @@ int launch_rows(const ShardMapView& v, const uint8_t* src, uint8_t* dst, uint64_
                 cudaStream_t stream) {
   if (use_tma_rows()) {
     auto k = tma_row_kernel<M>;
-    static bool attr = false;
-    if (!attr) {
-      EW_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
-      attr = true;
-    }
+    // per device and cheap: set on every launch rather than caching
+    EW_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTmaThreads, kTmaSmem);
     const int64_t grid = std::min<int64_t>(v.n_rows, static_cast<int64_t>(num_sms()) * std::max(1, per_sm));
