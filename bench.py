@@ -51,6 +51,8 @@ def parse_args():
     # config E: a 7B-sized fp32 gradient per rank
     p.add_argument("--reduce-elems", type=int, default=6_738_415_616)
     p.add_argument("--cpu-sample-bytes", type=int, default=1 << 30)
+    p.add_argument("--reshard-state-gb", type=float, default=0.0,
+                   help="config D: per-GPU ZeRO state for the reshard leg (fill-HBM geometry)")
     p.add_argument("--skip", default="", help="comma list of: e2e,reshard,philox,reduce,cpu")
     p.add_argument("--json-out", default="")
     return p.parse_args()
@@ -329,8 +331,12 @@ def run_reshard(args, rank, world, out):
     from paper_2510_00606_b200.reshard import ReshardExecutor, ReshardPlan, shard_map
 
     base = configs.llama2_7b()
-    # 7B-per-GPU state over `world` ranks (exactly config B at world = 8)
-    lb = base.layer_bytes if world == 8 else [x * world // 8 for x in base.layer_bytes]
+    # 7B-per-GPU state over `world` ranks (exactly config B at world = 8), or
+    # config D's fill-HBM geometry with --reshard-state-gb per GPU
+    if args.reshard_state_gb > 0:
+        lb = configs.fill_hbm(world, int(args.reshard_state_gb * 1e9)).layer_bytes
+    else:
+        lb = base.layer_bytes if world == 8 else [x * world // 8 for x in base.layer_bytes]
     drop = min(3, world - 1)
     old = list(range(world))
     new = [r for r in old if r != drop]
