@@ -43,3 +43,23 @@ def test_cpp_consumer_builds_and_plans(tmp_path):
     n_entries, moved, n_copies, mapped = map(int, out)
     assert moved == 402 and n_entries == 9 and mapped == 1
     assert n_copies >= n_entries  # every entry lowered once (pull), plus retained bytes
+
+
+def test_cpp_recovery_driver_builds():
+    """tools/cpp/recover_demo.cpp — the DP recovery driven from C++ only."""
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    subprocess.run(["make", "-s", "-C", str(ROOT / "tools" / "cpp")], check=True)
+    assert (ROOT / "tools" / "cpp" / "recover_demo").exists()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d,failed", [(4, 1), (8, 3), (8, 0), (3, 2)])
+def test_cpp_recovery_driver_runs(d, failed):
+    import json
+    subprocess.run(["make", "-s", "-C", str(ROOT / "tools" / "cpp")], check=True)
+    out = subprocess.run([str(ROOT / "tools" / "cpp" / "recover_demo"), str(d), str(failed), "0.01"],
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    res = json.loads(out.stdout.strip().splitlines()[-1])
+    assert res["conserved"] and res["bytes_ok"]
