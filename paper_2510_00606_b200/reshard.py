@@ -213,22 +213,19 @@ class ReshardExecutor:
         new = dev.empty_bytes(n_new) if r in rp.new_ranks else None
         return RankBuffers(old, replica, new)
 
-    def bind(self, bufs: RankBuffers, group=None) -> None:
-        """Exchange IPC handles with every rank and build this GPU's program."""
-        import torch.distributed as dist
+    def premap(self, bufs: RankBuffers, group=None) -> None:
+        """Steady-state peer mapping (before any failure): import every peer's
+        OLD and REPLICA buffers.  A pull-mode reshard reads only those, so a
+        recovery that premapped pays no cudaIpcOpenMemHandle on its critical
+        path (bind() then only builds the program)."""
+        self._exchange(bufs, group, roles=(ROLE_OLD, ROLE_REPLICA), needed=None)
+        self._premapped = True
 
-        mine = {}
-        for role, t in ((ROLE_OLD, bufs.old), (ROLE_REPLICA, bufs.replica), (ROLE_NEW, bufs.new)):
-            if t is not None:
-                mine[role] = dev.ipc_handle(t)
-        world = dist.get_world_size(group)
-        gathered: List[Dict[int, Tuple[bytes, int]]] = [None] * world  # type: ignore
-        dist.all_gather_object(gathered, (self.rank, mine), group=group)
-        table: Dict[Tuple[int, int], int] = {}
-        local = {ROLE_OLD: bufs.old, ROLE_REPLICA: bufs.replica, ROLE_NEW: bufs.new}
-        for role, t in local.items():
-            if t is not None:
-                table[(role, self.rank)] = t.data_ptr()
+    def bind(self, bufs: RankBuffers, group=None) -> None:
+        """Map the peer buffers this GPU's copies touch (unless premapped) and
+        build its program.  Collective over `group`: every rank calls it, and
+        the exchange is skipped only when every rank premapped for a pull
+        (the same decision everywhere, so no rank waits on a missing peer)."""
         descs = self.rp.copies(self.rank, self.push)
         needed = set()
         for c in descs:
@@ -236,14 +233,41 @@ class ReshardExecutor:
                                (int(c["dst_role"]), int(c["dst_rank"]))):
                 if rank != self.rank:
                     needed.add((role, rank))
-        for peer_rank, handles in gathered:
-            for role, (h, off) in handles.items():
-                if (role, peer_rank) in needed:
-                    p = dev.ipc_open(h, off)
-                    self._opened.append(p)
-                    table[(role, peer_rank)] = p
+        if not (getattr(self, "_premapped", False) and not self.push):
+            self._exchange(bufs, group, roles=(ROLE_OLD, ROLE_REPLICA, ROLE_NEW), needed=needed)
+        table = getattr(self, "_table", {})
+        missing = needed - set(table)
+        if missing:
+            raise RuntimeError(f"peer buffers {sorted(missing)} are not mapped")
+        for role, t in ((ROLE_OLD, bufs.old), (ROLE_REPLICA, bufs.replica), (ROLE_NEW, bufs.new)):
+            if t is not None:
+                table[(role, self.rank)] = t.data_ptr()
+        import torch.distributed as dist
+        world = dist.get_world_size(group)
         n_table = max(max(self.rp.old_ranks + self.rp.new_ranks) + 1, world)
         self.program = dev.CopyProgram.from_descs(descs, table, n_table, self.rank)
+
+    def _exchange(self, bufs: RankBuffers, group, roles, needed) -> None:
+        import torch.distributed as dist
+
+        mine = {}
+        for role, t in ((ROLE_OLD, bufs.old), (ROLE_REPLICA, bufs.replica), (ROLE_NEW, bufs.new)):
+            if t is not None and role in roles:
+                mine[role] = dev.ipc_handle(t)
+        world = dist.get_world_size(group)
+        gathered: List[Dict[int, Tuple[bytes, int]]] = [None] * world  # type: ignore
+        dist.all_gather_object(gathered, (self.rank, mine), group=group)
+        table: Dict[Tuple[int, int], int] = getattr(self, "_table", {})
+        for peer_rank, handles in gathered:
+            if peer_rank == self.rank:
+                continue
+            for role, (h, off) in handles.items():
+                if (role, peer_rank) in table or (needed is not None and (role, peer_rank) not in needed):
+                    continue
+                p = dev.ipc_open(h, off)
+                self._opened.append(p)
+                table[(role, peer_rank)] = p
+        self._table = table
 
     def launch(self, n_ctas: int = 0, remote_ctas: int = 0, stream=None) -> None:
         if self.program is not None:
@@ -254,6 +278,8 @@ class ReshardExecutor:
         for p in self._opened:
             dev.ipc_close(p)
         self._opened = []
+        self._table = {}
+        self._premapped = False
 
 
 def emulate_on_one_gpu(rp: ReshardPlan, seed: int, push: bool = True,

@@ -201,6 +201,7 @@ def _worker(rank, world, port, result_dir):
     dist.destroy_process_group()
 
 
+@pytest.mark.timeout(420)  # a collective mismatch must fail, not hang the box
 @pytest.mark.parametrize("world", [2, 4])
 def test_multi_gpu_reshard_comm_reduce(world, tmp_path):
     if torch.cuda.device_count() < world:
