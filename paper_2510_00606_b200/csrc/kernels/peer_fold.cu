@@ -13,6 +13,7 @@
 // pointers (no NCCL communicator to shrink).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "ew_device.cuh"
@@ -24,6 +25,94 @@ struct PeerUnit {
   const float* p;
   double w;
 };
+
+// TMA-staged reduce-scatter (up to kPfUnitsMax units): one producer lane
+// bulk-loads the same 4 KiB slice of every unit — local or in peer HBM — into
+// a shared-memory stage (one mbarrier per stage), four consumer warps
+// quantise-and-sum the slices from shared memory and write the fp32 output
+// chunk.  The loads keep ~kPfStages x U x 4 KiB in flight per CTA without
+// register traffic, which is what NVLink latency needs.
+constexpr int kPfUnitsMax = 8;
+
+static int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e && *e ? atoi(e) : dflt;
+}
+constexpr int kPfSlice = 4096;  // default bytes per unit per stage = 256 float4
+constexpr int kPfStages = 4;    // default ring depth
+constexpr int kPfStagesMax = 8;
+constexpr int kPfConsumers = 4;
+constexpr int kPfThreads = 32 * (kPfConsumers + 1);
+
+__global__ void __launch_bounds__(kPfThreads) peer_fold_staged_kernel(
+    const PeerUnit* __restrict__ units, int n_units, int64_t lo4, int64_t hi4, double scale,
+    double inv_scale, float* __restrict__ out, int slice, int stages) {
+  extern __shared__ __align__(128) uint8_t ring[];
+  __shared__ __align__(8) uint64_t full[kPfStagesMax];
+  __shared__ __align__(8) uint64_t empty[kPfStagesMax];
+  const int64_t per_piece = slice / 16;
+  const int64_t n_pieces = (hi4 - lo4 + per_piece - 1) / per_piece;
+  const int64_t first = blockIdx.x, step = gridDim.x;
+  if (first >= n_pieces) return;
+  const int64_t mine = (n_pieces - first + step - 1) / step;
+  const int stage_bytes = n_units * slice;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kPfConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (warp == 0) {
+    if (lane != 0) return;
+    for (int64_t k = 0; k < mine; ++k) {
+      const int s = static_cast<int>(k % stages);
+      if (k >= stages) {
+        mbar_wait(&empty[s], static_cast<uint32_t>(((k / stages) - 1) & 1));
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      }
+      const int64_t start = lo4 + (first + k * step) * per_piece;
+      const uint32_t bytes = static_cast<uint32_t>(16 * min(per_piece, hi4 - start));
+      mbar_expect_tx(&full[s], bytes * n_units);
+      for (int u = 0; u < n_units; ++u)
+        tma_load(ring + s * stage_bytes + u * slice, units[u].p + 4 * start, bytes, &full[s]);
+    }
+    return;
+  }
+  double w[kPfUnitsMax];
+#pragma unroll
+  for (int u = 0; u < kPfUnitsMax; ++u) w[u] = u < n_units ? units[u].w : 0.0;
+  const int ctid = threadIdx.x - 32;
+  for (int64_t k = 0; k < mine; ++k) {
+    const int s = static_cast<int>(k % stages);
+    mbar_wait(&full[s], static_cast<uint32_t>((k / stages) & 1));
+    const int64_t start = lo4 + (first + k * step) * per_piece;
+    const int nf4 = static_cast<int>(min(per_piece, hi4 - start));
+    const uint8_t* stage = ring + s * stage_bytes;
+    for (int j = ctid; j < nf4; j += 32 * kPfConsumers) {
+      long long a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+      for (int u = 0; u < kPfUnitsMax; ++u) {
+        if (u < n_units) {
+          const uint4 raw = lds128(stage + u * slice + 16 * j);
+          a0 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.x))) * scale);
+          a1 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.y))) * scale);
+          a2 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.z))) * scale);
+          a3 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.w))) * scale);
+        }
+      }
+      reinterpret_cast<float4*>(out)[start + j] =
+          make_float4(static_cast<float>(static_cast<double>(a0) * inv_scale),
+                      static_cast<float>(static_cast<double>(a1) * inv_scale),
+                      static_cast<float>(static_cast<double>(a2) * inv_scale),
+                      static_cast<float>(static_cast<double>(a3) * inv_scale));
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
 
 // Rank `rank`'s chunk of float4 groups: [lo4, hi4); the last rank also owns
 // the scalar tail [4*n4, n).
@@ -251,10 +340,29 @@ int ew_peer_fold_reduce_scatter(ew_peer_fold* f, int frac_bits, ew_stream_t stre
       EW_CUDA_TRY(cudaMemsetAsync(f->out + f->tail_lo, 0, (f->n - f->tail_lo) * 4, (cudaStream_t)stream));
     return EW_OK;
   }
+  const double scale = std::ldexp(1.0, frac_bits), inv = std::ldexp(1.0, -frac_bits);
+  if (f->n_units <= kPfUnitsMax && f->hi4 > f->lo4) {
+    const int slice = env_int("EW_PF_SLICE", kPfSlice);
+    const int stages = std::min(env_int("EW_PF_STAGES", kPfStages), kPfStagesMax);
+    const int smem = stages * f->n_units * slice;
+    EW_CUDA_TRY(cudaFuncSetAttribute(peer_fold_staged_kernel,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int64_t pieces = (f->hi4 - f->lo4 + slice / 16 - 1) / (slice / 16);
+    const int grid = static_cast<int>(
+        std::min<int64_t>(pieces, env_int("EW_PF_CTAS_PER_SM", 2) * num_sms()));
+    peer_fold_staged_kernel<<<grid, kPfThreads, smem, (cudaStream_t)stream>>>(
+        f->d_units, f->n_units, f->lo4, f->hi4, scale, inv, f->out, slice, stages);
+    EW_CUDA_TRY(cudaGetLastError());
+    if (f->n > f->tail_lo) {  // scalar tail (last rank only)
+      peer_fold_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(f->d_units, f->n_units, 0, 0,
+                                                            f->tail_lo, f->n, scale, inv, f->out);
+      EW_CUDA_TRY(cudaGetLastError());
+    }
+    return EW_OK;
+  }
   const int grid = static_cast<int>(std::min<int64_t>((work + 255) / 256, 8 * num_sms()));
   peer_fold_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
-      f->d_units, f->n_units, f->lo4, f->hi4, f->tail_lo, f->n, std::ldexp(1.0, frac_bits),
-      std::ldexp(1.0, -frac_bits), f->out);
+      f->d_units, f->n_units, f->lo4, f->hi4, f->tail_lo, f->n, scale, inv, f->out);
   EW_CUDA_TRY(cudaGetLastError());
   return EW_OK;
 }
