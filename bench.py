@@ -565,6 +565,87 @@ def run_replica(args, rank, world, out):
     torch.cuda.empty_cache()
 
 
+def run_replay(args, rank, world, out):
+    """Ring replica by optimizer replay (the paper's mechanism, SURVEY §8(f)
+    #1): every rank runs its own AdamW step on its 7B ZeRO shard
+    (842 M params, 14 B/param = 11.79 GB), then every holder replays its ring
+    successor's step into its replica reading the successor's fp32 gradient
+    shard over NVLink (4 B/param), and verifies the replica against the
+    owner's checksum rows.  At N=1 only the owner's step is timed."""
+    import torch
+    from paper_2510_00606_b200 import device as dev
+    from paper_2510_00606_b200.recovery import ReplayReplica
+
+    n = 6_738_415_616 // 8
+    own = dev.AdamState(n)
+    grad = torch.empty(n, dtype=torch.float32, device="cuda").normal_(0, 1e-3)
+    own.master.normal_(0, 0.02)
+    hyper = dev.adam_hyper(lr=1e-4)
+    m = dev.ShardMap(own.segments(), args.block_bytes)
+    rows = m.new_row_sums()
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    step_t = []
+    for step in range(1, 5):
+        a, b = ev(), ev()
+        a.record()
+        dev.adam_step(grad, own, hyper, step)
+        b.record()
+        torch.cuda.synchronize()
+        step_t.append(a.elapsed_time(b) / 1e3)
+    t_step = max_over_ranks([min(step_t[1:])], world)[0]
+    res = {"what": "AdamW step on a 7B ZeRO shard (ew_adam_step)", "params_per_rank": n,
+           "state_bytes": own.nbytes, "owner_step_ms": round(t_step * 1e3, 3),
+           "owner_step_hbm_gbs": round(30 * n / t_step / 1e9, 1)}
+    if world > 1:
+        import torch.distributed as dist
+        replica = dev.AdamState(n)
+        # seed the replica with the successor's current state (one full pull,
+        # as when a ring is (re)formed), then keep it by replay
+        succ = (rank + 1) % world
+        allb = [None] * world
+        dist.all_gather_object(allb, (rank, dev.ipc_handle(own.buf)))
+        h0, o0 = dict(allb)[succ]
+        p0 = dev.ipc_open(h0, o0)
+        barrier(world)
+        dev.CopyProgram.from_pointers([p0], [replica.buf.data_ptr()], [replica.nbytes],
+                                      [True]).launch()
+        torch.cuda.synchronize()
+        barrier(world)
+        dev.ipc_close(p0)
+        rep = ReplayReplica(list(range(world)), rank, replica, grad, rows, args.block_bytes)
+        times, vt, bad = [], [], 0
+        for step in range(5, 9):
+            dev.adam_step(grad, own, hyper, step)
+            dev.checksum(m, own.buf, rows)
+            torch.cuda.synchronize()
+            barrier(world)
+            a, b, c = ev(), ev(), ev()
+            a.record()
+            rep.replay(hyper, step)
+            b.record()
+            rep.verify()
+            c.record()
+            torch.cuda.synchronize()
+            bad += int(rep.bad.item())
+            barrier(world)
+            times.append(a.elapsed_time(b) / 1e3)
+            vt.append(b.elapsed_time(c) / 1e3)
+        t = max_over_ranks([min(times[1:]), min(vt[1:])], world)
+        ok = torch.tensor([1 if bad == 0 else 0], device="cuda")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        res.update({"holder_replay_ms": round(t[0] * 1e3, 3),
+                    "holder_verify_ms": round(t[1] * 1e3, 3),
+                    "nvlink_bytes": 4 * n,
+                    "nvlink_gbs": round(4 * n / t[0] / 1e9, 1),
+                    "replica_verified_every_step": bool(ok.item())})
+        barrier(world)
+        rep.close()
+        del replica
+    out["replay"] = res
+    del own, grad
+    torch.cuda.empty_cache()
+
+
 # ------------------------------------------------------------- (c) and (d) ---
 
 def run_philox(args, rank, world, out):
@@ -691,6 +772,8 @@ def bench_b200(args):
         run_reshard(args, rank, world, out)
     if world > 1 and "replica" not in skip:
         run_replica(args, rank, world, out)
+    if "replay" not in skip:
+        run_replay(args, rank, world, out)
     if world > 1 and world % 2 == 0 and "stage" not in skip:
         run_stage_move(args, rank, world, out)
     if "philox" not in skip:

@@ -326,6 +326,30 @@ int ew_peer_barrier_wait(ew_peer_barrier* barrier, double timeout_s, ew_stream_t
 int ew_peer_barrier_timed_out(ew_peer_barrier* barrier, int* timed_out);
 void ew_peer_barrier_free(ew_peer_barrier* barrier);
 
+/* ------------------------------------------------------------------------
+ * Ring replica by optimizer replay: the
+ * holder of member r's replica applies r's AdamW step from r's reduced
+ * gradient shard (read over NVLink through an IPC pointer) instead of pulling
+ * r's whole 14 B/param state.  The owner runs the same call as its own
+ * optimizer step, so the replica stays byte-identical and r's checksum rows
+ * verify it.  Per element (torch.optim.AdamW, every op IEEE-rounded, no
+ * contraction):
+ *   m' = fma(b1, m, (1-b1)*g)          v' = fma(b2, v, ((1-b2)*g)*g)
+ *   d  = sqrt(v') * (1/sqrt(bc2)) + eps
+ *   p' = fma(-lr/bc1, m'/d, p*(1-lr*wd))   param_bf16 = bf16_rne(p')
+ * with bc_k = 1 - b_k^step and the scalars rounded to fp32 once on the host.
+ * ---------------------------------------------------------------------- */
+typedef struct ew_adam_hyper {
+  double lr, beta1, beta2, eps, weight_decay;
+} ew_adam_hyper;
+/* out8 = {b1, 1-b1, b2, 1-b2, eps, lr/bc1, 1/sqrt(bc2), 1-lr*wd} as fp32 */
+int ew_adam_scalars(const ew_adam_hyper* hyper, int64_t step, float* out8);
+/* In place over n elements; grad may be a peer (IPC) pointer.  fp32 arrays
+ * 16-byte aligned, param_bf16 8-byte aligned; step >= 1. */
+int ew_adam_step(const float* grad, float* master, float* exp_avg, float* exp_avg_sq,
+                 uint16_t* param_bf16, int64_t n, const ew_adam_hyper* hyper, int64_t step,
+                 ew_stream_t stream);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

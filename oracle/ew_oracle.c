@@ -378,3 +378,50 @@ int64_t ew_oracle_verify_mt(const int64_t* segs, int64_t n_segs, int64_t block,
                             const uint8_t* buf, const uint64_t* expected, int threads) {
   return run_mt(segs, n_segs, block, buf, NULL, NULL, expected, threads);
 }
+
+/* ---- ring replica by optimizer replay -------------------
+ * CPU restatement of ew_adam_step (include/ew_api.h): torch.optim.AdamW
+ * (decoupled weight decay) with every operation an explicitly rounded fp32
+ * op, fmaf where the device uses __fmaf_rn, scalars derived in fp64 and
+ * rounded once.  Built with -ffp-contract=off so gcc adds no contraction.
+ * The paper replays this step on the holder from the owner's gradient shard
+ * (PAPER.md:363-372); the reference only models its time (param_fabric.hpp:
+ * 86-96), so parity is pinned against torch.optim.AdamW in the tests. */
+uint16_t ew_oracle_bf16(float f) {
+  uint32_t u;
+  memcpy(&u, &f, 4);
+  if ((u & 0x7FFFFFFFu) > 0x7F800000u) return 0x7FC0u;
+  return (uint16_t)((u + 0x7FFFu + ((u >> 16) & 1u)) >> 16);
+}
+
+void ew_oracle_adam_scalars(double lr, double b1, double b2, double eps, double wd, int64_t step,
+                            float out8[8]) {
+  const double bc1 = 1.0 - pow(b1, (double)step);
+  const double bc2 = 1.0 - pow(b2, (double)step);
+  out8[0] = (float)b1;
+  out8[1] = (float)(1.0 - b1);
+  out8[2] = (float)b2;
+  out8[3] = (float)(1.0 - b2);
+  out8[4] = (float)eps;
+  out8[5] = (float)(lr / bc1);
+  out8[6] = (float)(1.0 / sqrt(bc2));
+  out8[7] = (float)(1.0 - lr * wd);
+}
+
+void ew_oracle_adam_step(const float* grad, float* master, float* exp_avg, float* exp_avg_sq,
+                         uint16_t* param, int64_t n, double lr, double b1, double b2, double eps,
+                         double wd, int64_t step) {
+  float s[8];
+  ew_oracle_adam_scalars(lr, b1, b2, eps, wd, step, s);
+  for (int64_t i = 0; i < n; ++i) {
+    const float g = grad[i];
+    const float m1 = fmaf(s[0], exp_avg[i], s[1] * g);
+    const float v1 = fmaf(s[2], exp_avg_sq[i], (s[3] * g) * g);
+    const float denom = sqrtf(v1) * s[6] + s[4];
+    const float p1 = fmaf(-s[5], m1 / denom, master[i] * s[7]);
+    master[i] = p1;
+    exp_avg[i] = m1;
+    exp_avg_sq[i] = v1;
+    param[i] = ew_oracle_bf16(p1);
+  }
+}

@@ -39,6 +39,13 @@ int ew_oracle_fixed_point_bits(double absmax, int64_t total_units);
 void ew_oracle_weighted_fixed(const double* w, const float* g, int n_units, int64_t dim,
                               int frac_bits, int64_t* acc);
 
+uint16_t ew_oracle_bf16(float f);
+void ew_oracle_adam_scalars(double lr, double b1, double b2, double eps, double wd, int64_t step,
+                            float out8[8]);
+void ew_oracle_adam_step(const float* grad, float* master, float* exp_avg, float* exp_avg_sq,
+                         uint16_t* param, int64_t n, double lr, double b1, double b2, double eps,
+                         double wd, int64_t step);
+
 #ifdef __cplusplus
 }
 #endif

@@ -56,6 +56,8 @@ class Oracle:
         L.ew_oracle_fixed_point_bits.argtypes = [f64, i64]
         L.ew_oracle_fixed_point_bits.restype = i32
         L.ew_oracle_weighted_fixed.argtypes = [P(f64), P(C.c_float), i32, i64, i32, P(i64)]
+        L.ew_oracle_adam_scalars.argtypes = [f64, f64, f64, f64, f64, i64, P(C.c_float)]
+        L.ew_oracle_adam_step.argtypes = [P(C.c_float)] * 4 + [P(C.c_uint16), i64] + [f64] * 5 + [i64]
         L.ew_oracle_snapshot_mt.argtypes = [P(i64), i64, i64, vp, vp, P(u64), i32]
         L.ew_oracle_snapshot_mt.restype = i64
         L.ew_oracle_verify_mt.argtypes = [P(i64), i64, i64, vp, P(u64), i32]
@@ -170,6 +172,22 @@ class Oracle:
         self.lib.ew_oracle_weighted_fixed(_np_ptr(w, f64), _np_ptr(g, C.c_float), len(w),
                                           g.shape[1], frac_bits, _np_ptr(out, i64))
         return out
+
+    # -- ring replica by optimizer replay
+    def adam_scalars(self, hyper, step: int) -> np.ndarray:
+        out = np.zeros(8, dtype=np.float32)
+        self.lib.ew_oracle_adam_scalars(*hyper, step, _np_ptr(out, C.c_float))
+        return out
+
+    def adam_step(self, grad: np.ndarray, master: np.ndarray, exp_avg: np.ndarray,
+                  exp_avg_sq: np.ndarray, param: np.ndarray, hyper, step: int) -> None:
+        """In place; hyper = (lr, beta1, beta2, eps, weight_decay)."""
+        arrs = [grad, master, exp_avg, exp_avg_sq]
+        for a in arrs:
+            assert a.dtype == np.float32 and a.flags.c_contiguous
+        assert param.dtype == np.uint16 and param.flags.c_contiguous
+        self.lib.ew_oracle_adam_step(*[_np_ptr(a, C.c_float) for a in arrs],
+                                     _np_ptr(param, C.c_uint16), len(grad), *hyper, step)
 
 
 class Reference:

@@ -106,6 +106,11 @@ class TransferEntry(C.Structure):
                 ("medium", C.c_int32), ("reserved", C.c_int32)]
 
 
+class AdamHyper(C.Structure):
+    _fields_ = [("lr", C.c_double), ("beta1", C.c_double), ("beta2", C.c_double),
+                ("eps", C.c_double), ("weight_decay", C.c_double)]
+
+
 class CopyDesc(C.Structure):
     _fields_ = [("src_role", C.c_int32), ("src_rank", C.c_int32), ("dst_role", C.c_int32),
                 ("dst_rank", C.c_int32), ("src_off", i64), ("dst_off", i64), ("bytes", i64)]
@@ -203,6 +208,8 @@ _sig("ew_peer_barrier_create", i32, i32, i32, P(vp), P(vp))
 _sig("ew_peer_barrier_wait", i32, vp, f64, vp)
 _sig("ew_peer_barrier_timed_out", i32, vp, P(i32))
 _sig("ew_peer_barrier_free", None, vp)
+_sig("ew_adam_scalars", i32, P(AdamHyper), i64, P(C.c_float))
+_sig("ew_adam_step", i32, vp, vp, vp, vp, vp, i64, P(AdamHyper), i64, vp)
 
 def int_array(values) -> C.Array:
     values = list(values)

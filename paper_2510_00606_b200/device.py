@@ -453,3 +453,58 @@ class Communicator:
                                      _ptr(ws_acc), _ptr(ws_max), _ptr(out), C.byref(f),
                                      _stream(stream)))
         return f.value
+
+
+# ------------------------------------- ring replica by optimizer replay ---
+class AdamState:
+    """One ZeRO shard's AdamW state in HBM, the layout ew_adam_step updates:
+    fp32 master weights, fp32 exp_avg, fp32 exp_avg_sq and the bf16
+    parameter copy (14 B/param, the mixed-precision state of SURVEY §8(d)),
+    structure of arrays in ONE allocation with 256-byte aligned sections and
+    zeroed padding, so the whole state is a single byte image that kernel (a)
+    snapshots and checksums and kernel (b) moves."""
+
+    def __init__(self, n: int, device=None, buf: Optional[torch.Tensor] = None):
+        a = lambda b: (int(b) + 255) // 256 * 256
+        self.n = int(n)
+        sec = a(4 * self.n)
+        self.nbytes = 3 * sec + a(2 * self.n)
+        if buf is None:
+            buf = torch.zeros(self.nbytes, dtype=torch.uint8, device=device or "cuda")
+        if buf.numel() < self.nbytes or buf.data_ptr() % 256:
+            raise ValueError("AdamState buffer too small or not 256-byte aligned")
+        self.buf = buf
+        f32 = lambda k: buf[k * sec:k * sec + 4 * self.n].view(torch.float32)
+        self.master, self.exp_avg, self.exp_avg_sq = f32(0), f32(1), f32(2)
+        self.param = buf[3 * sec:3 * sec + 2 * self.n].view(torch.bfloat16)
+
+    def segments(self) -> np.ndarray:
+        """The state's byte image as one segment at global offset 0."""
+        s = np.zeros(1, dtype=SEGMENT_DTYPE)
+        s[0] = (0, self.nbytes, 0)
+        return s
+
+
+def adam_hyper(lr: float = 1e-4, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+               weight_decay: float = 0.01) -> N.AdamHyper:
+    return N.AdamHyper(lr, beta1, beta2, eps, weight_decay)
+
+
+def adam_scalars(hyper: N.AdamHyper, step: int) -> np.ndarray:
+    out = (C.c_float * 8)()
+    check(lib.ew_adam_scalars(C.byref(hyper), int(step), out))
+    return np.frombuffer(out, dtype=np.float32).copy()
+
+
+def adam_step(grad, state: AdamState, hyper: N.AdamHyper, step: int, stream=None) -> None:
+    """ew_adam_step over the whole shard.  `grad`: fp32 tensor of state.n
+    elements, or a raw device pointer (an IPC-mapped peer gradient shard)."""
+    if isinstance(grad, torch.Tensor):
+        if grad.dtype != torch.float32 or grad.numel() < state.n:
+            raise ValueError("grad must be fp32 with state.n elements")
+        g = _ptr(grad)
+    else:
+        g = C.c_void_p(int(grad))
+    check(lib.ew_adam_step(g, _ptr(state.master), _ptr(state.exp_avg), _ptr(state.exp_avg_sq),
+                           _ptr(state.param), state.n, C.byref(hyper), int(step),
+                           _stream(stream)))

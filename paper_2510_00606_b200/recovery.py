@@ -122,6 +122,63 @@ class RingReplica:
         self._opened = []
 
 
+class ReplayReplica:
+    """Ring replica kept by optimizer replay: the paper's own mechanism
+     with the replica in the holder's HBM.
+
+    Each step the owner reduces its gradient shard and runs ew_adam_step on
+    its AdamState; the holder runs the same ew_adam_step on its replica with
+    the gradient read out of the owner's HBM through an IPC peer pointer —
+    4 B/param cross NVLink instead of the 14 B/param a full state pull
+    (RingReplica) moves.  The replica stays byte-identical because both sides
+    execute the same explicitly-rounded kernel on the same inputs; verify()
+    proves it against the owner's checksum rows without a second transfer.
+    Ordering contract: the owner must not overwrite its gradient shard before
+    the holder's replay of that step finished (a barrier between the replay
+    and the next step's reduce)."""
+
+    def __init__(self, ring_members: Sequence[int], rank: int, replica: "dev.AdamState",
+                 grad: torch.Tensor, rows: torch.Tensor,
+                 block_bytes: int = dev.DEFAULT_BLOCK_BYTES, group=None):
+        """`grad`/`rows`: THIS rank's gradient shard and the checksum rows of
+        its own AdamState (exported to its holder); `replica`: the AdamState
+        of the member this rank backs up (same n as that member's shard)."""
+        from .fabric import SnapshotRing
+        ring = SnapshotRing(list(ring_members))
+        self.rank = rank
+        self.owner = ring.backs_up(rank)
+        self.replica = replica
+        self.map = dev.ShardMap(replica.segments(), block_bytes)
+        world = dist.get_world_size(group)
+        allh = [None] * world
+        dist.all_gather_object(allh, (rank, (dev.ipc_handle(grad), dev.ipc_handle(rows))),
+                               group=group)
+        (h_g, o_g), (h_r, o_r) = dict(allh)[self.owner]
+        self._opened = [dev.ipc_open(h_g, o_g), dev.ipc_open(h_r, o_r)]
+        self.owner_rows = torch.empty(2 * max(1, self.map.num_rows), dtype=torch.int64,
+                                      device="cuda")
+        self.rows_copy = dev.CopyProgram.from_pointers([self._opened[1]],
+                                                       [self.owner_rows.data_ptr()],
+                                                       [16 * self.map.num_rows], [True])
+        self.bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+    def replay(self, hyper, step: int, stream=None) -> None:
+        """Apply the owner's step `step` to the replica (fused NVLink pull)."""
+        dev.adam_step(self._opened[0], self.replica, hyper, step, stream=stream)
+
+    def verify(self, stream=None) -> None:
+        """Compare the replica with the owner's rows (published after the
+        owner's own step); mismatching rows counted in self.bad."""
+        self.rows_copy.launch(stream=stream)
+        dev.verify(self.map, self.replica.buf, self.owner_rows, self.bad, stream=stream)
+
+    def close(self) -> None:
+        self.rows_copy = None
+        for p in self._opened:
+            dev.ipc_close(p)
+        self._opened = []
+
+
 class DpGroup:
     """One rank's view of an interleaved-ZeRO DP group (one process per GPU)."""
 

@@ -106,6 +106,57 @@ def _worker(rank, world, port, result_dir):
                                                    exp[:lay.shard_bytes(owner)]))
         dist.barrier()
         rr.close()
+        # ring replica by optimizer replay: the holder steps its replica from
+        # the owner's gradient read over NVLink; byte-identical, rows verify
+        from paper_2510_00606_b200.recovery import ReplayReplica
+        n_par = 1_000_003 + 17 * rank  # ragged, different per rank
+        n_own = 1_000_003 + 17 * ((rank + 1) % world)
+        gen = torch.Generator(device="cuda").manual_seed(rank)
+        own = dev.AdamState(n_par)
+        own.master.normal_(0, 0.02, generator=gen)
+        grad = torch.empty(n_par, dtype=torch.float32, device="cuda")
+        own_map = dev.ShardMap(own.segments())
+        own_rows = own_map.new_row_sums()
+        replica_state = dev.AdamState(n_own)
+        # initial replica = owner's state at step 0 (one full pull, as at start)
+        allb = [None] * world
+        dist.all_gather_object(allb, (rank, dev.ipc_handle(own.buf)))
+        h0, o0 = dict(allb)[(rank + 1) % world]
+        p0 = dev.ipc_open(h0, o0)
+        dist.barrier()
+        dev.CopyProgram.from_pointers([p0], [replica_state.buf.data_ptr()],
+                                      [replica_state.nbytes], [True]).launch()
+        torch.cuda.synchronize()
+        dist.barrier()
+        dev.ipc_close(p0)
+        rep = ReplayReplica(list(range(world)), rank, replica_state, grad, own_rows)
+        hyper = dev.adam_hyper(lr=1e-3)
+        ok = True
+        for step in range(1, 4):
+            grad.normal_(0, 1e-3, generator=gen)
+            dev.adam_step(grad, own, hyper, step)
+            dev.checksum(own_map, own.buf, own_rows)
+            torch.cuda.synchronize()
+            dist.barrier()   # owner's grad + rows published
+            rep.replay(hyper, step)
+            rep.verify()
+            torch.cuda.synchronize()
+            ok = ok and int(rep.bad.item()) == 0
+            dist.barrier()   # holder done reading before the next step's grad
+        report["replay replica verified"] = ok
+        allb = [None] * world
+        dist.all_gather_object(allb, (rank, dev.ipc_handle(own.buf)))
+        h1, o1 = dict(allb)[(rank + 1) % world]
+        p1 = dev.ipc_open(h1, o1)
+        pulled = dev.empty_bytes(replica_state.nbytes)
+        dev.CopyProgram.from_pointers([p1], [pulled.data_ptr()], [replica_state.nbytes],
+                                      [True]).launch()
+        torch.cuda.synchronize()
+        report["replay replica bytes"] = bool(torch.equal(pulled[:replica_state.nbytes],
+                                                          replica_state.buf))
+        dist.barrier()
+        dev.ipc_close(p1)
+        rep.close()
         # full DP recovery of the last rank (recovery.DpGroup): plan_edit +
         # ncclCommShrink, reshape, remap, checksum verification
         from paper_2510_00606_b200.recovery import DpGroup
