@@ -148,12 +148,12 @@ def barrier(world):
     torch.cuda.synchronize()
 
 
-def max_over_ranks(values, world):
+def max_over_ranks(values, world, group=None):
     import torch
     import torch.distributed as dist
     t = torch.tensor(values, dtype=torch.float64, device="cuda")
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return t.tolist()
 
 
@@ -646,6 +646,115 @@ def run_replay(args, rank, world, out):
     torch.cuda.empty_cache()
 
 
+def run_layer_migration(args, rank, world, out):
+    """Non-blocking migration of one 7B decoder layer (202 M params) from
+    rank 0 to rank 1 with shadow-gradient payback.  The
+    target's step: M = 8 micro-batch folds of the layer's fp32 gradient on a
+    high-priority stream (micro-batches < k fold the target's other work at
+    the same cost), the bf16 parameters pulled over NVLink on a low-priority
+    stream, the source's shadow folds [0, k), its int64 accumulator is pulled
+    behind a device-side barrier and joins the target's last fold.  The
+    reference planner is fed the measured link bandwidth and slot time (its
+    k is used from the second repetition on); the migrated gradient is
+    compared with the static step's bit for bit."""
+    import torch
+    import torch.distributed as dist
+    from paper_2510_00606_b200 import device as dev, fabric
+    from paper_2510_00606_b200.migration import LayerMigration
+
+    pair = dist.new_group([0, 1])
+    if rank > 1:
+        barrier(world)
+        return
+    n, M = 202_383_360, 8
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    unit = torch.empty(n, dtype=torch.float32, device="cuda").normal_(0, 1e-3, generator=gen)
+    units, w = [unit] * M, [1.0 / M] * M
+    f = dev.fixed_point_bits(float(unit.abs().max().item()) / M, M)
+    params = torch.full((n,), 7, dtype=torch.int16, device="cuda") if rank == 0 else \
+        torch.zeros(n, dtype=torch.int16, device="cuda")
+    acc = torch.zeros(n, dtype=torch.int64, device="cuda")
+    scratch = torch.zeros(n, dtype=torch.int64, device="cuda")
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+    hi, lo = torch.cuda.Stream(priority=-1), torch.cuda.Stream(priority=0)
+    # slot = one micro-batch's fold of the layer gradient (stand-in for its compute)
+    with torch.cuda.stream(hi):
+        for _ in range(2):
+            dev.weighted_fold([unit], [w[0]], f, scratch, accumulate=True, stream=hi)
+        a, b = ev(), ev()
+        a.record(hi)
+        dev.weighted_fold([unit], [w[0]], f, scratch, accumulate=True, stream=hi)
+        b.record(hi)
+    torch.cuda.synchronize()
+    slot = max_over_ranks([a.elapsed_time(b) / 1e3], 2, group=pair)[0]
+    other = lambda mb, st: dev.weighted_fold([unit], [w[mb]], f, scratch, accumulate=True,
+                                             stream=st)
+    mig = LayerMigration((16, 0, 1), 0, 1, rank, params, acc, group=pair,
+                         transfer_ctas=int(os.environ.get("EW_MIG_CTAS", 32)))
+    res = {"what": "7B layer (202 M params) stage move 0->1, non-blocking + payback",
+           "param_bytes": 2 * n, "payback_bytes": 8 * n, "microbatches": M,
+           "slot_ms": round(slot * 1e3, 3)}
+    def step(k):
+        acc.zero_()
+        if rank == 1:
+            params.zero_()
+        torch.cuda.synchronize()
+        dist.barrier(group=pair)
+        mig.events.clear()
+        t0, t1 = ev(), ev()
+        t0.record(hi)
+        if rank == 1:
+            mig.run_target(units, w, f, k, hi, lo, other_work=other)
+        else:
+            mig.run_shadow(units, w, f, k, hi)
+        t1.record(hi)
+        torch.cuda.synchronize()
+        info = [None, None]
+        dist.all_gather_object(info, (mig.measured() if rank == 1 else {},
+                                      t0.elapsed_time(t1), mig.timed_out()), group=pair)
+        return info[1]
+
+    static_ms = M * slot * 1e3
+    blocking = [step(0) for _ in range(3)][-1]          # k = 0: blocking move
+    bw = 2 * n / (blocking[0]["params"] / 1e3)
+    plan = {m: fabric.plan_layer_migration((16, 0, 1), m, param_bytes=2 * n, grad_bytes=8 * n,
+                                           link_bw_bytes_per_s=bw, microbatch_slot_s=slot,
+                                           num_microbatches=M, target_headroom_bytes=1 << 40)
+            for m in (fabric.BLOCKING, fabric.NON_BLOCKING)}
+    k = max(1, plan[fabric.NON_BLOCKING].shadow_microbatches)
+    ms, step_ms, timed_out = [step(k) for _ in range(3)][-1]
+    res.update({"link_gbs_measured": round(bw / 1e9, 1),
+                "static_step_ms": round(static_ms, 3),
+                "blocking": {"params_ms": round(blocking[0]["params"], 3),
+                             "target_step_ms": round(blocking[1], 3),
+                             "measured_stall_ms": round(blocking[1] - static_ms, 3),
+                             "planned_stall_ms": round(plan[fabric.BLOCKING].stall_s * 1e3, 3)},
+                "non_blocking": {"k": k, "params_ms": round(ms["params"], 3),
+                                 "payback_pull_ms": round(ms["payback_grad"], 3),
+                                 "payback_gbs": round(8 * n / ms["payback_grad"] / 1e6, 1),
+                                 "target_step_ms": round(step_ms, 3),
+                                 "measured_stall_ms": round(step_ms - static_ms, 3),
+                                 "planned_stall_ms": round(
+                                     plan[fabric.NON_BLOCKING].stall_s * 1e3, 3)},
+                "barrier_timed_out": bool(timed_out)})
+    if rank == 1:
+        static = torch.empty_like(acc)
+        dev.weighted_fold(units, w, f, static)
+        torch.cuda.synchronize()
+        ok = bool(torch.equal(acc, static)) and bool((params == 7).all().item())
+    else:
+        ok = True
+    flag = [None, None]
+    dist.all_gather_object(flag, ok, group=pair)
+    res["gradient_bit_identical_to_static"] = all(flag)
+    dist.barrier(group=pair)
+    mig.close()
+    out["layer_migration"] = res
+    del unit, params, acc, scratch
+    torch.cuda.empty_cache()
+    barrier(world)
+
+
 # ------------------------------------------------------------- (c) and (d) ---
 
 def run_philox(args, rank, world, out):
@@ -774,6 +883,8 @@ def bench_b200(args):
         run_replica(args, rank, world, out)
     if "replay" not in skip:
         run_replay(args, rank, world, out)
+    if world > 1 and "migration" not in skip:
+        run_layer_migration(args, rank, world, out)
     if world > 1 and world % 2 == 0 and "stage" not in skip:
         run_stage_move(args, rank, world, out)
     if "philox" not in skip:

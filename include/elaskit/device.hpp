@@ -16,6 +16,7 @@
 #include "elaskit/b200.hpp"
 #include "elaskit/communicator.hpp"
 #include "elaskit/dataflow.hpp"
+#include "elaskit/migration.hpp"
 #include "elaskit/param_fabric.hpp"
 #include "elaskit/rng.hpp"
 #include "ew_api.h"
@@ -36,7 +37,9 @@ inline void check(int status) {
     case EW_ERR_MISSING_BACKUP: throw MissingBackup(msg);
     case EW_ERR_NO_SURVIVORS: throw NoSurvivors(msg);
     case EW_ERR_DIMENSION_MISMATCH: throw DimensionMismatch(msg);
+    case EW_ERR_MISMATCHED_DP: throw MismatchedDpDegree(msg);
     case EW_ERR_DISCONNECTED: throw DisconnectedGroup(msg);
+    case EW_ERR_INSUFFICIENT_MEMORY: throw InsufficientTargetMemory(msg);
     case EW_ERR_OUT_OF_RANGE: throw std::out_of_range(msg);
     case EW_ERR_CUDA:
     case EW_ERR_NCCL: throw CudaError(msg);

@@ -42,7 +42,8 @@ enum ew_status {
   EW_ERR_CAPACITY = 9,           /* output buffer too small          */
   EW_ERR_CUDA = 10,
   EW_ERR_NCCL = 11,
-  EW_ERR_INTERNAL = 12
+  EW_ERR_INTERNAL = 12,
+  EW_ERR_INSUFFICIENT_MEMORY = 13 /* elaskit::InsufficientTargetMemory */
 };
 
 const char* ew_last_error(void);
@@ -144,6 +145,29 @@ int ew_sample_reassignments(const int* old_slots, const int* old_mbs, int n_old,
 int ew_plan_zero_migration(int kind, int dp_degree, const int64_t* layer_bytes, int n_layers,
                            int layer_idx, int dst_dp_degree, int64_t* rows, int64_t cap,
                            int64_t* n_out, int64_t* totals);
+/* plan_layer_migration (migration.cpp:9-61): mode 0 = Blocking,
+ * 1 = NonBlocking.  Fields mirror MigrationContext / MigrationSchedule
+ * (migration.hpp:22-46); transfers[k].what: 0 = "params", 1 = "payback_grad". */
+typedef struct ew_migration_context {
+  int64_t param_bytes, grad_bytes;
+  double link_bw_bytes_per_s, microbatch_slot_s;
+  int32_t num_microbatches;
+  int64_t target_headroom_bytes;
+  double fixed_overhead_s;
+} ew_migration_context;
+typedef struct ew_transfer_segment {
+  int32_t what;
+  double start_s, end_s;
+  int64_t bytes;
+} ew_transfer_segment;
+typedef struct ew_migration_schedule {
+  int32_t mode, shadow_microbatches, n_transfers;
+  ew_transfer_segment transfers[2];
+  int64_t payback_bytes;
+  double stall_s, total_time_s;
+} ew_migration_schedule;
+int ew_plan_layer_migration(int layer, int src_stage, int dst_stage, int mode,
+                            const ew_migration_context* ctx, ew_migration_schedule* out);
 /* weighted_grad_average (dataflow.cpp:71-83), fp64, grads row-major [n][dim] */
 int ew_weighted_grad_average(const double* weights, const double* grads, int n, int64_t dim,
                              double* out);
@@ -273,6 +297,17 @@ int ew_fixed_point_bits(double global_absmax, int64_t total_units, int* frac_bit
 int ew_weighted_fold(const float* const* units, const double* weights, int n_units,
                      int64_t n_elems, int frac_bits, int64_t* acc, int accumulate,
                      ew_stream_t stream);
+/* Shadow-gradient payback of a non-blocking layer migration: acc[i] +=
+ * payback[i] (int64 fixed point, so the split of micro-batches between the
+ * source's shadow instance and the target is bit-exactly invisible).
+ * payback may be a peer (IPC) pointer: the pull and the add are one pass. */
+int ew_payback_accumulate(int64_t* acc, const int64_t* payback, int64_t n, ew_stream_t stream);
+/* Same, plus acc[i] += addend[i] in the same pass (addend: int64, device or
+ * peer pointer; NULL = none) — used to fold a migration's payback into the
+ * target's last micro-batch instead of a separate pass. */
+int ew_weighted_fold_addend(const float* const* units, const double* weights, int n_units,
+                            int64_t n_elems, int frac_bits, int64_t* acc, int accumulate,
+                            const int64_t* addend, ew_stream_t stream);
 int ew_fixed_to_float(const int64_t* acc, int64_t n, int frac_bits, float* out,
                       ew_stream_t stream);
 int ew_fixed_to_double(const int64_t* acc, int64_t n, int frac_bits, double* out,

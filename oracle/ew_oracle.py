@@ -195,7 +195,7 @@ class Reference:
 
     STATUS = {1: "invalid_argument", 2: "CoverageMismatch", 3: "MissingBackup", 4: "NoSurvivors",
               5: "DimensionMismatch", 6: "MismatchedDpDegree", 7: "DisconnectedGroup",
-              8: "out_of_range", 9: "capacity", 12: "exception"}
+              8: "out_of_range", 9: "capacity", 12: "exception", 13: "InsufficientTargetMemory"}
 
     def __init__(self, path: Path = REF_LIB):
         if not path.exists():
@@ -211,6 +211,8 @@ class Reference:
         L.ref_integrity_check.argtypes = [P(i32), i32, P(i32), P(i32), i32, P(i64), i64, P(i32),
                                           i32, P(i32), P(i32), P(i32)]
         L.ref_zero_shard.argtypes = [P(i64), i32, i32, i32, i32, P(i64), P(i64), P(i64)]
+        L.ref_plan_layer_migration.argtypes = [i32, i32, i32, i32, P(i64), P(f64), P(i64), P(f64)]
+        L.ref_plan_layer_migration.restype = i32
         L.ref_plan_zero_migration.argtypes = [i32, i32, P(i64), i32, i32, i32, P(i64), i64,
                                               P(i64), P(i64)]
         L.ref_philox4x64.argtypes = [P(u64), P(u64), P(u64)]
@@ -305,6 +307,23 @@ class Reference:
         if st:
             return st, None, None
         return 0, out[:6 * n.value].reshape(-1, 6), tot
+
+    def plan_layer_migration(self, layer, src, dst, nonblocking: bool, ctx: dict):
+        """-> (status, dict) with the MigrationSchedule fields (migration.hpp:29-39)."""
+        ic = np.array([ctx["param_bytes"], ctx["grad_bytes"], ctx["num_microbatches"],
+                       ctx["target_headroom_bytes"]], dtype=np.int64)
+        dc = np.array([ctx["link_bw_bytes_per_s"], ctx["microbatch_slot_s"],
+                       ctx["fixed_overhead_s"]], dtype=np.float64)
+        io, do = np.zeros(8, dtype=np.int64), np.zeros(6, dtype=np.float64)
+        st = self.lib.ref_plan_layer_migration(layer, src, dst, int(nonblocking), _np_ptr(ic, i64),
+                                               _np_ptr(dc, f64), _np_ptr(io, i64), _np_ptr(do, f64))
+        if st:
+            return st, None
+        tr = [("payback_grad" if io[4 + 2 * k] else "params", float(do[2 + 2 * k]),
+               float(do[3 + 2 * k]), int(io[5 + 2 * k])) for k in range(int(io[2]))]
+        return 0, {"mode": int(io[0]), "shadow_microbatches": int(io[1]), "transfers": tr,
+                   "payback_bytes": int(io[3]), "stall_s": float(do[0]),
+                   "total_time_s": float(do[1])}
 
     def philox4x64(self, counter, key):
         c, k, o = (u64 * 4)(*counter), (u64 * 2)(*key), (u64 * 4)()

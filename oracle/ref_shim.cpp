@@ -47,6 +47,9 @@ int guarded(F&& f) {
   } catch (const DisconnectedGroup& e) {
     g_err = e.what();
     return 7;
+  } catch (const InsufficientTargetMemory& e) {
+    g_err = e.what();
+    return 13;
   } catch (const std::invalid_argument& e) {
     g_err = e.what();
     return 1;
@@ -182,6 +185,42 @@ int ref_plan_zero_migration(int kind, int dp, const int64_t* layer_bytes, int n_
       row[3] = t.iv.lo;
       row[4] = t.iv.hi;
       row[5] = t.round;
+    }
+    return 0;
+  });
+}
+
+// plan_layer_migration (migration.cpp:9-61).  ictx {param_bytes, grad_bytes,
+// num_microbatches, target_headroom}, dctx {link_bw, slot_s, fixed_overhead};
+// iout {mode, shadow_mbs, n_transfers, payback_bytes, what0, bytes0, what1,
+// bytes1}, dout {stall, total, start0, end0, start1, end1}.
+int ref_plan_layer_migration(int layer, int src, int dst, int mode, const int64_t* ictx,
+                             const double* dctx, int64_t* iout, double* dout) {
+  return guarded([&]() -> int {
+    LayerMove mv;
+    mv.layer = layer;
+    mv.src_stage = src;
+    mv.dst_stage = dst;
+    MigrationContext c;
+    c.param_bytes = ictx[0];
+    c.grad_bytes = ictx[1];
+    c.num_microbatches = static_cast<int>(ictx[2]);
+    c.target_headroom_bytes = ictx[3];
+    c.link_bw_bytes_per_s = dctx[0];
+    c.microbatch_slot_s = dctx[1];
+    c.fixed_overhead_s = dctx[2];
+    const auto s = plan_layer_migration(mv, mode ? MigrationMode::NonBlocking : MigrationMode::Blocking, c);
+    iout[0] = s.mode == MigrationMode::NonBlocking ? 1 : 0;
+    iout[1] = s.shadow_microbatches;
+    iout[2] = static_cast<int64_t>(s.transfers.size());
+    iout[3] = s.payback_bytes;
+    dout[0] = s.stall_s;
+    dout[1] = s.total_time_s;
+    for (std::size_t i = 0; i < s.transfers.size() && i < 2; ++i) {
+      iout[4 + 2 * i] = s.transfers[i].what == "payback_grad" ? 1 : 0;
+      iout[5 + 2 * i] = s.transfers[i].bytes;
+      dout[2 + 2 * i] = s.transfers[i].start_s;
+      dout[3 + 2 * i] = s.transfers[i].end_s;
     }
     return 0;
   });

@@ -54,6 +54,10 @@ class CapacityError(ElaskitError):
     pass
 
 
+class InsufficientTargetMemory(ElaskitError):
+    """elaskit::InsufficientTargetMemory (migration.hpp:13-15)."""
+
+
 class CudaError(ElaskitError):
     pass
 
@@ -73,7 +77,7 @@ class OutOfRange(ElaskitError, IndexError):
 _STATUS = {
     1: InvalidArgument, 2: CoverageMismatch, 3: MissingBackup, 4: NoSurvivors,
     5: DimensionMismatch, 6: MismatchedDpDegree, 7: DisconnectedGroup, 8: OutOfRange,
-    9: CapacityError, 10: CudaError, 11: NcclError, 12: ElaskitError,
+    9: CapacityError, 10: CudaError, 11: NcclError, 12: ElaskitError, 13: InsufficientTargetMemory,
 }
 
 lib.ew_last_error.restype = C.c_char_p
@@ -104,6 +108,25 @@ class Interval(C.Structure):
 class TransferEntry(C.Structure):
     _fields_ = [("src_rank", C.c_int32), ("dst_rank", C.c_int32), ("lo", i64), ("hi", i64),
                 ("medium", C.c_int32), ("reserved", C.c_int32)]
+
+
+class MigrationContext(C.Structure):
+    _fields_ = [("param_bytes", C.c_int64), ("grad_bytes", C.c_int64),
+                ("link_bw_bytes_per_s", C.c_double), ("microbatch_slot_s", C.c_double),
+                ("num_microbatches", C.c_int32), ("target_headroom_bytes", C.c_int64),
+                ("fixed_overhead_s", C.c_double)]
+
+
+class TransferSegment(C.Structure):
+    _fields_ = [("what", C.c_int32), ("start_s", C.c_double), ("end_s", C.c_double),
+                ("bytes", C.c_int64)]
+
+
+class MigrationSchedule(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("shadow_microbatches", C.c_int32),
+                ("n_transfers", C.c_int32), ("transfers", TransferSegment * 2),
+                ("payback_bytes", C.c_int64), ("stall_s", C.c_double),
+                ("total_time_s", C.c_double)]
 
 
 class AdamHyper(C.Structure):
@@ -188,6 +211,7 @@ _sig("ew_philox_words", i32, u64, u64, u32, u32, u64, i64, vp, vp)
 _sig("ew_weighted_absmax", i32, P(vp), P(f64), i32, i64, vp, vp)
 _sig("ew_fixed_point_bits", i32, f64, i64, P(i32))
 _sig("ew_weighted_fold", i32, P(vp), P(f64), i32, i64, i32, vp, i32, vp)
+_sig("ew_weighted_fold_addend", i32, P(vp), P(f64), i32, i64, i32, vp, i32, vp, vp)
 _sig("ew_fixed_to_float", i32, vp, i64, i32, vp, vp)
 _sig("ew_fixed_to_double", i32, vp, i64, i32, vp, vp)
 
@@ -208,6 +232,8 @@ _sig("ew_peer_barrier_create", i32, i32, i32, P(vp), P(vp))
 _sig("ew_peer_barrier_wait", i32, vp, f64, vp)
 _sig("ew_peer_barrier_timed_out", i32, vp, P(i32))
 _sig("ew_peer_barrier_free", None, vp)
+_sig("ew_plan_layer_migration", i32, i32, i32, i32, i32, P(MigrationContext), P(MigrationSchedule))
+_sig("ew_payback_accumulate", i32, vp, vp, i64, vp)
 _sig("ew_adam_scalars", i32, P(AdamHyper), i64, P(C.c_float))
 _sig("ew_adam_step", i32, vp, vp, vp, vp, vp, i64, P(AdamHyper), i64, vp)
 

@@ -46,6 +46,8 @@ int guarded(F&& body) {
     return set_error(EW_ERR_MISMATCHED_DP, e.what());
   } catch (const elaskit::DisconnectedGroup& e) {
     return set_error(EW_ERR_DISCONNECTED, e.what());
+  } catch (const elaskit::InsufficientTargetMemory& e) {
+    return set_error(EW_ERR_INSUFFICIENT_MEMORY, e.what());
   } catch (const std::invalid_argument& e) {
     return set_error(EW_ERR_INVALID_ARGUMENT, e.what());
   } catch (const std::out_of_range& e) {
@@ -327,6 +329,40 @@ int ew_plan_zero_migration(int kind, int dp_degree, const int64_t* layer_bytes, 
       row[5] = t.round;
     }
     return *n_out > cap ? set_error(EW_ERR_CAPACITY, "row buffer too small") : EW_OK;
+  });
+}
+
+int ew_plan_layer_migration(int layer, int src_stage, int dst_stage, int mode,
+                            const ew_migration_context* ctx, ew_migration_schedule* out) {
+  return guarded([&]() -> int {
+    if (ctx == nullptr || out == nullptr || (mode != 0 && mode != 1))
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_plan_layer_migration: bad arguments");
+    elaskit::LayerMove mv;
+    mv.layer = layer;
+    mv.src_stage = src_stage;
+    mv.dst_stage = dst_stage;
+    elaskit::MigrationContext c;
+    c.param_bytes = ctx->param_bytes;
+    c.grad_bytes = ctx->grad_bytes;
+    c.link_bw_bytes_per_s = ctx->link_bw_bytes_per_s;
+    c.microbatch_slot_s = ctx->microbatch_slot_s;
+    c.num_microbatches = ctx->num_microbatches;
+    c.target_headroom_bytes = ctx->target_headroom_bytes;
+    c.fixed_overhead_s = ctx->fixed_overhead_s;
+    const auto s = elaskit::plan_layer_migration(
+        mv, mode ? elaskit::MigrationMode::NonBlocking : elaskit::MigrationMode::Blocking, c);
+    *out = ew_migration_schedule{};
+    out->mode = s.mode == elaskit::MigrationMode::NonBlocking ? 1 : 0;
+    out->shadow_microbatches = s.shadow_microbatches;
+    out->n_transfers = static_cast<int32_t>(std::min<std::size_t>(2, s.transfers.size()));
+    for (int i = 0; i < out->n_transfers; ++i) {
+      const auto& t = s.transfers[static_cast<std::size_t>(i)];
+      out->transfers[i] = {t.what == "payback_grad" ? 1 : 0, t.start_s, t.end_s, t.bytes};
+    }
+    out->payback_bytes = s.payback_bytes;
+    out->stall_s = s.stall_s;
+    out->total_time_s = s.total_time_s;
+    return EW_OK;
   });
 }
 

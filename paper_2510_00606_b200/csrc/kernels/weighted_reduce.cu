@@ -55,10 +55,11 @@ __global__ void __launch_bounds__(256) absmax_kernel(Units u, int64_t n,
 
 template <bool kAccumulate>
 __global__ void __launch_bounds__(256) fold_kernel(Units u, int64_t n, double scale,
-                                                   long long* __restrict__ acc) {
+                                                   long long* __restrict__ acc,
+                                                   const long long* __restrict__ addend) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t n4 = n / 4;
-  bool vec_ok = (reinterpret_cast<uintptr_t>(acc) & 15) == 0;
+  bool vec_ok = ((reinterpret_cast<uintptr_t>(acc) | reinterpret_cast<uintptr_t>(addend)) & 15) == 0;
   for (int k = 0; k < u.n; ++k) vec_ok = vec_ok && ((reinterpret_cast<uintptr_t>(u.p[k]) & 15) == 0);
   if (vec_ok) {
     // kDepth independent float4 groups per thread keep enough loads in flight
@@ -95,6 +96,14 @@ __global__ void __launch_bounds__(256) fold_kernel(Units u, int64_t n, double sc
           s[d][2] += b.x;
           s[d][3] += b.y;
         }
+        if (addend != nullptr) {  // e.g. a migration's shadow-gradient payback
+          const longlong2* src = reinterpret_cast<const longlong2*>(addend + 4 * i);
+          const longlong2 a = __ldcs(src), b = __ldcs(src + 1);
+          s[d][0] += a.x;
+          s[d][1] += a.y;
+          s[d][2] += b.x;
+          s[d][3] += b.y;
+        }
         __stcs(dst, make_longlong2(s[d][0], s[d][1]));
         __stcs(dst + 1, make_longlong2(s[d][2], s[d][3]));
       }
@@ -103,6 +112,7 @@ __global__ void __launch_bounds__(256) fold_kernel(Units u, int64_t n, double sc
   const int64_t start = vec_ok ? 4 * n4 : 0;
   for (int64_t i = start + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
     long long s = kAccumulate ? acc[i] : 0;
+    if (addend != nullptr) s += addend[i];
     for (int k = 0; k < u.n; ++k)
       s += __double2ll_rn((u.w[k] * static_cast<double>(u.p[k][i])) * scale);
     acc[i] = s;
@@ -179,6 +189,13 @@ int ew_fixed_point_bits(double global_absmax, int64_t total_units, int* frac_bit
 int ew_weighted_fold(const float* const* units, const double* weights, int n_units,
                      int64_t n_elems, int frac_bits, int64_t* acc, int accumulate,
                      ew_stream_t stream) {
+  return ew_weighted_fold_addend(units, weights, n_units, n_elems, frac_bits, acc, accumulate,
+                                 nullptr, stream);
+}
+
+int ew_weighted_fold_addend(const float* const* units, const double* weights, int n_units,
+                            int64_t n_elems, int frac_bits, int64_t* acc, int accumulate,
+                            const int64_t* addend, ew_stream_t stream) {
   if (acc == nullptr || n_units < 0 || n_elems < 0 || (n_units > 0 && (!units || !weights)))
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_weighted_fold: bad arguments");
   if (frac_bits > 1000 || frac_bits < -1000)
@@ -188,17 +205,18 @@ int ew_weighted_fold(const float* const* units, const double* weights, int n_uni
   if (n_units == 0) {
     if (!accumulate)
       EW_CUDA_TRY(cudaMemsetAsync(acc, 0, n_elems * sizeof(int64_t), (cudaStream_t)stream));
-    return EW_OK;
+    return addend ? ew_payback_accumulate(acc, addend, n_elems, stream) : EW_OK;
   }
   for (int off = 0; off < n_units; off += kMaxUnits) {
     Units u;
     if (int st = pack_units(units, weights, n_units, off, u)) return st;
     const int grid = grid_for((n_elems + 3) / 4);
     long long* a = reinterpret_cast<long long*>(acc);
+    const long long* add = off == 0 ? reinterpret_cast<const long long*>(addend) : nullptr;
     if (accumulate || off > 0)
-      fold_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a);
+      fold_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a, add);
     else
-      fold_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a);
+      fold_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a, add);
     EW_CUDA_TRY(cudaGetLastError());
   }
   return EW_OK;
@@ -227,3 +245,53 @@ int ew_fixed_to_double(const int64_t* acc, int64_t n, int frac_bits, double* out
 }
 
 }  // extern "C"
+
+namespace ew {
+namespace {
+
+__global__ void __launch_bounds__(256) payback_kernel(long long* __restrict__ acc,
+                                                      const long long* __restrict__ payback,
+                                                      int64_t n) {
+  // 2 x 16 B per thread-iteration in flight; payback usually lives in peer HBM
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const int64_t n2 = n / 2;
+  const longlong2* p2 = reinterpret_cast<const longlong2*>(payback);
+  longlong2* a2 = reinterpret_cast<longlong2*>(acc);
+  for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n2; i0 += 2 * stride) {
+    const int64_t i1 = i0 + stride;
+    const longlong2 x0 = __ldcs(p2 + i0);
+    const longlong2 y0 = a2[i0];
+    longlong2 x1 = make_longlong2(0, 0), y1 = make_longlong2(0, 0);
+    if (i1 < n2) {
+      x1 = __ldcs(p2 + i1);
+      y1 = a2[i1];
+    }
+    // two's-complement wrap, like the int64 NCCL sum
+    a2[i0] = make_longlong2(static_cast<long long>(static_cast<unsigned long long>(y0.x) + static_cast<unsigned long long>(x0.x)),
+                            static_cast<long long>(static_cast<unsigned long long>(y0.y) + static_cast<unsigned long long>(x0.y)));
+    if (i1 < n2)
+      a2[i1] = make_longlong2(static_cast<long long>(static_cast<unsigned long long>(y1.x) + static_cast<unsigned long long>(x1.x)),
+                              static_cast<long long>(static_cast<unsigned long long>(y1.y) + static_cast<unsigned long long>(x1.y)));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (n & 1))
+    acc[n - 1] = static_cast<long long>(static_cast<unsigned long long>(acc[n - 1]) +
+                                        static_cast<unsigned long long>(payback[n - 1]));
+}
+
+}  // namespace
+}  // namespace ew
+
+extern "C" int ew_payback_accumulate(int64_t* acc, const int64_t* payback, int64_t n,
+                                     ew_stream_t stream) {
+  using namespace ew;
+  if (n < 0 || (n > 0 && (!acc || !payback)))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_payback_accumulate: bad arguments");
+  if ((reinterpret_cast<uintptr_t>(acc) | reinterpret_cast<uintptr_t>(payback)) & 15)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_payback_accumulate: buffers must be 16-byte aligned");
+  if (n == 0) return EW_OK;
+  const int grid = grid_for((n + 3) / 4);
+  payback_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(reinterpret_cast<long long*>(acc),
+                                                         reinterpret_cast<const long long*>(payback), n);
+  EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}

@@ -256,12 +256,15 @@ def fixed_point_bits(global_absmax: float, total_units: int) -> int:
 
 
 def weighted_fold(units, weights, frac_bits: int, acc: torch.Tensor, accumulate: bool = False,
-                  stream=None) -> torch.Tensor:
+                  stream=None, addend: Optional[torch.Tensor] = None) -> torch.Tensor:
+    """acc (+)= sum_u rint(w_u g_u 2^F) [+ addend], one pass (ew_weighted_fold_addend)."""
     ptrs, w, n = _units(units, weights)
     if acc.dtype != torch.int64 or acc.numel() < n:
         raise ValueError("acc must be int64 with one slot per element")
-    check(lib.ew_weighted_fold(ptrs, w, len(units), n, int(frac_bits), _ptr(acc),
-                               int(accumulate), _stream(stream)))
+    if addend is not None and (addend.dtype != torch.int64 or addend.numel() < n):
+        raise ValueError("addend must be int64 with one slot per element")
+    check(lib.ew_weighted_fold_addend(ptrs, w, len(units), n, int(frac_bits), _ptr(acc),
+                                      int(accumulate), _ptr(addend), _stream(stream)))
     return acc
 
 

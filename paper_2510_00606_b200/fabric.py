@@ -263,6 +263,39 @@ def plan_zero_migration(interleaved: bool, dp_degree: int, layer_bytes: Sequence
     return rows[:6 * n.value].reshape(-1, 6), tot
 
 
+BLOCKING, NON_BLOCKING = 0, 1
+
+
+@dataclass
+class MigrationSchedule:
+    """Reference MigrationSchedule (migration.hpp:29-39); transfers are
+    (what, start_s, end_s, bytes) with what in {"params", "payback_grad"}."""
+
+    mode: int
+    transfers: List[Tuple[str, float, float, int]]
+    shadow_microbatches: int
+    payback_bytes: int
+    stall_s: float
+    total_time_s: float
+
+
+def plan_layer_migration(move: Tuple[int, int, int], mode: int, *, param_bytes: int,
+                         grad_bytes: int, link_bw_bytes_per_s: float, microbatch_slot_s: float,
+                         num_microbatches: int, target_headroom_bytes: int,
+                         fixed_overhead_s: float = 0.0) -> MigrationSchedule:
+    """Reference plan_layer_migration (migration.cpp:9-61); move = (layer,
+    src_stage, dst_stage).  Raises InsufficientTargetMemory like the reference."""
+    ctx = N.MigrationContext(param_bytes, grad_bytes, link_bw_bytes_per_s, microbatch_slot_s,
+                             num_microbatches, target_headroom_bytes, fixed_overhead_s)
+    out = N.MigrationSchedule()
+    check(lib.ew_plan_layer_migration(int(move[0]), int(move[1]), int(move[2]), int(mode),
+                                      C.byref(ctx), C.byref(out)))
+    tr = [("payback_grad" if out.transfers[k].what else "params", out.transfers[k].start_s,
+           out.transfers[k].end_s, out.transfers[k].bytes) for k in range(out.n_transfers)]
+    return MigrationSchedule(out.mode, tr, out.shadow_microbatches, out.payback_bytes,
+                             out.stall_s, out.total_time_s)
+
+
 def weighted_grad_average(weights: Sequence[float], grads: np.ndarray) -> np.ndarray:
     """Reference dataflow.cpp:71-83 (fp64 left fold, host)."""
     g = np.ascontiguousarray(grads, dtype=np.float64)

@@ -259,6 +259,38 @@ def test_plan_zero_migration_matches_reference(reference):
         assert tot.tolist() == want_tot.tolist()
 
 
+def test_plan_layer_migration_matches_reference(reference):
+    """plan_layer_migration (migration.cpp:9-61), both modes, incl. the
+    micro-batch-boundary tie rule and InsufficientTargetMemory; doubles
+    compared bit for bit."""
+    from paper_2510_00606_b200._native import InsufficientTargetMemory, InvalidArgument
+    rng = random.Random(41)
+    for trial in range(2000):
+        slot = rng.choice([0.0, 1e-3, 2.5e-3, rng.uniform(1e-4, 1e-2)])
+        bw = rng.choice([1e9, 2.5e10, 7.0e11, rng.uniform(1e8, 1e12), 0.0])
+        pb = rng.choice([0, rng.randint(1, 1 << 34)])
+        if rng.random() < 0.2 and slot > 0 and bw > 0:
+            pb = int(bw * slot * rng.randint(1, 8))  # arrival exactly on a boundary
+        ctx = dict(param_bytes=pb, grad_bytes=rng.choice([0, rng.randint(1, 1 << 34)]),
+                   link_bw_bytes_per_s=bw, microbatch_slot_s=slot,
+                   num_microbatches=rng.randint(0, 64),
+                   target_headroom_bytes=rng.randint(0, 1 << 36),
+                   fixed_overhead_s=rng.choice([0.0, 0.012]))
+        move = (rng.randint(0, 40), rng.randint(0, 7), rng.randint(0, 7))
+        nb = rng.random() < 0.8
+        st, want = reference.plan_layer_migration(*move, nb, ctx)
+        if st:
+            exc = {13: InsufficientTargetMemory, 1: InvalidArgument}[st]
+            with pytest.raises(exc):
+                fabric.plan_layer_migration(move, int(nb), **ctx)
+            continue
+        got = fabric.plan_layer_migration(move, int(nb), **ctx)
+        assert got.mode == want["mode"] and got.shadow_microbatches == want["shadow_microbatches"]
+        assert got.payback_bytes == want["payback_bytes"], trial
+        assert [tuple(t) for t in got.transfers] == want["transfers"], trial
+        assert (got.stall_s, got.total_time_s) == (want["stall_s"], want["total_time_s"]), trial
+
+
 def _reassign_restated(old_slots, old_mbs, new_slots, new_mbs):
     """sim.cpp:694-715, restated: offsets of micro-batch 0 whose slot changes."""
     def slot_at(slots, mbs, off):
