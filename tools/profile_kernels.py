@@ -6,6 +6,8 @@ CUDA-event times so the same command can run without ncu first.
   (b) staged_copy_kernel, local 4 GiB aligned + 1 GiB misaligned
   (c) mask_kernel, config E busiest rank (224 x 4096^2)
   (d) fold_kernel, 1 Gi fp32 elements
+  §8(f)#1 adam_kernel, 7B rank shard (842 M params, 11.79 GB state)
+  §8(f)#2 payback_kernel, one 7B layer (202 M int64), local source
 """
 import json
 import sys
@@ -61,6 +63,23 @@ def main():
     g = torch.empty(1 << 30, dtype=torch.float32, device="cuda").normal_(0, 1e-3)
     acc = torch.empty(1 << 30, dtype=torch.int64, device="cuda")
     out["fold_ms"] = timed(lambda: dev.weighted_fold([g], [0.2], 60, acc))
+    del g, acc
+    torch.cuda.empty_cache()
+
+    n = 6_738_415_616 // 8
+    st = dev.AdamState(n)
+    grad = torch.empty(n, dtype=torch.float32, device="cuda").normal_(0, 1e-3)
+    h = dev.adam_hyper()
+    dev.adam_step(grad, st, h, 1)
+    out["adam_ms"] = timed(lambda: dev.adam_step(grad, st, h, 2))
+    del st, grad
+    torch.cuda.empty_cache()
+
+    from paper_2510_00606_b200.migration import payback_accumulate
+    a = torch.zeros(202_383_360, dtype=torch.int64, device="cuda")
+    b = torch.ones_like(a)
+    payback_accumulate(a, b)
+    out["payback_ms"] = timed(lambda: payback_accumulate(a, b))
     print(json.dumps(out))
 
 
