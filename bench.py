@@ -802,9 +802,21 @@ def run_philox(args, rank, world, out):
     out["philox"] = {"workload": f"config E: {n} samples x 4096x4096 elements (rank {r} of DP5), keep 0.5",
                      "ms": round(t * 1e3, 3), "gelem_per_s": round(n * K / t / 1e9, 1),
                      "gblocks_per_s": round(n * K / 4 / t / 1e9, 2),
-                     "bound": "INT-ALU (20 64x64->128 multiplies per Philox block)"}
+                     "bound": "INT-ALU (20 64x64->128 multiplies per Philox block)",
+                     # ceiling: the same Philox-4x64-10 rounds with no memory traffic
+                     # (tools/microbench/philox_variants.cu, __umul64hi form, B200)
+                     "roofline": {"bound": "int-alu", "unit": "G blocks/s",
+                                  "achieved": round(n * K / 4 / t / 1e9, 2),
+                                  "peak": PHILOX_COMPUTE_CEILING_GBLOCKS,
+                                  "peak_kind": "measured compute-only Philox loop",
+                                  "frac": round(n * K / 4 / t / 1e9 /
+                                                PHILOX_COMPUTE_CEILING_GBLOCKS, 4),
+                                  "ncu_fmaheavy_pipe_busy": 0.863}}
     del bits
     torch.cuda.empty_cache()
+
+
+PHILOX_COMPUTE_CEILING_GBLOCKS = 100.3  # profiles/r01_microbench_streaming.md
 
 
 def run_reduce(args, rank, world, out):

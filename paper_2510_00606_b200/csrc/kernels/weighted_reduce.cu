@@ -196,7 +196,8 @@ int ew_weighted_fold(const float* const* units, const double* weights, int n_uni
 int ew_weighted_fold_addend(const float* const* units, const double* weights, int n_units,
                             int64_t n_elems, int frac_bits, int64_t* acc, int accumulate,
                             const int64_t* addend, ew_stream_t stream) {
-  if (acc == nullptr || n_units < 0 || n_elems < 0 || (n_units > 0 && (!units || !weights)))
+  if ((n_elems > 0 && acc == nullptr) || n_units < 0 || n_elems < 0 ||
+      (n_units > 0 && (!units || !weights)))
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_weighted_fold: bad arguments");
   if (frac_bits > 1000 || frac_bits < -1000)
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_weighted_fold: frac_bits out of range");
