@@ -613,10 +613,19 @@ def run_replay(args, rank, world, out):
         b.record()
         torch.cuda.synchronize()
         step_t.append(a.elapsed_time(b) / 1e3)
-    t_step = max_over_ranks([min(step_t[1:])], world)[0]
+    rows_t = []
+    for step in range(5, 8):
+        a, b = ev(), ev()
+        a.record()
+        dev.adam_step(grad, own, hyper, step, rows=rows, block_bytes=args.block_bytes)
+        b.record()
+        torch.cuda.synchronize()
+        rows_t.append(a.elapsed_time(b) / 1e3)
+    t_step, t_rows = max_over_ranks([min(step_t[1:]), min(rows_t)], world)
     res = {"what": "AdamW step on a 7B ZeRO shard (ew_adam_step)", "params_per_rank": n,
            "state_bytes": own.nbytes, "owner_step_ms": round(t_step * 1e3, 3),
-           "owner_step_hbm_gbs": round(30 * n / t_step / 1e9, 1)}
+           "owner_step_hbm_gbs": round(30 * n / t_step / 1e9, 1),
+           "owner_step_with_fused_rows_ms": round(t_rows * 1e3, 3)}
     if world > 1:
         import torch.distributed as dist
         replica = dev.AdamState(n)
@@ -635,9 +644,8 @@ def run_replay(args, rank, world, out):
         dev.ipc_close(p0)
         rep = ReplayReplica(list(range(world)), rank, replica, grad, rows, args.block_bytes)
         times, vt, bad = [], [], 0
-        for step in range(5, 9):
-            dev.adam_step(grad, own, hyper, step)
-            dev.checksum(m, own.buf, rows)
+        for step in range(8, 12):
+            dev.adam_step(grad, own, hyper, step, rows=rows, block_bytes=args.block_bytes)
             torch.cuda.synchronize()
             barrier(world)
             a, b, c = ev(), ev(), ev()

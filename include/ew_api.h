@@ -384,6 +384,19 @@ int ew_adam_scalars(const ew_adam_hyper* hyper, int64_t step, float* out8);
 int ew_adam_step(const float* grad, float* master, float* exp_avg, float* exp_avg_sq,
                  uint16_t* param_bf16, int64_t n, const ew_adam_hyper* hyper, int64_t step,
                  ew_stream_t stream);
+/* Same step with kernel (a)'s checksum rows of the whole state image fused
+ * in: the four arrays lie inside [image_base, image_base + image_bytes)
+ * (bytes of the image the step does not write must be zero), rows
+ * (device u64 [ceil(image_bytes/block_bytes)][2]) are overwritten with the
+ * per-block (s0, s1) of the image after the step — equal to ew_checksum of
+ * the image as one segment at global offset 0, without re-reading it. */
+int ew_adam_step_rows(const float* grad, float* master, float* exp_avg, float* exp_avg_sq,
+                      uint16_t* param_bf16, int64_t n, const ew_adam_hyper* hyper, int64_t step,
+                      const void* image_base, int64_t image_bytes, int64_t block_bytes,
+                      uint64_t* rows, ew_stream_t stream);
+/* *bad_count (device u32, zeroed by the call) = rows where a != b. */
+int ew_rows_diff(const uint64_t* a, const uint64_t* b, int64_t n_rows, uint32_t* bad_count,
+                 ew_stream_t stream);
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -236,6 +236,8 @@ _sig("ew_plan_layer_migration", i32, i32, i32, i32, i32, P(MigrationContext), P(
 _sig("ew_payback_accumulate", i32, vp, vp, i64, vp)
 _sig("ew_adam_scalars", i32, P(AdamHyper), i64, P(C.c_float))
 _sig("ew_adam_step", i32, vp, vp, vp, vp, vp, i64, P(AdamHyper), i64, vp)
+_sig("ew_adam_step_rows", i32, vp, vp, vp, vp, vp, i64, P(AdamHyper), i64, vp, i64, i64, vp, vp)
+_sig("ew_rows_diff", i32, vp, vp, i64, vp, vp)
 
 def int_array(values) -> C.Array:
     values = list(values)

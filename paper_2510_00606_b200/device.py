@@ -463,19 +463,26 @@ class AdamState:
     """One ZeRO shard's AdamW state in HBM, the layout ew_adam_step updates:
     fp32 master weights, fp32 exp_avg, fp32 exp_avg_sq and the bf16
     parameter copy (14 B/param, the mixed-precision state of SURVEY §8(d)),
-    structure of arrays in ONE allocation with 256-byte aligned sections and
-    zeroed padding, so the whole state is a single byte image that kernel (a)
-    snapshots and checksums and kernel (b) moves."""
+    structure of arrays in ONE allocation with zeroed padding, so the whole
+    state is a single byte image that kernel (a) snapshots and checksums and
+    kernel (b) moves.  Sections start on 1 MiB boundaries (the largest
+    checksum block), which lets ew_adam_step_rows give each CTA exactly one
+    block per section (≤ 3 MiB of padding per shard)."""
+
+    SECTION_ALIGN = 1 << 20
 
     def __init__(self, n: int, device=None, buf: Optional[torch.Tensor] = None):
-        a = lambda b: (int(b) + 255) // 256 * 256
+        al = self.SECTION_ALIGN
+        a = lambda b: (int(b) + al - 1) // al * al
         self.n = int(n)
         sec = a(4 * self.n)
-        self.nbytes = 3 * sec + a(2 * self.n)
+        self.nbytes = 3 * sec + (int(2 * self.n) + 255) // 256 * 256
         if buf is None:
             buf = torch.zeros(self.nbytes, dtype=torch.uint8, device=device or "cuda")
         if buf.numel() < self.nbytes or buf.data_ptr() % 256:
             raise ValueError("AdamState buffer too small or not 256-byte aligned")
+        # the image's block grid is relative to buf, so buf's own alignment
+        # does not matter for the rows; only section offsets do
         self.buf = buf
         f32 = lambda k: buf[k * sec:k * sec + 4 * self.n].view(torch.float32)
         self.master, self.exp_avg, self.exp_avg_sq = f32(0), f32(1), f32(2)
@@ -499,15 +506,33 @@ def adam_scalars(hyper: N.AdamHyper, step: int) -> np.ndarray:
     return np.frombuffer(out, dtype=np.float32).copy()
 
 
-def adam_step(grad, state: AdamState, hyper: N.AdamHyper, step: int, stream=None) -> None:
+def adam_step(grad, state: AdamState, hyper: N.AdamHyper, step: int, stream=None,
+              rows: Optional[torch.Tensor] = None,
+              block_bytes: int = DEFAULT_BLOCK_BYTES) -> None:
     """ew_adam_step over the whole shard.  `grad`: fp32 tensor of state.n
-    elements, or a raw device pointer (an IPC-mapped peer gradient shard)."""
+    elements, or a raw device pointer (an IPC-mapped peer gradient shard).
+    With `rows` (int64 [2 * rows]), the checksum rows of the state image after
+    the step are produced in the same pass (ew_adam_step_rows); they equal
+    checksum(ShardMap(state.segments(), block_bytes), state.buf)."""
     if isinstance(grad, torch.Tensor):
         if grad.dtype != torch.float32 or grad.numel() < state.n:
             raise ValueError("grad must be fp32 with state.n elements")
         g = _ptr(grad)
     else:
         g = C.c_void_p(int(grad))
-    check(lib.ew_adam_step(g, _ptr(state.master), _ptr(state.exp_avg), _ptr(state.exp_avg_sq),
-                           _ptr(state.param), state.n, C.byref(hyper), int(step),
-                           _stream(stream)))
+    args = (g, _ptr(state.master), _ptr(state.exp_avg), _ptr(state.exp_avg_sq),
+            _ptr(state.param), state.n, C.byref(hyper), int(step))
+    if rows is None:
+        check(lib.ew_adam_step(*args, _stream(stream)))
+        return
+    n_rows = (state.nbytes + block_bytes - 1) // block_bytes
+    if rows.dtype != torch.int64 or rows.numel() < 2 * n_rows:
+        raise ValueError("rows must be int64 with 2 slots per block of the state image")
+    check(lib.ew_adam_step_rows(*args, _ptr(state.buf), state.nbytes, block_bytes, _ptr(rows),
+                                _stream(stream)))
+
+
+def rows_diff(a: torch.Tensor, b: torch.Tensor, n_rows: int, bad_count: torch.Tensor,
+              stream=None) -> None:
+    """bad_count (device int32[1]) <- number of rows where a and b differ."""
+    check(lib.ew_rows_diff(_ptr(a), _ptr(b), int(n_rows), _ptr(bad_count), _stream(stream)))

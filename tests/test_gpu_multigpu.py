@@ -134,12 +134,14 @@ def _worker(rank, world, port, result_dir):
         ok = True
         for step in range(1, 4):
             grad.normal_(0, 1e-3, generator=gen)
-            dev.adam_step(grad, own, hyper, step)
-            dev.checksum(own_map, own.buf, own_rows)
+            dev.adam_step(grad, own, hyper, step, rows=own_rows)  # rows fused
             torch.cuda.synchronize()
             dist.barrier()   # owner's grad + rows published
             rep.replay(hyper, step)
             rep.verify()
+            torch.cuda.synchronize()
+            ok = ok and int(rep.bad.item()) == 0
+            rep.verify_by_reread()
             torch.cuda.synchronize()
             ok = ok and int(rep.bad.item()) == 0
             dist.barrier()   # holder done reading before the next step's grad

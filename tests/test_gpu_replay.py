@@ -70,6 +70,33 @@ def test_replay_reproduces_state_and_rows():
     assert int(bad.item()) == 1
 
 
+@pytest.mark.parametrize("n", [1, 3, 5, 4099, (1 << 20) + 3, 3 * (1 << 20) + 1])
+@pytest.mark.parametrize("block", [4096, 65536])
+def test_fused_rows_equal_checksum_of_image(n, block):
+    """ew_adam_step_rows' rows == kernel (a)'s rows of the state image
+    (bit-exact), incl. partial words of ragged tails and rows straddled by
+    warps; and rows_diff finds a planted mismatch."""
+    rng = np.random.default_rng(n)
+    st = dev.AdamState(n)
+    st.master.copy_(torch.from_numpy(rng.normal(0, 0.02, n).astype(np.float32)))
+    m = dev.ShardMap(st.segments(), block)
+    fused = m.new_row_sums()
+    for step in (1, 2):
+        g = torch.from_numpy(_grads(rng, n, step)).cuda()
+        dev.adam_step(g, st, dev.adam_hyper(), step, rows=fused, block_bytes=block)
+    ref = m.new_row_sums()
+    dev.checksum(m, st.buf, ref)
+    torch.cuda.synchronize()
+    assert torch.equal(fused[:2 * m.num_rows], ref[:2 * m.num_rows])
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dev.rows_diff(fused, ref, m.num_rows, bad)
+    fused[2 * (m.num_rows - 1) + 1] += 1
+    bad2 = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dev.rows_diff(fused, ref, m.num_rows, bad2)
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0 and int(bad2.item()) == 1
+
+
 def test_adam_step_rejects_misaligned():
     st = dev.AdamState(64)
     g = torch.zeros(65, dtype=torch.float32, device="cuda")
