@@ -263,6 +263,21 @@ int ew_copy_program_stats(const ew_copy_program* prog, int64_t* n_copies, int64_
  * n_ctas / remote_ctas == 0 pick defaults (all SMs; CTAs split by bytes). */
 int ew_copy_program_launch(const ew_copy_program* prog, int n_ctas, int remote_ctas,
                            ew_stream_t stream);
+/* Verification on arrival.  A verified program also checksums (kernel (a)'s
+ * spec) every byte it lands in this GPU's NEW buffer, labelled with the
+ * global position that byte's destination offset has in new_map (NEW's
+ * segment map on exec_rank), and adds the sums into block_sums (device
+ * u64 [n_blocks][2], caller-zeroed; n_blocks from ew_copy_program_num_blocks
+ * covers global blocks up to NEW's last byte).  In-place retained bytes are
+ * read and checksummed but not rewritten.  The sum of every NEW rank's
+ * block_sums equals the block sums of the source state when — and only when
+ * — every byte landed where the target layout says, with no re-read of NEW. */
+int ew_copy_program_create_verified(const ew_copy_desc* descs, int64_t n,
+                                    void* const* buf_table, int table_ranks, int exec_rank,
+                                    const ew_shardmap* new_map, ew_copy_program** out);
+int ew_copy_program_launch_verified(const ew_copy_program* prog, int n_ctas, int remote_ctas,
+                                    uint64_t* block_sums, ew_stream_t stream);
+int ew_copy_program_num_blocks(const ew_copy_program* prog, int64_t* n_blocks);
 
 /* ------------------------------------------------------------------------
  * (c) Philox-4x64-10 dropout masks keyed by global sample id

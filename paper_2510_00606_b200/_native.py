@@ -203,6 +203,9 @@ _sig("ew_copy_program_create_raw", i32, P(vp), P(vp), P(i64), P(i32), i64, P(vp)
 _sig("ew_copy_program_free", None, vp)
 _sig("ew_copy_program_stats", i32, vp, P(i64), P(i64), P(i64))
 _sig("ew_copy_program_launch", i32, vp, i32, i32, vp)
+_sig("ew_copy_program_create_verified", i32, P(CopyDesc), i64, vp, i32, i32, vp, P(vp))
+_sig("ew_copy_program_launch_verified", i32, vp, i32, i32, vp, vp)
+_sig("ew_copy_program_num_blocks", i32, vp, P(i64))
 
 _sig("ew_philox_dropout_mask", i32, u64, i64, i64, u32, u32, i64, f64, vp, vp)
 _sig("ew_philox_uniforms", i32, u64, i64, i64, u32, u32, i64, vp, vp)

@@ -14,14 +14,20 @@
 //     16-byte-aligned source window of each piece, completing on a per-stage
 //     mbarrier — the Tensor Memory Accelerator keeps ~kStages x 16 KiB in
 //     flight per CTA with no register traffic;
-//   consumers (4 warps): read the stage, realign it to the destination when
+//   consumers (8 warps): read the stage, realign it to the destination when
 //     source and destination are not congruent mod 16 (byte-granular plans,
-//     SURVEY fact 9), write 16-byte vectors, and byte-store the partial
-//     vectors at copy ends so adjacent copies from other GPUs never race on a
-//     vector; then release the stage on its "empty" mbarrier.
+//     SURVEY fact 9), write 16-byte vectors (or one bulk shared->global
+//     store when congruent), and byte-store the partial vectors at copy ends
+//     so adjacent copies from other GPUs never race on a vector; in a
+//     verified program they also checksum what lands (kernel (a)'s spec,
+//     labelled by NEW's segment map) while the bulk store drains; then
+//     release the stage on its "empty" mbarrier.
+// The producer resolves each piece (binary search over the items) once and
+// passes the descriptor to the consumers in shared memory with the stage.
 // Pieces are <= 16 KiB and cut at 16 KiB-aligned destination addresses, so
 // no two pieces share a destination vector.
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "ew_device.cuh"
@@ -29,7 +35,7 @@
 namespace ew {
 namespace {
 
-constexpr int kConsumerWarps = 4;
+constexpr int kConsumerWarps = 8;
 constexpr int kThreads = 32 * (kConsumerWarps + 1);
 constexpr int kStages = 6;
 constexpr int kPiece = 16 * 1024;          // destination bytes per piece
@@ -43,6 +49,8 @@ struct CopyItem {
   uint8_t* dst;
   int64_t bytes;
   int64_t piece_base;  // first piece id of this item within its class
+  int64_t glob;        // global position of dst[0] (verified programs), else -1
+  int64_t no_store;    // 1: checksum only (in-place retained bytes), no write
 };
 
 __host__ __device__ __forceinline__ int64_t pieces_of(const uint8_t* dst, int64_t bytes) {
@@ -65,6 +73,8 @@ struct Piece {
   const uint8_t* src;  // first source byte
   uint8_t* dst;        // first destination byte
   int32_t bytes;
+  bool no_store;
+  int64_t glob;        // global position of dst[0], or -1
 };
 
 __device__ __forceinline__ Piece piece_at(const CopyItem* list, int64_t n_items, int64_t p) {
@@ -73,7 +83,86 @@ __device__ __forceinline__ Piece piece_at(const CopyItem* list, int64_t n_items,
   const uint64_t cut = (d / kPiece + static_cast<uint64_t>(p - it.piece_base)) * kPiece;
   const uint64_t lo = max(d, cut);
   const uint64_t hi = min(d + static_cast<uint64_t>(it.bytes), cut + kPiece);
-  return Piece{it.src + (lo - d), it.dst + (lo - d), static_cast<int32_t>(hi - lo)};
+  return Piece{it.src + (lo - d), it.dst + (lo - d), static_cast<int32_t>(hi - lo),
+               it.no_store != 0,
+               it.glob >= 0 ? it.glob + static_cast<int64_t>(lo - d) : int64_t{-1}};
+}
+
+// Verification on arrival: kernel (a)'s checksum (s0 = sum w, s1 = sum (i+1) w
+// over global u64 words) of the bytes a piece lands, labelled with the
+// global position of their destination, added to global block sums.  Warp w
+// takes a contiguous quarter of the piece's words (<= 513 words, so at most
+// two checksum blocks of >= 4 KiB), lanes stride by one word (conflict-free
+// 8-byte shared loads), and lane 0 adds the warp's sums with <= 4 atomics.
+// Warp sum mod 2^64 with the single-instruction 32-bit reduction (REDUX):
+// four 16-bit limbs, each limb's 32-lane sum exact in 21 bits.
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t x) {
+  const unsigned m = 0xffffffffu;
+  const uint64_t l0 = __reduce_add_sync(m, static_cast<unsigned>(x & 0xffff));
+  const uint64_t l1 = __reduce_add_sync(m, static_cast<unsigned>((x >> 16) & 0xffff));
+  const uint64_t l2 = __reduce_add_sync(m, static_cast<unsigned>((x >> 32) & 0xffff));
+  const uint64_t l3 = __reduce_add_sync(m, static_cast<unsigned>(x >> 48));
+  return l0 + (l1 << 16) + (l2 << 32) + (l3 << 48);
+}
+
+__device__ __forceinline__ uint64_t lds64(const uint8_t* p) {
+  return *reinterpret_cast<const uint64_t*>(p);
+}
+
+__device__ void checksum_piece(const uint8_t* stage, const Piece& pc, int warp_c, int lane,
+                               unsigned long long* block_sums, int word_shift) {
+  const int r = static_cast<int>(reinterpret_cast<uintptr_t>(pc.src) & 15);
+  const int64_t g0 = pc.glob;
+  const int64_t W0 = g0 >> 3, W1 = (g0 + pc.bytes - 1) >> 3;
+  const int64_t nw = W1 - W0 + 1;
+  const int64_t q0 = W0 + nw * warp_c / kConsumerWarps;
+  const int64_t q1 = W0 + nw * (warp_c + 1) / kConsumerWarps;
+  if (q0 >= q1) return;  // uniform per warp
+  const int64_t blkA = q0 >> word_shift;
+  uint64_t a0 = 0, b0 = 0, a1 = 0, b1 = 0;
+#pragma unroll 4
+  for (int64_t w = q0 + lane; w < q1; w += 32) {
+    // the word's 8 bytes sit at stage[r + k0 ..]; bytes outside the piece
+    // (first/last word) are masked off — their 8-byte-aligned shared loads
+    // may touch neighbouring shared memory, which is harmless
+    const int k0 = static_cast<int>(8 * w - g0);  // -7 .. bytes-1
+    const int p = r + k0;
+    const int sh = (p & 7) * 8;
+    const uint8_t* q = stage + (p & ~7);
+    const uint64_t lo = lds64(q);
+    uint64_t v = sh ? (lo >> sh) | (lds64(q + 8) << (64 - sh)) : lo;
+    const int lo_t = max(0, -k0), hi_t = min(8, pc.bytes - k0);
+    if (lo_t > 0 || hi_t < 8) {
+      const uint64_t keep = (hi_t >= 8 ? ~uint64_t{0} : ((uint64_t{1} << (8 * hi_t)) - 1)) &
+                            ~((uint64_t{1} << (8 * lo_t)) - 1);
+      v &= keep;
+    }
+    const uint64_t wi = static_cast<uint64_t>(w) + 1;
+    if ((w >> word_shift) == blkA) {
+      a0 += v;
+      b0 += wi * v;
+    } else {
+      a1 += v;
+      b1 += wi * v;
+    }
+  }
+  const bool two = __any_sync(0xffffffffu, (a1 | b1) != 0);  // block boundary inside
+  a0 = warp_sum64(a0);
+  b0 = warp_sum64(b0);
+  if (two) {
+    a1 = warp_sum64(a1);
+    b1 = warp_sum64(b1);
+  }
+  if (lane == 0) {
+    if (a0 | b0) {
+      atomicAdd(block_sums + 2 * blkA, static_cast<unsigned long long>(a0));
+      atomicAdd(block_sums + 2 * blkA + 1, static_cast<unsigned long long>(b0));
+    }
+    if (a1 | b1) {
+      atomicAdd(block_sums + 2 * (blkA + 1), static_cast<unsigned long long>(a1));
+      atomicAdd(block_sums + 2 * (blkA + 1) + 1, static_cast<unsigned long long>(b1));
+    }
+  }
 }
 
 __device__ __forceinline__ uint32_t pick(const uint32_t (&x)[8], int i) {
@@ -127,10 +216,16 @@ __global__ void __launch_bounds__(kThreads) staged_copy_kernel(const CopyItem* _
                                                                int64_t remote_pieces,
                                                                int64_t n_local,
                                                                int64_t local_pieces,
-                                                               int remote_ctas) {
+                                                               int remote_ctas,
+                                                               unsigned long long* block_sums,
+                                                               int word_shift) {
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ __align__(8) uint64_t empty[kStages];
+  // the producer resolves each piece once (binary search over the items)
+  // and hands it to the consumers with the stage: the mbarrier's
+  // arrive (release) / wait (acquire) orders these plain shared stores
+  __shared__ Piece staged[kStages];
 
   const bool remote = static_cast<int>(blockIdx.x) < remote_ctas;
   const CopyItem* list = remote ? items : items + n_remote;
@@ -161,6 +256,7 @@ __global__ void __launch_bounds__(kThreads) staged_copy_kernel(const CopyItem* _
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
         const Piece pc = piece_at(list, n_items, first + k * step);
+        staged[s] = pc;
         const uintptr_t s0 = reinterpret_cast<uintptr_t>(pc.src) & ~uintptr_t{15};
         const uintptr_t s1 = (reinterpret_cast<uintptr_t>(pc.src) + pc.bytes + 15) & ~uintptr_t{15};
         const uint32_t n = static_cast<uint32_t>(s1 - s0);
@@ -175,11 +271,14 @@ __global__ void __launch_bounds__(kThreads) staged_copy_kernel(const CopyItem* _
   for (int64_t k = 0; k < mine; ++k) {
     const int s = static_cast<int>(k % kStages);
     mbar_wait(&full[s], static_cast<uint32_t>((k / kStages) & 1));
-    const Piece pc = piece_at(list, n_items, first + k * step);
+    const Piece pc = staged[s];
     const uint8_t* stage = ring + s * kStageBytes;
     const bool aligned =
         ((reinterpret_cast<uintptr_t>(pc.src) | reinterpret_cast<uintptr_t>(pc.dst)) & 15) == 0;
-    if (aligned && pc.bytes >= 16) {
+    const bool bulk = !pc.no_store && aligned && pc.bytes >= 16;
+    if (pc.no_store) {
+      // retained in place: only checksummed below, nothing to move
+    } else if (bulk) {
       // 16-byte-congruent piece: one bulk shared->global store of the body
       // (no register traffic); the <16-byte tail by byte stores
       const int body = pc.bytes & ~15;
@@ -188,10 +287,13 @@ __global__ void __launch_bounds__(kThreads) staged_copy_kernel(const CopyItem* _
         bulk_commit();
       }
       if (ctid >= 32 && ctid < 32 + (pc.bytes - body)) pc.dst[body + ctid - 32] = stage[body + ctid - 32];
-      if (ctid == 0) bulk_wait_read<0>();  // the stage may be reused once read
     } else {
       write_piece(stage, pc, ctid);
     }
+    // verification on arrival, overlapped with the bulk store's smem read
+    if (block_sums != nullptr && pc.glob >= 0)
+      checksum_piece(stage, pc, warp - 1, lane, block_sums, word_shift);
+    if (bulk && ctid == 0) bulk_wait_read<0>();  // the stage may be reused once read
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -208,6 +310,8 @@ struct ew_copy_program {
   int64_t n_remote = 0, n_local = 0, remote_pieces = 0, local_pieces = 0;
   int64_t remote_bytes = 0, local_bytes = 0, copies = 0;
   CopyItem* d_items = nullptr;
+  int word_shift = -1;  // verified programs: log2(block bytes / 8)
+  int64_t n_blocks = 0;  // global blocks covered by the block sums
 };
 
 namespace {
@@ -257,8 +361,9 @@ int build_program(std::vector<CopyItem> remote, std::vector<CopyItem> local,
 
 extern "C" {
 
-int ew_copy_program_create(const ew_copy_desc* descs, int64_t n, void* const* buf_table,
-                           int table_ranks, int exec_rank, ew_copy_program** out) {
+static int create_program(const ew_copy_desc* descs, int64_t n, void* const* buf_table,
+                          int table_ranks, int exec_rank, const ew_shardmap* new_map,
+                          ew_copy_program** out) {
   if (out == nullptr || (n > 0 && (descs == nullptr || buf_table == nullptr)) || table_ranks <= 0)
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_copy_program_create: bad arguments");
   *out = nullptr;
@@ -275,6 +380,7 @@ int ew_copy_program_create(const ew_copy_desc* descs, int64_t n, void* const* bu
   std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t b) {
     return peer_of(descs[a]) < peer_of(descs[b]);
   });
+  constexpr int kNewRole = 2;  // b200::BufRole::New
   for (const int64_t i : order) {
     const ew_copy_desc& c = descs[i];
     if (c.bytes < 0 || c.src_role < 0 || c.src_role > 2 || c.dst_role < 0 || c.dst_role > 2 ||
@@ -290,12 +396,58 @@ int ew_copy_program_create(const ew_copy_desc* descs, int64_t n, void* const* bu
       return set_error(EW_ERR_INVALID_ARGUMENT,
                        "copy descriptor " + std::to_string(i) + " refers to an unmapped buffer");
     // in-place reshards alias OLD and NEW: retained bytes already in place
-    if (src + c.src_off == dst + c.dst_off) continue;
+    const bool in_place = src + c.src_off == dst + c.dst_off;
     // remote = the copy crosses NVLink (the other end is not exec_rank)
     const bool crosses = c.dst_rank != exec_rank || c.src_rank != exec_rank;
-    (crosses ? remote : local).push_back({src + c.src_off, dst + c.dst_off, c.bytes, 0});
+    const bool tracked = new_map != nullptr && c.dst_role == kNewRole && c.dst_rank == exec_rank;
+    if (!tracked) {
+      if (!in_place)
+        (crosses ? remote : local).push_back({src + c.src_off, dst + c.dst_off, c.bytes, 0, -1, 0});
+      continue;
+    }
+    // label the landed bytes with the global position their destination
+    // offset has in NEW's segment map (independent of the plan's interval),
+    // splitting at segment boundaries
+    int64_t off = c.dst_off, left = c.bytes, soff = c.src_off;
+    const auto& segs = new_map->h_segs;
+    while (left > 0) {
+      auto it = std::upper_bound(segs.begin(), segs.end(), off,
+                                 [](int64_t v, const DevSeg& sg) { return v < sg.local_off; });
+      if (it == segs.begin())
+        return set_error(EW_ERR_COVERAGE_MISMATCH, "copy lands outside NEW's segment map");
+      const DevSeg& sg = *(it - 1);
+      if (off >= sg.local_off + sg.length)
+        return set_error(EW_ERR_COVERAGE_MISMATCH, "copy lands outside NEW's segment map");
+      const int64_t take = std::min(left, sg.local_off + sg.length - off);
+      const int64_t glob = sg.global_lo + (off - sg.local_off);
+      (crosses ? remote : local)
+          .push_back({src + soff, dst + off, take, 0, glob, in_place ? 1 : 0});
+      off += take;
+      soff += take;
+      left -= take;
+    }
   }
-  return build_program(std::move(remote), std::move(local), out);
+  const int rc = build_program(std::move(remote), std::move(local), out);
+  if (rc == EW_OK && new_map != nullptr) {
+    (*out)->word_shift = new_map->block_shift - 3;
+    const auto& segs = new_map->h_segs;
+    (*out)->n_blocks = segs.empty() ? 0
+        : ((segs.back().global_lo + segs.back().length - 1) >> new_map->block_shift) + 1;
+  }
+  return rc;
+}
+
+int ew_copy_program_create(const ew_copy_desc* descs, int64_t n, void* const* buf_table,
+                           int table_ranks, int exec_rank, ew_copy_program** out) {
+  return create_program(descs, n, buf_table, table_ranks, exec_rank, nullptr, out);
+}
+
+int ew_copy_program_create_verified(const ew_copy_desc* descs, int64_t n,
+                                    void* const* buf_table, int table_ranks, int exec_rank,
+                                    const ew_shardmap* new_map, ew_copy_program** out) {
+  if (new_map == nullptr)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_copy_program_create_verified: NULL map");
+  return create_program(descs, n, buf_table, table_ranks, exec_rank, new_map, out);
 }
 
 int ew_copy_program_create_raw(const void* const* srcs, void* const* dsts, const int64_t* bytes,
@@ -307,7 +459,8 @@ int ew_copy_program_create_raw(const void* const* srcs, void* const* dsts, const
   for (int64_t i = 0; i < n; ++i) {
     if (bytes[i] < 0) return set_error(EW_ERR_INVALID_ARGUMENT, "negative copy size");
     if (bytes[i] == 0) continue;
-    CopyItem it{static_cast<const uint8_t*>(srcs[i]), static_cast<uint8_t*>(dsts[i]), bytes[i], 0};
+    CopyItem it{static_cast<const uint8_t*>(srcs[i]), static_cast<uint8_t*>(dsts[i]), bytes[i], 0,
+                -1, 0};
     (is_remote[i] ? remote : local).push_back(it);
   }
   return build_program(std::move(remote), std::move(local), out);
@@ -328,19 +481,45 @@ int ew_copy_program_stats(const ew_copy_program* prog, int64_t* n_copies, int64_
   return EW_OK;
 }
 
-int ew_copy_program_launch(const ew_copy_program* prog, int n_ctas, int remote_ctas,
-                           ew_stream_t stream) {
+static int launch_program(const ew_copy_program* prog, int n_ctas, int remote_ctas,
+                          uint64_t* block_sums, ew_stream_t stream) {
   if (prog == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL program");
   if (prog->remote_pieces + prog->local_pieces == 0) return EW_OK;
   const int sms = num_sms();
   if (n_ctas <= 0) n_ctas = 2 * sms;  // two 96 KiB rings per SM
   if (prog->remote_pieces == 0) remote_ctas = 0;
   else if (prog->local_pieces == 0) remote_ctas = n_ctas;
-  else if (remote_ctas <= 0 || remote_ctas >= n_ctas) remote_ctas = std::max(1, n_ctas / 4);
+  else if (remote_ctas <= 0 || remote_ctas >= n_ctas)
+    // a verifying consumer spends longer per piece, so the latency-bound
+    // NVLink class gets a third of the CTAs instead of a quarter (N=4 sweep,
+    // tools/verify_dbg.sh: 11.6 ms verified vs 11.1 ms plain); EW_REMOTE_CTAS
+    // overrides for sweeps
+    remote_ctas = getenv("EW_REMOTE_CTAS")
+                      ? std::min(n_ctas - 1, atoi(getenv("EW_REMOTE_CTAS")))
+                      : std::max(1, block_sums ? n_ctas / 3 : n_ctas / 4);
   staged_copy_kernel<<<n_ctas, kThreads, kSmem, (cudaStream_t)stream>>>(
       prog->d_items, prog->n_remote, prog->remote_pieces, prog->n_local, prog->local_pieces,
-      remote_ctas);
+      remote_ctas, reinterpret_cast<unsigned long long*>(block_sums), prog->word_shift);
   EW_CUDA_TRY(cudaGetLastError());
+  return EW_OK;
+}
+
+int ew_copy_program_launch(const ew_copy_program* prog, int n_ctas, int remote_ctas,
+                           ew_stream_t stream) {
+  return launch_program(prog, n_ctas, remote_ctas, nullptr, stream);
+}
+
+int ew_copy_program_launch_verified(const ew_copy_program* prog, int n_ctas, int remote_ctas,
+                                    uint64_t* block_sums, ew_stream_t stream) {
+  if (prog == nullptr || prog->word_shift < 0 || block_sums == nullptr)
+    return set_error(EW_ERR_INVALID_ARGUMENT,
+                     "ew_copy_program_launch_verified: needs a verified program and block sums");
+  return launch_program(prog, n_ctas, remote_ctas, block_sums, stream);
+}
+
+int ew_copy_program_num_blocks(const ew_copy_program* prog, int64_t* n_blocks) {
+  if (prog == nullptr || n_blocks == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+  *n_blocks = prog->n_blocks;
   return EW_OK;
 }
 

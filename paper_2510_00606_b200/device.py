@@ -138,15 +138,25 @@ class CopyProgram:
 
     @classmethod
     def from_descs(cls, descs: np.ndarray, buf_table: Dict[Tuple[int, int], int],
-                   table_ranks: int, exec_rank: int) -> "CopyProgram":
+                   table_ranks: int, exec_rank: int,
+                   verify_map: Optional["ShardMap"] = None) -> "CopyProgram":
+        """verify_map: NEW's segment map on exec_rank -> a verified program
+        (ew_copy_program_create_verified: checksums what lands, see launch)."""
         d = np.ascontiguousarray(descs, dtype=COPY_DTYPE)
         table = (C.c_void_p * (3 * table_ranks))()
         for (role, rank), ptr in buf_table.items():
             table[role * table_ranks + rank] = ptr
         h = C.c_void_p()
-        check(lib.ew_copy_program_create(d.ctypes.data_as(C.POINTER(N.CopyDesc)), len(d), table,
-                                         table_ranks, exec_rank, C.byref(h)))
-        return cls(h)
+        dp = d.ctypes.data_as(C.POINTER(N.CopyDesc))
+        if verify_map is None:
+            check(lib.ew_copy_program_create(dp, len(d), table, table_ranks, exec_rank,
+                                             C.byref(h)))
+        else:
+            check(lib.ew_copy_program_create_verified(dp, len(d), table, table_ranks, exec_rank,
+                                                      verify_map.handle, C.byref(h)))
+        prog = cls(h)
+        prog._verify_map = verify_map  # keep the map alive with the program
+        return prog
 
     @classmethod
     def from_pointers(cls, srcs: Sequence[int], dsts: Sequence[int], nbytes: Sequence[int],
@@ -170,8 +180,20 @@ class CopyProgram:
         check(lib.ew_copy_program_stats(self._h, C.byref(n), C.byref(r), C.byref(l)))
         return n.value, r.value, l.value
 
-    def launch(self, n_ctas: int = 0, remote_ctas: int = 0, stream=None) -> None:
-        check(lib.ew_copy_program_launch(self._h, n_ctas, remote_ctas, _stream(stream)))
+    def launch(self, n_ctas: int = 0, remote_ctas: int = 0, stream=None,
+               block_sums: Optional[torch.Tensor] = None) -> None:
+        """block_sums (int64 [2 * num_blocks()], zeroed by the caller): the
+        landed bytes' checksums are added there (verified programs only)."""
+        if block_sums is None:
+            check(lib.ew_copy_program_launch(self._h, n_ctas, remote_ctas, _stream(stream)))
+        else:
+            check(lib.ew_copy_program_launch_verified(self._h, n_ctas, remote_ctas,
+                                                      _ptr(block_sums), _stream(stream)))
+
+    def num_blocks(self) -> int:
+        n = C.c_int64()
+        check(lib.ew_copy_program_num_blocks(self._h, C.byref(n)))
+        return n.value
 
 
 def ipc_handle(t: torch.Tensor) -> Tuple[bytes, int]:

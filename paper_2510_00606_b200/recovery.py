@@ -10,8 +10,9 @@ ScaleOut) each surviving rank runs, in the reference's order:
   dataflow      reshard_microbatches (dataflow.cpp:52-69) -> new weights
   remap         integrity_check + overlap_matrix on the interleaved layouts,
                 lowering to this GPU's copy program, CUDA-IPC peer mapping,
-                one copy launch (kernel (b)), verification of every moved
-                byte by checksum conservation (no source re-read)
+                one copy launch (kernel (b)) that checksums every byte it
+                lands, verification by checksum conservation against the
+                snapshot rows (no re-read of source or target)
 
 and reports an MttrEvent with the reference's fields (sim.hpp:31-45) filled
 with measured seconds (`mttr_csv` row format of sim.cpp:1119-1132).
@@ -206,9 +207,11 @@ class DpGroup:
         self.links = {(a, b) for i, a in enumerate(self.members) for b in self.members[i + 1:]}
 
     def recover(self, departed: Sequence[int], bufs, push: bool = False, step: int = 0,
-                kind: int = FAIL_STOP, group=None) -> MttrEvent:
+                kind: int = FAIL_STOP, group=None, source_sums=None) -> MttrEvent:
         """Run the DP recovery for `departed` on this (surviving) rank.
-        `bufs` are this rank's RankBuffers for the change (old/replica filled)."""
+        `bufs` are this rank's RankBuffers for the change (old/replica filled);
+        `source_sums`: global block sums of the state before the change
+        (from the per-step snapshot rows), else recomputed from OLD/replica."""
         ev = MttrEvent(step=step, kind=KIND_NAMES.get(kind, "fail_stop"))
         t0 = time.perf_counter()
         # comm repair: edit plan, then the NCCL communicator shrink
@@ -230,21 +233,31 @@ class DpGroup:
         t2 = time.perf_counter()
         ev.other_s = t2 - t1
 
-        # remap: plan -> program -> peer map -> copy -> verify
+        # remap: plan -> program -> peer map -> copy -> verify.  In pull mode
+        # the copy verifies on arrival (it checksums what it lands), so the
+        # check is one all-reduce of block sums against the source's sums
+        # (the per-step snapshot rows; recomputed here when not supplied).
         rp = ReshardPlan.build(self.layer_bytes, self.members, survivors)
         ex = ReshardExecutor(rp, self.rank, push=push)
+        before = source_sums if source_sums is not None else \
+            self.source_block_sums(rp, bufs, group)
         t3 = time.perf_counter()
-        ex.bind(bufs, group=group)
+        ex.bind(bufs, group=group, verify=not push, block_bytes=self.block_bytes)
         t4 = time.perf_counter()
+        after = torch.zeros_like(before)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         dist.barrier(group=group)
         s.record()
-        ex.launch()
+        ex.launch(block_sums=after)
         e.record()
         torch.cuda.synchronize()
         dist.barrier(group=group)
         t5 = time.perf_counter()
-        ev.verified = self.verify_conservation(rp, bufs, group)
+        if push:
+            ev.verified = self.verify_conservation(rp, bufs, group)
+        else:
+            dist.all_reduce(after, group=group)
+            ev.verified = bool(torch.equal(before, after))
         t6 = time.perf_counter()
         ev.remap_s = t6 - t2
         ev.phases.update(plan_s=t3 - t2, peer_map_s=t4 - t3, copy_s=s.elapsed_time(e) / 1e3,
@@ -256,8 +269,29 @@ class DpGroup:
         self.comm = new_comm
         return ev
 
+    def source_block_sums(self, rp: ReshardPlan, bufs, group=None) -> torch.Tensor:
+        """Global block sums of the state before the change: every live
+        rank's OLD shard plus the departed ranks' bytes as their ring holders
+        keep them (what the per-step snapshot rows already hold)."""
+        block = self.block_bytes
+        nblocks = (sum(self.layer_bytes) + block - 1) // block
+        before = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+        if bufs.old is not None and self.rank in rp.old_ranks and self.rank not in rp.failed:
+            m = shard_map(rp.src, self.rank, block)
+            rows = m.new_row_sums()
+            dev.checksum(m, bufs.old, rows)
+            dev.rows_to_blocks(m, rows, before)
+        if bufs.replica is not None:
+            owner = rp.replica_of(self.rank)
+            m = shard_map(rp.src, owner, block)
+            rows = m.new_row_sums()
+            dev.checksum(m, bufs.replica, rows)
+            dev.rows_to_blocks(m, rows, before)
+        dist.all_reduce(before, group=group)
+        return before
+
     def verify_conservation(self, rp: ReshardPlan, bufs, group=None) -> bool:
-        """Block sums of all NEW shards == block sums of all OLD shards."""
+        """Block sums of all NEW shards (re-read) == block sums of all OLD shards."""
         block = self.block_bytes
         nblocks = (sum(self.layer_bytes) + block - 1) // block
         before = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")

@@ -221,11 +221,17 @@ class ReshardExecutor:
         self._exchange(bufs, group, roles=(ROLE_OLD, ROLE_REPLICA), needed=None)
         self._premapped = True
 
-    def bind(self, bufs: RankBuffers, group=None) -> None:
+    def bind(self, bufs: RankBuffers, group=None, verify: bool = False,
+             block_bytes: int = dev.DEFAULT_BLOCK_BYTES) -> None:
         """Map the peer buffers this GPU's copies touch (unless premapped) and
         build its program.  Collective over `group`: every rank calls it, and
         the exchange is skipped only when every rank premapped for a pull
-        (the same decision everywhere, so no rank waits on a missing peer)."""
+        (the same decision everywhere, so no rank waits on a missing peer).
+        verify=True (pull mode): the program checksums every byte it lands
+        in NEW (verification on arrival, launch(block_sums=...))."""
+        if verify and self.push:
+            raise ValueError("verification on arrival needs pull mode (every byte landing "
+                             "in NEW is then issued by its own GPU)")
         descs = self.rp.copies(self.rank, self.push)
         needed = set()
         for c in descs:
@@ -245,7 +251,9 @@ class ReshardExecutor:
         import torch.distributed as dist
         world = dist.get_world_size(group)
         n_table = max(max(self.rp.old_ranks + self.rp.new_ranks) + 1, world)
-        self.program = dev.CopyProgram.from_descs(descs, table, n_table, self.rank)
+        vmap = shard_map(self.rp.dst, self.rank, block_bytes) \
+            if verify and bufs.new is not None else None
+        self.program = dev.CopyProgram.from_descs(descs, table, n_table, self.rank, vmap)
 
     def _exchange(self, bufs: RankBuffers, group, roles, needed) -> None:
         import torch.distributed as dist
@@ -269,9 +277,12 @@ class ReshardExecutor:
                 table[(role, peer_rank)] = p
         self._table = table
 
-    def launch(self, n_ctas: int = 0, remote_ctas: int = 0, stream=None) -> None:
+    def launch(self, n_ctas: int = 0, remote_ctas: int = 0, stream=None,
+               block_sums=None) -> None:
         if self.program is not None:
-            self.program.launch(n_ctas, remote_ctas, stream)
+            self.program.launch(n_ctas, remote_ctas, stream,
+                                block_sums if getattr(self.program, "_verify_map", None)
+                                is not None else None)
 
     def close(self) -> None:
         self.program = None
@@ -283,9 +294,12 @@ class ReshardExecutor:
 
 
 def emulate_on_one_gpu(rp: ReshardPlan, seed: int, push: bool = True,
-                       block_bytes: int = dev.DEFAULT_BLOCK_BYTES):
+                       block_bytes: int = dev.DEFAULT_BLOCK_BYTES, block_sums=None,
+                       tamper=None):
     """Run every rank's program on the current GPU; returns (new buffers,
-    expected buffers) keyed by rank for comparison."""
+    expected buffers) keyed by rank for comparison.  block_sums (pull only):
+    run verified programs, every rank adding what it lands there.
+    tamper(rank, descs) may edit a rank's descriptors (negative tests)."""
     bufs: Dict[int, RankBuffers] = {}
     for r in sorted(set(rp.old_ranks) | set(rp.new_ranks)):
         ex = ReshardExecutor(rp, r, push)
@@ -307,9 +321,14 @@ def emulate_on_one_gpu(rp: ReshardPlan, seed: int, push: bool = True,
     for r in bufs:
         if r in rp.failed:
             continue
-        progs.append(dev.CopyProgram.from_descs(rp.copies(r, push), table, n_table, r))
+        descs = rp.copies(r, push)
+        if tamper is not None:
+            descs = tamper(r, descs)
+        vmap = shard_map(rp.dst, r, block_bytes) \
+            if block_sums is not None and r in rp.new_ranks else None
+        progs.append(dev.CopyProgram.from_descs(descs, table, n_table, r, vmap))
     for p in progs:
-        p.launch()
+        p.launch(block_sums=block_sums if getattr(p, "_verify_map", None) is not None else None)
     torch.cuda.synchronize()
     expected = {}
     for r in rp.new_ranks:

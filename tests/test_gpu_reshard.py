@@ -81,6 +81,53 @@ def test_membership_change_on_one_gpu(name, cfg, old, new, scale, push, oracle):
     assert np.array_equal(acc.cpu().numpy().view(np.uint64), want)
 
 
+@pytest.mark.parametrize("name,cfg,old,new,scale", CASES, ids=[c[0] for c in CASES])
+def test_verification_on_arrival(name, cfg, old, new, scale, oracle):
+    """Verified pull programs: the checksums of what every rank lands in NEW,
+    labelled by NEW's own segment map, add up to the source state's block
+    sums — no re-read of NEW — and the bytes are still exact."""
+    small = configs.scaled(cfg, scale)
+    rp = ReshardPlan.build(small.layer_bytes, old, new)
+    block = 65536
+    nblocks = (small.total_bytes + block - 1) // block
+    sums = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+    got, expected = emulate_on_one_gpu(rp, seed=77, push=False, block_sums=sums)
+    for r in rp.new_ranks:
+        n = rp.dst.shard_bytes(r)
+        assert torch.equal(got[r][:n], expected[r][:n]), (name, r)
+    torch.cuda.synchronize()
+    want = oracle.block_sums_synthetic(77, small.total_bytes, block)
+    assert np.array_equal(sums.cpu().numpy().view(np.uint64), want)
+
+
+def test_verification_on_arrival_catches_misplacement_and_corruption(oracle):
+    small = configs.scaled(configs.llama2_7b(), 1e-3)
+    rp = ReshardPlan.build(small.layer_bytes, list(range(8)), [0, 1, 2, 4, 5, 6, 7])
+    block = 65536
+    nblocks = (small.total_bytes + block - 1) // block
+    want = oracle.block_sums_synthetic(5, small.total_bytes, block)
+
+    def shifted(rank, descs):  # one copy lands 8 bytes early in NEW
+        d = descs.copy()
+        if rank == 2:
+            k = int(np.argmax(d["dst_off"] >= 64))
+            d["dst_off"][k] -= 8
+        return d
+
+    sums = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+    emulate_on_one_gpu(rp, seed=5, push=False, block_sums=sums, tamper=shifted)
+    torch.cuda.synchronize()
+    assert not np.array_equal(sums.cpu().numpy().view(np.uint64), want)
+
+    def dropped(rank, descs):  # one copy never issued
+        return descs[1:] if rank == 4 else descs
+
+    sums.zero_()
+    emulate_on_one_gpu(rp, seed=5, push=False, block_sums=sums, tamper=dropped)
+    torch.cuda.synchronize()
+    assert not np.array_equal(sums.cpu().numpy().view(np.uint64), want)
+
+
 def test_full_size_7b_one_rank_program_locally():
     """Config B at full size for the receive side of one survivor: the
     executing rank's push program runs with every peer buffer placed on the
