@@ -82,16 +82,23 @@ class ShardMap {
 class CopyProgram {
  public:
   // table[role * table_ranks + rank]: local or IPC-mapped buffer pointers.
+  // verify_map (NEW's segment map on exec_rank, pull programs): the copy
+  // also checksums what it lands — see launch(s, block_sums).
   CopyProgram(const std::vector<b200::CopyDesc>& copies, const std::vector<void*>& table,
-              int table_ranks, int exec_rank) {
+              int table_ranks, int exec_rank, const ShardMap* verify_map = nullptr) {
     std::vector<ew_copy_desc> d;
     d.reserve(copies.size());
     for (const b200::CopyDesc& c : copies)
       d.push_back({static_cast<std::int32_t>(c.src_role), c.src_rank,
                    static_cast<std::int32_t>(c.dst_role), c.dst_rank, c.src_off, c.dst_off,
                    c.bytes});
-    check(ew_copy_program_create(d.data(), static_cast<std::int64_t>(d.size()), table.data(),
-                                 table_ranks, exec_rank, &prog_));
+    if (verify_map != nullptr)
+      check(ew_copy_program_create_verified(d.data(), static_cast<std::int64_t>(d.size()),
+                                            table.data(), table_ranks, exec_rank,
+                                            verify_map->get(), &prog_));
+    else
+      check(ew_copy_program_create(d.data(), static_cast<std::int64_t>(d.size()), table.data(),
+                                   table_ranks, exec_rank, &prog_));
   }
   ~CopyProgram() { ew_copy_program_free(prog_); }
   CopyProgram(const CopyProgram&) = delete;
@@ -99,6 +106,17 @@ class CopyProgram {
 
   void launch(ew_stream_t s, int n_ctas = 0, int remote_ctas = 0) const {
     check(ew_copy_program_launch(prog_, n_ctas, remote_ctas, s));
+  }
+  // Verified programs: add the landed bytes' block checksums to block_sums
+  // (device u64 [2 * num_blocks()], zeroed by the caller).
+  void launch(ew_stream_t s, std::uint64_t* block_sums, int n_ctas = 0,
+              int remote_ctas = 0) const {
+    check(ew_copy_program_launch_verified(prog_, n_ctas, remote_ctas, block_sums, s));
+  }
+  std::int64_t num_blocks() const {
+    std::int64_t n = 0;
+    check(ew_copy_program_num_blocks(prog_, &n));
+    return n;
   }
 
  private:
