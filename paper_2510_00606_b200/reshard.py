@@ -293,9 +293,16 @@ class ReshardExecutor:
         self._premapped = False
 
 
+def _aliases(a, b) -> bool:
+    """True when two byte tensors share storage bytes (in-place buffers)."""
+    a0, a1 = a.data_ptr(), a.data_ptr() + a.numel()
+    b0, b1 = b.data_ptr(), b.data_ptr() + b.numel()
+    return a0 < b1 and b0 < a1
+
+
 def emulate_on_one_gpu(rp: ReshardPlan, seed: int, push: bool = True,
                        block_bytes: int = dev.DEFAULT_BLOCK_BYTES, block_sums=None,
-                       tamper=None):
+                       tamper=None, in_place: bool = False):
     """Run every rank's program on the current GPU; returns (new buffers,
     expected buffers) keyed by rank for comparison.  block_sums (pull only):
     run verified programs, every rank adding what it lands there.
@@ -303,14 +310,15 @@ def emulate_on_one_gpu(rp: ReshardPlan, seed: int, push: bool = True,
     bufs: Dict[int, RankBuffers] = {}
     for r in sorted(set(rp.old_ranks) | set(rp.new_ranks)):
         ex = ReshardExecutor(rp, r, push)
-        bufs[r] = ex.allocate()
+        bufs[r] = ex.allocate(in_place)
         if bufs[r].old is not None and r not in rp.failed:
             dev.fill_synthetic(shard_map(rp.src, r, block_bytes), bufs[r].old, seed)
         if bufs[r].replica is not None:
             dev.fill_synthetic(shard_map(rp.src, rp.replica_of(r), block_bytes), bufs[r].replica,
                                seed)
-        if bufs[r].new is not None:
-            bufs[r].new.fill_(0xA5)
+        b = bufs[r]
+        if b.new is not None and (b.old is None or not _aliases(b.new, b.old)):
+            b.new.fill_(0xA5)  # poison (an in-place NEW holds the retained bytes)
     table = {}
     for r, b in bufs.items():
         for role, t in ((ROLE_OLD, b.old), (ROLE_REPLICA, b.replica), (ROLE_NEW, b.new)):

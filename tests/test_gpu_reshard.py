@@ -100,6 +100,26 @@ def test_verification_on_arrival(name, cfg, old, new, scale, oracle):
     assert np.array_equal(sums.cpu().numpy().view(np.uint64), want)
 
 
+@pytest.mark.parametrize("contiguous", [False, True])
+def test_verification_on_arrival_in_place_stage_move(contiguous, oracle):
+    """Cross-stage layer move with in-place buffers: retained bytes are not
+    rewritten but still read and checksummed, so conservation holds."""
+    small = configs.scaled(configs.llama2_7b(), 1e-3)
+    lb = small.layer_bytes
+    rp = ReshardPlan.for_stage_move(lb[:17], lb[17:], [0, 1], [2, 3], contiguous)
+    block = 65536
+    total = sum(lb)
+    nblocks = (total + block - 1) // block
+    sums = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+    got, expected = emulate_on_one_gpu(rp, seed=9, push=False, block_sums=sums, in_place=True)
+    for r in rp.new_ranks:
+        n = rp.dst.shard_bytes(r)
+        assert torch.equal(got[r][:n], expected[r][:n]), r
+    torch.cuda.synchronize()
+    want = oracle.block_sums_synthetic(9, total, block)
+    assert np.array_equal(sums.cpu().numpy().view(np.uint64), want)
+
+
 def test_verification_on_arrival_catches_misplacement_and_corruption(oracle):
     small = configs.scaled(configs.llama2_7b(), 1e-3)
     rp = ReshardPlan.build(small.layer_bytes, list(range(8)), [0, 1, 2, 4, 5, 6, 7])
