@@ -171,7 +171,7 @@ class CopyProgram:
         return cls(h)
 
     def __del__(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
             lib.ew_copy_program_free(self._h)
             self._h = None
 
@@ -326,7 +326,7 @@ class PeerFold:
         self._h = h
 
     def __del__(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
             lib.ew_peer_fold_free(self._h)
             self._h = None
 

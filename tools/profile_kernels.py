@@ -8,6 +8,8 @@ CUDA-event times so the same command can run without ncu first.
   (d) fold_kernel, 1 Gi fp32 elements
   §8(f)#1 adam_kernel, 7B rank shard (842 M params, 11.79 GB state)
   §8(f)#2 payback_kernel, one 7B layer (202 M int64), local source
+  (b) staged_copy_kernel verified: 4->3 of 7B-per-GPU state, every rank's
+      pull program on this GPU (peers emulated by local buffers)
 """
 import json
 import sys
@@ -80,6 +82,21 @@ def main():
     b = torch.ones_like(a)
     payback_accumulate(a, b)
     out["payback_ms"] = timed(lambda: payback_accumulate(a, b))
+    del a, b
+    torch.cuda.empty_cache()
+
+    from paper_2510_00606_b200.reshard import ReshardPlan, emulate_on_one_gpu
+    lb = [x * 4 // 8 for x in configs.llama2_7b().layer_bytes]
+    rp = ReshardPlan.build(lb, [0, 1, 2, 3], [0, 1, 2])
+    nblocks = (sum(lb) + 65535) // 65536
+    sums = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record()
+    emulate_on_one_gpu(rp, seed=1, push=False, block_sums=sums)
+    t1.record()
+    torch.cuda.synchronize()
+    out["verified_reshard_emulation_ms"] = t0.elapsed_time(t1)
     print(json.dumps(out))
 
 
