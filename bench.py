@@ -915,6 +915,48 @@ def run_reduce(args, rank, world, out):
         for p in opened:
             dev.ipc_close(p)
         del peer_out
+        torch.cuda.empty_cache()
+        # world-size-invariant form: every rank has folded its micro-batch
+        # units into an int64 accumulator during backward (accumulate=1); the
+        # collective sums accumulators.  NCCL int64 all-reduce + dequant vs
+        # the peer int64 reduce-scatter + dequant + all-gather.
+        acc = torch.empty(n, dtype=torch.int64, device="cuda")
+        dev.weighted_fold([g], w, f, acc)
+        out64 = torch.empty(n, dtype=torch.float32, device="cuda")
+        fold64, opened64 = dev.peer_sum_i64_setup(acc, out64)
+        bar = dev.PeerBarrier()
+        fold64.run(f, bar)
+        bar.wait()
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(3):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            barrier(world)
+            s.record()
+            fold64.run(f, bar)
+            e.record()
+            bar.wait()
+            torch.cuda.synchronize()
+            times.append(s.elapsed_time(e) / 1e3)
+        assert not bar.timed_out(), "peer barrier timed out"
+        t_p64 = max_over_ranks([min(times)], world)[0]
+        same = torch.tensor([1 if torch.equal(out64, res) else 0], device="cuda")
+        dist.all_reduce(same, op=dist.ReduceOp.MIN)
+        out["reduce"].update({
+            "int64_accumulators": {
+                "nccl_allreduce_plus_dequant_ms": round((t_ar + t_deq) * 1e3, 3),
+                "peer_ms": round(t_p64 * 1e3, 3),
+                "peer_speedup": round((t_ar + t_deq) / t_p64, 2),
+                "peer_nvlink_gbs": round((world - 1) / world * 12 * n / t_p64 / 1e9, 1),
+                "bit_identical": bool(same.item())}})
+        bar.wait()
+        torch.cuda.synchronize()
+        barrier(world)
+        bar.close()
+        del fold64
+        for p in opened64:
+            dev.ipc_close(p)
+        del acc, out64
     del g, res
     torch.cuda.empty_cache()
 

@@ -360,6 +360,12 @@ typedef struct ew_peer_fold ew_peer_fold;
 int ew_peer_fold_create(int world, int rank, int64_t n_elems, const float* const* unit_ptrs,
                         const double* unit_weights, int n_units, float* const* out_ptrs,
                         ew_peer_fold** out);
+/* Same collective over per-rank int64 accumulators (each rank folded its own
+ * micro-batch units with ew_weighted_fold, accumulate=1): acc_ptrs lists every
+ * rank's accumulator (IPC-mapped or local), 16-byte aligned.  Reduce-scatter
+ * sums the int64 values exactly and dequantises with frac_bits. */
+int ew_peer_fold_create_i64(int world, int rank, int64_t n_elems, const int64_t* const* acc_ptrs,
+                            float* const* out_ptrs, ew_peer_fold** out);
 int ew_peer_fold_reduce_scatter(ew_peer_fold* fold, int frac_bits, ew_stream_t stream);
 int ew_peer_fold_all_gather(ew_peer_fold* fold, ew_stream_t stream);
 void ew_peer_fold_free(ew_peer_fold* fold);

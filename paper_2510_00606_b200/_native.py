@@ -228,6 +228,7 @@ _sig("ew_allreduce_u64", i32, vp, vp, i64, vp)
 _sig("ew_allreduce_max_f64", i32, vp, vp, i64, vp)
 _sig("ew_weighted_reduce", i32, vp, P(vp), P(f64), i32, i64, i64, vp, vp, vp, P(i32), vp)
 _sig("ew_peer_fold_create", i32, i32, i32, i64, P(vp), P(f64), i32, P(vp), P(vp))
+_sig("ew_peer_fold_create_i64", i32, i32, i32, i64, P(vp), P(vp), P(vp))
 _sig("ew_peer_fold_reduce_scatter", i32, vp, i32, vp)
 _sig("ew_peer_fold_all_gather", i32, vp, vp)
 _sig("ew_peer_fold_free", None, vp)

@@ -44,13 +44,17 @@ constexpr int kPfStagesMax = 8;
 constexpr int kPfConsumers = 4;
 constexpr int kPfThreads = 32 * (kPfConsumers + 1);
 
+// kI64: the units are per-rank int64 accumulators (32 B per group of 4
+// elements instead of 16), summed without weights.
+template <bool kI64>
 __global__ void __launch_bounds__(kPfThreads) peer_fold_staged_kernel(
     const PeerUnit* __restrict__ units, int n_units, int64_t lo4, int64_t hi4, double scale,
     double inv_scale, float* __restrict__ out, int slice, int stages) {
+  constexpr int kGroupBytes = kI64 ? 32 : 16;
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kPfStagesMax];
   __shared__ __align__(8) uint64_t empty[kPfStagesMax];
-  const int64_t per_piece = slice / 16;
+  const int64_t per_piece = slice / kGroupBytes;
   const int64_t n_pieces = (hi4 - lo4 + per_piece - 1) / per_piece;
   const int64_t first = blockIdx.x, step = gridDim.x;
   if (first >= n_pieces) return;
@@ -74,10 +78,12 @@ __global__ void __launch_bounds__(kPfThreads) peer_fold_staged_kernel(
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       }
       const int64_t start = lo4 + (first + k * step) * per_piece;
-      const uint32_t bytes = static_cast<uint32_t>(16 * min(per_piece, hi4 - start));
+      const uint32_t bytes = static_cast<uint32_t>(kGroupBytes * min(per_piece, hi4 - start));
       mbar_expect_tx(&full[s], bytes * n_units);
       for (int u = 0; u < n_units; ++u)
-        tma_load(ring + s * stage_bytes + u * slice, units[u].p + 4 * start, bytes, &full[s]);
+        tma_load(ring + s * stage_bytes + u * slice,
+                 reinterpret_cast<const uint8_t*>(units[u].p) + kGroupBytes * start, bytes,
+                 &full[s]);
     }
     return;
   }
@@ -96,11 +102,24 @@ __global__ void __launch_bounds__(kPfThreads) peer_fold_staged_kernel(
 #pragma unroll
       for (int u = 0; u < kPfUnitsMax; ++u) {
         if (u < n_units) {
-          const uint4 raw = lds128(stage + u * slice + 16 * j);
-          a0 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.x))) * scale);
-          a1 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.y))) * scale);
-          a2 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.z))) * scale);
-          a3 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.w))) * scale);
+          if (kI64) {  // wrapping int64 adds, like ncclInt64
+            const uint4 x = lds128(stage + u * slice + 32 * j);
+            const uint4 y = lds128(stage + u * slice + 32 * j + 16);
+            a0 = static_cast<long long>(static_cast<unsigned long long>(a0) +
+                                        (static_cast<unsigned long long>(x.y) << 32 | x.x));
+            a1 = static_cast<long long>(static_cast<unsigned long long>(a1) +
+                                        (static_cast<unsigned long long>(x.w) << 32 | x.z));
+            a2 = static_cast<long long>(static_cast<unsigned long long>(a2) +
+                                        (static_cast<unsigned long long>(y.y) << 32 | y.x));
+            a3 = static_cast<long long>(static_cast<unsigned long long>(a3) +
+                                        (static_cast<unsigned long long>(y.w) << 32 | y.z));
+          } else {
+            const uint4 raw = lds128(stage + u * slice + 16 * j);
+            a0 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.x))) * scale);
+            a1 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.y))) * scale);
+            a2 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.z))) * scale);
+            a3 += __double2ll_rn((w[u] * static_cast<double>(__uint_as_float(raw.w))) * scale);
+          }
         }
       }
       reinterpret_cast<float4*>(out)[start + j] =
@@ -158,6 +177,61 @@ __global__ void __launch_bounds__(256) peer_fold_kernel(const PeerUnit* __restri
     for (int k = 0; k < n_units; ++k)
       acc += __double2ll_rn((units[k].w * static_cast<double>(units[k].p[i])) * scale);
     out[i] = static_cast<float>(static_cast<double>(acc) * inv_scale);
+  }
+}
+
+// Reduce-scatter of per-rank int64 accumulators (each rank already folded
+// its micro-batch units locally, accumulate=1): GPU r sums element chunk r of
+// every rank's accumulator straight from peer HBM (wrapping int64 adds, like
+// ncclInt64), dequantises and writes its fp32 chunk.  8 B/element cross
+// NVLink per peer instead of the 2 x 8 B of an int64 all-reduce.
+__global__ void __launch_bounds__(256) peer_sum_i64_kernel(const PeerUnit* __restrict__ accs,
+                                                           int n_accs, int64_t lo4, int64_t hi4,
+                                                           int64_t tail_lo, int64_t n,
+                                                           double inv_scale,
+                                                           float* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  constexpr int kDepth = 2;
+  for (int64_t i0 = lo4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < hi4;
+       i0 += kDepth * stride) {
+    unsigned long long sum[kDepth][4] = {};
+    for (int k = 0; k < n_accs; ++k) {
+      const longlong2* src = reinterpret_cast<const longlong2*>(accs[k].p);
+      longlong2 x[kDepth][2];
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) {
+        const int64_t i = i0 + d * stride;
+        if (i < hi4) {
+          x[d][0] = src[2 * i];
+          x[d][1] = src[2 * i + 1];
+        } else {
+          x[d][0] = x[d][1] = make_longlong2(0, 0);
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) {
+        sum[d][0] += static_cast<unsigned long long>(x[d][0].x);
+        sum[d][1] += static_cast<unsigned long long>(x[d][0].y);
+        sum[d][2] += static_cast<unsigned long long>(x[d][1].x);
+        sum[d][3] += static_cast<unsigned long long>(x[d][1].y);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d) {
+      const int64_t i = i0 + d * stride;
+      if (i >= hi4) break;
+      reinterpret_cast<float4*>(out)[i] = make_float4(
+          static_cast<float>(static_cast<double>(static_cast<long long>(sum[d][0])) * inv_scale),
+          static_cast<float>(static_cast<double>(static_cast<long long>(sum[d][1])) * inv_scale),
+          static_cast<float>(static_cast<double>(static_cast<long long>(sum[d][2])) * inv_scale),
+          static_cast<float>(static_cast<double>(static_cast<long long>(sum[d][3])) * inv_scale));
+    }
+  }
+  for (int64_t i = tail_lo + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    unsigned long long a = 0;
+    for (int k = 0; k < n_accs; ++k)
+      a += static_cast<unsigned long long>(reinterpret_cast<const long long*>(accs[k].p)[i]);
+    out[i] = static_cast<float>(static_cast<double>(static_cast<long long>(a)) * inv_scale);
   }
 }
 
@@ -253,6 +327,7 @@ void ew_peer_barrier_free(ew_peer_barrier* b) {
 
 struct ew_peer_fold {
   int world = 0, rank = 0, n_units = 0;
+  bool i64 = false;  // units are per-rank int64 accumulators (create_i64)
   int64_t n = 0, lo4 = 0, hi4 = 0, tail_lo = 0, tail_hi = 0;
   PeerUnit* d_units = nullptr;
   float* out = nullptr;
@@ -261,9 +336,9 @@ struct ew_peer_fold {
 
 extern "C" {
 
-int ew_peer_fold_create(int world, int rank, int64_t n_elems, const float* const* unit_ptrs,
-                        const double* unit_weights, int n_units, float* const* out_ptrs,
-                        ew_peer_fold** out) {
+static int peer_fold_create(int world, int rank, int64_t n_elems, const float* const* unit_ptrs,
+                            const double* unit_weights, int n_units, float* const* out_ptrs,
+                            bool i64, ew_peer_fold** out) {
   if (out == nullptr || world < 1 || rank < 0 || rank >= world || n_elems < 0 || n_units < 0 ||
       (n_units > 0 && (!unit_ptrs || !unit_weights)) || out_ptrs == nullptr)
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_peer_fold_create: bad arguments");
@@ -275,6 +350,7 @@ int ew_peer_fold_create(int world, int rank, int64_t n_elems, const float* const
     if (out_ptrs[r] == nullptr || (reinterpret_cast<uintptr_t>(out_ptrs[r]) & 15))
       return set_error(EW_ERR_INVALID_ARGUMENT, "output pointers must be non-null and 16-byte aligned");
   auto* f = new ew_peer_fold();
+  f->i64 = i64;
   f->world = world;
   f->rank = rank;
   f->n = n_elems;
@@ -328,6 +404,23 @@ int ew_peer_fold_create(int world, int rank, int64_t n_elems, const float* const
   return EW_OK;
 }
 
+int ew_peer_fold_create(int world, int rank, int64_t n_elems, const float* const* unit_ptrs,
+                        const double* unit_weights, int n_units, float* const* out_ptrs,
+                        ew_peer_fold** out) {
+  return peer_fold_create(world, rank, n_elems, unit_ptrs, unit_weights, n_units, out_ptrs,
+                          false, out);
+}
+
+int ew_peer_fold_create_i64(int world, int rank, int64_t n_elems, const int64_t* const* acc_ptrs,
+                            float* const* out_ptrs, ew_peer_fold** out) {
+  if (acc_ptrs == nullptr || world < 1)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_peer_fold_create_i64: bad arguments");
+  std::vector<const float*> p(static_cast<std::size_t>(world));
+  std::vector<double> w(static_cast<std::size_t>(world), 0.0);
+  for (int r = 0; r < world; ++r) p[r] = reinterpret_cast<const float*>(acc_ptrs[r]);
+  return peer_fold_create(world, rank, n_elems, p.data(), w.data(), world, out_ptrs, true, out);
+}
+
 int ew_peer_fold_reduce_scatter(ew_peer_fold* f, int frac_bits, ew_stream_t stream) {
   if (f == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL peer fold");
   if (frac_bits > 1000 || frac_bits < -1000)
@@ -341,21 +434,35 @@ int ew_peer_fold_reduce_scatter(ew_peer_fold* f, int frac_bits, ew_stream_t stre
     return EW_OK;
   }
   const double scale = std::ldexp(1.0, frac_bits), inv = std::ldexp(1.0, -frac_bits);
+  if (f->i64 && (f->n_units > kPfUnitsMax || f->hi4 <= f->lo4)) {  // LDG fallback
+    const int64_t work = std::max<int64_t>(f->hi4 - f->lo4, f->n - f->tail_lo);
+    const int grid = static_cast<int>(
+        std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 8 * num_sms())));
+    peer_sum_i64_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+        f->d_units, f->n_units, f->lo4, f->hi4, f->tail_lo, f->n, inv, f->out);
+    EW_CUDA_TRY(cudaGetLastError());
+    return EW_OK;
+  }
   if (f->n_units <= kPfUnitsMax && f->hi4 > f->lo4) {
     const int slice = env_int("EW_PF_SLICE", kPfSlice);
     const int stages = std::min(env_int("EW_PF_STAGES", kPfStages), kPfStagesMax);
     const int smem = stages * f->n_units * slice;
-    EW_CUDA_TRY(cudaFuncSetAttribute(peer_fold_staged_kernel,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    const int64_t pieces = (f->hi4 - f->lo4 + slice / 16 - 1) / (slice / 16);
+    const auto kern = f->i64 ? peer_fold_staged_kernel<true> : peer_fold_staged_kernel<false>;
+    EW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int gb = f->i64 ? 32 : 16;
+    const int64_t pieces = (f->hi4 - f->lo4 + slice / gb - 1) / (slice / gb);
     const int grid = static_cast<int>(
         std::min<int64_t>(pieces, env_int("EW_PF_CTAS_PER_SM", 2) * num_sms()));
-    peer_fold_staged_kernel<<<grid, kPfThreads, smem, (cudaStream_t)stream>>>(
+    kern<<<grid, kPfThreads, smem, (cudaStream_t)stream>>>(
         f->d_units, f->n_units, f->lo4, f->hi4, scale, inv, f->out, slice, stages);
     EW_CUDA_TRY(cudaGetLastError());
     if (f->n > f->tail_lo) {  // scalar tail (last rank only)
-      peer_fold_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(f->d_units, f->n_units, 0, 0,
-                                                            f->tail_lo, f->n, scale, inv, f->out);
+      if (f->i64)
+        peer_sum_i64_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(
+            f->d_units, f->n_units, 0, 0, f->tail_lo, f->n, inv, f->out);
+      else
+        peer_fold_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(
+            f->d_units, f->n_units, 0, 0, f->tail_lo, f->n, scale, inv, f->out);
       EW_CUDA_TRY(cudaGetLastError());
     }
     return EW_OK;

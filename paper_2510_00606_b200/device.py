@@ -316,13 +316,20 @@ class PeerFold:
     all_gather leaves the full reduced fp32 vector in this rank's output."""
 
     def __init__(self, world: int, rank: int, n_elems: int, unit_ptrs: Sequence[int],
-                 weights: Sequence[float], out_ptrs: Sequence[int]):
+                 weights: Optional[Sequence[float]], out_ptrs: Sequence[int]):
+        """weights=None: unit_ptrs are the world's per-rank int64
+        accumulators (ew_peer_fold_create_i64), one per rank in rank order."""
         u = (C.c_void_p * max(1, len(unit_ptrs)))(*unit_ptrs)
-        w = (C.c_double * max(1, len(weights)))(*[float(x) for x in weights])
         o = (C.c_void_p * max(1, len(out_ptrs)))(*out_ptrs)
         h = C.c_void_p()
-        check(lib.ew_peer_fold_create(world, rank, int(n_elems), u, w, len(unit_ptrs), o,
-                                      C.byref(h)))
+        if weights is None:
+            if len(unit_ptrs) != world:
+                raise ValueError("one int64 accumulator per rank")
+            check(lib.ew_peer_fold_create_i64(world, rank, int(n_elems), u, o, C.byref(h)))
+        else:
+            w = (C.c_double * max(1, len(weights)))(*[float(x) for x in weights])
+            check(lib.ew_peer_fold_create(world, rank, int(n_elems), u, w, len(unit_ptrs), o,
+                                          C.byref(h)))
         self._h = h
 
     def __del__(self):
@@ -425,6 +432,33 @@ def peer_weighted_reduce_setup(units: Sequence[torch.Tensor], weights: Sequence[
         wts += d["w"]
     fold = PeerFold(world, rank, out.numel(), unit_ptrs, wts, out_ptrs)
     return fold, len(unit_ptrs), opened
+
+
+def peer_sum_i64_setup(acc: torch.Tensor, out: torch.Tensor, group=None):
+    """Peer collective over per-rank int64 accumulators (each rank folded its
+    own micro-batch units into `acc`): exchange IPC handles and build the
+    PeerFold.  fold.run(frac_bits, barrier) leaves the dequantised sum in
+    `out` on every rank.  Returns (fold, opened_peer_pointers)."""
+    import torch.distributed as dist
+    if acc.dtype != torch.int64 or acc.numel() != out.numel():
+        raise ValueError("acc must be int64 with out.numel() elements")
+    rank = dist.get_rank(group)
+    world = dist.get_world_size(group)
+    allv = [None] * world
+    dist.all_gather_object(allv, (ipc_handle(acc), ipc_handle(out), out.numel()), group=group)
+    opened, acc_ptrs, out_ptrs = [], [], []
+    for r, (ha, ho, n) in enumerate(allv):
+        if n != out.numel():
+            raise N.DimensionMismatch("ranks disagree on the gradient length")
+        if r == rank:
+            acc_ptrs.append(acc.data_ptr())
+            out_ptrs.append(out.data_ptr())
+        else:
+            for h, lst in ((ha, acc_ptrs), (ho, out_ptrs)):
+                p = ipc_open(*h)
+                opened.append(p)
+                lst.append(p)
+    return PeerFold(world, rank, out.numel(), acc_ptrs, None, out_ptrs), opened
 
 
 class Communicator:

@@ -242,10 +242,23 @@ def _worker(rank, world, port, result_dir):
         torch.cuda.synchronize()
         report["device barrier ok"] = not bar.timed_out()
         report["peer reduce (device barriers) bit-identical"] = bool(torch.equal(out, single))
+        # per-rank int64 accumulators (each rank folded its own units)
+        # summed over peer memory: same bits again
+        acc_mine = torch.empty(dim, dtype=torch.int64, device="cuda")
+        dev.weighted_fold(units, [w[u] for u in mine], f, acc_mine) if units else acc_mine.zero_()
+        out64 = torch.full((dim,), -1.0, dtype=torch.float32, device="cuda")
+        fold64, opened64 = dev.peer_sum_i64_setup(acc_mine, out64)
+        torch.cuda.synchronize()
+        dist.barrier()
+        for _ in range(2):
+            fold64.run(f, bar)
+        bar.wait()
+        torch.cuda.synchronize()
+        report["peer int64-accumulator reduce bit-identical"] = bool(torch.equal(out64, single))
         dist.barrier()
         bar.close()
-        del fold
-        for p in opened:
+        del fold, fold64
+        for p in opened + opened64:
             dev.ipc_close(p)
     except Exception as e:  # report, do not hang the other ranks
         report["error"] = repr(e)
