@@ -104,3 +104,32 @@ def test_adam_step_rejects_misaligned():
         dev.adam_step(g.data_ptr() + 4, st, dev.adam_hyper(), 1)
     with pytest.raises(ValueError):
         dev.adam_step(g, st, dev.adam_hyper(), 0)
+
+
+def test_fused_rows_fallback_for_unaligned_sections():
+    """Sections that do not start on checksum-block boundaries take the
+    warp-atomic path of ew_adam_step_rows; its rows still equal kernel (a)'s."""
+    import ctypes as C
+    from paper_2510_00606_b200._native import lib
+    n = 100_003
+    sec = 4 * n + 256 - (4 * n) % 256          # 256-aligned, not 64 KiB-aligned
+    nbytes = 3 * sec + 2 * n + 14
+    buf = torch.zeros(nbytes + 16, dtype=torch.uint8, device="cuda")
+    f32 = lambda k: buf[k * sec:k * sec + 4 * n].view(torch.float32)
+    master, m, v = f32(0), f32(1), f32(2)
+    param = buf[3 * sec:3 * sec + 2 * n].view(torch.bfloat16)
+    rng = np.random.default_rng(4)
+    master.copy_(torch.from_numpy(rng.normal(0, 0.02, n).astype(np.float32)))
+    g = torch.from_numpy(_grads(rng, n, 1)).cuda()
+    segs = np.zeros(1, dtype=[("global_lo", np.int64), ("length", np.int64), ("local_off", np.int64)])
+    segs[0] = (0, nbytes, 0)
+    mp = dev.ShardMap(segs, 65536)
+    rows = mp.new_row_sums()
+    h = dev.adam_hyper()
+    dev.check(lib.ew_adam_step_rows(dev._ptr(g), dev._ptr(master), dev._ptr(m), dev._ptr(v),
+                                    dev._ptr(param), n, C.byref(h), 1, dev._ptr(buf), nbytes,
+                                    65536, dev._ptr(rows), dev._stream()))
+    ref = mp.new_row_sums()
+    dev.checksum(mp, buf, ref)
+    torch.cuda.synchronize()
+    assert torch.equal(rows[:2 * mp.num_rows], ref[:2 * mp.num_rows])
