@@ -171,12 +171,28 @@ def _worker(rank, world, port, result_dir):
         grp = dist.new_group(survivors)
         rp = ReshardPlan.build(cfg.layer_bytes, range(world), survivors)
         shrunk = None
+        # before the failure: every rank's live shard, and the ring replica
+        # its holder keeps of it (RingReplica pull), which is what the
+        # recovery reads for the departed rank's bytes
+        ex = ReshardExecutor(rp, rank) if rank != drop else None
+        bufs = ex.allocate() if ex is not None else None
+        live = bufs.old if bufs is not None else dev.empty_bytes(rp.src.shard_bytes(rank))
+        lm = shard_map(rp.src, rank)
+        dev.fill_synthetic(lm, live, 5)
+        live_rows = lm.new_row_sums()
+        dev.checksum(lm, live, live_rows)
+        owner = (rank + 1) % world
+        holds_drop = bufs is not None and bufs.replica is not None
+        rbuf = bufs.replica if holds_drop else dev.empty_bytes(rp.src.shard_bytes(owner))
+        torch.cuda.synchronize()
+        ring = RingReplica(rp.src, list(range(world)), rank, rbuf, live, live_rows)
+        dist.barrier()
+        ring.refresh()
+        torch.cuda.synchronize()
+        report["ring replica before failure verified"] = int(ring.bad.item()) == 0
+        dist.barrier()
+        ring.close()
         if rank != drop:
-            ex = ReshardExecutor(rp, rank)
-            bufs = ex.allocate()
-            dev.fill_synthetic(shard_map(rp.src, rank), bufs.old, 5)
-            if bufs.replica is not None:
-                dev.fill_synthetic(shard_map(rp.src, rp.replica_of(rank)), bufs.replica, 5)
             group = DpGroup(cfg.layer_bytes, range(world), rank, comm)
             ev = group.recover([drop], bufs, group=grp)
             report["recovery verified by checksums"] = ev.verified
