@@ -842,6 +842,79 @@ def run_philox(args, rank, world, out):
 PHILOX_COMPUTE_CEILING_GBLOCKS = 100.3  # profiles/r01_microbench_streaming.md
 
 
+def run_cpu_beside(args, out):
+    """The CPU paths of BASELINE.md §3 timed on this box's host cores in the
+    same run, beside kernels (b), (c), (d) — reported baselines, not targets
+    (test infrastructure: oracle/ restatements and the reference library).
+    Each is a bounded sample (a few seconds)."""
+    import numpy as np
+    from oracle.ew_oracle import load_oracle, load_reference
+    from paper_2510_00606_b200 import configs, fabric
+    orc, ref = load_oracle(), load_reference()
+    T = os.cpu_count() or 1
+    res = {"cores": T}
+    # (b) plan: reference overlap_matrix (1 thread, as shipped) on 7B 8->7;
+    # execution: one memcpy per entry of the bottleneck rank's copies on host
+    # buffers, T threads, first ~2 GiB of entries
+    cfg = configs.llama2_7b()
+    src = fabric.interleaved_layout(cfg.layer_bytes, range(8))
+    dst = fabric.interleaved_layout(cfg.layer_bytes, [0, 1, 2, 4, 5, 6, 7])
+    ring = fabric.SnapshotRing(list(range(8)))
+    t0 = time.perf_counter()
+    plan = fabric.overlap_matrix(src, dst, [3], ring)
+    res["b_plan_b200_incl_python_ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+    if ref is not None:
+        rs, rd = ref.interleaved(cfg.layer_bytes, range(8)), ref.interleaved(cfg.layer_bytes, [0, 1, 2, 4, 5, 6, 7])
+        res["b_plan_reference_ms"] = round(min(ref.overlap_matrix(rs, rd, cfg.total_bytes, [3], list(range(8)))[2]
+                                               for _ in range(3)) * 1e3, 3)
+    ent = plan.entries
+    lens = (ent["hi"] - ent["lo"]).astype(np.int64)
+    keep = np.cumsum(lens) <= (2 << 30)
+    keep[0] = True
+    lens = lens[keep]
+    total = int(lens.sum())
+    a = np.empty(total, dtype=np.uint8)
+    a[::4096] = 1
+    b = np.empty(total, dtype=np.uint8)
+    offs = np.concatenate([[0], np.cumsum(lens)[:-1]])
+    srcs = [a.ctypes.data + int(o) for o in offs]
+    dsts = [b.ctypes.data + int(o) for o in offs]
+    orc.memcpy_mt(srcs, dsts, lens.tolist(), T)
+    t0 = time.perf_counter()
+    reps = 3
+    for _ in range(reps):
+        orc.memcpy_mt(srcs, dsts, lens.tolist(), T)
+    dt = (time.perf_counter() - t0) / reps
+    res["b_execute_gbs"] = round(total / dt / 1e9, 2)
+    res["b_execute_sample"] = f"{len(lens)} entries of the 7B 8->7 plan, {total} bytes, host memcpy"
+    del a, b
+    # (c) draw() over disjoint samples on T threads (reference rng.cpp:38-53)
+    ns, k = 4 * T, 1 << 20
+    orc.draw_mt(0, 0, T, 1, 0, 1024, T)
+    t0 = time.perf_counter()
+    orc.draw_mt(0, 0, ns, 1, 0, k, T)
+    dt = time.perf_counter() - t0
+    res["c_draw_gblocks_per_s"] = round(ns * k / 4 / dt / 1e9, 3)
+    if ref is not None:
+        t0 = time.perf_counter()
+        ref.draw(0, 0, 1, 0, 1 << 20)
+        res["c_reference_draw_gblocks_per_s_1thread"] = round((1 << 20) / 4 / (time.perf_counter() - t0) / 1e9, 4)
+    # (d) weighted_grad_average: reference (1 thread) and the element-parallel
+    # restatement (T threads, identical per-element fold, bit-identical)
+    g = np.random.default_rng(5).normal(0, 1e-3, size=(5, 1 << 24))
+    w = np.full(5, 0.2)
+    t0 = time.perf_counter()
+    mt = orc.weighted_average_mt(w, g, T)
+    dt = time.perf_counter() - t0
+    res["d_weighted_average_mt_gbs"] = round(6 * 8 * (1 << 24) / dt / 1e9, 2)
+    if ref is not None:
+        t0 = time.perf_counter()
+        one = ref.weighted_grad_average(w, g)
+        res["d_reference_gbs_1thread"] = round(6 * 8 * (1 << 24) / (time.perf_counter() - t0) / 1e9, 2)
+        res["d_mt_bit_identical_to_reference"] = bool(np.array_equal(mt, one))
+    out["cpu_beside"] = res
+
+
 def run_reduce(args, rank, world, out):
     import torch
     import torch.distributed as dist
@@ -989,6 +1062,8 @@ def bench_b200(args):
         run_philox(args, rank, world, out)
     if "reduce" not in skip:
         run_reduce(args, rank, world, out)
+    if rank == 0 and "cpu" not in skip:
+        run_cpu_beside(args, out)
     if rank == 0:
         line = json.dumps(out)
         print(line, flush=True)

@@ -425,3 +425,112 @@ void ew_oracle_adam_step(const float* grad, float* master, float* exp_avg, float
     param[i] = ew_oracle_bf16(p1);
   }
 }
+
+/* ---- multi-threaded CPU paths timed beside the GPU kernels (BASELINE §3) --
+ * Reported baselines, not optimisation targets: the reference's own
+ * functions are single-threaded planners/models, so these restate the byte
+ * work on T host threads with the same per-element arithmetic. */
+typedef struct {
+  int64_t lo, hi;
+  const uint8_t* const* src;
+  uint8_t* const* dst;
+  const int64_t* bytes;
+  /* draw */
+  uint64_t seed, sample_lo;
+  uint32_t layer, op;
+  int64_t n_per_sample;
+  double* out;
+  /* weighted average */
+  const double* w;
+  const double* g;
+  int n_units;
+  int64_t dim;
+} cpu_job;
+
+static void* copy_worker(void* p) {
+  cpu_job* j = (cpu_job*)p;
+  for (int64_t k = j->lo; k < j->hi; ++k) memcpy(j->dst[k], j->src[k], (size_t)j->bytes[k]);
+  return NULL;
+}
+
+/* (b) plan execution: one memcpy per TransferEntry, entries split over T
+ * threads (SURVEY §8(d) "builder CPU plan executor") */
+void ew_oracle_memcpy_mt(const uint8_t* const* src, uint8_t* const* dst, const int64_t* bytes,
+                         int64_t n, int threads) {
+  if (threads < 1) threads = 1;
+  pthread_t th[256];
+  cpu_job jobs[256];
+  if (threads > 256) threads = 256;
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (cpu_job){0};
+    jobs[t].lo = n * t / threads;
+    jobs[t].hi = n * (t + 1) / threads;
+    jobs[t].src = src;
+    jobs[t].dst = dst;
+    jobs[t].bytes = bytes;
+    pthread_create(&th[t], NULL, copy_worker, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+}
+
+static void* draw_worker(void* p) {
+  cpu_job* j = (cpu_job*)p;
+  for (int64_t s = j->lo; s < j->hi; ++s)
+    ew_oracle_draw(j->seed, j->sample_lo + (uint64_t)s, j->layer, j->op, j->n_per_sample,
+                   j->out + s * j->n_per_sample);
+  return NULL;
+}
+
+/* (c) draw() (rng.cpp:38-53) over disjoint samples on T threads */
+void ew_oracle_draw_mt(uint64_t seed, uint64_t sample_lo, int64_t n_samples, uint32_t layer,
+                       uint32_t op, int64_t n_per_sample, double* out, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  cpu_job jobs[256];
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (cpu_job){0};
+    jobs[t].lo = n_samples * t / threads;
+    jobs[t].hi = n_samples * (t + 1) / threads;
+    jobs[t].seed = seed;
+    jobs[t].sample_lo = sample_lo;
+    jobs[t].layer = layer;
+    jobs[t].op = op;
+    jobs[t].n_per_sample = n_per_sample;
+    jobs[t].out = out;
+    pthread_create(&th[t], NULL, draw_worker, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+}
+
+static void* wavg_worker(void* p) {
+  cpu_job* j = (cpu_job*)p;
+  for (int64_t i = j->lo; i < j->hi; ++i) {
+    double acc = 0.0;
+    for (int u = 0; u < j->n_units; ++u) acc += j->w[u] * j->g[(int64_t)u * j->dim + i];
+    j->out[i] = acc;
+  }
+  return NULL;
+}
+
+/* (d) weighted_grad_average (dataflow.cpp:71-83) element-parallel on T
+ * threads with the reference's per-element left-fold order (bit-identical) */
+void ew_oracle_weighted_average_mt(const double* w, const double* g, int n_units, int64_t dim,
+                                   double* out, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  cpu_job jobs[256];
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (cpu_job){0};
+    jobs[t].lo = dim * t / threads;
+    jobs[t].hi = dim * (t + 1) / threads;
+    jobs[t].w = w;
+    jobs[t].g = g;
+    jobs[t].n_units = n_units;
+    jobs[t].dim = dim;
+    jobs[t].out = out;
+    pthread_create(&th[t], NULL, wavg_worker, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+}

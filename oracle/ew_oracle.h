@@ -40,6 +40,12 @@ void ew_oracle_weighted_fixed(const double* w, const float* g, int n_units, int6
                               int frac_bits, int64_t* acc);
 
 uint16_t ew_oracle_bf16(float f);
+void ew_oracle_memcpy_mt(const uint8_t* const* src, uint8_t* const* dst, const int64_t* bytes,
+                         int64_t n, int threads);
+void ew_oracle_draw_mt(uint64_t seed, uint64_t sample_lo, int64_t n_samples, uint32_t layer,
+                       uint32_t op, int64_t n_per_sample, double* out, int threads);
+void ew_oracle_weighted_average_mt(const double* w, const double* g, int n_units, int64_t dim,
+                                   double* out, int threads);
 void ew_oracle_adam_scalars(double lr, double b1, double b2, double eps, double wd, int64_t step,
                             float out8[8]);
 void ew_oracle_adam_step(const float* grad, float* master, float* exp_avg, float* exp_avg_sq,

@@ -56,6 +56,9 @@ class Oracle:
         L.ew_oracle_fixed_point_bits.argtypes = [f64, i64]
         L.ew_oracle_fixed_point_bits.restype = i32
         L.ew_oracle_weighted_fixed.argtypes = [P(f64), P(C.c_float), i32, i64, i32, P(i64)]
+        L.ew_oracle_memcpy_mt.argtypes = [P(vp), P(vp), P(i64), i64, i32]
+        L.ew_oracle_draw_mt.argtypes = [u64, u64, i64, u32, u32, i64, P(f64), i32]
+        L.ew_oracle_weighted_average_mt.argtypes = [P(f64), P(f64), i32, i64, P(f64), i32]
         L.ew_oracle_adam_scalars.argtypes = [f64, f64, f64, f64, f64, i64, P(C.c_float)]
         L.ew_oracle_adam_step.argtypes = [P(C.c_float)] * 4 + [P(C.c_uint16), i64] + [f64] * 5 + [i64]
         L.ew_oracle_snapshot_mt.argtypes = [P(i64), i64, i64, vp, vp, P(u64), i32]
@@ -172,6 +175,28 @@ class Oracle:
         self.lib.ew_oracle_weighted_fixed(_np_ptr(w, f64), _np_ptr(g, C.c_float), len(w),
                                           g.shape[1], frac_bits, _np_ptr(out, i64))
         return out
+
+    # -- multi-threaded CPU paths timed beside the GPU kernels
+    def memcpy_mt(self, srcs, dsts, nbytes, threads: int) -> None:
+        n = len(nbytes)
+        s = (vp * max(1, n))(*srcs)
+        d = (vp * max(1, n))(*dsts)
+        b = np.ascontiguousarray(nbytes, dtype=np.int64)
+        self.lib.ew_oracle_memcpy_mt(s, d, _np_ptr(b, i64), n, threads)
+
+    def draw_mt(self, seed, sample_lo, n_samples, layer, op, n_per_sample, threads) -> np.ndarray:
+        out = np.empty(max(1, n_samples * n_per_sample), dtype=np.float64)
+        self.lib.ew_oracle_draw_mt(seed, sample_lo, n_samples, layer, op, n_per_sample,
+                                   _np_ptr(out, f64), threads)
+        return out[:n_samples * n_per_sample].reshape(n_samples, n_per_sample)
+
+    def weighted_average_mt(self, weights, grads: np.ndarray, threads: int) -> np.ndarray:
+        g = np.ascontiguousarray(grads, dtype=np.float64)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        out = np.empty(max(1, g.shape[1]), dtype=np.float64)
+        self.lib.ew_oracle_weighted_average_mt(_np_ptr(w, f64), _np_ptr(g, f64), len(w),
+                                               g.shape[1], _np_ptr(out, f64), threads)
+        return out[:g.shape[1]]
 
     # -- ring replica by optimizer replay
     def adam_scalars(self, hyper, step: int) -> np.ndarray:
