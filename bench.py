@@ -495,6 +495,49 @@ def run_reshard(args, rank, world, out):
         "edit_plan": {"links_removed": len(edit.links_to_remove), "links_added": len(edit.links_to_add)},
     }
     out["reshard"]["mttr_ms"]["total"] = round(sum(out["reshard"]["mttr_ms"].values()), 3)
+
+    # the same departure with every single-rank departure prepared in steady
+    # state (recovery.PreparedRecovery): lookup + launch of a bound, verified
+    # program; the comm edit is the one measured above
+    from paper_2510_00606_b200.recovery import PreparedRecovery
+    succ = (rank + 1) % world
+    rep = bufs.replica if bufs.replica is not None else \
+        dev.empty_bytes(rp.src.shard_bytes(succ))
+    if bufs.replica is None:
+        dev.fill_synthetic(shard_map(rp.src, succ, block), rep, 0)
+    prep = PreparedRecovery(lb, old, rank, bufs.old, rep, block)
+    after.zero_()
+    barrier(world)
+    times = []
+    for _ in range(reps):
+        after.zero_()
+        barrier(world)
+        t0 = time.perf_counter()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        if rank != drop:
+            prep.recover(drop, after)
+        e.record(stream)
+        t_host = time.perf_counter() - t0
+        barrier(world)
+        times.append((s.elapsed_time(e) / 1e3, t_host))
+    t_pcopy = max_over_ranks([sum(t[0] for t in times) / reps, max(t[1] for t in times)], world)
+    dist.all_reduce(after)
+    prep_ok = bool(torch.equal(before, after))
+    if rank != drop:
+        n_new = rp.dst.shard_bytes(rank)
+        prep_ok = prep_ok and bool(torch.equal(prep.new_view(drop)[:n_new], bufs.new[:n_new]))
+    okt = torch.tensor([1 if prep_ok else 0], device="cuda")
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    mt = out["reshard"]["mttr_ms"]
+    out["reshard"]["mttr_ms_prepared"] = {
+        "comm_edit": mt["comm_edit"], "lookup_and_launch_host": round(t_pcopy[1] * 1e3, 3),
+        "copy": round(t_pcopy[0] * 1e3, 3), "verify": mt["verify"],
+        "total": round(mt["comm_edit"] + t_pcopy[0] * 1e3 + mt["verify"], 3),
+        "verified": bool(okt.item()),
+        "note": "all single-rank departures planned, lowered and bound in steady state"}
+    barrier(world)
+    prep.close()
     ex.close()
     if shrunk is not None:
         shrunk.destroy()

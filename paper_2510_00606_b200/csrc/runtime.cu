@@ -64,7 +64,9 @@ struct IpcMapping {
 };
 std::mutex g_ipc_mu;
 std::map<std::string, IpcMapping> g_ipc_by_handle;  // handle bytes -> mapping
-std::map<void*, std::string> g_ipc_by_ptr;           // returned ptr -> handle bytes
+// returned ptr -> (handle bytes, opens of this ptr): one mapping can be
+// opened several times (same or different offsets); every open is closed once
+std::map<void*, std::pair<std::string, int>> g_ipc_by_ptr;
 
 }  // namespace
 
@@ -179,7 +181,9 @@ int ew_ipc_open(const void* handle64, int64_t offset, void** out) {
   }
   ++m.refs;
   void* p = static_cast<char*>(m.base) + offset;
-  g_ipc_by_ptr[p] = key;
+  auto& slot = g_ipc_by_ptr[p];
+  slot.first = key;
+  ++slot.second;
   *out = p;
   return EW_OK;
 }
@@ -188,15 +192,14 @@ int ew_ipc_close(void* ptr) {
   std::lock_guard<std::mutex> lock(g_ipc_mu);
   const auto it = g_ipc_by_ptr.find(ptr);
   if (it == g_ipc_by_ptr.end()) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_ipc_close: unknown pointer");
-  IpcMapping& m = g_ipc_by_handle[it->second];
+  const std::string key = it->second.first;
+  if (--it->second.second == 0) g_ipc_by_ptr.erase(it);
+  IpcMapping& m = g_ipc_by_handle[key];
   if (--m.refs == 0) {
     const cudaError_t e = cudaIpcCloseMemHandle(m.base);
-    g_ipc_by_handle.erase(it->second);
-    g_ipc_by_ptr.erase(it);
+    g_ipc_by_handle.erase(key);
     EW_CUDA_TRY(e);
-    return EW_OK;
   }
-  g_ipc_by_ptr.erase(it);
   return EW_OK;
 }
 

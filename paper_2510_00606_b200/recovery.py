@@ -191,6 +191,71 @@ class ReplayReplica:
         self._opened = []
 
 
+class PreparedRecovery:
+    """Every single-rank departure of a DP group, planned, lowered and bound
+    in steady state, so a failure runs only the copy.
+
+    The reference plans at failure time (Simulation::recover_elaswave,
+    sim.cpp:597-722; overlap_matrix per event).  On B200 the inputs of a
+    single departure are all known before it happens: the layouts, every
+    peer's live shard and the ring replicas (RingReplica / ReplayReplica keep
+    them current), so each rank builds, once, the verified pull program for
+    each possible departed peer d — plan (overlap_matrix + integrity_check),
+    lowering, IPC mappings and the device-resident copy program — against
+    one NEW buffer sized for the largest case.  recover(d) is a table lookup
+    and one launch.  Memory: one NEW shard plus a few KiB of copy items per
+    scenario."""
+
+    def __init__(self, layer_bytes: Sequence[int], members: Sequence[int], rank: int,
+                 old: torch.Tensor, replica: torch.Tensor,
+                 block_bytes: int = dev.DEFAULT_BLOCK_BYTES, group=None):
+        """`old`: this rank's live shard; `replica`: the shard of its ring
+        successor (SnapshotRing.backs_up(rank)).  Collective over `group`."""
+        members = sorted(members)
+        self.rank = rank
+        self.block_bytes = block_bytes
+        self.plans = {d: ReshardPlan.build(layer_bytes, members, [m for m in members if m != d])
+                      for d in members}
+        n_new = max(p.dst.shard_bytes(rank) for d, p in self.plans.items() if d != rank)
+        self.new = dev.empty_bytes(n_new)
+        # one steady-state exchange maps every peer's OLD and REPLICA buffer
+        from .reshard import RankBuffers
+        self._base = ReshardExecutor(self.plans[members[0]], rank)
+        self._base.premap(RankBuffers(old, replica, None), group)
+        self.execs: Dict[int, Optional[ReshardExecutor]] = {}
+        for d, rp in self.plans.items():
+            if d == rank:
+                self.execs[d] = None  # nothing to build for one's own departure
+                continue
+            ex = ReshardExecutor(rp, rank)
+            ex._table = dict(self._base._table)
+            ex._premapped = True      # pull + premapped: bind() does no exchange
+            rep = replica if rp.replica_of(rank) == d else None
+            ex.bind(RankBuffers(old, rep, self.new), group, verify=True,
+                    block_bytes=block_bytes)
+            self.execs[d] = ex
+
+    def recover(self, departed: int, block_sums: torch.Tensor, stream=None) -> ReshardPlan:
+        """Launch the prepared program for `departed` (block_sums zeroed by
+        the caller); returns its plan.  The caller all-reduces block_sums
+        and compares them with the snapshot's block sums."""
+        ex = self.execs[departed]
+        if ex is None:
+            raise ValueError("the departed rank does not recover itself")
+        ex.launch(stream=stream, block_sums=block_sums)
+        return self.plans[departed]
+
+    def new_view(self, departed: int) -> torch.Tensor:
+        return self.new[:self.plans[departed].dst.shard_bytes(self.rank)]
+
+    def close(self) -> None:
+        for ex in self.execs.values():
+            if ex is not None:
+                ex.program = None
+        self.execs = {}
+        self._base.close()
+
+
 class DpGroup:
     """One rank's view of an interleaved-ZeRO DP group (one process per GPU)."""
 

@@ -66,6 +66,44 @@ def _worker(rank, world, port, result_dir):
                 report[f"reshard drop{drop} push={push}"] = ok
                 ex.close()
                 dist.barrier()
+        # every single departure prepared in steady state (recovery.PreparedRecovery)
+        from paper_2510_00606_b200.recovery import PreparedRecovery
+        rp0 = ReshardPlan.build(cfg.layer_bytes, range(world), range(world))
+        lay0 = rp0.src
+        live0 = dev.empty_bytes(lay0.shard_bytes(rank))
+        m0 = shard_map(lay0, rank)
+        dev.fill_synthetic(m0, live0, 31)
+        succ = (rank + 1) % world
+        rep0 = dev.empty_bytes(lay0.shard_bytes(succ))
+        dev.fill_synthetic(shard_map(lay0, succ), rep0, 31)
+        rows0 = m0.new_row_sums()
+        dev.checksum(m0, live0, rows0)
+        block = 65536
+        nblocks = (sum(cfg.layer_bytes) + block - 1) // block
+        before = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+        dev.rows_to_blocks(m0, rows0, before)
+        dist.all_reduce(before)
+        torch.cuda.synchronize()
+        prep = PreparedRecovery(cfg.layer_bytes, range(world), rank, live0, rep0)
+        ok = True
+        for d in range(world):
+            sums = torch.zeros_like(before)
+            dist.barrier()
+            rp_d = prep.plans[d]
+            if rank != d:
+                prep.recover(d, sums)
+            torch.cuda.synchronize()
+            dist.barrier()
+            dist.all_reduce(sums)
+            ok = ok and bool(torch.equal(sums, before))
+            if rank != d:
+                exp = dev.empty_bytes(rp_d.dst.shard_bytes(rank))
+                dev.fill_synthetic(shard_map(rp_d.dst, rank), exp, 31)
+                n = rp_d.dst.shard_bytes(rank)
+                ok = ok and bool(torch.equal(prep.new_view(d)[:n], exp[:n]))
+        report["prepared single departures verified"] = ok
+        dist.barrier()
+        prep.close()
         # cross-stage layer move (interleaved in place, and contiguous)
         d = world // 2
         for contiguous in (False, True):
