@@ -501,6 +501,19 @@ def run_reshard(args, rank, world, out):
     # program; the comm edit is the one measured above
     from paper_2510_00606_b200.recovery import PreparedRecovery
     succ = (rank + 1) % world
+    need = rp.dst.shard_bytes(rank) + (0 if bufs.replica is not None else rp.src.shard_bytes(succ))
+    fits = torch.tensor([1 if torch.cuda.mem_get_info()[0] > need + (4 << 30) else 0],
+                        device="cuda")
+    dist.all_reduce(fits, op=dist.ReduceOp.MIN)
+    if not fits.item():  # e.g. config D: a second NEW shard does not fit in HBM
+        out["reshard"]["mttr_ms_prepared"] = {"skipped": "a second NEW shard does not fit"}
+        ex.close()
+        if shrunk is not None:
+            shrunk.destroy()
+        comm.destroy()
+        del bufs
+        torch.cuda.empty_cache()
+        return
     rep = bufs.replica if bufs.replica is not None else \
         dev.empty_bytes(rp.src.shard_bytes(succ))
     if bufs.replica is None:

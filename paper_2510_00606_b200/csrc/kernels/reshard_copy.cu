@@ -109,6 +109,36 @@ __device__ __forceinline__ uint64_t lds64(const uint8_t* p) {
   return *reinterpret_cast<const uint64_t*>(p);
 }
 
+// Sum over one lane's words w = s + lane + 32 j (j < J) of a segment [s, e)
+// that lies in one block: a += sum v, b += sum (w+1) v, with the (w+1)
+// weights folded in once at the end from two running sums (T1 = sum v,
+// T2 = sum_j sum_{i<j} v_i, so sum_j j v_j = (J-1) T1 - T2).  Interior words
+// only (no masking); word w's bytes start at A0 + 8 (w - W0), shifted by sh.
+__device__ __forceinline__ void segment_sums(const uint8_t* A0, int64_t W0, int sh, int64_t s,
+                                             int64_t e, int lane, uint64_t& a, uint64_t& b) {
+  const int64_t w0 = s + lane;
+  if (w0 >= e) return;
+  const uint64_t J = static_cast<uint64_t>((e - w0 + 31) / 32);
+  const uint8_t* q = A0 + 8 * (w0 - W0);
+  uint64_t t1 = 0, t2 = 0;
+  if (sh == 0) {
+#pragma unroll 4
+    for (uint64_t j = 0; j < J; ++j, q += 256) {
+      t2 += t1;
+      t1 += lds64(q);
+    }
+  } else {
+    const int rs = 8 * sh, ls = 64 - 8 * sh;
+#pragma unroll 4
+    for (uint64_t j = 0; j < J; ++j, q += 256) {
+      t2 += t1;
+      t1 += (lds64(q) >> rs) | (lds64(q + 8) << ls);
+    }
+  }
+  a += t1;
+  b += (static_cast<uint64_t>(w0) + 1) * t1 + 32 * ((J - 1) * t1 - t2);
+}
+
 __device__ void checksum_piece(const uint8_t* stage, const Piece& pc, int warp_c, int lane,
                                unsigned long long* block_sums, int word_shift) {
   const int r = static_cast<int>(reinterpret_cast<uintptr_t>(pc.src) & 15);
@@ -118,27 +148,34 @@ __device__ void checksum_piece(const uint8_t* stage, const Piece& pc, int warp_c
   const int64_t q0 = W0 + nw * warp_c / kConsumerWarps;
   const int64_t q1 = W0 + nw * (warp_c + 1) / kConsumerWarps;
   if (q0 >= q1) return;  // uniform per warp
+  // word W0's first byte sits at stage[p0], p0 = r + 8 W0 - g0 in [r-7, r];
+  // the 8-byte-aligned loads below may touch up to 8 bytes of neighbouring
+  // shared memory before the stage, only ever for masked-off bytes
+  const int p0 = r + static_cast<int>(8 * W0 - g0);
+  const int sh = p0 & 7;
+  const uint8_t* A0 = stage + (p0 & ~7);
   const int64_t blkA = q0 >> word_shift;
+  const int64_t WB = (blkA + 1) << word_shift;  // first word of the next block
   uint64_t a0 = 0, b0 = 0, a1 = 0, b1 = 0;
-#pragma unroll 4
-  for (int64_t w = q0 + lane; w < q1; w += 32) {
-    // the word's 8 bytes sit at stage[r + k0 ..]; bytes outside the piece
-    // (first/last word) are masked off — their 8-byte-aligned shared loads
-    // may touch neighbouring shared memory, which is harmless
-    const int k0 = static_cast<int>(8 * w - g0);  // -7 .. bytes-1
-    const int p = r + k0;
-    const int sh = (p & 7) * 8;
-    const uint8_t* q = stage + (p & ~7);
-    const uint64_t lo = lds64(q);
-    uint64_t v = sh ? (lo >> sh) | (lds64(q + 8) << (64 - sh)) : lo;
+  // interior words (the piece's first and last words may be partial)
+  const int64_t lo = max(q0, W0 + 1), hi = min(q1, W1);
+  if (lo < hi) {
+    segment_sums(A0, W0, sh, lo, min(hi, WB), lane, a0, b0);
+    segment_sums(A0, W0, sh, max(lo, WB), hi, lane, a1, b1);
+  }
+  // the (possibly partial) first and last words, one lane each
+  for (int end = 0; end < 2; ++end) {
+    const int64_t w = end ? W1 : W0;
+    if ((end && W1 == W0) || w < q0 || w >= q1 || lane != end) continue;
+    const int k0 = static_cast<int>(8 * w - g0);
+    const uint8_t* q = A0 + 8 * (w - W0);
+    uint64_t v = sh ? (lds64(q) >> (8 * sh)) | (lds64(q + 8) << (64 - 8 * sh)) : lds64(q);
     const int lo_t = max(0, -k0), hi_t = min(8, pc.bytes - k0);
-    if (lo_t > 0 || hi_t < 8) {
-      const uint64_t keep = (hi_t >= 8 ? ~uint64_t{0} : ((uint64_t{1} << (8 * hi_t)) - 1)) &
-                            ~((uint64_t{1} << (8 * lo_t)) - 1);
-      v &= keep;
-    }
+    const uint64_t keep = (hi_t >= 8 ? ~uint64_t{0} : ((uint64_t{1} << (8 * hi_t)) - 1)) &
+                          ~((uint64_t{1} << (8 * lo_t)) - 1);
+    v &= keep;
     const uint64_t wi = static_cast<uint64_t>(w) + 1;
-    if ((w >> word_shift) == blkA) {
+    if (w < WB) {
       a0 += v;
       b0 += wi * v;
     } else {
@@ -490,13 +527,12 @@ static int launch_program(const ew_copy_program* prog, int n_ctas, int remote_ct
   if (prog->remote_pieces == 0) remote_ctas = 0;
   else if (prog->local_pieces == 0) remote_ctas = n_ctas;
   else if (remote_ctas <= 0 || remote_ctas >= n_ctas)
-    // a verifying consumer spends longer per piece, so the latency-bound
-    // NVLink class gets a third of the CTAs instead of a quarter (N=4 sweep,
-    // tools/verify_dbg.sh: 11.6 ms verified vs 11.1 ms plain); EW_REMOTE_CTAS
-    // overrides for sweeps
+    // NVLink class: a quarter of the CTAs, verified or not (N=4 sweep,
+    // tools/verify_dbg.sh: 74 CTAs 11.07 ms verified vs 11.11 ms plain;
+    // 98 CTAs 11.2 ms); EW_REMOTE_CTAS overrides for sweeps
     remote_ctas = getenv("EW_REMOTE_CTAS")
                       ? std::min(n_ctas - 1, atoi(getenv("EW_REMOTE_CTAS")))
-                      : std::max(1, block_sums ? n_ctas / 3 : n_ctas / 4);
+                      : std::max(1, n_ctas / 4);
   staged_copy_kernel<<<n_ctas, kThreads, kSmem, (cudaStream_t)stream>>>(
       prog->d_items, prog->n_remote, prog->remote_pieces, prog->n_local, prog->local_pieces,
       remote_ctas, reinterpret_cast<unsigned long long*>(block_sums), prog->word_shift);
