@@ -1120,7 +1120,7 @@ def bench_b200(args):
         run_philox(args, rank, world, out)
     if "reduce" not in skip:
         run_reduce(args, rank, world, out)
-    if rank == 0 and "cpu" not in skip:
+    if world == 1 and rank == 0 and "cpu" not in skip:
         run_cpu_beside(args, out)  # cpu_baseline leg, continued
     if rank == 0:
         line = json.dumps(out)
