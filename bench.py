@@ -559,6 +559,85 @@ def run_reshard(args, rank, world, out):
     torch.cuda.empty_cache()
 
 
+def run_config_c(args, rank, world, out):
+    """Config C at N GPUs: 8B-sized ZeRO state (14.05 GB per GPU), two
+    non-adjacent ranks leave (8->6 drops {2, 5}; 4->2 drops {1, 3}), then
+    rejoin (N-2 -> N).  Each change is one verified pull program per GPU
+    (verification on arrival + block-sum conservation), bytes checked."""
+    import torch
+    import torch.distributed as dist
+    from paper_2510_00606_b200 import configs, device as dev
+    from paper_2510_00606_b200.reshard import ReshardExecutor, ReshardPlan, shard_map
+
+    torch.cuda.empty_cache()
+    base = configs.llama3_8b()
+    lb = base.layer_bytes if world == 8 else [x * world // 8 for x in base.layer_bytes]
+    block = args.block_bytes
+    nblocks = (sum(lb) + block - 1) // block
+    gone = [2, 5] if world == 8 else [1, 3]
+    members = list(range(world))
+    kept = [r for r in members if r not in gone]
+    res = {"state_bytes": int(sum(lb)), "per_gpu_shard_bytes": int(sum(lb) // world)}
+    for label, old, new in (("scale_in", members, kept), ("rejoin", kept, members)):
+        rp = ReshardPlan.build(lb, old, new)
+        ex = ReshardExecutor(rp, rank)
+        bufs = ex.allocate()
+        if bufs.old is not None:
+            dev.fill_synthetic(shard_map(rp.src, rank, block), bufs.old, 8)
+        if bufs.replica is not None:
+            dev.fill_synthetic(shard_map(rp.src, rp.replica_of(rank), block), bufs.replica, 8)
+        before = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+        if bufs.old is not None and rank not in rp.failed:
+            mo = shard_map(rp.src, rank, block)
+            rows = mo.new_row_sums()
+            dev.checksum(mo, bufs.old, rows)
+            dev.rows_to_blocks(mo, rows, before)
+        if bufs.replica is not None:
+            mr = shard_map(rp.src, rp.replica_of(rank), block)
+            rows = mr.new_row_sums()
+            dev.checksum(mr, bufs.replica, rows)
+            dev.rows_to_blocks(mr, rows, before)
+        dist.all_reduce(before)
+        barrier(world)
+        ex.bind(bufs, verify=True, block_bytes=block)
+        after = torch.zeros_like(before)
+        ex.launch(block_sums=after)
+        barrier(world)
+        times = []
+        for _ in range(args.reshard_reps):
+            after.zero_()
+            barrier(world)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            ex.launch(block_sums=after)
+            b.record()
+            barrier(world)
+            times.append(a.elapsed_time(b) / 1e3)
+        t = max_over_ranks([sum(times) / len(times)], world)[0]
+        dist.all_reduce(after)
+        ok = bool(torch.equal(before, after))
+        if bufs.new is not None:
+            n = rp.dst.shard_bytes(rank)
+            exp = dev.empty_bytes(n)
+            dev.fill_synthetic(shard_map(rp.dst, rank, block), exp, 8)
+            ok = ok and bool(torch.equal(bufs.new[:n], exp[:n]))
+            del exp
+        okt = torch.tensor([1 if ok else 0], device="cuda")
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        tr = rp.traffic()
+        bott = tr["bottleneck_bytes"]
+        res[label] = {"change": f"{len(old)}->{len(new)}", "departed": gone if label == "scale_in" else [],
+                      "joined": gone if label == "rejoin" else [],
+                      "copy_ms": round(t * 1e3, 3), "bottleneck_gpu_bytes": bott,
+                      "bottleneck_nvlink_gbs": round(bott / t / 1e9, 1) if bott else None,
+                      "verified_on_arrival_and_bytes": bool(okt.item())}
+        barrier(world)
+        ex.close()
+        del bufs, before, after
+        torch.cuda.empty_cache()
+    out["config_c"] = res
+
+
 def run_stage_move(args, rank, world, out):
     """Cross-stage ZeRO layer move (PAPER Fig. 10): the 7B
     model split over two pipeline stages of DP = world/2; stage 0's tail
@@ -1114,6 +1193,8 @@ def bench_b200(args):
         run_replay(args, rank, world, out)
     if world > 1 and "migration" not in skip:
         run_layer_migration(args, rank, world, out)
+    if world >= 4 and "config_c" not in skip:
+        run_config_c(args, rank, world, out)
     if world > 1 and world % 2 == 0 and "stage" not in skip:
         run_stage_move(args, rank, world, out)
     if "philox" not in skip:
