@@ -123,6 +123,51 @@ def _worker(rank, world, port, result_dir):
             report[f"stage move contiguous={contiguous}"] = bool(torch.equal(bufs.new[:n], exp[:n]))
             ex.close()
             dist.barrier()
+        # staged in-place reshard (config D geometry): OLD and NEW in one
+        # buffer, many phases; every departure, and a rejoin (phases upward)
+        from paper_2510_00606_b200.inplace import StagedInPlaceReshard
+        block = 65536
+        nblk = (cfg.total_bytes + block - 1) // block
+        for drop in range(world):
+            for old, new in ((list(range(world)), [r for r in range(world) if r != drop]),
+                             ([r for r in range(world) if r != drop], list(range(world)))):
+                if len(old) < 1 or len(new) < 1 or (len(old) < 2 and len(new) < len(old)):
+                    continue
+                rp = ReshardPlan.build(cfg.layer_bytes, old, new)
+                sub = dist.new_group(ranks=new)
+                ex = StagedInPlaceReshard(rp, rank, stage_bytes=max(
+                    1 << 16, max(rp.dst.shard_bytes(r) for r in new) // 7), block_bytes=block)
+                bufs = ex.allocate()
+                before = torch.zeros(2 * nblk, dtype=torch.int64, device="cuda")
+                if bufs.old is not None:
+                    mo = shard_map(rp.src, rank, block)
+                    dev.fill_synthetic(mo, bufs.old, 17)
+                    rows = mo.new_row_sums()
+                    dev.checksum(mo, bufs.old, rows)
+                    dev.rows_to_blocks(mo, rows, before)
+                if bufs.replica is not None:
+                    dev.fill_synthetic(shard_map(rp.src, rp.replica_of(rank), block),
+                                       bufs.replica, 17)
+                dist.all_reduce(before)
+                ex.bind(bufs, None, sub if rank in new else None)
+                after = torch.zeros_like(before)
+                torch.cuda.synchronize()
+                dist.barrier()
+                ex.launch(after)
+                torch.cuda.synchronize()
+                dist.all_reduce(after)
+                ok = bool(torch.equal(before, after)) and len(ex.sched.phases) > 2
+                if rank in new:
+                    n = rp.dst.shard_bytes(rank)
+                    exp = dev.empty_bytes(n)
+                    dev.fill_synthetic(shard_map(rp.dst, rank, block), exp, 17)
+                    ok = ok and bool(torch.equal(bufs.new[:n], exp[:n]))
+                    ok = ok and not ex.barrier.timed_out()
+                report[f"in-place {len(old)}->{len(new)} r{drop}"] = ok
+                dist.barrier()
+                ex.close()
+                dist.destroy_process_group(sub)
+                dist.barrier()
         # ring replica refresh: pull the successor's snapshot, verify by rows
         from paper_2510_00606_b200.recovery import RingReplica
         lay = ReshardPlan.build(cfg.layer_bytes, range(world), range(world)).src
