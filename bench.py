@@ -57,6 +57,8 @@ def parse_args():
                    help="config D: per-GPU state for the staged in-place reshard leg (0 = skip)")
     p.add_argument("--inplace-stage-gb", type=float, default=1.0)
     p.add_argument("--inplace-reps", type=int, default=3)
+    p.add_argument("--inplace-phase-gb", type=float, default=2.0)
+    p.add_argument("--inplace-slack", type=int, default=2)
     p.add_argument("--only-inplace", action="store_true",
                    help="run only the snapshot leg and the in-place reshard leg")
     p.add_argument("--skip", default="", help="comma list of: e2e,reshard,philox,reduce,cpu")
@@ -696,7 +698,8 @@ def run_inplace(args, rank, world, out):
     t0 = time.perf_counter()
     rp = ReshardPlan.build(lb, old, new)
     ex = StagedInPlaceReshard(rp, rank, stage_bytes=int(args.inplace_stage_gb * 1e9),
-                              block_bytes=block)
+                              block_bytes=block, phase_bytes=int(args.inplace_phase_gb * 1e9),
+                              slack=args.inplace_slack)
     t_plan = time.perf_counter() - t0
     bufs = ex.allocate()
     nblocks = (sum(lb) + block - 1) // block
@@ -751,7 +754,9 @@ def run_inplace(args, rank, world, out):
         "workload": f"config D fill-HBM {world}->{world - 1} (drop rank {drop}), staged in place",
         "per_gpu_state_bytes": rp.src.shard_bytes(0), "state_bytes": int(sum(lb)),
         "total_bytes_moved": traffic["total_bytes_moved"], "bottleneck_gpu_bytes": bott,
-        "phases": len(sched.phases), "stage_bytes": sched.stage_alloc,
+        "phases": len(sched.phases), "slack": sched.slack,
+        "staging_buffers": sched.ring, "stage_bytes": sched.stage_alloc,
+        "staged_bytes_max_rank": max(sched.staged_bytes.values()),
         "copy_ms": round(t_copy[0] * 1e3, 3), "copy_ms_best": round(t_copy[1] * 1e3, 3),
         "bottleneck_nvlink_gbs": round(bott / t_copy[0] / 1e9, 1) if bott else None,
         "plan_ms": round(t_plan * 1e3, 3), "bind_ms": round(t_bind * 1e3, 3),

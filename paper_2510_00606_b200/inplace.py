@@ -1,39 +1,41 @@
 """Staged in-place reshard for ZeRO state that fills HBM.
 
 The plain executor keeps a rank's OLD shard, the ring replica it holds and
-the NEW shard side by side: about 3.1 S of HBM for a shard of S bytes, so
-a 180 GB B200 reshards at most S ~ 55 GB that way.  Here OLD and NEW share
-one allocation of max(|OLD|, |NEW|) bytes and the move is cut into phases
-over the global byte space, plus two staging buffers of one phase each:
+the NEW shard side by side: about 3.1 S of HBM for a shard of S bytes, so a
+180 GB B200 reshards at most S ~ 55 GB that way.  Here OLD and NEW share one
+allocation of max(|OLD|, |NEW|) bytes, and the move runs in phases over the
+global byte space.
 
-  phase i (global range P_i):
-    gather  every rank pulls the NEW bytes it owns in P_i — from peers' OLD,
-            ring replicas or its own OLD — into staging[i % 2], checksumming
-            what lands (verification on arrival, kernel (a)'s spec labelled by
-            the global position the byte has in NEW);
-    barrier stream-ordered cross-GPU barrier: every rank has finished reading
-            P_i's OLD bytes;
-    flush   staging[i % 2] -> the rank's NEW range of P_i (one local copy,
-            on a second stream, overlapping the next phase's gather).
+Geometry.  A rank's packed offsets are monotone in the global position: for
+a global boundary G let old(G), new(G) be the bytes the rank holds below G
+in OLD and in NEW.  When shards grow (a departure) phases run from the top
+of the global space down, cut only where new(G) >= old(G) on every rank
+(every layer boundary qualifies; cut points inside a layer are tested); when
+shards shrink (a join) they run upwards with new(G) <= old(G).  Phase j in
+processing order reads R_j = [old(G_lo_j), old(G_hi_j)) of every rank's OLD
+and writes W_j = [new(G_lo_j), new(G_hi_j)) of its NEW; with the cut rule,
+the reads of every later phase lie beyond W_j (below it for departures).
 
-Why it is safe.  A rank's packed offsets are monotone in the global
-position: for a boundary G let old(G), new(G) be the packed bytes it holds
-below G in OLD and NEW.  When shards grow (a departure) the phases run from
-the top of the global space down and every boundary satisfies
-new(G) >= old(G) on every surviving rank: then phase i's flush writes
-[new(G_i), new(G_i+1)) while everything still to be read lies below
-old(G_i) <= new(G_i).  When shards shrink (a join) the phases run upwards
-with new(G) <= old(G).  Boundaries are chosen only where that holds for
-every rank (layer boundaries always qualify for N -> N-1; cut points inside
-a layer are tested), phases are grown greedily up to the staging size, and
-`check()` re-verifies the no-overlap property interval by interval.
+Execution, per rank (three streams, `s` = slack):
+  gather_j   waits until every rank finished gather_{j-s-1}, then pulls the
+             phase's NEW bytes (peers' OLD, ring replicas, own OLD): the part
+             of W_j clear of R_{j-s} .. R_j lands DIRECTLY in NEW, the rest in
+             staging[j % (s+2)]; both checksummed on arrival (kernel (a)'s
+             spec, labelled by the byte's global position in NEW);
+  barrier_j  (own stream) stream-ordered cross-GPU barrier after gather_j:
+             every rank has read R_j;
+  flush_j    (own stream) after barrier_j: staging -> its W_j range.
+So ranks run up to s+1 phases apart and only the bytes of the few phases
+whose W_j still overlaps unread OLD bytes (the bottom layers of a departure)
+are staged and copied twice.  `check()` re-verifies every write against every
+read interval by interval.
 
-The reference only models a remap (remap_time, sim.cpp:452-483); the plan
-itself is overlap_matrix (param_fabric.cpp:82-121) via ReshardPlan.
+The reference only models a remap (remap_time, sim.cpp:452-483); the plan is
+overlap_matrix (param_fabric.cpp:82-121) via ReshardPlan.
 """
 from __future__ import annotations
 
-from typing import Dict, List, Optional, Sequence, Tuple
+from typing import Dict, List, Optional, Tuple
 
 import numpy as np
 import torch
@@ -41,6 +43,8 @@ import torch
 from . import device as dev
 from .fabric import ROLE_NEW, ROLE_OLD, ROLE_REPLICA, SEGMENT_DTYPE
 from .reshard import ReshardExecutor, ReshardPlan, RankBuffers
+
+Range = Tuple[int, int]
 
 
 def prefix_bytes(segs: np.ndarray, g) -> np.ndarray:
@@ -53,160 +57,223 @@ def prefix_bytes(segs: np.ndarray, g) -> np.ndarray:
     return np.clip(g[:, None] - lo, 0, ln).sum(axis=1)
 
 
-class InPlaceSchedule:
-    """Phase boundaries and per-rank packed cuts of one staged in-place
-    reshard; identical on every rank (pure function of the plan)."""
+def clip_descs(descs: np.ndarray, lo: int, hi: int, shift: int = 0) -> np.ndarray:
+    """Copy descriptors restricted to destinations in [lo, hi); dst_off moved
+    by -lo + shift (shift = 0 and lo = 0 keep NEW's own offsets)."""
+    d0 = descs["dst_off"].astype(np.int64)
+    d1 = d0 + descs["bytes"].astype(np.int64)
+    a, b = np.maximum(d0, lo), np.minimum(d1, hi)
+    sel = b > a
+    out = descs[sel].copy()
+    out["src_off"] = out["src_off"] + (a[sel] - d0[sel])
+    out["dst_off"] = a[sel] - lo + shift
+    out["bytes"] = b[sel] - a[sel]
+    return out
 
-    def __init__(self, rp: ReshardPlan, stage_bytes: int = 2 << 30):
+
+def clip_segments(segs: np.ndarray, lo: int, hi: int, pad: int) -> np.ndarray:
+    """A segment map restricted to packed offsets [lo, hi), re-based to start
+    at `pad` (a leading pad segment keeps the map packed from 0; nothing is
+    ever landed there)."""
+    a = segs["local_off"].astype(np.int64)
+    b = a + segs["length"].astype(np.int64)
+    x, y = np.maximum(a, lo), np.minimum(b, hi)
+    sel = y > x
+    if not sel.any():
+        return np.zeros(0, dtype=SEGMENT_DTYPE)
+    out = np.zeros(int(sel.sum()) + (1 if pad else 0), dtype=SEGMENT_DTYPE)
+    j = 0
+    if pad:
+        first_g = int(segs["global_lo"][sel][0] + (x[sel][0] - a[sel][0]))
+        out[0] = (first_g - pad, pad, 0)
+        j = 1
+    out["global_lo"][j:] = segs["global_lo"][sel] + (x[sel] - a[sel])
+    out["length"][j:] = y[sel] - x[sel]
+    out["local_off"][j:] = x[sel] - lo + pad
+    return out
+
+
+class InPlaceSchedule:
+    """Phases, per-rank write ranges (direct / staged) and the read ranges
+    they must avoid; identical on every rank (pure function of the plan)."""
+
+    def __init__(self, rp: ReshardPlan, stage_bytes: int = 1 << 30,
+                 phase_bytes: int = 2 << 30, slack: int = 2):
         self.rp = rp
         self.stage_bytes = int(stage_bytes)
+        self.phase_bytes = int(phase_bytes)
+        self.slack = int(slack)
+        self.ring = self.slack + 2           # staging buffers in rotation
         self.total = int(sum(rp.layer_bytes))
-        self.execs = [r for r in rp.new_ranks]
+        self.execs = list(rp.new_ranks)
         self.old_segs = {r: rp.src.segments(r) for r in rp.old_ranks}
         self.new_segs = {r: rp.dst.segments(r) for r in rp.new_ranks}
-        both = [r for r in rp.new_ranks if r in rp.old_ranks and r not in rp.failed]
-        grow = all(rp.dst.shard_bytes(r) >= rp.src.shard_bytes(r) for r in both)
-        shrink = all(rp.dst.shard_bytes(r) <= rp.src.shard_bytes(r) for r in both)
+        # ranks whose OLD is read in place (a departed rank's is not: its
+        # bytes come from the ring replica)
+        self.holders = [r for r in rp.new_ranks if r in rp.old_ranks and r not in rp.failed]
+        grow = all(rp.dst.shard_bytes(r) >= rp.src.shard_bytes(r) for r in self.holders)
+        shrink = all(rp.dst.shard_bytes(r) <= rp.src.shard_bytes(r) for r in self.holders)
         if not (grow or shrink):
             raise ValueError("in-place staging needs every retained shard to grow "
                              "(departures) or every one to shrink (joins)")
         self.descending = grow
 
         # candidate boundaries: layer boundaries plus points inside each layer
-        # spaced so that a rank's share between them is ~ a quarter stage
+        # spaced at ~ a quarter phase of one rank's share; keep the safe ones
         n_new = max(1, len(rp.new_ranks))
-        step = max(4096, self.stage_bytes * n_new // 4)
-        cands = []
-        off = 0
+        step = max(4096, min(self.phase_bytes, self.stage_bytes) * n_new // 4)
+        cands, off = [], 0
         for sz in rp.layer_bytes:
             cands.extend(range(off, off + sz, step))
             off += sz
-        c = np.unique(np.asarray(cands[1:] + [self.total], dtype=np.int64))
+        c = np.unique(np.asarray(cands, dtype=np.int64))
         c = c[(c > 0) & (c < self.total)]
         ok = np.ones(len(c), dtype=bool)
-        for r in both:
+        for r in self.holders:
             d = prefix_bytes(self.new_segs[r], c) - prefix_bytes(self.old_segs[r], c)
             ok &= (d >= 0) if self.descending else (d <= 0)
-        safe = np.concatenate([[0], c[ok], [self.total]])
-        newpos = {r: prefix_bytes(self.new_segs[r], safe) for r in self.execs}
+        safe = np.concatenate([[0], c[ok], [self.total]]).astype(np.int64)
+        # processing order over the safe boundaries
+        order = safe[::-1] if self.descending else safe
+        newp = {r: prefix_bytes(self.new_segs[r], order) for r in self.execs}
+        oldp = {r: prefix_bytes(self.old_segs[r], order) for r in self.holders}
 
-        # greedy phases over the safe boundaries, largest that fits the stage
-        def phase_bytes(i, j):
-            return max((int(abs(newpos[r][j] - newpos[r][i])) for r in self.execs), default=0)
-
-        bounds = []  # indices into `safe`, in processing order
-        if self.descending:
-            hi = len(safe) - 1
-            bounds.append(hi)
-            while hi > 0:
-                lo = hi - 1
-                while lo > 0 and phase_bytes(lo - 1, hi) <= self.stage_bytes:
-                    lo -= 1
-                bounds.append(lo)
-                hi = lo
-        else:
-            lo = 0
-            bounds.append(lo)
-            last = len(safe) - 1
-            while lo < last:
-                hi = lo + 1
-                while hi < last and phase_bytes(lo, hi + 1) <= self.stage_bytes:
-                    hi += 1
-                bounds.append(hi)
-                lo = hi
-        g = [int(safe[b]) for b in bounds]
-        # phases as (glo, ghi), in processing order
-        self.phases: List[Tuple[int, int]] = [
-            (min(a, b), max(a, b)) for a, b in zip(g[:-1], g[1:])]
-        self.cuts: Dict[int, List[Tuple[int, int]]] = {}
+        # greedy phases: grow while every rank's phase share fits phase_bytes
+        # and its staged part fits stage_bytes
+        bounds = [0]                   # indices into `order`
+        self.phases: List[Range] = []  # (glo, ghi), processing order
+        while bounds[-1] < len(order) - 1:
+            a = bounds[-1]
+            b = a + 1
+            while b + 1 < len(order) and self._fits(a, b + 1, bounds, newp, oldp):
+                b += 1
+            bounds.append(b)
+            ga, gb = int(order[a]), int(order[b])
+            self.phases.append((min(ga, gb), max(ga, gb)))
+        n = len(self.phases)
+        # per-rank NEW cut of each phase and the direct / staged split
+        self.cuts: Dict[int, List[Range]] = {}
+        self.staged: Dict[int, List[Range]] = {}
+        self.direct: Dict[int, List[Range]] = {}
         for r in self.execs:
             k = prefix_bytes(self.new_segs[r], [x for p in self.phases for x in p]).reshape(-1, 2)
             self.cuts[r] = [(int(a), int(b)) for a, b in k]
-        biggest = max((b - a for r in self.execs for a, b in self.cuts[r]), default=0)
-        self.stage_alloc = ((biggest + 15 + 255) // 256) * 256
+            self.staged[r], self.direct[r] = [], []
+            for j in range(n):
+                st, di = self._split(r, j)
+                self.staged[r].append(st)
+                self.direct[r].append(di)
+        biggest = max((b - a for r in self.execs for a, b in self.staged[r]), default=0)
+        self.stage_alloc = ((biggest + 15 + 255) // 256) * 256 if biggest else 0
+        self.staged_bytes = {r: sum(b - a for a, b in self.staged[r]) for r in self.execs}
         self.check()
+
+    # -------------------------------------------------------------- geometry
+    def _threshold(self, r: int, j: int, gbounds=None) -> int:
+        """Packed OLD offset on rank r separating what gather_j may write
+        directly from what it must stage: the reads of phases j-s .. j (and
+        any later) lie below it (departures) / above it (joins)."""
+        k = j - self.slack
+        if self.descending:
+            if k < 0:
+                return int(self.rp.src.shard_bytes(r))
+            ghi = self.phases[k][1] if gbounds is None else gbounds[k][1]
+            return int(prefix_bytes(self.old_segs[r], [ghi])[0])
+        if k < 0:
+            return 0
+        glo = self.phases[k][0] if gbounds is None else gbounds[k][0]
+        return int(prefix_bytes(self.old_segs[r], [glo])[0])
+
+    def _split(self, r: int, j: int) -> Tuple[Range, Range]:
+        k_lo, k_hi = self.cuts[r][j]
+        if r not in self.holders:          # nobody reads this rank's buffer
+            return (k_lo, k_lo), (k_lo, k_hi)
+        t = self._threshold(r, j)
+        if self.descending:
+            m = min(max(t, k_lo), k_hi)
+            return (k_lo, m), (m, k_hi)
+        m = max(min(t, k_hi), k_lo)
+        return (m, k_hi), (k_lo, m)
+
+    def _fits(self, a: int, b: int, bounds, newp, oldp) -> bool:
+        j = len(bounds) - 1            # index of the phase being grown
+        for r in self.execs:
+            lo, hi = sorted((int(newp[r][a]), int(newp[r][b])))
+            if hi - lo > self.phase_bytes:
+                return False
+            if r in self.holders:
+                k = j - self.slack
+                if self.descending:
+                    t = int(self.rp.src.shard_bytes(r)) if k < 0 else int(oldp[r][bounds[k]])
+                    staged = max(0, min(hi, t) - lo)
+                else:
+                    t = 0 if k < 0 else int(oldp[r][bounds[k]])
+                    staged = max(0, hi - max(lo, t))
+                if staged > self.stage_bytes:
+                    return False
+        return True
 
     # ---------------------------------------------------------------- checks
     def check(self) -> None:
-        """Phase i's flush on rank r writes NEW[cut_i]; nothing a later phase
-        reads from r's OLD (its own gathers or its peers') may lie there."""
-        rp = self.rp
+        """Every write against every read it could race with:
+        gather_j's direct writes vs the reads of phases >= j - slack;
+        flush_j's writes vs the reads of phases > j (on the same rank's OLD)."""
+        n = len(self.phases)
         for r in self.execs:
-            if r not in rp.old_ranks or r in rp.failed:
+            if r not in self.holders:
                 continue
             o = self.old_segs[r]
-            for i, (k_lo, k_hi) in enumerate(self.cuts[r]):
-                for glo, ghi in self.phases[i + 1:]:
-                    a, b = prefix_bytes(o, [glo, ghi])
-                    if a < b and a < k_hi and k_lo < b:
-                        raise AssertionError(
-                            f"rank {r}: phase {i} flush [{k_lo},{k_hi}) overlaps OLD bytes "
-                            f"[{a},{b}) a later phase reads")
+            reads = [tuple(int(x) for x in prefix_bytes(o, list(p))) for p in self.phases]
+            for j in range(n):
+                for what, (lo, hi), first in (("direct", self.direct[r][j], j - self.slack),
+                                              ("staged", self.staged[r][j], j + 1)):
+                    if hi <= lo:
+                        continue
+                    for k in range(max(0, first), n):
+                        a, b = reads[k]
+                        if a < b and a < hi and lo < b:
+                            raise AssertionError(
+                                f"rank {r}: phase {j} {what} write [{lo},{hi}) overlaps OLD "
+                                f"bytes [{a},{b}) phase {k} reads")
 
     # ------------------------------------------------------------ programs
     @staticmethod
-    def _pad(k_lo: int) -> int:
-        return k_lo % 16  # staging keeps NEW's alignment mod 16 (bulk stores)
+    def pad(k: int) -> int:
+        return k % 16  # staging keeps NEW's alignment mod 16 (bulk stores)
 
-    def phase_descs(self, rank: int, i: int, descs: Optional[np.ndarray] = None) -> np.ndarray:
-        """This rank's pull descriptors restricted to phase i, re-targeted to
-        the staging buffer (dst_off relative to the phase's NEW cut + pad)."""
-        if descs is None:
-            descs = self.rp.copies(rank, push=False)
-        k_lo, k_hi = self.cuts[rank][i]
-        pad = self._pad(k_lo)
-        d0 = descs["dst_off"].astype(np.int64)
-        d1 = d0 + descs["bytes"].astype(np.int64)
-        lo = np.maximum(d0, k_lo)
-        hi = np.minimum(d1, k_hi)
-        sel = hi > lo
-        out = descs[sel].copy()
-        shift = lo[sel] - d0[sel]
-        out["src_off"] = out["src_off"] + shift
-        out["dst_off"] = lo[sel] - k_lo + pad
-        out["bytes"] = hi[sel] - lo[sel]
-        return out
+    def direct_descs(self, rank: int, j: int, descs: np.ndarray) -> np.ndarray:
+        lo, hi = self.direct[rank][j]
+        return clip_descs(descs, lo, hi, lo)
 
-    def phase_segments(self, rank: int, i: int) -> np.ndarray:
-        """NEW's segment map clipped to phase i, as laid out in staging."""
-        k_lo, k_hi = self.cuts[rank][i]
-        pad = self._pad(k_lo)
-        segs = self.new_segs[rank]
-        a = segs["local_off"].astype(np.int64)
-        b = a + segs["length"].astype(np.int64)
-        lo, hi = np.maximum(a, k_lo), np.minimum(b, k_hi)
-        sel = hi > lo
-        if not sel.any():
-            return np.zeros(0, dtype=SEGMENT_DTYPE)
-        out = np.zeros(int(sel.sum()) + (1 if pad else 0), dtype=SEGMENT_DTYPE)
-        j = 0
-        if pad:
-            first_g = int(segs["global_lo"][sel][0] + (lo[sel][0] - a[sel][0]))
-            out[0] = (first_g - pad, pad, 0)  # nothing lands here
-            j = 1
-        out["global_lo"][j:] = segs["global_lo"][sel] + (lo[sel] - a[sel])
-        out["length"][j:] = hi[sel] - lo[sel]
-        out["local_off"][j:] = lo[sel] - k_lo + pad
-        return out
+    def staged_descs(self, rank: int, j: int, descs: np.ndarray) -> np.ndarray:
+        lo, hi = self.staged[rank][j]
+        return clip_descs(descs, lo, hi, self.pad(lo))
+
+    def staged_segments(self, rank: int, j: int) -> np.ndarray:
+        lo, hi = self.staged[rank][j]
+        return clip_segments(self.new_segs[rank], lo, hi, self.pad(lo))
 
 
 class StagedInPlaceReshard:
     """One rank's executor of an InPlaceSchedule (one process per GPU).
 
     Buffers: `buf` (OLD on entry, NEW on exit; max(|OLD|, |NEW|) bytes), the
-    ring replica when this rank holds a departed rank's replica, and two
-    staging buffers of `schedule.stage_alloc` bytes."""
+    ring replica when this rank holds a departed rank's replica, and
+    `schedule.ring` staging buffers of `schedule.stage_alloc` bytes."""
 
-    def __init__(self, rp: ReshardPlan, rank: int, stage_bytes: int = 2 << 30,
-                 block_bytes: int = dev.DEFAULT_BLOCK_BYTES):
+    def __init__(self, rp: ReshardPlan, rank: int, stage_bytes: int = 1 << 30,
+                 block_bytes: int = dev.DEFAULT_BLOCK_BYTES, phase_bytes: int = 2 << 30,
+                 slack: int = 2):
         self.rp = rp
         self.rank = rank
         self.block_bytes = block_bytes
-        self.sched = InPlaceSchedule(rp, stage_bytes)
+        self.sched = InPlaceSchedule(rp, stage_bytes, phase_bytes, slack)
         self.n_old = rp.src.shard_bytes(rank) if rank in rp.old_ranks else 0
         self.n_new = rp.dst.shard_bytes(rank) if rank in rp.new_ranks else 0
-        self.gathers: List[dev.CopyProgram] = []
-        self.flushes: List[dev.CopyProgram] = []
+        self.direct: List[Optional[dev.CopyProgram]] = []
+        self.staged: List[Optional[dev.CopyProgram]] = []
+        self.flushes: List[Optional[dev.CopyProgram]] = []
+        self.staging: List[torch.Tensor] = []
         self._base: Optional[ReshardExecutor] = None
         self.barrier: Optional[dev.PeerBarrier] = None
 
@@ -224,66 +291,92 @@ class StagedInPlaceReshard:
 
     def bind(self, bufs: RankBuffers, group=None, survivors_group=None) -> None:
         """Collective over `group`: map peers' OLD/REPLICA (as in steady
-        state), build every phase's verified gather and its flush.
+        state) and build every phase's verified gathers and flush.
         `survivors_group`: the process group of the NEW members (barrier)."""
         self._base = ReshardExecutor(self.rp, self.rank, push=False)
         self._base.premap(bufs, group)
         if self.rank not in self.rp.new_ranks:
             return
+        sc, r = self.sched, self.rank
         self.barrier = dev.PeerBarrier(survivors_group)
-        sa = self.sched.stage_alloc
-        self.staging = [dev.empty_bytes(sa), dev.empty_bytes(sa)]
+        self.staging = [dev.empty_bytes(sc.stage_alloc) for _ in range(sc.ring)] \
+            if sc.stage_alloc else []
         table = dict(self._base._table)
-        if bufs.old is not None:
-            table[(ROLE_OLD, self.rank)] = bufs.old.data_ptr()
-        if bufs.replica is not None:
-            table[(ROLE_REPLICA, self.rank)] = bufs.replica.data_ptr()
+        for role, t in ((ROLE_OLD, bufs.old), (ROLE_REPLICA, bufs.replica),
+                        (ROLE_NEW, bufs.new)):
+            if t is not None:
+                table[(role, r)] = t.data_ptr()
         import torch.distributed as dist
         world = dist.get_world_size(group)
         n_table = max(max(self.rp.old_ranks + self.rp.new_ranks) + 1, world)
-        descs = self.rp.copies(self.rank, push=False)
-        self.gathers, self.flushes = [], []
-        for i in range(len(self.sched.phases)):
-            st = self.staging[i % 2]
-            t = dict(table)
-            t[(ROLE_NEW, self.rank)] = st.data_ptr()
-            pd = self.sched.phase_descs(self.rank, i, descs)
-            vmap = dev.ShardMap(self.sched.phase_segments(self.rank, i), self.block_bytes)
-            self.gathers.append(dev.CopyProgram.from_descs(pd, t, n_table, self.rank, vmap))
-            k_lo, k_hi = self.sched.cuts[self.rank][i]
-            pad = InPlaceSchedule._pad(k_lo)
-            self.flushes.append(dev.CopyProgram.from_pointers(
-                [st.data_ptr() + pad], [self.buf.data_ptr() + k_lo], [k_hi - k_lo], [False]))
+        descs = self.rp.copies(r, push=False)
+        full_map = dev.ShardMap(sc.new_segs[r], self.block_bytes)
+        self.direct, self.staged, self.flushes = [], [], []
+        for j in range(len(sc.phases)):
+            d = sc.direct_descs(r, j, descs)
+            self.direct.append(dev.CopyProgram.from_descs(d, table, n_table, r, full_map)
+                               if len(d) else None)
+            lo, hi = sc.staged[r][j]
+            if hi > lo:
+                st = self.staging[j % sc.ring]
+                t = dict(table)
+                t[(ROLE_NEW, r)] = st.data_ptr()
+                vmap = dev.ShardMap(sc.staged_segments(r, j), self.block_bytes)
+                self.staged.append(dev.CopyProgram.from_descs(sc.staged_descs(r, j, descs), t,
+                                                              n_table, r, vmap))
+                self.flushes.append(dev.CopyProgram.from_pointers(
+                    [st.data_ptr() + sc.pad(lo)], [self.buf.data_ptr() + lo], [hi - lo],
+                    [False]))
+            else:
+                self.staged.append(None)
+                self.flushes.append(None)
+        self.sync_stream = torch.cuda.Stream()
         self.flush_stream = torch.cuda.Stream()
 
-    def launch(self, block_sums: torch.Tensor, stream=None, flush_ctas: int = 32) -> None:
-        """Enqueue the whole reshard on `stream` (+ the flush stream).  The
+    def launch(self, block_sums: torch.Tensor, stream=None, n_ctas: int = 0,
+               flush_ctas: int = 64) -> None:
+        """Enqueue the whole reshard (gathers on `stream`, barriers and
+        flushes on their own streams, joined back into `stream`).  The
         caller zeroes block_sums and all-reduces them afterwards."""
         if self.rank not in self.rp.new_ranks:
             return
+        sc = self.sched
         main = stream or torch.cuda.current_stream()
-        fs = self.flush_stream
+        ys, fs = self.sync_stream, self.flush_stream
+        ys.wait_stream(main)
         fs.wait_stream(main)
-        done: List[torch.cuda.Event] = []
-        for i, (g, f) in enumerate(zip(self.gathers, self.flushes)):
-            if i >= 2:
-                main.wait_event(done[i - 2])      # staging[i % 2] flushed
-            g.launch(stream=main, block_sums=block_sums)
-            self.barrier.wait(stream=main)        # every rank read P_i's OLD bytes
-            ev = torch.cuda.Event()
-            ev.record(main)
-            fs.wait_event(ev)
-            f.launch(flush_ctas, 0, stream=fs)
-            d = torch.cuda.Event()
-            d.record(fs)
-            done.append(d)
-        if done:
-            main.wait_event(done[-1])
-            if len(done) > 1:
-                main.wait_event(done[-2])
+        bar: List[torch.cuda.Event] = []
+        flushed: List[Optional[torch.cuda.Event]] = []
+        for j in range(len(sc.phases)):
+            k = j - sc.slack - 1
+            if k >= 0:
+                main.wait_event(bar[k])             # every rank finished gather_k
+            if j >= sc.ring and flushed[j - sc.ring] is not None:
+                main.wait_event(flushed[j - sc.ring])  # staging buffer free again
+            if self.staged[j] is not None:
+                self.staged[j].launch(n_ctas, 0, stream=main, block_sums=block_sums)
+            if self.direct[j] is not None:
+                self.direct[j].launch(n_ctas, 0, stream=main, block_sums=block_sums)
+            g = torch.cuda.Event()
+            g.record(main)
+            ys.wait_event(g)
+            self.barrier.wait(stream=ys)             # every rank has read R_j
+            b = torch.cuda.Event()
+            b.record(ys)
+            bar.append(b)
+            if self.flushes[j] is not None:
+                fs.wait_event(b)
+                self.flushes[j].launch(flush_ctas, 0, stream=fs)
+                f = torch.cuda.Event()
+                f.record(fs)
+                flushed.append(f)
+            else:
+                flushed.append(None)
+        main.wait_stream(ys)
+        main.wait_stream(fs)
 
     def close(self) -> None:
-        self.gathers, self.flushes = [], []
+        self.direct, self.staged, self.flushes = [], [], []
         if self.barrier is not None:
             self.barrier.close()
             self.barrier = None

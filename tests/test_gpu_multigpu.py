@@ -135,8 +135,9 @@ def _worker(rank, world, port, result_dir):
                     continue
                 rp = ReshardPlan.build(cfg.layer_bytes, old, new)
                 sub = dist.new_group(ranks=new)
-                ex = StagedInPlaceReshard(rp, rank, stage_bytes=max(
-                    1 << 16, max(rp.dst.shard_bytes(r) for r in new) // 7), block_bytes=block)
+                stage = max(1 << 16, max(rp.dst.shard_bytes(r) for r in new) // 7)
+                ex = StagedInPlaceReshard(rp, rank, stage_bytes=stage, block_bytes=block,
+                                          phase_bytes=2 * stage, slack=1 + drop % 2)
                 bufs = ex.allocate()
                 before = torch.zeros(2 * nblk, dtype=torch.int64, device="cuda")
                 if bufs.old is not None:

@@ -1,10 +1,10 @@
 """Staged in-place reshard (paper_2510_00606_b200/inplace.py), executed on the
 host by a numpy byte mover with the real aliasing: each rank holds ONE
-buffer that is its OLD shard on entry and its NEW shard on exit.  Every
-phase runs all ranks' gathers (reading peers' buffers as the earlier
-phases' flushes left them), then all flushes — the worst interleaving the
-GPU's barrier + flush stream allow — so a flush that clobbered bytes a later
-phase still reads shows up as a wrong target byte."""
+buffer that is its OLD shard on entry and its NEW shard on exit.  Phases run
+in the adversarial order the GPU's streams allow (run-ahead gathers' direct
+writes land before a phase reads, flushes right after its barrier), so a
+write that clobbered bytes some phase still reads shows up as a wrong target
+byte; `check()` is the independent interval-level proof."""
 import numpy as np
 import pytest
 
@@ -35,6 +35,9 @@ def _small(cfg):
 
 
 def _simulate(rp, sched, oracle):
+    """Adversarial order: before phase j's gathers read, the gathers of phases
+    j+1 .. j+slack (which may run ahead) have already written their direct
+    ranges — poisoned here, so any read they could clobber is caught."""
     bufs, reps = {}, {}
     for r in sorted(set(rp.old_ranks) | set(rp.new_ranks)):
         n_old = rp.src.shard_bytes(r) if r in rp.old_ranks else 0
@@ -47,41 +50,47 @@ def _simulate(rp, sched, oracle):
         if rep is not None and rep in rp.failed and r not in rp.failed:
             reps[r] = oracle.fill_synthetic(rp.src.segments(rep), rp.src.shard_bytes(rep), SEED)
     landed = {r: 0 for r in rp.new_ranks}
-    for i, (glo, ghi) in enumerate(sched.phases):
+    descs = {r: rp.copies(r, push=False) for r in rp.new_ranks}
+    n = len(sched.phases)
+    for j in range(n):
+        for r in rp.new_ranks:
+            for jj in range(j + 1, min(n, j + sched.slack + 1)):
+                lo, hi = sched.direct[r][jj]
+                bufs[r][lo:hi] = 0xEE
         staged = {}
         for r in rp.new_ranks:
-            st = np.full(sched.stage_alloc, 0x5A, dtype=np.uint8)
-            for c in sched.phase_descs(r, i):
-                s = int(c["src_rank"])
-                assert s not in rp.failed
-                src = bufs[s] if int(c["src_role"]) == ROLE_OLD else reps[s]
-                assert int(c["src_role"]) in (ROLE_OLD, ROLE_REPLICA)
-                n, so, do = int(c["bytes"]), int(c["src_off"]), int(c["dst_off"])
-                assert do + n <= sched.stage_alloc
-                st[do:do + n] = src[so:so + n]
-                landed[r] += n
-            # the phase's segment map labels staging exactly like NEW
-            segs = sched.phase_segments(r, i)
-            k_lo, k_hi = sched.cuts[r][i]
-            pad = k_lo % 16
-            if k_hi > k_lo:
-                want = oracle.fill_synthetic(segs, pad + k_hi - k_lo, SEED)
-                assert np.array_equal(st[pad:pad + k_hi - k_lo], want[pad:]), (r, i)
+            st = np.full(max(16, sched.stage_alloc), 0x5A, dtype=np.uint8)
+            for part, target in ((sched.staged_descs(r, j, descs[r]), st),
+                                 (sched.direct_descs(r, j, descs[r]), bufs[r])):
+                for c in part:
+                    s = int(c["src_rank"])
+                    assert s not in rp.failed
+                    assert int(c["src_role"]) in (ROLE_OLD, ROLE_REPLICA)
+                    src = bufs[s] if int(c["src_role"]) == ROLE_OLD else reps[s]
+                    nb, so, do = int(c["bytes"]), int(c["src_off"]), int(c["dst_off"])
+                    assert do + nb <= len(target)
+                    target[do:do + nb] = src[so:so + nb]
+                    landed[r] += nb
+            lo, hi = sched.staged[r][j]
+            if hi > lo:
+                # the staged segment map labels staging exactly like NEW
+                pad = lo % 16
+                want = oracle.fill_synthetic(sched.staged_segments(r, j), pad + hi - lo, SEED)
+                assert np.array_equal(st[pad:pad + hi - lo], want[pad:]), (r, j)
             staged[r] = st
-        for r in rp.new_ranks:
-            k_lo, k_hi = sched.cuts[r][i]
-            pad = k_lo % 16
-            bufs[r][k_lo:k_hi] = staged[r][pad:pad + k_hi - k_lo]
+        for r in rp.new_ranks:  # barrier_j, then flush_j
+            lo, hi = sched.staged[r][j]
+            bufs[r][lo:hi] = staged[r][lo % 16:lo % 16 + hi - lo]
     return bufs, landed
 
 
 @pytest.mark.parametrize("name,cfg,old,new", CASES, ids=[c[0] for c in CASES])
-@pytest.mark.parametrize("stage_div", [3, 40])
-def test_inplace_reconstructs_target_bytes(name, cfg, old, new, stage_div, oracle):
+@pytest.mark.parametrize("stage_div,slack", [(3, 0), (40, 2), (40, 0), (11, 5)])
+def test_inplace_reconstructs_target_bytes(name, cfg, old, new, stage_div, slack, oracle):
     small = _small(cfg)
     rp = ReshardPlan.build(small.layer_bytes, old, new)
     stage = max(256, max(rp.dst.shard_bytes(r) for r in rp.new_ranks) // stage_div)
-    sched = InPlaceSchedule(rp, stage)
+    sched = InPlaceSchedule(rp, stage, phase_bytes=2 * stage, slack=slack)
     assert sched.descending == (len(new) < len(old))
     # phases tile the global space, in processing order
     gl = sorted(sched.phases)
@@ -102,13 +111,18 @@ def test_inplace_fits_fill_hbm_where_side_by_side_does_not():
     # two stages in place (2.33 S + 4 GB) vs OLD + replica + NEW (3.33 S)
     S = 74_000_000_000
     rp = ReshardPlan.build(configs.fill_hbm(4, S).layer_bytes, range(4), [0, 1, 2])
-    sched = InPlaceSchedule(rp, 2 << 30)
+    sched = InPlaceSchedule(rp, 1 << 30)
     holder = 2  # holds the departed r3's replica
     in_place = (max(rp.src.shard_bytes(holder), rp.dst.shard_bytes(holder))
-                + rp.src.shard_bytes(3) + 2 * sched.stage_alloc)
+                + rp.src.shard_bytes(3) + sched.ring * sched.stage_alloc)
     side_by_side = rp.src.shard_bytes(holder) + rp.src.shard_bytes(3) + rp.dst.shard_bytes(holder)
     assert in_place < 180e9 < side_by_side
-    assert sched.stage_alloc <= (2 << 30) + 256
+    # a phase is staged only up to the stage size, or one layer's share where
+    # no safe cut exists inside the layer (the bottom layers)
+    layer_share = max(rp.layer_bytes) // 3 + 1
+    assert sched.stage_alloc <= max(1 << 30, layer_share) + 256
+    # only the bottom layers' phases are staged (copied twice)
+    assert sched.staged_bytes[holder] < 0.15 * rp.dst.shard_bytes(holder)
     # layer boundaries are always safe cut points for a departure
     for r in rp.new_ranks:
         off = np.cumsum([0] + list(rp.layer_bytes))
@@ -119,11 +133,12 @@ def test_inplace_fits_fill_hbm_where_side_by_side_does_not():
 def test_check_rejects_an_unsafe_schedule():
     small = _small(configs.llama2_7b())
     rp = ReshardPlan.build(small.layer_bytes, range(8), [0, 1, 2, 4, 5, 6, 7])
-    sched = InPlaceSchedule(rp, 1 << 12)
-    # process the same phases bottom-up: the first flush lands on OLD bytes
-    # a later (higher) phase still reads
-    sched.phases = sched.phases[::-1]
-    for r in sched.cuts:
-        sched.cuts[r] = sched.cuts[r][::-1]
+    sched = InPlaceSchedule(rp, 1 << 12, phase_bytes=1 << 13, slack=1)
+    assert sum(sched.staged_bytes.values()) > 0
+    # write everything directly: the bottom phases then land on OLD bytes
+    # that the same or a run-ahead phase still reads
+    for r in sched.execs:
+        sched.direct[r] = list(sched.cuts[r])
+        sched.staged[r] = [(a, a) for a, _ in sched.cuts[r]]
     with pytest.raises(AssertionError):
         sched.check()
