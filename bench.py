@@ -57,8 +57,9 @@ def parse_args():
                    help="config D: per-GPU state for the staged in-place reshard leg (0 = skip)")
     p.add_argument("--inplace-stage-gb", type=float, default=1.0)
     p.add_argument("--inplace-reps", type=int, default=3)
-    p.add_argument("--inplace-phase-gb", type=float, default=2.0)
-    p.add_argument("--inplace-slack", type=int, default=2)
+    p.add_argument("--inplace-phase-gb", type=float, default=4.0)
+    p.add_argument("--inplace-slack", type=int, default=1)
+    p.add_argument("--inplace-gather-streams", type=int, default=2)
     p.add_argument("--only-inplace", action="store_true",
                    help="run only the snapshot leg and the in-place reshard leg")
     p.add_argument("--skip", default="", help="comma list of: e2e,reshard,philox,reduce,cpu")
@@ -727,7 +728,7 @@ def run_inplace(args, rank, world, out):
         barrier(world)
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         s.record(stream)
-        ex.launch(after)
+        ex.launch(after, gather_streams=args.inplace_gather_streams)
         e.record(stream)
         barrier(world)
         times.append(s.elapsed_time(e) / 1e3)
@@ -755,6 +756,7 @@ def run_inplace(args, rank, world, out):
         "per_gpu_state_bytes": rp.src.shard_bytes(0), "state_bytes": int(sum(lb)),
         "total_bytes_moved": traffic["total_bytes_moved"], "bottleneck_gpu_bytes": bott,
         "phases": len(sched.phases), "slack": sched.slack,
+        "gather_streams": args.inplace_gather_streams,
         "staging_buffers": sched.ring, "stage_bytes": sched.stage_alloc,
         "staged_bytes_max_rank": max(sched.staged_bytes.values()),
         "copy_ms": round(t_copy[0] * 1e3, 3), "copy_ms_best": round(t_copy[1] * 1e3, 3),

@@ -262,8 +262,11 @@ class StagedInPlaceReshard:
     `schedule.ring` staging buffers of `schedule.stage_alloc` bytes."""
 
     def __init__(self, rp: ReshardPlan, rank: int, stage_bytes: int = 1 << 30,
-                 block_bytes: int = dev.DEFAULT_BLOCK_BYTES, phase_bytes: int = 2 << 30,
-                 slack: int = 2):
+                 block_bytes: int = dev.DEFAULT_BLOCK_BYTES, phase_bytes: int = 4 << 30,
+                 slack: int = 1):
+        # defaults from the config D sweep (profiles/r01_config_d_inplace_sweep_70gb.log):
+        # 4 GB phases, slack 1, two gather streams: 66.9 ms vs 72-85 ms for
+        # 1-2 GB phases or one gather stream
         self.rp = rp
         self.rank = rank
         self.block_bytes = block_bytes
@@ -332,33 +335,40 @@ class StagedInPlaceReshard:
                 self.flushes.append(None)
         self.sync_stream = torch.cuda.Stream()
         self.flush_stream = torch.cuda.Stream()
+        self.gather_streams: List[torch.cuda.Stream] = []
 
     def launch(self, block_sums: torch.Tensor, stream=None, n_ctas: int = 0,
-               flush_ctas: int = 64) -> None:
-        """Enqueue the whole reshard (gathers on `stream`, barriers and
-        flushes on their own streams, joined back into `stream`).  The
-        caller zeroes block_sums and all-reduces them afterwards."""
+               flush_ctas: int = 64, gather_streams: int = 2) -> None:
+        """Enqueue the whole reshard: gathers alternate over `gather_streams`
+        streams (`stream` first) so one phase's tail overlaps the next
+        phase's start, barriers and flushes run on their own streams, and
+        everything is joined back into `stream`.  The caller zeroes
+        block_sums and all-reduces them afterwards."""
         if self.rank not in self.rp.new_ranks:
             return
         sc = self.sched
         main = stream or torch.cuda.current_stream()
+        while len(self.gather_streams) < gather_streams - 1:
+            self.gather_streams.append(torch.cuda.Stream())
+        gs = [main] + self.gather_streams[:max(0, gather_streams - 1)]
         ys, fs = self.sync_stream, self.flush_stream
-        ys.wait_stream(main)
-        fs.wait_stream(main)
+        for st in gs[1:] + [ys, fs]:
+            st.wait_stream(main)
         bar: List[torch.cuda.Event] = []
         flushed: List[Optional[torch.cuda.Event]] = []
         for j in range(len(sc.phases)):
+            g_s = gs[j % len(gs)]
             k = j - sc.slack - 1
             if k >= 0:
-                main.wait_event(bar[k])             # every rank finished gather_k
+                g_s.wait_event(bar[k])              # every rank finished gather_k
             if j >= sc.ring and flushed[j - sc.ring] is not None:
-                main.wait_event(flushed[j - sc.ring])  # staging buffer free again
+                g_s.wait_event(flushed[j - sc.ring])  # staging buffer free again
             if self.staged[j] is not None:
-                self.staged[j].launch(n_ctas, 0, stream=main, block_sums=block_sums)
+                self.staged[j].launch(n_ctas, 0, stream=g_s, block_sums=block_sums)
             if self.direct[j] is not None:
-                self.direct[j].launch(n_ctas, 0, stream=main, block_sums=block_sums)
+                self.direct[j].launch(n_ctas, 0, stream=g_s, block_sums=block_sums)
             g = torch.cuda.Event()
-            g.record(main)
+            g.record(g_s)
             ys.wait_event(g)
             self.barrier.wait(stream=ys)             # every rank has read R_j
             b = torch.cuda.Event()
@@ -372,8 +382,8 @@ class StagedInPlaceReshard:
                 flushed.append(f)
             else:
                 flushed.append(None)
-        main.wait_stream(ys)
-        main.wait_stream(fs)
+        for st in gs[1:] + [ys, fs]:
+            main.wait_stream(st)
 
     def close(self) -> None:
         self.direct, self.staged, self.flushes = [], [], []
