@@ -9,7 +9,9 @@
 #pragma once
 
 #include <cstdint>
+#include <map>
 #include <set>
+#include <utility>
 #include <vector>
 
 #include "elaskit/dataflow.hpp"
@@ -66,6 +68,49 @@ struct CopyDesc {
 std::vector<CopyDesc> reshard_copies(const TransferPlan& plan, const PartitionLayout& src,
                                      const PartitionLayout& dst, const std::set<int>& failed,
                                      const SnapshotRing* ring, int exec_rank, bool push);
+
+// Staged in-place reshard (state that fills HBM).
+// Each rank keeps ONE buffer that holds its OLD shard on entry and its NEW
+// shard on exit; the move runs in phases over the global byte space.  Phases
+// are cut only where every rank that keeps its OLD bytes in place has
+// new_prefix(G) >= old_prefix(G) (departures, phases run downwards) or <=
+// (joins, upwards), so the OLD bytes later phases read lie beyond each
+// phase's NEW range.  Per phase and rank, `direct` is the part of the NEW
+// range clear of the OLD bytes phases j-slack .. j still read (written in
+// place by gather_j once every rank finished gather_{j-slack-1}) and
+// `staged` the rest (gathered into a staging buffer, flushed after the
+// phase's cross-GPU barrier).  Offsets are packed NEW offsets; phases are
+// global [lo, hi) in processing order.
+using ByteRange = std::pair<std::int64_t, std::int64_t>;
+
+struct InPlaceRanges {
+  std::vector<ByteRange> cut, direct, staged;  // one per phase
+};
+
+struct InPlaceSchedule {
+  bool descending = true;
+  int slack = 1;
+  int ring = 3;                          // staging buffers in rotation (slack + 2)
+  std::vector<ByteRange> phases;         // global ranges, processing order
+  std::map<int, InPlaceRanges> ranks;    // every member of the target layout
+  std::vector<int> holders;              // members whose OLD is read in place
+  std::int64_t stage_alloc = 0;          // bytes per staging buffer (0: none)
+};
+
+// Greedy phases over the safe cut points (layer boundaries of layer_bytes,
+// plus points inside a layer that pass the prefix test), each as large as
+// phase_bytes of NEW per rank and stage_bytes of staged bytes allow.
+// Throws std::invalid_argument when shards neither all grow nor all shrink,
+// CoverageMismatch if check_inplace fails (it is run before returning).
+InPlaceSchedule inplace_schedule(const std::vector<std::int64_t>& layer_bytes,
+                                 const PartitionLayout& src, const PartitionLayout& dst,
+                                 const std::set<int>& failed, std::int64_t stage_bytes,
+                                 std::int64_t phase_bytes, int slack);
+
+// Every write against every read it could race with: gather_j's direct
+// writes vs the OLD reads of phases >= j - slack, flush_j's writes vs the
+// reads of phases > j.  Throws CoverageMismatch naming the first overlap.
+void check_inplace(const InPlaceSchedule& s, const PartitionLayout& src);
 
 // Sample offsets of micro-batch 0 whose owning slot changes between two
 // assignments — the SampleReassignment list recover_elaswave derives before

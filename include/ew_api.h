@@ -127,6 +127,25 @@ int ew_reshard_copies(const ew_plan* plan, const ew_layout* src, const ew_layout
                       const int* failed, int n_failed, const int* ring_members, int n_ring,
                       int exec_rank, int push, ew_copy_desc* out, int64_t cap, int64_t* n_out);
 
+/* Staged in-place reshard schedule (b200.hpp inplace_schedule; config D):
+ * OLD and NEW share one buffer per rank, the plan's copies run in phases.
+ * Phases are global [lo, hi) pairs in processing order; per rank and phase,
+ * `cut` is the packed NEW range, `direct` the part gather_j writes in place,
+ * `staged` the part it stages and flushes after the phase's barrier.
+ * Ranges of a rank are arrays of 2 * n_phases int64.  ew_inplace_schedule
+ * fails with EW_ERR_INVALID_ARGUMENT when shards neither all grow nor all
+ * shrink, EW_ERR_COVERAGE_MISMATCH if the hazard check fails. */
+typedef struct ew_inplace ew_inplace;
+int ew_inplace_schedule(const int64_t* layer_bytes, int n_layers, const ew_layout* src,
+                        const ew_layout* dst, const int* failed, int n_failed,
+                        int64_t stage_bytes, int64_t phase_bytes, int slack, ew_inplace** out);
+int ew_inplace_info(const ew_inplace* s, int* descending, int* slack, int* ring,
+                    int64_t* n_phases, int64_t* stage_alloc);
+int ew_inplace_phases(const ew_inplace* s, int64_t* out);
+int ew_inplace_ranges(const ew_inplace* s, int rank, int64_t* cut, int64_t* direct,
+                      int64_t* staged);
+void ew_inplace_free(ew_inplace* s);
+
 /* ------------------------------------------------------------------------
  * Host planners of the other hot-path modules
  * ---------------------------------------------------------------------- */

@@ -166,6 +166,11 @@ _sig("ew_plan_entries", i32, vp, P(TransferEntry), i64)
 _sig("ew_plan_to_json", i32, vp, C.c_char_p, i64, P(i64))
 _sig("ew_reshard_copies", i32, vp, vp, vp, P(i32), i32, P(i32), i32, i32, i32, P(CopyDesc), i64,
      P(i64))
+_sig("ew_inplace_schedule", i32, P(i64), i32, vp, vp, P(i32), i32, i64, i64, i32, P(vp))
+_sig("ew_inplace_info", i32, vp, P(i32), P(i32), P(i32), P(i64), P(i64))
+_sig("ew_inplace_phases", i32, vp, P(i64))
+_sig("ew_inplace_ranges", i32, vp, i32, P(i64), P(i64), P(i64))
+_sig("ew_inplace_free", None, vp)
 _sig("ew_reshard_microbatches", i32, P(i32), i32, i32, P(i32), i32, P(i32), P(i32))
 _sig("ew_weighted_grad_average", i32, P(f64), P(f64), i32, i64, P(f64))
 _sig("ew_sample_reassignments", i32, P(i32), P(i32), i32, P(i32), P(i32), i32, P(i64), i64, P(i64))

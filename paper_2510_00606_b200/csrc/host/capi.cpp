@@ -26,6 +26,10 @@ struct ew_plan {
   elaskit::TransferPlan plan;
 };
 
+struct ew_inplace {
+  elaskit::b200::InPlaceSchedule s;
+};
+
 namespace {
 
 using ew::set_error;
@@ -259,6 +263,65 @@ int ew_reshard_copies(const ew_plan* plan, const ew_layout* src, const ew_layout
                : EW_OK;
   });
 }
+
+int ew_inplace_schedule(const int64_t* layer_bytes, int n_layers, const ew_layout* src,
+                        const ew_layout* dst, const int* failed, int n_failed,
+                        int64_t stage_bytes, int64_t phase_bytes, int slack, ew_inplace** out) {
+  return guarded([&]() -> int {
+    if (out == nullptr || src == nullptr || dst == nullptr || n_layers < 0 ||
+        (n_layers > 0 && layer_bytes == nullptr))
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_inplace_schedule: bad arguments");
+    *out = nullptr;
+    auto* h = new ew_inplace{elaskit::b200::inplace_schedule(
+        std::vector<int64_t>(layer_bytes, layer_bytes + n_layers), src->layout, dst->layout,
+        to_set(failed, n_failed), stage_bytes, phase_bytes, slack)};
+    *out = h;
+    return EW_OK;
+  });
+}
+
+int ew_inplace_info(const ew_inplace* s, int* descending, int* slack, int* ring,
+                    int64_t* n_phases, int64_t* stage_alloc) {
+  if (s == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL schedule");
+  if (descending) *descending = s->s.descending ? 1 : 0;
+  if (slack) *slack = s->s.slack;
+  if (ring) *ring = s->s.ring;
+  if (n_phases) *n_phases = static_cast<int64_t>(s->s.phases.size());
+  if (stage_alloc) *stage_alloc = s->s.stage_alloc;
+  return EW_OK;
+}
+
+int ew_inplace_phases(const ew_inplace* s, int64_t* out) {
+  if (s == nullptr || (out == nullptr && !s->s.phases.empty()))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_inplace_phases: bad arguments");
+  for (std::size_t j = 0; j < s->s.phases.size(); ++j) {
+    out[2 * j] = s->s.phases[j].first;
+    out[2 * j + 1] = s->s.phases[j].second;
+  }
+  return EW_OK;
+}
+
+int ew_inplace_ranges(const ew_inplace* s, int rank, int64_t* cut, int64_t* direct,
+                      int64_t* staged) {
+  if (s == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL schedule");
+  const auto it = s->s.ranks.find(rank);
+  if (it == s->s.ranks.end())
+    return set_error(EW_ERR_INVALID_ARGUMENT, "rank " + std::to_string(rank) +
+                                                  " is not in the target layout");
+  const auto put = [](const std::vector<elaskit::b200::ByteRange>& v, int64_t* o) {
+    if (o == nullptr) return;
+    for (std::size_t j = 0; j < v.size(); ++j) {
+      o[2 * j] = v[j].first;
+      o[2 * j + 1] = v[j].second;
+    }
+  };
+  put(it->second.cut, cut);
+  put(it->second.direct, direct);
+  put(it->second.staged, staged);
+  return EW_OK;
+}
+
+void ew_inplace_free(ew_inplace* s) { delete s; }
 
 int ew_reshard_microbatches(const int* old_per_slot_mbs, int n_old, int num_microbatches,
                             const int* survivors, int n_survivors, int* out_slots,

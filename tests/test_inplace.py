@@ -13,6 +13,8 @@ from paper_2510_00606_b200.fabric import ROLE_OLD, ROLE_REPLICA
 from paper_2510_00606_b200.inplace import InPlaceSchedule, prefix_bytes
 from paper_2510_00606_b200.reshard import ReshardPlan
 
+from inplace_restatement import InPlaceRestatement
+
 SEED = 7
 
 CASES = [
@@ -98,6 +100,16 @@ def test_inplace_reconstructs_target_bytes(name, cfg, old, new, stage_div, slack
     assert all(a[1] == b[0] for a, b in zip(gl[:-1], gl[1:]))
     order = [p[0] for p in sched.phases]
     assert order == sorted(order, reverse=sched.descending)
+    sched.check()
+    # the C++ planner and the independent numpy restatement agree exactly
+    ref = InPlaceRestatement(rp, stage, phase_bytes=2 * stage, slack=slack)
+    assert (sched.descending, sched.slack, sched.ring, sched.stage_alloc) == \
+        (ref.descending, ref.slack, ref.ring, ref.stage_alloc)
+    assert sched.phases == ref.phases
+    for r in rp.new_ranks:
+        assert sched.cuts[r] == ref.cuts[r]
+        assert sched.direct[r] == ref.direct[r]
+        assert sched.staged[r] == ref.staged[r]
     bufs, landed = _simulate(rp, sched, oracle)
     for r in rp.new_ranks:
         n = rp.dst.shard_bytes(r)
@@ -142,3 +154,17 @@ def test_check_rejects_an_unsafe_schedule():
         sched.staged[r] = [(a, a) for a, _ in sched.cuts[r]]
     with pytest.raises(AssertionError):
         sched.check()
+
+
+def test_schedule_errors():
+    from paper_2510_00606_b200._native import CoverageMismatch
+    small = _small(configs.gpt_125m())
+    rp = ReshardPlan.build(small.layer_bytes, [0, 1, 2, 3], [0, 2, 3])
+    with pytest.raises(ValueError):
+        InPlaceSchedule(rp, 0)
+    sched = InPlaceSchedule(rp, 1 << 16, phase_bytes=1 << 17, slack=0)
+    assert sched.ring == 2 and len(sched.phases) > 3
+    # layer bytes that do not describe the layouts
+    rp.layer_bytes = rp.layer_bytes[:-1]
+    with pytest.raises(CoverageMismatch):
+        InPlaceSchedule(rp, 1 << 16)
