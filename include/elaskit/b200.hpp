@@ -107,6 +107,12 @@ InPlaceSchedule inplace_schedule(const std::vector<std::int64_t>& layer_bytes,
                                  const std::set<int>& failed, std::int64_t stage_bytes,
                                  std::int64_t phase_bytes, int slack);
 
+// Rank's pull copies restricted to NEW offsets [lo, hi), destination offsets
+// moved by -lo + shift (the staged part of a phase: shift = lo % 16 into a
+// staging buffer; the direct part: shift = lo keeps NEW's own offsets).
+std::vector<CopyDesc> clip_copies(const std::vector<CopyDesc>& copies, std::int64_t lo,
+                                  std::int64_t hi, std::int64_t shift);
+
 // Every write against every read it could race with: gather_j's direct
 // writes vs the OLD reads of phases >= j - slack, flush_j's writes vs the
 // reads of phases > j.  Throws CoverageMismatch naming the first overlap.

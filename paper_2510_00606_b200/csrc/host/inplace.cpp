@@ -181,6 +181,21 @@ InPlaceSchedule inplace_schedule(const std::vector<std::int64_t>& layer_bytes,
   return s;
 }
 
+std::vector<CopyDesc> clip_copies(const std::vector<CopyDesc>& copies, std::int64_t lo,
+                                  std::int64_t hi, std::int64_t shift) {
+  std::vector<CopyDesc> out;
+  for (const CopyDesc& c : copies) {
+    const std::int64_t a = std::max(c.dst_off, lo), b = std::min(c.dst_off + c.bytes, hi);
+    if (b <= a) continue;
+    CopyDesc d = c;
+    d.src_off = c.src_off + (a - c.dst_off);
+    d.dst_off = a - lo + shift;
+    d.bytes = b - a;
+    out.push_back(d);
+  }
+  return out;
+}
+
 void check_inplace(const InPlaceSchedule& s, const PartitionLayout& src) {
   const long n = static_cast<long>(s.phases.size());
   for (const int r : s.holders) {

@@ -319,3 +319,80 @@ class StagedInPlaceReshard:
             self._base.close()
             self._base = None
         self.staging = []
+
+
+def emulate_inplace_on_one_gpu(rp: ReshardPlan, seed: int, stage_bytes: int, phase_bytes: int,
+                               slack: int, block_sums: Optional[torch.Tensor],
+                               block_bytes: int = dev.DEFAULT_BLOCK_BYTES):
+    """Every rank's in-place programs on the current GPU (one buffer per rank,
+    OLD on entry, NEW on exit), phase by phase in the adversarial order the
+    multi-GPU executor allows: the direct ranges of the run-ahead phases
+    j+1 .. j+slack are poisoned before phase j reads, the flush follows the
+    phase (the barrier is the stream order).  Returns (NEW views, expected)."""
+    sc = InPlaceSchedule(rp, stage_bytes, phase_bytes, slack)
+    ranks = sorted(set(rp.old_ranks) | set(rp.new_ranks))
+    bufs, reps = {}, {}
+    for r in ranks:
+        n_old = rp.src.shard_bytes(r) if r in rp.old_ranks else 0
+        n_new = rp.dst.shard_bytes(r) if r in rp.new_ranks else 0
+        bufs[r] = dev.empty_bytes(max(n_old, n_new, 1))
+        bufs[r].fill_(0xA5)
+        if n_old and r not in rp.failed:
+            dev.fill_synthetic(dev.ShardMap(rp.src.segments(r), block_bytes), bufs[r], seed)
+        rep = rp.replica_of(r)
+        if rep is not None and rep in rp.failed and r not in rp.failed:
+            reps[r] = dev.empty_bytes(rp.src.shard_bytes(rep))
+            dev.fill_synthetic(dev.ShardMap(rp.src.segments(rep), block_bytes), reps[r], seed)
+    staging = {r: [dev.empty_bytes(max(16, sc.stage_alloc)) for _ in range(sc.ring)]
+               for r in rp.new_ranks}
+    table = {(ROLE_OLD, r): bufs[r].data_ptr() for r in ranks}
+    table.update({(ROLE_REPLICA, r): t.data_ptr() for r, t in reps.items()})
+    n_table = max(ranks) + 1
+    progs = {}
+    for r in rp.new_ranks:
+        descs = rp.copies(r, push=False)
+        full = dev.ShardMap(sc.new_segs[r], block_bytes) if block_sums is not None else None
+        t_new = dict(table)
+        t_new[(ROLE_NEW, r)] = bufs[r].data_ptr()
+        for j in range(len(sc.phases)):
+            d = sc.direct_descs(r, j, descs)
+            direct = dev.CopyProgram.from_descs(d, t_new, n_table, r, full) if len(d) else None
+            staged = flush = None
+            lo, hi = sc.staged[r][j]
+            if hi > lo:
+                st = staging[r][j % sc.ring]
+                t = dict(table)
+                t[(ROLE_NEW, r)] = st.data_ptr()
+                staged = dev.CopyProgram.from_descs(
+                    sc.staged_descs(r, j, descs), t, n_table, r,
+                    dev.ShardMap(sc.staged_segments(r, j), block_bytes)
+                    if block_sums is not None else None)
+                flush = dev.CopyProgram.from_pointers([st.data_ptr() + sc.pad(lo)],
+                                                      [bufs[r].data_ptr() + lo], [hi - lo],
+                                                      [False])
+            progs[(r, j)] = (direct, staged, flush)
+    n = len(sc.phases)
+    for j in range(n):
+        for r in rp.new_ranks:
+            for jj in range(j + 1, min(n, j + sc.slack + 1)):
+                lo, hi = sc.direct[r][jj]
+                if hi > lo:
+                    bufs[r][lo:hi].fill_(0xEE)
+        for r in rp.new_ranks:
+            direct, staged, _ = progs[(r, j)]
+            for p in (staged, direct):
+                if p is not None:
+                    p.launch(block_sums=block_sums)
+        for r in rp.new_ranks:
+            flush = progs[(r, j)][2]
+            if flush is not None:
+                flush.launch(64, 0)
+    torch.cuda.synchronize()
+    got, expected = {}, {}
+    for r in rp.new_ranks:
+        n_new = rp.dst.shard_bytes(r)
+        got[r] = bufs[r][:n_new]
+        e = dev.empty_bytes(n_new)
+        dev.fill_synthetic(dev.ShardMap(rp.dst.segments(r), block_bytes), e, seed)
+        expected[r] = e[:n_new]
+    return got, expected, sc

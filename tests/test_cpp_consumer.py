@@ -54,12 +54,14 @@ def test_cpp_recovery_driver_builds():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("d,failed", [(4, 1), (8, 3), (8, 0), (3, 2)])
-def test_cpp_recovery_driver_runs(d, failed):
+@pytest.mark.parametrize("d,failed,mode", [(4, 1, ""), (8, 3, ""), (8, 0, ""), (3, 2, ""),
+                                           (8, 3, "inplace"), (4, 0, "inplace")])
+def test_cpp_recovery_driver_runs(d, failed, mode):
     import json
     subprocess.run(["make", "-s", "-C", str(ROOT / "tools" / "cpp")], check=True)
-    out = subprocess.run([str(ROOT / "tools" / "cpp" / "recover_demo"), str(d), str(failed), "0.01"],
-                         capture_output=True, text=True, timeout=600)
+    args = [str(ROOT / "tools" / "cpp" / "recover_demo"), str(d), str(failed), "0.01"]
+    out = subprocess.run(args + ([mode] if mode else []), capture_output=True, text=True,
+                         timeout=600)
     assert out.returncode == 0, out.stdout + out.stderr
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["conserved"] and res["bytes_ok"]

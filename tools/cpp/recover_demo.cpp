@@ -11,7 +11,11 @@
 //      synthetic state, run every program, verify by checksum conservation
 //      and by regenerating the expected target bytes.
 //
-//   recover_demo [D=4] [failed=1] [scale=0.02]
+//   recover_demo [D=4] [failed=1] [scale=0.02] [inplace]
+//
+// "inplace": the staged in-place variant (b200::inplace_schedule) — each
+// rank keeps ONE buffer (OLD on entry, NEW on exit); per phase every rank's
+// direct and staged copies run, then the staged bytes are flushed.
 #include <cuda_runtime.h>
 
 #include <chrono>
@@ -19,6 +23,7 @@
 #include <cstdlib>
 #include <map>
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "elaskit/device.hpp"
@@ -69,6 +74,8 @@ void add_blocks(const PartitionLayout& l, int rank, const void* buf, std::uint64
   cudaFree(rows);
 }
 
+int holder_of(const SnapshotRing& ring, int r) { return ring.backed_up_by(r); }
+
 }  // namespace
 
 int main(int argc, char** argv) {
@@ -101,6 +108,110 @@ int main(int argc, char** argv) {
   }
   const TransferPlan plan = overlap_matrix(src, dst, failed, &ring);
   const auto t1 = std::chrono::steady_clock::now();
+
+  const bool in_place = argc > 4 && std::string(argv[4]) == "inplace";
+  if (in_place) {
+    const b200::InPlaceSchedule sc = b200::inplace_schedule(
+        z.layer_bytes, src, dst, failed, /*stage=*/1 << 20, /*phase=*/2 << 20, /*slack=*/1);
+    std::map<int, std::unique_ptr<Buffer>> buf;
+    std::vector<void*> tab(3 * D, nullptr);
+    for (int r : old_ranks) {
+      const std::int64_t n = std::max(b200::shard_bytes(src, r), b200::shard_bytes(dst, r));
+      buf[r] = std::make_unique<Buffer>(n);
+      if (!failed.count(r)) fill(src, r, buf[r]->p, 7);
+      tab[0 * D + r] = buf[r]->p;
+    }
+    Buffer replica(b200::shard_bytes(src, failed_rank));
+    fill(src, failed_rank, replica.p, 7);
+    tab[1 * D + holder_of(ring, failed_rank)] = replica.p;
+    const std::int64_t n_blocks = (src.total_bytes + 65535) / 65536;
+    std::uint64_t* before = nullptr;
+    cuda(cudaMalloc(&before, 16 * n_blocks), "malloc");
+    cudaMemset(before, 0, 16 * n_blocks);
+    for (int r : old_ranks)
+      if (!failed.count(r)) add_blocks(src, r, buf[r]->p, before, n_blocks);
+    add_blocks(src, failed_rank, replica.p, before, n_blocks);
+    // one staging buffer per rank: phases run one after another here (the
+    // multi-GPU executor rotates sc.ring of them to let ranks run ahead)
+    std::map<int, std::unique_ptr<Buffer>> staging;
+    for (int r : new_ranks)
+      staging[r] = std::make_unique<Buffer>(std::max<std::int64_t>(16, sc.stage_alloc));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a);
+    int programs = 0;
+    for (std::size_t j = 0; j < sc.phases.size(); ++j) {
+      std::vector<std::unique_ptr<device::CopyProgram>> keep;
+      std::vector<ew_copy_program*> flushes;
+      for (int r : new_ranks) {
+        const auto copies = b200::reshard_copies(plan, src, dst, failed, &ring, r, false);
+        const b200::InPlaceRanges& rr = sc.ranks.at(r);
+        // direct part: lands in NEW at its own offsets
+        std::vector<void*> t = tab;
+        t[2 * D + r] = buf[r]->p;
+        const auto d = b200::clip_copies(copies, rr.direct[j].first, rr.direct[j].second,
+                                         rr.direct[j].first);
+        if (!d.empty()) {
+          keep.push_back(std::make_unique<device::CopyProgram>(d, t, D, r));
+          keep.back()->launch(nullptr);
+        }
+        // staged part: into staging (alignment kept mod 16), flushed once
+        // every rank has gathered the phase (the barrier)
+        const auto [lo, hi] = rr.staged[j];
+        if (hi > lo) {
+          void* st = staging[r]->p;
+          std::vector<void*> ts = tab;
+          ts[2 * D + r] = st;
+          keep.push_back(std::make_unique<device::CopyProgram>(
+              b200::clip_copies(copies, lo, hi, lo % 16), ts, D, r));
+          keep.back()->launch(nullptr);
+          const void* fs[1] = {static_cast<char*>(st) + lo % 16};
+          void* fd[1] = {static_cast<char*>(buf[r]->p) + lo};
+          const std::int64_t fb[1] = {hi - lo};
+          const int rem[1] = {0};
+          ew_copy_program* flush = nullptr;
+          device::check(ew_copy_program_create_raw(fs, fd, fb, rem, 1, &flush));
+          flushes.push_back(flush);
+        }
+      }
+      programs += static_cast<int>(keep.size() + flushes.size());
+      for (ew_copy_program* f : flushes) device::check(ew_copy_program_launch(f, 64, 0, nullptr));
+      cuda(cudaDeviceSynchronize(), "phase");
+      for (ew_copy_program* f : flushes) ew_copy_program_free(f);
+    }
+    cudaEventRecord(b);
+    cuda(cudaEventSynchronize(b), "in-place");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    std::uint64_t* after = nullptr;
+    cuda(cudaMalloc(&after, 16 * n_blocks), "malloc");
+    cudaMemset(after, 0, 16 * n_blocks);
+    for (int r : new_ranks) add_blocks(dst, r, buf[r]->p, after, n_blocks);
+    std::vector<std::uint64_t> hb(2 * n_blocks), ha(2 * n_blocks);
+    cudaMemcpy(hb.data(), before, 16 * n_blocks, cudaMemcpyDeviceToHost);
+    cudaMemcpy(ha.data(), after, 16 * n_blocks, cudaMemcpyDeviceToHost);
+    const bool conserved = hb == ha;
+    bool bytes_ok = true;
+    for (int r : new_ranks) {
+      const std::int64_t n = b200::shard_bytes(dst, r);
+      Buffer expect(n);
+      fill(dst, r, expect.p, 7);
+      std::vector<unsigned char> x(n), y(n);
+      cudaMemcpy(x.data(), buf[r]->p, n, cudaMemcpyDeviceToHost);
+      cudaMemcpy(y.data(), expect.p, n, cudaMemcpyDeviceToHost);
+      bytes_ok = bytes_ok && x == y;
+    }
+    std::printf("{\"D\": %d, \"failed\": %d, \"mode\": \"inplace\", \"state_bytes\": %lld, "
+                "\"phases\": %zu, \"programs\": %d, \"stage_alloc\": %lld, \"ms\": %.3f, "
+                "\"conserved\": %s, \"bytes_ok\": %s}\n",
+                D, failed_rank, static_cast<long long>(src.total_bytes), sc.phases.size(), programs,
+                static_cast<long long>(sc.stage_alloc), ms, conserved ? "true" : "false",
+                bytes_ok ? "true" : "false");
+    cudaFree(before);
+    cudaFree(after);
+    return conserved && bytes_ok ? 0 : 1;
+  }
 
   // buffers: OLD (role 0), REPLICA (role 1, ring holder of the failed rank), NEW (role 2)
   std::map<std::pair<int, int>, std::unique_ptr<Buffer>> bufs;
