@@ -17,6 +17,7 @@ from pathlib import Path
 
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -82,6 +83,27 @@ def main():
             f = lambda: None
         t = timed(f)
         emit({"test": "kernel pull", "ctas": ctas, "GBps": round(n / t / 1e9, 1)})
+
+    # misaligned source (realign path) and verification on arrival
+    from paper_2510_00606_b200.fabric import SEGMENT_DTYPE, ROLE_NEW, ROLE_OLD
+    from paper_2510_00606_b200.fabric import COPY_DTYPE
+    m = n - 4096
+    seg = np.zeros(1, dtype=SEGMENT_DTYPE)
+    seg[0] = (0, m, 0)
+    vmap = dev.ShardMap(seg, 65536)
+    sums = torch.zeros(2 * ((m + 65535) // 65536), dtype=torch.int64, device="cuda")
+    for shift, verify in ((0, False), (8, False), (3, False), (0, True), (8, True)):
+        if rank == 1:
+            d = np.zeros(1, dtype=COPY_DTYPE)
+            d[0] = (ROLE_OLD, 0, ROLE_NEW, 1, shift, 0, m)
+            tbl = {(ROLE_OLD, 0): peer, (ROLE_NEW, 1): dst.data_ptr()}
+            p = dev.CopyProgram.from_descs(d, tbl, 2, 1, vmap if verify else None)
+            f = (lambda: p.launch(block_sums=sums)) if verify else (lambda: p.launch())
+        else:
+            f = lambda: None
+        t = timed(f)
+        emit({"test": "kernel pull (descriptor)", "src_shift": shift, "verified": verify,
+              "GBps": round(m / t / 1e9, 1)})
 
     for streams in (1, 2, 4):
         ss = [main_s] + [torch.cuda.Stream() for _ in range(streams - 1)]
