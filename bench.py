@@ -62,7 +62,9 @@ def parse_args():
     p.add_argument("--inplace-gather-streams", type=int, default=2)
     p.add_argument("--only-inplace", action="store_true",
                    help="run only the snapshot leg and the in-place reshard leg")
-    p.add_argument("--skip", default="", help="comma list of: e2e,reshard,philox,reduce,cpu")
+    p.add_argument("--skip", default="",
+                   help="comma list of: e2e,cpu,inplace,reshard,replica,replay,migration,"
+                        "config_c,stage,philox,reduce")
     p.add_argument("--json-out", default="")
     return p.parse_args()
 
@@ -690,8 +692,13 @@ def run_inplace(args, rank, world, out):
 
     torch.cuda.empty_cache()
     torch.cuda.reset_peak_memory_stats()
-    S = int(args.inplace_state_gb * 1e9)
-    lb = configs.fill_hbm(world, S).layer_bytes
+    if args.inplace_state_gb > 0:   # config D geometry, S bytes per GPU
+        lb = configs.fill_hbm(world, int(args.inplace_state_gb * 1e9)).layer_bytes
+        geometry = "config D fill-HBM"
+    else:                           # the reshard leg's 7B-per-GPU state, for comparison
+        base = configs.llama2_7b()
+        lb = base.layer_bytes if world == 8 else [x * world // 8 for x in base.layer_bytes]
+        geometry = "llama2-7b per GPU"
     drop = min(3, world - 1)
     old = list(range(world))
     new = [r for r in old if r != drop]
@@ -752,7 +759,7 @@ def run_inplace(args, rank, world, out):
     bott = traffic["bottleneck_bytes"]
     sched = ex.sched
     out["inplace"] = {
-        "workload": f"config D fill-HBM {world}->{world - 1} (drop rank {drop}), staged in place",
+        "workload": f"{geometry} {world}->{world - 1} (drop rank {drop}), staged in place",
         "per_gpu_state_bytes": rp.src.shard_bytes(0), "state_bytes": int(sum(lb)),
         "total_bytes_moved": traffic["total_bytes_moved"], "bottleneck_gpu_bytes": bott,
         "phases": len(sched.phases), "slack": sched.slack,
@@ -1324,7 +1331,7 @@ def bench_b200(args):
         run_e2e(args, rank, world, out, m, live, snap, rows, bad, S)
     del live, snap
     torch.cuda.empty_cache()
-    if world > 1 and args.inplace_state_gb > 0:
+    if world > 1 and (args.inplace_state_gb > 0 or "inplace" not in skip):
         run_inplace(args, rank, world, out)
     if world == 1 and rank == 0 and "cpu" not in skip:
         run_cpu_baseline(args, out, segs, S)
