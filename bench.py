@@ -57,7 +57,8 @@ def parse_args():
                    help="config D: per-GPU state for the staged in-place reshard leg (0 = skip)")
     p.add_argument("--inplace-stage-gb", type=float, default=1.0)
     p.add_argument("--inplace-reps", type=int, default=3)
-    p.add_argument("--inplace-phase-gb", type=float, default=4.0)
+    p.add_argument("--inplace-phase-gb", type=float, default=0.0,
+                   help="0: the executor's default (largest NEW shard / 28)")
     p.add_argument("--inplace-slack", type=int, default=1)
     p.add_argument("--inplace-gather-streams", type=int, default=2)
     p.add_argument("--only-inplace", action="store_true",
@@ -706,7 +707,8 @@ def run_inplace(args, rank, world, out):
     t0 = time.perf_counter()
     rp = ReshardPlan.build(lb, old, new)
     ex = StagedInPlaceReshard(rp, rank, stage_bytes=int(args.inplace_stage_gb * 1e9),
-                              block_bytes=block, phase_bytes=int(args.inplace_phase_gb * 1e9),
+                              block_bytes=block,
+                              phase_bytes=int(args.inplace_phase_gb * 1e9) or None,
                               slack=args.inplace_slack)
     t_plan = time.perf_counter() - t0
     bufs = ex.allocate()

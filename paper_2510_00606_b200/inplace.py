@@ -187,11 +187,16 @@ class StagedInPlaceReshard:
     `schedule.ring` staging buffers of `schedule.stage_alloc` bytes."""
 
     def __init__(self, rp: ReshardPlan, rank: int, stage_bytes: int = 1 << 30,
-                 block_bytes: int = dev.DEFAULT_BLOCK_BYTES, phase_bytes: int = 4 << 30,
-                 slack: int = 1):
-        # defaults from the config D sweep (profiles/r01_config_d_inplace_sweep_70gb.log):
-        # 4 GB phases, slack 1, two gather streams: 66.9 ms vs 72-85 ms for
-        # 1-2 GB phases or one gather stream
+                 block_bytes: int = dev.DEFAULT_BLOCK_BYTES,
+                 phase_bytes: Optional[int] = None, slack: int = 1):
+        # defaults from the sweeps (profiles/r01_config_d_inplace_sweep_70gb.log,
+        # profiles/r01_inplace_sweep_7b_4gpu.log): slack 1, two gather streams
+        # and ~28 phases — smaller phases stage less of the bottom layers,
+        # each phase costs a launch tail (config D 70 GB: 4 GB phases 66.9 ms
+        # vs 1-2 GB 69-85 ms; 7B per GPU: 0.5 GB 11.7 ms vs 2 GB 12.9 ms)
+        if phase_bytes is None:
+            biggest = max(rp.dst.shard_bytes(r) for r in rp.new_ranks)
+            phase_bytes = min(8 << 30, max(256 << 20, biggest // 28))
         self.rp = rp
         self.rank = rank
         self.block_bytes = block_bytes
