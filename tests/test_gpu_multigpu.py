@@ -243,6 +243,31 @@ def _worker(rank, world, port, result_dir):
         dist.barrier()
         dev.ipc_close(p1)
         rep.close()
+        # toy consistency across real ranks: one slot per GPU, the last rank
+        # leaves before step 2, survivors reshape and sum on the shrunk NCCL
+        # communicator; final parameters equal the static run bit for bit
+        from paper_2510_00606_b200.toy import ToyConfig, ToyRun
+        tcfg = ToyConfig(dp=world, global_batch=2 * world, steps=4)
+        uid = [dev.Communicator.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        tcomm = dev.Communicator.init(uid[0], world, rank)
+        state = {"comm": tcomm, "shrunk": False}
+
+        def toy_reduce(total, members):
+            if len(members) < world and not state["shrunk"]:
+                state["comm"] = tcomm.shrink([world - 1])
+                state["shrunk"] = True
+            state["comm"].allreduce_i64(total)
+
+        got = ToyRun(tcfg, {2: [world - 1]}).run(toy_reduce, my_slots=[rank])
+        if rank != world - 1:
+            static = ToyRun(tcfg).run()
+            report["toy elastic == static (NCCL, shrunk)"] = bool(torch.equal(
+                got.view(torch.int64), static.view(torch.int64)))
+        dist.barrier()
+        if state["shrunk"] and state["comm"] is not None:
+            state["comm"].destroy()
+        tcomm.destroy()
         # full DP recovery of the last rank (recovery.DpGroup): plan_edit +
         # ncclCommShrink, reshape, remap, checksum verification
         from paper_2510_00606_b200.recovery import DpGroup
