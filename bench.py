@@ -231,6 +231,20 @@ def run_snapshot(args, rank, world, local, out):
     bytes_step = 3 * S
     peak, peak_kind = measured_peaks()
     achieved = 2 * S / t_snap / 1e9
+    # the plain-copy ceiling of the same bytes on this GPU, measured live after
+    # the timed region (cudaMemcpyAsync D2D via torch copy_, best of 3): at
+    # this size it runs above MEASURED_PEAKS' 2 GiB copy figure
+    # (profiles/r01_snapshot_size_probe.log), so the fused kernel is also
+    # graded against it
+    t_copy = 1e30
+    for _ in range(4):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        snap.copy_(live)
+        b.record(stream)
+        torch.cuda.synchronize()
+        t_copy = min(t_copy, a.elapsed_time(b) / 1e3)
+    copy_gbs = max_over_ranks([-2 * S / t_copy / 1e9], world)[0] * -1  # min over ranks
     out.update({
         "metric": METRIC, "value": round(world * bytes_step / step / 1e9, 2), "unit": "GB/s",
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": round(step * 1e3, 4),
@@ -251,6 +265,8 @@ def run_snapshot(args, rank, world, local, out):
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "frac_of_8tbs_spec": round(achieved / 8000.0, 4),
+                     "plain_copy_gbs": round(copy_gbs, 1),
+                     "frac_of_plain_copy": round(achieved / copy_gbs, 4),
                      "traffic": profiled_traffic("snapshot_7b")},
         "clocks": clk, "gpu_launches": 2 * K,
     })
