@@ -1373,7 +1373,7 @@ def bench_b200(args):
         run_cpu_beside(args, out)  # cpu_baseline leg, continued
     if rank == 0:
         line = json.dumps(out)
-        print(line, flush=True)
+        emit(line)
         if args.json_out:
             Path(args.json_out).write_text(line + "\n")
     if world > 1:
@@ -1430,12 +1430,33 @@ def bench_reference(args):
         extra["weighted_grad_average_gbs_1thread"] = round(5 * 4_194_304 * 8 / dt / 1e9, 2)
         res["reference_cpu"] = extra
         res["cpu_baseline"]["reference_planner"] = "oracle/_ref (unmodified reference sources)"
-    print(json.dumps(res), flush=True)
+    emit(json.dumps(res))
     if args.json_out:
         Path(args.json_out).write_text(json.dumps(res) + "\n")
 
 
+_JSON_FD = None
+
+
+def quiet_stdout():
+    """Route fd 1 to stderr for the whole run, so banners printed by native
+    libraries (NCCL's version line at communicator init) cannot precede the
+    JSON line; emit() writes that one line to the original stdout."""
+    global _JSON_FD
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
+
+
+def emit(line):
+    if _JSON_FD is None:
+        print(line, flush=True)
+    else:
+        os.write(_JSON_FD, (line + "\n").encode())
+
+
 def main():
+    quiet_stdout()
     args = parse_args()
     if args.impl == "reference":
         bench_reference(args)

@@ -77,8 +77,32 @@ struct Piece {
   int64_t glob;        // global position of dst[0], or -1
 };
 
-__device__ __forceinline__ Piece piece_at(const CopyItem* list, int64_t n_items, int64_t p) {
-  const CopyItem it = list[item_of_piece(list, n_items, p)];
+// The producer's pieces increase (first + k * step), so the item they fall
+// in only moves forward: keep it and the next item's first piece in
+// registers and touch the item list only when a piece crosses into a new
+// item (a binary search per piece is ~log2(items) dependent L2 loads, a
+// bubble in the producer's issue loop).
+struct ItemCursor {
+  int64_t idx = -1;
+  int64_t next_base = 0;
+  CopyItem it{};
+
+  __device__ __forceinline__ const CopyItem& at(const CopyItem* list, int64_t n, int64_t p) {
+    if (idx < 0) {
+      idx = item_of_piece(list, n, p);
+      it = list[idx];
+      next_base = idx + 1 < n ? list[idx + 1].piece_base : INT64_MAX;
+    }
+    while (p >= next_base) {
+      ++idx;
+      it = list[idx];
+      next_base = idx + 1 < n ? list[idx + 1].piece_base : INT64_MAX;
+    }
+    return it;
+  }
+};
+
+__device__ __forceinline__ Piece piece_at(const CopyItem& it, int64_t p) {
   const uint64_t d = reinterpret_cast<uintptr_t>(it.dst);
   const uint64_t cut = (d / kPiece + static_cast<uint64_t>(p - it.piece_base)) * kPiece;
   const uint64_t lo = max(d, cut);
@@ -286,13 +310,15 @@ __global__ void __launch_bounds__(kThreads) staged_copy_kernel(const CopyItem* _
 
   if (warp == 0) {  // producer
     if (lane == 0) {
+      ItemCursor cur;
       for (int64_t k = 0; k < mine; ++k) {
         const int s = static_cast<int>(k % kStages);
         if (k >= kStages) {
           mbar_wait(&empty[s], static_cast<uint32_t>(((k / kStages) - 1) & 1));
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         }
-        const Piece pc = piece_at(list, n_items, first + k * step);
+        const int64_t p = first + k * step;
+        const Piece pc = piece_at(cur.at(list, n_items, p), p);
         staged[s] = pc;
         const uintptr_t s0 = reinterpret_cast<uintptr_t>(pc.src) & ~uintptr_t{15};
         const uintptr_t s1 = (reinterpret_cast<uintptr_t>(pc.src) + pc.bytes + 15) & ~uintptr_t{15};

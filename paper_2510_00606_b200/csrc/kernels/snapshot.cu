@@ -269,8 +269,9 @@ bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 
 // conflict-free), the first consumer lane writes the snapshot copy of the
 // stage back with one bulk shared->global store, and the stage is released
 // once both the consumers and the store engine have read it.  Row sums are
-// reduced among the consumers only (named barrier 1), so the producer keeps
-// loading the next row meanwhile.  Checksum arithmetic is the same as
+// reduced through shared-memory slots (each consumer warp adds its sums, the
+// last to arrive finishes the row), so neither the producer nor any consumer
+// waits at a row end.  Checksum arithmetic is the same as
 // row_kernel (unit k of a row's 32-byte-aligned window holds global words
 // q_t + 256*i, i = the thread's iteration).
 constexpr int kTmaConsumers = 4;                  // warps
@@ -280,9 +281,8 @@ constexpr int kTmaPiece = 16 * 1024;              // bytes per stage
 constexpr int kTmaSmem = kTmaStages * kTmaPiece;  // 64 KiB -> 3 CTAs per SM
 constexpr int kTmaUnitsPerThread = kTmaPiece / 16 / (32 * kTmaConsumers);  // 8
 
-__device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(32 * kTmaConsumers) : "memory");
-}
+constexpr int kRowSlots = 8;                     // >= kTmaStages + 1, power of 2
+static_assert(kRowSlots > kTmaStages, "row slots must cover the ring");
 
 struct TmaRow {
   int64_t w0;      // first local byte of the 32-byte-aligned window
@@ -291,8 +291,9 @@ struct TmaRow {
   int64_t window_bytes;
 };
 
-__device__ __forceinline__ TmaRow tma_row(const ShardMapView& m, int64_t r, RowGeom& g) {
-  g = row_geom(m, r);
+__device__ __forceinline__ TmaRow tma_row(const ShardMapView& m, int64_t r, RowGeom& g,
+                                          RowCursor& cur) {
+  g = cur.at(m, r);
   TmaRow t;
   t.w0 = g.local_lo & ~int64_t{31};
   t.head = static_cast<int>(g.local_lo - t.w0);
@@ -314,8 +315,18 @@ __global__ void __launch_bounds__(kTmaThreads) tma_row_kernel(ShardMapView map,
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kTmaStages];
   __shared__ __align__(8) uint64_t empty[kTmaStages];
-  __shared__ uint64_t red0[kTmaConsumers], red1[kTmaConsumers];
+  // per-row reduction slots: each consumer warp adds its sums, the last of
+  // the four to arrive finishes the row (no consumer barrier, so no warp
+  // ever waits for another at a row end).  A warp runs at most kTmaStages
+  // pieces (so <= kTmaStages rows) ahead of the slowest: 8 slots suffice.
+  __shared__ unsigned long long slot_s0[kRowSlots], slot_s1[kRowSlots];
+  __shared__ unsigned slot_n[kRowSlots];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x < kRowSlots) {
+    slot_s0[threadIdx.x] = 0;
+    slot_s1[threadIdx.x] = 0;
+    slot_n[threadIdx.x] = 0;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < kTmaStages; ++s) {
       mbar_init(&full[s], 1);
@@ -327,10 +338,11 @@ __global__ void __launch_bounds__(kTmaThreads) tma_row_kernel(ShardMapView map,
 
   if (warp == 0) {  // producer
     if (lane != 0) return;
+    RowCursor cur;
     int64_t k = 0;
     for (int64_t r = blockIdx.x; r < map.n_rows; r += gridDim.x) {
       RowGeom g;
-      const TmaRow t = tma_row(map, r, g);
+      const TmaRow t = tma_row(map, r, g, cur);
       for (int p = 0; p < t.n_pieces; ++p, ++k) {
         const int s = static_cast<int>(k % kTmaStages);
         if (k >= kTmaStages) {
@@ -348,13 +360,14 @@ __global__ void __launch_bounds__(kTmaThreads) tma_row_kernel(ShardMapView map,
   }
 
   const int ctid = threadIdx.x - 32;
-  const int cwarp = warp - 1;
   const int64_t last_vec_byte = (map.total_bytes - 1) & ~int64_t{31};  // start of the last 32-B vector
   const int partial = static_cast<int>(map.total_bytes & 31);
   int64_t k = 0;
+  unsigned row_iter = 0;
+  RowCursor cur;
   for (int64_t r = blockIdx.x; r < map.n_rows; r += gridDim.x) {
     RowGeom g;
-    const TmaRow t = tma_row(map, r, g);
+    const TmaRow t = tma_row(map, r, g, cur);
     const int sh = static_cast<int>(g.delta & 7);
     const int64_t q_t = floor_div(t.w0 + 16 * ctid + g.delta, 8);
     uint64_t t1 = 0, t2 = 0, odd = 0, bsum = 0;
@@ -416,18 +429,22 @@ __global__ void __launch_bounds__(kTmaThreads) tma_row_kernel(ShardMapView map,
                       (static_cast<uint64_t>(n_exec) * t1 - t2) + odd + bsum;
     s0 = warp_sum_u64(s0);
     s1 = warp_sum_u64(s1);
+    const int sl = static_cast<int>(row_iter++ & (kRowSlots - 1));
+    bool last = false;
+    uint64_t x0 = 0, x1 = 0;
     if (lane == 0) {
-      red0[cwarp] = s0;
-      red1[cwarp] = s1;
-    }
-    consumer_sync();
-    if (ctid == 0) {
-      uint64_t x0 = 0, x1 = 0;
-#pragma unroll
-      for (int w = 0; w < kTmaConsumers; ++w) {
-        x0 += red0[w];
-        x1 += red1[w];
+      atomicAdd(&slot_s0[sl], static_cast<unsigned long long>(s0));
+      atomicAdd(&slot_s1[sl], static_cast<unsigned long long>(s1));
+      __threadfence_block();
+      last = atomicAdd(&slot_n[sl], 1u) == kTmaConsumers - 1;
+      if (last) {
+        __threadfence_block();
+        x0 = atomicExch(&slot_s0[sl], 0ull);
+        x1 = atomicExch(&slot_s1[sl], 0ull);
+        atomicExch(&slot_n[sl], 0u);
       }
+    }
+    if (last) {
       if (M == Mode::kVerify) {
         if (x0 != expected[2 * r] || x1 != expected[2 * r + 1]) {
           const uint32_t slot = atomicAdd(bad_count, 1u);
@@ -438,7 +455,6 @@ __global__ void __launch_bounds__(kTmaThreads) tma_row_kernel(ShardMapView map,
         row_sums[2 * r + 1] = x1;
       }
     }
-    consumer_sync();
   }
   if (M == Mode::kSnapshot && ctid == 0) bulk_wait_all();
 }
