@@ -14,6 +14,7 @@
 #include <utility>
 #include <vector>
 
+#include "elaskit/cluster.hpp"
 #include "elaskit/dataflow.hpp"
 #include "elaskit/migration.hpp"
 #include "elaskit/param_fabric.hpp"
@@ -117,6 +118,22 @@ std::vector<CopyDesc> clip_copies(const std::vector<CopyDesc>& copies, std::int6
 // writes vs the OLD reads of phases >= j - slack, flush_j's writes vs the
 // reads of phases > j.  Throws CoverageMismatch naming the first overlap.
 void check_inplace(const InPlaceSchedule& s, const PartitionLayout& src);
+
+// One stage's DP membership change under one event — the input of the
+// recovery path: old = dp_group(state, stage), next = apply_event(state, ev),
+// members = dp_group(next, stage) (empty when the stage emptied: EmptyStage
+// is the graph planner's case, not a DP reshard), departed = old \ members
+// (the `failed` set of integrity_check / overlap_matrix), slow = members whose
+// slow_factor changed.  ScaleOut arrivals wait in next.free_pool until a
+// placement puts them in the grid, so a pure ScaleOut yields no change here.
+struct DpTransition {
+  ClusterState next;
+  std::vector<DeviceId> old_members, members;
+  std::set<int> departed;
+  std::vector<DeviceId> slow;
+};
+
+DpTransition dp_transition(const ClusterState& state, const ElasticEvent& ev, int stage);
 
 // Sample offsets of micro-batch 0 whose owning slot changes between two
 // assignments — the SampleReassignment list recover_elaswave derives before

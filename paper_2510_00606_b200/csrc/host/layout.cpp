@@ -188,4 +188,24 @@ std::vector<SampleReassignment> sample_reassignments(const MicrobatchAssignment&
   return out;
 }
 
+// The recovery path's input from the cluster model (SURVEY §8(a) A17:
+// ElasticEvent feeds plan_edit; the survivor set feeds the layouts).
+DpTransition dp_transition(const ClusterState& state, const ElasticEvent& ev, int stage) {
+  DpTransition t;
+  t.old_members = dp_group(state, stage);
+  t.next = apply_event(state, ev);
+  try {
+    t.members = dp_group(t.next, stage);
+  } catch (const EmptyStage&) {
+    t.members.clear();
+  }
+  for (const DeviceId d : t.old_members) {
+    if (std::find(t.members.begin(), t.members.end(), d) == t.members.end())
+      t.departed.insert(d);
+    else if (t.next.devices.at(d).slow_factor != state.devices.at(d).slow_factor)
+      t.slow.push_back(d);
+  }
+  return t;
+}
+
 }  // namespace elaskit::b200

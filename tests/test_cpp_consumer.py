@@ -65,3 +65,58 @@ def test_cpp_recovery_driver_runs(d, failed, mode):
     assert out.returncode == 0, out.stdout + out.stderr
     res = json.loads(out.stdout.strip().splitlines()[-1])
     assert res["conserved"] and res["bytes_ok"]
+
+
+EVENT_SRC = r'''
+#include "elaskit/b200.hpp"
+#include <cstdio>
+int main() {
+  using namespace elaskit;
+  // one pipeline stage of DP 8 (config B), rank r = device r
+  ClusterState st = make_uniform_cluster(1, 8, 180LL << 30);
+  ElasticEvent ev; ev.kind = EventKind::FailStop; ev.targets = {3};
+  const b200::DpTransition t = b200::dp_transition(st, ev, 1);
+  ZeroLayout z; z.kind = ZeroKind::Interleaved;
+  z.layer_bytes.push_back(131072000LL * 14);
+  for (int l = 0; l < 32; ++l) z.layer_bytes.push_back(202383360LL * 14);
+  z.layer_bytes.push_back(131076096LL * 14);
+  const auto src = b200::interleaved_layout(z, t.old_members);
+  const auto dst = b200::interleaved_layout(z, t.members);
+  SnapshotRing ring; ring.members = t.old_members;
+  const auto rep = integrity_check(ring, src, t.departed);
+  const auto plan = overlap_matrix(src, dst, t.departed, &ring);
+  // a second, adjacent failure leaves rank 3's bytes without a holder
+  ElasticEvent ev2; ev2.kind = EventKind::FailStop; ev2.targets = {2};
+  const b200::DpTransition t2 = b200::dp_transition(t.next, ev2, 1);
+  std::set<int> both = {2, 3};
+  const auto rep2 = integrity_check(ring, src, both);
+  ElasticEvent slow; slow.kind = EventKind::FailSlow; slow.targets = {5}; slow.slow_factor = 1.5;
+  const b200::DpTransition t3 = b200::dp_transition(st, slow, 1);
+  std::printf("%zu %zu %d %lld %zu %d %zu %zu %zu\n", t.old_members.size(), t.members.size(),
+              *t.departed.begin(), (long long)plan.total_bytes_moved, plan.entries.size(),
+              (int)rep.recoverable, t2.members.size(), (std::size_t)rep2.recoverable,
+              t3.slow.size() + 10 * t3.departed.size());
+  return 0;
+}
+'''
+
+
+def test_cpp_event_to_plan(tmp_path):
+    """Cluster model -> DP membership -> layouts -> plan from C++: a FailStop
+    of device 3 in config B's DP 8 stage yields the reference's 7B 8->7 drop-r3
+    plan (238 entries, 26.954 GB moved, SURVEY Appendix A)."""
+    if shutil.which("g++") is None:
+        pytest.skip("no g++")
+    src = tmp_path / "event.cpp"
+    src.write_text(EVENT_SRC)
+    exe = tmp_path / "event"
+    lib = ROOT / "paper_2510_00606_b200"
+    subprocess.run(["g++", "-std=c++20", f"-I{ROOT / 'include'}", f"-I{ROOT / 'third_party' / 'nlohmann'}",
+                    str(src), f"-L{lib}", "-l:libelaskit_b200.so", f"-Wl,-rpath,{lib}", "-o", str(exe)],
+                   check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()
+    old_n, new_n, departed, moved, entries, ok, new2, ok2, slow = map(int, out)
+    assert (old_n, new_n, departed) == (8, 7, 3)
+    assert entries == 238 and round(moved / 1e9, 3) == 26.954
+    assert ok == 1 and new2 == 6 and ok2 == 0
+    assert slow == 1  # one slow member, nobody departed

@@ -12,7 +12,7 @@ import pytest
 
 ROOT = Path(__file__).resolve().parents[1]
 REF_DIR = ROOT / "oracle" / "_ref"
-MODULES = ["param_fabric", "rng", "dataflow", "communicator", "migration"]
+MODULES = ["param_fabric", "rng", "dataflow", "communicator", "migration", "cluster"]
 KNOWN_REFERENCE_FAILURES = {
     "migration": {"stall dominance over fuzzed configurations", "byte-count law across D"},
 }
