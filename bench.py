@@ -606,6 +606,9 @@ def run_reshard(args, rank, world, out):
             "bottleneck_nvlink_gbs": round(tr["bottleneck_bytes"] / t_d / 1e9, 1)
             if tr["bottleneck_bytes"] else None}
     out["reshard"]["per_departure_prepared"] = per_drop
+    if world in (2, 4, 6) and args.reshard_state_gb <= 0:
+        out["reshard"]["projection_8to7"] = project_8to7(base, world, per_drop,
+                                                         out["reshard"]["mttr_ms_prepared"])
     barrier(world)
     prep.close()
     ex.close()
@@ -614,6 +617,36 @@ def run_reshard(args, rank, world, out):
     comm.destroy()
     del bufs
     torch.cuda.empty_cache()
+
+
+def project_8to7(base, world, per_drop, prepared):
+    """Config B's 8->7 MTTR from this run, for pools that lend fewer than 8
+    GPUs (labelled a projection; at N = 8 the reshard leg measures it).  The
+    8->7 plans come from the planner (exact bytes); each departure kind takes
+    the bottleneck-link rate measured here for the same kind of departure at
+    N -> N-1 (first rank: its ring holder's egress; last rank: self-lane
+    heavy; interior ranks: the slowest interior one), plus the prepared
+    path's measured host and verification overheads."""
+    from paper_2510_00606_b200.reshard import ReshardPlan
+
+    rate = {k: v["bottleneck_nvlink_gbs"] for k, v in per_drop.items()}
+    interior = [rate[f"r{d}"] for d in range(1, world - 1) if rate.get(f"r{d}")]
+    kinds = {0: rate.get("r0"), 7: rate.get(f"r{world - 1}"),
+             3: min(interior) if interior else rate.get(f"r{world - 1}")}
+    overhead_ms = prepared["total"] - prepared["copy"]
+    res = {"what": "projection, not a measurement: 8->7 bottleneck bytes (planner, exact) / "
+                   f"bottleneck-link rate measured at {world}->{world - 1} for the same kind of "
+                   "departure + measured host/verify overhead of the prepared path",
+           "overhead_ms": round(overhead_ms, 3)}
+    for d, gbs in kinds.items():
+        rp = ReshardPlan.build(base.layer_bytes, list(range(8)), [r for r in range(8) if r != d])
+        b = rp.traffic()["bottleneck_bytes"]
+        if not gbs or not b:
+            continue
+        copy_ms = b / (gbs * 1e9) * 1e3
+        res[f"drop_r{d}"] = {"bottleneck_gpu_bytes": b, "rate_gbs": gbs,
+                             "copy_ms": round(copy_ms, 2), "mttr_ms": round(copy_ms + overhead_ms, 2)}
+    return res
 
 
 def run_config_c(args, rank, world, out):
