@@ -1,4 +1,6 @@
 #!/bin/bash
+# NOTE: the EW_REALIGN / EW_COPY_CTAS switches were removed after this sweep
+# (no net gain); the script documents the experiment in profiles/r01_realign_ab_4gpu.log.
 # Reshard copy A/B on 4 GPUs (bench reshard leg only): realign variant
 # (EW_REALIGN=static | default select chain) x total CTAs (EW_COPY_CTAS; the
 # NVLink class keeps a quarter unless EW_REMOTE_CTAS is set).
