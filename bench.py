@@ -64,8 +64,8 @@ def parse_args():
     p.add_argument("--only-inplace", action="store_true",
                    help="run only the snapshot leg and the in-place reshard leg")
     p.add_argument("--skip", default="",
-                   help="comma list of: e2e,cpu,inplace,reshard,replica,replay,migration,"
-                        "config_c,stage,philox,reduce")
+                   help="comma list of: e2e,cpu,inplace,reshard,host_replica,replica,replay,"
+                        "migration,config_c,stage,philox,reduce")
     p.add_argument("--json-out", default="")
     return p.parse_args()
 
@@ -633,6 +633,100 @@ def run_reshard(args, rank, world, out):
     if shrunk is not None:
         shrunk.destroy()
     comm.destroy()
+    del bufs
+    torch.cuda.empty_cache()
+
+
+def run_host_replica(args, rank, world, out):
+    """The same N->N-1 departure with the departed rank's bytes sourced from
+    node-shared host memory (hostsnap.HostSnapshots: the reference's
+    H2D_D2D medium) instead of the holder's HBM replica: per-step publish
+    (D2H of every rank's shard at once) and the verified recovery, timed."""
+    import shutil
+    import torch
+    import torch.distributed as dist
+    from paper_2510_00606_b200 import configs, device as dev
+    from paper_2510_00606_b200.fabric import ROLE_REPLICA
+    from paper_2510_00606_b200.hostsnap import HostSnapshots
+    from paper_2510_00606_b200.reshard import ReshardExecutor, ReshardPlan, shard_map
+
+    torch.cuda.empty_cache()
+    base = configs.llama2_7b()
+    lb = base.layer_bytes if world == 8 else [x * world // 8 for x in base.layer_bytes]
+    members = list(range(world))
+    drop = min(3, world - 1)
+    rp = ReshardPlan.build(lb, members, [r for r in members if r != drop])
+    room = torch.tensor([shutil.disk_usage("/dev/shm").free], dtype=torch.float64, device="cuda")
+    dist.all_reduce(room, op=dist.ReduceOp.MIN)
+    if room.item() < 1.3 * sum(lb):
+        if rank == 0:
+            out["host_replica"] = {"skipped": "/dev/shm smaller than 1.3x the state"}
+        return
+    S = rp.src.shard_bytes(rank)
+    stream = torch.cuda.current_stream()
+    ex = ReshardExecutor(rp, rank, push=False)
+    bufs = ex.allocate(device_replica=False)
+    dev.fill_synthetic(shard_map(rp.src, rank), bufs.old, 0)
+    hs = HostSnapshots(rp.src, members, rank, tag=f"bench{os.getppid()}")
+    times = []
+    for _ in range(3):
+        barrier(world)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        hs.publish(bufs.old, stream)
+        e.record(stream)
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e) / 1e3)
+    t_pub = max_over_ranks([min(times)], world)[0]
+    hs.attach(ex, [drop])
+    barrier(world)
+    ex.bind(bufs, verify=True)
+    nblocks = (sum(lb) + args.block_bytes - 1) // args.block_bytes
+    m_old = shard_map(rp.src, rank, args.block_bytes)
+    rows = m_old.new_row_sums()
+    dev.checksum(m_old, bufs.old, rows)
+    before = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+    dev.rows_to_blocks(m_old, rows, before)
+    dist.all_reduce(before)
+    times = []
+    ok = True
+    for _ in range(3):
+        sums = torch.zeros_like(before)
+        barrier(world)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record(stream)
+        ex.launch(stream=stream, block_sums=sums)
+        e.record(stream)
+        torch.cuda.synchronize()
+        times.append(s.elapsed_time(e) / 1e3)
+        dist.all_reduce(sums)
+        ok = ok and bool(torch.equal(sums, before))
+    t_copy = max_over_ranks([sum(times) / len(times)], world)[0]
+    if bufs.new is not None:
+        n = rp.dst.shard_bytes(rank)
+        exp = dev.empty_bytes(n)
+        dev.fill_synthetic(shard_map(rp.dst, rank), exp, 0)
+        ok = ok and bool(torch.equal(bufs.new[:n], exp[:n]))
+        del exp
+    okt = torch.tensor([1 if ok else 0], device="cuda")
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    pulls = rp.copies(rank, push=False)
+    host_b = int(pulls[pulls["src_role"] == ROLE_REPLICA]["bytes"].sum()) if rank != drop else 0
+    host_max = int(max_over_ranks([float(host_b)], world)[0])
+    res = {"change": f"{world}->{world - 1} (drop rank {drop})",
+           "source_of_departed_bytes": "node-shared pinned host memory (POSIX shm), read by "
+                                       "each destination's copy kernel over its own PCIe link",
+           "publish_ms": round(t_pub * 1e3, 2),
+           "publish_gbs_per_gpu": round(S / t_pub / 1e9, 1),
+           "copy_ms": round(t_copy * 1e3, 2), "host_bytes_busiest_gpu": host_max,
+           "host_read_gbs_busiest_gpu": round(host_max / t_copy / 1e9, 1) if host_max else None,
+           "verified_on_arrival_and_bytes": bool(okt.item())}
+    if "reshard" in out and "copy_ms" in out["reshard"]:
+        res["hbm_replica_copy_ms"] = out["reshard"]["copy_ms"]
+    out["host_replica"] = res
+    barrier(world)
+    ex.close()
+    hs.close()
     del bufs
     torch.cuda.empty_cache()
 
@@ -1406,6 +1500,8 @@ def bench_b200(args):
         run_cpu_baseline(args, out, segs, S)
     if world > 1 and "reshard" not in skip:
         run_reshard(args, rank, world, out)
+    if world > 1 and "host_replica" not in skip:
+        run_host_replica(args, rank, world, out)
     if world > 1 and "replica" not in skip:
         run_replica(args, rank, world, out)
     if "replay" not in skip:

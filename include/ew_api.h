@@ -219,6 +219,13 @@ int ew_device_sync(void);
 int ew_ipc_get_handle(const void* ptr, void* handle64, int64_t* offset);
 int ew_ipc_open(const void* handle64, int64_t offset, void** out);
 int ew_ipc_close(void* ptr);
+/* Host memory as a transfer source (Medium::H2D_D2D, param_fabric.hpp:63):
+ * pin [host, host + bytes) for every device of this process (portable,
+ * mapped) and return the device address the copy kernels read it through
+ * over PCIe.  `host` may be node-shared memory (POSIX shm) that other ranks
+ * register too.  Unregister before unmapping the range. */
+int ew_host_register(void* host, int64_t bytes, void** dev_ptr);
+int ew_host_unregister(void* host);
 
 /* ------------------------------------------------------------------------
  * (a) Snapshot + per-block checksum, verification

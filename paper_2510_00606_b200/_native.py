@@ -191,6 +191,8 @@ _sig("ew_device_sync", i32)
 _sig("ew_ipc_get_handle", i32, vp, C.c_char_p, P(i64))
 _sig("ew_ipc_open", i32, C.c_char_p, i64, P(vp))
 _sig("ew_ipc_close", i32, vp)
+_sig("ew_host_register", i32, vp, i64, P(vp))
+_sig("ew_host_unregister", i32, vp)
 
 _sig("ew_shardmap_create", i32, P(Segment), i64, i64, P(vp))
 _sig("ew_shardmap_free", None, vp)

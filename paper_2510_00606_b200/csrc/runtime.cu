@@ -203,6 +203,25 @@ int ew_ipc_close(void* ptr) {
   return EW_OK;
 }
 
+int ew_host_register(void* host, int64_t bytes, void** dev_ptr) {
+  if (host == nullptr || bytes <= 0 || dev_ptr == nullptr)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_host_register: bad arguments");
+  EW_CUDA_TRY(cudaHostRegister(host, static_cast<size_t>(bytes),
+                               cudaHostRegisterPortable | cudaHostRegisterMapped));
+  const cudaError_t e = cudaHostGetDevicePointer(dev_ptr, host, 0);
+  if (e != cudaSuccess) {
+    cudaHostUnregister(host);
+    return cuda_status(e, "cudaHostGetDevicePointer");
+  }
+  return EW_OK;
+}
+
+int ew_host_unregister(void* host) {
+  if (host == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_host_unregister: NULL");
+  EW_CUDA_TRY(cudaHostUnregister(host));
+  return EW_OK;
+}
+
 // ---- NCCL communicator ----
 
 int ew_comm_unique_id(void* id128) {

@@ -213,6 +213,18 @@ def ipc_close(ptr: int) -> None:
     check(lib.ew_ipc_close(C.c_void_p(ptr)))
 
 
+def host_register(addr: int, nbytes: int) -> int:
+    """Pin host range [addr, addr + nbytes) (e.g. node-shared memory) and
+    return the device address copy programs read it through (ew_host_register)."""
+    p = C.c_void_p()
+    check(lib.ew_host_register(C.c_void_p(addr), int(nbytes), C.byref(p)))
+    return p.value
+
+
+def host_unregister(addr: int) -> None:
+    check(lib.ew_host_unregister(C.c_void_p(addr)))
+
+
 # ---------------------------------------------------------------- (c) ---
 
 def mask_words(n_elems: int) -> int:

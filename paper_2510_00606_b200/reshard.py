@@ -183,18 +183,20 @@ class ReshardExecutor:
         self.program: Optional[dev.CopyProgram] = None
         self._opened: List[int] = []
 
-    def allocate(self, in_place: bool = False) -> RankBuffers:
+    def allocate(self, in_place: bool = False, device_replica: bool = True) -> RankBuffers:
         """Buffers of this rank.  in_place=True aliases NEW and OLD inside one
         allocation when that is provably safe — every retained byte keeps
         its address (one common shift s: OLD = buf[s:], NEW = buf[:]) and no
         incoming byte lands on the OLD range — so retained bytes are not
         copied at all (the program skips self-copies).  This is the case for
         cross-stage layer moves (the source stage drops its tail, the
-        destination stage grows at its head); otherwise separate buffers."""
+        destination stage grows at its head); otherwise separate buffers.
+        device_replica=False: the departed ranks' bytes come from host
+        images (hostsnap.HostSnapshots.attach), no HBM replica buffer."""
         rp, r = self.rp, self.rank
         rep_of = rp.replica_of(r)
         replica = (dev.empty_bytes(rp.src.shard_bytes(rep_of))
-                   if rep_of is not None and rep_of in rp.failed else None)
+                   if device_replica and rep_of is not None and rep_of in rp.failed else None)
         n_old = rp.src.shard_bytes(r) if r in rp.old_ranks else 0
         n_new = rp.dst.shard_bytes(r) if r in rp.new_ranks else 0
         if in_place and n_old and n_new:
