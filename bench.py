@@ -667,7 +667,20 @@ def run_host_replica(args, rank, world, out):
     ex = ReshardExecutor(rp, rank, push=False)
     bufs = ex.allocate(device_replica=False)
     dev.fill_synthetic(shard_map(rp.src, rank), bufs.old, 0)
-    hs = HostSnapshots(rp.src, members, rank, tag=f"bench{os.getppid()}")
+    try:
+        hs = HostSnapshots(rp.src, members, rank, tag=f"bench{os.getppid()}", readable=[drop])
+        err = ""
+    except Exception as e:  # the constructor fails on every rank together
+        hs, err = None, repr(e)
+    okt = torch.tensor([0 if hs is None else 1], device="cuda")
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    if not okt.item():
+        if hs is not None:
+            hs.close()
+        if rank == 0:
+            out["host_replica"] = {"skipped": "host images could not be mapped: " + (err or "peer")}
+        ex.close()
+        return
     times = []
     for _ in range(3):
         barrier(world)

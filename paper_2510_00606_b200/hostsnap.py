@@ -40,7 +40,12 @@ from .reshard import ReshardExecutor
 class HostSnapshots:
     """One node-shared host image per member's shard (source layout)."""
 
-    def __init__(self, layout, members: Sequence[int], rank: int, tag: str, group=None):
+    def __init__(self, layout, members: Sequence[int], rank: int, tag: str, group=None,
+                 readable: Optional[Iterable[int]] = None):
+        """Collective over `group`.  `readable`: members whose images this
+        rank maps for reading at recovery (default all; its own image is
+        always mapped).  A failure to map is raised only after the closing
+        barrier, so no rank is left waiting."""
         self.members = list(members)
         self.rank = rank
         self.ring = SnapshotRing(self.members)
@@ -53,20 +58,31 @@ class HostSnapshots:
         own = shared_memory.SharedMemory(name=name(rank), create=True,
                                          size=max(1, self.nbytes[rank]))
         self._segs[rank] = own
-        dist.barrier(group)
-        for r in self.members:
-            if r != rank:
-                seg = shared_memory.SharedMemory(name=name(r))
-                # the creator owns the name; do not let this process's
-                # tracker unlink a peer's segment at exit
-                resource_tracker.unregister(seg._name, "shared_memory")
-                self._segs[r] = seg
-            view = torch.frombuffer(self._segs[r].buf, dtype=torch.uint8)
-            self._views[r] = view
-            self._addr[r] = view.data_ptr()
-            self._dev[r] = self._register(r)
-        dist.barrier(group)
+        self._pieces: Dict[int, list] = {}
         self._closed = False
+        dist.barrier(group)
+        want = set(self.members if readable is None else readable) | {rank}
+        failure = None
+        try:
+            for r in self.members:
+                if r not in want:
+                    continue
+                if r != rank:
+                    seg = shared_memory.SharedMemory(name=name(r))
+                    # the creator owns the name; do not let this process's
+                    # tracker unlink a peer's segment at exit
+                    resource_tracker.unregister(seg._name, "shared_memory")
+                    self._segs[r] = seg
+                view = torch.frombuffer(self._segs[r].buf, dtype=torch.uint8)
+                self._views[r] = view
+                self._addr[r] = view.data_ptr()
+                self._dev[r] = self._register(r)
+        except Exception as e:  # noqa: BLE001 - re-raised after the barrier
+            failure = e
+        dist.barrier(group)
+        if failure is not None:
+            self.close()
+            raise failure
 
     _CHUNK = 1 << 30
 
@@ -76,7 +92,6 @@ class HostSnapshots:
         registered host memory (device address == host address) to stay one
         contiguous device range."""
         addr, n = self._addr[r], max(1, self.nbytes[r])
-        self._pieces = getattr(self, "_pieces", {})
         try:
             p = dev.host_register(addr, n)
             self._pieces[r] = [addr]
@@ -130,7 +145,10 @@ class HostSnapshots:
                 dev.host_unregister(a)
         self._views.clear()
         for r, seg in self._segs.items():
-            seg.close()
+            try:
+                seg.close()
+            except BufferError:  # a caller still holds an image() view
+                pass
             if r == self.rank:
                 seg.unlink()
         self._segs.clear()
