@@ -123,6 +123,26 @@ class CopyProgram {
   ew_copy_program* prog_ = nullptr;
 };
 
+// A host range pinned and mapped for the copy kernels (Medium::H2D_D2D
+// sources: a departed rank's image in node-shared host memory).  device()
+// goes into a CopyProgram table slot like any peer pointer.
+class HostRegistration {
+ public:
+  HostRegistration(void* host, std::int64_t bytes) : host_(host) {
+    check(ew_host_register(host, bytes, &dev_));
+  }
+  ~HostRegistration() {
+    if (host_ != nullptr) ew_host_unregister(host_);
+  }
+  HostRegistration(const HostRegistration&) = delete;
+  HostRegistration& operator=(const HostRegistration&) = delete;
+  void* device() const { return dev_; }
+
+ private:
+  void* host_ = nullptr;
+  void* dev_ = nullptr;
+};
+
 // Dropout keep-bits for samples [sample_lo, sample_lo + n_samples) of one
 // (layer, op) stream — the masks the reference derives from draw().
 inline void dropout_mask(std::uint64_t seed, std::int64_t sample_lo, std::int64_t n_samples,
