@@ -1190,7 +1190,7 @@ def run_layer_migration(args, rank, world, out):
     other = lambda mb, st: dev.weighted_fold([unit], [w[mb]], f, scratch, accumulate=True,
                                              stream=st)
     mig = LayerMigration((16, 0, 1), 0, 1, rank, params, acc, group=pair,
-                         transfer_ctas=int(os.environ.get("EW_MIG_CTAS", 32)))
+                         transfer_ctas=32)
     res = {"what": "7B layer (202 M params) stage move 0->1, non-blocking + payback",
            "param_bytes": 2 * n, "payback_bytes": 8 * n, "microbatches": M,
            "slot_ms": round(slot * 1e3, 3)}

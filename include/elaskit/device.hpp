@@ -145,7 +145,7 @@ class HostRegistration {
 
 // Dropout keep-bits for samples [sample_lo, sample_lo + n_samples) of one
 // (layer, op) stream — the masks the reference derives from draw().
-inline void dropout_mask(std::uint64_t seed, std::int64_t sample_lo, std::int64_t n_samples,
+inline void dropout_mask(std::uint64_t seed, std::uint64_t sample_lo, std::int64_t n_samples,
                          std::uint32_t layer, std::uint32_t op, std::int64_t n_elems, double keep,
                          std::uint32_t* bits, ew_stream_t s) {
   check(ew_philox_dropout_mask(seed, sample_lo, n_samples, layer, op, n_elems, keep, bits, s));

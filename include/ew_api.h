@@ -16,6 +16,16 @@
  *   - Device pointers are caller-owned and live on the CUDA device current on
  *     the calling thread.  ew_stream_t is a cudaStream_t (NULL = default).
  *   - Device calls are asynchronous on the given stream unless stated.
+ *   - Access granularity: the streaming kernels move memory with bulk (TMA)
+ *     transfers that cover whole aligned granules — 16 bytes for copy
+ *     sources (ew_copy_program_*), 32 bytes for snapshot / checksum / verify
+ *     buffers.  A granule holding at least one byte of a caller's range may
+ *     be read in full, so up to 15 (31) bytes before or past the range are
+ *     READ (never written) and their values ignored.  Such a granule never
+ *     straddles a 4 KiB page, so the over-read cannot fault on any mapping
+ *     the range itself lives in (device allocations, IPC mappings,
+ *     page-granular host registrations); callers need no padding.  Writes
+ *     are byte-exact.
  */
 #ifndef EW_API_H
 #define EW_API_H
@@ -286,18 +296,28 @@ void ew_copy_program_free(ew_copy_program* prog);
 int ew_copy_program_stats(const ew_copy_program* prog, int64_t* n_copies, int64_t* remote_bytes,
                           int64_t* local_bytes);
 /* One launch: remote copies on the first CTAs, local copies on the rest.
- * n_ctas / remote_ctas == 0 pick defaults (all SMs; CTAs split by bytes). */
+ * n_ctas == 0 picks 2 CTAs per SM; remote_ctas == 0 (or out of range) gives
+ * the remote class a quarter of them when the program has both classes. */
 int ew_copy_program_launch(const ew_copy_program* prog, int n_ctas, int remote_ctas,
                            ew_stream_t stream);
+/* Same launch, gated on a device flag (e.g. ew_peer_barrier_error_flag): if
+ * *abort_flag != 0 when the kernel starts, it writes nothing.  block_sums may
+ * be NULL (plain program) or the verified program's block sums. */
+int ew_copy_program_launch_guarded(const ew_copy_program* prog, int n_ctas, int remote_ctas,
+                                   uint64_t* block_sums, const int* abort_flag,
+                                   ew_stream_t stream);
 /* Verification on arrival.  A verified program also checksums (kernel (a)'s
  * spec) every byte it lands in this GPU's NEW buffer, labelled with the
  * global position that byte's destination offset has in new_map (NEW's
  * segment map on exec_rank), and adds the sums into block_sums (device
  * u64 [n_blocks][2], caller-zeroed; n_blocks from ew_copy_program_num_blocks
  * covers global blocks up to NEW's last byte).  In-place retained bytes are
- * read and checksummed but not rewritten.  The sum of every NEW rank's
- * block_sums equals the block sums of the source state when — and only when
- * — every byte landed where the target layout says, with no re-read of NEW. */
+ * read and checksummed but not rewritten.  When every byte landed where the
+ * target layout says, the sum of every NEW rank's block_sums equals the block
+ * sums of the source state, with no re-read of NEW.  The converse is
+ * probabilistic: the checksum is linear mod 2^64, so a misplaced or corrupted
+ * landing goes unnoticed only if its error terms cancel in both s0 and s1 of
+ * every block (a swap of two equal words, or a crafted collision). */
 int ew_copy_program_create_verified(const ew_copy_desc* descs, int64_t n,
                                     void* const* buf_table, int table_ranks, int exec_rank,
                                     const ew_shardmap* new_map, ew_copy_program** out);
@@ -311,11 +331,13 @@ int ew_copy_program_num_blocks(const ew_copy_program* prog, int64_t* n_blocks);
 /* bits[s][k/32] bit (k%32) = 1 iff element k of sample sample_lo+s is KEPT
  * (reference rule sim.cpp:926-928: dropped iff u < keep_probability); rows
  * are ceil(n_elems/32) words, trailing bits 0. */
-int ew_philox_dropout_mask(uint64_t seed, int64_t sample_lo, int64_t n_samples,
+int ew_philox_dropout_mask(uint64_t seed, uint64_t sample_lo, int64_t n_samples,
                            uint32_t layer_id, uint32_t op_index, int64_t n_elems,
                            double keep_probability, uint32_t* bits, ew_stream_t stream);
-/* out[s][k] = draw({seed, sample_lo+s, layer, op}, n_elems)[k] */
-int ew_philox_uniforms(uint64_t seed, int64_t sample_lo, int64_t n_samples, uint32_t layer_id,
+/* out[s][k] = draw({seed, sample_lo+s, layer, op}, n_elems)[k].  Sample ids
+ * are the reference's uint64 RngKey::sample_id (rng.hpp:21-26) over the full
+ * domain; sample_lo + s wraps mod 2^64 as the reference's does. */
+int ew_philox_uniforms(uint64_t seed, uint64_t sample_lo, int64_t n_samples, uint32_t layer_id,
                        uint32_t op_index, int64_t n_elems, double* out, ew_stream_t stream);
 /* raw words of blocks block_lo .. block_lo+n_blocks-1 of one stream */
 int ew_philox_words(uint64_t seed, uint64_t sample_id, uint32_t layer_id, uint32_t op_index,
@@ -406,6 +428,11 @@ int ew_peer_barrier_create(int world, int rank, unsigned long long* const* flag_
                            ew_peer_barrier** out);
 int ew_peer_barrier_wait(ew_peer_barrier* barrier, double timeout_s, ew_stream_t stream);
 int ew_peer_barrier_timed_out(ew_peer_barrier* barrier, int* timed_out);
+/* Device int the barrier sets to 1 on a timeout (and never clears): pass it to
+ * ew_copy_program_launch_guarded so writes ordered after a failed barrier do
+ * not run (an in-place reshard must not overwrite OLD bytes a lagging peer
+ * has not read yet). */
+int ew_peer_barrier_error_flag(ew_peer_barrier* barrier, const int** flag);
 void ew_peer_barrier_free(ew_peer_barrier* barrier);
 
 /* ------------------------------------------------------------------------

@@ -61,14 +61,14 @@ void ew_oracle_draw(uint64_t seed, uint64_t sample, uint32_t layer, uint32_t op,
 }
 
 /* sim.cpp:926-928 literally: mask = u < keep ? 0 : 1/keep.  bit 1 = kept. */
-void ew_oracle_dropout_mask(uint64_t seed, int64_t sample_lo, int64_t n_samples, uint32_t layer,
+void ew_oracle_dropout_mask(uint64_t seed, uint64_t sample_lo, int64_t n_samples, uint32_t layer,
                             uint32_t op, int64_t n_elems, double keep, uint32_t* bits) {
   const int64_t wpr = (n_elems + 31) / 32;
   double* u = (double*)malloc((size_t)(n_elems > 0 ? n_elems : 1) * sizeof(double));
   for (int64_t s = 0; s < n_samples; ++s) {
     uint32_t* row = bits + s * wpr;
     memset(row, 0, (size_t)wpr * 4);
-    ew_oracle_draw(seed, (uint64_t)(sample_lo + s), layer, op, n_elems, u);
+    ew_oracle_draw(seed, sample_lo + (uint64_t)s, layer, op, n_elems, u);
     for (int64_t k = 0; k < n_elems; ++k)
       if (!(u[k] < keep)) row[k / 32] |= 1u << (k % 32);
   }

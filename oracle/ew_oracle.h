@@ -12,7 +12,7 @@ extern "C" {
 void ew_oracle_philox4x64(const uint64_t counter[4], const uint64_t key[2], uint64_t out[4]);
 void ew_oracle_draw(uint64_t seed, uint64_t sample, uint32_t layer, uint32_t op, int64_t n,
                     double* out);
-void ew_oracle_dropout_mask(uint64_t seed, int64_t sample_lo, int64_t n_samples, uint32_t layer,
+void ew_oracle_dropout_mask(uint64_t seed, uint64_t sample_lo, int64_t n_samples, uint32_t layer,
                             uint32_t op, int64_t n_elems, double keep, uint32_t* bits);
 
 uint64_t ew_oracle_splitmix64(uint64_t x);

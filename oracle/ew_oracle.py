@@ -39,7 +39,7 @@ class Oracle:
         L = self.lib
         L.ew_oracle_philox4x64.argtypes = [P(u64), P(u64), P(u64)]
         L.ew_oracle_draw.argtypes = [u64, u64, u32, u32, i64, P(f64)]
-        L.ew_oracle_dropout_mask.argtypes = [u64, i64, i64, u32, u32, i64, f64, P(u32)]
+        L.ew_oracle_dropout_mask.argtypes = [u64, u64, i64, u32, u32, i64, f64, P(u32)]
         L.ew_oracle_splitmix64.argtypes = [u64]
         L.ew_oracle_splitmix64.restype = u64
         L.ew_oracle_num_rows.argtypes = [P(i64), i64, i64]
@@ -242,7 +242,7 @@ class Reference:
                                               P(i64), P(i64)]
         L.ref_philox4x64.argtypes = [P(u64), P(u64), P(u64)]
         L.ref_draw.argtypes = [u64, u64, u32, u32, i32, P(f64)]
-        L.ref_dropout_mask.argtypes = [u64, i64, i64, u32, u32, i32, f64, P(u32)]
+        L.ref_dropout_mask.argtypes = [u64, u64, i64, u32, u32, i32, f64, P(u32)]
         L.ref_weighted_grad_average.argtypes = [P(f64), P(f64), i32, i64, P(f64)]
         L.ref_reshard_microbatches.argtypes = [P(i32), i32, i32, P(i32), i32, P(i32), P(i32)]
         L.ref_plan_edit.argtypes = [i32, P(C.c_char_p), P(i32), P(i32), P(i32), i32, P(i32), i32,

@@ -242,12 +242,12 @@ int ref_draw(uint64_t seed, uint64_t sample, uint32_t layer, uint32_t op, int n,
 
 // Reference draw() over many samples, as the CPU baseline of the mask kernel:
 // out bits use the sim.cpp:926-928 rule (bit set = kept).
-int ref_dropout_mask(uint64_t seed, int64_t sample_lo, int64_t n_samples, uint32_t layer,
+int ref_dropout_mask(uint64_t seed, uint64_t sample_lo, int64_t n_samples, uint32_t layer,
                      uint32_t op, int n_elems, double keep, uint32_t* bits) {
   return guarded([&]() -> int {
     const int64_t wpr = (n_elems + 31) / 32;
     for (int64_t s = 0; s < n_samples; ++s) {
-      const auto u = draw({seed, static_cast<uint64_t>(sample_lo + s), layer, op}, n_elems);
+      const auto u = draw({seed, sample_lo + static_cast<uint64_t>(s), layer, op}, n_elems);
       uint32_t* row = bits + s * wpr;
       std::memset(row, 0, static_cast<std::size_t>(wpr) * 4);
       for (int k = 0; k < n_elems; ++k)

@@ -210,12 +210,13 @@ _sig("ew_copy_program_create_raw", i32, P(vp), P(vp), P(i64), P(i32), i64, P(vp)
 _sig("ew_copy_program_free", None, vp)
 _sig("ew_copy_program_stats", i32, vp, P(i64), P(i64), P(i64))
 _sig("ew_copy_program_launch", i32, vp, i32, i32, vp)
+_sig("ew_copy_program_launch_guarded", i32, vp, i32, i32, vp, vp, vp)
 _sig("ew_copy_program_create_verified", i32, P(CopyDesc), i64, vp, i32, i32, vp, P(vp))
 _sig("ew_copy_program_launch_verified", i32, vp, i32, i32, vp, vp)
 _sig("ew_copy_program_num_blocks", i32, vp, P(i64))
 
-_sig("ew_philox_dropout_mask", i32, u64, i64, i64, u32, u32, i64, f64, vp, vp)
-_sig("ew_philox_uniforms", i32, u64, i64, i64, u32, u32, i64, vp, vp)
+_sig("ew_philox_dropout_mask", i32, u64, u64, i64, u32, u32, i64, f64, vp, vp)
+_sig("ew_philox_uniforms", i32, u64, u64, i64, u32, u32, i64, vp, vp)
 _sig("ew_philox_words", i32, u64, u64, u32, u32, u64, i64, vp, vp)
 
 _sig("ew_weighted_absmax", i32, P(vp), P(f64), i32, i64, vp, vp)
@@ -242,6 +243,7 @@ _sig("ew_peer_fold_free", None, vp)
 _sig("ew_peer_barrier_create", i32, i32, i32, P(vp), P(vp))
 _sig("ew_peer_barrier_wait", i32, vp, f64, vp)
 _sig("ew_peer_barrier_timed_out", i32, vp, P(i32))
+_sig("ew_peer_barrier_error_flag", i32, vp, P(vp))
 _sig("ew_peer_barrier_free", None, vp)
 _sig("ew_plan_layer_migration", i32, i32, i32, i32, i32, P(MigrationContext), P(MigrationSchedule))
 _sig("ew_payback_accumulate", i32, vp, vp, i64, vp)

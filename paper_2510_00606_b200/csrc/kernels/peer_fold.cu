@@ -34,13 +34,10 @@ struct PeerUnit {
 // register traffic, which is what NVLink latency needs.
 constexpr int kPfUnitsMax = 8;
 
-static int env_int(const char* name, int dflt) {
-  const char* e = getenv(name);
-  return e && *e ? atoi(e) : dflt;
-}
-constexpr int kPfSlice = 4096;  // default bytes per unit per stage = 256 float4
-constexpr int kPfStages = 4;    // default ring depth
+constexpr int kPfSlice = 4096;  // bytes per unit per stage = 256 float4
+constexpr int kPfStages = 4;    // ring depth
 constexpr int kPfStagesMax = 8;
+constexpr int kPfCtasPerSm = 2;
 constexpr int kPfConsumers = 4;
 constexpr int kPfThreads = 32 * (kPfConsumers + 1);
 
@@ -316,6 +313,12 @@ int ew_peer_barrier_timed_out(ew_peer_barrier* b, int* timed_out) {
   return EW_OK;
 }
 
+int ew_peer_barrier_error_flag(ew_peer_barrier* b, const int** flag) {
+  if (b == nullptr || flag == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+  *flag = b->d_err;
+  return EW_OK;
+}
+
 void ew_peer_barrier_free(ew_peer_barrier* b) {
   if (b == nullptr) return;
   if (b->d_flags) cudaFree(b->d_flags);
@@ -444,15 +447,15 @@ int ew_peer_fold_reduce_scatter(ew_peer_fold* f, int frac_bits, ew_stream_t stre
     return EW_OK;
   }
   if (f->n_units <= kPfUnitsMax && f->hi4 > f->lo4) {
-    const int slice = env_int("EW_PF_SLICE", kPfSlice);
-    const int stages = std::min(env_int("EW_PF_STAGES", kPfStages), kPfStagesMax);
+    const int slice = kPfSlice;
+    const int stages = kPfStages;
     const int smem = stages * f->n_units * slice;
     const auto kern = f->i64 ? peer_fold_staged_kernel<true> : peer_fold_staged_kernel<false>;
     EW_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int gb = f->i64 ? 32 : 16;
     const int64_t pieces = (f->hi4 - f->lo4 + slice / gb - 1) / (slice / gb);
     const int grid = static_cast<int>(
-        std::min<int64_t>(pieces, env_int("EW_PF_CTAS_PER_SM", 2) * num_sms()));
+        std::min<int64_t>(pieces, kPfCtasPerSm * num_sms()));
     kern<<<grid, kPfThreads, smem, (cudaStream_t)stream>>>(
         f->d_units, f->n_units, f->lo4, f->hi4, scale, inv, f->out, slice, stages);
     EW_CUDA_TRY(cudaGetLastError());

@@ -76,7 +76,7 @@ __device__ __forceinline__ void philox_block(const Stream& s, uint64_t block, ui
 }
 
 // One thread -> one 32-bit mask word = 8 Philox blocks of one sample.
-__global__ void __launch_bounds__(256) mask_kernel(uint64_t seed, int64_t sample_lo,
+__global__ void __launch_bounds__(256) mask_kernel(uint64_t seed, uint64_t sample_lo,
                                                    int64_t n_samples, uint64_t lane,
                                                    int64_t n_elems, int64_t words_per_row,
                                                    uint64_t threshold, uint32_t* __restrict__ bits) {
@@ -85,7 +85,8 @@ __global__ void __launch_bounds__(256) mask_kernel(uint64_t seed, int64_t sample
        w += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = w / words_per_row;
     const int64_t col = w - row * words_per_row;
-    const Stream s = make_stream(seed, static_cast<uint64_t>(sample_lo + row), lane);
+    // sample ids wrap mod 2^64 like the reference's uint64 RngKey::sample_id
+    const Stream s = make_stream(seed, sample_lo + static_cast<uint64_t>(row), lane);
     const int64_t e0 = col * 32;
     const int nvalid = static_cast<int>(min((int64_t)32, n_elems - e0));
     uint32_t word = 0;
@@ -118,7 +119,7 @@ __global__ void __launch_bounds__(256) mask_kernel(uint64_t seed, int64_t sample
   }
 }
 
-__global__ void uniform_kernel(uint64_t seed, int64_t sample_lo, int64_t n_samples, uint64_t lane,
+__global__ void uniform_kernel(uint64_t seed, uint64_t sample_lo, int64_t n_samples, uint64_t lane,
                                int64_t n_elems, double* __restrict__ out) {
   const int64_t blocks_per_row = (n_elems + 3) / 4;
   const int64_t total = n_samples * blocks_per_row;
@@ -126,7 +127,7 @@ __global__ void uniform_kernel(uint64_t seed, int64_t sample_lo, int64_t n_sampl
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = t / blocks_per_row;
     const int64_t blk = t - row * blocks_per_row;
-    const Stream s = make_stream(seed, static_cast<uint64_t>(sample_lo + row), lane);
+    const Stream s = make_stream(seed, sample_lo + static_cast<uint64_t>(row), lane);
     uint64_t w[4];
     philox_block(s, static_cast<uint64_t>(blk + 1), w);
     for (int i = 0; i < 4; ++i) {
@@ -159,10 +160,10 @@ using namespace ew;
 
 extern "C" {
 
-int ew_philox_dropout_mask(uint64_t seed, int64_t sample_lo, int64_t n_samples,
+int ew_philox_dropout_mask(uint64_t seed, uint64_t sample_lo, int64_t n_samples,
                            uint32_t layer_id, uint32_t op_index, int64_t n_elems,
                            double keep_probability, uint32_t* bits, ew_stream_t stream) {
-  if (n_samples < 0 || n_elems < 0 || sample_lo < 0)
+  if (n_samples < 0 || n_elems < 0)
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_philox_dropout_mask: negative extent");
   if (n_samples == 0 || n_elems == 0) return EW_OK;
   if (bits == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_philox_dropout_mask: NULL bits");
@@ -179,9 +180,9 @@ int ew_philox_dropout_mask(uint64_t seed, int64_t sample_lo, int64_t n_samples,
   return EW_OK;
 }
 
-int ew_philox_uniforms(uint64_t seed, int64_t sample_lo, int64_t n_samples, uint32_t layer_id,
+int ew_philox_uniforms(uint64_t seed, uint64_t sample_lo, int64_t n_samples, uint32_t layer_id,
                        uint32_t op_index, int64_t n_elems, double* out, ew_stream_t stream) {
-  if (n_samples < 0 || n_elems < 0 || sample_lo < 0)
+  if (n_samples < 0 || n_elems < 0)
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_philox_uniforms: negative extent");
   if (n_samples == 0 || n_elems == 0) return EW_OK;
   if (out == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_philox_uniforms: NULL out");

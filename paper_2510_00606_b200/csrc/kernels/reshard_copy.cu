@@ -279,7 +279,10 @@ __global__ void __launch_bounds__(kThreads) staged_copy_kernel(const CopyItem* _
                                                                int64_t local_pieces,
                                                                int remote_ctas,
                                                                unsigned long long* block_sums,
-                                                               int word_shift) {
+                                                               int word_shift,
+                                                               const int* abort_flag) {
+  // gated launch: a failed barrier upstream in stream order vetoes the copy
+  if (abort_flag != nullptr && *reinterpret_cast<const volatile int*>(abort_flag) != 0) return;
   extern __shared__ __align__(128) uint8_t ring[];
   __shared__ __align__(8) uint64_t full[kStages];
   __shared__ __align__(8) uint64_t empty[kStages];
@@ -545,7 +548,7 @@ int ew_copy_program_stats(const ew_copy_program* prog, int64_t* n_copies, int64_
 }
 
 static int launch_program(const ew_copy_program* prog, int n_ctas, int remote_ctas,
-                          uint64_t* block_sums, ew_stream_t stream) {
+                          uint64_t* block_sums, const int* abort_flag, ew_stream_t stream) {
   if (prog == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL program");
   if (prog->remote_pieces + prog->local_pieces == 0) return EW_OK;
   const int sms = num_sms();
@@ -555,20 +558,30 @@ static int launch_program(const ew_copy_program* prog, int n_ctas, int remote_ct
   else if (remote_ctas <= 0 || remote_ctas >= n_ctas)
     // NVLink class: a quarter of the CTAs, verified or not (N=4 sweep,
     // tools/verify_dbg.sh: 74 CTAs 11.07 ms verified vs 11.11 ms plain;
-    // 98 CTAs 11.2 ms); EW_REMOTE_CTAS overrides for sweeps
-    remote_ctas = getenv("EW_REMOTE_CTAS")
-                      ? std::min(n_ctas - 1, atoi(getenv("EW_REMOTE_CTAS")))
-                      : std::max(1, n_ctas / 4);
+    // 98 CTAs 11.2 ms); callers sweep through the remote_ctas argument
+    remote_ctas = std::max(1, n_ctas / 4);
   staged_copy_kernel<<<n_ctas, kThreads, kSmem, (cudaStream_t)stream>>>(
       prog->d_items, prog->n_remote, prog->remote_pieces, prog->n_local, prog->local_pieces,
-      remote_ctas, reinterpret_cast<unsigned long long*>(block_sums), prog->word_shift);
+      remote_ctas, reinterpret_cast<unsigned long long*>(block_sums), prog->word_shift,
+      abort_flag);
   EW_CUDA_TRY(cudaGetLastError());
   return EW_OK;
 }
 
 int ew_copy_program_launch(const ew_copy_program* prog, int n_ctas, int remote_ctas,
                            ew_stream_t stream) {
-  return launch_program(prog, n_ctas, remote_ctas, nullptr, stream);
+  return launch_program(prog, n_ctas, remote_ctas, nullptr, nullptr, stream);
+}
+
+int ew_copy_program_launch_guarded(const ew_copy_program* prog, int n_ctas, int remote_ctas,
+                                   uint64_t* block_sums, const int* abort_flag,
+                                   ew_stream_t stream) {
+  if (prog != nullptr && block_sums != nullptr && prog->word_shift < 0)
+    return set_error(EW_ERR_INVALID_ARGUMENT,
+                     "ew_copy_program_launch_guarded: block sums need a verified program");
+  return launch_program(prog, n_ctas, remote_ctas, prog && prog->word_shift >= 0 ? block_sums
+                                                                                  : nullptr,
+                        abort_flag, stream);
 }
 
 int ew_copy_program_launch_verified(const ew_copy_program* prog, int n_ctas, int remote_ctas,
@@ -576,7 +589,7 @@ int ew_copy_program_launch_verified(const ew_copy_program* prog, int n_ctas, int
   if (prog == nullptr || prog->word_shift < 0 || block_sums == nullptr)
     return set_error(EW_ERR_INVALID_ARGUMENT,
                      "ew_copy_program_launch_verified: needs a verified program and block sums");
-  return launch_program(prog, n_ctas, remote_ctas, block_sums, stream);
+  return launch_program(prog, n_ctas, remote_ctas, block_sums, nullptr, stream);
 }
 
 int ew_copy_program_num_blocks(const ew_copy_program* prog, int64_t* n_blocks) {

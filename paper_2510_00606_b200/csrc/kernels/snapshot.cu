@@ -5,8 +5,9 @@
 // sim.cpp:861-880) with the byte-moving operation: one HBM pass copies a
 // rank's packed shard live -> snapshot while checksumming it, a second pass
 // re-reads the snapshot and compares.  Both are HBM-bound streaming kernels:
-// 128-bit non-allocating loads, one 64 KiB checksum row per CTA iteration,
-// persistent grid of SMs x resident CTAs.
+// a warp-specialised CTA streams its rows through a shared-memory ring with
+// cp.async.bulk (TMA) loads and stores, one checksum row (<= 64 KiB) per CTA
+// iteration, persistent grid of SMs x resident CTAs.
 //
 // Checksum spec (ew_api.h, oracle/ew_oracle.c ew_oracle_row_sums): per global
 // block b, s0 = sum w_i and s1 = sum (i+1) w_i (mod 2^64) over the global
@@ -17,11 +18,10 @@
 // word q with A = W << 8sh and word q+1 with B = W >> (64-8sh) (sh > 0), so
 // with C = A + B:  s0 += C,  s1 += (q+1) C + B.  Bytes outside the row are
 // masked before the split, hence every nonzero contribution lands in the
-// row's own block.  Per thread the word indices are q_t + 512 i (+1 for the
+// row's own block.  Per thread the word indices are q_t + 256 i (+1 for the
 // odd word), so s1 needs only additions: sum i*D_i = n*T1 - T2 with the
 // running sums T1 += D_i, T2 += T1 (D_i = C_even + C_odd of iteration i).
 #include <algorithm>
-#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -29,9 +29,6 @@
 
 namespace ew {
 namespace {
-
-constexpr int kThreads = 256;
-constexpr int kUnroll = 4;  // 4 x 32 B in flight per thread
 
 __device__ __forceinline__ uint64_t byte_mask(int x, int a, int e) {
   // bytes of the 8-byte word at row-relative x that fall in [a, e)
@@ -49,146 +46,6 @@ __device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
 }
 
 enum class Mode { kSnapshot, kChecksum, kVerify };
-
-// One 32-byte vector (four local words) of a row: optional copy, edge
-// masking, checksum terms.  `idx` is the vector index inside the row.
-template <Mode M, bool kShift>
-__device__ __forceinline__ void row_vector(const Vec32& v, int idx, int nvec, int head, int end,
-                                           int sh, bool copy_first, int pidx, int partial,
-                                           uint8_t* __restrict__ dvec, uint64_t& t1, uint64_t& t2,
-                                           uint64_t& odd, uint64_t& bsum) {
-  if (M == Mode::kSnapshot && idx < nvec) {
-    // each 32-byte vector is copied by the row that holds its first byte
-    if (idx > 0 || copy_first) {
-      if (idx != pidx) {
-        st_stream32(dvec + 32 * idx, v);
-      } else {  // the buffer ends inside this vector: copy its valid bytes only
-        uint8_t* d = dvec + 32 * idx;
-#pragma unroll
-        for (int k = 0; k < 32; ++k)  // register extraction keeps v out of local memory
-          if (k < partial) d[k] = static_cast<uint8_t>(v.w[k >> 3] >> (8 * (k & 7)));
-      }
-    }
-  }
-  uint64_t w[4] = {v.w[0], v.w[1], v.w[2], v.w[3]};
-  if ((idx == 0) | (idx == nvec - 1)) {  // row-relative byte coordinates: the row is [head, end)
-#pragma unroll
-    for (int k = 0; k < 4; ++k) w[k] &= byte_mask(32 * idx + 8 * k, head, end);
-  }
-  uint64_t c[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    c[k] = w[k];
-    if (kShift) {
-      const uint64_t b = w[k] >> (64 - 8 * sh);
-      c[k] = (w[k] << (8 * sh)) + b;
-      bsum += b;
-    }
-  }
-  const uint64_t c23 = c[2] + c[3];
-  t1 += (c[0] + c[1]) + c23;
-  t2 += t1;
-  odd += c[1] + c23 + c23 + c[3];  // 1*c1 + 2*c2 + 3*c3
-}
-
-template <Mode M, bool kShift>
-__device__ __forceinline__ void row_body(const uint8_t* __restrict__ svec, uint8_t* __restrict__ dvec,
-                                         int nvec, int head, int end, int sh, bool copy_first,
-                                         int pidx, int partial, int& n_exec, uint64_t& t1,
-                                         uint64_t& t2, uint64_t& odd, uint64_t& bsum) {
-  const int tid = threadIdx.x;
-  const int iters = (nvec + kThreads - 1) / kThreads;
-  n_exec = (iters + kUnroll - 1) / kUnroll * kUnroll;
-  for (int it = 0; it < iters; it += kUnroll) {
-    Vec32 val[kUnroll];
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u) {
-      const int idx = tid + (it + u) * kThreads;
-      if (idx < nvec) val[u] = ld_stream32(svec + 32 * idx);
-      else val[u] = Vec32{{0, 0, 0, 0}};
-    }
-#pragma unroll
-    for (int u = 0; u < kUnroll; ++u)
-      row_vector<M, kShift>(val[u], tid + (it + u) * kThreads, nvec, head, end, sh, copy_first,
-                            pidx, partial, dvec, t1, t2, odd, bsum);
-  }
-}
-
-template <Mode M>
-__global__ void __launch_bounds__(kThreads, 4) row_kernel(ShardMapView map,
-                                                          const uint8_t* __restrict__ src,
-                                                          uint8_t* __restrict__ dst,
-                                                          uint64_t* __restrict__ row_sums,
-                                                          const uint64_t* __restrict__ expected,
-                                                          uint32_t* __restrict__ bad_count,
-                                                          int64_t* __restrict__ bad_rows,
-                                                          int64_t bad_cap) {
-  __shared__ uint64_t red0[kThreads / 32];
-  __shared__ uint64_t red1[kThreads / 32];
-  const int tid = threadIdx.x;
-
-  for (int64_t r = blockIdx.x; r < map.n_rows; r += gridDim.x) {
-    const RowGeom g = row_geom(map, r);
-    const int64_t a = g.local_lo;
-    const int64_t e = g.local_lo + g.len;
-    const int64_t v_lo = a >> 5;
-    // row-local 32-bit geometry (a row is at most one checksum block)
-    const int nvec = static_cast<int>(((e + 31) >> 5) - v_lo);
-    const int head = static_cast<int>(a & 31);
-    const int end = head + static_cast<int>(g.len);
-    const int sh = static_cast<int>(g.delta & 7);  // delta >= 0 for packed shards
-    const bool copy_first = head == 0;
-    // the buffer's last vector may be partial: copy only its valid bytes
-    const int partial = static_cast<int>(map.total_bytes & 31);
-    const int64_t last_vec = (map.total_bytes - 1) >> 5;
-    const int pidx = (partial && last_vec >= v_lo && last_vec < v_lo + nvec)
-                         ? static_cast<int>(last_vec - v_lo) : -1;
-    // global word index of this thread's first word
-    const int64_t q_t = floor_div(32 * (v_lo + tid) + g.delta, 8);
-    const uint8_t* svec = src + 32 * v_lo;
-    uint8_t* dvec = (M == Mode::kSnapshot) ? dst + 32 * v_lo : nullptr;
-
-    uint64_t t1 = 0, t2 = 0, odd = 0, bsum = 0;
-    int n_exec = 0;
-    if (sh == 0)
-      row_body<M, false>(svec, dvec, nvec, head, end, sh, copy_first, pidx, partial, n_exec, t1,
-                         t2, odd, bsum);
-    else
-      row_body<M, true>(svec, dvec, nvec, head, end, sh, copy_first, pidx, partial, n_exec, t1,
-                        t2, odd, bsum);
-    // words of iteration i start at q_t + 4*kThreads*i: sum_i i*D_i = n*T1 - T2
-    uint64_t s0 = t1;
-    uint64_t s1 = static_cast<uint64_t>(q_t + 1) * t1 +
-                  static_cast<uint64_t>(4 * kThreads) *
-                      (static_cast<uint64_t>(n_exec) * t1 - t2) + odd + bsum;
-
-    s0 = warp_sum_u64(s0);
-    s1 = warp_sum_u64(s1);
-    if ((tid & 31) == 0) {
-      red0[tid >> 5] = s0;
-      red1[tid >> 5] = s1;
-    }
-    __syncthreads();
-    if (tid == 0) {
-      uint64_t x0 = 0, x1 = 0;
-#pragma unroll
-      for (int w = 0; w < kThreads / 32; ++w) {
-        x0 += red0[w];
-        x1 += red1[w];
-      }
-      if (M == Mode::kVerify) {
-        if (x0 != expected[2 * r] || x1 != expected[2 * r + 1]) {
-          const uint32_t slot = atomicAdd(bad_count, 1u);
-          if (bad_rows != nullptr && static_cast<int64_t>(slot) < bad_cap) bad_rows[slot] = r;
-        }
-      } else {
-        row_sums[2 * r] = x0;
-        row_sums[2 * r + 1] = x1;
-      }
-    }
-    __syncthreads();
-  }
-}
 
 __global__ void rows_to_blocks_kernel(ShardMapView map, const uint64_t* __restrict__ rows,
                                       unsigned long long* __restrict__ blocks, int64_t n_blocks) {
@@ -249,14 +106,6 @@ __global__ void fill_kernel(ShardMapView map, uint8_t* __restrict__ buf, uint64_
   }
 }
 
-int row_grid(const void* kernel, int64_t n_rows) {
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, 0);
-  if (per_sm < 1) per_sm = 1;
-  const int64_t full = static_cast<int64_t>(num_sms()) * per_sm;
-  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(n_rows, full)));
-}
-
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
 
@@ -271,9 +120,8 @@ bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 
 // once both the consumers and the store engine have read it.  Row sums are
 // reduced through shared-memory slots (each consumer warp adds its sums, the
 // last to arrive finishes the row), so neither the producer nor any consumer
-// waits at a row end.  Checksum arithmetic is the same as
-// row_kernel (unit k of a row's 32-byte-aligned window holds global words
-// q_t + 256*i, i = the thread's iteration).
+// waits at a row end.  Unit k of a row's 32-byte-aligned window holds global
+// words q_t + 256*i (+1 for the odd word), i = the thread's iteration.
 constexpr int kTmaConsumers = 4;                  // warps
 constexpr int kTmaThreads = 32 * (kTmaConsumers + 1);
 constexpr int kTmaStages = 4;
@@ -304,7 +152,7 @@ __device__ __forceinline__ TmaRow tma_row(const ShardMapView& m, int64_t r, RowG
 }
 
 template <Mode M>
-__global__ void __launch_bounds__(kTmaThreads) tma_row_kernel(ShardMapView map,
+__global__ void __launch_bounds__(kTmaThreads, 3) tma_row_kernel(ShardMapView map,
                                                               const uint8_t* __restrict__ src,
                                                               uint8_t* __restrict__ dst,
                                                               uint64_t* __restrict__ row_sums,
@@ -459,33 +307,18 @@ __global__ void __launch_bounds__(kTmaThreads) tma_row_kernel(ShardMapView map,
   if (M == Mode::kSnapshot && ctid == 0) bulk_wait_all();
 }
 
-// EW_ROW_KERNEL=reg selects the register-streaming row_kernel (A/B runs).
-bool use_tma_rows() {
-  static const bool tma = [] {
-    const char* e = getenv("EW_ROW_KERNEL");
-    return !(e && std::string(e) == "reg");
-  }();
-  return tma;
-}
-
 template <Mode M>
 int launch_rows(const ShardMapView& v, const uint8_t* src, uint8_t* dst, uint64_t* rows,
                 const uint64_t* expected, uint32_t* bad, int64_t* bad_rows, int64_t cap,
                 cudaStream_t stream) {
-  if (use_tma_rows()) {
-    auto k = tma_row_kernel<M>;
-    // per device and cheap: set on every launch rather than caching
-    EW_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTmaThreads, kTmaSmem);
-    const int64_t grid = std::min<int64_t>(v.n_rows, static_cast<int64_t>(num_sms()) * std::max(1, per_sm));
-    k<<<static_cast<int>(grid), kTmaThreads, kTmaSmem, stream>>>(v, src, dst, rows, expected, bad,
-                                                                  bad_rows, cap);
-  } else {
-    auto k = row_kernel<M>;
-    k<<<row_grid((const void*)k, v.n_rows), kThreads, 0, stream>>>(v, src, dst, rows, expected,
-                                                                    bad, bad_rows, cap);
-  }
+  auto k = tma_row_kernel<M>;
+  // per device and cheap: set on every launch rather than caching
+  EW_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTmaThreads, kTmaSmem);
+  const int64_t grid = std::min<int64_t>(v.n_rows, static_cast<int64_t>(num_sms()) * std::max(1, per_sm));
+  k<<<static_cast<int>(grid), kTmaThreads, kTmaSmem, stream>>>(v, src, dst, rows, expected, bad,
+                                                                bad_rows, cap);
   EW_CUDA_TRY(cudaGetLastError());
   return EW_OK;
 }

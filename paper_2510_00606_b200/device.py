@@ -181,10 +181,16 @@ class CopyProgram:
         return n.value, r.value, l.value
 
     def launch(self, n_ctas: int = 0, remote_ctas: int = 0, stream=None,
-               block_sums: Optional[torch.Tensor] = None) -> None:
+               block_sums: Optional[torch.Tensor] = None, abort_flag: Optional[int] = None) -> None:
         """block_sums (int64 [2 * num_blocks()], zeroed by the caller): the
-        landed bytes' checksums are added there (verified programs only)."""
-        if block_sums is None:
+        landed bytes' checksums are added there (verified programs only).
+        abort_flag: device address of an int (PeerBarrier.error_flag); the
+        copy writes nothing if it is set when the kernel starts."""
+        if abort_flag is not None:
+            check(lib.ew_copy_program_launch_guarded(self._h, n_ctas, remote_ctas,
+                                                     _ptr(block_sums), C.c_void_p(abort_flag),
+                                                     _stream(stream)))
+        elif block_sums is None:
             check(lib.ew_copy_program_launch(self._h, n_ctas, remote_ctas, _stream(stream)))
         else:
             check(lib.ew_copy_program_launch_verified(self._h, n_ctas, remote_ctas,
@@ -398,6 +404,14 @@ class PeerBarrier:
         t = C.c_int()
         check(lib.ew_peer_barrier_timed_out(self._h, C.byref(t)))
         return bool(t.value)
+
+    @property
+    def error_flag(self) -> int:
+        """Device address of the int a timeout sets (CopyProgram.launch
+        abort_flag): writes ordered after a failed barrier do not run."""
+        p = C.c_void_p()
+        check(lib.ew_peer_barrier_error_flag(self._h, C.byref(p)))
+        return int(p.value)
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:

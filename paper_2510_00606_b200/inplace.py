@@ -286,6 +286,10 @@ class StagedInPlaceReshard:
             st.wait_stream(main)
         bar: List[torch.cuda.Event] = []
         flushed: List[Optional[torch.cuda.Event]] = []
+        # every gather and flush is gated on the barrier's error flag: after
+        # a timed-out barrier (a peer that has not read its bytes) nothing
+        # more is written, so no OLD byte a lagging peer still needs is lost
+        veto = self.barrier.error_flag
         for j in range(len(sc.phases)):
             g_s = gs[j % len(gs)]
             k = j - sc.slack - 1
@@ -294,9 +298,11 @@ class StagedInPlaceReshard:
             if j >= sc.ring and flushed[j - sc.ring] is not None:
                 g_s.wait_event(flushed[j - sc.ring])  # staging buffer free again
             if self.staged[j] is not None:
-                self.staged[j].launch(n_ctas, 0, stream=g_s, block_sums=block_sums)
+                self.staged[j].launch(n_ctas, 0, stream=g_s, block_sums=block_sums,
+                                      abort_flag=veto)
             if self.direct[j] is not None:
-                self.direct[j].launch(n_ctas, 0, stream=g_s, block_sums=block_sums)
+                self.direct[j].launch(n_ctas, 0, stream=g_s, block_sums=block_sums,
+                                      abort_flag=veto)
             g = torch.cuda.Event()
             g.record(g_s)
             ys.wait_event(g)
@@ -306,7 +312,7 @@ class StagedInPlaceReshard:
             bar.append(b)
             if self.flushes[j] is not None:
                 fs.wait_event(b)
-                self.flushes[j].launch(flush_ctas, 0, stream=fs)
+                self.flushes[j].launch(flush_ctas, 0, stream=fs, abort_flag=veto)
                 f = torch.cuda.Event()
                 f.record(fs)
                 flushed.append(f)
@@ -314,6 +320,14 @@ class StagedInPlaceReshard:
                 flushed.append(None)
         for st in gs[1:] + [ys, fs]:
             main.wait_stream(st)
+
+    def check(self) -> None:
+        """Raise if a phase barrier timed out (call after the launch's stream
+        completed).  The gated copies then stopped writing at that phase:
+        NEW is incomplete, but every OLD byte not yet read is intact."""
+        if self.barrier is not None and self.barrier.timed_out():
+            raise RuntimeError("in-place reshard aborted: a phase barrier timed out (a peer "
+                               "did not arrive); later gathers and flushes were vetoed")
 
     def close(self) -> None:
         self.direct, self.staged, self.flushes = [], [], []

@@ -277,14 +277,27 @@ class DpGroup:
         `bufs` are this rank's RankBuffers for the change (old/replica filled);
         `source_sums`: global block sums of the state before the change
         (from the per-step snapshot rows), else recomputed from OLD/replica."""
+        if kind == SCALE_OUT:
+            raise NotImplementedError("DpGroup.recover handles departures (FailStop/ScaleIn); "
+                                      "a rejoin grows the communicator, not shrinks it")
+        unknown = sorted(set(departed) - set(self.members))
+        if unknown:
+            raise ValueError(f"departed ranks {unknown} are not members of the group")
         ev = MttrEvent(step=step, kind=KIND_NAMES.get(kind, "fail_stop"))
         t0 = time.perf_counter()
-        # comm repair: edit plan, then the NCCL communicator shrink
+        # comm repair: edit plan, then the NCCL communicator shrink.  NCCL
+        # excludes by rank in the CURRENT communicator, which numbers the
+        # members 0..n-1 in ascending id order (it was built, or last shrunk,
+        # over self.members), not by member id
         edit = plan_edit([CommGroup("dp", self.members)], kind, list(departed), self.links)
         for l in edit.links_to_remove:
             self.links.discard(l)
         self.links |= edit.links_to_add
-        new_comm = self.comm.shrink(list(departed)) if self.comm is not None else None
+        comm_rank = {m: i for i, m in enumerate(self.members)}
+        new_comm = None
+        if self.comm is not None:
+            new_comm = self.comm.shrink(sorted(comm_rank[d] for d in departed))
+            self.comm.destroy()  # the child exists: the parent is no longer used
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         ev.comm_repair_s = t1 - t0

@@ -78,3 +78,20 @@ def test_snapshot_of_single_byte_segment_at_odd_global_offset(oracle):
     want = oracle.row_sums(segs, 65536, live.cpu().numpy()[:1])
     assert np.array_equal(rows.cpu().numpy().view(np.uint64)[:2], want[:2])
     assert int(snap[0].item()) == 0xAB
+
+
+def test_guarded_copy_vetoed_by_flag():
+    """ew_copy_program_launch_guarded: a set abort flag (a timed-out peer
+    barrier upstream) makes the copy write nothing; a clear one copies."""
+    src = torch.arange(40000, dtype=torch.int32, device="cuda").view(torch.uint8)
+    dst = torch.zeros_like(src)
+    prog = dev.CopyProgram.from_pointers([src.data_ptr() + 3], [dst.data_ptr() + 5],
+                                         [src.numel() - 8], [False])
+    flag = torch.ones(1, dtype=torch.int32, device="cuda")
+    prog.launch(abort_flag=flag.data_ptr())
+    torch.cuda.synchronize()
+    assert int(dst.count_nonzero()) == 0
+    flag.zero_()
+    prog.launch(abort_flag=flag.data_ptr())
+    torch.cuda.synchronize()
+    assert torch.equal(dst[5:5 + src.numel() - 8], src[3:3 + src.numel() - 8])

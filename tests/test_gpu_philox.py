@@ -26,19 +26,11 @@ def test_words_match_reference_golden(rng_golden):
 
 def test_uniforms_match_golden_draws(rng_golden):
     for c in rng_golden["cases"]:
-        if c["sample"] >= 2**63:
-            # the all-ones key: sample ids are int64 on the range API, check
-            # the stream through the raw-words entry point (uint64 sample)
-            w = dev.philox_words(c["seed"], c["sample"], c["layer"], c["op"], 1, 1)
-            words = w.cpu().numpy().view(np.uint64)[0]
-            assert [float(x >> np.uint64(11)) * 2.0**-53 for x in words][:len(c["draws"])] == c["draws"][:4]
-            continue
+        # the all-ones key included: sample ids span the full uint64 domain
         u = dev.philox_uniforms(c["seed"], c["sample"], 1, c["layer"], c["op"], len(c["draws"]))
         assert u.cpu().numpy()[0].tolist() == c["draws"]
     for c in rng_golden["ref_draws"]:
         want = [float.fromhex(x) for x in c["draws_hex"]]
-        if c["sample"] >= 2**63:
-            continue  # sample ids are int64 on the device API
         u = dev.philox_uniforms(c["seed"] % 2**64, c["sample"], 1, c["layer"], c["op"], len(want))
         assert u.cpu().numpy()[0].tolist() == want
 
@@ -64,6 +56,17 @@ def test_masks_match_oracle_rule(oracle, keep, n_elems):
     bits = dev.dropout_mask(seed, lo, ns, 3, 1, n_elems, keep).cpu().numpy().view(np.uint32)
     want = oracle.dropout_mask(seed, lo, ns, 3, 1, n_elems, keep)
     assert np.array_equal(bits, want)
+
+
+def test_masks_full_uint64_sample_domain(oracle):
+    """Sample ids >= 2^63 and the wrap past 2^64 - 1 (reference RngKey::
+    sample_id is uint64, rng.hpp:21-26; sample_lo + s wraps like its sum)."""
+    for lo in (2**63 - 2, 2**63, 2**64 - 3):
+        bits = dev.dropout_mask(11, lo, 5, 2, 1, 77, 0.5).cpu().numpy().view(np.uint32)
+        assert np.array_equal(bits, oracle.dropout_mask(11, lo, 5, 2, 1, 77, 0.5))
+        u = dev.philox_uniforms(11, lo, 5, 2, 1, 9).cpu().numpy()
+        for s in range(5):
+            assert u[s].tolist() == oracle.draw(11, (lo + s) % 2**64, 2, 1, 9).tolist()
 
 
 def test_masks_are_layout_independent():
