@@ -534,3 +534,82 @@ void ew_oracle_weighted_average_mt(const double* w, const double* g, int n_units
   }
   for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
 }
+
+/* ------------------------------------------------------------------------
+ * Synthetic-state checksums without a buffer, on T threads (checker for
+ * full-size GPU runs: config B rank shards of 11.8 GB, the 94.3 GB space).
+ * A row / block is summed straight from w_i = splitmix64(seed ^ i), the
+ * words at a range's ends masked to the bytes inside it. */
+typedef struct {
+  uint64_t seed;
+  const row_geom* rows;
+  int64_t lo, hi, block, total;
+  uint64_t* out;
+} synth_job;
+
+static void range_sums_synthetic(uint64_t seed, int64_t glo, int64_t ghi, uint64_t* s0o,
+                                 uint64_t* s1o) {
+  uint64_t s0 = 0, s1 = 0;
+  for (int64_t i = glo / 8; i <= (ghi - 1) / 8; ++i) {
+    uint64_t w = ew_oracle_splitmix64(seed ^ (uint64_t)i);
+    const int64_t a = glo > 8 * i ? glo - 8 * i : 0;        /* first byte kept */
+    const int64_t e = ghi < 8 * i + 8 ? ghi - 8 * i : 8;    /* one past last   */
+    if (a > 0) w &= ~0ULL << (8 * a);
+    if (e < 8) w &= (1ULL << (8 * e)) - 1;
+    s0 += w;
+    s1 += (uint64_t)(i + 1) * w;
+  }
+  *s0o = s0;
+  *s1o = s1;
+}
+
+static void* synth_rows_worker(void* p) {
+  synth_job* j = (synth_job*)p;
+  for (int64_t r = j->lo; r < j->hi; ++r) {
+    const int64_t glo = j->rows[r].local_lo + j->rows[r].delta;
+    range_sums_synthetic(j->seed, glo, glo + j->rows[r].len, &j->out[2 * r], &j->out[2 * r + 1]);
+  }
+  return NULL;
+}
+
+static void* synth_blocks_worker(void* p) {
+  synth_job* j = (synth_job*)p;
+  for (int64_t b = j->lo; b < j->hi; ++b) {
+    const int64_t lo = b * j->block;
+    const int64_t hi = lo + j->block < j->total ? lo + j->block : j->total;
+    range_sums_synthetic(j->seed, lo, hi, &j->out[2 * b], &j->out[2 * b + 1]);
+  }
+  return NULL;
+}
+
+static void run_synth(void* (*fn)(void*), synth_job base, int64_t n, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  synth_job jobs[256];
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = base;
+    jobs[t].lo = n * t / threads;
+    jobs[t].hi = n * (t + 1) / threads;
+    pthread_create(&th[t], NULL, fn, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+}
+
+/* Rows (segment order, blocks ascending) of the synthetic state placed by
+ * segs; returns the row count. */
+int64_t ew_oracle_rows_synthetic_mt(uint64_t seed, const int64_t* segs, int64_t n_segs,
+                                    int64_t block, uint64_t* out, int threads) {
+  row_geom* rows = NULL;
+  const int64_t n = build_rows(segs, n_segs, block, &rows);
+  synth_job base = {seed, rows, 0, 0, block, 0, out};
+  run_synth(synth_rows_worker, base, n, threads);
+  free(rows);
+  return n;
+}
+
+void ew_oracle_block_sums_synthetic_mt(uint64_t seed, int64_t total_bytes, int64_t block,
+                                       uint64_t* out, int threads) {
+  synth_job base = {seed, NULL, 0, 0, block, total_bytes, out};
+  run_synth(synth_blocks_worker, base, (total_bytes + block - 1) / block, threads);
+}

@@ -52,6 +52,12 @@ void ew_oracle_adam_step(const float* grad, float* master, float* exp_avg, float
                          uint16_t* param, int64_t n, double lr, double b1, double b2, double eps,
                          double wd, int64_t step);
 
+/* synthetic-state rows / whole-space block sums on T threads (no buffer) */
+int64_t ew_oracle_rows_synthetic_mt(uint64_t seed, const int64_t* segs, int64_t n_segs,
+                                    int64_t block, uint64_t* out, int threads);
+void ew_oracle_block_sums_synthetic_mt(uint64_t seed, int64_t total_bytes, int64_t block,
+                                       uint64_t* out, int threads);
+
 #ifdef __cplusplus
 }
 #endif

@@ -12,6 +12,7 @@ Two libraries:
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 from typing import Dict, List, Optional, Sequence, Tuple
 
@@ -23,6 +24,10 @@ REF_LIB = HERE / "_ref" / "libelaskit_ref.so"
 
 P = C.POINTER
 i32, i64, u32, u64, f64, vp = C.c_int, C.c_int64, C.c_uint32, C.c_uint64, C.c_double, C.c_void_p
+
+
+def _cores() -> int:
+    return max(1, len(os.sched_getaffinity(0)))
 
 
 def _np_ptr(a: np.ndarray, ctype):
@@ -47,6 +52,9 @@ class Oracle:
         L.ew_oracle_row_sums.argtypes = [P(i64), i64, i64, vp, P(u64)]
         L.ew_oracle_row_sums.restype = i64
         L.ew_oracle_block_sums_synthetic.argtypes = [u64, i64, i64, P(u64)]
+        L.ew_oracle_rows_synthetic_mt.argtypes = [u64, P(i64), i64, i64, P(u64), C.c_int]
+        L.ew_oracle_rows_synthetic_mt.restype = i64
+        L.ew_oracle_block_sums_synthetic_mt.argtypes = [u64, i64, i64, P(u64), C.c_int]
         L.ew_oracle_fill_synthetic.argtypes = [P(i64), i64, u64, vp]
         L.ew_oracle_interleaved.argtypes = [P(i64), i32, P(i32), i32, P(i32), P(i64)]
         L.ew_oracle_interleaved.restype = i64
@@ -121,6 +129,24 @@ class Oracle:
         nb = (total + block_bytes - 1) // block_bytes
         out = np.zeros(2 * max(1, nb), dtype=np.uint64)
         self.lib.ew_oracle_block_sums_synthetic(seed, total, block_bytes, _np_ptr(out, u64))
+        return out[:2 * nb]
+
+    def rows_synthetic_mt(self, segments, block_bytes: int, seed: int,
+                          threads: int = 0) -> np.ndarray:
+        """Rows of the synthetic state placed by `segments`, no buffer."""
+        s = self._segs(segments)
+        n = self.lib.ew_oracle_num_rows(_np_ptr(s, i64), len(s), block_bytes)
+        out = np.zeros(2 * max(1, n), dtype=np.uint64)
+        self.lib.ew_oracle_rows_synthetic_mt(seed, _np_ptr(s, i64), len(s), block_bytes,
+                                             _np_ptr(out, u64), threads or _cores())
+        return out[:2 * n]
+
+    def block_sums_synthetic_mt(self, seed: int, total: int, block_bytes: int,
+                                threads: int = 0) -> np.ndarray:
+        nb = (total + block_bytes - 1) // block_bytes
+        out = np.zeros(2 * max(1, nb), dtype=np.uint64)
+        self.lib.ew_oracle_block_sums_synthetic_mt(seed, total, block_bytes, _np_ptr(out, u64),
+                                                   threads or _cores())
         return out[:2 * nb]
 
     def fill_synthetic(self, segments, nbytes: int, seed: int) -> np.ndarray:

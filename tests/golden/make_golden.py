@@ -11,8 +11,11 @@ Sources, by fixture:
   plan_golden.json        reference overlap_matrix (oracle/_ref) at the
                           BASELINE configs: entry counts, bytes moved, sha256
                           of the entry list, per-rank lane bytes.
-  checksum_golden.json    PARITY UNPINNED (no reference checksum exists): the
-                          oracle restatement's row sums for fixed inputs.
+  checksum_golden.json    no reference checksum exists: row sums for fixed
+                          inputs from oracle/checksum_spec.py, the pure-Python
+                          restatement of the ew_api.h spec that shares no code
+                          with oracle/ew_oracle.c (the C oracle and the GPU are
+                          both checked against it).
   reduce_golden.json      oracle fixed-point fold for a fixed small input.
 """
 from __future__ import annotations
@@ -27,6 +30,7 @@ import numpy as np
 ROOT = Path(__file__).resolve().parents[2]
 sys.path.insert(0, str(ROOT))
 
+from oracle import checksum_spec  # noqa: E402
 from oracle.ew_oracle import load_oracle, load_reference  # noqa: E402
 from paper_2510_00606_b200 import configs  # noqa: E402
 
@@ -110,14 +114,27 @@ def checksum_golden(orc) -> dict:
             local += length
             g += length + int(rng.integers(1, 40000))
         buf = rng.integers(0, 256, size=local, dtype=np.uint8)
-        rows = orc.row_sums(segs, block, buf)
+        rows = checksum_spec.rows_of_buffer(segs, block, buf.tobytes())
+        assert rows == [int(x) for x in orc.row_sums(segs, block, buf)], "C oracle != spec"
         cases.append({"block_bytes": block, "segments": segs,
                       "buf_sha256": hashlib.sha256(buf.tobytes()).hexdigest(),
-                      "buf_seed": 2024, "rows": [str(int(x)) for x in rows]})
-    synth = {str(seed): [str(int(x)) for x in orc.block_sums_synthetic(seed, 300_007, 65536)]
-             for seed in (0, 2024)}
-    return {"unpinned": "builder-defined checksum; no reference implementation exists",
-            "cases": cases, "synthetic_300007": synth}
+                      "buf_seed": 2024, "rows": [str(x) for x in rows]})
+    synth = {}
+    for seed in (0, 2024):
+        s = checksum_spec.synthetic_block_sums(seed, 300_007, 65536)
+        assert s == [int(x) for x in orc.block_sums_synthetic(seed, 300_007, 65536)]
+        synth[str(seed)] = [str(x) for x in s]
+    # synthetic state placed by a misaligned 3-segment map: rows straight
+    # from the spec (GPU fill + snapshot must reproduce them)
+    segs3 = [{"global_lo": 13, "length": 9001, "local_off": 0},
+             {"global_lo": 70003, "length": 4, "local_off": 9001},
+             {"global_lo": 131069, "length": 70000, "local_off": 9005}]
+    synth_rows = {str(seed): [str(x) for x in checksum_spec.rows_of_synthetic(segs3, 4096, seed)]
+                  for seed in (0, 2024)}
+    return {"spec": "include/ew_api.h 'Checksum spec'; no reference implementation exists",
+            "generated_by": "oracle/checksum_spec.py (independent of oracle/ew_oracle.c)",
+            "cases": cases, "synthetic_300007": synth,
+            "synthetic_rows": {"block_bytes": 4096, "segments": segs3, "rows": synth_rows}}
 
 
 def reduce_golden(orc) -> dict:

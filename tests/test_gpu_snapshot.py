@@ -155,6 +155,20 @@ def test_checksum_golden_on_gpu(golden_dir):
         dev.checksum(m, buf, rows)
         torch.cuda.synchronize()
         assert [str(int(x)) for x in to_host_u64(rows)[:2 * m.num_rows]] == case["rows"]
+    # GPU synthetic fill + fused snapshot rows == the spec restatement's rows
+    sr = g["synthetic_rows"]
+    segs = np.zeros(len(sr["segments"]), dtype=fabric.SEGMENT_DTYPE)
+    for i, s in enumerate(sr["segments"]):
+        segs[i] = (s["global_lo"], s["length"], s["local_off"])
+    m = dev.ShardMap(segs, sr["block_bytes"])
+    for seed, want in sr["rows"].items():
+        live = dev.empty_bytes(m.nbytes)
+        dev.fill_synthetic(m, live, int(seed))
+        snap = dev.empty_bytes(m.nbytes)
+        rows = m.new_row_sums()
+        dev.snapshot(m, live, snap, rows)
+        torch.cuda.synchronize()
+        assert [str(int(x)) for x in to_host_u64(rows)[:2 * m.num_rows]] == want
 
 
 def test_empty_and_tiny_shards(oracle):
@@ -175,10 +189,41 @@ def test_empty_and_tiny_shards(oracle):
         assert torch.equal(snap[:total], live[:total])
 
 
+@pytest.mark.timeout(900)
+def test_full_size_7b_rows_and_blocks_vs_oracle(oracle):
+    """Config B at full size: every checksum row of rank 3's 11.79 GB shard
+    (GPU fill + fused snapshot) equals the C oracle's rows recomputed from
+    the synthetic words on the host cores, and the rows of all 8 ranks'
+    shards, folded into block sums, equal the oracle's block sums of the
+    whole 94.3 GB space."""
+    cfg = configs.llama2_7b()
+    layout = fabric.interleaved_layout(cfg.layer_bytes, range(8))
+    block = 65536
+    nb = (cfg.total_bytes + block - 1) // block
+    acc = torch.zeros(2 * nb, dtype=torch.int64, device="cuda")
+    n_max = max(layout.shard_bytes(r) for r in range(8))
+    live = dev.empty_bytes(n_max)
+    snap = dev.empty_bytes(n_max)
+    for r in range(8):
+        m = dev.ShardMap(layout.segments(r), block)
+        dev.fill_synthetic(m, live, 0)
+        rows = m.new_row_sums()
+        dev.snapshot(m, live, snap, rows)
+        dev.rows_to_blocks(m, rows, acc)
+        if r == 3:
+            torch.cuda.synchronize()
+            want = oracle.rows_synthetic_mt(layout.segments(r), block, 0)
+            assert np.array_equal(to_host_u64(rows)[:2 * m.num_rows], want)
+    torch.cuda.synchronize()
+    del live, snap
+    torch.cuda.empty_cache()
+    assert np.array_equal(to_host_u64(acc), oracle.block_sums_synthetic_mt(0, cfg.total_bytes,
+                                                                           block))
+
+
 def test_full_size_7b_shard_properties():
-    """At the config-B per-rank size (11.79 GB): snapshot then verify passes,
-    a single flipped bit is caught, and the rank's checksum rows sum (mod
-    2^64) to the rows of the synthetic generator recomputed separately."""
+    """At the config-B per-rank size (11.79 GB): snapshot then verify passes
+    and a single flipped bit is caught."""
     cfg = configs.llama2_7b()
     layout = fabric.interleaved_layout(cfg.layer_bytes, range(8))
     m = dev.ShardMap(layout.segments(3), 65536)

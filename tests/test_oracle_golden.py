@@ -71,6 +71,44 @@ def test_checksum_golden(oracle, golden_dir):
         assert [str(int(x)) for x in got] == rows
 
 
+def test_checksum_spec_reproduces_golden(golden_dir):
+    """The golden rows come from oracle/checksum_spec.py, the pure-Python
+    restatement of the ew_api.h spec (no code shared with the C oracle)."""
+    from oracle import checksum_spec as cs
+    g = json.loads((golden_dir / "checksum_golden.json").read_text())
+    for case in g["cases"]:
+        buf = _fixture_buffer(case).tobytes()
+        assert [str(x) for x in cs.rows_of_buffer(case["segments"], case["block_bytes"],
+                                                  buf)] == case["rows"]
+    for seed, rows in g["synthetic_300007"].items():
+        assert [str(x) for x in cs.synthetic_block_sums(int(seed), 300_007, 65536)] == rows
+    sr = g["synthetic_rows"]
+    for seed, rows in sr["rows"].items():
+        assert [str(x) for x in cs.rows_of_synthetic(sr["segments"], sr["block_bytes"],
+                                                     int(seed))] == rows
+
+
+def test_c_oracle_synthetic_rows_match_spec_golden(oracle, golden_dir):
+    """C oracle, two ways (fill + row_sums, and the buffer-free MT rows the
+    full-size GPU tests check against) == the spec's golden rows."""
+    sr = json.loads((golden_dir / "checksum_golden.json").read_text())["synthetic_rows"]
+    total = sum(s["length"] for s in sr["segments"])
+    for seed, rows in sr["rows"].items():
+        buf = oracle.fill_synthetic(sr["segments"], total, int(seed))
+        assert [str(int(x)) for x in oracle.row_sums(sr["segments"], sr["block_bytes"],
+                                                     buf)] == rows
+        for threads in (1, 3):
+            got = oracle.rows_synthetic_mt(sr["segments"], sr["block_bytes"], int(seed), threads)
+            assert [str(int(x)) for x in got] == rows
+
+
+def test_c_oracle_mt_block_sums(oracle):
+    for total in (1, 8, 4097, 300_007):
+        for threads in (1, 4):
+            assert np.array_equal(oracle.block_sums_synthetic_mt(9, total, 4096, threads),
+                                  oracle.block_sums_synthetic(9, total, 4096))
+
+
 def _fixture_buffer(case) -> np.ndarray:
     """Replays make_golden.checksum_golden's generator stream for one case."""
     rng = np.random.default_rng(2024)
