@@ -37,6 +37,22 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "snapshot+verify GB/s per GPU; reshard MTTR (ms) 8→7 B200 at 7B ZeRO state"
 FALLBACK_HBM_GBS = 6650.0
+# config B's ZeroLayout layer sizes (llama2-7b, 14 B/param),
+# restated here so the reference arm builds its workload without importing the
+# product package (tests/test_cpu_baselines.py pins it to configs.llama2_7b)
+LLAMA2_7B_LAYER_BYTES = [14 * p for p in [131_072_000] + [202_383_360] * 32 + [131_076_096]]
+HEADLINE_SHARD_RANK = 0  # GPU k holds rank (k mod 8)'s shard; rank 0 at N=1
+
+
+def workload_config(shard_bytes: int, block_bytes: int, world: int) -> dict:
+    """The headline workload, identical in both arms' JSON lines."""
+    return {"workload": "llama2-7b ZeRO interleaved DP=8, one rank's shard per GPU: "
+                        "snapshot (copy + per-block checksum) then verify",
+            "shard_bytes": shard_bytes, "block_bytes": block_bytes,
+            "bytes_per_step_per_gpu": 3 * shard_bytes,
+            "bytes_counted": "HBM read+write: 2S snapshot + S verify",
+            "l2": "inputs 11.8 GB/GPU >> 126 MB L2; no flush needed",
+            "parallelism": f"dp{world} (independent shards)"}
 
 
 def parse_args():
@@ -186,7 +202,7 @@ def run_snapshot(args, rank, world, local, out):
 
     cfg = configs.llama2_7b()
     layout = fabric.interleaved_layout(cfg.layer_bytes, range(cfg.dp))
-    shard_rank = rank % cfg.dp
+    shard_rank = (HEADLINE_SHARD_RANK + rank) % cfg.dp
     segs = layout.segments(shard_rank)
     S = layout.shard_bytes(shard_rank)
     m = dev.ShardMap(segs, args.block_bytes)
@@ -250,13 +266,7 @@ def run_snapshot(args, rank, world, local, out):
         "n_gpus": world, "steps": K, "warmup": args.warmup, "ms_per_step": round(step * 1e3, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (word i = splitmix64(seed ^ i))",
-        "config": {"workload": "llama2-7b ZeRO interleaved DP=8, one rank's shard per GPU: "
-                               "snapshot (copy + per-block checksum) then verify",
-                   "shard_bytes": S, "block_bytes": args.block_bytes,
-                   "bytes_per_step_per_gpu": bytes_step,
-                   "bytes_counted": "HBM read+write: 2S snapshot + S verify",
-                   "l2": "inputs 11.8 GB/GPU >> 126 MB L2; no flush needed",
-                   "parallelism": f"dp{world} (independent shards)"},
+        "config": workload_config(S, args.block_bytes, world),
         "per_gpu_gbs": round(bytes_step / step / 1e9, 2),
         "state_gbs_per_gpu": round(S / step / 1e9, 2),
         "kernels": {"ew_snapshot_ms": round(t_snap * 1e3, 4), "ew_verify_ms": round(t_ver * 1e3, 4),
@@ -363,8 +373,9 @@ def run_cpu_baseline(args, out, segs, S):
     assert bad == 0
     out["cpu_baseline"] = {"value": round(3 * local / dt / 1e9, 3), "unit": "GB/s",
                            "cores": threads, "kind": "port",
-                           "sample": f"first {local} bytes of the 7B rank-3 shard, {reps} reps "
-                                     "(memcpy + word-wise checksum, then verify re-read)"}
+                           "sample": f"first {local} bytes of the 7B rank-{HEADLINE_SHARD_RANK} "
+                                     f"shard (the GPU arm's shard at N=1), {reps} reps (memcpy + "
+                                     "word-wise checksum, then verify re-read)"}
     return out["cpu_baseline"]
 
 
@@ -1543,56 +1554,88 @@ def bench_b200(args):
 
 
 def bench_reference(args):
-    """CPU path on the host cores, rank 0 only (other ranks exit 0)."""
+    """The reference arm: the CPU path on the host cores, rank 0 only (other
+    ranks exit 0), on the GPU arm's exact workload and config — rank
+    HEADLINE_SHARD_RANK's full config-B shard (11.79 GB).  The layout comes
+    from the unmodified reference sources (oracle/_ref: ZeroLayout::shard
+    composed per SURVEY A4); snapshot + verify is the oracle port on every
+    host thread (the reference has no byte-moving snapshot or checksum).
+    Nothing from the product package is imported or loaded here."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import numpy as np
     from oracle.ew_oracle import load_oracle, load_reference
-    from paper_2510_00606_b200 import configs, fabric
 
-    cfg = configs.llama2_7b()
-    layout = fabric.interleaved_layout(cfg.layer_bytes, range(cfg.dp))
-    segs = layout.segments(3)
-    S = layout.shard_bytes(3)
-    out = {}
-    cb = run_cpu_baseline(argparse.Namespace(cpu_sample_bytes=args.cpu_sample_bytes,
-                                             block_bytes=args.block_bytes), out, segs, S)
-    res = {"metric": METRIC, "value": cb["value"], "unit": "GB/s", "n_gpus": args.gpus,
-           "steps": args.steps, "warmup": args.warmup, "impl": "reference",
-           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+    orc, ref = load_oracle(), load_reference()
+    if ref is None:
+        raise SystemExit("oracle/_ref is not built (make -C oracle where /root/reference exists)")
+    ivs = ref.interleaved(LLAMA2_7B_LAYER_BYTES, range(8))[HEADLINE_SHARD_RANK]
+    segs, local = [], 0
+    for lo, hi in ivs:
+        segs.append({"global_lo": int(lo), "length": int(hi - lo), "local_off": local})
+        local += int(hi - lo)
+    S = local
+    threads = len(os.sched_getaffinity(0))
+    live = orc.fill_synthetic_mt(segs, S, 0, threads)
+    snap = np.zeros_like(live)
+    block = args.block_bytes
+    for _ in range(args.warmup):
+        sums = orc.snapshot_mt(segs, block, live, snap, threads)
+        assert orc.verify_mt(segs, block, snap, sums, threads) == 0
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        sums = orc.snapshot_mt(segs, block, live, snap, threads)
+        bad = orc.verify_mt(segs, block, snap, sums, threads)
+        times.append(time.perf_counter() - t0)
+        assert bad == 0, "reference arm: verification failed"
+    step = sum(times) / len(times)
+    value = round(3 * S / step / 1e9, 3)
+    res = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(step * 1e3, 3),
+           "impl": "reference", "higher_is_better": True, "scaling": "weak",
+           "vs_baseline": None, "dtype": "u64",
            "data": "synthetic (word i = splitmix64(seed ^ i))",
-           "config": {"workload": "llama2-7b ZeRO interleaved DP=8, one rank's shard: snapshot "
-                                  "(copy + per-block checksum) then verify, bounded sample on host "
-                                  "cores", "bytes_counted": "2S + S per step",
-                      "block_bytes": args.block_bytes},
-           "cpu_baseline": cb,
-           "e2e": {"value": cb["value"], "unit": "GB/s", "h2d_bytes_per_step": 0,
+           "config": workload_config(S, block, args.gpus),
+           "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+                            "sample": f"the full rank-{HEADLINE_SHARD_RANK} config-B shard "
+                                      f"({S} bytes) per step: oracle snapshot (memcpy + "
+                                      "word-wise checksum) then verify re-read, layout from "
+                                      "oracle/_ref (unmodified reference sources)"},
+           "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
-    ref = load_reference()
-    if ref is not None:
-        extra = {}
-        for name, c in (("per-layer", cfg), ("per-tensor", configs.llama2_7b_per_tensor())):
-            src = ref.interleaved(c.layer_bytes, range(8))
-            dst = ref.interleaved(c.layer_bytes, [0, 1, 2, 4, 5, 6, 7])
-            secs = []
-            for _ in range(5):
-                _, _, s = ref.overlap_matrix(src, dst, c.total_bytes, [3], list(range(8)))
-                secs.append(s)
-            extra[f"overlap_matrix_8to7_{name}_ms"] = round(min(secs) * 1e3, 3)
-        t0 = time.perf_counter()
-        ref.draw(0, 0, 1, 0, 4_000_000)
-        extra["draw_muniform_per_s_1thread"] = round(4.0 / (time.perf_counter() - t0), 1)
-        g = np.random.default_rng(5).normal(size=(5, 4_194_304))
-        t0 = time.perf_counter()
-        ref.weighted_grad_average(np.full(5, 0.2), g)
-        dt = time.perf_counter() - t0
-        extra["weighted_grad_average_gbs_1thread"] = round(5 * 4_194_304 * 8 / dt / 1e9, 2)
-        res["reference_cpu"] = extra
-        res["cpu_baseline"]["reference_planner"] = "oracle/_ref (unmodified reference sources)"
+    extra = {}
+    cfg_pt = _llama2_7b_per_tensor_layer_bytes()
+    for name, lb in (("per-layer", LLAMA2_7B_LAYER_BYTES), ("per-tensor", cfg_pt)):
+        src = ref.interleaved(lb, range(8))
+        dst = ref.interleaved(lb, [0, 1, 2, 4, 5, 6, 7])
+        secs = []
+        for _ in range(5):
+            _, _, sec = ref.overlap_matrix(src, dst, sum(lb), [3], list(range(8)))
+            secs.append(sec)
+        extra[f"overlap_matrix_8to7_{name}_ms"] = round(min(secs) * 1e3, 3)
+    t0 = time.perf_counter()
+    ref.draw(0, 0, 1, 0, 4_000_000)
+    extra["draw_muniform_per_s_1thread"] = round(4.0 / (time.perf_counter() - t0), 1)
+    g = np.random.default_rng(5).normal(size=(5, 4_194_304))
+    t0 = time.perf_counter()
+    ref.weighted_grad_average(np.full(5, 0.2), g)
+    dt = time.perf_counter() - t0
+    extra["weighted_grad_average_gbs_1thread"] = round(5 * 4_194_304 * 8 / dt / 1e9, 2)
+    res["reference_cpu"] = extra
     emit(json.dumps(res))
     if args.json_out:
         Path(args.json_out).write_text(json.dumps(res) + "\n")
+
+
+def _llama2_7b_per_tensor_layer_bytes():
+    h, f = 4096, 11008
+    layers = [131_072_000]
+    for _ in range(32):
+        layers += [h * h] * 4 + [h * f] * 3 + [h, h]
+    layers += [h, 131_072_000]
+    return [14 * p for p in layers]
 
 
 _JSON_FD = None

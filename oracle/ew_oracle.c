@@ -613,3 +613,39 @@ void ew_oracle_block_sums_synthetic_mt(uint64_t seed, int64_t total_bytes, int64
   synth_job base = {seed, NULL, 0, 0, block, total_bytes, out};
   run_synth(synth_blocks_worker, base, (total_bytes + block - 1) / block, threads);
 }
+
+/* ew_oracle_fill_synthetic on T threads: the packed buffer [0, total) is cut
+ * into T byte ranges, each thread fills the segment bytes inside its range. */
+typedef struct {
+  const int64_t* segs;
+  int64_t n_segs, lo, hi;
+  uint64_t seed;
+  uint8_t* buf;
+} fill_job;
+
+static void* fill_worker(void* p) {
+  fill_job* j = (fill_job*)p;
+  for (int64_t k = 0; k < j->n_segs; ++k) {
+    const int64_t glo = j->segs[3 * k], len = j->segs[3 * k + 1], loff = j->segs[3 * k + 2];
+    const int64_t a = loff > j->lo ? loff : j->lo;
+    const int64_t e = loff + len < j->hi ? loff + len : j->hi;
+    for (int64_t x = a; x < e; ++x) {
+      const int64_t g = glo + (x - loff);
+      j->buf[x] = (uint8_t)(ew_oracle_splitmix64(j->seed ^ (uint64_t)(g / 8)) >> (8 * (g % 8)));
+    }
+  }
+  return NULL;
+}
+
+void ew_oracle_fill_synthetic_mt(const int64_t* segs, int64_t n_segs, uint64_t seed,
+                                 uint8_t* buf, int64_t total, int threads) {
+  if (threads < 1) threads = 1;
+  if (threads > 256) threads = 256;
+  pthread_t th[256];
+  fill_job jobs[256];
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (fill_job){segs, n_segs, total * t / threads, total * (t + 1) / threads, seed, buf};
+    pthread_create(&th[t], NULL, fill_worker, &jobs[t]);
+  }
+  for (int t = 0; t < threads; ++t) pthread_join(th[t], NULL);
+}

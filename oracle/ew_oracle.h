@@ -58,6 +58,9 @@ int64_t ew_oracle_rows_synthetic_mt(uint64_t seed, const int64_t* segs, int64_t 
 void ew_oracle_block_sums_synthetic_mt(uint64_t seed, int64_t total_bytes, int64_t block,
                                        uint64_t* out, int threads);
 
+void ew_oracle_fill_synthetic_mt(const int64_t* segs, int64_t n_segs, uint64_t seed,
+                                 uint8_t* buf, int64_t total, int threads);
+
 #ifdef __cplusplus
 }
 #endif

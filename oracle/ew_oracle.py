@@ -55,6 +55,7 @@ class Oracle:
         L.ew_oracle_rows_synthetic_mt.argtypes = [u64, P(i64), i64, i64, P(u64), C.c_int]
         L.ew_oracle_rows_synthetic_mt.restype = i64
         L.ew_oracle_block_sums_synthetic_mt.argtypes = [u64, i64, i64, P(u64), C.c_int]
+        L.ew_oracle_fill_synthetic_mt.argtypes = [P(i64), i64, u64, vp, i64, C.c_int]
         L.ew_oracle_fill_synthetic.argtypes = [P(i64), i64, u64, vp]
         L.ew_oracle_interleaved.argtypes = [P(i64), i32, P(i32), i32, P(i32), P(i64)]
         L.ew_oracle_interleaved.restype = i64
@@ -148,6 +149,13 @@ class Oracle:
         self.lib.ew_oracle_block_sums_synthetic_mt(seed, total, block_bytes, _np_ptr(out, u64),
                                                    threads or _cores())
         return out[:2 * nb]
+
+    def fill_synthetic_mt(self, segments, nbytes: int, seed: int, threads: int = 0) -> np.ndarray:
+        s = self._segs(segments)
+        buf = np.empty(max(1, nbytes), dtype=np.uint8)
+        self.lib.ew_oracle_fill_synthetic_mt(_np_ptr(s, i64), len(s), seed, buf.ctypes.data_as(vp),
+                                             nbytes, threads or _cores())
+        return buf[:nbytes]
 
     def fill_synthetic(self, segments, nbytes: int, seed: int) -> np.ndarray:
         s = self._segs(segments)

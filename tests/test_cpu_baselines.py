@@ -40,3 +40,26 @@ def test_plan_executor_mt_moves_every_entry(oracle):
     for e in entries:
         moved[int(e["lo"]):int(e["hi"])] = True
     assert np.array_equal(out[moved], state[moved]) and moved.any()
+
+
+def test_reference_arm_workload_matches_gpu_arm(reference):
+    """bench.py's reference arm restates config B's layer sizes (it must not
+    import the product package); they, the per-tensor variant, and the
+    reference library's interleaved rank-0 shard equal the GPU arm's."""
+    import importlib.util
+    from pathlib import Path
+    spec = importlib.util.spec_from_file_location(
+        "bench_mod", Path(__file__).resolve().parents[1] / "bench.py")
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    assert bench.LLAMA2_7B_LAYER_BYTES == configs.llama2_7b().layer_bytes
+    assert bench._llama2_7b_per_tensor_layer_bytes() == \
+        configs.llama2_7b_per_tensor().layer_bytes
+    r = bench.HEADLINE_SHARD_RANK
+    lay = fabric.interleaved_layout(configs.llama2_7b().layer_bytes, range(8))
+    ref_ivs = reference.interleaved(bench.LLAMA2_7B_LAYER_BYTES, range(8))[r]
+    segs = lay.segments(r)
+    assert [(int(s["global_lo"]), int(s["global_lo"] + s["length"])) for s in segs] == \
+        [(int(a), int(b)) for a, b in ref_ivs]
+    assert bench.workload_config(lay.shard_bytes(r), 65536, 1) == \
+        bench.workload_config(sum(b - a for a, b in ref_ivs), 65536, 1)
