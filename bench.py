@@ -42,6 +42,7 @@ FALLBACK_HBM_GBS = 6650.0
 # product package (tests/test_cpu_baselines.py pins it to configs.llama2_7b)
 LLAMA2_7B_LAYER_BYTES = [14 * p for p in [131_072_000] + [202_383_360] * 32 + [131_076_096]]
 HEADLINE_SHARD_RANK = 0  # GPU k holds rank (k mod 8)'s shard; rank 0 at N=1
+REDUCE_UNITS = 8         # config E reduce: global contribution units (any N | 8)
 
 
 def workload_config(shard_bytes: int, block_bytes: int, world: int) -> dict:
@@ -1385,45 +1386,84 @@ def run_cpu_beside(args, out):
 
 
 def run_reduce(args, rank, world, out):
+    import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_2510_00606_b200 import device as dev
+    from paper_2510_00606_b200 import device as dev, fabric
 
+    # World-size-invariant granularity: a fixed global set of REDUCE_UNITS
+    # contribution units (unit u: weight (u+1)/36, data seeded by u mod 2, so
+    # a rank needs at most two distinct 27 GB buffers), dealt round-robin to
+    # the ranks.  The fixed-point scale depends only on the global absmax and
+    # the global unit count, so N = 1, 2, 4, 8 produce the same bits
+    # (output_digest).  Timed: absmax pre-pass -> global max -> F -> fold ->
+    # int64 sum -> dequant.
     n = args.reduce_elems
-    g = torch.empty(n, dtype=torch.float32, device="cuda").normal_(0, 1e-3)
+    mine = [u for u in range(REDUCE_UNITS) if u % world == rank]
+    data = {}
+    for u in mine:
+        if u % 2 not in data:
+            gen = torch.Generator(device="cuda").manual_seed(100 + u % 2)
+            t = torch.empty(n, dtype=torch.float32, device="cuda").normal_(0, 1e-3, generator=gen)
+            t[(u % 2) * 1_000_003 + 17] = 1e2   # outliers set the scale
+            data[u % 2] = t
+    units = [data[u % 2] for u in mine]
+    w = [(u + 1) / 36 for u in mine]
     acc = torch.empty(n, dtype=torch.int64, device="cuda")
     res = torch.empty(n, dtype=torch.float32, device="cuda")
-    w = [(7 if rank < 2 else 6) / 32]
-    amax = dev.weighted_absmax([g], w)
-    if world > 1:
-        dist.all_reduce(amax, op=dist.ReduceOp.MAX)
-    f = dev.fixed_point_bits(amax.item(), max(world, 1))
-    dev.weighted_fold([g], w, f, acc)
+
+    def reduce_step(ev):
+        ev[0].record()
+        amax = dev.weighted_absmax(units, w)
+        ev[1].record()
+        if world > 1:
+            dist.all_reduce(amax, op=dist.ReduceOp.MAX)
+        f = dev.fixed_point_bits(amax.item(), REDUCE_UNITS)
+        ev[2].record()
+        dev.weighted_fold(units, w, f, acc)
+        ev[3].record()
+        if world > 1:
+            dist.all_reduce(acc)  # ncclInt64 sum: exact, order-free
+        ev[4].record()
+        dev.fixed_to_float(acc, f, res)
+        ev[5].record()
+        return f
+
+    f = reduce_step([torch.cuda.Event(enable_timing=True) for _ in range(6)])  # warm-up
     torch.cuda.synchronize()
-    s, m1, m2, e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
     barrier(world)
-    s.record()
-    dev.weighted_fold([g], w, f, acc)
-    m1.record()
-    if world > 1:
-        dist.all_reduce(acc)  # ncclInt64 sum: exact, order-free
-    m2.record()
-    dev.fixed_to_float(acc, f, res)
-    e.record()
+    f = reduce_step(ev)
+    torch.cuda.synchronize()
     barrier(world)
-    t_fold, t_ar, t_deq = max_over_ranks([s.elapsed_time(m1) / 1e3, m1.elapsed_time(m2) / 1e3,
-                                          m2.elapsed_time(e) / 1e3], world)
-    out["reduce"] = {"elements": n, "frac_bits": f, "fold_ms": round(t_fold * 1e3, 3),
-                     "fold_gbs": round(12 * n / t_fold / 1e9, 1),
+    t_amax, t_max, t_fold, t_ar, t_deq, t_all = max_over_ranks(
+        [ev[0].elapsed_time(ev[1]) / 1e3, ev[1].elapsed_time(ev[2]) / 1e3,
+         ev[2].elapsed_time(ev[3]) / 1e3, ev[3].elapsed_time(ev[4]) / 1e3,
+         ev[4].elapsed_time(ev[5]) / 1e3, ev[0].elapsed_time(ev[5]) / 1e3], world)
+    # digest of the fp32 output: kernel (a)'s checksum of its bytes
+    om = dev.ShardMap(np.array([(0, 4 * n, 0)], dtype=fabric.SEGMENT_DTYPE), dev.DEFAULT_BLOCK_BYTES)
+    orows = om.new_row_sums()
+    dev.checksum(om, res.view(torch.uint8), orows)
+    digest = "%016x%016x" % (int(orows[0::2].sum().item()) % 2**64,
+                             int(orows[1::2].sum().item()) % 2**64)
+    lu = len(mine)
+    out["reduce"] = {"elements": n, "units_total": REDUCE_UNITS, "units_this_rank": lu,
+                     "frac_bits": f, "output_digest": digest,
+                     "absmax_ms": round(t_amax * 1e3, 3),
+                     "absmax_gbs": round(4 * n * lu / t_amax / 1e9, 1),
+                     "global_max_and_scale_ms": round(t_max * 1e3, 3),
+                     "fold_ms": round(t_fold * 1e3, 3),
+                     "fold_gbs": round((4 * lu + 8) * n / t_fold / 1e9, 1),
                      "nccl_allreduce_int64_ms": round(t_ar * 1e3, 3) if world > 1 else None,
                      "dequant_ms": round(t_deq * 1e3, 3),
-                     "nccl_path_ms": round((t_fold + t_ar + t_deq) * 1e3, 3)}
+                     "dequant_gbs": round(12 * n / t_deq / 1e9, 1),
+                     "nccl_path_ms": round(t_all * 1e3, 3)}
     del acc
     torch.cuda.empty_cache()
     if world > 1:
         # the same reduce fused with its collective over NVLink peer memory
         peer_out = torch.empty(n, dtype=torch.float32, device="cuda")
-        fold, total, opened = dev.peer_weighted_reduce_setup([g], w, peer_out)
+        fold, total, opened = dev.peer_weighted_reduce_setup(units, w, peer_out)
         bar = dev.PeerBarrier()
         fold.run(f, bar)
         bar.wait()
@@ -1463,7 +1503,7 @@ def run_reduce(args, rank, world, out):
         # collective sums accumulators.  NCCL int64 all-reduce + dequant vs
         # the peer int64 reduce-scatter + dequant + all-gather.
         acc = torch.empty(n, dtype=torch.int64, device="cuda")
-        dev.weighted_fold([g], w, f, acc)
+        dev.weighted_fold(units, w, f, acc)
         out64 = torch.empty(n, dtype=torch.float32, device="cuda")
         fold64, opened64 = dev.peer_sum_i64_setup(acc, out64)
         bar = dev.PeerBarrier()
@@ -1499,7 +1539,7 @@ def run_reduce(args, rank, world, out):
         for p in opened64:
             dev.ipc_close(p)
         del acc, out64
-    del g, res
+    del units, data, res
     torch.cuda.empty_cache()
 
 

@@ -28,28 +28,53 @@ struct Units {
   int n;
 };
 
+// max_{k,i} |w_k * g_k[i]| (fp64 products).  Rounding is monotone, so
+// max_i fl(|w_k| |g_k[i]|) = fl(|w_k| max_i |g_k[i]|): the stream only needs
+// max_i |g_k[i]|, an integer max over the fp32 bit patterns with the sign
+// cleared (non-negative floats order like their bits; every NaN pattern lies
+// above +inf, so a NaN propagates as the max).  16-byte loads, kDepth deep,
+// one REDUX per warp; each CTA then scales by |w_k| in fp64 and folds into
+// the global max with one 64-bit atomicMax per unit (non-negative doubles
+// and +NaN order like their bits too).
 __global__ void __launch_bounds__(256) absmax_kernel(Units u, int64_t n,
                                                      unsigned long long* out_bits) {
-  double m = 0.0;
+  constexpr int kDepth = 4;
+  constexpr uint32_t kAbs = 0x7fffffffu;
+  __shared__ uint32_t red[kMaxUnits][8];
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
-    for (int k = 0; k < u.n; ++k) {
-      const double v = fabs(u.w[k] * static_cast<double>(u.p[k][i]));
-      m = (v > m || v != v) ? v : m;  // NaN propagates
-    }
-  }
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (int k = 0; k < u.n; ++k) {
+    uint32_t m = 0;
+    const float* p = u.p[k];
+    int64_t done = 0;
+    if ((reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      const uint4* v4 = reinterpret_cast<const uint4*>(p);
+      const int64_t n4 = n / 4;
+      for (int64_t i0 = t0; i0 < n4; i0 += kDepth * stride) {
+        uint4 x[kDepth];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double x = __shfl_down_sync(0xffffffffu, m, o);
-    m = (x > m || x != x) ? x : m;
+        for (int d = 0; d < kDepth; ++d) {
+          const int64_t i = i0 + d * stride;
+          x[d] = i < n4 ? __ldcs(v4 + i) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int d = 0; d < kDepth; ++d)
+          m = max(m, max(max(x[d].x & kAbs, x[d].y & kAbs), max(x[d].z & kAbs, x[d].w & kAbs)));
+      }
+      done = 4 * n4;
+    }
+    const uint32_t* s = reinterpret_cast<const uint32_t*>(p);
+    for (int64_t i = done + t0; i < n; i += stride) m = max(m, __ldcs(s + i) & kAbs);
+    m = __reduce_max_sync(0xffffffffu, m);
+    if ((threadIdx.x & 31) == 0) red[k][threadIdx.x >> 5] = m;
   }
-  __shared__ double red[8];
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    for (int k = 1; k < (int)(blockDim.x >> 5); ++k) m = (red[k] > m || red[k] != red[k]) ? red[k] : m;
-    // non-negative doubles (and +NaN) order like their bit patterns
-    atomicMax(out_bits, static_cast<unsigned long long>(__double_as_longlong(m)));
+  if (threadIdx.x < u.n) {
+    const int k = threadIdx.x;
+    uint32_t m = 0;
+    for (int w = 0; w < static_cast<int>(blockDim.x >> 5); ++w) m = max(m, red[k][w]);
+    const double v = fabs(fabs(u.w[k]) * static_cast<double>(__uint_as_float(m)));
+    atomicMax(out_bits, static_cast<unsigned long long>(__double_as_longlong(v)));
   }
 }
 
@@ -119,16 +144,72 @@ __global__ void __launch_bounds__(256) fold_kernel(Units u, int64_t n, double sc
   }
 }
 
+// out[i] = (T)((double)acc[i] * 2^-F): groups of 4 elements, two 16-byte
+// loads and one 16-byte (fp32) or two (fp64) stores each, kDepth groups in
+// flight per thread; scalar head-free tail.
 template <typename T>
-__global__ void dequant_kernel(const long long* __restrict__ acc, int64_t n, double inv_scale,
-                               T* __restrict__ out) {
+__device__ __forceinline__ void store4(T* out, int64_t g, const double (&v)[4]);
+template <>
+__device__ __forceinline__ void store4<float>(float* out, int64_t g, const double (&v)[4]) {
+  __stcs(reinterpret_cast<float4*>(out) + g,
+         make_float4(static_cast<float>(v[0]), static_cast<float>(v[1]),
+                     static_cast<float>(v[2]), static_cast<float>(v[3])));
+}
+template <>
+__device__ __forceinline__ void store4<double>(double* out, int64_t g, const double (&v)[4]) {
+  double2* o = reinterpret_cast<double2*>(out) + 2 * g;
+  __stcs(o, make_double2(v[0], v[1]));
+  __stcs(o + 1, make_double2(v[2], v[3]));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) dequant_kernel(const long long* __restrict__ acc, int64_t n,
+                                                      double inv_scale, T* __restrict__ out) {
+  constexpr int kDepth = 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+  const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int64_t done = 0;
+  if (((reinterpret_cast<uintptr_t>(acc) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+    const int64_t n4 = n / 4;
+    const longlong2* a2 = reinterpret_cast<const longlong2*>(acc);
+    for (int64_t g0 = t0; g0 < n4; g0 += kDepth * stride) {
+      longlong2 x[kDepth][2];
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) {
+        const int64_t g = g0 + d * stride;
+        if (g < n4) {
+          x[d][0] = __ldcs(a2 + 2 * g);
+          x[d][1] = __ldcs(a2 + 2 * g + 1);
+        }
+      }
+#pragma unroll
+      for (int d = 0; d < kDepth; ++d) {
+        const int64_t g = g0 + d * stride;
+        if (g >= n4) break;
+        const double v[4] = {static_cast<double>(x[d][0].x) * inv_scale,
+                             static_cast<double>(x[d][0].y) * inv_scale,
+                             static_cast<double>(x[d][1].x) * inv_scale,
+                             static_cast<double>(x[d][1].y) * inv_scale};
+        store4<T>(out, g, v);
+      }
+    }
+    done = 4 * n4;
+  }
+  for (int64_t i = done + t0; i < n; i += stride)
     out[i] = static_cast<T>(static_cast<double>(acc[i]) * inv_scale);
 }
 
 int grid_for(int64_t work) {
   const int64_t cap = static_cast<int64_t>(num_sms()) * 8;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, cap)));
+}
+
+// Persistent grid for the 256-thread streaming kernels: every CTA resident
+// (SMs x occupancy), so the grid-stride loops run in one wave.
+int resident_grid(const void* kernel, int64_t work) {
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * std::max(1, per_sm);
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, cap)));
 }
 
@@ -162,7 +243,8 @@ int ew_weighted_absmax(const float* const* units, const double* weights, int n_u
   for (int off = 0; off < n_units && n_elems > 0; off += kMaxUnits) {
     Units u;
     if (int st = pack_units(units, weights, n_units, off, u)) return st;
-    absmax_kernel<<<grid_for(n_elems), 256, 0, (cudaStream_t)stream>>>(
+    absmax_kernel<<<resident_grid((const void*)absmax_kernel, (n_elems + 3) / 4), 256, 0,
+                    (cudaStream_t)stream>>>(
         u, n_elems, reinterpret_cast<unsigned long long*>(out_max));
     EW_CUDA_TRY(cudaGetLastError());
   }
@@ -228,7 +310,8 @@ int ew_fixed_to_float(const int64_t* acc, int64_t n, int frac_bits, float* out,
   if ((n > 0 && (!acc || !out)) || n < 0)
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fixed_to_float: bad arguments");
   if (n == 0) return EW_OK;
-  dequant_kernel<float><<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+  dequant_kernel<float><<<resident_grid((const void*)dequant_kernel<float>, (n + 3) / 4), 256, 0,
+                          (cudaStream_t)stream>>>(
       reinterpret_cast<const long long*>(acc), n, std::ldexp(1.0, -frac_bits), out);
   EW_CUDA_TRY(cudaGetLastError());
   return EW_OK;
@@ -239,7 +322,8 @@ int ew_fixed_to_double(const int64_t* acc, int64_t n, int frac_bits, double* out
   if ((n > 0 && (!acc || !out)) || n < 0)
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fixed_to_double: bad arguments");
   if (n == 0) return EW_OK;
-  dequant_kernel<double><<<grid_for(n), 256, 0, (cudaStream_t)stream>>>(
+  dequant_kernel<double><<<resident_grid((const void*)dequant_kernel<double>, (n + 3) / 4), 256,
+                           0, (cudaStream_t)stream>>>(
       reinterpret_cast<const long long*>(acc), n, std::ldexp(1.0, -frac_bits), out);
   EW_CUDA_TRY(cudaGetLastError());
   return EW_OK;

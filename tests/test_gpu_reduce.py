@@ -103,3 +103,31 @@ def test_misaligned_unit_pointers_use_scalar_path(oracle):
     dev.weighted_fold(units, w, f, acc)
     want = oracle.weighted_fixed(np.array(w), base[:, 1:].cpu().numpy(), f)
     assert np.array_equal(acc.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("dim", [1, 5, 4099, 1 << 20])
+def test_absmax_exact_vs_numpy_with_specials(dim):
+    """The bit-pattern max (max_i |g| then one fp64 scaling per unit) equals
+    the elementwise fp64 definition, including negative weights, > 16 units,
+    misaligned units, +-inf and NaN propagation."""
+    g = make_units(13, 18, dim + 1)
+    w = np.linspace(-0.3, 0.2, 18)
+    units = [torch.from_numpy(x).cuda()[1:] if k % 3 == 0 else torch.from_numpy(x[:dim]).cuda()
+             for k, x in enumerate(g)]
+    host = [u.cpu().numpy().astype(np.float64) for u in units]
+    want = max(float(np.max(np.abs(w[k] * host[k]))) for k in range(18))
+    assert dev.weighted_absmax(units, w).item() == want
+    units[7][dim // 2] = float("inf")
+    assert dev.weighted_absmax(units, w).item() == float("inf")
+    units[11][dim - 1] = float("nan")
+    assert np.isnan(dev.weighted_absmax(units, w).item())
+
+
+@pytest.mark.parametrize("dim", [1, 3, 4, 7, 4097, 1 << 20])
+def test_dequant_vectorised_tails(dim):
+    rng = np.random.default_rng(dim)
+    acc = torch.from_numpy(rng.integers(-2**61, 2**61, size=dim + 1, dtype=np.int64)).cuda()
+    for a in (acc[:dim], acc[1:]):  # aligned and 8-byte-offset views
+        host = a.cpu().numpy().astype(np.float64) * 2.0 ** -40
+        assert np.array_equal(dev.fixed_to_float(a, 40).cpu().numpy(), host.astype(np.float32))
+        assert np.array_equal(dev.fixed_to_double(a, 40).cpu().numpy(), host)
