@@ -1,0 +1,406 @@
+// Multi-process DP recovery on B200 — the executed counterpart of the
+// reference's Simulation::recover_elaswave DP slice (sim.cpp:597-722), which
+// only prices the steps (comm_edit_time sim.cpp:436-450, remap_time
+// sim.cpp:452-483) and fills MttrEvent (sim.hpp:31-45) / mttr.csv
+// (sim.cpp:1119-1132).
+//
+// One process per GPU (or, for tests, several processes sharing one GPU:
+// CUDA IPC maps a peer process's allocation on the same device too).  The
+// ranks of a DP group meet through a pluggable key-value Store (a TCP store
+// ships in the library; a caller can plug its own, e.g. torch.distributed's
+// c10d store through the C ABI).  The store carries plumbing only — CUDA IPC
+// handles, barriers, per-rank verdict counts; every byte of model state and
+// every checksum moves GPU to GPU through peer pointers.
+//
+//   Store / Channel      rendezvous: set/get + allgather/barrier over members
+//   PeerBuffers          every member's OLD / REPLICA / NEW / block-sum arrays,
+//                        IPC-mapped once (steady state) for the copy kernels
+//   ReshardExecutor      plan (interleaved_layout + integrity_check +
+//                        overlap_matrix) -> this GPU's pull program ->
+//                        one launch that checksums what it lands
+//   BlockVerifier        global checksum conservation: sum over survivors of
+//                        landed block sums == sum of the source's block sums,
+//                        reduce-scattered over peer memory, verdicts via Store
+//   PreparedRecovery     every single departure planned, lowered and bound in
+//                        steady state: recover(d) = comm lookup + one launch
+//                        + one verification
+//   DpGroup              the membership owner: plan_edit, the prepared NCCL
+//                        communicators (comm repair = lookup), reshaper,
+//                        recovery, MttrEvent
+//   InPlaceExecutor      staged in-place reshard (config D): OLD and NEW in
+//                        one buffer, phases behind device-side barriers
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <map>
+#include <memory>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "elaskit/b200.hpp"
+#include "elaskit/cluster.hpp"
+#include "elaskit/communicator.hpp"
+#include "elaskit/migration.hpp"
+#include "elaskit/param_fabric.hpp"
+#include "ew_api.h"
+
+namespace elaskit::b200 {
+
+// ---------------------------------------------------------------- rendezvous
+
+// Blocking key-value store shared by the ranks (the out-of-band channel).
+// get() waits until the key is set; implementations throw
+// std::runtime_error on timeout.
+class Store {
+ public:
+  virtual ~Store() = default;
+  virtual void set(const std::string& key, const std::string& value) = 0;
+  virtual std::string get(const std::string& key) = 0;
+};
+
+// TCP store: rank `is_server` hosts it on host:port (a listening thread), every
+// process (the host included) talks to it over one connection.
+std::unique_ptr<Store> tcp_store(const std::string& host, int port, bool is_server,
+                                 double timeout_s = 300.0);
+
+// Store over two caller callbacks (the C ABI's ew_store_callbacks).
+std::unique_ptr<Store> callback_store(std::function<void(const std::string&, const std::string&)> set,
+                                      std::function<std::string(const std::string&)> get);
+
+// Collective operations among an ordered member list over a Store.  Every
+// member issues the same sequence of calls; a per-channel counter names the
+// keys, so channels with distinct `name`s never collide.
+class Channel {
+ public:
+  Channel(Store& store, std::string name, std::vector<int> members, int me);
+  const std::vector<int>& members() const { return members_; }
+  int me() const { return me_; }
+  int index() const { return index_; }
+  const std::string& name() const { return name_; }
+  // every member's blob, in member order
+  std::vector<std::string> allgather(const std::string& mine);
+  void barrier() { allgather(std::string()); }
+  std::int64_t sum(std::int64_t mine);
+  Store& store() { return store_; }
+
+ private:
+  Store& store_;
+  std::string name_;
+  std::vector<int> members_;
+  int me_ = -1, index_ = -1;
+  std::uint64_t seq_ = 0;
+};
+
+// ------------------------------------------------------------ peer buffers
+
+// Buffers one rank contributes to a reshard (device pointers, caller-owned;
+// null where the rank has none).  Roles as BufRole (Old/Replica/New).
+struct RankBuffers {
+  void* old_buf = nullptr;
+  void* replica = nullptr;
+  void* new_buf = nullptr;
+};
+
+// Device buffers of every member keyed by (role, member), IPC-mapped in this
+// process (own buffers entered as is).  Exchange once, look up many times.
+class PeerBuffers {
+ public:
+  PeerBuffers() = default;
+  ~PeerBuffers();
+  PeerBuffers(const PeerBuffers&) = delete;
+  PeerBuffers& operator=(const PeerBuffers&) = delete;
+
+  // Collective over `ch`: publish `mine` (key -> local device pointer) and
+  // map every other member's entries whose key passes `want` (all if empty).
+  void exchange(Channel& ch, const std::map<int, void*>& mine,
+                const std::function<bool(int key, int member)>& want = {});
+  void* get(int key, int member) const;  // nullptr if absent
+  bool has(int key, int member) const { return get(key, member) != nullptr; }
+  void put(int key, int member, void* p) { table_[{key, member}] = p; }
+  void close();
+
+ private:
+  std::map<std::pair<int, int>, void*> table_;
+  std::vector<void*> opened_;
+};
+
+// ---------------------------------------------------------------- reshard
+
+// One membership change of an interleaved-ZeRO DP group, planned exactly as
+// the reference plans it: integrity_check + overlap_matrix on the interleaved
+// layouts (A4, A6, A7), the departed ranks' bytes sourced from their ring
+// holders (SnapshotRing over the old members).
+struct ReshardPlan {
+  std::vector<std::int64_t> layer_bytes;
+  std::vector<int> old_members, new_members;
+  std::set<int> failed;
+  PartitionLayout src, dst;
+  SnapshotRing ring;
+  TransferPlan plan;
+  double plan_seconds = 0.0;
+
+  static ReshardPlan build(const std::vector<std::int64_t>& layer_bytes,
+                           std::vector<int> old_members, std::vector<int> new_members);
+  // Arbitrary layouts (e.g. a cross-stage layer move); ring_members empty:
+  // no ring (no failed members allowed).  integrity_check when failed.
+  static ReshardPlan from_layouts(PartitionLayout src, PartitionLayout dst, std::set<int> failed,
+                                  std::vector<int> ring_members);
+  // member whose OLD shard `holder` keeps (-1 if none)
+  int replica_of(int holder) const;
+  std::int64_t n_blocks(std::int64_t block_bytes) const {
+    return (src.total_bytes + block_bytes - 1) / block_bytes;
+  }
+};
+
+// This GPU's share of a reshard: pull copies landing in its NEW buffer,
+// verified on arrival (the landed bytes' block sums are added to a device
+// array), or push copies sourced from its buffers.  Peer pointers come from
+// a PeerBuffers table.
+class ReshardExecutor {
+ public:
+  ReshardExecutor(const ReshardPlan& rp, int me, bool push = false,
+                  std::int64_t block_bytes = 65536);
+  ~ReshardExecutor();
+  ReshardExecutor(const ReshardExecutor&) = delete;
+  ReshardExecutor& operator=(const ReshardExecutor&) = delete;
+
+  // Build the program; every (role, member) a copy touches must be in
+  // `peers` (own buffers included).  verify (pull only): checksum what
+  // lands.  Throws std::runtime_error naming a missing peer buffer.
+  void bind(const PeerBuffers& peers, bool verify);
+  // block_sums: device u64 [2 * n_blocks] (caller-zeroed) when verified;
+  // abort_flag: optional device int vetoing the launch (peer barrier error)
+  void launch(ew_stream_t stream, std::uint64_t* block_sums = nullptr,
+              const int* abort_flag = nullptr, int n_ctas = 0, int remote_ctas = 0) const;
+  // (role, member) pairs the program reads or writes on other GPUs
+  std::set<std::pair<int, int>> peers_needed() const;
+  std::int64_t new_bytes() const;
+  bool bound() const { return prog_ != nullptr; }
+  const ReshardPlan& plan() const { return rp_; }
+
+ private:
+  ReshardPlan rp_;
+  int me_;
+  bool push_;
+  std::int64_t block_bytes_;
+  std::vector<CopyDesc> copies_;
+  ew_shardmap* new_map_ = nullptr;
+  ew_copy_program* prog_ = nullptr;
+};
+
+// Global checksum conservation over peer memory.  Every survivor holds three
+// device arrays of 2 * n_blocks u64: `landed` (its verified copy's block
+// sums), `old_blocks` (the block sums of its own OLD shard, from the per-step
+// snapshot rows) and `replica_blocks` (its ring replica's).  Conservation:
+//   sum_r landed_r == sum_r old_blocks_r + replica_blocks_{holder of d}
+// checked on slice [lo, hi) of the blocks by each survivor (a reduce-scatter
+// over NVLink reads), mismatch counts summed over the Store.
+class BlockVerifier {
+ public:
+  BlockVerifier() = default;
+  ~BlockVerifier();
+  BlockVerifier(const BlockVerifier&) = delete;
+  BlockVerifier& operator=(const BlockVerifier&) = delete;
+  // plus / minus: device arrays (local or peer) to add / subtract
+  void set(const std::vector<const std::uint64_t*>& plus,
+           const std::vector<const std::uint64_t*>& minus, std::int64_t n_words,
+           std::int64_t lo, std::int64_t hi);
+  // enqueue the slice check; *bad_dev (device u32) receives the mismatches
+  void run(ew_stream_t stream, std::uint32_t* bad_dev) const;
+
+ private:
+  ew_block_verifier* v_ = nullptr;
+};
+
+// ------------------------------------------------------------ MTTR record
+
+// Reference MttrEvent (sim.hpp:31-45) with measured seconds.
+struct MttrEvent {
+  int step = 0;
+  double t_event_s = 0.0;
+  std::string kind = "fail_stop";
+  double detect_s = 0.0;          // detection: the agent's, outside this library
+  double comm_repair_s = 0.0;     // plan_edit + NCCL communicator repair
+  double remap_s = 0.0;           // copy + verification
+  double migration_stall_s = 0.0; // no layer migration on the DP path
+  double other_s = 0.0;           // micro-batch reshape + bookkeeping
+  double lost_work_s = 0.0;
+  bool verified = false;
+  std::map<std::string, double> phases;
+  double total_s() const {
+    return detect_s + comm_repair_s + remap_s + migration_stall_s + other_s;
+  }
+};
+// mttr.csv of the reference (sim.cpp:1119-1132)
+std::string mttr_csv_header();
+std::string mttr_csv_row(int index, const MttrEvent& ev);
+
+// ------------------------------------------------------- prepared recovery
+
+// Every single departure of a DP group planned, lowered and bound before it
+// happens (steady state): the layouts, every peer's live shard and the ring
+// replicas are known, so each rank builds, once, the verified pull program
+// for each possible departed member d against one NEW buffer sized for the
+// largest case, and maps every peer's verification arrays.  recover(d) is a
+// table lookup, one copy launch and one verification.
+struct PreparedOptions {
+  std::int64_t block_bytes = 65536;
+  double barrier_timeout_s = 30.0;
+};
+
+class PreparedRecovery {
+ public:
+  // old_buf: this rank's live shard (source layout); replica: the shard of
+  // the member it backs up (SnapshotRing::backs_up); old_rows / replica_rows:
+  // their checksum rows (per-step snapshot rows; nullptr = computed here).
+  // new_buf: caller-owned NEW buffer of new_capacity bytes (nullptr: the
+  // object allocates one sized for the largest departure).  Collective over
+  // `ch` (all members).
+  PreparedRecovery(Channel& ch, const std::vector<std::int64_t>& layer_bytes, void* old_buf,
+                   const std::uint64_t* old_rows, void* replica,
+                   const std::uint64_t* replica_rows, void* new_buf = nullptr,
+                   std::int64_t new_capacity = 0, PreparedOptions opt = {});
+  ~PreparedRecovery();
+  PreparedRecovery(const PreparedRecovery&) = delete;
+  PreparedRecovery& operator=(const PreparedRecovery&) = delete;
+
+  // Survivors only, all of them: copy the departed member's share into NEW,
+  // verify by conservation.  Returns the verdict; phases (seconds) in `ev`.
+  bool recover(int departed, ew_stream_t stream, MttrEvent* ev = nullptr);
+  void* new_buf() const { return new_buf_; }
+  std::int64_t new_bytes(int departed) const;
+  const ReshardPlan& plan(int departed) const { return *plans_.at(departed); }
+  const std::vector<int>& members() const { return members_; }
+
+ private:
+  Channel& ch_;
+  std::vector<int> members_;
+  int me_;
+  PreparedOptions opt_;
+  std::int64_t n_words_ = 0;
+  void* new_buf_ = nullptr;
+  bool own_new_ = true;
+  std::uint64_t *landed_ = nullptr, *old_blocks_ = nullptr, *replica_blocks_ = nullptr;
+  std::uint32_t* bad_ = nullptr;
+  std::map<int, std::unique_ptr<ReshardPlan>> plans_;
+  std::map<int, std::unique_ptr<ReshardExecutor>> execs_;
+  std::map<int, std::unique_ptr<BlockVerifier>> verifiers_;
+  std::map<int, std::unique_ptr<Channel>> survivors_;   // departed -> survivor channel
+  std::map<int, ew_peer_barrier*> barriers_;            // departed -> survivor barrier
+  PeerBuffers peers_;
+  unsigned long long* flags_ = nullptr;  // u64 [n][n]: region d for departure d
+
+  void release();
+};
+
+// The DP group as one rank sees it: members, communication links, the NCCL
+// communicator of the (d) reduce, and micro-batch assignment.  recover()
+// runs the reference's order (comm repair, dataflow, remap) and returns the
+// measured MttrEvent.
+struct DpGroupOptions {
+  int per_slot_mbs = 4;
+  int num_microbatches = 32;
+  std::int64_t block_bytes = 65536;
+  bool prepare_comms = true;  // one shrunk communicator per possible departure
+};
+
+class DpGroup {
+ public:
+  // comm: the group's NCCL communicator over `members` in ascending order
+  // (nullptr: no (d) collective, e.g. processes sharing one GPU).  Takes
+  // ownership.  Collective over ch when prepare_comms (ncclCommSplit per
+  // departure, done in steady state).
+  DpGroup(Channel& ch, const std::vector<std::int64_t>& layer_bytes, ew_comm* comm,
+          DpGroupOptions opt = {});
+  ~DpGroup();
+  DpGroup(const DpGroup&) = delete;
+  DpGroup& operator=(const DpGroup&) = delete;
+
+  // Attach a prepared recovery (steady state; borrowed) — single departures
+  // then run its programs instead of planning at failure time.
+  void attach(PreparedRecovery* prepared) { prepared_ = prepared; }
+  // Survivors call this for a FailStop / ScaleIn of `departed`.  bufs: this
+  // rank's OLD / REPLICA / NEW buffers for the change when not prepared.
+  MttrEvent recover(const std::vector<int>& departed, EventKind kind, const RankBuffers& bufs,
+                    ew_stream_t stream, int step = 0);
+  // (Re)build one shrunk communicator per possible single departure of the
+  // current membership (ncclCommSplit, splitShare) and run one collective on
+  // each: steady-state work, collective over the members.  The constructor
+  // calls it when opt.prepare_comms.
+  void prepare();
+  ew_comm* comm() const { return comm_; }
+  const std::vector<int>& members() const { return members_; }
+  const std::vector<int>& microbatch_sizes() const { return mb_sizes_; }
+
+ private:
+  Channel& ch_;
+  std::vector<std::int64_t> layer_bytes_;
+  std::vector<int> members_;
+  std::vector<int> mb_sizes_;
+  std::set<Link> links_;
+  ew_comm* comm_ = nullptr;
+  std::map<int, ew_comm*> prepared_comms_;  // departed member -> shrunk comm
+  std::vector<ew_comm*> retired_;           // parents of splits, freed last
+  DpGroupOptions opt_;
+  PreparedRecovery* prepared_ = nullptr;
+  int events_ = 0;
+};
+
+// --------------------------------------------------------- in place (D)
+
+// Staged in-place reshard executor (InPlaceSchedule, config D): one buffer
+// per rank holds OLD on entry and NEW on exit.  Per phase j each rank gathers
+// (staged part into a rotating staging buffer, direct part in place), a
+// device-side barrier across the survivors marks "every rank has read phase
+// j's OLD bytes", then the staged bytes are flushed.  All gathers and
+// flushes are gated on the barrier's error flag, so a timed-out barrier
+// vetoes every later write (no OLD byte a lagging peer still needs is lost).
+struct InPlaceOptions {
+  std::int64_t stage_bytes = 1 << 30;
+  std::int64_t phase_bytes = 0;  // 0: 2 * stage_bytes
+  int slack = 1;
+  int gather_streams = 2;
+  int flush_ctas = 64;
+  std::int64_t block_bytes = 65536;
+  double barrier_timeout_s = 30.0;
+};
+
+class InPlaceExecutor {
+ public:
+  // buf: this rank's single buffer (>= max(OLD, NEW) bytes); replica: the
+  // departed member's shard if this rank holds it, else nullptr.  Collective
+  // over `ch` (old members; departed members take part in the mapping
+  // exchange only when they are still alive — here: all old members call).
+  InPlaceExecutor(Channel& ch, const ReshardPlan& rp, void* buf, void* replica,
+                  InPlaceOptions opt = {});
+  ~InPlaceExecutor();
+  InPlaceExecutor(const InPlaceExecutor&) = delete;
+  InPlaceExecutor& operator=(const InPlaceExecutor&) = delete;
+
+  // Enqueue every phase on `stream` (+ internal streams joined back);
+  // block_sums: device u64 [2 * n_blocks] (caller-zeroed) or nullptr.
+  void launch(ew_stream_t stream, std::uint64_t* block_sums);
+  bool timed_out() const;
+  const InPlaceSchedule& schedule() const { return sched_; }
+
+ private:
+  struct Phase;
+  ReshardPlan rp_;
+  int me_;
+  InPlaceOptions opt_;
+  InPlaceSchedule sched_;
+  void* buf_;
+  std::vector<void*> staging_;
+  std::vector<std::unique_ptr<Phase>> phases_;
+  std::vector<ew_shardmap*> maps_;
+  PeerBuffers peers_;
+  ew_peer_barrier* barrier_ = nullptr;
+  unsigned long long* flags_ = nullptr;
+  std::vector<void*> streams_;  // cudaStream_t
+
+  void release();
+};
+
+}  // namespace elaskit::b200

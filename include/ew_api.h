@@ -384,6 +384,12 @@ int ew_comm_init(const void* id128, int nranks, int rank, ew_comm** out);
  * NCCL_SHRINK_ABORT (a member died mid-operation). */
 int ew_comm_shrink(ew_comm* parent, const int* exclude_ranks, int n_exclude, int abort,
                    ew_comm** out);
+/* ncclCommSplit: every rank of `parent` calls it; color < 0 (NCCL_SPLIT_NOCOLOR)
+ * leaves this rank out (*out = NULL).  share != 0 shares the parent's
+ * buffers and connections (splitShare): a split prepared in steady state for
+ * every possible departure then costs little memory, and the repair at
+ * failure time is a lookup (recovery.hpp DpGroup). */
+int ew_comm_split(ew_comm* parent, int color, int key, int share, ew_comm** out);
 int ew_comm_rank(const ew_comm* comm, int* rank, int* nranks);
 int ew_comm_destroy(ew_comm* comm);
 /* In-place sums over the communicator. */
@@ -417,6 +423,17 @@ int ew_peer_fold_create_i64(int world, int rank, int64_t n_elems, const int64_t*
 int ew_peer_fold_reduce_scatter(ew_peer_fold* fold, int frac_bits, ew_stream_t stream);
 int ew_peer_fold_all_gather(ew_peer_fold* fold, ew_stream_t stream);
 void ew_peer_fold_free(ew_peer_fold* fold);
+
+/* Checksum conservation over peer memory (reshard verification): counts the
+ * words i in [lo, hi) (even bounds: whole blocks) where
+ *   sum_k plus[k][i] != sum_k minus[k][i]   (mod 2^64)
+ * with plus / minus local or IPC-mapped u64 arrays (16-byte aligned).  Each
+ * survivor checks its slice; *bad_count (device u32) is zeroed by run(). */
+typedef struct ew_block_verifier ew_block_verifier;
+int ew_block_verifier_create(const uint64_t* const* plus, int n_plus, const uint64_t* const* minus,
+                             int n_minus, int64_t lo, int64_t hi, ew_block_verifier** out);
+int ew_block_verifier_run(const ew_block_verifier* v, uint32_t* bad_count, ew_stream_t stream);
+void ew_block_verifier_free(ew_block_verifier* v);
 
 /* Stream-ordered barrier across the GPUs of a group over peer memory.
  * flag_ptrs[r] is rank r's zero-initialised uint64[world] array (IPC-mapped
@@ -471,6 +488,129 @@ int ew_adam_step_rows(const float* grad, float* master, float* exp_avg, float* e
 /* *bad_count (device u32, zeroed by the call) = rows where a != b. */
 int ew_rows_diff(const uint64_t* a, const uint64_t* b, int64_t n_rows, uint32_t* bad_count,
                  ew_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Multi-process recovery runtime (include/elaskit/recovery.hpp): the DP
+ * slice of the reference's recover_elaswave (sim.cpp:597-722) executed
+ * across processes — one per GPU, or several sharing one GPU.  Ranks meet
+ * through a key-value store (plumbing only: IPC handles, barriers, verdict
+ * counts); state and checksums move GPU to GPU through peer pointers.
+ * ---------------------------------------------------------------------- */
+typedef struct ew_store ew_store;
+/* TCP store hosted by the is_server process on host:port (a listening
+ * thread); every process, the host included, connects to it. */
+int ew_store_tcp(const char* host, int port, int is_server, double timeout_s, ew_store** out);
+/* Store over caller callbacks (e.g. torch.distributed's c10d store).  get
+ * blocks until the key exists, writes min(len, cap) bytes and *len; it
+ * returns EW_ERR_CAPACITY when cap < *len (the library retries once with a
+ * buffer of *len bytes), another nonzero value on failure. */
+typedef int (*ew_store_set_fn)(void* ctx, const char* key, int64_t key_len, const char* val,
+                               int64_t len);
+typedef int (*ew_store_get_fn)(void* ctx, const char* key, int64_t key_len, char* buf,
+                               int64_t cap, int64_t* len);
+int ew_store_callbacks(ew_store_set_fn set, ew_store_get_fn get, void* ctx, ew_store** out);
+int ew_store_set(ew_store* store, const char* key, const void* val, int64_t len);
+int ew_store_get(ew_store* store, const char* key, void* buf, int64_t cap, int64_t* len);
+void ew_store_free(ew_store* store);
+
+/* Ordered member list on a store; collectives name their keys by channel
+ * name and call count, so every member makes the same sequence of calls. */
+typedef struct ew_channel ew_channel;
+int ew_channel_create(ew_store* store, const char* name, const int* members, int n, int me,
+                      ew_channel** out);
+int ew_channel_barrier(ew_channel* ch);
+int ew_channel_sum(ew_channel* ch, int64_t mine, int64_t* total);
+void ew_channel_free(ew_channel* ch);
+
+/* MttrEvent (reference sim.hpp:31-45) with measured phases; phases a path
+ * does not run read -1. */
+typedef struct ew_mttr_event {
+  int32_t step, verified;
+  double t_event_s;
+  char kind[16];
+  double detect_s, comm_repair_s, remap_s, migration_stall_s, other_s, lost_work_s;
+  double plan_edit_s, comm_acquire_s, first_collective_s, comm_prepared;
+  double plan_s, map_bind_s, copy_s, barrier_verify_s, verdict_exchange_s, launch_to_verdict_s;
+  double mismatched_block_words, barrier_timeouts;
+} ew_mttr_event;
+/* mttr.csv (reference sim.cpp:1119-1132): header line and one row, no '\n' */
+int ew_mttr_csv_header(char* buf, int64_t cap);
+int ew_mttr_csv_row(const ew_mttr_event* ev, int index, char* buf, int64_t cap);
+
+/* Peer buffer table: (key, member) -> device pointer; keys 0/1/2 are the
+ * OLD / REPLICA / NEW roles of ew_copy_desc.  exchange() is collective over
+ * the channel: publishes this rank's (key, ptr) pairs as CUDA IPC handles and
+ * maps every other member's. */
+typedef struct ew_peers ew_peers;
+int ew_peers_create(ew_peers** out);
+int ew_peers_exchange(ew_peers* peers, ew_channel* ch, const int* keys, void* const* ptrs, int n);
+int ew_peers_put(ew_peers* peers, int key, int member, void* ptr);
+int ew_peers_get(const ew_peers* peers, int key, int member, void** ptr);
+void ew_peers_free(ew_peers* peers);
+
+/* One rank's reshard executor over arbitrary layouts (overlap_matrix +
+ * reshard_copies); bind() resolves its copies against a peer table (own
+ * buffers put in it too), verify != 0 (pull) checksums what lands. */
+typedef struct ew_reshard ew_reshard;
+int ew_reshard_create(const ew_layout* src, const ew_layout* dst, const int* failed, int n_failed,
+                      const int* ring_members, int n_ring, int me, int push, int64_t block_bytes,
+                      ew_reshard** out);
+int ew_reshard_bind(ew_reshard* r, const ew_peers* peers, int verify);
+int ew_reshard_launch(const ew_reshard* r, uint64_t* block_sums, const int* abort_flag,
+                      int n_ctas, int remote_ctas, ew_stream_t stream);
+void ew_reshard_free(ew_reshard* r);
+
+/* Every single departure of an interleaved-ZeRO DP group planned, lowered
+ * and bound in steady state (collective over the channel's members).
+ * old_rows / replica_rows: the per-step snapshot's checksum rows of this
+ * rank's OLD shard and of the replica it keeps (NULL: re-read here).
+ * new_buf: caller-owned NEW buffer of new_capacity bytes, large enough for
+ * every departure (NULL: allocated here).  recover() (survivors only, all of
+ * them): one verified copy launch into the NEW buffer, a device barrier,
+ * checksum conservation over peer memory, the verdict summed over the
+ * survivors. */
+typedef struct ew_prepared ew_prepared;
+int ew_prepared_create(ew_channel* ch, const int64_t* layer_bytes, int n_layers, void* old_buf,
+                       const uint64_t* old_rows, void* replica, const uint64_t* replica_rows,
+                       void* new_buf, int64_t new_capacity, int64_t block_bytes,
+                       double barrier_timeout_s, ew_prepared** out);
+int ew_prepared_recover(ew_prepared* p, int departed, ew_stream_t stream, ew_mttr_event* ev,
+                        int* verified);
+int ew_prepared_new(const ew_prepared* p, int departed, void** ptr, int64_t* bytes);
+void ew_prepared_free(ew_prepared* p);
+
+/* The DP group: plan_edit, NCCL communicator (owned; NULL = none) with one
+ * prepared shrunk communicator per possible departure (prepare_comms: a
+ * collective ncclCommSplit per member, splitShare, warmed by one
+ * all-reduce), micro-batch reshaper, recovery -> MttrEvent.  kind: 0
+ * FailStop, 2 ScaleIn (elaskit::EventKind).  old_buf / replica / new_buf are
+ * used when no prepared recovery is attached (planning at failure time). */
+typedef struct ew_dp_group ew_dp_group;
+int ew_dp_group_create(ew_channel* ch, const int64_t* layer_bytes, int n_layers, ew_comm* comm,
+                       int per_slot_mbs, int num_microbatches, int64_t block_bytes,
+                       int prepare_comms, ew_dp_group** out);
+int ew_dp_group_attach(ew_dp_group* g, ew_prepared* prepared);
+int ew_dp_group_prepare(ew_dp_group* g);
+int ew_dp_group_recover(ew_dp_group* g, const int* departed, int n, int kind, void* old_buf,
+                        void* replica, void* new_buf, int step, ew_stream_t stream,
+                        ew_mttr_event* ev);
+int ew_dp_group_comm(const ew_dp_group* g, ew_comm** comm); /* borrowed */
+int ew_dp_group_members(const ew_dp_group* g, int* out, int cap, int* n);
+int ew_dp_group_microbatches(const ew_dp_group* g, int* out, int cap, int* n);
+void ew_dp_group_free(ew_dp_group* g);
+
+/* Staged in-place reshard executor (config D): collective over a channel of
+ * old + new members; buf holds OLD on entry and NEW on exit. */
+typedef struct ew_inplace_exec ew_inplace_exec;
+int ew_inplace_exec_create(ew_channel* ch, const int64_t* layer_bytes, int n_layers,
+                           const int* old_members, int n_old, const int* new_members, int n_new,
+                           void* buf, void* replica, int64_t stage_bytes, int64_t phase_bytes,
+                           int slack, int gather_streams, int flush_ctas, int64_t block_bytes,
+                           double barrier_timeout_s, ew_inplace_exec** out);
+int ew_inplace_exec_launch(ew_inplace_exec* x, uint64_t* block_sums, ew_stream_t stream);
+int ew_inplace_exec_timed_out(const ew_inplace_exec* x, int* timed_out);
+int ew_inplace_exec_info(const ew_inplace_exec* x, int64_t* n_phases, int64_t* stage_alloc);
+void ew_inplace_exec_free(ew_inplace_exec* x);
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -251,6 +251,66 @@ _sig("ew_adam_scalars", i32, P(AdamHyper), i64, P(C.c_float))
 _sig("ew_adam_step", i32, vp, vp, vp, vp, vp, i64, P(AdamHyper), i64, vp)
 _sig("ew_adam_step_rows", i32, vp, vp, vp, vp, vp, i64, P(AdamHyper), i64, vp, i64, i64, vp, vp)
 _sig("ew_rows_diff", i32, vp, vp, i64, vp, vp)
+_sig("ew_comm_split", i32, vp, i32, i32, i32, P(vp))
+_sig("ew_block_verifier_create", i32, P(vp), i32, P(vp), i32, i64, i64, P(vp))
+_sig("ew_block_verifier_run", i32, vp, vp, vp)
+_sig("ew_block_verifier_free", None, vp)
+
+
+# --------------------------------------------- multi-process recovery ---
+
+class MttrEventC(C.Structure):
+    """ew_mttr_event (ew_api.h): reference MttrEvent (sim.hpp:31-45) + phases."""
+    _fields_ = [("step", C.c_int32), ("verified", C.c_int32), ("t_event_s", f64),
+                ("kind", C.c_char * 16)] + [(n, f64) for n in (
+                    "detect_s", "comm_repair_s", "remap_s", "migration_stall_s", "other_s",
+                    "lost_work_s", "plan_edit_s", "comm_acquire_s", "first_collective_s",
+                    "comm_prepared", "plan_s", "map_bind_s", "copy_s", "barrier_verify_s",
+                    "verdict_exchange_s", "launch_to_verdict_s", "mismatched_block_words",
+                    "barrier_timeouts")]
+
+
+STORE_SET_FN = C.CFUNCTYPE(i32, vp, C.POINTER(C.c_char), i64, C.POINTER(C.c_char), i64)
+STORE_GET_FN = C.CFUNCTYPE(i32, vp, C.POINTER(C.c_char), i64, C.POINTER(C.c_char), i64, P(i64))
+
+_sig("ew_store_tcp", i32, C.c_char_p, i32, i32, f64, P(vp))
+_sig("ew_store_callbacks", i32, STORE_SET_FN, STORE_GET_FN, vp, P(vp))
+_sig("ew_store_set", i32, vp, C.c_char_p, vp, i64)
+_sig("ew_store_get", i32, vp, C.c_char_p, vp, i64, P(i64))
+_sig("ew_store_free", None, vp)
+_sig("ew_channel_create", i32, vp, C.c_char_p, P(i32), i32, i32, P(vp))
+_sig("ew_channel_barrier", i32, vp)
+_sig("ew_channel_sum", i32, vp, i64, P(i64))
+_sig("ew_channel_free", None, vp)
+_sig("ew_mttr_csv_header", i32, C.c_char_p, i64)
+_sig("ew_mttr_csv_row", i32, P(MttrEventC), i32, C.c_char_p, i64)
+_sig("ew_peers_create", i32, P(vp))
+_sig("ew_peers_exchange", i32, vp, vp, P(i32), P(vp), i32)
+_sig("ew_peers_put", i32, vp, i32, i32, vp)
+_sig("ew_peers_get", i32, vp, i32, i32, P(vp))
+_sig("ew_peers_free", None, vp)
+_sig("ew_reshard_create", i32, vp, vp, P(i32), i32, P(i32), i32, i32, i32, i64, P(vp))
+_sig("ew_reshard_bind", i32, vp, vp, i32)
+_sig("ew_reshard_launch", i32, vp, vp, vp, i32, i32, vp)
+_sig("ew_reshard_free", None, vp)
+_sig("ew_prepared_create", i32, vp, P(i64), i32, vp, vp, vp, vp, vp, i64, i64, f64, P(vp))
+_sig("ew_prepared_recover", i32, vp, i32, vp, P(MttrEventC), P(i32))
+_sig("ew_prepared_new", i32, vp, i32, P(vp), P(i64))
+_sig("ew_prepared_free", None, vp)
+_sig("ew_dp_group_create", i32, vp, P(i64), i32, vp, i32, i32, i64, i32, P(vp))
+_sig("ew_dp_group_attach", i32, vp, vp)
+_sig("ew_dp_group_prepare", i32, vp)
+_sig("ew_dp_group_recover", i32, vp, P(i32), i32, i32, vp, vp, vp, i32, vp, P(MttrEventC))
+_sig("ew_dp_group_comm", i32, vp, P(vp))
+_sig("ew_dp_group_members", i32, vp, P(i32), i32, P(i32))
+_sig("ew_dp_group_microbatches", i32, vp, P(i32), i32, P(i32))
+_sig("ew_dp_group_free", None, vp)
+_sig("ew_inplace_exec_create", i32, vp, P(i64), i32, P(i32), i32, P(i32), i32, vp, vp, i64, i64,
+     i32, i32, i32, i64, f64, P(vp))
+_sig("ew_inplace_exec_launch", i32, vp, vp, vp)
+_sig("ew_inplace_exec_timed_out", i32, vp, P(i32))
+_sig("ew_inplace_exec_info", i32, vp, P(i64), P(i64))
+_sig("ew_inplace_exec_free", None, vp)
 
 def int_array(values) -> C.Array:
     values = list(values)

@@ -1,0 +1,1164 @@
+// Multi-process DP recovery (include/elaskit/recovery.hpp): the rendezvous
+// store, peer mappings, the reshard executor, checksum-conservation
+// verification, prepared recoveries, the DP group with prepared NCCL
+// communicators, and the staged in-place executor — host C++ over the C ABI
+// (include/ew_api.h) plus the CUDA runtime for streams and events.
+//
+// Reference: Simulation::recover_elaswave (sim.cpp:597-722) prices comm
+// repair (comm_edit_time, sim.cpp:436-450), dataflow and remap (remap_time,
+// sim.cpp:452-483) and records MttrEvent (sim.hpp:31-45); here the same
+// sequence runs on the GPUs and the record carries measured seconds.
+#include "elaskit/recovery.hpp"
+
+#include <arpa/inet.h>
+#include <cuda_runtime.h>
+#include <netdb.h>
+#include <netinet/in.h>
+#include <netinet/tcp.h>
+#include <sys/socket.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <thread>
+#include <unordered_map>
+
+#include "elaskit/dataflow.hpp"
+#include "elaskit/device.hpp"
+
+namespace elaskit::b200 {
+
+using device::check;
+
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double seconds(Clock::time_point a, Clock::time_point b) {
+  return std::chrono::duration<double>(b - a).count();
+}
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw device::CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------- TCP store
+//
+// Frames: 'S' u32 klen key u64 vlen value -> u8 ack;  'G' u32 klen key ->
+// u64 vlen value (the server answers once the key exists).
+
+bool send_all(int fd, const void* p, std::size_t n) {
+  const char* c = static_cast<const char*>(p);
+  while (n > 0) {
+    const ssize_t k = ::send(fd, c, n, MSG_NOSIGNAL);
+    if (k <= 0) return false;
+    c += k;
+    n -= static_cast<std::size_t>(k);
+  }
+  return true;
+}
+
+bool recv_all(int fd, void* p, std::size_t n) {
+  char* c = static_cast<char*>(p);
+  while (n > 0) {
+    const ssize_t k = ::recv(fd, c, n, 0);
+    if (k <= 0) return false;
+    c += k;
+    n -= static_cast<std::size_t>(k);
+  }
+  return true;
+}
+
+class TcpServer {
+ public:
+  explicit TcpServer(int port) {
+    fd_ = ::socket(AF_INET, SOCK_STREAM, 0);
+    if (fd_ < 0) throw std::runtime_error("tcp store: socket() failed");
+    int one = 1;
+    ::setsockopt(fd_, SOL_SOCKET, SO_REUSEADDR, &one, sizeof(one));
+    sockaddr_in a{};
+    a.sin_family = AF_INET;
+    a.sin_addr.s_addr = htonl(INADDR_ANY);
+    a.sin_port = htons(static_cast<uint16_t>(port));
+    if (::bind(fd_, reinterpret_cast<sockaddr*>(&a), sizeof(a)) != 0 || ::listen(fd_, 256) != 0) {
+      ::close(fd_);
+      throw std::runtime_error("tcp store: cannot listen on port " + std::to_string(port));
+    }
+    accept_ = std::thread([this] { accept_loop(); });
+  }
+  ~TcpServer() {
+    {
+      // the host process leaving must not cut its peers' last reads short
+      // (e.g. a final barrier): wait until every client has disconnected
+      std::unique_lock<std::mutex> lk(mu_);
+      cv_.wait_for(lk, std::chrono::seconds(60), [&] { return live_ == 0; });
+    }
+    stop_ = true;
+    ::shutdown(fd_, SHUT_RDWR);
+    ::close(fd_);
+    accept_.join();
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (int c : conns_) ::shutdown(c, SHUT_RDWR);
+    }
+    cv_.notify_all();
+    for (std::thread& t : workers_) t.join();
+    for (int c : conns_) ::close(c);  // closed only here: no fd number is reused meanwhile
+  }
+
+ private:
+  void accept_loop() {
+    while (!stop_) {
+      const int c = ::accept(fd_, nullptr, nullptr);
+      if (c < 0) {
+        if (stop_) break;
+        continue;
+      }
+      int one = 1;
+      ::setsockopt(c, IPPROTO_TCP, TCP_NODELAY, &one, sizeof(one));
+      std::lock_guard<std::mutex> lk(mu_);
+      conns_.push_back(c);
+      ++live_;
+      workers_.emplace_back([this, c] {
+        serve(c);
+        {
+          std::lock_guard<std::mutex> g(mu_);
+          --live_;
+        }
+        cv_.notify_all();
+      });
+    }
+  }
+  void serve(int c) {
+    for (;;) {
+      char op = 0;
+      uint32_t kl = 0;
+      if (!recv_all(c, &op, 1) || !recv_all(c, &kl, 4)) break;
+      std::string key(kl, '\0');
+      if (!recv_all(c, key.data(), kl)) break;
+      if (op == 'S') {
+        uint64_t vl = 0;
+        if (!recv_all(c, &vl, 8)) break;
+        std::string v(vl, '\0');
+        if (!recv_all(c, v.data(), vl)) break;
+        {
+          std::lock_guard<std::mutex> lk(mu_);
+          data_[key] = std::move(v);
+        }
+        cv_.notify_all();
+        const char ack = 1;
+        if (!send_all(c, &ack, 1)) break;
+      } else if (op == 'G') {
+        std::string v;
+        {
+          std::unique_lock<std::mutex> lk(mu_);
+          cv_.wait(lk, [&] { return stop_.load() || data_.count(key) > 0; });
+          if (stop_) break;
+          v = data_[key];
+        }
+        const uint64_t vl = v.size();
+        if (!send_all(c, &vl, 8) || !send_all(c, v.data(), vl)) break;
+      } else {
+        break;
+      }
+    }
+  }
+
+  int fd_ = -1;
+  std::atomic<bool> stop_{false};
+  std::thread accept_;
+  std::vector<std::thread> workers_;
+  std::vector<int> conns_;
+  int live_ = 0;  // connected clients
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::unordered_map<std::string, std::string> data_;
+};
+
+class TcpStore final : public Store {
+ public:
+  TcpStore(const std::string& host, int port, bool is_server, double timeout_s) {
+    if (is_server) server_ = std::make_unique<TcpServer>(port);
+    addrinfo hints{}, *res = nullptr;
+    hints.ai_family = AF_INET;
+    hints.ai_socktype = SOCK_STREAM;
+    if (::getaddrinfo(host.c_str(), std::to_string(port).c_str(), &hints, &res) != 0 || !res)
+      throw std::runtime_error("tcp store: cannot resolve " + host);
+    const auto t0 = Clock::now();
+    for (;;) {
+      fd_ = ::socket(AF_INET, SOCK_STREAM, 0);
+      if (fd_ >= 0 && ::connect(fd_, res->ai_addr, res->ai_addrlen) == 0) break;
+      if (fd_ >= 0) ::close(fd_);
+      fd_ = -1;
+      if (seconds(t0, Clock::now()) > timeout_s) {
+        ::freeaddrinfo(res);
+        throw std::runtime_error("tcp store: cannot connect to " + host + ":" +
+                                 std::to_string(port));
+      }
+      std::this_thread::sleep_for(std::chrono::milliseconds(20));
+    }
+    ::freeaddrinfo(res);
+    int one = 1;
+    ::setsockopt(fd_, IPPROTO_TCP, TCP_NODELAY, &one, sizeof(one));
+    timeval tv{};
+    tv.tv_sec = static_cast<long>(timeout_s);
+    tv.tv_usec = static_cast<long>((timeout_s - static_cast<double>(tv.tv_sec)) * 1e6);
+    ::setsockopt(fd_, SOL_SOCKET, SO_RCVTIMEO, &tv, sizeof(tv));
+  }
+  ~TcpStore() override {
+    if (fd_ >= 0) ::close(fd_);  // own connection first: the server waits for all clients
+    server_.reset();
+  }
+  void set(const std::string& key, const std::string& value) override {
+    std::lock_guard<std::mutex> lk(mu_);
+    const char op = 'S';
+    const uint32_t kl = static_cast<uint32_t>(key.size());
+    const uint64_t vl = value.size();
+    char ack = 0;
+    if (!send_all(fd_, &op, 1) || !send_all(fd_, &kl, 4) || !send_all(fd_, key.data(), kl) ||
+        !send_all(fd_, &vl, 8) || !send_all(fd_, value.data(), vl) || !recv_all(fd_, &ack, 1))
+      throw std::runtime_error("tcp store: set(" + key + ") failed");
+  }
+  std::string get(const std::string& key) override {
+    std::lock_guard<std::mutex> lk(mu_);
+    const char op = 'G';
+    const uint32_t kl = static_cast<uint32_t>(key.size());
+    uint64_t vl = 0;
+    if (!send_all(fd_, &op, 1) || !send_all(fd_, &kl, 4) || !send_all(fd_, key.data(), kl) ||
+        !recv_all(fd_, &vl, 8))
+      throw std::runtime_error("tcp store: get(" + key + ") failed or timed out");
+    std::string v(vl, '\0');
+    if (!recv_all(fd_, v.data(), vl)) throw std::runtime_error("tcp store: get(" + key + ") cut");
+    return v;
+  }
+
+ private:
+  std::unique_ptr<TcpServer> server_;
+  int fd_ = -1;
+  std::mutex mu_;
+};
+
+class CallbackStore final : public Store {
+ public:
+  CallbackStore(std::function<void(const std::string&, const std::string&)> s,
+                std::function<std::string(const std::string&)> g)
+      : set_(std::move(s)), get_(std::move(g)) {}
+  void set(const std::string& k, const std::string& v) override { set_(k, v); }
+  std::string get(const std::string& k) override { return get_(k); }
+
+ private:
+  std::function<void(const std::string&, const std::string&)> set_;
+  std::function<std::string(const std::string&)> get_;
+};
+
+// ------------------------------------------------------------ small helpers
+
+template <typename T>
+T* dalloc(std::int64_t count) {
+  void* p = nullptr;
+  check(ew_alloc(std::max<std::int64_t>(32, count * static_cast<std::int64_t>(sizeof(T))), &p));
+  return static_cast<T*>(p);
+}
+
+void dfree(void* p) {
+  if (p != nullptr) ew_free(p);
+}
+
+std::vector<ew_segment> to_ew(const std::vector<Segment>& segs) {
+  std::vector<ew_segment> out;
+  out.reserve(segs.size());
+  for (const Segment& s : segs) out.push_back({s.global_lo, s.length, s.local_off});
+  return out;
+}
+
+ew_shardmap* make_map(const std::vector<Segment>& segs, std::int64_t block) {
+  const std::vector<ew_segment> e = to_ew(segs);
+  ew_shardmap* m = nullptr;
+  check(ew_shardmap_create(e.data(), static_cast<std::int64_t>(e.size()), block, &m));
+  return m;
+}
+
+// blocks[2b..2b+1] += checksum rows of member r's packed shard (rows given:
+// the per-step snapshot rows; else re-read from buf)
+void add_blocks(const PartitionLayout& layout, int r, const void* buf, const std::uint64_t* rows,
+                std::uint64_t* blocks, std::int64_t n_blocks, std::int64_t block,
+                ew_stream_t s) {
+  ew_shardmap* m = make_map(shard_segments(layout, r), block);
+  const std::int64_t n_rows = ew_shardmap_num_rows(m);
+  std::uint64_t* tmp = nullptr;
+  try {
+    if (rows == nullptr && n_rows > 0) {
+      tmp = dalloc<std::uint64_t>(2 * n_rows);
+      check(ew_checksum(m, buf, tmp, s));
+      rows = tmp;
+    }
+    if (n_rows > 0) check(ew_rows_to_blocks(m, rows, blocks, n_blocks, s));
+    check(ew_stream_sync(s));
+  } catch (...) {
+    dfree(tmp);
+    ew_shardmap_free(m);
+    throw;
+  }
+  dfree(tmp);
+  ew_shardmap_free(m);
+}
+
+std::vector<int> without(const std::vector<int>& v, const std::set<int>& drop) {
+  std::vector<int> out;
+  for (int x : v)
+    if (!drop.count(x)) out.push_back(x);
+  return out;
+}
+
+int index_of(const std::vector<int>& v, int x) {
+  const auto it = std::find(v.begin(), v.end(), x);
+  return it == v.end() ? -1 : static_cast<int>(it - v.begin());
+}
+
+// PeerBuffers keys beyond the BufRole values
+constexpr int kLanded = 10, kOldBlocks = 11, kReplicaBlocks = 12, kFlags = 13;
+
+// Slice [lo, hi) (even) of n_words owned by survivor i of k.
+std::pair<std::int64_t, std::int64_t> slice_of(std::int64_t n_words, int i, int k) {
+  const std::int64_t pairs = n_words / 2;
+  return {2 * (pairs * i / k), 2 * (pairs * (i + 1) / k)};
+}
+
+// Stream-ordered barrier among `members` over flag arrays registered under
+// key kFlags in `peers`, using region `region` (of n_regions * stride u64).
+ew_peer_barrier* make_barrier(const PeerBuffers& peers, const std::vector<int>& members, int me,
+                              std::int64_t region_off) {
+  std::vector<unsigned long long*> ptrs;
+  for (int m : members) {
+    auto* base = static_cast<unsigned long long*>(peers.get(kFlags, m));
+    if (base == nullptr) throw std::runtime_error("barrier flags of member " + std::to_string(m) +
+                                                  " are not mapped");
+    ptrs.push_back(base + region_off);
+  }
+  ew_peer_barrier* b = nullptr;
+  check(ew_peer_barrier_create(static_cast<int>(members.size()), index_of(members, me),
+                               ptrs.data(), &b));
+  return b;
+}
+
+}  // namespace
+
+std::unique_ptr<Store> tcp_store(const std::string& host, int port, bool is_server,
+                                 double timeout_s) {
+  return std::make_unique<TcpStore>(host, port, is_server, timeout_s);
+}
+
+std::unique_ptr<Store> callback_store(
+    std::function<void(const std::string&, const std::string&)> set,
+    std::function<std::string(const std::string&)> get) {
+  return std::make_unique<CallbackStore>(std::move(set), std::move(get));
+}
+
+// ------------------------------------------------------------------ Channel
+
+Channel::Channel(Store& store, std::string name, std::vector<int> members, int me)
+    : store_(store), name_(std::move(name)), members_(std::move(members)), me_(me) {
+  std::sort(members_.begin(), members_.end());
+  index_ = index_of(members_, me);
+  if (index_ < 0)
+    throw std::invalid_argument("channel " + name_ + ": rank " + std::to_string(me) +
+                                " is not a member");
+}
+
+std::vector<std::string> Channel::allgather(const std::string& mine) {
+  const std::string base = name_ + "/" + std::to_string(seq_++) + "/";
+  store_.set(base + std::to_string(me_), mine);
+  std::vector<std::string> out;
+  out.reserve(members_.size());
+  for (int m : members_) out.push_back(m == me_ ? mine : store_.get(base + std::to_string(m)));
+  return out;
+}
+
+std::int64_t Channel::sum(std::int64_t mine) {
+  std::int64_t total = 0;
+  for (const std::string& s : allgather(std::to_string(mine))) total += std::stoll(s);
+  return total;
+}
+
+// -------------------------------------------------------------- PeerBuffers
+
+PeerBuffers::~PeerBuffers() { close(); }
+
+void PeerBuffers::exchange(Channel& ch, const std::map<int, void*>& mine,
+                           const std::function<bool(int, int)>& want) {
+  // blob: n x {int32 key, 64-byte IPC handle, int64 offset}
+  std::string blob;
+  for (const auto& [key, ptr] : mine) {
+    if (ptr == nullptr) continue;
+    char rec[4 + 64 + 8];
+    std::int64_t off = 0;
+    const std::int32_t k = key;
+    check(ew_ipc_get_handle(ptr, rec + 4, &off));
+    std::memcpy(rec, &k, 4);
+    std::memcpy(rec + 68, &off, 8);
+    blob.append(rec, sizeof(rec));
+    table_[{key, ch.me()}] = ptr;
+  }
+  const std::vector<std::string> all = ch.allgather(blob);
+  for (std::size_t i = 0; i < all.size(); ++i) {
+    const int m = ch.members()[i];
+    if (m == ch.me()) continue;
+    const std::string& b = all[i];
+    for (std::size_t p = 0; p + 76 <= b.size(); p += 76) {
+      std::int32_t key = 0;
+      std::int64_t off = 0;
+      std::memcpy(&key, b.data() + p, 4);
+      std::memcpy(&off, b.data() + p + 68, 8);
+      if (table_.count({key, m}) || (want && !want(key, m))) continue;
+      void* q = nullptr;
+      check(ew_ipc_open(b.data() + p + 4, off, &q));
+      opened_.push_back(q);
+      table_[{key, m}] = q;
+    }
+  }
+}
+
+void* PeerBuffers::get(int key, int member) const {
+  const auto it = table_.find({key, member});
+  return it == table_.end() ? nullptr : it->second;
+}
+
+void PeerBuffers::close() {
+  for (void* p : opened_) ew_ipc_close(p);
+  opened_.clear();
+  table_.clear();
+}
+
+// -------------------------------------------------------------- ReshardPlan
+
+ReshardPlan ReshardPlan::build(const std::vector<std::int64_t>& layer_bytes,
+                               std::vector<int> old_members, std::vector<int> new_members) {
+  const auto t0 = Clock::now();
+  std::sort(old_members.begin(), old_members.end());
+  std::sort(new_members.begin(), new_members.end());
+  ReshardPlan rp;
+  rp.layer_bytes = layer_bytes;
+  rp.old_members = old_members;
+  rp.new_members = new_members;
+  for (int m : old_members)
+    if (!std::binary_search(new_members.begin(), new_members.end(), m)) rp.failed.insert(m);
+  ZeroLayout z;
+  z.kind = ZeroKind::Interleaved;
+  z.dp_degree = static_cast<int>(old_members.size());
+  z.layer_bytes = layer_bytes;
+  rp.src = interleaved_layout(z, old_members);
+  rp.dst = interleaved_layout(z, new_members);
+  rp.ring.members = old_members;
+  if (!rp.failed.empty()) {
+    const IntegrityReport rep = integrity_check(rp.ring, rp.src, rp.failed);
+    if (!rep.recoverable) {
+      std::string who;
+      for (const auto& [r, ivs] : rep.missing) who += (who.empty() ? "" : ",") + std::to_string(r);
+      throw CoverageMismatch("members {" + who + "} lost together with their ring holders");
+    }
+  }
+  rp.plan = overlap_matrix(rp.src, rp.dst, rp.failed, &rp.ring);
+  rp.plan_seconds = seconds(t0, Clock::now());
+  return rp;
+}
+
+ReshardPlan ReshardPlan::from_layouts(PartitionLayout src, PartitionLayout dst,
+                                      std::set<int> failed, std::vector<int> ring_members) {
+  const auto t0 = Clock::now();
+  ReshardPlan rp;
+  for (const auto& [r, ivs] : src.ranges) rp.old_members.push_back(r);
+  for (const auto& [r, ivs] : dst.ranges) rp.new_members.push_back(r);
+  rp.failed = std::move(failed);
+  rp.src = std::move(src);
+  rp.dst = std::move(dst);
+  rp.ring.members = std::move(ring_members);
+  const SnapshotRing* ring = rp.ring.members.empty() ? nullptr : &rp.ring;
+  if (!rp.failed.empty()) {
+    if (ring == nullptr) throw std::invalid_argument("failed members need a snapshot ring");
+    if (!integrity_check(rp.ring, rp.src, rp.failed).recoverable)
+      throw CoverageMismatch("failed members lost together with their ring holders");
+  }
+  rp.plan = overlap_matrix(rp.src, rp.dst, rp.failed, ring);
+  rp.plan_seconds = seconds(t0, Clock::now());
+  return rp;
+}
+
+int ReshardPlan::replica_of(int holder) const {
+  if (ring.members.size() < 2 ||
+      std::find(ring.members.begin(), ring.members.end(), holder) == ring.members.end())
+    return -1;
+  return ring.backs_up(holder);
+}
+
+// ---------------------------------------------------------- ReshardExecutor
+
+ReshardExecutor::ReshardExecutor(const ReshardPlan& rp, int me, bool push,
+                                 std::int64_t block_bytes)
+    : rp_(rp), me_(me), push_(push), block_bytes_(block_bytes) {
+  copies_ = reshard_copies(rp_.plan, rp_.src, rp_.dst, rp_.failed,
+                           rp_.ring.members.empty() ? nullptr : &rp_.ring, me_, push_);
+}
+
+ReshardExecutor::~ReshardExecutor() {
+  ew_copy_program_free(prog_);
+  ew_shardmap_free(new_map_);
+}
+
+std::set<std::pair<int, int>> ReshardExecutor::peers_needed() const {
+  std::set<std::pair<int, int>> out;
+  for (const CopyDesc& c : copies_) {
+    if (c.src_rank != me_) out.insert({static_cast<int>(c.src_role), c.src_rank});
+    if (c.dst_rank != me_) out.insert({static_cast<int>(c.dst_role), c.dst_rank});
+  }
+  return out;
+}
+
+std::int64_t ReshardExecutor::new_bytes() const {
+  return rp_.dst.ranges.count(me_) ? shard_bytes(rp_.dst, me_) : 0;
+}
+
+void ReshardExecutor::bind(const PeerBuffers& peers, bool verify) {
+  if (verify && push_)
+    throw std::invalid_argument("verification on arrival needs pull mode (every byte landing in "
+                                "NEW is then issued by its own GPU)");
+  int top = me_;
+  for (int m : rp_.old_members) top = std::max(top, m);
+  for (int m : rp_.new_members) top = std::max(top, m);
+  const int tr = top + 1;
+  std::vector<void*> table(3 * static_cast<std::size_t>(tr), nullptr);
+  std::vector<ew_copy_desc> d;
+  d.reserve(copies_.size());
+  for (const CopyDesc& c : copies_) {
+    for (const auto& [role, rank] : {std::pair<int, int>{static_cast<int>(c.src_role), c.src_rank},
+                                     std::pair<int, int>{static_cast<int>(c.dst_role), c.dst_rank}}) {
+      void* p = peers.get(role, rank);
+      if (p == nullptr)
+        throw std::runtime_error("peer buffer (role " + std::to_string(role) + ", member " +
+                                 std::to_string(rank) + ") is not mapped");
+      table[static_cast<std::size_t>(role) * tr + rank] = p;
+    }
+    d.push_back({static_cast<std::int32_t>(c.src_role), c.src_rank,
+                 static_cast<std::int32_t>(c.dst_role), c.dst_rank, c.src_off, c.dst_off,
+                 c.bytes});
+  }
+  ew_copy_program_free(prog_);
+  prog_ = nullptr;
+  if (verify && rp_.dst.ranges.count(me_)) {
+    if (new_map_ == nullptr) new_map_ = make_map(shard_segments(rp_.dst, me_), block_bytes_);
+    check(ew_copy_program_create_verified(d.data(), static_cast<std::int64_t>(d.size()),
+                                          table.data(), tr, me_, new_map_, &prog_));
+  } else {
+    check(ew_copy_program_create(d.data(), static_cast<std::int64_t>(d.size()), table.data(), tr,
+                                 me_, &prog_));
+  }
+}
+
+void ReshardExecutor::launch(ew_stream_t stream, std::uint64_t* block_sums,
+                             const int* abort_flag, int n_ctas, int remote_ctas) const {
+  if (prog_ == nullptr) throw std::logic_error("ReshardExecutor::launch before bind");
+  check(ew_copy_program_launch_guarded(prog_, n_ctas, remote_ctas,
+                                       new_map_ != nullptr ? block_sums : nullptr, abort_flag,
+                                       stream));
+}
+
+// ------------------------------------------------------------ BlockVerifier
+
+BlockVerifier::~BlockVerifier() { ew_block_verifier_free(v_); }
+
+void BlockVerifier::set(const std::vector<const std::uint64_t*>& plus,
+                        const std::vector<const std::uint64_t*>& minus, std::int64_t n_words,
+                        std::int64_t lo, std::int64_t hi) {
+  if (hi > n_words) throw std::invalid_argument("BlockVerifier: slice beyond the arrays");
+  ew_block_verifier_free(v_);
+  v_ = nullptr;
+  check(ew_block_verifier_create(plus.data(), static_cast<int>(plus.size()), minus.data(),
+                                 static_cast<int>(minus.size()), lo, hi, &v_));
+}
+
+void BlockVerifier::run(ew_stream_t stream, std::uint32_t* bad_dev) const {
+  check(ew_block_verifier_run(v_, bad_dev, stream));
+}
+
+// ------------------------------------------------------------------ MTTR
+
+std::string mttr_csv_header() {
+  return "event,step,t_event_s,kind,detect_s,comm_repair_s,remap_s,migration_stall_s,"
+         "other_s,lost_work_s,total_s";
+}
+
+std::string mttr_csv_row(int index, const MttrEvent& m) {
+  char buf[320];
+  std::snprintf(buf, sizeof(buf), "%d,%d,%.9g,%s,%.9g,%.9g,%.9g,%.9g,%.9g,%.9g,%.9g", index,
+                m.step, m.t_event_s, m.kind.c_str(), m.detect_s, m.comm_repair_s, m.remap_s,
+                m.migration_stall_s, m.other_s, m.lost_work_s, m.total_s());
+  return buf;
+}
+
+// ------------------------------------------------------- VerifiedMove (impl)
+
+namespace {
+
+// One verified pull move among `survivors` (the executor, the three block-sum
+// arrays on every survivor, the slice verifier); shared by the prepared and
+// the failure-time paths.
+struct VerifiedMove {
+  std::unique_ptr<ReshardExecutor> exec;
+  std::unique_ptr<BlockVerifier> verifier = std::make_unique<BlockVerifier>();
+
+  void wire(const PeerBuffers& peers, const ReshardPlan& rp, int me, std::int64_t n_words) {
+    const std::vector<int> survivors = without(rp.old_members, rp.failed);
+    std::vector<const std::uint64_t*> plus, minus;
+    for (int s : rp.new_members)
+      plus.push_back(static_cast<const std::uint64_t*>(peers.get(kLanded, s)));
+    for (int s : survivors)
+      minus.push_back(static_cast<const std::uint64_t*>(peers.get(kOldBlocks, s)));
+    for (int d : rp.failed)
+      minus.push_back(static_cast<const std::uint64_t*>(peers.get(kReplicaBlocks,
+                                                                   rp.ring.backed_up_by(d))));
+    for (const std::uint64_t* p : plus)
+      if (!p) throw std::runtime_error("landed block sums of a survivor are not mapped");
+    for (const std::uint64_t* p : minus)
+      if (!p) throw std::runtime_error("source block sums of a survivor are not mapped");
+    const auto [lo, hi] = slice_of(n_words, index_of(rp.new_members, me),
+                                   static_cast<int>(rp.new_members.size()));
+    verifier->set(plus, minus, n_words, lo, hi);
+  }
+};
+
+// Shared launch + verdict: zero landed, copy (verified), device barrier,
+// slice check, host verdict over the survivors' channel.
+bool run_move(const ReshardExecutor& exec, const BlockVerifier& verifier, std::uint64_t* landed,
+              std::int64_t n_words,
+              std::uint32_t* bad, ew_peer_barrier* barrier, double timeout_s, Channel& survivors,
+              ew_stream_t stream, MttrEvent* ev) {
+  cudaEvent_t e[3];
+  for (cudaEvent_t& x : e) cuda_check(cudaEventCreate(&x), "cudaEventCreate");
+  const auto t0 = Clock::now();
+  check(ew_memset_async(landed, 0, n_words * 8, stream));
+  cuda_check(cudaEventRecord(e[0], reinterpret_cast<cudaStream_t>(stream)), "record");
+  exec.launch(stream, landed);
+  cuda_check(cudaEventRecord(e[1], reinterpret_cast<cudaStream_t>(stream)), "record");
+  if (barrier != nullptr) {
+    check(ew_peer_barrier_wait(barrier, timeout_s, stream));  // every survivor landed
+  } else {
+    check(ew_stream_sync(stream));
+    survivors.barrier();
+  }
+  verifier.run(stream, bad);
+  cuda_check(cudaEventRecord(e[2], reinterpret_cast<cudaStream_t>(stream)), "record");
+  std::uint32_t bad_host = 0;
+  check(ew_memcpy_async(&bad_host, bad, 4, stream));
+  check(ew_stream_sync(stream));
+  int timed_out = 0;
+  if (barrier != nullptr) check(ew_peer_barrier_timed_out(barrier, &timed_out));
+  const auto t1 = Clock::now();
+  const std::int64_t total = survivors.sum(static_cast<std::int64_t>(bad_host) +
+                                           (timed_out ? (std::int64_t{1} << 40) : 0));
+  const auto t2 = Clock::now();
+  float copy_ms = 0.f, verify_ms = 0.f;
+  cudaEventElapsedTime(&copy_ms, e[0], e[1]);
+  cudaEventElapsedTime(&verify_ms, e[1], e[2]);
+  for (cudaEvent_t x : e) cudaEventDestroy(x);
+  if (ev != nullptr) {
+    ev->phases["copy_s"] = copy_ms / 1e3;
+    ev->phases["barrier_verify_s"] = verify_ms / 1e3;
+    ev->phases["verdict_exchange_s"] = seconds(t1, t2);
+    ev->phases["launch_to_verdict_s"] = seconds(t0, t2);
+    ev->phases["mismatched_block_words"] = static_cast<double>(total % (std::int64_t{1} << 40));
+    ev->phases["barrier_timeouts"] = static_cast<double>(total >> 40);
+  }
+  return total == 0;
+}
+
+}  // namespace
+
+// --------------------------------------------------------- PreparedRecovery
+
+PreparedRecovery::PreparedRecovery(Channel& ch, const std::vector<std::int64_t>& layer_bytes,
+                                   void* old_buf, const std::uint64_t* old_rows, void* replica,
+                                   const std::uint64_t* replica_rows, void* new_buf,
+                                   std::int64_t new_capacity, PreparedOptions opt)
+    : ch_(ch), members_(ch.members()), me_(ch.me()), opt_(opt) {
+  const int n = static_cast<int>(members_.size());
+  if (n < 2) throw std::invalid_argument("PreparedRecovery needs at least two members");
+  std::int64_t max_new = 0;
+  for (int d : members_) {
+    if (d == me_) continue;
+    plans_[d] = std::make_unique<ReshardPlan>(
+        ReshardPlan::build(layer_bytes, members_, without(members_, {d})));
+    max_new = std::max(max_new, shard_bytes(plans_[d]->dst, me_));
+  }
+  const ReshardPlan& any = *plans_.begin()->second;
+  n_words_ = 2 * any.n_blocks(opt_.block_bytes);
+  try {
+    if (new_buf != nullptr) {
+      if (new_capacity < max_new)
+        throw std::invalid_argument("PreparedRecovery: NEW buffer of " +
+                                    std::to_string(new_capacity) + " bytes, the largest "
+                                    "departure needs " + std::to_string(max_new));
+      new_buf_ = new_buf;
+      own_new_ = false;
+    } else {
+      new_buf_ = dalloc<std::uint8_t>((max_new + 31) / 32 * 32);
+    }
+    landed_ = dalloc<std::uint64_t>(n_words_);
+    old_blocks_ = dalloc<std::uint64_t>(n_words_);
+    replica_blocks_ = dalloc<std::uint64_t>(n_words_);
+    bad_ = dalloc<std::uint32_t>(4);
+    flags_ = dalloc<unsigned long long>(static_cast<std::int64_t>(n) * n);
+    check(ew_memset_async(old_blocks_, 0, n_words_ * 8, nullptr));
+    check(ew_memset_async(replica_blocks_, 0, n_words_ * 8, nullptr));
+    check(ew_memset_async(landed_, 0, n_words_ * 8, nullptr));
+    check(ew_memset_async(flags_, 0, 8 * static_cast<std::int64_t>(n) * n, nullptr));
+    // this rank's share of the source block sums: its OLD shard and the
+    // replica it keeps (from the snapshot rows when given)
+    const std::int64_t nb = n_words_ / 2;
+    add_blocks(any.src, me_, old_buf, old_rows, old_blocks_, nb, opt_.block_bytes, nullptr);
+    if (replica != nullptr)
+      add_blocks(any.src, any.ring.backs_up(me_), replica, replica_rows, replica_blocks_, nb,
+                 opt_.block_bytes, nullptr);
+    check(ew_device_sync());
+    peers_.exchange(ch_, {{static_cast<int>(BufRole::Old), old_buf},
+                          {static_cast<int>(BufRole::Replica), replica},
+                          {kLanded, landed_},
+                          {kOldBlocks, old_blocks_},
+                          {kReplicaBlocks, replica_blocks_},
+                          {kFlags, flags_}});
+    peers_.put(static_cast<int>(BufRole::New), me_, new_buf_);
+    for (const auto& [d, rp] : plans_) {
+      auto mv = std::make_unique<VerifiedMove>();
+      mv->exec = std::make_unique<ReshardExecutor>(*rp, me_, false, opt_.block_bytes);
+      mv->exec->bind(peers_, true);
+      mv->wire(peers_, *rp, me_, n_words_);
+      execs_[d] = std::move(mv->exec);
+      verifiers_[d] = std::move(mv->verifier);
+      survivors_[d] = std::make_unique<Channel>(ch_.store(), ch_.name() + "/without" +
+                                                                  std::to_string(d),
+                                                rp->new_members, me_);
+      barriers_[d] = make_barrier(peers_, rp->new_members, me_,
+                                  static_cast<std::int64_t>(index_of(members_, d)) * n);
+    }
+  } catch (...) {
+    release();
+    throw;
+  }
+  ch_.barrier();  // every flag array zeroed and every mapping in place
+}
+
+PreparedRecovery::~PreparedRecovery() { release(); }
+
+void PreparedRecovery::release() {
+  for (auto& [d, b] : barriers_) ew_peer_barrier_free(b);
+  barriers_.clear();
+  verifiers_.clear();
+  execs_.clear();
+  peers_.close();
+  if (!own_new_) new_buf_ = nullptr;
+  for (void* p : {static_cast<void*>(new_buf_), static_cast<void*>(landed_),
+                  static_cast<void*>(old_blocks_), static_cast<void*>(replica_blocks_),
+                  static_cast<void*>(bad_), static_cast<void*>(flags_)})
+    dfree(p);
+  new_buf_ = nullptr;
+  landed_ = old_blocks_ = replica_blocks_ = nullptr;
+  bad_ = nullptr;
+  flags_ = nullptr;
+}
+
+std::int64_t PreparedRecovery::new_bytes(int departed) const {
+  return shard_bytes(plans_.at(departed)->dst, me_);
+}
+
+bool PreparedRecovery::recover(int departed, ew_stream_t stream, MttrEvent* ev) {
+  if (departed == me_) throw std::invalid_argument("the departed member does not recover itself");
+  if (!plans_.count(departed))
+    throw std::invalid_argument("member " + std::to_string(departed) + " is not in the group");
+  const bool ok = run_move(*execs_.at(departed), *verifiers_.at(departed), landed_, n_words_,
+                           bad_, barriers_.at(departed), opt_.barrier_timeout_s,
+                           *survivors_.at(departed), stream, ev);
+  if (ev != nullptr) {
+    ev->phases["plan_s"] = 0.0;  // planned in steady state
+    ev->phases["prepared"] = 1.0;
+    ev->verified = ok;
+  }
+  return ok;
+}
+
+// ----------------------------------------------------------------- DpGroup
+
+DpGroup::DpGroup(Channel& ch, const std::vector<std::int64_t>& layer_bytes, ew_comm* comm,
+                 DpGroupOptions opt)
+    : ch_(ch), layer_bytes_(layer_bytes), members_(ch.members()), comm_(comm), opt_(opt) {
+  mb_sizes_.assign(members_.size(), opt_.per_slot_mbs);
+  for (std::size_t i = 0; i < members_.size(); ++i)
+    for (std::size_t j = i + 1; j < members_.size(); ++j)
+      links_.insert(make_link(members_[i], members_[j]));
+  if (opt_.prepare_comms && comm_ != nullptr) prepare();
+}
+
+DpGroup::~DpGroup() {
+  for (auto& [d, c] : prepared_comms_) ew_comm_destroy(c);
+  prepared_comms_.clear();
+  ew_comm_destroy(comm_);
+  for (auto it = retired_.rbegin(); it != retired_.rend(); ++it) ew_comm_destroy(*it);
+}
+
+void DpGroup::prepare() {
+  if (comm_ == nullptr || members_.size() < 2) return;
+  for (auto& [d, c] : prepared_comms_) ew_comm_destroy(c);
+  prepared_comms_.clear();
+  const int me = ch_.me();
+  const int key = index_of(members_, me);
+  for (int d : members_) {
+    ew_comm* c = nullptr;
+    check(ew_comm_split(comm_, me == d ? -1 : 0, key, 1, &c));
+    if (c != nullptr) prepared_comms_[d] = c;
+  }
+  // one collective on each (NCCL connects lazily): the repair at failure
+  // time is then a lookup of a live communicator
+  std::int64_t* one = dalloc<std::int64_t>(1);
+  for (int d : members_)
+    if (d != me) check(ew_allreduce_i64(prepared_comms_.at(d), one, 1, nullptr));
+  check(ew_device_sync());
+  dfree(one);
+}
+
+MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
+                           const RankBuffers& bufs, ew_stream_t stream, int step) {
+  if (kind == EventKind::ScaleOut || kind == EventKind::FailSlow)
+    throw std::invalid_argument("DpGroup::recover handles departures (FailStop / ScaleIn)");
+  std::set<int> gone(departed.begin(), departed.end());
+  for (int d : gone)
+    if (index_of(members_, d) < 0)
+      throw std::invalid_argument("departed member " + std::to_string(d) + " is not in the group");
+  if (gone.count(ch_.me())) throw std::invalid_argument("a departed member does not recover");
+  const std::vector<int> survivors = without(members_, gone);
+  MttrEvent ev;
+  ev.step = step;
+  ev.kind = to_string(kind);
+  const auto t0 = Clock::now();
+
+  // comm repair: the edit plan (communicator.cpp:54-105), then the NCCL
+  // communicator: a prepared split (lookup) or a shrink at failure time;
+  // its first collective is part of the repair
+  ElasticEvent e;
+  e.kind = kind;
+  e.targets = std::vector<DeviceId>(gone.begin(), gone.end());
+  const EditPlan edit = plan_edit({CommGroup{"dp", members_, GroupTopology::Mesh}}, e, links_);
+  for (const Link& l : edit.links_to_remove) links_.erase(l);
+  links_.insert(edit.links_to_add.begin(), edit.links_to_add.end());
+  const auto t_edit = Clock::now();
+  ew_comm* new_comm = nullptr;
+  if (comm_ != nullptr) {
+    if (gone.size() == 1 && prepared_comms_.count(*gone.begin())) {
+      new_comm = prepared_comms_.at(*gone.begin());
+      prepared_comms_.erase(*gone.begin());
+      ev.phases["comm_prepared"] = 1.0;
+    } else {
+      std::vector<int> ranks;
+      for (int d : gone) ranks.push_back(index_of(members_, d));  // ranks of the CURRENT comm
+      check(ew_comm_shrink(comm_, ranks.data(), static_cast<int>(ranks.size()), 0, &new_comm));
+      ev.phases["comm_prepared"] = 0.0;
+    }
+    const auto t_c = Clock::now();
+    std::int64_t* one = dalloc<std::int64_t>(1);
+    check(ew_allreduce_i64(new_comm, one, 1, stream));
+    check(ew_stream_sync(stream));
+    dfree(one);
+    ev.phases["comm_acquire_s"] = seconds(t_edit, t_c);
+    ev.phases["first_collective_s"] = seconds(t_c, Clock::now());
+  }
+  ev.phases["plan_edit_s"] = seconds(t0, t_edit);
+  const auto t1 = Clock::now();
+  ev.comm_repair_s = seconds(t0, t1);
+
+  // dataflow: the global batch over the survivors (dataflow.cpp:52-69)
+  MicrobatchAssignment mb;
+  for (std::size_t i = 0; i < members_.size(); ++i) mb.slots.push_back(static_cast<int>(i));
+  mb.per_slot_mbs = mb_sizes_;
+  mb.num_microbatches = opt_.num_microbatches;
+  std::vector<int> idx;
+  for (int s : survivors) idx.push_back(index_of(members_, s));
+  const MicrobatchAssignment next = reshard_microbatches(mb, idx);
+  const auto t2 = Clock::now();
+  ev.other_s = seconds(t1, t2);
+
+  // remap
+  if (prepared_ != nullptr && gone.size() == 1 && prepared_->members() == members_) {
+    ev.verified = prepared_->recover(*gone.begin(), stream, &ev);
+  } else {
+    Channel sc(ch_.store(), ch_.name() + "/event" + std::to_string(events_), survivors,
+               ch_.me());
+    const ReshardPlan rp = ReshardPlan::build(layer_bytes_, members_, survivors);
+    const std::int64_t n_words = 2 * rp.n_blocks(opt_.block_bytes);
+    std::uint64_t* landed = dalloc<std::uint64_t>(n_words);
+    std::uint64_t* old_blocks = dalloc<std::uint64_t>(n_words);
+    std::uint64_t* rep_blocks = dalloc<std::uint64_t>(n_words);
+    std::uint32_t* bad = dalloc<std::uint32_t>(4);
+    try {
+      const auto tp = Clock::now();
+      check(ew_memset_async(old_blocks, 0, n_words * 8, stream));
+      check(ew_memset_async(rep_blocks, 0, n_words * 8, stream));
+      add_blocks(rp.src, ch_.me(), bufs.old_buf, nullptr, old_blocks, n_words / 2,
+                 opt_.block_bytes, stream);
+      const int owner = rp.replica_of(ch_.me());
+      if (owner >= 0 && rp.failed.count(owner)) {
+        if (bufs.replica == nullptr)
+          throw std::invalid_argument("this rank holds the departed member's replica: pass it");
+        add_blocks(rp.src, owner, bufs.replica, nullptr, rep_blocks, n_words / 2,
+                   opt_.block_bytes, stream);
+      }
+      PeerBuffers peers;
+      std::map<int, void*> mine = {{static_cast<int>(BufRole::Old), bufs.old_buf},
+                                   {kLanded, landed}, {kOldBlocks, old_blocks},
+                                   {kReplicaBlocks, rep_blocks}};
+      if (owner >= 0 && rp.failed.count(owner)) mine[static_cast<int>(BufRole::Replica)] = bufs.replica;
+      peers.exchange(sc, mine);
+      peers.put(static_cast<int>(BufRole::New), ch_.me(), bufs.new_buf);
+      VerifiedMove mv;
+      mv.exec = std::make_unique<ReshardExecutor>(rp, ch_.me(), false, opt_.block_bytes);
+      mv.exec->bind(peers, true);
+      mv.wire(peers, rp, ch_.me(), n_words);
+      ev.phases["plan_s"] = rp.plan_seconds;
+      ev.phases["map_bind_s"] = seconds(tp, Clock::now());
+      sc.barrier();  // every survivor bound and its source sums ready
+      ev.verified = run_move(*mv.exec, *mv.verifier, landed, n_words, bad, nullptr, 0.0, sc,
+                             stream, &ev);
+      mv.exec.reset();
+      peers.close();
+    } catch (...) {
+      for (void* p : {static_cast<void*>(landed), static_cast<void*>(old_blocks),
+                      static_cast<void*>(rep_blocks), static_cast<void*>(bad)})
+        dfree(p);
+      throw;
+    }
+    for (void* p : {static_cast<void*>(landed), static_cast<void*>(old_blocks),
+                    static_cast<void*>(rep_blocks), static_cast<void*>(bad)})
+      dfree(p);
+  }
+  ++events_;
+  ev.remap_s = seconds(t2, Clock::now());
+
+  // commit the new membership; the communicators of other departures were
+  // built over the old membership
+  members_ = survivors;
+  mb_sizes_ = next.per_slot_mbs;
+  if (comm_ != nullptr) {
+    for (auto& [d, c] : prepared_comms_) ew_comm_destroy(c);
+    prepared_comms_.clear();
+    retired_.push_back(comm_);  // children share its resources: freed last
+    comm_ = new_comm;
+  }
+  return ev;
+}
+
+// --------------------------------------------------------- InPlaceExecutor
+
+struct InPlaceExecutor::Phase {
+  ew_copy_program* direct = nullptr;
+  ew_copy_program* staged = nullptr;
+  ew_copy_program* flush = nullptr;
+  ~Phase() {
+    ew_copy_program_free(direct);
+    ew_copy_program_free(staged);
+    ew_copy_program_free(flush);
+  }
+};
+
+namespace {
+
+// NEW's segment map restricted to packed offsets [lo, hi), re-based at `pad`
+// with a leading pad segment (nothing lands there) so the map stays packed.
+std::vector<Segment> clip_segments(const std::vector<Segment>& segs, std::int64_t lo,
+                                   std::int64_t hi, std::int64_t pad) {
+  std::vector<Segment> out;
+  for (const Segment& s : segs) {
+    const std::int64_t x = std::max(s.local_off, lo), y = std::min(s.local_off + s.length, hi);
+    if (y <= x) continue;
+    if (out.empty() && pad > 0)
+      out.push_back({s.global_lo + (x - s.local_off) - pad, pad, 0});
+    out.push_back({s.global_lo + (x - s.local_off), y - x, x - lo + pad});
+  }
+  return out;
+}
+
+ew_copy_program* program(const std::vector<CopyDesc>& copies, const std::vector<void*>& table,
+                         int tr, int me, ew_shardmap* verify_map) {
+  std::vector<ew_copy_desc> d;
+  for (const CopyDesc& c : copies)
+    d.push_back({static_cast<std::int32_t>(c.src_role), c.src_rank,
+                 static_cast<std::int32_t>(c.dst_role), c.dst_rank, c.src_off, c.dst_off,
+                 c.bytes});
+  ew_copy_program* p = nullptr;
+  if (verify_map != nullptr)
+    check(ew_copy_program_create_verified(d.data(), static_cast<std::int64_t>(d.size()),
+                                          table.data(), tr, me, verify_map, &p));
+  else
+    check(ew_copy_program_create(d.data(), static_cast<std::int64_t>(d.size()), table.data(), tr,
+                                 me, &p));
+  return p;
+}
+
+}  // namespace
+
+InPlaceExecutor::InPlaceExecutor(Channel& ch, const ReshardPlan& rp, void* buf, void* replica,
+                                 InPlaceOptions opt)
+    : rp_(rp), me_(ch.me()), opt_(opt), buf_(buf) {
+  std::int64_t biggest = 0;
+  for (int r : rp_.new_members) biggest = std::max(biggest, shard_bytes(rp_.dst, r));
+  std::int64_t phase = opt_.phase_bytes;
+  if (phase <= 0)  // ~28 phases: profiles/r01_config_d_inplace_sweep_70gb.log
+    phase = std::min<std::int64_t>(std::int64_t{8} << 30,
+                                   std::max<std::int64_t>(std::int64_t{256} << 20, biggest / 28));
+  sched_ = inplace_schedule(rp_.layer_bytes, rp_.src, rp_.dst, rp_.failed, opt_.stage_bytes,
+                            phase, opt_.slack);
+  const bool in_new = std::find(rp_.new_members.begin(), rp_.new_members.end(), me_) !=
+                      rp_.new_members.end();
+  const bool in_old = std::find(rp_.old_members.begin(), rp_.old_members.end(), me_) !=
+                      rp_.old_members.end();
+  const int n_new = static_cast<int>(rp_.new_members.size());
+  if (in_new) {
+    flags_ = dalloc<unsigned long long>(std::max(2, n_new));
+    check(ew_memset_async(flags_, 0, 8 * std::max(2, n_new), nullptr));
+    check(ew_device_sync());
+  }
+  std::map<int, void*> mine = {{kFlags, flags_}};
+  if (in_old && !rp_.failed.count(me_)) mine[static_cast<int>(BufRole::Old)] = buf_;
+  if (replica != nullptr) mine[static_cast<int>(BufRole::Replica)] = replica;
+  peers_.exchange(ch, mine);
+  if (!in_new) {
+    ch.barrier();
+    return;
+  }
+  try {
+    for (int k = 0; k < sched_.ring && sched_.stage_alloc > 0; ++k)
+      staging_.push_back(dalloc<std::uint8_t>(std::max<std::int64_t>(16, sched_.stage_alloc)));
+    int top = me_;
+    for (int m : rp_.old_members) top = std::max(top, m);
+    for (int m : rp_.new_members) top = std::max(top, m);
+    const int tr = top + 1;
+    std::vector<void*> table(3 * static_cast<std::size_t>(tr), nullptr);
+    for (int role = 0; role < 2; ++role)
+      for (int m = 0; m < tr; ++m) table[static_cast<std::size_t>(role) * tr + m] = peers_.get(role, m);
+    table[2 * static_cast<std::size_t>(tr) + me_] = buf_;
+    const std::vector<CopyDesc> copies =
+        reshard_copies(rp_.plan, rp_.src, rp_.dst, rp_.failed, &rp_.ring, me_, false);
+    const std::vector<Segment> new_segs = shard_segments(rp_.dst, me_);
+    maps_.push_back(make_map(new_segs, opt_.block_bytes));
+    const InPlaceRanges& rr = sched_.ranks.at(me_);
+    for (std::size_t j = 0; j < sched_.phases.size(); ++j) {
+      auto ph = std::make_unique<Phase>();
+      const auto [dlo, dhi] = rr.direct[j];
+      const std::vector<CopyDesc> d = clip_copies(copies, dlo, dhi, dlo);
+      if (!d.empty()) ph->direct = program(d, table, tr, me_, maps_.front());
+      const auto [slo, shi] = rr.staged[j];
+      if (shi > slo) {
+        void* st = staging_[j % static_cast<std::size_t>(sched_.ring)];
+        const std::int64_t pad = slo % 16;  // staging keeps NEW's alignment mod 16
+        std::vector<void*> t2 = table;
+        t2[2 * static_cast<std::size_t>(tr) + me_] = st;
+        maps_.push_back(make_map(clip_segments(new_segs, slo, shi, pad), opt_.block_bytes));
+        ph->staged = program(clip_copies(copies, slo, shi, pad), t2, tr, me_, maps_.back());
+        const void* src = static_cast<std::uint8_t*>(st) + pad;
+        void* dst = static_cast<std::uint8_t*>(buf_) + slo;
+        const std::int64_t bytes = shi - slo;
+        const int remote = 0;
+        check(ew_copy_program_create_raw(&src, &dst, &bytes, &remote, 1, &ph->flush));
+      }
+      phases_.push_back(std::move(ph));
+    }
+    barrier_ = make_barrier(peers_, rp_.new_members, me_, 0);
+    const int n_streams = std::max(1, opt_.gather_streams) - 1 + 2;  // extra gathers + sync + flush
+    for (int k = 0; k < n_streams; ++k) {
+      cudaStream_t s = nullptr;
+      cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "cudaStreamCreate");
+      streams_.push_back(s);
+    }
+  } catch (...) {
+    release();
+    throw;
+  }
+  ch.barrier();
+}
+
+InPlaceExecutor::~InPlaceExecutor() { release(); }
+
+void InPlaceExecutor::release() {
+  for (void* s : streams_) cudaStreamDestroy(static_cast<cudaStream_t>(s));
+  streams_.clear();
+  phases_.clear();
+  for (ew_shardmap* m : maps_) ew_shardmap_free(m);
+  maps_.clear();
+  if (barrier_ != nullptr) ew_peer_barrier_free(barrier_);
+  barrier_ = nullptr;
+  peers_.close();
+  for (void* p : staging_) dfree(p);
+  staging_.clear();
+  dfree(flags_);
+  flags_ = nullptr;
+}
+
+void InPlaceExecutor::launch(ew_stream_t stream, std::uint64_t* block_sums) {
+  if (barrier_ == nullptr) return;  // not a member of the target layout
+  const int ng = std::max(1, opt_.gather_streams);
+  cudaStream_t main = reinterpret_cast<cudaStream_t>(stream);
+  std::vector<cudaStream_t> gs = {main};
+  for (int k = 0; k < ng - 1; ++k) gs.push_back(static_cast<cudaStream_t>(streams_[k]));
+  cudaStream_t ys = static_cast<cudaStream_t>(streams_[ng - 1]);
+  cudaStream_t fs = static_cast<cudaStream_t>(streams_[ng]);
+  std::vector<cudaEvent_t> events;
+  auto event = [&](cudaStream_t s) {
+    cudaEvent_t e = nullptr;
+    cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventRecord(e, s), "cudaEventRecord");
+    events.push_back(e);
+    return e;
+  };
+  const cudaEvent_t start = event(main);
+  for (std::size_t k = 1; k < gs.size(); ++k) cudaStreamWaitEvent(gs[k], start, 0);
+  cudaStreamWaitEvent(ys, start, 0);
+  cudaStreamWaitEvent(fs, start, 0);
+  const int* veto = nullptr;
+  check(ew_peer_barrier_error_flag(barrier_, &veto));
+  std::vector<cudaEvent_t> bar;
+  std::vector<cudaEvent_t> flushed;
+  const int slack = sched_.slack, ring = sched_.ring;
+  for (std::size_t j = 0; j < phases_.size(); ++j) {
+    cudaStream_t g = gs[j % gs.size()];
+    const long k = static_cast<long>(j) - slack - 1;
+    if (k >= 0) cudaStreamWaitEvent(g, bar[static_cast<std::size_t>(k)], 0);  // all read R_k
+    if (static_cast<long>(j) >= ring && flushed[j - ring] != nullptr)
+      cudaStreamWaitEvent(g, flushed[j - ring], 0);  // staging buffer free again
+    const Phase& ph = *phases_[j];
+    if (ph.staged) check(ew_copy_program_launch_guarded(ph.staged, 0, 0, block_sums, veto, g));
+    if (ph.direct) check(ew_copy_program_launch_guarded(ph.direct, 0, 0, block_sums, veto, g));
+    cudaStreamWaitEvent(ys, event(g), 0);
+    check(ew_peer_barrier_wait(barrier_, opt_.barrier_timeout_s, ys));  // all read R_j
+    bar.push_back(event(ys));
+    if (ph.flush) {
+      cudaStreamWaitEvent(fs, bar.back(), 0);
+      check(ew_copy_program_launch_guarded(ph.flush, opt_.flush_ctas, 0, nullptr, veto, fs));
+      flushed.push_back(event(fs));
+    } else {
+      flushed.push_back(nullptr);
+    }
+  }
+  for (std::size_t k = 1; k < gs.size(); ++k) cudaStreamWaitEvent(main, event(gs[k]), 0);
+  cudaStreamWaitEvent(main, event(ys), 0);
+  cudaStreamWaitEvent(main, event(fs), 0);
+  for (cudaEvent_t e : events) cudaEventDestroy(e);  // released once their waits resolve
+}
+
+bool InPlaceExecutor::timed_out() const {
+  if (barrier_ == nullptr) return false;
+  int t = 0;
+  check(ew_peer_barrier_timed_out(barrier_, &t));
+  return t != 0;
+}
+
+}  // namespace elaskit::b200

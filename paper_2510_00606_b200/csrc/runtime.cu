@@ -278,6 +278,29 @@ int ew_comm_shrink(ew_comm* parent, const int* exclude_ranks, int n_exclude, int
   return EW_OK;
 }
 
+int ew_comm_split(ew_comm* parent, int color, int key, int share, ew_comm** out) {
+  if (parent == nullptr || out == nullptr)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_comm_split: bad arguments");
+  *out = nullptr;
+  auto* c = new ew_comm();
+  ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+  cfg.splitShare = share ? 1 : 0;
+  const ncclResult_t r =
+      ncclCommSplit(parent->nccl, color < 0 ? NCCL_SPLIT_NOCOLOR : color, key, &c->nccl, &cfg);
+  if (r != ncclSuccess) {
+    delete c;
+    return nccl_status(r, "ncclCommSplit");
+  }
+  if (c->nccl == nullptr) {  // NCCL_SPLIT_NOCOLOR: not a member of any child
+    delete c;
+    return EW_OK;
+  }
+  ncclCommUserRank(c->nccl, &c->rank);
+  ncclCommCount(c->nccl, &c->nranks);
+  *out = c;
+  return EW_OK;
+}
+
 int ew_comm_rank(const ew_comm* comm, int* rank, int* nranks) {
   if (comm == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL comm");
   if (rank) *rank = comm->rank;

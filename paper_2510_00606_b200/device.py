@@ -516,9 +516,20 @@ class Communicator:
         return Communicator(h) if h.value else None
 
     def destroy(self) -> None:
+        """Free the communicator; a no-op on a borrowed one (a recovery.DpGroup
+        owns its communicators) or one whose ownership moved."""
+        if getattr(self, "_borrowed", False):
+            self._h = None
+            return
         if self._h is not None and self._h.value:
             check(lib.ew_comm_destroy(self._h))
             self._h = None
+
+    def split(self, color: int, key: int, share: bool = True) -> Optional["Communicator"]:
+        """ncclCommSplit; color < 0 leaves this rank out (returns None)."""
+        h = C.c_void_p()
+        check(lib.ew_comm_split(self._h, int(color), int(key), int(bool(share)), C.byref(h)))
+        return Communicator(h) if h.value else None
 
     def allreduce_i64(self, t: torch.Tensor, stream=None) -> None:
         check(lib.ew_allreduce_i64(self._h, _ptr(t), t.numel(), _stream(stream)))

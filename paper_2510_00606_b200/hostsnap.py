@@ -173,13 +173,11 @@ class HostSnapshots:
         return epoch
 
     def attach(self, ex: ReshardExecutor, departed: Iterable[int]) -> None:
-        """Point the holder's REPLICA entry of ex's copy table at each
-        departed rank's host image (call before ex.bind; allocate the
-        executor's buffers without a device replica)."""
-        table = getattr(ex, "_table", {})
+        """Point the holder's REPLICA entry of ex's peer table at each
+        departed rank's last committed host image (call before ex.bind;
+        allocate the executor's buffers without a device replica)."""
         for d in departed:
-            table[(ROLE_REPLICA, self.ring.backed_up_by(d))] = self.device_ptr(d)
-        ex._table = table
+            ex.put_peer(ROLE_REPLICA, self.ring.backed_up_by(d), self.device_ptr(d))
 
     def close(self) -> None:
         if self._closed:

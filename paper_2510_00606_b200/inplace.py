@@ -16,7 +16,8 @@ processing order reads R_j = [old(G_lo_j), old(G_hi_j)) of every rank's OLD
 and writes W_j = [new(G_lo_j), new(G_hi_j)) of its NEW; with the cut rule,
 the reads of every later phase lie beyond W_j (below it for departures).
 
-Execution, per rank (three streams, `s` = slack):
+Execution (C++, elaskit::b200::InPlaceExecutor), per rank (three streams,
+`s` = slack):
   gather_j   waits until every rank finished gather_{j-s-1}, then pulls the
              phase's NEW bytes (peers' OLD, ring replicas, own OLD): the part
              of W_j clear of R_{j-s} .. R_j lands DIRECTLY in NEW, the rest in
@@ -180,15 +181,20 @@ class InPlaceSchedule:
 
 
 class StagedInPlaceReshard:
-    """One rank's executor of an InPlaceSchedule (one process per GPU).
+    """One rank's executor of an InPlaceSchedule (one process per GPU): a
+    binding of the C++ elaskit::b200::InPlaceExecutor (ew_inplace_exec),
+    which maps the peers, builds every phase's verified gathers and flush
+    and enqueues the phases behind device-side barriers.
 
     Buffers: `buf` (OLD on entry, NEW on exit; max(|OLD|, |NEW|) bytes), the
     ring replica when this rank holds a departed rank's replica, and
-    `schedule.ring` staging buffers of `schedule.stage_alloc` bytes."""
+    `schedule.ring` staging buffers of `schedule.stage_alloc` bytes (owned by
+    the executor)."""
 
     def __init__(self, rp: ReshardPlan, rank: int, stage_bytes: int = 1 << 30,
                  block_bytes: int = dev.DEFAULT_BLOCK_BYTES,
-                 phase_bytes: Optional[int] = None, slack: int = 1):
+                 phase_bytes: Optional[int] = None, slack: int = 1, gather_streams: int = 2,
+                 flush_ctas: int = 64, barrier_timeout_s: float = 30.0):
         # defaults from the sweeps (profiles/r01_config_d_inplace_sweep_70gb.log,
         # profiles/r01_inplace_sweep_7b_4gpu.log): slack 1, two gather streams
         # and ~28 phases — smaller phases stage less of the bottom layers,
@@ -200,15 +206,14 @@ class StagedInPlaceReshard:
         self.rp = rp
         self.rank = rank
         self.block_bytes = block_bytes
+        self.stage_bytes, self.phase_bytes, self.slack = stage_bytes, phase_bytes, slack
+        self.gather_streams, self.flush_ctas = gather_streams, flush_ctas
+        self.barrier_timeout_s = barrier_timeout_s
         self.sched = InPlaceSchedule(rp, stage_bytes, phase_bytes, slack)
         self.n_old = rp.src.shard_bytes(rank) if rank in rp.old_ranks else 0
         self.n_new = rp.dst.shard_bytes(rank) if rank in rp.new_ranks else 0
-        self.direct: List[Optional[dev.CopyProgram]] = []
-        self.staged: List[Optional[dev.CopyProgram]] = []
-        self.flushes: List[Optional[dev.CopyProgram]] = []
-        self.staging: List[torch.Tensor] = []
-        self._base: Optional[ReshardExecutor] = None
-        self.barrier: Optional[dev.PeerBarrier] = None
+        self._h: Optional[C.c_void_p] = None
+        self.buf: Optional[torch.Tensor] = None
 
     def allocate(self) -> RankBuffers:
         """OLD and NEW alias one allocation; staging is allocated at bind()."""
@@ -223,121 +228,61 @@ class StagedInPlaceReshard:
         return RankBuffers(old, replica, new)
 
     def bind(self, bufs: RankBuffers, group=None, survivors_group=None) -> None:
-        """Collective over `group`: map peers' OLD/REPLICA (as in steady
-        state) and build every phase's verified gathers and flush.
-        `survivors_group`: the process group of the NEW members (barrier)."""
-        self._base = ReshardExecutor(self.rp, self.rank, push=False)
-        self._base.premap(bufs, group)
-        if self.rank not in self.rp.new_ranks:
-            return
-        sc, r = self.sched, self.rank
-        self.barrier = dev.PeerBarrier(survivors_group)
-        self.staging = [dev.empty_bytes(sc.stage_alloc) for _ in range(sc.ring)] \
-            if sc.stage_alloc else []
-        table = dict(self._base._table)
-        for role, t in ((ROLE_OLD, bufs.old), (ROLE_REPLICA, bufs.replica),
-                        (ROLE_NEW, bufs.new)):
-            if t is not None:
-                table[(role, r)] = t.data_ptr()
-        import torch.distributed as dist
-        world = dist.get_world_size(group)
-        n_table = max(max(self.rp.old_ranks + self.rp.new_ranks) + 1, world)
-        descs = self.rp.copies(r, push=False)
-        full_map = dev.ShardMap(sc.new_segs[r], self.block_bytes)
-        self.direct, self.staged, self.flushes = [], [], []
-        for j in range(len(sc.phases)):
-            d = sc.direct_descs(r, j, descs)
-            self.direct.append(dev.CopyProgram.from_descs(d, table, n_table, r, full_map)
-                               if len(d) else None)
-            lo, hi = sc.staged[r][j]
-            if hi > lo:
-                st = self.staging[j % sc.ring]
-                t = dict(table)
-                t[(ROLE_NEW, r)] = st.data_ptr()
-                vmap = dev.ShardMap(sc.staged_segments(r, j), self.block_bytes)
-                self.staged.append(dev.CopyProgram.from_descs(sc.staged_descs(r, j, descs), t,
-                                                              n_table, r, vmap))
-                self.flushes.append(dev.CopyProgram.from_pointers(
-                    [st.data_ptr() + sc.pad(lo)], [self.buf.data_ptr() + lo], [hi - lo],
-                    [False]))
-            else:
-                self.staged.append(None)
-                self.flushes.append(None)
-        self.sync_stream = torch.cuda.Stream()
-        self.flush_stream = torch.cuda.Stream()
-        self.gather_streams: List[torch.cuda.Stream] = []
+        """Collective over `group` (old and new members): map the peers and
+        build the programs (C++).  `survivors_group` is accepted for API
+        compatibility; the executor's barrier spans the NEW members."""
+        from .rendezvous import Channel
+        ch = Channel.from_group(group, "inplace")
+        rp = self.rp
+        buf = self.buf if self.buf is not None else (bufs.old if bufs.old is not None else bufs.new)
+        h = C.c_void_p()
+        check(lib.ew_inplace_exec_create(
+            ch.handle, N.i64_array(rp.layer_bytes), len(rp.layer_bytes),
+            N.int_array(rp.old_ranks), len(rp.old_ranks), N.int_array(rp.new_ranks),
+            len(rp.new_ranks), C.c_void_p(buf.data_ptr() if buf is not None else None),
+            C.c_void_p(bufs.replica.data_ptr() if bufs.replica is not None else None),
+            int(self.stage_bytes), int(self.phase_bytes), int(self.slack),
+            int(self.gather_streams), int(self.flush_ctas), int(self.block_bytes),
+            float(self.barrier_timeout_s), C.byref(h)))
+        self._h = h
+        self._channel = ch  # the executor keeps a reference to it
+        n, alloc = C.c_int64(), C.c_int64()
+        check(lib.ew_inplace_exec_info(h, C.byref(n), C.byref(alloc)))
+        if n.value != len(self.sched.phases):
+            raise RuntimeError("C++ and Python in-place schedules disagree")
 
-    def launch(self, block_sums: torch.Tensor, stream=None, n_ctas: int = 0,
-               flush_ctas: int = 64, gather_streams: int = 2) -> None:
-        """Enqueue the whole reshard: gathers alternate over `gather_streams`
-        streams (`stream` first) so one phase's tail overlaps the next
-        phase's start, barriers and flushes run on their own streams, and
-        everything is joined back into `stream`.  The caller zeroes
-        block_sums and all-reduces them afterwards."""
-        if self.rank not in self.rp.new_ranks:
-            return
-        sc = self.sched
-        main = stream or torch.cuda.current_stream()
-        while len(self.gather_streams) < gather_streams - 1:
-            self.gather_streams.append(torch.cuda.Stream())
-        gs = [main] + self.gather_streams[:max(0, gather_streams - 1)]
-        ys, fs = self.sync_stream, self.flush_stream
-        for st in gs[1:] + [ys, fs]:
-            st.wait_stream(main)
-        bar: List[torch.cuda.Event] = []
-        flushed: List[Optional[torch.cuda.Event]] = []
-        # every gather and flush is gated on the barrier's error flag: after
-        # a timed-out barrier (a peer that has not read its bytes) nothing
-        # more is written, so no OLD byte a lagging peer still needs is lost
-        veto = self.barrier.error_flag
-        for j in range(len(sc.phases)):
-            g_s = gs[j % len(gs)]
-            k = j - sc.slack - 1
-            if k >= 0:
-                g_s.wait_event(bar[k])              # every rank finished gather_k
-            if j >= sc.ring and flushed[j - sc.ring] is not None:
-                g_s.wait_event(flushed[j - sc.ring])  # staging buffer free again
-            if self.staged[j] is not None:
-                self.staged[j].launch(n_ctas, 0, stream=g_s, block_sums=block_sums,
-                                      abort_flag=veto)
-            if self.direct[j] is not None:
-                self.direct[j].launch(n_ctas, 0, stream=g_s, block_sums=block_sums,
-                                      abort_flag=veto)
-            g = torch.cuda.Event()
-            g.record(g_s)
-            ys.wait_event(g)
-            self.barrier.wait(stream=ys)             # every rank has read R_j
-            b = torch.cuda.Event()
-            b.record(ys)
-            bar.append(b)
-            if self.flushes[j] is not None:
-                fs.wait_event(b)
-                self.flushes[j].launch(flush_ctas, 0, stream=fs, abort_flag=veto)
-                f = torch.cuda.Event()
-                f.record(fs)
-                flushed.append(f)
-            else:
-                flushed.append(None)
-        for st in gs[1:] + [ys, fs]:
-            main.wait_stream(st)
+    def launch(self, block_sums: Optional[torch.Tensor], stream=None) -> None:
+        """Enqueue the whole reshard on `stream` (gathers alternate over the
+        executor's gather streams, barriers and flushes on their own, all
+        joined back).  The caller zeroes block_sums and all-reduces them."""
+        if self._h is None:
+            raise RuntimeError("launch before bind")
+        check(lib.ew_inplace_exec_launch(self._h, dev._ptr(block_sums), dev._stream(stream)))
+
+    def timed_out(self) -> bool:
+        t = C.c_int()
+        if self._h is not None:
+            check(lib.ew_inplace_exec_timed_out(self._h, C.byref(t)))
+        return bool(t.value)
 
     def check(self) -> None:
         """Raise if a phase barrier timed out (call after the launch's stream
         completed).  The gated copies then stopped writing at that phase:
         NEW is incomplete, but every OLD byte not yet read is intact."""
-        if self.barrier is not None and self.barrier.timed_out():
+        if self.timed_out():
             raise RuntimeError("in-place reshard aborted: a phase barrier timed out (a peer "
                                "did not arrive); later gathers and flushes were vetoed")
 
     def close(self) -> None:
-        self.direct, self.staged, self.flushes = [], [], []
-        if self.barrier is not None:
-            self.barrier.close()
-            self.barrier = None
-        if self._base is not None:
-            self._base.close()
-            self._base = None
-        self.staging = []
+        if self._h is not None and self._h.value and lib is not None:
+            lib.ew_inplace_exec_free(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 def emulate_inplace_on_one_gpu(rp: ReshardPlan, seed: int, stage_bytes: int, phase_bytes: int,

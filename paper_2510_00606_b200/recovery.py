@@ -1,68 +1,105 @@
 """Measured DP recovery on B200: the data-parallel slice of the reference's
 Simulation::recover_elaswave (sim.cpp:597-722), executed instead of modelled.
 
+The recovery runs in C++ (include/elaskit/recovery.hpp, elaskit::b200 over
+the C ABI); this module is its Python binding plus the ring-replica helpers.
 Per step the group keeps a same-GPU snapshot of every rank's ZeRO shard with
-checksum rows (kernel (a)).  On a membership change (FailStop / ScaleIn /
-ScaleOut) each surviving rank runs, in the reference's order:
+checksum rows (kernel (a)) and a ring replica on the holder.  On a membership
+change (FailStop / ScaleIn) each surviving rank runs, in the reference's
+order:
 
   comm repair   plan_edit on the DP mesh (communicator.cpp:54-105), then the
-                edit applied: ncclCommShrink of the DP communicator
+                NCCL communicator: a shrunk communicator prepared in steady
+                state for every possible departure (ncclCommSplit,
+                splitShare; repair = lookup + first collective) or, without
+                one, ncclCommShrink at failure time
   dataflow      reshard_microbatches (dataflow.cpp:52-69) -> new weights
   remap         integrity_check + overlap_matrix on the interleaved layouts,
-                lowering to this GPU's copy program, CUDA-IPC peer mapping,
-                one copy launch (kernel (b)) that checksums every byte it
-                lands, verification by checksum conservation against the
-                snapshot rows (no re-read of source or target)
+                lowered to this GPU's copy program (prepared in steady state
+                or planned now), one copy launch (kernel (b)) that checksums
+                every byte it lands, a device barrier, and checksum
+                conservation reduce-scattered over peer memory
 
 and reports an MttrEvent with the reference's fields (sim.hpp:31-45) filled
-with measured seconds (`mttr_csv` row format of sim.cpp:1119-1132).
+with measured seconds, rendered as the reference's mttr.csv rows
+(sim.cpp:1119-1132) by the C++ library.
 """
 from __future__ import annotations
 
-import time
+import ctypes as C
 from dataclasses import dataclass, field
-from typing import Dict, List, Optional, Sequence
+from typing import Dict, Optional, Sequence
 
 import torch
 import torch.distributed as dist
 
+from . import _native as N
 from . import device as dev
-from .fabric import FAIL_STOP, SCALE_IN, SCALE_OUT, CommGroup, plan_edit, reshard_microbatches
-from .reshard import ReshardExecutor, ReshardPlan, shard_map
+from ._native import check, lib
+from .fabric import FAIL_STOP, SCALE_IN, SCALE_OUT
+from .rendezvous import Channel
+from .reshard import ReshardPlan, shard_map
 
 KIND_NAMES = {FAIL_STOP: "fail_stop", SCALE_IN: "scale_in", SCALE_OUT: "scale_out"}
+
+_PHASES = ("plan_edit_s", "comm_acquire_s", "first_collective_s", "comm_prepared", "plan_s",
+           "map_bind_s", "copy_s", "barrier_verify_s", "verdict_exchange_s",
+           "launch_to_verdict_s", "mismatched_block_words", "barrier_timeouts")
 
 
 @dataclass
 class MttrEvent:
-    """Reference MttrEvent (sim.hpp:31-45) with measured phases."""
+    """Reference MttrEvent (sim.hpp:31-45) with measured phases (a view of
+    the C++ record, ew_mttr_event)."""
 
     step: int = 0
     t_event_s: float = 0.0
     kind: str = "fail_stop"
     detect_s: float = 0.0          # detection is outside this library (agent)
-    comm_repair_s: float = 0.0     # plan_edit + ncclCommShrink
-    remap_s: float = 0.0           # plan + peer map + copy + verify
+    comm_repair_s: float = 0.0     # plan_edit + communicator repair + first collective
+    remap_s: float = 0.0           # copy + verification (+ planning when not prepared)
     migration_stall_s: float = 0.0  # no layer migration on the DP path
     other_s: float = 0.0           # micro-batch reshape + bookkeeping
     lost_work_s: float = 0.0
     phases: Dict[str, float] = field(default_factory=dict)
     verified: bool = False
 
+    @classmethod
+    def from_c(cls, c: "N.MttrEventC") -> "MttrEvent":
+        ev = cls(step=c.step, t_event_s=c.t_event_s, kind=c.kind.decode(),
+                 detect_s=c.detect_s, comm_repair_s=c.comm_repair_s, remap_s=c.remap_s,
+                 migration_stall_s=c.migration_stall_s, other_s=c.other_s,
+                 lost_work_s=c.lost_work_s, verified=bool(c.verified))
+        ev.phases = {k: getattr(c, k) for k in _PHASES if getattr(c, k) >= 0}
+        return ev
+
+    def to_c(self) -> "N.MttrEventC":
+        c = N.MttrEventC()
+        c.step, c.verified, c.t_event_s = self.step, int(self.verified), self.t_event_s
+        c.kind = self.kind.encode()[:15]
+        for k in ("detect_s", "comm_repair_s", "remap_s", "migration_stall_s", "other_s",
+                  "lost_work_s"):
+            setattr(c, k, getattr(self, k))
+        return c
+
     def total_s(self) -> float:
         return (self.detect_s + self.comm_repair_s + self.remap_s + self.migration_stall_s +
                 self.other_s)
 
     def csv_row(self, index: int) -> str:
-        """One line of the reference's mttr.csv (sim.cpp:1119-1132)."""
-        f = lambda x: f"{x:.9g}"
-        return ",".join([str(index), str(self.step), f(self.t_event_s), self.kind, f(self.detect_s),
-                         f(self.comm_repair_s), f(self.remap_s), f(self.migration_stall_s),
-                         f(self.other_s), f(self.lost_work_s), f(self.total_s())])
+        """One line of the reference's mttr.csv (sim.cpp:1119-1132), from C++."""
+        buf = C.create_string_buffer(512)
+        check(lib.ew_mttr_csv_row(C.byref(self.to_c()), int(index), buf, 512))
+        return buf.value.decode()
 
 
-MTTR_CSV_HEADER = ("event,step,t_event_s,kind,detect_s,comm_repair_s,remap_s,migration_stall_s,"
-                   "other_s,lost_work_s,total_s")
+def _csv_header() -> str:
+    buf = C.create_string_buffer(256)
+    check(lib.ew_mttr_csv_header(buf, 256))
+    return buf.value.decode()
+
+
+MTTR_CSV_HEADER = _csv_header()
 
 
 class RingReplica:
@@ -192,25 +229,28 @@ class ReplayReplica:
 
 
 class PreparedRecovery:
-    """Every single-rank departure of a DP group, planned, lowered and bound
-    in steady state, so a failure runs only the copy.
+    """Every single departure of a DP group, planned, lowered and bound in
+    steady state, so a failure runs only the copy and its verification —
+    a binding of the C++ elaskit::b200::PreparedRecovery (ew_prepared).
 
     The reference plans at failure time (Simulation::recover_elaswave,
     sim.cpp:597-722; overlap_matrix per event).  On B200 the inputs of a
     single departure are all known before it happens: the layouts, every
     peer's live shard and the ring replicas (RingReplica / ReplayReplica keep
     them current), so each rank builds, once, the verified pull program for
-    each possible departed peer d — plan (overlap_matrix + integrity_check),
-    lowering, IPC mappings and the device-resident copy program — against
-    one NEW buffer sized for the largest case.  recover(d) is a table lookup
-    and one launch.  Memory: one NEW shard plus a few KiB of copy items per
-    scenario."""
+    each possible departed peer d against one NEW buffer sized for the
+    largest case, and maps every peer's verification arrays.  recover(d) is
+    a table lookup, one copy launch, a device barrier and a conservation
+    check over peer memory."""
 
     def __init__(self, layer_bytes: Sequence[int], members: Sequence[int], rank: int,
                  old: torch.Tensor, replica: torch.Tensor,
-                 block_bytes: int = dev.DEFAULT_BLOCK_BYTES, group=None):
+                 block_bytes: int = dev.DEFAULT_BLOCK_BYTES, group=None,
+                 old_rows: Optional[torch.Tensor] = None,
+                 replica_rows: Optional[torch.Tensor] = None, barrier_timeout_s: float = 30.0):
         """`old`: this rank's live shard; `replica`: the shard of its ring
-        successor (SnapshotRing.backs_up(rank)).  Collective over `group`."""
+        successor (SnapshotRing.backs_up(rank)); `*_rows`: their per-step
+        snapshot checksum rows (None: recomputed).  Collective over `group`."""
         members = sorted(members)
         self.rank = rank
         self.block_bytes = block_bytes
@@ -218,178 +258,128 @@ class PreparedRecovery:
                       for d in members}
         n_new = max(p.dst.shard_bytes(rank) for d, p in self.plans.items() if d != rank)
         self.new = dev.empty_bytes(n_new)
-        # one steady-state exchange maps every peer's OLD and REPLICA buffer
-        from .reshard import RankBuffers
-        self._base = ReshardExecutor(self.plans[members[0]], rank)
-        self._base.premap(RankBuffers(old, replica, None), group)
-        self.execs: Dict[int, Optional[ReshardExecutor]] = {}
-        for d, rp in self.plans.items():
-            if d == rank:
-                self.execs[d] = None  # nothing to build for one's own departure
-                continue
-            ex = ReshardExecutor(rp, rank)
-            ex._table = dict(self._base._table)
-            ex._premapped = True      # pull + premapped: bind() does no exchange
-            rep = replica if rp.replica_of(rank) == d else None
-            ex.bind(RankBuffers(old, rep, self.new), group, verify=True,
-                    block_bytes=block_bytes)
-            self.execs[d] = ex
+        self.channel = Channel.from_group(group, "prepared")
+        if self.channel.members != members:
+            raise ValueError("the group's ranks must be the DP members")
+        lb = list(layer_bytes)
+        h = C.c_void_p()
+        check(lib.ew_prepared_create(
+            self.channel.handle, N.i64_array(lb), len(lb), C.c_void_p(old.data_ptr()),
+            dev._ptr(old_rows), C.c_void_p(replica.data_ptr()), dev._ptr(replica_rows),
+            C.c_void_p(self.new.data_ptr()), int(self.new.numel()), int(block_bytes),
+            float(barrier_timeout_s), C.byref(h)))
+        self._h = h
+        self._keep = (old, replica, old_rows, replica_rows)
 
-    def recover(self, departed: int, block_sums: torch.Tensor, stream=None) -> ReshardPlan:
-        """Launch the prepared program for `departed` (block_sums zeroed by
-        the caller); returns its plan.  The caller all-reduces block_sums
-        and compares them with the snapshot's block sums."""
-        ex = self.execs[departed]
-        if ex is None:
-            raise ValueError("the departed rank does not recover itself")
-        ex.launch(stream=stream, block_sums=block_sums)
-        return self.plans[departed]
+    def recover(self, departed: int, stream=None) -> MttrEvent:
+        """Survivors (all of them) run the prepared move for `departed`;
+        returns the event with `verified` (checksum conservation) and the
+        measured copy / barrier+verify / verdict phases."""
+        ev = N.MttrEventC()
+        ok = C.c_int()
+        check(lib.ew_prepared_recover(self._h, int(departed), dev._stream(stream), C.byref(ev),
+                                      C.byref(ok)))
+        return MttrEvent.from_c(ev)
 
     def new_view(self, departed: int) -> torch.Tensor:
         return self.new[:self.plans[departed].dst.shard_bytes(self.rank)]
 
     def close(self) -> None:
-        for ex in self.execs.values():
-            if ex is not None:
-                ex.program = None
-        self.execs = {}
-        self._base.close()
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
+            lib.ew_prepared_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 class DpGroup:
-    """One rank's view of an interleaved-ZeRO DP group (one process per GPU)."""
+    """One rank's view of an interleaved-ZeRO DP group (one process per GPU,
+    or several sharing one GPU): a binding of the C++ elaskit::b200::DpGroup
+    (ew_dp_group).  It owns the NCCL communicator of the (d) reduce and, in
+    steady state, one shrunk communicator per possible single departure."""
 
     def __init__(self, layer_bytes: Sequence[int], members: Sequence[int], rank: int,
                  comm: Optional[dev.Communicator], per_slot_mbs: int = 4,
-                 num_microbatches: int = 32, block_bytes: int = dev.DEFAULT_BLOCK_BYTES):
+                 num_microbatches: int = 32, block_bytes: int = dev.DEFAULT_BLOCK_BYTES,
+                 prepare_comms: bool = True, group=None):
+        """`comm` (over `members` in ascending order) is taken over: the
+        group destroys it.  Collective over `group` (all members)."""
         self.layer_bytes = list(layer_bytes)
-        self.members = sorted(members)
         self.rank = rank
-        self.comm = comm
-        self.block_bytes = block_bytes
-        self.mb_sizes = [per_slot_mbs] * len(self.members)
-        self.num_microbatches = num_microbatches
-        self.links = {(a, b) for i, a in enumerate(self.members) for b in self.members[i + 1:]}
+        self.channel = Channel.from_group(group, "dp")
+        if self.channel.members != sorted(members):
+            raise ValueError("the group's ranks must be the DP members")
+        raw = None
+        if comm is not None:
+            raw, comm._h = comm._h, None  # ownership moves to the C++ group
+        h = C.c_void_p()
+        check(lib.ew_dp_group_create(self.channel.handle, N.i64_array(self.layer_bytes),
+                                     len(self.layer_bytes), raw, int(per_slot_mbs),
+                                     int(num_microbatches), int(block_bytes),
+                                     int(bool(prepare_comms)), C.byref(h)))
+        self._h = h
+        self._prepared: Optional[PreparedRecovery] = None
 
-    def recover(self, departed: Sequence[int], bufs, push: bool = False, step: int = 0,
-                kind: int = FAIL_STOP, group=None, source_sums=None) -> MttrEvent:
+    def attach(self, prepared: Optional[PreparedRecovery]) -> None:
+        self._prepared = prepared
+        check(lib.ew_dp_group_attach(self._h, prepared._h if prepared is not None else None))
+
+    def prepare(self) -> None:
+        """Steady state after a change: rebuild the per-departure communicators."""
+        check(lib.ew_dp_group_prepare(self._h))
+
+    def recover(self, departed: Sequence[int], bufs=None, step: int = 0,
+                kind: int = FAIL_STOP, stream=None) -> MttrEvent:
         """Run the DP recovery for `departed` on this (surviving) rank.
-        `bufs` are this rank's RankBuffers for the change (old/replica filled);
-        `source_sums`: global block sums of the state before the change
-        (from the per-step snapshot rows), else recomputed from OLD/replica."""
-        if kind == SCALE_OUT:
-            raise NotImplementedError("DpGroup.recover handles departures (FailStop/ScaleIn); "
-                                      "a rejoin grows the communicator, not shrinks it")
-        unknown = sorted(set(departed) - set(self.members))
-        if unknown:
-            raise ValueError(f"departed ranks {unknown} are not members of the group")
-        ev = MttrEvent(step=step, kind=KIND_NAMES.get(kind, "fail_stop"))
-        t0 = time.perf_counter()
-        # comm repair: edit plan, then the NCCL communicator shrink.  NCCL
-        # excludes by rank in the CURRENT communicator, which numbers the
-        # members 0..n-1 in ascending id order (it was built, or last shrunk,
-        # over self.members), not by member id
-        edit = plan_edit([CommGroup("dp", self.members)], kind, list(departed), self.links)
-        for l in edit.links_to_remove:
-            self.links.discard(l)
-        self.links |= edit.links_to_add
-        comm_rank = {m: i for i, m in enumerate(self.members)}
-        new_comm = None
-        if self.comm is not None:
-            new_comm = self.comm.shrink(sorted(comm_rank[d] for d in departed))
-            self.comm.destroy()  # the child exists: the parent is no longer used
-        torch.cuda.synchronize()
-        t1 = time.perf_counter()
-        ev.comm_repair_s = t1 - t0
-        ev.phases["plan_edit_links_removed"] = len(edit.links_to_remove)
+        `bufs` (reshard.RankBuffers: old / replica / new) are used when no
+        prepared recovery is attached (planning at failure time)."""
+        p = lambda t: C.c_void_p(t.data_ptr() if t is not None else None)  # noqa: E731
+        ev = N.MttrEventC()
+        d = list(departed)
+        check(lib.ew_dp_group_recover(
+            self._h, N.int_array(d), len(d), int(kind),
+            p(bufs.old if bufs is not None else None),
+            p(bufs.replica if bufs is not None else None),
+            p(bufs.new if bufs is not None else None), int(step), dev._stream(stream),
+            C.byref(ev)))
+        return MttrEvent.from_c(ev)
 
-        # dataflow: global batch conserved over the survivors
-        survivors = [m for m in self.members if m not in set(departed)]
-        old_idx = {m: i for i, m in enumerate(self.members)}
-        _, sizes = reshard_microbatches(self.mb_sizes, self.num_microbatches,
-                                        [old_idx[m] for m in survivors])
-        t2 = time.perf_counter()
-        ev.other_s = t2 - t1
+    @property
+    def comm(self) -> Optional[dev.Communicator]:
+        """The group's current NCCL communicator (borrowed: the group owns it)."""
+        h = C.c_void_p()
+        check(lib.ew_dp_group_comm(self._h, C.byref(h)))
+        if not h.value:
+            return None
+        c = dev.Communicator(h)
+        c._borrowed = True
+        return c
 
-        # remap: plan -> program -> peer map -> copy -> verify.  In pull mode
-        # the copy verifies on arrival (it checksums what it lands), so the
-        # check is one all-reduce of block sums against the source's sums
-        # (the per-step snapshot rows; recomputed here when not supplied).
-        rp = ReshardPlan.build(self.layer_bytes, self.members, survivors)
-        ex = ReshardExecutor(rp, self.rank, push=push)
-        before = source_sums if source_sums is not None else \
-            self.source_block_sums(rp, bufs, group)
-        t3 = time.perf_counter()
-        ex.bind(bufs, group=group, verify=not push, block_bytes=self.block_bytes)
-        t4 = time.perf_counter()
-        after = torch.zeros_like(before)
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        dist.barrier(group=group)
-        s.record()
-        ex.launch(block_sums=after)
-        e.record()
-        torch.cuda.synchronize()
-        dist.barrier(group=group)
-        t5 = time.perf_counter()
-        if push:
-            ev.verified = self.verify_conservation(rp, bufs, group)
-        else:
-            dist.all_reduce(after, group=group)
-            ev.verified = bool(torch.equal(before, after))
-        t6 = time.perf_counter()
-        ev.remap_s = t6 - t2
-        ev.phases.update(plan_s=t3 - t2, peer_map_s=t4 - t3, copy_s=s.elapsed_time(e) / 1e3,
-                         copy_wall_s=t5 - t4, verify_s=t6 - t5)
-        ex.close()
-        # commit the new membership
-        self.members = survivors
-        self.mb_sizes = sizes
-        self.comm = new_comm
-        return ev
+    @property
+    def members(self):
+        out = N.int_array([0] * 1024)
+        n = C.c_int()
+        check(lib.ew_dp_group_members(self._h, out, 1024, C.byref(n)))
+        return list(out[:n.value])
 
-    def source_block_sums(self, rp: ReshardPlan, bufs, group=None) -> torch.Tensor:
-        """Global block sums of the state before the change: every live
-        rank's OLD shard plus the departed ranks' bytes as their ring holders
-        keep them (what the per-step snapshot rows already hold)."""
-        block = self.block_bytes
-        nblocks = (sum(self.layer_bytes) + block - 1) // block
-        before = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
-        if bufs.old is not None and self.rank in rp.old_ranks and self.rank not in rp.failed:
-            m = shard_map(rp.src, self.rank, block)
-            rows = m.new_row_sums()
-            dev.checksum(m, bufs.old, rows)
-            dev.rows_to_blocks(m, rows, before)
-        if bufs.replica is not None:
-            owner = rp.replica_of(self.rank)
-            m = shard_map(rp.src, owner, block)
-            rows = m.new_row_sums()
-            dev.checksum(m, bufs.replica, rows)
-            dev.rows_to_blocks(m, rows, before)
-        dist.all_reduce(before, group=group)
-        return before
+    @property
+    def mb_sizes(self):
+        out = N.int_array([0] * 1024)
+        n = C.c_int()
+        check(lib.ew_dp_group_microbatches(self._h, out, 1024, C.byref(n)))
+        return list(out[:n.value])
 
-    def verify_conservation(self, rp: ReshardPlan, bufs, group=None) -> bool:
-        """Block sums of all NEW shards (re-read) == block sums of all OLD shards."""
-        block = self.block_bytes
-        nblocks = (sum(self.layer_bytes) + block - 1) // block
-        before = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
-        after = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
-        if bufs.old is not None and self.rank in rp.old_ranks and self.rank not in rp.failed:
-            m = shard_map(rp.src, self.rank, block)
-            rows = m.new_row_sums()
-            dev.checksum(m, bufs.old, rows)
-            dev.rows_to_blocks(m, rows, before)
-        if bufs.replica is not None:  # the dead rank's bytes as its ring holder keeps them
-            owner = rp.replica_of(self.rank)
-            m = shard_map(rp.src, owner, block)
-            rows = m.new_row_sums()
-            dev.checksum(m, bufs.replica, rows)
-            dev.rows_to_blocks(m, rows, before)
-        if bufs.new is not None:
-            m = shard_map(rp.dst, self.rank, block)
-            rows = m.new_row_sums()
-            dev.checksum(m, bufs.new, rows)
-            dev.rows_to_blocks(m, rows, after)
-        dist.all_reduce(before, group=group)
-        dist.all_reduce(after, group=group)
-        return bool(torch.equal(before, after))
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
+            lib.ew_dp_group_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

@@ -2,8 +2,9 @@
 
 One process per GPU.  Every rank runs the same host planning (integrity
 check -> overlap_matrix -> lowering to its copy program, all C++), peers
-exchange CUDA IPC handles of their shard buffers over torch.distributed
-(plumbing only), and each GPU then executes its program in ONE kernel launch:
+exchange CUDA IPC handles of their shard buffers through the recovery
+runtime's rendezvous (C++ Channel over torch.distributed's store; plumbing
+only), and each GPU then executes its program in ONE kernel launch:
 remote copies are 128-bit stores into peer HBM over NVLink/NVSwitch, local
 copies (retained bytes, ring-holder self lanes) stream through local HBM.
 No NCCL on this path — the exchange is the plan.
@@ -18,10 +19,14 @@ import time
 from dataclasses import dataclass, field
 from typing import Dict, List, Optional, Sequence, Tuple
 
+import ctypes as C
+
 import numpy as np
 import torch
 
+from . import _native as N
 from . import device as dev
+from ._native import check, lib
 from .fabric import (ROLE_NEW, ROLE_OLD, ROLE_REPLICA, PartitionLayout, SnapshotRing,
                      TransferPlan, integrity_check, interleaved_layout, overlap_matrix,
                      reshard_copies)
@@ -170,8 +175,49 @@ def shard_map(layout: PartitionLayout, rank: int, block_bytes: int = dev.DEFAULT
     return dev.ShardMap(layout.segments(rank), block_bytes)
 
 
+class PeerTable:
+    """ew_peers: (role/key, member) -> device pointer, peers IPC-mapped by a
+    collective exchange over a Channel (recovery.hpp PeerBuffers)."""
+
+    def __init__(self):
+        h = C.c_void_p()
+        check(lib.ew_peers_create(C.byref(h)))
+        self._h = h
+
+    @property
+    def handle(self) -> C.c_void_p:
+        return self._h
+
+    def exchange(self, channel, mine: Dict[int, Optional[int]]) -> None:
+        items = [(k, p) for k, p in mine.items() if p]
+        keys = N.int_array([k for k, _ in items])
+        ptrs = (C.c_void_p * max(1, len(items)))(*[p for _, p in items])
+        check(lib.ew_peers_exchange(self._h, channel.handle, keys, ptrs, len(items)))
+
+    def put(self, key: int, member: int, ptr: int) -> None:
+        check(lib.ew_peers_put(self._h, int(key), int(member), C.c_void_p(ptr)))
+
+    def get(self, key: int, member: int) -> Optional[int]:
+        p = C.c_void_p()
+        check(lib.ew_peers_get(self._h, int(key), int(member), C.byref(p)))
+        return p.value
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
+            lib.ew_peers_free(self._h)  # closes the IPC mappings
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 class ReshardExecutor:
-    """Multi-process executor: one instance per rank/GPU."""
+    """One rank's reshard executor: the C++ elaskit::b200::ReshardExecutor
+    (ew_reshard) over a peer table exchanged through the recovery runtime's
+    rendezvous (Channel over the torch.distributed group's store)."""
 
     def __init__(self, rp: ReshardPlan, rank: int, push: bool = False):
         # pull is the default: each receiver's TMA ring keeps ~100 KB of peer
@@ -180,8 +226,9 @@ class ReshardExecutor:
         self.rp = rp
         self.rank = rank
         self.push = push
-        self.program: Optional[dev.CopyProgram] = None
-        self._opened: List[int] = []
+        self.program: Optional[C.c_void_p] = None  # the bound ew_reshard
+        self.peers = PeerTable()
+        self._premapped = False
 
     def allocate(self, in_place: bool = False, device_replica: bool = True) -> RankBuffers:
         """Buffers of this rank.  in_place=True aliases NEW and OLD inside one
@@ -215,84 +262,81 @@ class ReshardExecutor:
         new = dev.empty_bytes(n_new) if r in rp.new_ranks else None
         return RankBuffers(old, replica, new)
 
+    @staticmethod
+    def _ptr(t: Optional[torch.Tensor]) -> Optional[int]:
+        return t.data_ptr() if t is not None else None
+
     def premap(self, bufs: RankBuffers, group=None) -> None:
         """Steady-state peer mapping (before any failure): import every peer's
         OLD and REPLICA buffers.  A pull-mode reshard reads only those, so a
         recovery that premapped pays no cudaIpcOpenMemHandle on its critical
-        path (bind() then only builds the program)."""
-        self._exchange(bufs, group, roles=(ROLE_OLD, ROLE_REPLICA), needed=None)
+        path (bind() then only builds the program).  Collective over group."""
+        from .rendezvous import Channel
+        ch = Channel.from_group(group, "premap")
+        self.peers.exchange(ch, {ROLE_OLD: self._ptr(bufs.old),
+                                 ROLE_REPLICA: self._ptr(bufs.replica)})
         self._premapped = True
+
+    def put_peer(self, role: int, member: int, ptr: int) -> None:
+        """Enter a buffer by hand (e.g. a departed rank's host image as the
+        holder's REPLICA, hostsnap.HostSnapshots.attach)."""
+        self.peers.put(role, member, ptr)
 
     def bind(self, bufs: RankBuffers, group=None, verify: bool = False,
              block_bytes: int = dev.DEFAULT_BLOCK_BYTES) -> None:
-        """Map the peer buffers this GPU's copies touch (unless premapped) and
-        build its program.  Collective over `group`: every rank calls it, and
-        the exchange is skipped only when every rank premapped for a pull
-        (the same decision everywhere, so no rank waits on a missing peer).
-        verify=True (pull mode): the program checksums every byte it lands
-        in NEW (verification on arrival, launch(block_sums=...))."""
+        """Map the peer buffers (unless premapped for a pull) and build this
+        GPU's program.  Collective over `group`: every rank calls it, and the
+        exchange is skipped only when every rank premapped for a pull (the
+        same decision everywhere).  verify=True (pull mode): the program
+        checksums every byte it lands in NEW (verification on arrival,
+        launch(block_sums=...))."""
         if verify and self.push:
             raise ValueError("verification on arrival needs pull mode (every byte landing "
                              "in NEW is then issued by its own GPU)")
-        descs = self.rp.copies(self.rank, self.push)
-        needed = set()
-        for c in descs:
-            for role, rank in ((int(c["src_role"]), int(c["src_rank"])),
-                               (int(c["dst_role"]), int(c["dst_rank"]))):
-                if rank != self.rank:
-                    needed.add((role, rank))
-        if not (getattr(self, "_premapped", False) and not self.push):
-            self._exchange(bufs, group, roles=(ROLE_OLD, ROLE_REPLICA, ROLE_NEW), needed=needed)
-        table = getattr(self, "_table", {})
-        missing = needed - set(table)
-        if missing:
-            raise RuntimeError(f"peer buffers {sorted(missing)} are not mapped")
+        if not (self._premapped and not self.push):
+            from .rendezvous import Channel
+            ch = Channel.from_group(group, "bind")
+            self.peers.exchange(ch, {ROLE_OLD: self._ptr(bufs.old),
+                                     ROLE_REPLICA: self._ptr(bufs.replica),
+                                     ROLE_NEW: self._ptr(bufs.new)})
         for role, t in ((ROLE_OLD, bufs.old), (ROLE_REPLICA, bufs.replica), (ROLE_NEW, bufs.new)):
             if t is not None:
-                table[(role, self.rank)] = t.data_ptr()
-        import torch.distributed as dist
-        world = dist.get_world_size(group)
-        n_table = max(max(self.rp.old_ranks + self.rp.new_ranks) + 1, world)
-        vmap = shard_map(self.rp.dst, self.rank, block_bytes) \
-            if verify and bufs.new is not None else None
-        self.program = dev.CopyProgram.from_descs(descs, table, n_table, self.rank, vmap)
-
-    def _exchange(self, bufs: RankBuffers, group, roles, needed) -> None:
-        import torch.distributed as dist
-
-        mine = {}
-        for role, t in ((ROLE_OLD, bufs.old), (ROLE_REPLICA, bufs.replica), (ROLE_NEW, bufs.new)):
-            if t is not None and role in roles:
-                mine[role] = dev.ipc_handle(t)
-        world = dist.get_world_size(group)
-        gathered: List[Dict[int, Tuple[bytes, int]]] = [None] * world  # type: ignore
-        dist.all_gather_object(gathered, (self.rank, mine), group=group)
-        table: Dict[Tuple[int, int], int] = getattr(self, "_table", {})
-        for peer_rank, handles in gathered:
-            if peer_rank == self.rank:
-                continue
-            for role, (h, off) in handles.items():
-                if (role, peer_rank) in table or (needed is not None and (role, peer_rank) not in needed):
-                    continue
-                p = dev.ipc_open(h, off)
-                self._opened.append(p)
-                table[(role, peer_rank)] = p
-        self._table = table
+                self.peers.put(role, self.rank, t.data_ptr())
+        self._free_program()
+        rp = self.rp
+        ring = rp.ring.members if rp.ring is not None else []
+        h = C.c_void_p()
+        check(lib.ew_reshard_create(rp.src.handle, rp.dst.handle, N.int_array(rp.failed),
+                                    len(rp.failed), N.int_array(ring), len(ring), self.rank,
+                                    int(self.push), int(block_bytes), C.byref(h)))
+        self.program = h
+        self._verified = bool(verify) and bufs.new is not None
+        check(lib.ew_reshard_bind(h, self.peers.handle, int(bool(verify))))
 
     def launch(self, n_ctas: int = 0, remote_ctas: int = 0, stream=None,
-               block_sums=None) -> None:
+               block_sums=None, abort_flag: Optional[int] = None) -> None:
         if self.program is not None:
-            self.program.launch(n_ctas, remote_ctas, stream,
-                                block_sums if getattr(self.program, "_verify_map", None)
-                                is not None else None)
+            check(lib.ew_reshard_launch(self.program,
+                                        dev._ptr(block_sums) if self._verified else None,
+                                        C.c_void_p(abort_flag) if abort_flag else None,
+                                        int(n_ctas), int(remote_ctas), dev._stream(stream)))
+
+    def _free_program(self) -> None:
+        if self.program is not None and self.program.value and lib is not None:
+            lib.ew_reshard_free(self.program)
+        self.program = None
 
     def close(self) -> None:
-        self.program = None
-        for p in self._opened:
-            dev.ipc_close(p)
-        self._opened = []
-        self._table = {}
+        self._free_program()
+        self.peers.close()
+        self.peers = PeerTable()
         self._premapped = False
+
+    def __del__(self):
+        try:
+            self._free_program()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 def _aliases(a, b) -> bool:

@@ -1,0 +1,323 @@
+"""The multi-rank recovery path on ONE GPU: N = 4 and N = 8 processes share
+cuda:0, meet on gloo (plumbing: the c10d store behind the C++ rendezvous) and
+map each other's buffers with CUDA IPC, which works between processes on the
+same device.  No NCCL (it refuses duplicate GPUs).  Everything the
+one-process-per-GPU deployment runs across processes runs here, through the
+C++ runtime (include/elaskit/recovery.hpp):
+
+  * PreparedRecovery: every departure position of N -> N-1, pull programs
+    verified on arrival, device barrier, checksum conservation reduce-
+    scattered over peer memory; landed bytes == the target layout's bytes;
+  * DpGroup: the same departure planned at failure time (survivor channel,
+    IPC mapping, copy, verification) with the MttrEvent / mttr.csv record;
+  * InPlaceExecutor (config D): OLD and NEW in one buffer, phases behind
+    device barriers, departures and a rejoin, the barrier never timing out;
+  * fp32 and int64 peer folds over peer memory with device barriers,
+    bit-identical to the single-process fold;
+  * ReplayReplica: the holder replays the owner's AdamW step from the
+    owner's gradient read through an IPC pointer, byte-identical;
+  * host-memory images (hostsnap, double-buffered) as the departed rank's
+    H2D_D2D source.
+
+Bandwidth numbers need one process per GPU (test_gpu_multigpu.py, bench.py);
+this file proves the cross-process control and data paths on any 1-GPU box.
+Reference: overlap_matrix / integrity_check (param_fabric.cpp:82-121),
+remap_time (sim.cpp:452-483), recover_elaswave (sim.cpp:597-722)."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _fill_expected(dev, shard_map, layout, rank, seed, n):
+    e = dev.empty_bytes(n)
+    dev.fill_synthetic(shard_map(layout, rank), e, seed)
+    return e
+
+
+def _worker(rank, world, port, out_dir, scale):
+    import json
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch.distributed as dist
+    from paper_2510_00606_b200 import configs, device as dev
+    from paper_2510_00606_b200.reshard import RankBuffers, ReshardExecutor, ReshardPlan, shard_map
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rep = {}
+    try:
+        cfg = configs.scaled(configs.llama2_7b_per_tensor(), scale)
+        members = list(range(world))
+        lay = ReshardPlan.build(cfg.layer_bytes, members, members).src
+        block = 65536
+
+        # ---- PreparedRecovery: every departure position, C++ end to end
+        from paper_2510_00606_b200.recovery import PreparedRecovery
+        live = dev.empty_bytes(lay.shard_bytes(rank))
+        m0 = shard_map(lay, rank, block)
+        dev.fill_synthetic(m0, live, 31)
+        rows = m0.new_row_sums()
+        snap = dev.empty_bytes(lay.shard_bytes(rank))
+        dev.snapshot(m0, live, snap, rows)          # the per-step snapshot rows
+        succ = (rank + 1) % world
+        replica = dev.empty_bytes(lay.shard_bytes(succ))
+        ms = shard_map(lay, succ, block)
+        dev.fill_synthetic(ms, replica, 31)
+        rep_rows = ms.new_row_sums()
+        dev.checksum(ms, replica, rep_rows)
+        torch.cuda.synchronize()
+        prep = PreparedRecovery(cfg.layer_bytes, members, rank, live, replica, block,
+                                old_rows=rows, replica_rows=rep_rows)
+        for d in members:
+            dist.barrier()
+            if rank == d:
+                continue
+            ev = prep.recover(d)
+            torch.cuda.synchronize()
+            n = prep.plans[d].dst.shard_bytes(rank)
+            exp = _fill_expected(dev, shard_map, prep.plans[d].dst, rank, 31, n)
+            rep[f"prepared drop{d} verified"] = ev.verified
+            rep[f"prepared drop{d} bytes"] = bool(torch.equal(prep.new_view(d)[:n], exp[:n]))
+            rep[f"prepared drop{d} no barrier timeout"] = ev.phases.get("barrier_timeouts") == 0
+        # a corrupted landing must be caught: poison a survivor's source
+        # byte after the snapshot rows were taken, then recover again
+        dist.barrier()
+        bad_drop = world - 1
+        if rank == 0:
+            live[12345] ^= 0x40
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank != bad_drop:
+            ev = prep.recover(bad_drop)
+            rep["corruption detected (not verified)"] = not ev.verified
+        dist.barrier()
+        if rank == 0:
+            live[12345] ^= 0x40
+        torch.cuda.synchronize()
+        dist.barrier()
+        prep.close()
+
+        # ---- DpGroup: plan at failure time, survivors only, MTTR record
+        from paper_2510_00606_b200.recovery import DpGroup
+        from paper_2510_00606_b200.fabric import FAIL_STOP
+        drop = 1 % world
+        rp = ReshardPlan.build(cfg.layer_bytes, members, [m for m in members if m != drop])
+        grp = DpGroup(cfg.layer_bytes, members, rank, None)
+        bufs = RankBuffers(live, replica if succ == drop else None,
+                           dev.empty_bytes(rp.dst.shard_bytes(rank)) if rank != drop else None)
+        dist.barrier()
+        if rank != drop:
+            ev = grp.recover([drop], bufs, step=5, kind=FAIL_STOP)
+            n = rp.dst.shard_bytes(rank)
+            exp = _fill_expected(dev, shard_map, rp.dst, rank, 31, n)
+            rep["dp_group verified"] = ev.verified
+            rep["dp_group bytes"] = bool(torch.equal(bufs.new[:n], exp[:n]))
+            rep["dp_group members"] = grp.members == [m for m in members if m != drop]
+            rep["dp_group csv"] = ev.csv_row(0).startswith("0,5,0,fail_stop,")
+            rep["dp_group microbatches conserve the batch"] = \
+                sum(grp.mb_sizes) == 4 * world
+        dist.barrier()
+        grp.close()
+
+        # ---- staged in-place reshard (C++ InPlaceExecutor): departures and a rejoin
+        from paper_2510_00606_b200.inplace import StagedInPlaceReshard
+        nblk = (cfg.total_bytes + block - 1) // block
+        for drop in sorted({0, world // 2, world - 1}):
+            for old, new in ((members, [r for r in members if r != drop]),
+                             ([r for r in members if r != drop], members)):
+                rp = ReshardPlan.build(cfg.layer_bytes, old, new)
+                stage = max(1 << 16, max(rp.dst.shard_bytes(r) for r in new) // 7)
+                ex = StagedInPlaceReshard(rp, rank, stage_bytes=stage, block_bytes=block,
+                                          phase_bytes=2 * stage, slack=1 + drop % 2)
+                bufs = ex.allocate()
+                before = torch.zeros(2 * nblk, dtype=torch.int64, device="cuda")
+                if bufs.old is not None:
+                    mo = shard_map(rp.src, rank, block)
+                    dev.fill_synthetic(mo, bufs.old, 17)
+                    r0 = mo.new_row_sums()
+                    dev.checksum(mo, bufs.old, r0)
+                    dev.rows_to_blocks(mo, r0, before)
+                if bufs.replica is not None:
+                    dev.fill_synthetic(shard_map(rp.src, rp.replica_of(rank), block),
+                                       bufs.replica, 17)
+                torch.cuda.synchronize()
+                b_all = before.cpu()
+                dist.all_reduce(b_all)
+                ex.bind(bufs, None)
+                after = torch.zeros(2 * nblk, dtype=torch.int64, device="cuda")
+                dist.barrier()
+                ex.launch(after)
+                torch.cuda.synchronize()
+                a_all = after.cpu()
+                dist.all_reduce(a_all)
+                tag = f"in-place {len(old)}->{len(new)} r{drop}"
+                ok = bool(torch.equal(b_all, a_all)) and len(ex.sched.phases) > 2
+                if rank in new:
+                    n = rp.dst.shard_bytes(rank)
+                    exp = _fill_expected(dev, shard_map, rp.dst, rank, 17, n)
+                    ok = ok and bool(torch.equal(bufs.new[:n], exp[:n]))
+                    rep[tag + " no barrier timeout"] = not ex.timed_out()
+                rep[tag] = ok
+                dist.barrier()
+                ex.close()
+                del bufs
+                dist.barrier()
+
+        # ---- peer folds with device barriers (fp32 units and int64 accumulators)
+        n_units, dim = 2 * world, 100_003
+        rng = np.random.default_rng(21)
+        g = rng.normal(0, 1e-3, size=(n_units, dim)).astype(np.float32)
+        g[3, 5] = 1e2
+        w = rng.random(n_units) / n_units
+        mine = [u for u in range(n_units) if u % world == rank]
+        units = [torch.from_numpy(g[u]).cuda() for u in mine]
+        out = torch.empty(dim, dtype=torch.float32, device="cuda")
+        fold, total, opened = dev.peer_weighted_reduce_setup(units, [w[u] for u in mine], out)
+        amax = dev.weighted_absmax(units, [w[u] for u in mine]).cpu()
+        dist.all_reduce(amax, op=dist.ReduceOp.MAX)
+        f = dev.fixed_point_bits(amax.item(), total)
+        all_units = [torch.from_numpy(x).cuda() for x in g]
+        acc1 = torch.empty(dim, dtype=torch.int64, device="cuda")
+        dev.weighted_fold(all_units, w, f, acc1)
+        single = dev.fixed_to_float(acc1, f)
+        bar = dev.PeerBarrier(timeout_s=60.0)
+        for _ in range(2):
+            fold.run(f, bar)
+        bar.wait()
+        torch.cuda.synchronize()
+        rep["fp32 peer fold bit-identical"] = bool(torch.equal(out, single))
+        acc_mine = torch.empty(dim, dtype=torch.int64, device="cuda")
+        dev.weighted_fold(units, [w[u] for u in mine], f, acc_mine)
+        out64 = torch.full((dim,), -1.0, dtype=torch.float32, device="cuda")
+        fold64, opened64 = dev.peer_sum_i64_setup(acc_mine, out64)
+        torch.cuda.synchronize()
+        dist.barrier()
+        for _ in range(2):
+            fold64.run(f, bar)
+        bar.wait()
+        torch.cuda.synchronize()
+        rep["int64 peer fold bit-identical"] = bool(torch.equal(out64, single))
+        rep["peer fold barrier never timed out"] = not bar.timed_out()
+        dist.barrier()
+        bar.close()
+        del fold, fold64
+        for p in opened + opened64:
+            dev.ipc_close(p)
+
+        # ---- ring replica by optimizer replay over an IPC pointer
+        from paper_2510_00606_b200.recovery import ReplayReplica
+        n_par = 200_003 + 17 * rank
+        n_own = 200_003 + 17 * ((rank + 1) % world)
+        gen = torch.Generator(device="cuda").manual_seed(rank)
+        own = dev.AdamState(n_par)
+        own.master.normal_(0, 0.02, generator=gen)
+        grad = torch.empty(n_par, dtype=torch.float32, device="cuda")
+        own_rows = dev.ShardMap(own.segments()).new_row_sums()
+        replica_state = dev.AdamState(n_own)
+        allb = [None] * world
+        dist.all_gather_object(allb, (rank, dev.ipc_handle(own.buf)))
+        h0, o0 = dict(allb)[(rank + 1) % world]
+        p0 = dev.ipc_open(h0, o0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        dev.CopyProgram.from_pointers([p0], [replica_state.buf.data_ptr()],
+                                      [replica_state.nbytes], [True]).launch()
+        torch.cuda.synchronize()
+        dist.barrier()
+        rr = ReplayReplica(members, rank, replica_state, grad, own_rows)
+        hyper = dev.adam_hyper(lr=1e-3)
+        ok = True
+        for step in range(1, 4):
+            grad.normal_(0, 1e-3, generator=gen)
+            dev.adam_step(grad, own, hyper, step, rows=own_rows)
+            torch.cuda.synchronize()
+            dist.barrier()
+            rr.replay(hyper, step)
+            rr.verify()
+            torch.cuda.synchronize()
+            ok = ok and int(rr.bad.item()) == 0
+            dist.barrier()
+        rep["replay replica verified by rows"] = ok
+        torch.cuda.synchronize()
+        dist.barrier()
+        pulled = dev.empty_bytes(replica_state.nbytes)
+        dev.CopyProgram.from_pointers([p0], [pulled.data_ptr()], [replica_state.nbytes],
+                                      [True]).launch()
+        torch.cuda.synchronize()
+        rep["replay replica byte-identical"] = bool(torch.equal(pulled[:replica_state.nbytes],
+                                                                replica_state.buf))
+        dist.barrier()
+        dev.ipc_close(p0)
+        rr.close()
+
+        # ---- host-memory images (double-buffered) as the H2D_D2D source
+        if world <= 4:
+            from paper_2510_00606_b200.hostsnap import HostSnapshots
+            hs = HostSnapshots(lay, members, rank, tag=f"mp{port}")
+            hs.publish(live)                      # epoch 0: the true state
+            torch.cuda.synchronize()
+            dist.barrier()
+            drop = world - 1
+            if rank == drop:                      # epoch 1 torn: D2H of garbage, no commit
+                junk = torch.full_like(live, 0x77)
+                slot = hs.image(rank, epoch=1)
+                slot.copy_(junk[:slot.numel()].cpu())
+            dist.barrier()
+            rp = ReshardPlan.build(cfg.layer_bytes, members, [m for m in members if m != drop])
+            ex = ReshardExecutor(rp, rank)
+            b = ex.allocate(device_replica=False)
+            if b.old is not None:
+                b.old.copy_(live[:b.old.numel()])
+            hs.attach(ex, [drop])
+            ex.bind(b, verify=False)
+            dist.barrier()
+            ex.launch()
+            torch.cuda.synchronize()
+            dist.barrier()
+            if b.new is not None:
+                n = rp.dst.shard_bytes(rank)
+                exp = _fill_expected(dev, shard_map, rp.dst, rank, 31, n)
+                rep["host image (committed epoch) source"] = bool(torch.equal(b.new[:n], exp[:n]))
+            dist.barrier()
+            ex.close()
+            hs.close()
+    except Exception as e:  # noqa: BLE001 - report, do not hang the other ranks
+        import traceback
+        rep["error"] = repr(e) + "\n" + traceback.format_exc()[-2000:]
+    import json
+    Path(out_dir, f"rank{rank}.json").write_text(json.dumps(rep))
+    try:
+        dist.barrier()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(900)
+@pytest.mark.parametrize("world", [4, 8])
+def test_multiprocess_recovery_on_one_gpu(world, tmp_path):
+    import json
+    import torch.multiprocessing as mp
+    mp.spawn(_worker, args=(world, _port(), str(tmp_path), 1e-3), nprocs=world, join=True)
+    checks = 0
+    for r in range(world):
+        rep = json.loads((tmp_path / f"rank{r}.json").read_text())
+        assert "error" not in rep, rep.get("error")
+        for k, v in rep.items():
+            assert v is True, (r, k, v)
+            checks += 1
+    assert checks > 20 * world

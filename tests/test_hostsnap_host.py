@@ -1,7 +1,8 @@
 """Host-side logic of hostsnap.HostSnapshots (no GPU): attach() points the
 ring holder's REPLICA slot of a copy table at each departed rank's image —
 the holder the reference's overlap_matrix names as the H2D_D2D source
-(param_fabric.cpp:112; SnapshotRing::backed_up_by, param_fabric.cpp:51-64)."""
+(param_fabric.cpp:112; SnapshotRing::backed_up_by, param_fabric.cpp:51-64),
+through the executor's peer table (ReshardExecutor.put_peer)."""
 import struct
 import types
 
@@ -31,13 +32,23 @@ def _fake(members, epochs=None):
     return hs
 
 
+class _FakeExecutor:
+    """Records ReshardExecutor.put_peer calls (the peer table)."""
+
+    def __init__(self, table=None):
+        self._table = dict(table or {})
+
+    def put_peer(self, role, member, ptr):
+        self._table[(role, member)] = ptr
+
+
 def _img(hs, r, slot):
     return hs._dev[r] + PAGE + slot * SLOT
 
 
 def test_attach_maps_holder_slot_to_departed_image():
     hs = _fake(range(8))
-    ex = types.SimpleNamespace()
+    ex = _FakeExecutor()
     hs.attach(ex, [3])
     assert ex._table == {(ROLE_REPLICA, 2): _img(hs, 3, 0)}  # holder of 3 is 2
     hs.attach(ex, [0, 5])  # wraps around: holder of 0 is 7
@@ -48,7 +59,7 @@ def test_attach_maps_holder_slot_to_departed_image():
 
 def test_attach_keeps_existing_peer_entries():
     hs = _fake([0, 2, 5])
-    ex = types.SimpleNamespace(_table={(0, 5): 123})
+    ex = _FakeExecutor({(0, 5): 123})
     hs.attach(ex, [2])
     assert ex._table == {(0, 5): 123, (ROLE_REPLICA, 0): _img(hs, 2, 0)}
 
@@ -57,7 +68,7 @@ def test_attach_uses_last_committed_slot():
     """Double-buffered images: epoch e lives in slot e mod 2; a publish that
     died before its commit word leaves the previous epoch's slot in use."""
     hs = _fake(range(4), epochs={1: 7, 2: 4})
-    ex = types.SimpleNamespace()
+    ex = _FakeExecutor()
     hs.attach(ex, [1])
     assert ex._table[(ROLE_REPLICA, 0)] == _img(hs, 1, 1)
     hs.attach(ex, [2])
@@ -67,4 +78,4 @@ def test_attach_uses_last_committed_slot():
 def test_attach_refuses_uncommitted_image():
     hs = _fake(range(3), epochs={1: -1})
     with pytest.raises(RuntimeError, match="not committed"):
-        hs.attach(types.SimpleNamespace(), [1])
+        hs.attach(_FakeExecutor(), [1])
