@@ -87,15 +87,12 @@ def _worker(rank, world, port, result_dir):
         prep = PreparedRecovery(cfg.layer_bytes, range(world), rank, live0, rep0)
         ok = True
         for d in range(world):
-            sums = torch.zeros_like(before)
             dist.barrier()
             rp_d = prep.plans[d]
             if rank != d:
-                prep.recover(d, sums)
+                ok = ok and prep.recover(d).verified  # C++: copy, barrier, conservation
             torch.cuda.synchronize()
             dist.barrier()
-            dist.all_reduce(sums)
-            ok = ok and bool(torch.equal(sums, before))
             if rank != d:
                 exp = dev.empty_bytes(rp_d.dst.shard_bytes(rank))
                 dev.fill_synthetic(shard_map(rp_d.dst, rank), exp, 31)
@@ -163,7 +160,7 @@ def _worker(rank, world, port, result_dir):
                     exp = dev.empty_bytes(n)
                     dev.fill_synthetic(shard_map(rp.dst, rank, block), exp, 17)
                     ok = ok and bool(torch.equal(bufs.new[:n], exp[:n]))
-                    ok = ok and not ex.barrier.timed_out()
+                    ok = ok and not ex.timed_out()
                 report[f"in-place {len(old)}->{len(new)} r{drop}"] = ok
                 dist.barrier()
                 ex.close()
@@ -301,10 +298,14 @@ def _worker(rank, world, port, result_dir):
         report["ring replica before failure verified"] = int(ring.bad.item()) == 0
         dist.barrier()
         ring.close()
+        # every member builds the group (collective: one prepared shrunk
+        # communicator per possible departure); the survivors recover
+        group = DpGroup(cfg.layer_bytes, range(world), rank, comm)
+        dist.barrier()
         if rank != drop:
-            group = DpGroup(cfg.layer_bytes, range(world), rank, comm)
-            ev = group.recover([drop], bufs, group=grp)
+            ev = group.recover([drop], bufs)
             report["recovery verified by checksums"] = ev.verified
+            report["comm repaired by a prepared split"] = ev.phases.get("comm_prepared") == 1.0
             report["recovery mttr row"] = ev.csv_row(0)
             shrunk = group.comm
             exp = dev.empty_bytes(rp.dst.shard_bytes(rank))
@@ -334,8 +335,8 @@ def _worker(rank, world, port, result_dir):
             single = dev.fixed_to_float(acc1, f)
             report["reduce bit-identical to 1-GPU fold"] = bool(torch.equal(out, single))
             report["shrunk size"] = shrunk.size
-            shrunk.destroy()
-        comm.destroy()
+        dist.barrier()
+        group.close()   # the group owns the communicators (parent and splits)
         # the same reduce fused with its collective over peer memory (no NCCL)
         dist.barrier()
         mine = [u for u in range(n_units) if u % world == rank]
