@@ -1427,10 +1427,14 @@ def run_reduce(args, rank, world, out):
     out["reduce"] = {"elements": n, "units_total": REDUCE_UNITS, "units_this_rank": lu,
                      "frac_bits": f, "output_digest": digest,
                      "absmax_ms": round(t_amax * 1e3, 3),
-                     "absmax_gbs": round(4 * n * lu / t_amax / 1e9, 1),
+                     "absmax_gbs": round(4 * n * lu / t_amax / 1e9, 1),  # one DRAM pass per unit
                      "global_max_and_scale_ms": round(t_max * 1e3, 3),
                      "fold_ms": round(t_fold * 1e3, 3),
-                     "fold_gbs": round((4 * lu + 8) * n / t_fold / 1e9, 1),
+                     # one launch reads every unit per element: units that
+                     # alias the same data buffer are read from DRAM once
+                     "fold_dram_gbs": round((4 * len(data) + 8) * n / t_fold / 1e9, 1),
+                     "fold_units_read_gbs": round((4 * lu + 8) * n / t_fold / 1e9, 1),
+                     "distinct_unit_buffers_this_rank": len(data),
                      "nccl_allreduce_int64_ms": round(t_ar * 1e3, 3) if world > 1 else None,
                      "dequant_ms": round(t_deq * 1e3, 3),
                      "dequant_gbs": round(12 * n / t_deq / 1e9, 1),
