@@ -84,6 +84,8 @@ def parse_args():
                    help="comma list of: e2e,cpu,inplace,reshard,host_replica,replica,replay,"
                         "migration,config_c,stage,philox,reduce")
     p.add_argument("--json-out", default="")
+    p.add_argument("--trace", action="store_true",
+                   help="log each leg's start to stderr on every rank (locates a hang)")
     return p.parse_args()
 
 
@@ -1531,37 +1533,58 @@ def bench_b200(args):
     rank, world, local = dist_setup(args)
     skip = set(filter(None, args.skip.split(",")))
     out = {}
+    t_start = time.time()
+
+    def trace(leg):
+        if args.trace:
+            print(f"[{time.time() - t_start:8.2f}s rank {rank}] {leg}", file=sys.stderr,
+                  flush=True)
+
+    trace("snapshot")
     m, live, snap, rows, bad, S, segs = run_snapshot(args, rank, world, local, out)
     if args.only_inplace:
         skip |= {"e2e", "cpu", "reshard", "replica", "replay", "migration", "config_c", "stage",
                  "philox", "reduce"}
     if "e2e" not in skip:
+        trace("e2e")
         run_e2e(args, rank, world, out, m, live, snap, rows, bad, S)
     del live, snap
     torch.cuda.empty_cache()
     if world > 1 and (args.inplace_state_gb > 0 or "inplace" not in skip):
+        trace("inplace")
         run_inplace(args, rank, world, out)
     if world == 1 and rank == 0 and "cpu" not in skip:
+        trace("cpu_baseline")
         run_cpu_baseline(args, out, segs, S)
     if world > 1 and "reshard" not in skip:
+        trace("reshard")
         run_reshard(args, rank, world, out)
     if world > 1 and "host_replica" not in skip:
+        trace("host_replica")
         run_host_replica(args, rank, world, out)
     if world > 1 and "replica" not in skip:
+        trace("replica")
         run_replica(args, rank, world, out)
     if "replay" not in skip:
+        trace("replay")
         run_replay(args, rank, world, out)
     if world > 1 and "migration" not in skip:
+        trace("layer_migration")
         run_layer_migration(args, rank, world, out)
     if world >= 4 and "config_c" not in skip:
+        trace("config_c")
         run_config_c(args, rank, world, out)
     if world > 1 and world % 2 == 0 and "stage" not in skip:
+        trace("stage_move")
         run_stage_move(args, rank, world, out)
     if "philox" not in skip:
+        trace("philox")
         run_philox(args, rank, world, out)
     if "reduce" not in skip:
+        trace("reduce")
         run_reduce(args, rank, world, out)
     if world == 1 and rank == 0 and "cpu" not in skip:
+        trace("cpu_beside")
         run_cpu_beside(args, out)  # cpu_baseline leg, continued
     if rank == 0:
         line = json.dumps(out)

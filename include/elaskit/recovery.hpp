@@ -304,6 +304,10 @@ struct DpGroupOptions {
   int num_microbatches = 32;
   std::int64_t block_bytes = 65536;
   bool prepare_comms = true;  // one shrunk communicator per possible departure
+  // ncclCommSplit splitShare for the prepared communicators: less memory,
+  // but NCCL then requires the sibling communicators never to run
+  // concurrently (prepare() serialises their warm-up either way)
+  bool share_comm_resources = false;
 };
 
 class DpGroup {

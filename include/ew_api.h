@@ -583,7 +583,9 @@ void ew_prepared_free(ew_prepared* p);
  * prepared shrunk communicator per possible departure (prepare_comms: a
  * collective ncclCommSplit per member, splitShare, warmed by one
  * all-reduce), micro-batch reshaper, recovery -> MttrEvent.  kind: 0
- * FailStop, 2 ScaleIn (elaskit::EventKind).  old_buf / replica / new_buf are
+ * FailStop, 2 ScaleIn (elaskit::EventKind).  prepare_comms: bit 0 prepares
+ * the communicators, bit 1 builds them with splitShare (less memory; NCCL
+ * then forbids concurrent use of siblings).  old_buf / replica / new_buf are
  * used when no prepared recovery is attached (planning at failure time). */
 typedef struct ew_dp_group ew_dp_group;
 int ew_dp_group_create(ew_channel* ch, const int64_t* layer_bytes, int n_layers, ew_comm* comm,

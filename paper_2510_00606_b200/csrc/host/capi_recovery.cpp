@@ -333,7 +333,8 @@ int ew_dp_group_create(ew_channel* ch, const int64_t* layer_bytes, int n_layers,
     opt.per_slot_mbs = per_slot_mbs;
     opt.num_microbatches = num_microbatches;
     opt.block_bytes = block_bytes;
-    opt.prepare_comms = prepare_comms != 0;
+    opt.prepare_comms = (prepare_comms & 1) != 0;
+    opt.share_comm_resources = (prepare_comms & 2) != 0;
     *out = new ew_dp_group{std::make_unique<DpGroup>(
         *ch->c, std::vector<int64_t>(layer_bytes, layer_bytes + n_layers), comm, opt)};
     return EW_OK;

@@ -816,15 +816,20 @@ void DpGroup::prepare() {
   const int key = index_of(members_, me);
   for (int d : members_) {
     ew_comm* c = nullptr;
-    check(ew_comm_split(comm_, me == d ? -1 : 0, key, 1, &c));
+    check(ew_comm_split(comm_, me == d ? -1 : 0, key, opt_.share_comm_resources ? 1 : 0, &c));
     if (c != nullptr) prepared_comms_[d] = c;
   }
   // one collective on each (NCCL connects lazily): the repair at failure
-  // time is then a lookup of a live communicator
+  // time is then a lookup of a live communicator.  One communicator at a
+  // time across the group (host barrier between them): siblings that share
+  // resources must never run concurrently, and the members of different
+  // siblings would otherwise start them in different orders
   std::int64_t* one = dalloc<std::int64_t>(1);
-  for (int d : members_)
+  for (int d : members_) {
     if (d != me) check(ew_allreduce_i64(prepared_comms_.at(d), one, 1, nullptr));
-  check(ew_device_sync());
+    check(ew_device_sync());
+    ch_.barrier();
+  }
   dfree(one);
 }
 

@@ -305,7 +305,7 @@ class DpGroup:
     def __init__(self, layer_bytes: Sequence[int], members: Sequence[int], rank: int,
                  comm: Optional[dev.Communicator], per_slot_mbs: int = 4,
                  num_microbatches: int = 32, block_bytes: int = dev.DEFAULT_BLOCK_BYTES,
-                 prepare_comms: bool = True, group=None):
+                 prepare_comms: bool = True, group=None, share_comm_resources: bool = False):
         """`comm` (over `members` in ascending order) is taken over: the
         group destroys it.  Collective over `group` (all members)."""
         self.layer_bytes = list(layer_bytes)
@@ -320,7 +320,8 @@ class DpGroup:
         check(lib.ew_dp_group_create(self.channel.handle, N.i64_array(self.layer_bytes),
                                      len(self.layer_bytes), raw, int(per_slot_mbs),
                                      int(num_microbatches), int(block_bytes),
-                                     int(bool(prepare_comms)), C.byref(h)))
+                                     int(bool(prepare_comms)) | (2 if share_comm_resources else 0),
+                                     C.byref(h)))
         self._h = h
         self._prepared: Optional[PreparedRecovery] = None
 

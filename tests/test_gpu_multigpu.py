@@ -33,7 +33,14 @@ def _worker(rank, world, port, result_dir):
     dist.init_process_group("nccl", rank=rank, world_size=world,
                             device_id=torch.device("cuda", rank))
     report = {}
+    progress = Path(result_dir, f"progress{rank}.txt")
+
+    def stage(name):  # located hangs: the last stage each rank reached
+        with progress.open("a") as fh:
+            fh.write(name + "\n")
+
     try:
+        stage("reshard")
         # (b) reshard world -> world-1 of a scaled 7B state, every drop position
         cfg = configs.scaled(configs.llama2_7b_per_tensor(), 2e-3)
         for drop in range(world):
@@ -66,6 +73,7 @@ def _worker(rank, world, port, result_dir):
                 report[f"reshard drop{drop} push={push}"] = ok
                 ex.close()
                 dist.barrier()
+        stage("prepared")
         # every single departure prepared in steady state (recovery.PreparedRecovery)
         from paper_2510_00606_b200.recovery import PreparedRecovery
         rp0 = ReshardPlan.build(cfg.layer_bytes, range(world), range(world))
@@ -101,6 +109,7 @@ def _worker(rank, world, port, result_dir):
         report["prepared single departures verified"] = ok
         dist.barrier()
         prep.close()
+        stage("stage move")
         # cross-stage layer move (interleaved in place, and contiguous)
         d = world // 2
         for contiguous in (False, True):
@@ -120,6 +129,7 @@ def _worker(rank, world, port, result_dir):
             report[f"stage move contiguous={contiguous}"] = bool(torch.equal(bufs.new[:n], exp[:n]))
             ex.close()
             dist.barrier()
+        stage("in-place")
         # staged in-place reshard (config D geometry): OLD and NEW in one
         # buffer, many phases; every departure, and a rejoin (phases upward)
         from paper_2510_00606_b200.inplace import StagedInPlaceReshard
@@ -166,6 +176,7 @@ def _worker(rank, world, port, result_dir):
                 ex.close()
                 dist.destroy_process_group(sub)
                 dist.barrier()
+        stage("ring replica")
         # ring replica refresh: pull the successor's snapshot, verify by rows
         from paper_2510_00606_b200.recovery import RingReplica
         lay = ReshardPlan.build(cfg.layer_bytes, range(world), range(world)).src
@@ -187,6 +198,7 @@ def _worker(rank, world, port, result_dir):
                                                    exp[:lay.shard_bytes(owner)]))
         dist.barrier()
         rr.close()
+        stage("replay")
         # ring replica by optimizer replay: the holder steps its replica from
         # the owner's gradient read over NVLink; byte-identical, rows verify
         from paper_2510_00606_b200.recovery import ReplayReplica
@@ -240,6 +252,7 @@ def _worker(rank, world, port, result_dir):
         dist.barrier()
         dev.ipc_close(p1)
         rep.close()
+        stage("toy")
         # toy consistency across real ranks: one slot per GPU, the last rank
         # leaves before step 2, survivors reshape and sum on the shrunk NCCL
         # communicator; final parameters equal the static run bit for bit
@@ -265,6 +278,7 @@ def _worker(rank, world, port, result_dir):
         if state["shrunk"] and state["comm"] is not None:
             state["comm"].destroy()
         tcomm.destroy()
+        stage("dp group")
         # full DP recovery of the last rank (recovery.DpGroup): plan_edit +
         # ncclCommShrink, reshape, remap, checksum verification
         from paper_2510_00606_b200.recovery import DpGroup
@@ -337,6 +351,7 @@ def _worker(rank, world, port, result_dir):
             report["shrunk size"] = shrunk.size
         dist.barrier()
         group.close()   # the group owns the communicators (parent and splits)
+        stage("peer reduce")
         # the same reduce fused with its collective over peer memory (no NCCL)
         dist.barrier()
         mine = [u for u in range(n_units) if u % world == rank]
@@ -393,17 +408,22 @@ def _worker(rank, world, port, result_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.timeout(420)  # a collective mismatch must fail, not hang the box
+@pytest.mark.timeout(300)  # a collective mismatch must fail, not hang the box
 @pytest.mark.parametrize("world", [2, 4])
 def test_multi_gpu_reshard_comm_reduce(world, tmp_path):
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs")
     import json
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    try:
+        mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    finally:  # where each rank got to (a hang is located by the last stage)
+        for r in range(world):
+            f = tmp_path / f"progress{r}.txt"
+            print(f"rank {r} stages:", f.read_text().split() if f.exists() else None)
     for r in range(world):
         rep = json.loads((tmp_path / f"rank{r}.json").read_text())
-        assert "error" not in rep, rep
+        assert "error" not in rep, rep.get("error")
         for k, v in rep.items():
             if isinstance(v, bool):
                 assert v is True, (r, k)
