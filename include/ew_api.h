@@ -391,6 +391,10 @@ int ew_comm_shrink(ew_comm* parent, const int* exclude_ranks, int n_exclude, int
  * failure time is a lookup (recovery.hpp DpGroup). */
 int ew_comm_split(ew_comm* parent, int color, int key, int share, ew_comm** out);
 int ew_comm_rank(const ew_comm* comm, int* rank, int* nranks);
+/* ncclCommAbort: frees the communicator without waiting for its peers (a
+ * communicator that includes a departed rank; ncclCommDestroy may block on
+ * peers that will never arrive). */
+int ew_comm_abort(ew_comm* comm);
 int ew_comm_destroy(ew_comm* comm);
 /* In-place sums over the communicator. */
 int ew_allreduce_i64(ew_comm* comm, int64_t* buf, int64_t n, ew_stream_t stream);

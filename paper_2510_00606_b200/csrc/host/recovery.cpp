@@ -802,16 +802,21 @@ DpGroup::DpGroup(Channel& ch, const std::vector<std::int64_t>& layer_bytes, ew_c
 }
 
 DpGroup::~DpGroup() {
-  for (auto& [d, c] : prepared_comms_) ew_comm_destroy(c);
+  // ncclCommAbort throughout: a communicator that includes a departed member
+  // cannot be destroyed collectively (its peer never arrives), and the group
+  // may be torn down on any subset of its members
+  for (auto& [d, c] : prepared_comms_) ew_comm_abort(c);
   prepared_comms_.clear();
-  ew_comm_destroy(comm_);
-  for (auto it = retired_.rbegin(); it != retired_.rend(); ++it) ew_comm_destroy(*it);
+  ew_comm_abort(comm_);
+  for (auto it = retired_.rbegin(); it != retired_.rend(); ++it) ew_comm_abort(*it);
 }
 
 void DpGroup::prepare() {
   if (comm_ == nullptr || members_.size() < 2) return;
-  for (auto& [d, c] : prepared_comms_) ew_comm_destroy(c);
+  for (auto& [d, c] : prepared_comms_) retired_.push_back(c);
   prepared_comms_.clear();
+  for (auto it = retired_.rbegin(); it != retired_.rend(); ++it) ew_comm_abort(*it);
+  retired_.clear();
   const int me = ch_.me();
   const int key = index_of(members_, me);
   for (int d : members_) {
@@ -954,9 +959,11 @@ MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
   members_ = survivors;
   mb_sizes_ = next.per_slot_mbs;
   if (comm_ != nullptr) {
-    for (auto& [d, c] : prepared_comms_) ew_comm_destroy(c);
+    // the parent and the other departures' communicators include the
+    // departed member: retired (aborted later, never destroyed collectively)
+    for (auto& [d, c] : prepared_comms_) retired_.push_back(c);
     prepared_comms_.clear();
-    retired_.push_back(comm_);  // children share its resources: freed last
+    retired_.push_back(comm_);
     comm_ = new_comm;
   }
   return ev;

@@ -301,6 +301,14 @@ int ew_comm_split(ew_comm* parent, int color, int key, int share, ew_comm** out)
   return EW_OK;
 }
 
+int ew_comm_abort(ew_comm* comm) {
+  if (comm == nullptr) return EW_OK;
+  const ncclResult_t r = ncclCommAbort(comm->nccl);
+  delete comm;
+  if (r != ncclSuccess) return nccl_status(r, "ncclCommAbort");
+  return EW_OK;
+}
+
 int ew_comm_rank(const ew_comm* comm, int* rank, int* nranks) {
   if (comm == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL comm");
   if (rank) *rank = comm->rank;

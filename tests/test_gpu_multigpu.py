@@ -35,12 +35,12 @@ def _worker(rank, world, port, result_dir):
     report = {}
     progress = Path(result_dir, f"progress{rank}.txt")
 
-    def stage(name):  # located hangs: the last stage each rank reached
+    def mark(name):  # located hangs: the last stage each rank reached
         with progress.open("a") as fh:
             fh.write(name + "\n")
 
     try:
-        stage("reshard")
+        mark("reshard")
         # (b) reshard world -> world-1 of a scaled 7B state, every drop position
         cfg = configs.scaled(configs.llama2_7b_per_tensor(), 2e-3)
         for drop in range(world):
@@ -73,7 +73,7 @@ def _worker(rank, world, port, result_dir):
                 report[f"reshard drop{drop} push={push}"] = ok
                 ex.close()
                 dist.barrier()
-        stage("prepared")
+        mark("prepared")
         # every single departure prepared in steady state (recovery.PreparedRecovery)
         from paper_2510_00606_b200.recovery import PreparedRecovery
         rp0 = ReshardPlan.build(cfg.layer_bytes, range(world), range(world))
@@ -109,7 +109,7 @@ def _worker(rank, world, port, result_dir):
         report["prepared single departures verified"] = ok
         dist.barrier()
         prep.close()
-        stage("stage move")
+        mark("stage move")
         # cross-stage layer move (interleaved in place, and contiguous)
         d = world // 2
         for contiguous in (False, True):
@@ -129,7 +129,7 @@ def _worker(rank, world, port, result_dir):
             report[f"stage move contiguous={contiguous}"] = bool(torch.equal(bufs.new[:n], exp[:n]))
             ex.close()
             dist.barrier()
-        stage("in-place")
+        mark("in-place")
         # staged in-place reshard (config D geometry): OLD and NEW in one
         # buffer, many phases; every departure, and a rejoin (phases upward)
         from paper_2510_00606_b200.inplace import StagedInPlaceReshard
@@ -176,7 +176,7 @@ def _worker(rank, world, port, result_dir):
                 ex.close()
                 dist.destroy_process_group(sub)
                 dist.barrier()
-        stage("ring replica")
+        mark("ring replica")
         # ring replica refresh: pull the successor's snapshot, verify by rows
         from paper_2510_00606_b200.recovery import RingReplica
         lay = ReshardPlan.build(cfg.layer_bytes, range(world), range(world)).src
@@ -198,7 +198,7 @@ def _worker(rank, world, port, result_dir):
                                                    exp[:lay.shard_bytes(owner)]))
         dist.barrier()
         rr.close()
-        stage("replay")
+        mark("replay")
         # ring replica by optimizer replay: the holder steps its replica from
         # the owner's gradient read over NVLink; byte-identical, rows verify
         from paper_2510_00606_b200.recovery import ReplayReplica
@@ -252,7 +252,7 @@ def _worker(rank, world, port, result_dir):
         dist.barrier()
         dev.ipc_close(p1)
         rep.close()
-        stage("toy")
+        mark("toy")
         # toy consistency across real ranks: one slot per GPU, the last rank
         # leaves before step 2, survivors reshape and sum on the shrunk NCCL
         # communicator; final parameters equal the static run bit for bit
@@ -278,7 +278,7 @@ def _worker(rank, world, port, result_dir):
         if state["shrunk"] and state["comm"] is not None:
             state["comm"].destroy()
         tcomm.destroy()
-        stage("dp group")
+        mark("dp group")
         # full DP recovery of the last rank (recovery.DpGroup): plan_edit +
         # ncclCommShrink, reshape, remap, checksum verification
         from paper_2510_00606_b200.recovery import DpGroup
@@ -351,7 +351,7 @@ def _worker(rank, world, port, result_dir):
             report["shrunk size"] = shrunk.size
         dist.barrier()
         group.close()   # the group owns the communicators (parent and splits)
-        stage("peer reduce")
+        mark("peer reduce")
         # the same reduce fused with its collective over peer memory (no NCCL)
         dist.barrier()
         mine = [u for u in range(n_units) if u % world == rank]
@@ -402,7 +402,8 @@ def _worker(rank, world, port, result_dir):
         for p in opened + opened64:
             dev.ipc_close(p)
     except Exception as e:  # report, do not hang the other ranks
-        report["error"] = repr(e)
+        import traceback
+        report["error"] = repr(e) + "\n" + traceback.format_exc()[-1500:]
     import json
     Path(result_dir, f"rank{rank}.json").write_text(json.dumps(report))
     dist.destroy_process_group()
