@@ -554,8 +554,8 @@ def run_reshard(args, rank, world, out):
         "total_ms": round(mt["total_s"] * 1e3, 3),
         "phases_ms": {k[:-2]: round(mt[k] * 1e3, 3) for k in phases},
         "verified_by_checksums_and_bytes": all_ranks_true(verified, world),
-        "comm_repair_path": "prepared shrunk communicator (ncclCommSplit, splitShare) looked "
-                            "up, then its first all-reduce",
+        "comm_repair_path": "prepared shrunk communicator (ncclCommSplit in steady state) "
+                            "looked up, then its first all-reduce",
         "mttr_csv_rank0_row": csv if rank == 0 else None,
         "steady_state_ms": {"prepare_comms": round(t_prep_comm * 1e3, 1),
                             "prepare_recovery": round(t_prep * 1e3, 1)}}
