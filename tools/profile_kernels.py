@@ -2,10 +2,11 @@
 size, for ncu captures (`ncu --set full -k regex:...`).  Prints per-kernel
 CUDA-event times so the same command can run without ncu first.
 
-  (a) row_kernel<0> snapshot, row_kernel<2> verify     7B rank shard 11.79 GB
+  (a) tma_row_kernel<0> snapshot, <2> verify          7B rank shard 11.79 GB
   (b) staged_copy_kernel, local 4 GiB aligned + 1 GiB misaligned
   (c) mask_kernel, config E busiest rank (224 x 4096^2)
-  (d) fold_kernel, 1 Gi fp32 elements
+  (d) absmax_kernel, fold_kernel, dequant_kernel: one 7B fp32 gradient
+      (6.74 G elements, config E's per-rank unit)
   §8(f)#1 adam_kernel, 7B rank shard (842 M params, 11.79 GB state)
   §8(f)#2 payback_kernel, one 7B layer (202 M int64), local source
   (b) staged_copy_kernel verified: 4->3 of 7B-per-GPU state, every rank's
@@ -62,10 +63,17 @@ def main():
     out["mask_ms"] = timed(lambda: dev.dropout_mask(0, 0, 224, 1, 0, 4096 * 4096, 0.5, bits))
     del bits
 
-    g = torch.empty(1 << 30, dtype=torch.float32, device="cuda").normal_(0, 1e-3)
-    acc = torch.empty(1 << 30, dtype=torch.int64, device="cuda")
-    out["fold_ms"] = timed(lambda: dev.weighted_fold([g], [0.2], 60, acc))
-    del g, acc
+    ng = 6_738_415_616
+    g = torch.empty(ng, dtype=torch.float32, device="cuda").normal_(0, 1e-3)
+    acc = torch.empty(ng, dtype=torch.int64, device="cuda")
+    res = torch.empty(ng, dtype=torch.float32, device="cuda")
+    out["absmax_ms"] = timed(lambda: dev.weighted_absmax([g], [0.2]))
+    out["fold_ms"] = timed(lambda: dev.weighted_fold([g], [0.2], 54, acc))
+    out["dequant_ms"] = timed(lambda: dev.fixed_to_float(acc, 54, res))
+    out["absmax_gbs"] = 4 * ng / out["absmax_ms"] / 1e6
+    out["fold_gbs"] = 12 * ng / out["fold_ms"] / 1e6
+    out["dequant_gbs"] = 12 * ng / out["dequant_ms"] / 1e6
+    del g, acc, res
     torch.cuda.empty_cache()
 
     n = 6_738_415_616 // 8
