@@ -293,7 +293,10 @@ int ew_weighted_fold_addend(const float* const* units, const double* weights, in
   for (int off = 0; off < n_units; off += kMaxUnits) {
     Units u;
     if (int st = pack_units(units, weights, n_units, off, u)) return st;
-    const int grid = grid_for((n_elems + 3) / 4);
+    // one resident wave: 62 registers x 256 threads allow 4 CTAs per SM
+    const int grid = resident_grid(accumulate || off > 0 ? (const void*)fold_kernel<true>
+                                                         : (const void*)fold_kernel<false>,
+                                   (n_elems + 3) / 4);
     long long* a = reinterpret_cast<long long*>(acc);
     const long long* add = off == 0 ? reinterpret_cast<const long long*>(addend) : nullptr;
     if (accumulate || off > 0)
