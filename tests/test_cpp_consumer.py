@@ -51,6 +51,11 @@ def test_cpp_recovery_driver_builds():
         pytest.skip("no g++")
     subprocess.run(["make", "-s", "-C", str(ROOT / "tools" / "cpp")], check=True)
     assert (ROOT / "tools" / "cpp" / "recover_demo").exists()
+    # the multi-process driver (C++ only, TCP store rendezvous, DpGroup)
+    assert (ROOT / "tools" / "cpp" / "dp_recover").exists()
+    r = subprocess.run([str(ROOT / "tools" / "cpp" / "dp_recover")], capture_output=True,
+                       text=True)
+    assert r.returncode == 2 and "usage" in r.stderr
 
 
 @pytest.mark.gpu
