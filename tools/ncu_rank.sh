@@ -6,8 +6,8 @@
 #       tools/ncu_rank.sh tools/nvlink_evidence.py --reps 2
 OUT=${NCU_OUT:-gpurun_out/ncu_nvlink_rank${NCU_RANK:-1}.csv}
 if [ "$RANK" = "${NCU_RANK:-1}" ]; then
-  exec ncu --clock-control none -k regex:"staged_copy|peer_fold" -c 16 --csv --log-file "$OUT" \
-    --metrics gpu__time_duration.sum,nvlrx__bytes.sum,nvlrx__bytes_data_user.sum,nvltx__bytes.sum,nvltx__bytes_data_user.sum,dram__bytes_read.sum,dram__bytes_write.sum \
+  exec ncu --replay-mode kernel --clock-control none -k regex:"staged_copy|peer_fold" -c 16 --csv --log-file "$OUT" \
+    --metrics gpu__time_duration.sum,nvlrx__bytes.sum,nvlrx__bytes_data_user.sum,nvltx__bytes.sum,nvltx__bytes_data_user.sum \
     python "$@"
 else
   exec python "$@"
