@@ -77,7 +77,15 @@ def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    # ncu's application replay re-runs every rank once per counter pass: each
+    # pass rendezvouses on its own port (a pass counter per rank), so no pass
+    # reads a previous pass's NCCL id from a shared store
+    base = int(os.environ["MASTER_PORT"])
+    counter = Path(f"/tmp/ew_nvlink_pass_{base}_{rank}")
+    k = int(counter.read_text()) + 1 if counter.exists() else 0
+    counter.write_text(str(k))
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{base + 1 + k}", rank=rank,
+                            world_size=world, device_id=torch.device("cuda", local))
     pynvml.nvmlInit()
     h = pynvml.nvmlDeviceGetHandleByIndex(nvml_index(local))
     res = {"rank": rank}
