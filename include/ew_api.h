@@ -219,6 +219,9 @@ int ew_plan_edit(int n_groups, const char* const* ids, const int* topo, const in
  * ---------------------------------------------------------------------- */
 int ew_device_count(int* n);
 int ew_set_device(int device);
+/* Map peer_device's memory into the current device's address space (one
+ * process driving several GPUs; processes use CUDA IPC instead). */
+int ew_peer_access_enable(int peer_device);
 int ew_alloc(int64_t bytes, void** out); /* cudaMalloc, 256-B aligned, current device */
 int ew_free(void* ptr);
 int ew_memset_async(void* ptr, int value, int64_t bytes, ew_stream_t stream);

@@ -252,6 +252,8 @@ _sig("ew_adam_step", i32, vp, vp, vp, vp, vp, i64, P(AdamHyper), i64, vp)
 _sig("ew_adam_step_rows", i32, vp, vp, vp, vp, vp, i64, P(AdamHyper), i64, vp, i64, i64, vp, vp)
 _sig("ew_rows_diff", i32, vp, vp, i64, vp, vp)
 _sig("ew_comm_split", i32, vp, i32, i32, i32, P(vp))
+_sig("ew_peer_access_enable", i32, i32)
+_sig("ew_set_device", i32, i32)
 _sig("ew_block_verifier_create", i32, P(vp), i32, P(vp), i32, i64, i64, P(vp))
 _sig("ew_block_verifier_run", i32, vp, vp, vp)
 _sig("ew_block_verifier_free", None, vp)

@@ -99,6 +99,16 @@ int ew_set_device(int device) {
   return EW_OK;
 }
 
+int ew_peer_access_enable(int peer_device) {
+  const cudaError_t e = cudaDeviceEnablePeerAccess(peer_device, 0);
+  if (e == cudaErrorPeerAccessAlreadyEnabled) {
+    cudaGetLastError();  // clear the sticky-free error state
+    return EW_OK;
+  }
+  EW_CUDA_TRY(e);
+  return EW_OK;
+}
+
 int ew_alloc(int64_t bytes, void** out) {
   if (out == nullptr || bytes < 0) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_alloc: bad arguments");
   *out = nullptr;
