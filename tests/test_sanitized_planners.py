@@ -1,0 +1,39 @@
+"""The product's host planners (csrc/host, the drop-in C++ API) under
+AddressSanitizer + UndefinedBehaviorSanitizer, driven by the reference's own
+six unit-test programs (no sanitizer runs existed in round 1).
+Every suite must finish with no sanitizer report and the same pass/fail
+counts as the same suite against the reference library (test_migration's two
+failing cases fail on the reference too)."""
+import os
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parents[1]
+REF = Path("/root/reference/proj")
+SUITES = ["param_fabric", "rng", "dataflow", "communicator", "migration", "cluster"]
+
+
+def _counts(text):
+    m = re.search(r"test cases: (\d+) \| (\d+) passed \| (\d+) failed", text)
+    assert m, text[-500:]
+    return tuple(int(x) for x in m.groups())
+
+
+@pytest.mark.timeout(900)
+def test_host_planners_asan_ubsan_reference_suites():
+    if not (REF / "src" / "rng.cpp").exists():
+        pytest.skip("reference sources absent (the suites compile from them)")
+    subprocess.run(["make", "-s", "-j", str(min(8, os.cpu_count() or 1)), "-C",
+                    str(ROOT / "oracle"), "asan", "ref"], check=True, capture_output=True)
+    env = dict(os.environ, ASAN_OPTIONS="detect_leaks=1", UBSAN_OPTIONS="print_stacktrace=1")
+    for s in SUITES:
+        san = subprocess.run([str(ROOT / "oracle" / "_ref" / "asan" / f"test_{s}")],
+                             capture_output=True, text=True, env=env)
+        out = san.stdout + san.stderr
+        assert "Sanitizer" not in out and "runtime error" not in out, out[-3000:]
+        ref = subprocess.run([str(ROOT / "oracle" / "_ref" / f"test_{s}_ref")],
+                             capture_output=True, text=True)
+        assert _counts(out) == _counts(ref.stdout + ref.stderr), s
