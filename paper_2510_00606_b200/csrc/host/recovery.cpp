@@ -13,6 +13,7 @@
 #include <arpa/inet.h>
 #include <cuda_runtime.h>
 #include <netdb.h>
+#include <nvtx3/nvToolsExt.h>
 #include <netinet/in.h>
 #include <netinet/tcp.h>
 #include <sys/socket.h>
@@ -39,6 +40,15 @@ using device::check;
 namespace {
 
 using Clock = std::chrono::steady_clock;
+
+// NVTX range per MTTR phase (header-only NVTX3: free without a tool attached;
+// ncu --nvtx / Nsight Systems show the recovery's phases on the timeline)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 double seconds(Clock::time_point a, Clock::time_point b) {
   return std::chrono::duration<double>(b - a).count();
 }
@@ -637,6 +647,7 @@ bool run_move(const ReshardExecutor& exec, const BlockVerifier& verifier, std::u
               std::int64_t n_words,
               std::uint32_t* bad, ew_peer_barrier* barrier, double timeout_s, Channel& survivors,
               ew_stream_t stream, MttrEvent* ev) {
+  NvtxRange range("ew.remap.copy_verify");
   cudaEvent_t e[3];
   for (cudaEvent_t& x : e) cuda_check(cudaEventCreate(&x), "cudaEventCreate");
   const auto t0 = Clock::now();
@@ -658,8 +669,10 @@ bool run_move(const ReshardExecutor& exec, const BlockVerifier& verifier, std::u
   int timed_out = 0;
   if (barrier != nullptr) check(ew_peer_barrier_timed_out(barrier, &timed_out));
   const auto t1 = Clock::now();
+  nvtxRangePushA("ew.remap.verdict");
   const std::int64_t total = survivors.sum(static_cast<std::int64_t>(bad_host) +
                                            (timed_out ? (std::int64_t{1} << 40) : 0));
+  nvtxRangePop();
   const auto t2 = Clock::now();
   float copy_ms = 0.f, verify_ms = 0.f;
   cudaEventElapsedTime(&copy_ms, e[0], e[1]);
@@ -685,6 +698,7 @@ PreparedRecovery::PreparedRecovery(Channel& ch, const std::vector<std::int64_t>&
                                    const std::uint64_t* replica_rows, void* new_buf,
                                    std::int64_t new_capacity, PreparedOptions opt)
     : ch_(ch), members_(ch.members()), me_(ch.me()), opt_(opt) {
+  NvtxRange range("ew.prepare_recovery");
   const int n = static_cast<int>(members_.size());
   if (n < 2) throw std::invalid_argument("PreparedRecovery needs at least two members");
   std::int64_t max_new = 0;
@@ -813,6 +827,7 @@ DpGroup::~DpGroup() {
 
 void DpGroup::prepare() {
   if (comm_ == nullptr || members_.size() < 2) return;
+  NvtxRange range("ew.prepare_comms");
   for (auto& [d, c] : prepared_comms_) retired_.push_back(c);
   prepared_comms_.clear();
   for (auto it = retired_.rbegin(); it != retired_.rend(); ++it) ew_comm_abort(*it);
@@ -851,7 +866,9 @@ MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
   MttrEvent ev;
   ev.step = step;
   ev.kind = to_string(kind);
+  NvtxRange range("ew.recover");
   const auto t0 = Clock::now();
+  nvtxRangePushA("ew.comm_repair");
 
   // comm repair: the edit plan (communicator.cpp:54-105), then the NCCL
   // communicator: a prepared split (lookup) or a shrink at failure time;
@@ -886,6 +903,8 @@ MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
   ev.phases["plan_edit_s"] = seconds(t0, t_edit);
   const auto t1 = Clock::now();
   ev.comm_repair_s = seconds(t0, t1);
+  nvtxRangePop();
+  nvtxRangePushA("ew.reshape");
 
   // dataflow: the global batch over the survivors (dataflow.cpp:52-69)
   MicrobatchAssignment mb;
@@ -897,6 +916,8 @@ MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
   const MicrobatchAssignment next = reshard_microbatches(mb, idx);
   const auto t2 = Clock::now();
   ev.other_s = seconds(t1, t2);
+  nvtxRangePop();
+  NvtxRange remap("ew.remap");
 
   // remap
   if (prepared_ != nullptr && gone.size() == 1 && prepared_->members() == members_) {
