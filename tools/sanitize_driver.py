@@ -32,7 +32,7 @@ dev.weighted_fold([g], [0.5], 40, acc)
 # round-2 kernels: bit-pattern absmax (aligned + misaligned units, > 16
 # units), vectorised dequant (fp32/fp64, ragged tails), guarded copy,
 # conservation verifier, AdamW replay with fused rows, in-place emulation
-units = [torch.randn(4099 + k, device="cuda")[k % 3:] for k in range(18)]
+units = [torch.randn(4102, device="cuda")[k % 3:k % 3 + 4099] for k in range(18)]
 dev.weighted_absmax(units, [0.1] * 18)
 for n in (1, 7, 4099):
     dev.fixed_to_float(acc[:n], 40)
