@@ -38,7 +38,7 @@ class PartitionLayout:
         self._h = C.c_void_p(handle)
 
     def __del__(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
             lib.ew_layout_free(self._h)
             self._h = None
 
@@ -159,7 +159,7 @@ class TransferPlan:
         self.total_bytes_moved = lib.ew_plan_total_bytes_moved(self._h)
 
     def __del__(self):
-        if getattr(self, "_h", None) is not None and self._h.value:
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
             lib.ew_plan_free(self._h)
             self._h = None
 
