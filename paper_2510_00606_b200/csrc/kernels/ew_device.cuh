@@ -94,6 +94,25 @@ __device__ __forceinline__ Vec32 ld_stream32(const void* p) {
   return v;
 }
 
+// 32-byte load of data this kernel also writes (no .nc): read-modify-write
+// of an accumulator
+__device__ __forceinline__ Vec32 ld_plain32(const void* p) {
+  uint32_t r[8];
+  asm volatile("ld.global.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                 "=r"(r[6]), "=r"(r[7])
+               : "l"(p));
+  Vec32 v;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v.w[k] = (static_cast<uint64_t>(r[2 * k + 1]) << 32) | r[2 * k];
+  return v;
+}
+
+// the j-th fp32 (j < 8) of a 32-byte vector
+__device__ __forceinline__ float f32_of(const Vec32& v, int j) {
+  return __uint_as_float(static_cast<uint32_t>(v.w[j >> 1] >> (32 * (j & 1))));
+}
+
 __device__ __forceinline__ void st_stream32(void* p, const Vec32& v) {
   asm volatile(
       "st.global.L1::no_allocate.L2::evict_first.v8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(p),
