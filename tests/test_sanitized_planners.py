@@ -30,7 +30,7 @@ def test_host_planners_asan_ubsan_reference_suites():
                     str(ROOT / "oracle"), "asan", "ref"], check=True, capture_output=True)
     env = dict(os.environ, ASAN_OPTIONS="detect_leaks=1", UBSAN_OPTIONS="print_stacktrace=1")
     for s in SUITES:
-        san = subprocess.run([str(ROOT / "build" / "asan" / f"test_{s}")],
+        san = subprocess.run([str(ROOT / "gpurun_out" / "asan" / f"test_{s}")],
                              capture_output=True, text=True, env=env)
         out = san.stdout + san.stderr
         assert "Sanitizer" not in out and "runtime error" not in out, out[-3000:]
