@@ -214,6 +214,93 @@ class BlockVerifier {
   ew_block_verifier* v_ = nullptr;
 };
 
+// ------------------------------------------------------------ ring replicas
+
+// The AdamW state of one ZeRO shard as the replay kernel updates it: device
+// pointers into one byte image (the Python device.AdamState layout: fp32
+// master, exp_avg, exp_avg_sq and the bf16 parameter copy, sections on
+// 1 MiB boundaries).
+struct AdamShard {
+  float* master = nullptr;
+  float* exp_avg = nullptr;
+  float* exp_avg_sq = nullptr;
+  std::uint16_t* param_bf16 = nullptr;
+  std::int64_t n = 0;
+  const void* image = nullptr;
+  std::int64_t image_bytes = 0;
+};
+
+// Ring replica kept by optimizer replay (the paper's
+// mechanism, with the replica in the holder's HBM): each
+// step the holder applies the owner's AdamW step to its replica, reading the
+// owner's reduced gradient shard over NVLink (4 B/param instead of the
+// 14 B/param of a state pull), and produces the replica's checksum rows in the
+// same pass; verification compares them with the owner's rows in the owner's
+// HBM.  Both sides run the same explicitly rounded kernel on the same inputs,
+// so the replica stays byte-identical.  Ordering contract: the owner must not
+// overwrite its gradient shard before the holder's replay of that step
+// finished.
+class ReplayReplica {
+ public:
+  // Collective over `ch` (the ring's members in ring order = ascending ids).
+  // my_grad / my_rows: this rank's gradient shard and the checksum rows of
+  // its own state (written by its ew_adam_step_rows); replica: the state of
+  // the member this rank backs up (SnapshotRing::backs_up).
+  ReplayReplica(Channel& ch, const float* my_grad, const std::uint64_t* my_rows,
+                AdamShard replica, std::int64_t block_bytes = 65536);
+  ~ReplayReplica();
+  ReplayReplica(const ReplayReplica&) = delete;
+  ReplayReplica& operator=(const ReplayReplica&) = delete;
+
+  int owner() const { return owner_; }
+  // the owner's step `step` applied to the replica (+ its rows, one pass)
+  void replay(const ew_adam_hyper& hyper, std::int64_t step, ew_stream_t stream);
+  // *bad_dev = rows where the replica's rows differ from the owner's
+  void verify(std::uint32_t* bad_dev, ew_stream_t stream) const;
+  // stronger: recompute the replica's rows from HBM and compare
+  void verify_by_reread(std::uint32_t* bad_dev, ew_stream_t stream) const;
+  const std::uint64_t* replica_rows() const { return rows_; }
+
+ private:
+  PeerBuffers peers_;
+  AdamShard rep_;
+  int owner_ = -1;
+  std::int64_t block_bytes_;
+  std::int64_t n_rows_ = 0;
+  std::uint64_t* rows_ = nullptr;
+  const float* owner_grad_ = nullptr;
+  const std::uint64_t* owner_rows_ = nullptr;
+  ew_shardmap* map_ = nullptr;
+};
+
+// Ring replica by a full pull of the owner's per-step snapshot (for
+// optimizers the library does not own): the staged copy over NVLink, then
+// kernel (a)'s verification of the replica against the owner's rows, read
+// in the owner's HBM.
+class RingReplica {
+ public:
+  // Collective over `ch`.  layout: the source layout (the packing of every
+  // member's shard); my_snap / my_rows: this rank's snapshot and its rows;
+  // replica: buffer for the owner's shard.
+  RingReplica(Channel& ch, const PartitionLayout& layout, const void* my_snap,
+              const std::uint64_t* my_rows, void* replica, std::int64_t block_bytes = 65536);
+  ~RingReplica();
+  RingReplica(const RingReplica&) = delete;
+  RingReplica& operator=(const RingReplica&) = delete;
+
+  int owner() const { return owner_; }
+  // pull the owner's snapshot into the replica and verify it (*bad_dev)
+  void refresh(std::uint32_t* bad_dev, ew_stream_t stream) const;
+
+ private:
+  PeerBuffers peers_;
+  int owner_ = -1;
+  void* replica_ = nullptr;
+  const std::uint64_t* owner_rows_ = nullptr;
+  ew_shardmap* map_ = nullptr;
+  ew_copy_program* copy_ = nullptr;
+};
+
 // ------------------------------------------------------------ MTTR record
 
 // Reference MttrEvent (sim.hpp:31-45) with measured seconds.

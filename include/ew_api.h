@@ -621,6 +621,31 @@ int ew_inplace_exec_timed_out(const ew_inplace_exec* x, int* timed_out);
 int ew_inplace_exec_info(const ew_inplace_exec* x, int64_t* n_phases, int64_t* stage_alloc);
 void ew_inplace_exec_free(ew_inplace_exec* x);
 
+/* Ring replicas (recovery.hpp ReplayReplica / RingReplica), collective over
+ * a channel of the ring's members.  Replay: the holder applies the owner's
+ * AdamW step to its replica with the owner's gradient shard read from peer
+ * memory (ew_adam_step_rows, replica rows in the same pass); verify compares
+ * those rows with the owner's (reread != 0: recompute the replica's rows from
+ * HBM).  Ring: the holder pulls the owner's snapshot and verifies it against
+ * the owner's rows.  *bad_count (device u32) = mismatching rows. */
+typedef struct ew_replay_replica ew_replay_replica;
+int ew_replay_replica_create(ew_channel* ch, const float* my_grad, const uint64_t* my_rows,
+                             float* master, float* exp_avg, float* exp_avg_sq,
+                             uint16_t* param_bf16, int64_t n, const void* image,
+                             int64_t image_bytes, int64_t block_bytes, ew_replay_replica** out);
+int ew_replay_replica_replay(ew_replay_replica* r, const ew_adam_hyper* hyper, int64_t step,
+                             ew_stream_t stream);
+int ew_replay_replica_verify(const ew_replay_replica* r, uint32_t* bad_count, int reread,
+                             ew_stream_t stream);
+int ew_replay_replica_owner(const ew_replay_replica* r, int* owner);
+void ew_replay_replica_free(ew_replay_replica* r);
+typedef struct ew_ring_replica ew_ring_replica;
+int ew_ring_replica_create(ew_channel* ch, const ew_layout* layout, const void* my_snap,
+                           const uint64_t* my_rows, void* replica, int64_t block_bytes,
+                           ew_ring_replica** out);
+int ew_ring_replica_refresh(const ew_ring_replica* r, uint32_t* bad_count, ew_stream_t stream);
+void ew_ring_replica_free(ew_ring_replica* r);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

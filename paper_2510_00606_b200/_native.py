@@ -313,6 +313,14 @@ _sig("ew_inplace_exec_launch", i32, vp, vp, vp)
 _sig("ew_inplace_exec_timed_out", i32, vp, P(i32))
 _sig("ew_inplace_exec_info", i32, vp, P(i64), P(i64))
 _sig("ew_inplace_exec_free", None, vp)
+_sig("ew_replay_replica_create", i32, vp, vp, vp, vp, vp, vp, vp, i64, vp, i64, i64, P(vp))
+_sig("ew_replay_replica_replay", i32, vp, P(AdamHyper), i64, vp)
+_sig("ew_replay_replica_verify", i32, vp, vp, i32, vp)
+_sig("ew_replay_replica_owner", i32, vp, P(i32))
+_sig("ew_replay_replica_free", None, vp)
+_sig("ew_ring_replica_create", i32, vp, vp, vp, vp, vp, i64, P(vp))
+_sig("ew_ring_replica_refresh", i32, vp, vp, vp)
+_sig("ew_ring_replica_free", None, vp)
 
 def int_array(values) -> C.Array:
     values = list(values)

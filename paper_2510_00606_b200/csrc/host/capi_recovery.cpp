@@ -46,6 +46,12 @@ struct ew_dp_group {
 struct ew_inplace_exec {
   std::unique_ptr<InPlaceExecutor> x;
 };
+struct ew_replay_replica {
+  std::unique_ptr<elaskit::b200::ReplayReplica> r;
+};
+struct ew_ring_replica {
+  std::unique_ptr<elaskit::b200::RingReplica> r;
+};
 
 namespace {
 
@@ -451,5 +457,80 @@ int ew_inplace_exec_info(const ew_inplace_exec* x, int64_t* n_phases, int64_t* s
 }
 
 void ew_inplace_exec_free(ew_inplace_exec* x) { delete x; }
+
+// ------------------------------------------------------------ ring replicas
+
+int ew_replay_replica_create(ew_channel* ch, const float* my_grad, const uint64_t* my_rows,
+                             float* master, float* exp_avg, float* exp_avg_sq,
+                             uint16_t* param_bf16, int64_t n, const void* image,
+                             int64_t image_bytes, int64_t block_bytes, ew_replay_replica** out) {
+  return guarded([&]() -> int {
+    if (ch == nullptr || out == nullptr || !my_grad || !my_rows || !master || !exp_avg ||
+        !exp_avg_sq || !param_bf16 || !image || n < 0 || image_bytes <= 0)
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_replay_replica_create: bad arguments");
+    elaskit::b200::AdamShard a;
+    a.master = master;
+    a.exp_avg = exp_avg;
+    a.exp_avg_sq = exp_avg_sq;
+    a.param_bf16 = param_bf16;
+    a.n = n;
+    a.image = image;
+    a.image_bytes = image_bytes;
+    *out = new ew_replay_replica{
+        std::make_unique<elaskit::b200::ReplayReplica>(*ch->c, my_grad, my_rows, a, block_bytes)};
+    return EW_OK;
+  });
+}
+
+int ew_replay_replica_replay(ew_replay_replica* r, const ew_adam_hyper* hyper, int64_t step,
+                             ew_stream_t stream) {
+  return guarded([&]() -> int {
+    if (r == nullptr || hyper == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    r->r->replay(*hyper, step, stream);
+    return EW_OK;
+  });
+}
+
+int ew_replay_replica_verify(const ew_replay_replica* r, uint32_t* bad_count, int reread,
+                             ew_stream_t stream) {
+  return guarded([&]() -> int {
+    if (r == nullptr || bad_count == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    if (reread)
+      r->r->verify_by_reread(bad_count, stream);
+    else
+      r->r->verify(bad_count, stream);
+    return EW_OK;
+  });
+}
+
+int ew_replay_replica_owner(const ew_replay_replica* r, int* owner) {
+  if (r == nullptr || owner == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+  *owner = r->r->owner();
+  return EW_OK;
+}
+
+void ew_replay_replica_free(ew_replay_replica* r) { delete r; }
+
+int ew_ring_replica_create(ew_channel* ch, const ew_layout* layout, const void* my_snap,
+                           const uint64_t* my_rows, void* replica, int64_t block_bytes,
+                           ew_ring_replica** out) {
+  return guarded([&]() -> int {
+    if (ch == nullptr || layout == nullptr || out == nullptr || !my_snap || !my_rows || !replica)
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_ring_replica_create: bad arguments");
+    *out = new ew_ring_replica{std::make_unique<elaskit::b200::RingReplica>(
+        *ch->c, layout->layout, my_snap, my_rows, replica, block_bytes)};
+    return EW_OK;
+  });
+}
+
+int ew_ring_replica_refresh(const ew_ring_replica* r, uint32_t* bad_count, ew_stream_t stream) {
+  return guarded([&]() -> int {
+    if (r == nullptr || bad_count == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    r->r->refresh(bad_count, stream);
+    return EW_OK;
+  });
+}
+
+void ew_ring_replica_free(ew_ring_replica* r) { delete r; }
 
 }  // extern "C"

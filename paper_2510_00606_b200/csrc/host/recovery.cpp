@@ -333,6 +333,7 @@ int index_of(const std::vector<int>& v, int x) {
 
 // PeerBuffers keys beyond the BufRole values
 constexpr int kLanded = 10, kOldBlocks = 11, kReplicaBlocks = 12, kFlags = 13;
+constexpr int kGrad = 20, kRows = 21, kSnap = 22;
 
 // Slice [lo, hi) (even) of n_words owned by survivor i of k.
 std::pair<std::int64_t, std::int64_t> slice_of(std::int64_t n_words, int i, int k) {
@@ -593,6 +594,83 @@ void BlockVerifier::set(const std::vector<const std::uint64_t*>& plus,
 
 void BlockVerifier::run(ew_stream_t stream, std::uint32_t* bad_dev) const {
   check(ew_block_verifier_run(v_, bad_dev, stream));
+}
+
+// ------------------------------------------------------------ ring replicas
+
+namespace {
+int ring_successor(const std::vector<int>& members, int me) {
+  const int i = index_of(members, me);
+  return members[static_cast<std::size_t>((i + 1) % static_cast<int>(members.size()))];
+}
+}  // namespace
+
+ReplayReplica::ReplayReplica(Channel& ch, const float* my_grad, const std::uint64_t* my_rows,
+                             AdamShard replica, std::int64_t block_bytes)
+    : rep_(replica), block_bytes_(block_bytes) {
+  if (ch.members().size() < 2) throw std::invalid_argument("a ring needs two members");
+  owner_ = ring_successor(ch.members(), ch.me());
+  n_rows_ = (rep_.image_bytes + block_bytes - 1) / block_bytes;
+  rows_ = dalloc<std::uint64_t>(2 * std::max<std::int64_t>(1, n_rows_));
+  const ew_segment seg{0, rep_.image_bytes, 0};
+  check(ew_shardmap_create(&seg, 1, block_bytes, &map_));
+  peers_.exchange(ch, {{kGrad, const_cast<float*>(my_grad)},
+                       {kRows, const_cast<std::uint64_t*>(my_rows)}},
+                  [&](int, int member) { return member == owner_; });
+  owner_grad_ = static_cast<const float*>(peers_.get(kGrad, owner_));
+  owner_rows_ = static_cast<const std::uint64_t*>(peers_.get(kRows, owner_));
+  if (owner_grad_ == nullptr || owner_rows_ == nullptr)
+    throw std::runtime_error("the owner's gradient shard / rows are not mapped");
+}
+
+ReplayReplica::~ReplayReplica() {
+  peers_.close();
+  ew_shardmap_free(map_);
+  dfree(rows_);
+}
+
+void ReplayReplica::replay(const ew_adam_hyper& hyper, std::int64_t step, ew_stream_t stream) {
+  check(ew_adam_step_rows(owner_grad_, rep_.master, rep_.exp_avg, rep_.exp_avg_sq,
+                          rep_.param_bf16, rep_.n, &hyper, step, rep_.image, rep_.image_bytes,
+                          block_bytes_, rows_, stream));
+}
+
+void ReplayReplica::verify(std::uint32_t* bad_dev, ew_stream_t stream) const {
+  // the owner's rows are read where they are (its HBM, over NVLink): 2.9 MB at 7B
+  check(ew_rows_diff(rows_, owner_rows_, n_rows_, bad_dev, stream));
+}
+
+void ReplayReplica::verify_by_reread(std::uint32_t* bad_dev, ew_stream_t stream) const {
+  check(ew_verify(map_, rep_.image, owner_rows_, bad_dev, nullptr, 0, stream));
+}
+
+RingReplica::RingReplica(Channel& ch, const PartitionLayout& layout, const void* my_snap,
+                         const std::uint64_t* my_rows, void* replica, std::int64_t block_bytes)
+    : replica_(replica) {
+  if (ch.members().size() < 2) throw std::invalid_argument("a ring needs two members");
+  owner_ = ring_successor(ch.members(), ch.me());
+  map_ = make_map(shard_segments(layout, owner_), block_bytes);
+  peers_.exchange(ch, {{kSnap, const_cast<void*>(my_snap)},
+                       {kRows, const_cast<std::uint64_t*>(my_rows)}},
+                  [&](int, int member) { return member == owner_; });
+  const void* src = peers_.get(kSnap, owner_);
+  owner_rows_ = static_cast<const std::uint64_t*>(peers_.get(kRows, owner_));
+  if (src == nullptr || owner_rows_ == nullptr)
+    throw std::runtime_error("the owner's snapshot / rows are not mapped");
+  const std::int64_t bytes = ew_shardmap_bytes(map_);
+  const int remote = 1;
+  check(ew_copy_program_create_raw(&src, &replica_, &bytes, &remote, 1, &copy_));
+}
+
+RingReplica::~RingReplica() {
+  ew_copy_program_free(copy_);
+  peers_.close();
+  ew_shardmap_free(map_);
+}
+
+void RingReplica::refresh(std::uint32_t* bad_dev, ew_stream_t stream) const {
+  check(ew_copy_program_launch(copy_, 0, 0, stream));
+  check(ew_verify(map_, replica_, owner_rows_, bad_dev, nullptr, 0, stream));
 }
 
 // ------------------------------------------------------------------ MTTR

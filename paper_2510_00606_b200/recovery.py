@@ -103,129 +103,126 @@ MTTR_CSV_HEADER = _csv_header()
 
 
 class RingReplica:
-    """Per-step ring replica maintenance on the holder.
+    """Per-step ring replica maintenance by a full pull —
+    a binding of the C++ elaskit::b200::RingReplica (ew_ring_replica).
 
     The paper keeps member (i+1)'s optimizer partition in member i's host
     memory and replays the Adam step there from a pushed gradient shard
     (modelled by SnapshotTimeline, param_fabric.hpp:86-96).
-    On B200 the holder keeps the replica in its own HBM and, after each
-    optimizer step, pulls the owner's updated shard over NVLink with the
-    TMA-staged copy (11.79 GB of 7B state in ~16 ms at ~720 GB/s, overlapped
-    with the next forward), then re-checksums the replica and compares it
-    with the owner's snapshot rows: bit-exact by construction, verified
-    without a second transfer, no optimizer replay.  The replica is packed
-    like the owner's shard, so the owner's segment map and rows apply as is.
-    """
+    For optimizers the library does not own, the holder pulls the owner's
+    per-step snapshot with the staged copy over NVLink (11.79 GB of 7B state
+    in ~16 ms) and verifies the replica against the owner's checksum rows,
+    read in the owner's HBM: bit-exact by construction, verified without a
+    second transfer.  The replica is packed like the owner's shard."""
 
     def __init__(self, layout, ring_members: Sequence[int], rank: int, replica: torch.Tensor,
                  snap: torch.Tensor, rows: torch.Tensor, block_bytes: int = dev.DEFAULT_BLOCK_BYTES,
                  group=None):
         """`snap`/`rows`: this rank's own per-step snapshot and its checksum
-        rows (exported to its holder; the snapshot stays stable while the
-        live state moves on to the next step); `replica`: buffer for the
-        shard this rank backs up."""
-        live = snap
+        rows (the holder reads them; the snapshot stays stable while the live
+        state moves on to the next step); `replica`: buffer for the shard
+        this rank backs up.  Collective over `group` (the ring's members)."""
         from .fabric import SnapshotRing
-        ring = SnapshotRing(list(ring_members))
         self.rank = rank
-        self.owner = ring.backs_up(rank)
+        self.owner = SnapshotRing(list(ring_members)).backs_up(rank)
         self.map = shard_map(layout, self.owner, block_bytes)
         self.replica = replica
-        world = dist.get_world_size(group)
-        mine = (dev.ipc_handle(live), dev.ipc_handle(rows))
-        allh = [None] * world
-        dist.all_gather_object(allh, (rank, mine), group=group)
-        handles = dict(allh)
-        (h_live, o_live), (h_rows, o_rows) = handles[self.owner]
-        self._opened = [dev.ipc_open(h_live, o_live), dev.ipc_open(h_rows, o_rows)]
-        n = self.map.nbytes
-        self.copy = dev.CopyProgram.from_pointers([self._opened[0]], [replica.data_ptr()], [n], [True])
-        self.owner_rows = torch.empty(2 * max(1, self.map.num_rows), dtype=torch.int64, device="cuda")
-        self.rows_copy = dev.CopyProgram.from_pointers([self._opened[1]], [self.owner_rows.data_ptr()],
-                                                       [16 * self.map.num_rows], [True])
+        self.channel = Channel.from_group(group, "ring")
+        if self.channel.members != sorted(ring_members):
+            raise ValueError("the group's ranks must be the ring's members")
+        h = C.c_void_p()
+        check(lib.ew_ring_replica_create(self.channel.handle, layout.handle,
+                                         C.c_void_p(snap.data_ptr()), C.c_void_p(rows.data_ptr()),
+                                         C.c_void_p(replica.data_ptr()), int(block_bytes),
+                                         C.byref(h)))
+        self._h = h
+        self._keep = (snap, rows, layout)
         self.bad = torch.zeros(1, dtype=torch.int32, device="cuda")
 
     def refresh(self, stream=None) -> None:
-        """Pull the owner's shard and its checksum rows, then verify the
-        replica (bad count in self.bad).  The owner must not be writing its
-        live shard meanwhile (call between its optimizer step and the next)."""
-        self.copy.launch(stream=stream)
-        self.rows_copy.launch(stream=stream)
-        dev.verify(self.map, self.replica, self.owner_rows, self.bad, stream=stream)
+        """Pull the owner's snapshot and verify the replica against the
+        owner's rows (bad count in self.bad).  The owner must not be writing
+        its snapshot meanwhile."""
+        check(lib.ew_ring_replica_refresh(self._h, dev._ptr(self.bad), dev._stream(stream)))
 
     def close(self) -> None:
-        self.copy = self.rows_copy = None
-        for p in self._opened:
-            dev.ipc_close(p)
-        self._opened = []
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
+            lib.ew_ring_replica_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 class ReplayReplica:
-    """Ring replica kept by optimizer replay: the paper's own mechanism
-     with the replica in the holder's HBM.
+    """Ring replica kept by optimizer replay — the paper's own mechanism
+     with the replica in the holder's HBM; a binding of the
+    C++ elaskit::b200::ReplayReplica (ew_replay_replica).
 
     Each step the owner reduces its gradient shard and runs ew_adam_step on
-    its AdamState; the holder runs the same ew_adam_step on its replica with
-    the gradient read out of the owner's HBM through an IPC peer pointer —
-    4 B/param cross NVLink instead of the 14 B/param a full state pull
-    (RingReplica) moves.  The replica stays byte-identical because both sides
-    execute the same explicitly-rounded kernel on the same inputs; verify()
-    proves it against the owner's checksum rows without a second transfer.
-    Ordering contract: the owner must not overwrite its gradient shard before
-    the holder's replay of that step finished (a barrier between the replay
-    and the next step's reduce)."""
+    its AdamState (with its checksum rows fused); the holder runs the same
+    ew_adam_step on its replica with the gradient read out of the owner's HBM
+    through an IPC peer pointer — 4 B/param cross NVLink instead of the
+    14 B/param a full state pull (RingReplica) moves.  The replica stays
+    byte-identical because both sides execute the same explicitly-rounded
+    kernel on the same inputs; verify() proves it against the owner's rows
+    without a second transfer.  Ordering contract: the owner must not
+    overwrite its gradient shard before the holder's replay of that step
+    finished (a barrier between the replay and the next step's reduce)."""
 
     def __init__(self, ring_members: Sequence[int], rank: int, replica: "dev.AdamState",
                  grad: torch.Tensor, rows: torch.Tensor,
                  block_bytes: int = dev.DEFAULT_BLOCK_BYTES, group=None):
         """`grad`/`rows`: THIS rank's gradient shard and the checksum rows of
-        its own AdamState (exported to its holder); `replica`: the AdamState
-        of the member this rank backs up (same n as that member's shard)."""
+        its own AdamState (read by its holder); `replica`: the AdamState of
+        the member this rank backs up.  Collective over `group`."""
         from .fabric import SnapshotRing
-        ring = SnapshotRing(list(ring_members))
         self.rank = rank
-        self.owner = ring.backs_up(rank)
+        self.owner = SnapshotRing(list(ring_members)).backs_up(rank)
         self.replica = replica
         self.map = dev.ShardMap(replica.segments(), block_bytes)
-        world = dist.get_world_size(group)
-        allh = [None] * world
-        dist.all_gather_object(allh, (rank, (dev.ipc_handle(grad), dev.ipc_handle(rows))),
-                               group=group)
-        (h_g, o_g), (h_r, o_r) = dict(allh)[self.owner]
-        self._opened = [dev.ipc_open(h_g, o_g), dev.ipc_open(h_r, o_r)]
         self.block_bytes = block_bytes
-        self.owner_rows = torch.empty(2 * max(1, self.map.num_rows), dtype=torch.int64,
-                                      device="cuda")
-        self.replica_rows = torch.empty_like(self.owner_rows)
-        self.rows_copy = dev.CopyProgram.from_pointers([self._opened[1]],
-                                                       [self.owner_rows.data_ptr()],
-                                                       [16 * self.map.num_rows], [True])
+        self.channel = Channel.from_group(group, "replay")
+        if self.channel.members != sorted(ring_members):
+            raise ValueError("the group's ranks must be the ring's members")
+        p = lambda t: C.c_void_p(t.data_ptr())  # noqa: E731
+        h = C.c_void_p()
+        check(lib.ew_replay_replica_create(
+            self.channel.handle, p(grad), p(rows), p(replica.master), p(replica.exp_avg),
+            p(replica.exp_avg_sq), p(replica.param), int(replica.n), p(replica.buf),
+            int(replica.nbytes), int(block_bytes), C.byref(h)))
+        self._h = h
+        self._keep = (grad, rows)
         self.bad = torch.zeros(1, dtype=torch.int32, device="cuda")
 
     def replay(self, hyper, step: int, stream=None) -> None:
         """Apply the owner's step `step` to the replica: gradient pulled over
         NVLink, update and the replica's checksum rows in one pass."""
-        dev.adam_step(self._opened[0], self.replica, hyper, step, stream=stream,
-                      rows=self.replica_rows, block_bytes=self.block_bytes)
+        check(lib.ew_replay_replica_replay(self._h, C.byref(hyper), int(step),
+                                           dev._stream(stream)))
 
     def verify(self, stream=None) -> None:
-        """Compare the replica's rows (from replay) with the owner's rows
-        (published by the owner's own fused step, pulled: 2.9 MB at 7B);
-        mismatching rows counted in self.bad.  No re-read of the replica."""
-        self.rows_copy.launch(stream=stream)
-        dev.rows_diff(self.replica_rows, self.owner_rows, self.map.num_rows, self.bad,
-                      stream=stream)
+        """Compare the replica's rows (from replay) with the owner's rows, read
+        in the owner's HBM (2.9 MB at 7B); mismatching rows in self.bad."""
+        check(lib.ew_replay_replica_verify(self._h, dev._ptr(self.bad), 0, dev._stream(stream)))
 
     def verify_by_reread(self, stream=None) -> None:
         """Stronger check: recompute the replica's rows from HBM."""
-        self.rows_copy.launch(stream=stream)
-        dev.verify(self.map, self.replica.buf, self.owner_rows, self.bad, stream=stream)
+        check(lib.ew_replay_replica_verify(self._h, dev._ptr(self.bad), 1, dev._stream(stream)))
 
     def close(self) -> None:
-        self.rows_copy = None
-        for p in self._opened:
-            dev.ipc_close(p)
-        self._opened = []
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
+            lib.ew_replay_replica_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
 
 
 class PreparedRecovery:
