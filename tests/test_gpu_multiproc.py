@@ -134,6 +134,33 @@ def _worker(rank, world, port, out_dir, scale):
         dist.barrier()
         grp.close()
 
+        # ---- two non-adjacent members leave at once (ScaleIn), planned at
+        # failure time: integrity_check passes (their holders survive), the
+        # copy sources both departed shards from their ring holders
+        from paper_2510_00606_b200.fabric import SCALE_IN, SCALE_OUT
+        gone = [0, 2]
+        survivors = [m for m in members if m not in gone]
+        rp = ReshardPlan.build(cfg.layer_bytes, members, survivors)
+        grp = DpGroup(cfg.layer_bytes, members, rank, None)
+        holds = rp.replica_of(rank) in gone
+        bufs = RankBuffers(live, replica if holds else None,
+                           dev.empty_bytes(rp.dst.shard_bytes(rank)) if rank in survivors else None)
+        dist.barrier()
+        if rank in survivors:
+            try:
+                grp.recover([1], bufs, kind=SCALE_OUT)
+                rep["scale-out rejected"] = False
+            except ValueError:
+                rep["scale-out rejected"] = True
+            ev = grp.recover(gone, bufs, step=9, kind=SCALE_IN)
+            n = rp.dst.shard_bytes(rank)
+            exp = _fill_expected(dev, shard_map, rp.dst, rank, 31, n)
+            rep["two departures verified"] = ev.verified
+            rep["two departures bytes"] = bool(torch.equal(bufs.new[:n], exp[:n]))
+            rep["two departures kind"] = ev.kind == "scale_in"
+        dist.barrier()
+        grp.close()
+
         # ---- staged in-place reshard (C++ InPlaceExecutor): departures and a rejoin
         from paper_2510_00606_b200.inplace import StagedInPlaceReshard
         nblk = (cfg.total_bytes + block - 1) // block
