@@ -1248,6 +1248,132 @@ def run_layer_migration(args, rank, world, out):
 
 # ------------------------------------------------------------- (c) and (d) ---
 
+def run_config_a(args, rank, world, out):
+    """Config A (BASELINE configs[0], the reference's CPU-runnable case):
+    125M params x 12 B (fp32 param + Adam m, v) interleaved over 4 ranks,
+    rank 1 leaves.  On one GPU: every rank's shard snapshot + verify, the
+    4 -> 3 reshard with every receiver's verified pull program (buffers side
+    by side), checksum conservation and bytes against the target layout, and
+    the config's dropout masks (seed 0, keep 0.5)."""
+    import torch
+    from paper_2510_00606_b200 import configs, device as dev
+    from paper_2510_00606_b200.reshard import ReshardPlan, emulate_on_one_gpu, shard_map
+
+    cfg = configs.gpt_125m()
+    block = args.block_bytes
+    rp = ReshardPlan.build(cfg.layer_bytes, [0, 1, 2, 3], [0, 2, 3])
+    t_snap = 0.0
+    ok = True
+    for r in rp.old_ranks:
+        m = shard_map(rp.src, r, block)
+        live, snap = dev.empty_bytes(m.nbytes), dev.empty_bytes(m.nbytes)
+        rows = m.new_row_sums()
+        bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+        dev.fill_synthetic(m, live, 0)
+        dev.snapshot(m, live, snap, rows)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        dev.snapshot(m, live, snap, rows)
+        dev.verify(m, snap, rows, bad)
+        e.record()
+        torch.cuda.synchronize()
+        t_snap += s.elapsed_time(e) / 1e3
+        ok = ok and int(bad.item()) == 0
+    nblocks = (cfg.total_bytes + block - 1) // block
+    sums = torch.zeros(2 * nblocks, dtype=torch.int64, device="cuda")
+    emulate_on_one_gpu(rp, seed=0, push=False, block_sums=sums)  # warm-up
+    sums.zero_()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    got, expected = emulate_on_one_gpu(rp, seed=0, push=False, block_sums=sums)
+    e.record()
+    torch.cuda.synchronize()
+    whole = torch.zeros_like(sums)
+    for r in rp.old_ranks:   # the source's block sums (every rank's snapshot rows)
+        m = shard_map(rp.src, r, block)
+        buf = dev.empty_bytes(m.nbytes)
+        dev.fill_synthetic(m, buf, 0)
+        rows = m.new_row_sums()
+        dev.checksum(m, buf, rows)
+        dev.rows_to_blocks(m, rows, whole)
+    torch.cuda.synchronize()
+    conserved = bool(torch.equal(whole, sums))
+    exact = all(torch.equal(got[r][:rp.dst.shard_bytes(r)], expected[r][:rp.dst.shard_bytes(r)])
+                for r in rp.new_ranks)
+    tr = rp.traffic()
+    bits = dev.dropout_mask(0, 0, 16, 1, 0, 768 * 2048, 0.5)
+    torch.cuda.synchronize()
+    out["config_a"] = {
+        "workload": "125M-param fp32+Adam state (1.484 GB), interleaved ZeRO over 4 ranks, "
+                    "drop rank 1; all ranks' buffers on one GPU",
+        "state_bytes": cfg.total_bytes, "snapshot_verify_all_ranks_ms": round(t_snap * 1e3, 3),
+        "snapshot_verified": ok, "plan_entries": len(rp.plan),
+        "total_bytes_moved": tr["total_bytes_moved"],
+        "reshard_all_programs_one_gpu_ms": round(s.elapsed_time(e), 3),
+        "reshard_verified_on_arrival": conserved, "reshard_bytes_exact": exact,
+        "masks": {"samples": 16, "elements_per_sample": 768 * 2048, "keep": 0.5,
+                  "kept_fraction": round(float(torch.stack([((bits >> b) & 1).sum()
+                                                            for b in range(32)]).sum().item())
+                                         / (16 * 768 * 2048), 4)}}
+    del got, expected, sums, whole
+    torch.cuda.empty_cache()
+
+
+def run_config_d_snapshot(args, rank, world, out):
+    """Config D's snapshot + verify on one GPU: ZeRO state sized to fill HBM
+    (live S + snapshot S of the 191.5 GB; S = 86 GB of an 8-way interleaved
+    80-layer state), steps timed like the headline leg, one flipped bit must
+    be caught."""
+    import torch
+    from paper_2510_00606_b200 import configs, device as dev, fabric
+
+    torch.cuda.empty_cache()
+    free = torch.cuda.mem_get_info()[0]
+    S_target = min(86_000_000_000, int((free - (4 << 30)) / 2))
+    if S_target < 40_000_000_000:
+        out["config_d_snapshot"] = {"skipped": f"only {free / 1e9:.1f} GB free"}
+        return
+    cfg = configs.fill_hbm(8, S_target)
+    layout = fabric.interleaved_layout(cfg.layer_bytes, range(8))
+    m = dev.ShardMap(layout.segments(3), args.block_bytes)
+    S = layout.shard_bytes(3)
+    live, snap = dev.empty_bytes(S), dev.empty_bytes(S)
+    rows = m.new_row_sums()
+    bad = torch.zeros(1, dtype=torch.int32, device="cuda")
+    dev.fill_synthetic(m, live, 7)
+    dev.snapshot(m, live, snap, rows)
+    dev.verify(m, snap, rows, bad)
+    torch.cuda.synchronize()
+    ok = int(bad.item()) == 0
+    reps = 3
+    s, mid, e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+    t_snap = t_ver = 0.0
+    for _ in range(reps):
+        s.record()
+        dev.snapshot(m, live, snap, rows)
+        mid.record()
+        dev.verify(m, snap, rows, bad)
+        e.record()
+        torch.cuda.synchronize()
+        t_snap += s.elapsed_time(mid) / 1e3 / reps
+        t_ver += mid.elapsed_time(e) / 1e3 / reps
+        ok = ok and int(bad.item()) == 0
+    snap[S // 3] ^= 0x40
+    dev.verify(m, snap, rows, bad)
+    torch.cuda.synchronize()
+    caught = int(bad.item()) == 1
+    used = torch.cuda.mem_get_info()
+    out["config_d_snapshot"] = {
+        "workload": "config D fill-HBM: one rank's shard of an 8-way interleaved 80-layer state",
+        "shard_bytes": S, "resident_gb": round((used[1] - used[0]) / 1e9, 1),
+        "snapshot_ms": round(t_snap * 1e3, 2), "verify_ms": round(t_ver * 1e3, 2),
+        "step_gbs": round(3 * S / (t_snap + t_ver) / 1e9, 1),
+        "snapshot_gbs": round(2 * S / t_snap / 1e9, 1),
+        "verified": ok, "flipped_bit_caught": caught}
+    del live, snap, rows
+    torch.cuda.empty_cache()
+
+
 def run_philox(args, rank, world, out):
     import torch
     from paper_2510_00606_b200 import device as dev, fabric
@@ -1583,6 +1709,12 @@ def bench_b200(args):
     if "reduce" not in skip:
         trace("reduce")
         run_reduce(args, rank, world, out)
+    if world == 1 and "config_a" not in skip:
+        trace("config_a")
+        run_config_a(args, rank, world, out)
+    if world == 1 and "config_d" not in skip:
+        trace("config_d_snapshot")
+        run_config_d_snapshot(args, rank, world, out)
     if world == 1 and rank == 0 and "cpu" not in skip:
         trace("cpu_beside")
         run_cpu_beside(args, out)  # cpu_baseline leg, continued
