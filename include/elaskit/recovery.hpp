@@ -301,6 +301,58 @@ class RingReplica {
   ew_copy_program* copy_ = nullptr;
 };
 
+// ------------------------------------------------- (d) over peer memory
+
+// The gradient-scale-preserving weighted reduce fused with
+// its collective over peer memory — no NCCL: each rank quantises its slice
+// of every rank's contribution units (read from peer HBM, TMA-staged) and
+// sums int64 (reduce-scatter), then pulls the other slices (all-gather),
+// between stream-ordered device barriers.  The fixed-point scale comes from
+// the global absmax (a local kernel, then one double per rank over the
+// channel).  Bit-identical to the NCCL int64 path and to one GPU folding
+// every unit, for any world size and split.  Reference: weighted_grad_average
+// (dataflow.cpp:71-83), the toy fold (sim.cpp:901-953).
+class PeerReduce {
+ public:
+  // fp32 units: this rank's units (n elements each) and weights, and its fp32
+  // output.  Collective over `ch`.
+  PeerReduce(Channel& ch, const std::vector<const float*>& units,
+             const std::vector<double>& weights, float* out, std::int64_t n,
+             double barrier_timeout_s = 30.0);
+  // int64 accumulators: each rank folded its own units into `acc`
+  // (ew_weighted_fold, accumulate=1); the collective sums accumulators.
+  PeerReduce(Channel& ch, const std::int64_t* acc, float* out, std::int64_t n,
+             double barrier_timeout_s = 30.0);
+  ~PeerReduce();
+  PeerReduce(const PeerReduce&) = delete;
+  PeerReduce& operator=(const PeerReduce&) = delete;
+
+  std::int64_t total_units() const { return total_units_; }
+  // fixed-point bits of the global unit set (fp32-unit form): the local
+  // weighted absmax, the max over ranks, ew_fixed_point_bits.  Synchronises
+  // `stream` once.
+  int scale(ew_stream_t stream);
+  // barrier -> reduce-scatter -> barrier -> all-gather, all stream-ordered
+  void run(int frac_bits, ew_stream_t stream);
+  // trailing barrier: nobody frees buffers a peer may still read
+  void wait(ew_stream_t stream);
+  bool timed_out() const;
+
+ private:
+  void connect(Channel& ch, std::map<int, void*> mine, const std::string& extra);
+  Channel& ch_;
+  std::int64_t n_ = 0;
+  std::int64_t total_units_ = 0;
+  std::vector<const float*> units_;
+  std::vector<double> weights_;
+  PeerBuffers peers_;
+  ew_peer_fold* fold_ = nullptr;
+  ew_peer_barrier* barrier_ = nullptr;
+  unsigned long long* flags_ = nullptr;
+  double* dmax_ = nullptr;
+  double timeout_s_;
+};
+
 // ------------------------------------------------------------ MTTR record
 
 // Reference MttrEvent (sim.hpp:31-45) with measured seconds.

@@ -646,6 +646,26 @@ int ew_ring_replica_create(ew_channel* ch, const ew_layout* layout, const void* 
 int ew_ring_replica_refresh(const ew_ring_replica* r, uint32_t* bad_count, ew_stream_t stream);
 void ew_ring_replica_free(ew_ring_replica* r);
 
+/* (d) fused with its collective over peer memory, through the rendezvous
+ * (recovery.hpp PeerReduce): collective over a channel; each rank passes its
+ * own units (or its int64 accumulator) and output; the library exchanges the
+ * IPC handles and weights, builds the peer fold and a device barrier.
+ * scale(): local absmax, max over ranks (one double each over the channel),
+ * fixed-point bits of the global unit set (synchronises the stream once).
+ * run(): barrier -> reduce-scatter -> barrier -> all-gather, stream-ordered.
+ * wait(): a trailing barrier before any rank frees its buffers. */
+typedef struct ew_peer_reduce ew_peer_reduce;
+int ew_peer_reduce_create(ew_channel* ch, const float* const* units, const double* weights,
+                          int n_units, float* out, int64_t n, double barrier_timeout_s,
+                          ew_peer_reduce** handle);
+int ew_peer_reduce_create_i64(ew_channel* ch, const int64_t* acc, float* out, int64_t n,
+                              double barrier_timeout_s, ew_peer_reduce** handle);
+int ew_peer_reduce_scale(ew_peer_reduce* r, ew_stream_t stream, int* frac_bits);
+int ew_peer_reduce_run(ew_peer_reduce* r, int frac_bits, ew_stream_t stream);
+int ew_peer_reduce_wait(ew_peer_reduce* r, ew_stream_t stream);
+int ew_peer_reduce_info(const ew_peer_reduce* r, int64_t* total_units, int* timed_out);
+void ew_peer_reduce_free(ew_peer_reduce* r);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -321,6 +321,13 @@ _sig("ew_replay_replica_free", None, vp)
 _sig("ew_ring_replica_create", i32, vp, vp, vp, vp, vp, i64, P(vp))
 _sig("ew_ring_replica_refresh", i32, vp, vp, vp)
 _sig("ew_ring_replica_free", None, vp)
+_sig("ew_peer_reduce_create", i32, vp, P(vp), P(f64), i32, vp, i64, f64, P(vp))
+_sig("ew_peer_reduce_create_i64", i32, vp, vp, vp, i64, f64, P(vp))
+_sig("ew_peer_reduce_scale", i32, vp, vp, P(i32))
+_sig("ew_peer_reduce_run", i32, vp, i32, vp)
+_sig("ew_peer_reduce_wait", i32, vp, vp)
+_sig("ew_peer_reduce_info", i32, vp, P(i64), P(i32))
+_sig("ew_peer_reduce_free", None, vp)
 
 def int_array(values) -> C.Array:
     values = list(values)

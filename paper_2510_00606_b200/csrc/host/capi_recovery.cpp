@@ -52,6 +52,9 @@ struct ew_replay_replica {
 struct ew_ring_replica {
   std::unique_ptr<elaskit::b200::RingReplica> r;
 };
+struct ew_peer_reduce {
+  std::unique_ptr<elaskit::b200::PeerReduce> r;
+};
 
 namespace {
 
@@ -532,5 +535,67 @@ int ew_ring_replica_refresh(const ew_ring_replica* r, uint32_t* bad_count, ew_st
 }
 
 void ew_ring_replica_free(ew_ring_replica* r) { delete r; }
+
+// ------------------------------------------------------- (d) over peers
+
+int ew_peer_reduce_create(ew_channel* ch, const float* const* units, const double* weights,
+                          int n_units, float* out, int64_t n, double barrier_timeout_s,
+                          ew_peer_reduce** handle) {
+  return guarded([&]() -> int {
+    if (ch == nullptr || handle == nullptr || out == nullptr || n_units < 0 || n < 0 ||
+        (n_units > 0 && (!units || !weights)))
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_peer_reduce_create: bad arguments");
+    *handle = new ew_peer_reduce{std::make_unique<elaskit::b200::PeerReduce>(
+        *ch->c, std::vector<const float*>(units, units + n_units),
+        std::vector<double>(weights, weights + n_units), out, n, barrier_timeout_s)};
+    return EW_OK;
+  });
+}
+
+int ew_peer_reduce_create_i64(ew_channel* ch, const int64_t* acc, float* out, int64_t n,
+                              double barrier_timeout_s, ew_peer_reduce** handle) {
+  return guarded([&]() -> int {
+    if (ch == nullptr || handle == nullptr || out == nullptr || acc == nullptr || n < 0)
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_peer_reduce_create_i64: bad arguments");
+    *handle = new ew_peer_reduce{
+        std::make_unique<elaskit::b200::PeerReduce>(*ch->c, acc, out, n, barrier_timeout_s)};
+    return EW_OK;
+  });
+}
+
+int ew_peer_reduce_scale(ew_peer_reduce* r, ew_stream_t stream, int* frac_bits) {
+  return guarded([&]() -> int {
+    if (r == nullptr || frac_bits == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    *frac_bits = r->r->scale(stream);
+    return EW_OK;
+  });
+}
+
+int ew_peer_reduce_run(ew_peer_reduce* r, int frac_bits, ew_stream_t stream) {
+  return guarded([&]() -> int {
+    if (r == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    r->r->run(frac_bits, stream);
+    return EW_OK;
+  });
+}
+
+int ew_peer_reduce_wait(ew_peer_reduce* r, ew_stream_t stream) {
+  return guarded([&]() -> int {
+    if (r == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    r->r->wait(stream);
+    return EW_OK;
+  });
+}
+
+int ew_peer_reduce_info(const ew_peer_reduce* r, int64_t* total_units, int* timed_out) {
+  return guarded([&]() -> int {
+    if (r == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    if (total_units) *total_units = r->r->total_units();
+    if (timed_out) *timed_out = r->r->timed_out() ? 1 : 0;
+    return EW_OK;
+  });
+}
+
+void ew_peer_reduce_free(ew_peer_reduce* r) { delete r; }
 
 }  // extern "C"

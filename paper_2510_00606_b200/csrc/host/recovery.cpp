@@ -334,6 +334,7 @@ int index_of(const std::vector<int>& v, int x) {
 // PeerBuffers keys beyond the BufRole values
 constexpr int kLanded = 10, kOldBlocks = 11, kReplicaBlocks = 12, kFlags = 13;
 constexpr int kGrad = 20, kRows = 21, kSnap = 22;
+constexpr int kOut = 30, kAcc = 31, kUnit0 = 100;  // units: kUnit0 + k
 
 // Slice [lo, hi) (even) of n_words owned by survivor i of k.
 std::pair<std::int64_t, std::int64_t> slice_of(std::int64_t n_words, int i, int k) {
@@ -671,6 +672,139 @@ RingReplica::~RingReplica() {
 void RingReplica::refresh(std::uint32_t* bad_dev, ew_stream_t stream) const {
   check(ew_copy_program_launch(copy_, 0, 0, stream));
   check(ew_verify(map_, replica_, owner_rows_, bad_dev, nullptr, 0, stream));
+}
+
+// ------------------------------------------------- (d) over peer memory
+
+PeerReduce::PeerReduce(Channel& ch, const std::vector<const float*>& units,
+                       const std::vector<double>& weights, float* out, std::int64_t n,
+                       double barrier_timeout_s)
+    : ch_(ch), n_(n), units_(units), weights_(weights), timeout_s_(barrier_timeout_s) {
+  if (units.size() != weights.size()) throw std::invalid_argument("one weight per unit");
+  std::map<int, void*> mine = {{kOut, out}};
+  for (std::size_t k = 0; k < units.size(); ++k)
+    mine[kUnit0 + static_cast<int>(k)] = const_cast<float*>(units[k]);
+  // the weights travel with the handles: n, count, then the doubles
+  std::string extra(sizeof(std::int64_t) * 2 + 8 * weights.size(), '\0');
+  const std::int64_t hdr[2] = {n, static_cast<std::int64_t>(units.size())};
+  std::memcpy(extra.data(), hdr, sizeof(hdr));
+  if (!weights.empty()) std::memcpy(extra.data() + sizeof(hdr), weights.data(), 8 * weights.size());
+  connect(ch, mine, extra);
+}
+
+PeerReduce::PeerReduce(Channel& ch, const std::int64_t* acc, float* out, std::int64_t n,
+                       double barrier_timeout_s)
+    : ch_(ch), n_(n), timeout_s_(barrier_timeout_s) {
+  std::string extra(sizeof(std::int64_t) * 2, '\0');
+  const std::int64_t hdr[2] = {n, -1};
+  std::memcpy(extra.data(), hdr, sizeof(hdr));
+  connect(ch, {{kOut, out}, {kAcc, const_cast<std::int64_t*>(acc)}}, extra);
+}
+
+void PeerReduce::connect(Channel& ch, std::map<int, void*> mine, const std::string& extra) {
+  const int world = static_cast<int>(ch.members().size());
+  try {
+    flags_ = dalloc<unsigned long long>(std::max(2, world));
+    dmax_ = dalloc<double>(1);
+    check(ew_memset_async(flags_, 0, 8 * std::max(2, world), nullptr));
+    check(ew_device_sync());
+    mine[kFlags] = flags_;
+    peers_.exchange(ch, mine);
+    const std::vector<std::string> meta = ch.allgather(extra);
+    std::vector<const float*> unit_ptrs;
+    std::vector<double> unit_w;
+    std::vector<const std::int64_t*> acc_ptrs;
+    std::vector<float*> out_ptrs;
+    for (std::size_t i = 0; i < meta.size(); ++i) {
+      const int m = ch.members()[i];
+      std::int64_t hdr[2];
+      std::memcpy(hdr, meta[i].data(), sizeof(hdr));
+      if (hdr[0] != n_)
+        throw DimensionMismatch("ranks disagree on the gradient length");
+      out_ptrs.push_back(static_cast<float*>(peers_.get(kOut, m)));
+      if (hdr[1] < 0) {
+        acc_ptrs.push_back(static_cast<const std::int64_t*>(peers_.get(kAcc, m)));
+        continue;
+      }
+      for (std::int64_t k = 0; k < hdr[1]; ++k) {
+        unit_ptrs.push_back(static_cast<const float*>(peers_.get(kUnit0 + static_cast<int>(k), m)));
+        double w = 0.0;
+        std::memcpy(&w, meta[i].data() + sizeof(hdr) + 8 * k, 8);
+        unit_w.push_back(w);
+      }
+    }
+    const int me = ch.index();
+    if (!acc_ptrs.empty()) {
+      if (static_cast<int>(acc_ptrs.size()) != world)
+        throw std::invalid_argument("every rank must contribute an int64 accumulator");
+      check(ew_peer_fold_create_i64(world, me, n_, acc_ptrs.data(), out_ptrs.data(), &fold_));
+    } else {
+      total_units_ = static_cast<std::int64_t>(unit_ptrs.size());
+      check(ew_peer_fold_create(world, me, n_, unit_ptrs.data(), unit_w.data(),
+                                static_cast<int>(unit_ptrs.size()), out_ptrs.data(), &fold_));
+    }
+    barrier_ = make_barrier(peers_, ch.members(), ch.me(), 0);
+  } catch (...) {
+    if (barrier_) ew_peer_barrier_free(barrier_);
+    barrier_ = nullptr;
+    ew_peer_fold_free(fold_);
+    fold_ = nullptr;
+    peers_.close();
+    dfree(flags_);
+    dfree(dmax_);
+    flags_ = nullptr;
+    dmax_ = nullptr;
+    throw;
+  }
+  ch.barrier();  // every flag array zeroed before the first device barrier
+}
+
+PeerReduce::~PeerReduce() {
+  if (barrier_) ew_peer_barrier_free(barrier_);
+  ew_peer_fold_free(fold_);
+  peers_.close();
+  dfree(flags_);
+  dfree(dmax_);
+}
+
+int PeerReduce::scale(ew_stream_t stream) {
+  NvtxRange range("ew.reduce.scale");
+  check(ew_weighted_absmax(units_.data(), weights_.data(), static_cast<int>(units_.size()), n_,
+                           dmax_, stream));
+  double local = 0.0;
+  check(ew_memcpy_async(&local, dmax_, 8, stream));
+  check(ew_stream_sync(stream));
+  std::string mine(8, '\0');
+  std::memcpy(mine.data(), &local, 8);
+  double global = 0.0;
+  bool nan = false;
+  for (const std::string& v : ch_.allgather(mine)) {
+    double x = 0.0;
+    std::memcpy(&x, v.data(), 8);
+    nan = nan || x != x;
+    global = std::max(global, x);
+  }
+  int bits = 0;
+  check(ew_fixed_point_bits(nan ? global * 0.0 / 0.0 : global, std::max<std::int64_t>(1, total_units_),
+                            &bits));
+  return bits;
+}
+
+void PeerReduce::run(int frac_bits, ew_stream_t stream) {
+  check(ew_peer_barrier_wait(barrier_, timeout_s_, stream));  // units written everywhere
+  check(ew_peer_fold_reduce_scatter(fold_, frac_bits, stream));
+  check(ew_peer_barrier_wait(barrier_, timeout_s_, stream));  // every slice reduced
+  check(ew_peer_fold_all_gather(fold_, stream));
+}
+
+void PeerReduce::wait(ew_stream_t stream) {
+  check(ew_peer_barrier_wait(barrier_, timeout_s_, stream));
+}
+
+bool PeerReduce::timed_out() const {
+  int t = 0;
+  check(ew_peer_barrier_timed_out(barrier_, &t));
+  return t != 0;
 }
 
 // ------------------------------------------------------------------ MTTR

@@ -225,6 +225,74 @@ class ReplayReplica:
             pass
 
 
+class PeerReduce:
+    """(d) — the gradient-scale-preserving weighted reduce — fused with its
+    collective over peer memory, no NCCL: a binding of the C++
+    elaskit::b200::PeerReduce (ew_peer_reduce).  Collective over `group`.
+
+    Units form: each rank passes its fp32 contribution units and weights;
+    `scale()` is the fixed-point scale of the global unit set (local absmax,
+    max over the ranks, ew_fixed_point_bits), `run(f)` the reduce-scatter /
+    all-gather between device barriers.  Accumulator form (`acc=`): each rank
+    already folded its units into an int64 accumulator; pass the scale used.
+    Bit-identical to the NCCL int64 path and to one GPU folding every unit."""
+
+    def __init__(self, out: torch.Tensor, units: Optional[Sequence[torch.Tensor]] = None,
+                 weights: Optional[Sequence[float]] = None, acc: Optional[torch.Tensor] = None,
+                 group=None, barrier_timeout_s: float = 30.0):
+        self.channel = Channel.from_group(group, "peer_reduce")
+        n = out.numel()
+        h = C.c_void_p()
+        if acc is not None:
+            check(lib.ew_peer_reduce_create_i64(self.channel.handle, C.c_void_p(acc.data_ptr()),
+                                                C.c_void_p(out.data_ptr()), n,
+                                                float(barrier_timeout_s), C.byref(h)))
+            self._keep = (out, acc)
+        else:
+            units = list(units or [])
+            w = list(weights or [])
+            arr = (C.c_void_p * max(1, len(units)))(*[u.data_ptr() for u in units])
+            wa = (C.c_double * max(1, len(w)))(*[float(x) for x in w])
+            check(lib.ew_peer_reduce_create(self.channel.handle, arr, wa, len(units),
+                                            C.c_void_p(out.data_ptr()), n,
+                                            float(barrier_timeout_s), C.byref(h)))
+            self._keep = (out, units)
+        self._h = h
+
+    @property
+    def total_units(self) -> int:
+        t = C.c_int64()
+        check(lib.ew_peer_reduce_info(self._h, C.byref(t), None))
+        return t.value
+
+    def scale(self, stream=None) -> int:
+        f = C.c_int()
+        check(lib.ew_peer_reduce_scale(self._h, dev._stream(stream), C.byref(f)))
+        return f.value
+
+    def run(self, frac_bits: int, stream=None) -> None:
+        check(lib.ew_peer_reduce_run(self._h, int(frac_bits), dev._stream(stream)))
+
+    def wait(self, stream=None) -> None:
+        check(lib.ew_peer_reduce_wait(self._h, dev._stream(stream)))
+
+    def timed_out(self) -> bool:
+        t = C.c_int()
+        check(lib.ew_peer_reduce_info(self._h, None, C.byref(t)))
+        return bool(t.value)
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
+            lib.ew_peer_reduce_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+
 class PreparedRecovery:
     """Every single departure of a DP group, planned, lowered and bound in
     steady state, so a failure runs only the copy and its verification —

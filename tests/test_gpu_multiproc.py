@@ -12,7 +12,8 @@ C++ runtime (include/elaskit/recovery.hpp):
     IPC mapping, copy, verification) with the MttrEvent / mttr.csv record;
   * InPlaceExecutor (config D): OLD and NEW in one buffer, phases behind
     device barriers, departures and a rejoin, the barrier never timing out;
-  * fp32 and int64 peer folds over peer memory with device barriers,
+  * PeerReduce: (d) with its collective over peer memory (fp32 units and
+    int64 accumulators, device barriers, the global scale over the store),
     bit-identical to the single-process fold;
   * ReplayReplica: the holder replays the owner's AdamW step from the
     owner's gradient read through an IPC pointer, byte-identical;
@@ -205,7 +206,9 @@ def _worker(rank, world, port, out_dir, scale):
                 del bufs
                 dist.barrier()
 
-        # ---- peer folds with device barriers (fp32 units and int64 accumulators)
+        # ---- (d) over peer memory through the C++ runtime (recovery.PeerReduce):
+        # fp32 units and int64 accumulators, device barriers, no NCCL
+        from paper_2510_00606_b200.recovery import PeerReduce
         n_units, dim = 2 * world, 100_003
         rng = np.random.default_rng(21)
         g = rng.normal(0, 1e-3, size=(n_units, dim)).astype(np.float32)
@@ -214,37 +217,32 @@ def _worker(rank, world, port, out_dir, scale):
         mine = [u for u in range(n_units) if u % world == rank]
         units = [torch.from_numpy(g[u]).cuda() for u in mine]
         out = torch.empty(dim, dtype=torch.float32, device="cuda")
-        fold, total, opened = dev.peer_weighted_reduce_setup(units, [w[u] for u in mine], out)
-        amax = dev.weighted_absmax(units, [w[u] for u in mine]).cpu()
-        dist.all_reduce(amax, op=dist.ReduceOp.MAX)
-        f = dev.fixed_point_bits(amax.item(), total)
+        pr = PeerReduce(out, units, [w[u] for u in mine], barrier_timeout_s=60.0)
+        f = pr.scale()
         all_units = [torch.from_numpy(x).cuda() for x in g]
+        f1 = dev.fixed_point_bits(dev.weighted_absmax(all_units, w).item(), n_units)
+        rep["peer reduce scale == single-GPU scale"] = f == f1 and pr.total_units == n_units
         acc1 = torch.empty(dim, dtype=torch.int64, device="cuda")
         dev.weighted_fold(all_units, w, f, acc1)
         single = dev.fixed_to_float(acc1, f)
-        bar = dev.PeerBarrier(timeout_s=60.0)
         for _ in range(2):
-            fold.run(f, bar)
-        bar.wait()
+            pr.run(f)
+        pr.wait()
         torch.cuda.synchronize()
         rep["fp32 peer fold bit-identical"] = bool(torch.equal(out, single))
         acc_mine = torch.empty(dim, dtype=torch.int64, device="cuda")
         dev.weighted_fold(units, [w[u] for u in mine], f, acc_mine)
         out64 = torch.full((dim,), -1.0, dtype=torch.float32, device="cuda")
-        fold64, opened64 = dev.peer_sum_i64_setup(acc_mine, out64)
-        torch.cuda.synchronize()
-        dist.barrier()
+        pr64 = PeerReduce(out64, acc=acc_mine, barrier_timeout_s=60.0)
         for _ in range(2):
-            fold64.run(f, bar)
-        bar.wait()
+            pr64.run(f)
+        pr64.wait()
         torch.cuda.synchronize()
         rep["int64 peer fold bit-identical"] = bool(torch.equal(out64, single))
-        rep["peer fold barrier never timed out"] = not bar.timed_out()
+        rep["peer fold barrier never timed out"] = not (pr.timed_out() or pr64.timed_out())
         dist.barrier()
-        bar.close()
-        del fold, fold64
-        for p in opened + opened64:
-            dev.ipc_close(p)
+        pr.close()
+        pr64.close()
 
         # ---- ring replica by optimizer replay over an IPC pointer
         from paper_2510_00606_b200.recovery import ReplayReplica
