@@ -1570,66 +1570,65 @@ def run_reduce(args, rank, world, out):
     del acc
     torch.cuda.empty_cache()
     if world > 1:
-        # the same reduce fused with its collective over NVLink peer memory
+        # the same reduce fused with its collective over NVLink peer memory,
+        # through the C++ runtime (recovery.PeerReduce): global scale (absmax
+        # + max over the store) and reduce-scatter / all-gather between
+        # device barriers, all inside the timed region, no NCCL
+        from paper_2510_00606_b200.recovery import PeerReduce
         peer_out = torch.empty(n, dtype=torch.float32, device="cuda")
-        fold, total, opened = dev.peer_weighted_reduce_setup(units, w, peer_out)
-        bar = dev.PeerBarrier()
-        fold.run(f, bar)
-        bar.wait()
+        pr = PeerReduce(peer_out, units, w)
+        fp = pr.scale()
+        pr.run(fp)
+        pr.wait()
         torch.cuda.synchronize()
         times = []
         for _ in range(3):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             barrier(world)
             s.record()
-            fold.run(f, bar)
+            fp = pr.scale()
+            pr.run(fp)
             e.record()
-            bar.wait()
+            pr.wait()
             torch.cuda.synchronize()
             times.append(s.elapsed_time(e) / 1e3)
-        assert not bar.timed_out(), "peer barrier timed out"
+        assert not pr.timed_out(), "peer barrier timed out"
         t_peer = max_over_ranks([min(times)], world)[0]
-        identical = bool(torch.equal(peer_out, res))
+        identical = bool(torch.equal(peer_out, res)) and fp == f
         ok = torch.tensor([1 if identical else 0], device="cuda")
         dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        nvl = 2 * (world - 1) / world * 4 * n  # bytes pulled per GPU (both phases)
         out["reduce"].update({
             "peer_path_ms": round(t_peer * 1e3, 3),
-            "peer_path_nvlink_gbs": round(nvl / t_peer / 1e9, 1),
-            "peer_vs_nccl_speedup": round((t_fold + t_ar + t_deq) / t_peer, 2),
+            "peer_path_includes": "local absmax + global max over the store + scale + "
+                                  "reduce-scatter + all-gather",
+            "peer_vs_nccl_speedup": round(t_all / t_peer, 2),
             "peer_bit_identical_to_nccl": bool(ok.item())})
-        bar.wait()
-        torch.cuda.synchronize()
         barrier(world)
-        bar.close()
-        del fold
-        for p in opened:
-            dev.ipc_close(p)
+        pr.close()
         del peer_out
         torch.cuda.empty_cache()
-        # world-size-invariant form: every rank has folded its micro-batch
-        # units into an int64 accumulator during backward (accumulate=1); the
-        # collective sums accumulators.  NCCL int64 all-reduce + dequant vs
-        # the peer int64 reduce-scatter + dequant + all-gather.
+        # world-size-invariant form over per-rank int64 accumulators (each
+        # rank folded its own units during backward, accumulate=1): NCCL
+        # int64 all-reduce + dequant vs the peer int64 reduce-scatter +
+        # dequant + all-gather
         acc = torch.empty(n, dtype=torch.int64, device="cuda")
         dev.weighted_fold(units, w, f, acc)
         out64 = torch.empty(n, dtype=torch.float32, device="cuda")
-        fold64, opened64 = dev.peer_sum_i64_setup(acc, out64)
-        bar = dev.PeerBarrier()
-        fold64.run(f, bar)
-        bar.wait()
+        pr64 = PeerReduce(out64, acc=acc)
+        pr64.run(f)
+        pr64.wait()
         torch.cuda.synchronize()
         times = []
         for _ in range(3):
             s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             barrier(world)
             s.record()
-            fold64.run(f, bar)
+            pr64.run(f)
             e.record()
-            bar.wait()
+            pr64.wait()
             torch.cuda.synchronize()
             times.append(s.elapsed_time(e) / 1e3)
-        assert not bar.timed_out(), "peer barrier timed out"
+        assert not pr64.timed_out(), "peer barrier timed out"
         t_p64 = max_over_ranks([min(times)], world)[0]
         same = torch.tensor([1 if torch.equal(out64, res) else 0], device="cuda")
         dist.all_reduce(same, op=dist.ReduceOp.MIN)
@@ -1640,13 +1639,8 @@ def run_reduce(args, rank, world, out):
                 "peer_speedup": round((t_ar + t_deq) / t_p64, 2),
                 "peer_nvlink_gbs": round((world - 1) / world * 12 * n / t_p64 / 1e9, 1),
                 "bit_identical": bool(same.item())}})
-        bar.wait()
-        torch.cuda.synchronize()
         barrier(world)
-        bar.close()
-        del fold64
-        for p in opened64:
-            dev.ipc_close(p)
+        pr64.close()
         del acc, out64
     del units, data, res
     torch.cuda.empty_cache()
