@@ -301,6 +301,61 @@ class RingReplica {
   ew_copy_program* copy_ = nullptr;
 };
 
+// ------------------------------------------------------------ host images
+
+// Host-memory images of every member's shard — the reference's
+// Medium::H2D_D2D source (param_fabric.hpp:59-79; the paper keeps the
+// replica in host DRAM).  One POSIX shm segment per member
+// ("/ew_<tag>_<member>": a header page with the committed epoch, then two
+// image slots), pinned and mapped for this GPU (ew_host_register).  The owner
+// publishes its shard each step with a D2H into the slot of epoch e (e mod
+// 2) followed, in stream order, by the commit word; a publish torn by a crash
+// leaves the previous epoch's image in use.  At recovery the holder's REPLICA
+// entry of the copy table points at the departed member's committed image,
+// so the destinations' copy kernels read those bytes from host memory over
+// their own PCIe links.  An image outlives its owner process.
+class HostImages {
+ public:
+  static constexpr std::int64_t kPage = 4096;
+  // Collective over `ch`.  readable: members whose images this rank maps
+  // (default all; its own always).  map_for_device = false skips the pinning
+  // (host-side users, CPU tests): device_ptr() then returns host addresses.
+  HostImages(Channel& ch, const PartitionLayout& layout, const std::string& tag,
+             const std::vector<int>& readable = {}, bool map_for_device = true);
+  ~HostImages();
+  HostImages(const HostImages&) = delete;
+  HostImages& operator=(const HostImages&) = delete;
+
+  // D2H of this member's live shard into the slot of `epoch` (default: the
+  // next one), then the commit word, both on `stream`.  Returns the epoch.
+  std::int64_t publish(const void* live, ew_stream_t stream, std::int64_t epoch = -1);
+  // host-side commit (a publisher without a GPU copy, tests)
+  void commit_host(std::int64_t epoch);
+  std::int64_t committed_epoch(int member) const;  // -1: none yet
+  // device address of member's last committed image (throws if none)
+  void* device_ptr(int member) const;
+  // host address of member's image of `epoch` (default: committed)
+  std::uint8_t* host_ptr(int member, std::int64_t epoch = -1) const;
+  std::int64_t image_bytes(int member) const { return bytes_.at(member); }
+  std::int64_t slot_bytes(int member) const { return slot_.at(member); }
+
+ private:
+  struct Segment {
+    std::uint8_t* addr = nullptr;
+    std::int64_t size = 0;
+    std::uint8_t* dev = nullptr;
+    std::vector<void*> pieces;  // registrations (unregistered at close)
+  };
+  void map_member(int member, bool create);
+  void release();
+  int me_;
+  std::string tag_;
+  bool map_for_device_;
+  std::map<int, std::int64_t> bytes_, slot_;
+  std::map<int, Segment> segs_;
+  std::int64_t next_epoch_ = -1;
+};
+
 // ------------------------------------------------- (d) over peer memory
 
 // The gradient-scale-preserving weighted reduce fused with

@@ -239,6 +239,9 @@ int ew_ipc_close(void* ptr);
  * register too.  Unregister before unmapping the range. */
 int ew_host_register(void* host, int64_t bytes, void** dev_ptr);
 int ew_host_unregister(void* host);
+/* Stream-ordered store of one u64 (a commit word), e.g. into registered host
+ * memory through its device address, after the stream's earlier copies. */
+int ew_write_u64_async(void* dev_ptr, uint64_t value, ew_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * (a) Snapshot + per-block checksum, verification
@@ -665,6 +668,24 @@ int ew_peer_reduce_run(ew_peer_reduce* r, int frac_bits, ew_stream_t stream);
 int ew_peer_reduce_wait(ew_peer_reduce* r, ew_stream_t stream);
 int ew_peer_reduce_info(const ew_peer_reduce* r, int64_t* total_units, int* timed_out);
 void ew_peer_reduce_free(ew_peer_reduce* r);
+
+/* Host-memory images (recovery.hpp HostImages, the H2D_D2D medium): one
+ * double-buffered POSIX shm image per member, pinned for this GPU unless
+ * map_for_device == 0; collective over the channel.  publish(): D2H into the
+ * slot of `epoch` (-1: next) then the commit word, stream-ordered.
+ * device_ptr(): the member's last committed image (for a copy-table slot). */
+typedef struct ew_host_images ew_host_images;
+int ew_host_images_create(ew_channel* ch, const ew_layout* layout, const char* tag,
+                          const int* readable, int n_readable, int map_for_device,
+                          ew_host_images** out);
+int ew_host_images_publish(ew_host_images* h, const void* live, int64_t epoch, ew_stream_t stream,
+                           int64_t* epoch_out);
+int ew_host_images_commit_host(ew_host_images* h, int64_t epoch);
+int ew_host_images_committed(const ew_host_images* h, int member, int64_t* epoch);
+int ew_host_images_device_ptr(const ew_host_images* h, int member, void** ptr);
+int ew_host_images_host_ptr(const ew_host_images* h, int member, int64_t epoch, void** ptr,
+                            int64_t* bytes);
+void ew_host_images_free(ew_host_images* h);
 
 #ifdef __cplusplus
 } /* extern "C" */

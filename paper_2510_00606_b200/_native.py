@@ -328,6 +328,14 @@ _sig("ew_peer_reduce_run", i32, vp, i32, vp)
 _sig("ew_peer_reduce_wait", i32, vp, vp)
 _sig("ew_peer_reduce_info", i32, vp, P(i64), P(i32))
 _sig("ew_peer_reduce_free", None, vp)
+_sig("ew_write_u64_async", i32, vp, u64, vp)
+_sig("ew_host_images_create", i32, vp, vp, C.c_char_p, P(i32), i32, i32, P(vp))
+_sig("ew_host_images_publish", i32, vp, vp, i64, vp, P(i64))
+_sig("ew_host_images_commit_host", i32, vp, i64)
+_sig("ew_host_images_committed", i32, vp, i32, P(i64))
+_sig("ew_host_images_device_ptr", i32, vp, i32, P(vp))
+_sig("ew_host_images_host_ptr", i32, vp, i32, i64, P(vp), P(i64))
+_sig("ew_host_images_free", None, vp)
 
 def int_array(values) -> C.Array:
     values = list(values)

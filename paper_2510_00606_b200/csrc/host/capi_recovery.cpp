@@ -55,6 +55,9 @@ struct ew_ring_replica {
 struct ew_peer_reduce {
   std::unique_ptr<elaskit::b200::PeerReduce> r;
 };
+struct ew_host_images {
+  std::unique_ptr<elaskit::b200::HostImages> h;
+};
 
 namespace {
 
@@ -597,5 +600,67 @@ int ew_peer_reduce_info(const ew_peer_reduce* r, int64_t* total_units, int* time
 }
 
 void ew_peer_reduce_free(ew_peer_reduce* r) { delete r; }
+
+// ------------------------------------------------------------ host images
+
+int ew_host_images_create(ew_channel* ch, const ew_layout* layout, const char* tag,
+                          const int* readable, int n_readable, int map_for_device,
+                          ew_host_images** out) {
+  return guarded([&]() -> int {
+    if (ch == nullptr || layout == nullptr || tag == nullptr || out == nullptr ||
+        n_readable < 0 || (n_readable > 0 && readable == nullptr))
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_host_images_create: bad arguments");
+    *out = new ew_host_images{std::make_unique<elaskit::b200::HostImages>(
+        *ch->c, layout->layout, tag, std::vector<int>(readable, readable + n_readable),
+        map_for_device != 0)};
+    return EW_OK;
+  });
+}
+
+int ew_host_images_publish(ew_host_images* h, const void* live, int64_t epoch, ew_stream_t stream,
+                           int64_t* epoch_out) {
+  return guarded([&]() -> int {
+    if (h == nullptr || live == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    const int64_t e = h->h->publish(live, stream, epoch);
+    if (epoch_out) *epoch_out = e;
+    return EW_OK;
+  });
+}
+
+int ew_host_images_commit_host(ew_host_images* h, int64_t epoch) {
+  return guarded([&]() -> int {
+    if (h == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    h->h->commit_host(epoch);
+    return EW_OK;
+  });
+}
+
+int ew_host_images_committed(const ew_host_images* h, int member, int64_t* epoch) {
+  return guarded([&]() -> int {
+    if (h == nullptr || epoch == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    *epoch = h->h->committed_epoch(member);
+    return EW_OK;
+  });
+}
+
+int ew_host_images_device_ptr(const ew_host_images* h, int member, void** ptr) {
+  return guarded([&]() -> int {
+    if (h == nullptr || ptr == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    *ptr = h->h->device_ptr(member);
+    return EW_OK;
+  });
+}
+
+int ew_host_images_host_ptr(const ew_host_images* h, int member, int64_t epoch, void** ptr,
+                            int64_t* bytes) {
+  return guarded([&]() -> int {
+    if (h == nullptr || ptr == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    *ptr = h->h->host_ptr(member, epoch);
+    if (bytes) *bytes = h->h->image_bytes(member);
+    return EW_OK;
+  });
+}
+
+void ew_host_images_free(ew_host_images* h) { delete h; }
 
 }  // extern "C"

@@ -15,8 +15,11 @@
 #include <netdb.h>
 #include <nvtx3/nvToolsExt.h>
 #include <netinet/in.h>
+#include <fcntl.h>
 #include <netinet/tcp.h>
+#include <sys/mman.h>
 #include <sys/socket.h>
+#include <sys/stat.h>
 #include <unistd.h>
 
 #include <algorithm>
@@ -672,6 +675,151 @@ RingReplica::~RingReplica() {
 void RingReplica::refresh(std::uint32_t* bad_dev, ew_stream_t stream) const {
   check(ew_copy_program_launch(copy_, 0, 0, stream));
   check(ew_verify(map_, replica_, owner_rows_, bad_dev, nullptr, 0, stream));
+}
+
+// ------------------------------------------------------------ host images
+
+namespace {
+std::string shm_name(const std::string& tag, int member) {
+  return "/ew_" + tag + "_" + std::to_string(member);
+}
+}  // namespace
+
+HostImages::HostImages(Channel& ch, const PartitionLayout& layout, const std::string& tag,
+                       const std::vector<int>& readable, bool map_for_device)
+    : me_(ch.me()), tag_(tag), map_for_device_(map_for_device) {
+  for (int m : ch.members()) {
+    bytes_[m] = layout.ranges.count(m) ? shard_bytes(layout, m) : 0;
+    slot_[m] = (std::max<std::int64_t>(1, bytes_[m]) + kPage - 1) / kPage * kPage;
+  }
+  std::string failure;
+  try {
+    map_member(me_, true);
+  } catch (const std::exception& e) {
+    failure = e.what();
+  }
+  ch.barrier();  // every segment exists before anyone opens a peer's
+  if (failure.empty()) {
+    try {
+      const std::vector<int> want = readable.empty() ? ch.members() : readable;
+      for (int m : want)
+        if (m != me_ && !segs_.count(m)) map_member(m, false);
+    } catch (const std::exception& e) {
+      failure = e.what();
+    }
+  }
+  // a failure surfaces only after the closing barrier: no rank is left waiting
+  const std::int64_t failed = ch.sum(failure.empty() ? 0 : 1);
+  if (failed != 0) {
+    release();
+    throw std::runtime_error("host images could not be mapped" +
+                             (failure.empty() ? std::string(" on a peer") : ": " + failure));
+  }
+  next_epoch_ = committed_epoch(me_) + 1;
+}
+
+void HostImages::map_member(int member, bool create) {
+  Segment seg;
+  seg.size = kPage + 2 * slot_.at(member);
+  const std::string name = shm_name(tag_, member);
+  const int fd = ::shm_open(name.c_str(), create ? (O_CREAT | O_EXCL | O_RDWR) : O_RDWR, 0600);
+  if (fd < 0) throw std::runtime_error("shm_open(" + name + ") failed");
+  if (create && ::ftruncate(fd, seg.size) != 0) {
+    ::close(fd);
+    ::shm_unlink(name.c_str());
+    throw std::runtime_error("ftruncate(" + name + ") failed (is /dev/shm large enough?)");
+  }
+  void* p = ::mmap(nullptr, static_cast<std::size_t>(seg.size), PROT_READ | PROT_WRITE, MAP_SHARED,
+                   fd, 0);
+  ::close(fd);
+  if (p == MAP_FAILED) {
+    if (create) ::shm_unlink(name.c_str());
+    throw std::runtime_error("mmap(" + name + ") failed");
+  }
+  seg.addr = static_cast<std::uint8_t*>(p);
+  if (create) *reinterpret_cast<volatile std::int64_t*>(seg.addr) = -1;
+  segs_[member] = seg;  // registered below; released by release() on failure
+  Segment& s = segs_[member];
+  if (!map_for_device_) {
+    s.dev = s.addr;
+    return;
+  }
+  void* d = nullptr;
+  if (ew_host_register(s.addr, s.size, &d) == EW_OK) {
+    s.dev = static_cast<std::uint8_t*>(d);
+    s.pieces.push_back(s.addr);
+    return;
+  }
+  // 1 GiB registrations: need the identity mapping of registered host memory
+  // (device address == host address) to stay one contiguous device range
+  constexpr std::int64_t kChunk = std::int64_t{1} << 30;
+  for (std::int64_t off = 0; off < s.size; off += kChunk) {
+    void* piece = s.addr + off;
+    check(ew_host_register(piece, std::min(kChunk, s.size - off), &d));
+    s.pieces.push_back(piece);
+    if (d != piece) throw std::runtime_error("registered host memory is not identity-mapped");
+  }
+  s.dev = s.addr;
+}
+
+void HostImages::release() {
+  for (auto& [m, s] : segs_) {
+    for (void* p : s.pieces) ew_host_unregister(p);
+    s.pieces.clear();
+    if (s.addr != nullptr) ::munmap(s.addr, static_cast<std::size_t>(s.size));
+    s.addr = nullptr;
+    if (m == me_) ::shm_unlink(shm_name(tag_, m).c_str());
+  }
+  segs_.clear();
+}
+
+HostImages::~HostImages() { release(); }
+
+std::int64_t HostImages::committed_epoch(int member) const {
+  return *reinterpret_cast<const volatile std::int64_t*>(segs_.at(member).addr);
+}
+
+std::uint8_t* HostImages::host_ptr(int member, std::int64_t epoch) const {
+  const std::int64_t e = epoch < 0 ? committed_epoch(member) : epoch;
+  if (e < 0) throw std::runtime_error("member " + std::to_string(member) +
+                                      " has not committed an image yet");
+  return segs_.at(member).addr + kPage + (e % 2) * slot_.at(member);
+}
+
+void* HostImages::device_ptr(int member) const {
+  const std::int64_t e = committed_epoch(member);
+  if (e < 0) throw std::runtime_error("member " + std::to_string(member) +
+                                      " has not committed an image yet");
+  return segs_.at(member).dev + kPage + (e % 2) * slot_.at(member);
+}
+
+std::int64_t HostImages::publish(const void* live, ew_stream_t stream, std::int64_t epoch) {
+  if (epoch < 0) epoch = next_epoch_;
+  next_epoch_ = epoch + 1;
+  const Segment& s = segs_.at(me_);
+  std::uint8_t* base = s.addr + kPage + (epoch % 2) * slot_.at(me_);
+  const std::int64_t n = bytes_.at(me_);
+  // one copy per registration piece the slot crosses
+  std::vector<std::uint8_t*> cuts = {base};
+  for (void* p : s.pieces) {
+    auto* q = static_cast<std::uint8_t*>(p);
+    if (q > base && q < base + n) cuts.push_back(q);
+  }
+  std::sort(cuts.begin(), cuts.end());
+  cuts.push_back(base + n);
+  for (std::size_t k = 0; k + 1 < cuts.size(); ++k)
+    if (cuts[k + 1] > cuts[k])
+      check(ew_memcpy_async(cuts[k], static_cast<const std::uint8_t*>(live) + (cuts[k] - base),
+                            cuts[k + 1] - cuts[k], stream));
+  // the commit word, after the image's last byte in stream order
+  check(ew_write_u64_async(s.dev, static_cast<std::uint64_t>(epoch), stream));
+  return epoch;
+}
+
+void HostImages::commit_host(std::int64_t epoch) {
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  *reinterpret_cast<volatile std::int64_t*>(segs_.at(me_).addr) = epoch;
+  next_epoch_ = epoch + 1;
 }
 
 // ------------------------------------------------- (d) over peer memory

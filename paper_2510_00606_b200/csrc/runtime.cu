@@ -27,6 +27,12 @@ int cuda_status(cudaError_t e, const char* what) {
                                     cudaGetErrorString(e) + ")");
 }
 
+__global__ void write_u64_kernel(volatile unsigned long long* p, unsigned long long v) {
+  __threadfence_system();  // the stream's earlier writes (a D2H image) come first
+  *p = v;
+  __threadfence_system();
+}
+
 int num_sms() {
   static std::mutex mu;
   static std::map<int, int> cache;
@@ -223,6 +229,15 @@ int ew_host_register(void* host, int64_t bytes, void** dev_ptr) {
     cudaHostUnregister(host);
     return cuda_status(e, "cudaHostGetDevicePointer");
   }
+  return EW_OK;
+}
+
+int ew_write_u64_async(void* dev_ptr, uint64_t value, ew_stream_t stream) {
+  if (dev_ptr == nullptr || (reinterpret_cast<uintptr_t>(dev_ptr) & 7))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_write_u64_async: NULL or unaligned");
+  ew::write_u64_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(
+      static_cast<volatile unsigned long long*>(dev_ptr), value);
+  EW_CUDA_TRY(cudaGetLastError());
   return EW_OK;
 }
 
