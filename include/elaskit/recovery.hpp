@@ -301,6 +301,63 @@ class RingReplica {
   ew_copy_program* copy_ = nullptr;
 };
 
+// ------------------------------------------------------- layer migration
+
+// Non-blocking layer migration with shadow-gradient payback (
+// the reference plans it, plan_layer_migration migration.cpp:9-61, and only
+// models its time, Simulation::migrate sim.cpp:485-530).  The target pulls
+// the layer's parameters over NVLink with a few CTAs on a low-priority
+// stream; the source's shadow instance folds micro-batches [0, k) into its
+// int64 accumulator and releases a device barrier; the target then pulls
+// that accumulator and adds it inside its last fold (ew_weighted_fold_addend).
+// Integer sums: the migrated step's gradient is bit-identical to the static
+// step's for every k.
+class LayerMigration {
+ public:
+  // Collective over `ch` = {source, target}.  Source: `params` is its layer's
+  // parameter buffer, `acc` its shadow accumulator.  Target: `params` is the
+  // destination buffer, `acc` its own accumulator (n int64 each).
+  LayerMigration(Channel& ch, int source, int target, void* params, std::int64_t param_bytes,
+                 std::int64_t* acc, std::int64_t n, int transfer_ctas = 32,
+                 double barrier_timeout_s = 30.0);
+  ~LayerMigration();
+  LayerMigration(const LayerMigration&) = delete;
+  LayerMigration& operator=(const LayerMigration&) = delete;
+
+  // target: the parameter pull on `stream` (low priority by convention)
+  void pull_params(ew_stream_t stream);
+  // source: after the shadow instance's last fold
+  void shadow_done(ew_stream_t stream);
+  // target: wait (on `stream`) for the source's shadow_done, then pull its
+  // accumulator into payback_buffer()
+  void prefetch_payback(ew_stream_t stream);
+  // target, unoverlapped: acc += the source's accumulator, read in peer HBM
+  void payback(ew_stream_t stream);
+  // The target's step for the layer: micro-batches [0, k) without it, the
+  // parameter wait before k, folds [k, M) into acc, the payback in the last
+  // fold.  `compute` / `transfer`: cudaStream_t.
+  void run_target(const std::vector<const float*>& units, const std::vector<double>& weights,
+                  std::int64_t n, int frac_bits, int k, ew_stream_t compute, ew_stream_t transfer);
+  // The source's shadow instance: folds [0, k) into acc, then shadow_done.
+  void run_shadow(const std::vector<const float*>& units, const std::vector<double>& weights,
+                  std::int64_t n, int frac_bits, int k, ew_stream_t compute);
+  const std::int64_t* payback_buffer() const { return payback_; }
+  bool timed_out() const;
+
+ private:
+  int me_, source_, target_, transfer_ctas_;
+  double timeout_s_;
+  std::int64_t* acc_;
+  std::int64_t n_;
+  PeerBuffers peers_;
+  ew_copy_program* pull_ = nullptr;
+  ew_copy_program* payback_pull_ = nullptr;
+  std::int64_t* payback_ = nullptr;
+  const std::int64_t* source_acc_ = nullptr;
+  ew_peer_barrier* barrier_ = nullptr;
+  unsigned long long* flags_ = nullptr;
+};
+
 // ------------------------------------------------------------ host images
 
 // Host-memory images of every member's shard — the reference's

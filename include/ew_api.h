@@ -687,6 +687,24 @@ int ew_host_images_host_ptr(const ew_host_images* h, int member, int64_t epoch, 
                             int64_t* bytes);
 void ew_host_images_free(ew_host_images* h);
 
+/* Non-blocking layer migration with shadow-gradient payback (recovery.hpp
+ * LayerMigration), collective over a channel of exactly {source, target}.
+ * step(): 0 pull_params (target), 1 shadow_done (source), 2 prefetch_payback
+ * (target: waits for shadow_done, pulls the source's accumulator), 3 payback
+ * (target, unoverlapped acc += peer acc).  run(): the target's (target_side
+ * != 0) or the shadow's whole schedule for M micro-batch units. */
+typedef struct ew_layer_migration ew_layer_migration;
+int ew_layer_migration_create(ew_channel* ch, int source, int target, void* params,
+                              int64_t param_bytes, int64_t* acc, int64_t n, int transfer_ctas,
+                              double barrier_timeout_s, ew_layer_migration** out);
+int ew_layer_migration_step(ew_layer_migration* m, int what, ew_stream_t stream);
+int ew_layer_migration_run(ew_layer_migration* m, int target_side, const float* const* units,
+                           const double* weights, int n_units, int64_t n, int frac_bits, int k,
+                           ew_stream_t compute, ew_stream_t transfer);
+int ew_layer_migration_info(const ew_layer_migration* m, const int64_t** payback_buffer,
+                            int* timed_out);
+void ew_layer_migration_free(ew_layer_migration* m);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -336,6 +336,11 @@ _sig("ew_host_images_committed", i32, vp, i32, P(i64))
 _sig("ew_host_images_device_ptr", i32, vp, i32, P(vp))
 _sig("ew_host_images_host_ptr", i32, vp, i32, i64, P(vp), P(i64))
 _sig("ew_host_images_free", None, vp)
+_sig("ew_layer_migration_create", i32, vp, i32, i32, vp, i64, vp, i64, i32, f64, P(vp))
+_sig("ew_layer_migration_step", i32, vp, i32, vp)
+_sig("ew_layer_migration_run", i32, vp, i32, P(vp), P(f64), i32, i64, i32, i32, vp, vp)
+_sig("ew_layer_migration_info", i32, vp, P(vp), P(i32))
+_sig("ew_layer_migration_free", None, vp)
 
 def int_array(values) -> C.Array:
     values = list(values)

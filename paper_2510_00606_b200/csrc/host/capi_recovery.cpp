@@ -58,6 +58,9 @@ struct ew_peer_reduce {
 struct ew_host_images {
   std::unique_ptr<elaskit::b200::HostImages> h;
 };
+struct ew_layer_migration {
+  std::unique_ptr<elaskit::b200::LayerMigration> m;
+};
 
 namespace {
 
@@ -662,5 +665,62 @@ int ew_host_images_host_ptr(const ew_host_images* h, int member, int64_t epoch, 
 }
 
 void ew_host_images_free(ew_host_images* h) { delete h; }
+
+// ------------------------------------------------------- layer migration
+
+int ew_layer_migration_create(ew_channel* ch, int source, int target, void* params,
+                              int64_t param_bytes, int64_t* acc, int64_t n, int transfer_ctas,
+                              double barrier_timeout_s, ew_layer_migration** out) {
+  return guarded([&]() -> int {
+    if (ch == nullptr || out == nullptr || params == nullptr || acc == nullptr || n < 0 ||
+        param_bytes < 0)
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_layer_migration_create: bad arguments");
+    *out = new ew_layer_migration{std::make_unique<elaskit::b200::LayerMigration>(
+        *ch->c, source, target, params, param_bytes, acc, n, transfer_ctas, barrier_timeout_s)};
+    return EW_OK;
+  });
+}
+
+int ew_layer_migration_step(ew_layer_migration* m, int what, ew_stream_t stream) {
+  return guarded([&]() -> int {
+    if (m == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    switch (what) {
+      case 0: m->m->pull_params(stream); break;
+      case 1: m->m->shadow_done(stream); break;
+      case 2: m->m->prefetch_payback(stream); break;
+      case 3: m->m->payback(stream); break;
+      default: return set_error(EW_ERR_INVALID_ARGUMENT, "unknown migration step");
+    }
+    return EW_OK;
+  });
+}
+
+int ew_layer_migration_run(ew_layer_migration* m, int target_side, const float* const* units,
+                           const double* weights, int n_units, int64_t n, int frac_bits, int k,
+                           ew_stream_t compute, ew_stream_t transfer) {
+  return guarded([&]() -> int {
+    if (m == nullptr || n_units < 0 || (n_units > 0 && (!units || !weights)))
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_layer_migration_run: bad arguments");
+    const std::vector<const float*> u(units, units + n_units);
+    const std::vector<double> w(weights, weights + n_units);
+    if (target_side)
+      m->m->run_target(u, w, n, frac_bits, k, compute, transfer);
+    else
+      m->m->run_shadow(u, w, n, frac_bits, k, compute);
+    return EW_OK;
+  });
+}
+
+int ew_layer_migration_info(const ew_layer_migration* m, const int64_t** payback_buffer,
+                            int* timed_out) {
+  return guarded([&]() -> int {
+    if (m == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
+    if (payback_buffer) *payback_buffer = m->m->payback_buffer();
+    if (timed_out) *timed_out = m->m->timed_out() ? 1 : 0;
+    return EW_OK;
+  });
+}
+
+void ew_layer_migration_free(ew_layer_migration* m) { delete m; }
 
 }  // extern "C"

@@ -338,6 +338,7 @@ int index_of(const std::vector<int>& v, int x) {
 constexpr int kLanded = 10, kOldBlocks = 11, kReplicaBlocks = 12, kFlags = 13;
 constexpr int kGrad = 20, kRows = 21, kSnap = 22;
 constexpr int kOut = 30, kAcc = 31, kUnit0 = 100;  // units: kUnit0 + k
+constexpr int kParams = 40;
 
 // Slice [lo, hi) (even) of n_words owned by survivor i of k.
 std::pair<std::int64_t, std::int64_t> slice_of(std::int64_t n_words, int i, int k) {
@@ -675,6 +676,141 @@ RingReplica::~RingReplica() {
 void RingReplica::refresh(std::uint32_t* bad_dev, ew_stream_t stream) const {
   check(ew_copy_program_launch(copy_, 0, 0, stream));
   check(ew_verify(map_, replica_, owner_rows_, bad_dev, nullptr, 0, stream));
+}
+
+// ------------------------------------------------------- layer migration
+
+LayerMigration::LayerMigration(Channel& ch, int source, int target, void* params,
+                               std::int64_t param_bytes, std::int64_t* acc, std::int64_t n,
+                               int transfer_ctas, double barrier_timeout_s)
+    : me_(ch.me()), source_(source), target_(target), transfer_ctas_(transfer_ctas),
+      timeout_s_(barrier_timeout_s), acc_(acc), n_(n) {
+  if (ch.members().size() != 2 || index_of(ch.members(), source) < 0 ||
+      index_of(ch.members(), target) < 0 || source == target)
+    throw std::invalid_argument("a layer migration's channel is exactly {source, target}");
+  try {
+    flags_ = dalloc<unsigned long long>(2);
+    check(ew_memset_async(flags_, 0, 16, nullptr));
+    check(ew_device_sync());
+    std::map<int, void*> mine = {{kFlags, flags_}};
+    if (me_ == source) {
+      mine[kParams] = params;
+      mine[kAcc] = acc;
+    }
+    peers_.exchange(ch, mine);
+    barrier_ = make_barrier(peers_, ch.members(), me_, 0);
+    if (me_ == target) {
+      const void* src = peers_.get(kParams, source);
+      source_acc_ = static_cast<const std::int64_t*>(peers_.get(kAcc, source));
+      if (src == nullptr || source_acc_ == nullptr)
+        throw std::runtime_error("the source's parameters / accumulator are not mapped");
+      const int remote = 1;
+      check(ew_copy_program_create_raw(&src, &params, &param_bytes, &remote, 1, &pull_));
+      payback_ = dalloc<std::int64_t>(std::max<std::int64_t>(4, n));
+      const void* asrc = source_acc_;
+      void* adst = payback_;
+      const std::int64_t abytes = 8 * n;
+      check(ew_copy_program_create_raw(&asrc, &adst, &abytes, &remote, 1, &payback_pull_));
+    }
+  } catch (...) {
+    if (barrier_) ew_peer_barrier_free(barrier_);
+    ew_copy_program_free(pull_);
+    ew_copy_program_free(payback_pull_);
+    peers_.close();
+    dfree(payback_);
+    dfree(flags_);
+    throw;
+  }
+  ch.barrier();
+}
+
+LayerMigration::~LayerMigration() {
+  if (barrier_) ew_peer_barrier_free(barrier_);
+  ew_copy_program_free(pull_);
+  ew_copy_program_free(payback_pull_);
+  peers_.close();
+  dfree(payback_);
+  dfree(flags_);
+}
+
+void LayerMigration::pull_params(ew_stream_t stream) {
+  if (me_ != target_) throw std::logic_error("pull_params runs on the target");
+  // stream priority only orders pending CTAs: a few dozen CTAs keep NVLink
+  // busy without holding every SM away from the compute stream
+  check(ew_copy_program_launch(pull_, transfer_ctas_, 0, stream));
+}
+
+void LayerMigration::shadow_done(ew_stream_t stream) {
+  if (me_ != source_) throw std::logic_error("shadow_done runs on the source");
+  check(ew_peer_barrier_wait(barrier_, timeout_s_, stream));
+}
+
+void LayerMigration::prefetch_payback(ew_stream_t stream) {
+  if (me_ != target_) throw std::logic_error("prefetch_payback runs on the target");
+  check(ew_peer_barrier_wait(barrier_, timeout_s_, stream));
+  const int* veto = nullptr;
+  check(ew_peer_barrier_error_flag(barrier_, &veto));
+  check(ew_copy_program_launch_guarded(payback_pull_, transfer_ctas_, 0, nullptr, veto, stream));
+}
+
+void LayerMigration::payback(ew_stream_t stream) {
+  if (me_ != target_) throw std::logic_error("payback runs on the target");
+  check(ew_payback_accumulate(acc_, source_acc_, n_, stream));
+}
+
+void LayerMigration::run_target(const std::vector<const float*>& units,
+                                const std::vector<double>& weights, std::int64_t n,
+                                int frac_bits, int k, ew_stream_t compute, ew_stream_t transfer) {
+  NvtxRange range("ew.migration.target");
+  const int M = static_cast<int>(units.size());
+  cudaStream_t cs = reinterpret_cast<cudaStream_t>(compute);
+  cudaStream_t ts = reinterpret_cast<cudaStream_t>(transfer);
+  cudaEvent_t arrived = nullptr, ready = nullptr;
+  cuda_check(cudaEventCreateWithFlags(&arrived, cudaEventDisableTiming), "cudaEventCreate");
+  pull_params(transfer);
+  cuda_check(cudaEventRecord(arrived, ts), "cudaEventRecord");
+  if (k > 0) {  // k == 0 is the blocking move: nothing to pay back
+    cuda_check(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming), "cudaEventCreate");
+    prefetch_payback(transfer);
+    cuda_check(cudaEventRecord(ready, ts), "cudaEventRecord");
+  }
+  for (int mb = std::min(k, M); mb < M; ++mb) {
+    if (mb == k) cuda_check(cudaStreamWaitEvent(cs, arrived, 0), "wait");
+    const bool last = mb == M - 1 && ready != nullptr;
+    if (last) cuda_check(cudaStreamWaitEvent(cs, ready, 0), "wait");
+    const float* u = units[static_cast<std::size_t>(mb)];
+    const double w = weights[static_cast<std::size_t>(mb)];
+    check(ew_weighted_fold_addend(&u, &w, 1, n, frac_bits, acc_, 1, last ? payback_ : nullptr,
+                                  compute));
+  }
+  if (k >= M) {
+    cuda_check(cudaStreamWaitEvent(cs, arrived, 0), "wait");
+    if (ready != nullptr) {
+      cuda_check(cudaStreamWaitEvent(cs, ready, 0), "wait");
+      check(ew_payback_accumulate(acc_, payback_, n_, compute));
+    }
+  }
+  cudaEventDestroy(arrived);
+  if (ready != nullptr) cudaEventDestroy(ready);
+}
+
+void LayerMigration::run_shadow(const std::vector<const float*>& units,
+                                const std::vector<double>& weights, std::int64_t n,
+                                int frac_bits, int k, ew_stream_t compute) {
+  if (k <= 0) return;  // blocking move: the target computes every micro-batch
+  NvtxRange range("ew.migration.shadow");
+  for (int mb = 0; mb < std::min(k, static_cast<int>(units.size())); ++mb) {
+    const float* u = units[static_cast<std::size_t>(mb)];
+    const double w = weights[static_cast<std::size_t>(mb)];
+    check(ew_weighted_fold_addend(&u, &w, 1, n, frac_bits, acc_, 1, nullptr, compute));
+  }
+  shadow_done(compute);
+}
+
+bool LayerMigration::timed_out() const {
+  int t = 0;
+  check(ew_peer_barrier_timed_out(barrier_, &t));
+  return t != 0;
 }
 
 // ------------------------------------------------------------ host images

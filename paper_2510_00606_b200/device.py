@@ -296,15 +296,21 @@ def fixed_point_bits(global_absmax: float, total_units: int) -> int:
 
 
 def weighted_fold(units, weights, frac_bits: int, acc: torch.Tensor, accumulate: bool = False,
-                  stream=None, addend: Optional[torch.Tensor] = None) -> torch.Tensor:
-    """acc (+)= sum_u rint(w_u g_u 2^F) [+ addend], one pass (ew_weighted_fold_addend)."""
+                  stream=None, addend=None) -> torch.Tensor:
+    """acc (+)= sum_u rint(w_u g_u 2^F) [+ addend], one pass (ew_weighted_fold_addend).
+    `addend`: int64 tensor, or a raw (library-owned or peer) device pointer to
+    at least n int64 values."""
     ptrs, w, n = _units(units, weights)
     if acc.dtype != torch.int64 or acc.numel() < n:
         raise ValueError("acc must be int64 with one slot per element")
-    if addend is not None and (addend.dtype != torch.int64 or addend.numel() < n):
-        raise ValueError("addend must be int64 with one slot per element")
+    if isinstance(addend, torch.Tensor):
+        if addend.dtype != torch.int64 or addend.numel() < n:
+            raise ValueError("addend must be int64 with one slot per element")
+        add = _ptr(addend)
+    else:
+        add = C.c_void_p(int(addend) if addend else None)
     check(lib.ew_weighted_fold_addend(ptrs, w, len(units), n, int(frac_bits), _ptr(acc),
-                                      int(accumulate), _ptr(addend), _stream(stream)))
+                                      int(accumulate), add, _stream(stream)))
     return acc
 
 

@@ -23,10 +23,10 @@ property the reference's toy simulator checks with fp64 folds
 """
 from __future__ import annotations
 
+import ctypes as C
 from typing import Optional
 
 import torch
-import torch.distributed as dist
 
 from . import device as dev
 from ._native import check, lib
@@ -43,7 +43,10 @@ def payback_accumulate(acc: torch.Tensor, payback, stream=None) -> None:
 
 
 class LayerMigration:
-    """One layer moving from the source rank to the target rank.
+    """One layer moving from the source rank to the target rank — a binding
+    of the C++ elaskit::b200::LayerMigration (ew_layer_migration): the IPC
+    mappings, the parameter and payback pulls, the device barrier and (for
+    the plain schedule) the whole target / shadow step run in C++.
 
     Both ranks construct it collectively over `group`, a process group of
     exactly {source, target}.  The source passes its parameter buffer and its
@@ -64,45 +67,43 @@ class LayerMigration:
     """
 
     def __init__(self, move, src_rank: int, dst_rank: int, rank: int, params: torch.Tensor,
-                 acc: torch.Tensor, group=None, transfer_ctas: int = 32):
+                 acc: torch.Tensor, group=None, transfer_ctas: int = 32,
+                 barrier_timeout_s: float = 30.0):
         """transfer_ctas: CTAs of the background pulls.  Stream priority
         only orders *pending* CTAs, so a full-width copy would hold every SM
         until it finished and stall the compute stream; a few dozen CTAs
         with 96 KiB in flight each still saturate NVLink."""
+        from .rendezvous import Channel
         self.transfer_ctas = transfer_ctas
         self.move = tuple(move)
         self.src, self.dst, self.rank = src_rank, dst_rank, rank
         self.params, self.acc = params, acc
-        world = dist.get_world_size(group)
-        mine = None
-        if rank == src_rank:
-            mine = (dev.ipc_handle(params), dev.ipc_handle(acc))
-        allh = [None] * world
-        dist.all_gather_object(allh, (rank, mine), group=group)
-        self._opened = []
-        self.copy: Optional[dev.CopyProgram] = None
-        self.payback_buf: Optional[torch.Tensor] = None
-        self.barrier = dev.PeerBarrier(group)
-        if rank == dst_rank:
-            (hp, op), (ha, oa) = dict(allh)[src_rank]
-            self._opened = [dev.ipc_open(hp, op), dev.ipc_open(ha, oa)]
-            self.copy = dev.CopyProgram.from_pointers([self._opened[0]], [params.data_ptr()],
-                                                      [params.numel() * params.element_size()],
-                                                      [True])
-            self.payback_buf = torch.empty_like(acc)
-            self.payback_copy = dev.CopyProgram.from_pointers(
-                [self._opened[1]], [self.payback_buf.data_ptr()], [acc.numel() * 8], [True])
+        self.channel = Channel.from_group(group, "migration")
+        h = C.c_void_p()
+        check(lib.ew_layer_migration_create(
+            self.channel.handle, int(src_rank), int(dst_rank), C.c_void_p(params.data_ptr()),
+            params.numel() * params.element_size(), C.c_void_p(acc.data_ptr()), acc.numel(),
+            int(transfer_ctas), float(barrier_timeout_s), C.byref(h)))
+        self._h = h
         self.events = {}
+        self.payback_buf = None
+        if rank == dst_rank:
+            p = C.c_void_p()
+            check(lib.ew_layer_migration_info(h, C.byref(p), None))
+            self._payback_ptr = p.value
 
     def plan(self, mode: int = NON_BLOCKING, **ctx) -> MigrationSchedule:
         """The reference planner (plan_layer_migration) on this move."""
         return plan_layer_migration(self.move, mode, **ctx)
 
-    def _timed(self, name, stream, fn):
+    def _step(self, what: int, stream) -> None:
+        check(lib.ew_layer_migration_step(self._h, what, dev._stream(stream)))
+
+    def _timed(self, name, stream, what):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         st = stream or torch.cuda.current_stream()
         s.record(st)
-        fn(st)
+        self._step(what, st)
         e.record(st)
         self.events[name] = (s, e)
         return e
@@ -110,45 +111,47 @@ class LayerMigration:
     def pull_params(self, stream: Optional[torch.cuda.Stream] = None) -> torch.cuda.Event:
         """Target: start the parameter pull on `stream` (low priority by
         convention); returns the event that marks the parameters' arrival."""
-        assert self.rank == self.dst
-        return self._timed("params", stream, lambda st: self.copy.launch(self.transfer_ctas, stream=st))
+        return self._timed("params", stream, 0)
 
     def shadow_done(self, stream: Optional[torch.cuda.Stream] = None) -> None:
         """Source: enqueue after the shadow instance's last fold."""
-        assert self.rank == self.src
-        self.barrier.wait(stream)
+        self._step(1, stream)
 
     def prefetch_payback(self, stream: Optional[torch.cuda.Stream] = None) -> torch.cuda.Event:
         """Target: wait (on `stream`) until the source's shadow is done, then
-        pull its accumulator into payback_buf; returns the arrival event."""
-        assert self.rank == self.dst
-        self.barrier.wait(stream)
-        return self._timed("payback_grad", stream, lambda st: self.payback_copy.launch(self.transfer_ctas, stream=st))
+        pull its accumulator into the payback buffer; returns the arrival
+        event (the barrier wait is part of the timed segment)."""
+        return self._timed("payback_grad", stream, 2)
 
     def payback(self, stream: Optional[torch.cuda.Stream] = None) -> torch.cuda.Event:
         """Target, unoverlapped variant: add the source's shadow accumulator
         into the target's straight from peer HBM (the caller orders it after
         the shadow's last fold)."""
-        assert self.rank == self.dst
-        return self._timed("payback_grad", stream,
-                           lambda st: payback_accumulate(self.acc, self._opened[1], stream=st))
+        return self._timed("payback_grad", stream, 3)
 
     def run_target(self, units, weights, frac_bits: int, k: int,
                    compute: torch.cuda.Stream, transfer: torch.cuda.Stream,
                    other_work=None) -> None:
         """Target's step for this layer: units[mb] is micro-batch mb's
         gradient of the layer (fp32), weights[mb] its weight.  Micro-batches
-        [0, k) run without the layer (other_work(mb, stream) stands for the
-        target's other layers); [k, M) fold into self.acc after the
-        parameters arrived; the payback joins in the last fold."""
+        [0, k) run without the layer; [k, M) fold into self.acc after the
+        parameters arrived; the payback joins in the last fold.  Without
+        `other_work` the whole schedule is one C++ call; `other_work(mb,
+        stream)` (the target's other layers during [0, k), e.g. in a
+        benchmark) keeps the same schedule with the micro-batch loop here."""
+        if other_work is None:
+            arr = (C.c_void_p * max(1, len(units)))(*[u.data_ptr() for u in units])
+            w = (C.c_double * max(1, len(weights)))(*[float(x) for x in weights])
+            check(lib.ew_layer_migration_run(self._h, 1, arr, w, len(units), units[0].numel(),
+                                             int(frac_bits), int(k), dev._stream(compute),
+                                             dev._stream(transfer)))
+            return
         M = len(units)
         arrived = self.pull_params(transfer)
-        # k == 0 is the blocking move: no shadow work, nothing to pay back
         ready = self.prefetch_payback(transfer) if k > 0 else None
         for mb in range(M):
             if mb < k:
-                if other_work is not None:
-                    other_work(mb, compute)
+                other_work(mb, compute)
                 continue
             if mb == k:
                 compute.wait_event(arrived)
@@ -156,33 +159,38 @@ class LayerMigration:
             if last:
                 compute.wait_event(ready)
             dev.weighted_fold([units[mb]], [weights[mb]], frac_bits, self.acc, accumulate=True,
-                              stream=compute, addend=self.payback_buf if last else None)
+                              stream=compute, addend=self._payback_ptr if last else None)
         if k >= M:
             compute.wait_event(arrived)
-            compute.wait_event(ready)
-            payback_accumulate(self.acc, self.payback_buf, stream=compute)
+            if ready is not None:
+                compute.wait_event(ready)
+                payback_accumulate(self.acc, self._payback_ptr, stream=compute)
 
     def run_shadow(self, units, weights, frac_bits: int, k: int,
                    compute: torch.cuda.Stream) -> None:
         """Source's shadow instance: micro-batches [0, k) of the layer, then
-        the signal that releases the target's payback pull."""
-        if k <= 0:
-            return  # blocking move: the target computes every micro-batch
-        for mb in range(min(k, len(units))):
-            dev.weighted_fold([units[mb]], [weights[mb]], frac_bits, self.acc, accumulate=True,
-                              stream=compute)
-        self.shadow_done(compute)
+        the signal that releases the target's payback pull (C++)."""
+        arr = (C.c_void_p * max(1, len(units)))(*[u.data_ptr() for u in units])
+        w = (C.c_double * max(1, len(weights)))(*[float(x) for x in weights])
+        check(lib.ew_layer_migration_run(self._h, 0, arr, w, len(units), units[0].numel(),
+                                         int(frac_bits), int(k), dev._stream(compute), None))
 
     def timed_out(self) -> bool:
-        return self.barrier.timed_out()
+        t = C.c_int()
+        check(lib.ew_layer_migration_info(self._h, None, C.byref(t)))
+        return bool(t.value)
 
     def measured(self) -> dict:
         """Measured transfer segments (ms) after synchronisation."""
         return {k: s.elapsed_time(e) for k, (s, e) in self.events.items()}
 
     def close(self) -> None:
-        self.copy = self.payback_copy = None
-        for p in self._opened:
-            dev.ipc_close(p)
-        self._opened = []
-        self.barrier.close()
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
+            lib.ew_layer_migration_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

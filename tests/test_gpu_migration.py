@@ -1,5 +1,7 @@
-"""Non-blocking layer migration with shadow-gradient payback on 2 GPUs
-(reference plan_layer_migration, migration.cpp:9-61): the
+"""Non-blocking layer migration with shadow-gradient payback (SURVEY §8(f)
+#2; reference plan_layer_migration, migration.cpp:9-61), through the C++
+executor (elaskit::b200::LayerMigration): on 2 GPUs over NVLink, and as two
+processes sharing one GPU (CUDA IPC on one device) so a 1-GPU lease runs it: the
 parameters arrive byte-exact over NVLink, and the layer's gradient — shadow
 instance folds micro-batches [0, k) on the source, the target folds [k, M),
 payback adds the shadow's int64 accumulator from peer HBM — is bit-identical
@@ -22,7 +24,7 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, result_dir):
+def _worker(rank, world, port, result_dir, same_device=False):
     import json
     import sys
     from pathlib import Path
@@ -32,9 +34,13 @@ def _worker(rank, world, port, result_dir):
     from paper_2510_00606_b200.migration import LayerMigration
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
-    torch.cuda.set_device(rank)
-    dist.init_process_group("nccl", rank=rank, world_size=world,
-                            device_id=torch.device("cuda", rank))
+    if same_device:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    else:
+        torch.cuda.set_device(rank)
+        dist.init_process_group("nccl", rank=rank, world_size=world,
+                                device_id=torch.device("cuda", rank))
     report = {}
     try:
         n, M = 1_000_003, 8
@@ -46,7 +52,10 @@ def _worker(rank, world, port, result_dir):
         units = [torch.from_numpy(g).cuda() for g in grads]
         src, dst = 0, 1
         base = torch.from_numpy(rng.integers(0, 2 ** 15, n, dtype=np.int16)).cuda()
-        for k in (0, 3, 8):
+        scratch = torch.zeros(n, dtype=torch.int64, device="cuda")
+        other = lambda mb, st: dev.weighted_fold([units[mb]], [w[mb]], f, scratch,  # noqa: E731
+                                                 accumulate=True, stream=st)
+        for k, with_other in ((0, False), (3, False), (8, False), (3, True)):
             params = base.clone() if rank == src else torch.zeros(n, dtype=torch.int16, device="cuda")
             acc = torch.zeros(n, dtype=torch.int64, device="cuda")
             mig = LayerMigration((5, 0, 1), src, dst, rank, params, acc)
@@ -54,8 +63,9 @@ def _worker(rank, world, port, result_dir):
             low, high = torch.cuda.Stream(priority=0), torch.cuda.Stream(priority=-1)
             if rank == src:
                 mig.run_shadow(units, w, f, k, high)
-            else:
-                mig.run_target(units, w, f, k, high, low)
+            else:  # one C++ call, or the loop here with the target's other work
+                mig.run_target(units, w, f, k, high, low, other_work=other if with_other else None)
+            k = f"{k}{'+other' if with_other else ''}"
             torch.cuda.synchronize()
             report[f"k={k} no barrier timeout"] = not mig.timed_out()
             dist.barrier()
@@ -70,8 +80,9 @@ def _worker(rank, world, port, result_dir):
                 mig.payback()
                 torch.cuda.synchronize()
                 shadow = torch.zeros(n, dtype=torch.int64, device="cuda")
-                if k:
-                    dev.weighted_fold(units[:k], w[:k], f, shadow)
+                kk = int(k.split("+")[0])
+                if kk:
+                    dev.weighted_fold(units[:kk], w[:kk], f, shadow)
                 torch.cuda.synchronize()
                 report[f"k={k} direct payback equals shadow"] = bool(torch.equal(acc, shadow))
             dist.barrier()
@@ -83,24 +94,26 @@ def _worker(rank, world, port, result_dir):
                                             target_headroom_bytes=1 << 40)
         report["planner k in range"] = 0 <= sched.shadow_microbatches <= M
     except Exception as e:
-        report["error"] = repr(e)
+        import traceback
+        report["error"] = repr(e) + traceback.format_exc()[-1500:]
     Path(result_dir, f"rank{rank}.json").write_text(json.dumps(report))
     dist.destroy_process_group()
 
 
 @pytest.mark.timeout(300)
-def test_layer_migration_payback_bit_exact(tmp_path):
-    if torch.cuda.device_count() < 2:
+@pytest.mark.parametrize("same_device", [False, True], ids=["two_gpus", "one_gpu_two_procs"])
+def test_layer_migration_payback_bit_exact(tmp_path, same_device):
+    if not same_device and torch.cuda.device_count() < 2:
         pytest.skip("needs 2 GPUs")
     import json
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path), same_device), nprocs=2, join=True)
     for r in range(2):
         rep = json.loads((tmp_path / f"rank{r}.json").read_text())
-        assert "error" not in rep, rep
+        assert "error" not in rep, rep.get("error")
         for key, v in rep.items():
             assert v is True, (r, key)
-    assert len(json.loads((tmp_path / "rank1.json").read_text())) == 13
+    assert len(json.loads((tmp_path / "rank1.json").read_text())) == 17
 
 
 def test_payback_accumulate_single_gpu():
