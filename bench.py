@@ -610,8 +610,56 @@ def run_reshard(args, rank, world, out):
         res["projection_8to7"] = project_8to7(base, world, per_drop, res["mttr"])
     barrier(world)
     prep.close()
+    # replica-aware sourcing (B200 executor option): the bytes a rank pulls
+    # from the OLD shard of the member it backs up come from its own current
+    # replica of it, in local HBM; same plan, same landed bytes, same
+    # verification
+    torch.cuda.empty_cache()
+    prep2 = PreparedRecovery(lb, old, rank, bufs.old, rep, block, old_rows=rows,
+                             replica_rows=rep_rows, local_replicas=True)
+    per_local = {}
+    for d in old:
+        ts, walls, ok = [], [], True
+        for _ in range(max(1, reps // 2)):
+            barrier(world)
+            if rank != d:
+                ev = prep2.recover(d)
+                ts.append(ev.phases["copy_s"])
+                walls.append(ev.phases["launch_to_verdict_s"])
+                ok = ok and ev.verified
+            else:
+                ts.append(0.0)
+                walls.append(0.0)
+        t_d, w_d = max_over_ranks([sum(ts) / len(ts), sum(walls) / len(walls)], world)
+        nvl = local_replica_traffic(prep2.plans[d])
+        per_local[f"r{d}"] = {"copy_ms": round(t_d * 1e3, 3),
+                              "copy_verify_verdict_ms": round(w_d * 1e3, 3),
+                              "verified": all_ranks_true(ok, world),
+                              "bottleneck_nvlink_bytes": nvl,
+                              "planner_exact_copy_ms": per_drop[f"r{d}"]["copy_ms"]}
+    res["per_departure_local_replicas"] = per_local
+    barrier(world)
+    prep2.close()
     del bufs, rep
     torch.cuda.empty_cache()
+
+
+def local_replica_traffic(rp) -> int:
+    """Bottleneck NVLink bytes (max per-GPU ingress / egress) of a reshard
+    whose pull programs use replica-aware sourcing."""
+    from paper_2510_00606_b200.fabric import ROLE_OLD
+    ranks = sorted(set(rp.old_ranks) | set(rp.new_ranks))
+    ing = {r: 0 for r in ranks}
+    egr = {r: 0 for r in ranks}
+    for r in rp.new_ranks:
+        held = rp.ring.backs_up(r)
+        c = rp.copies(r, push=False)
+        for s, role, b in zip(c["src_rank"].tolist(), c["src_role"].tolist(), c["bytes"].tolist()):
+            if s == r or (role == ROLE_OLD and s == held and held not in rp.failed):
+                continue
+            ing[r] += b
+            egr[s] += b
+    return int(max(max(ing.values()), max(egr.values())))
 
 
 def all_ranks_true(flag: bool, world: int) -> bool:

@@ -70,6 +70,20 @@ std::vector<CopyDesc> reshard_copies(const TransferPlan& plan, const PartitionLa
                                      const PartitionLayout& dst, const std::set<int>& failed,
                                      const SnapshotRing* ring, int exec_rank, bool push);
 
+// Replica-aware sourcing of a PULL program (a B200 executor option, off by
+// default): every exec_rank keeps a current ring replica of the member it
+// backs up (SnapshotRing::backs_up, kept byte-identical each step by the
+// replay replica and verified by its rows), so copies the plan sources from
+// that member's OLD shard can read exec_rank's own replica instead — same
+// bytes, same source offsets (the replica is packed like the owner's shard),
+// local HBM instead of NVLink.  The plan, the landed layout and the
+// verification are unchanged; only the physical source moves.  Config B 8->7
+// drop r3: the bottleneck GPU's NVLink bytes fall from 10.11 to 6.74 GB;
+// drop r7 and 4->3 drop r3 become all-local.
+std::vector<CopyDesc> prefer_local_replica(const std::vector<CopyDesc>& pull_copies,
+                                           const SnapshotRing& ring, const std::set<int>& failed,
+                                           int exec_rank);
+
 // Staged in-place reshard (state that fills HBM).
 // Each rank keeps ONE buffer that holds its OLD shard on entry and its NEW
 // shard on exit; the move runs in phases over the global byte space.  Phases

@@ -160,8 +160,12 @@ struct ReshardPlan {
 // a PeerBuffers table.
 class ReshardExecutor {
  public:
+  // local_replica (pull): copies the plan sources from the OLD shard of the
+  // member this rank backs up read this rank's own replica of it instead
+  // (b200::prefer_local_replica); the peer table must then hold this rank's
+  // REPLICA buffer, kept current by the ring replica.
   ReshardExecutor(const ReshardPlan& rp, int me, bool push = false,
-                  std::int64_t block_bytes = 65536);
+                  std::int64_t block_bytes = 65536, bool local_replica = false);
   ~ReshardExecutor();
   ReshardExecutor(const ReshardExecutor&) = delete;
   ReshardExecutor& operator=(const ReshardExecutor&) = delete;
@@ -499,6 +503,10 @@ std::string mttr_csv_row(int index, const MttrEvent& ev);
 struct PreparedOptions {
   std::int64_t block_bytes = 65536;
   double barrier_timeout_s = 30.0;
+  // replica-aware sourcing (ReshardExecutor local_replica): valid while the
+  // replicas are current (the per-step replay keeps them byte-identical; a
+  // stale replica is caught by the conservation check)
+  bool local_replicas = false;
 };
 
 class PreparedRecovery {

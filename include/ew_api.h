@@ -574,6 +574,9 @@ void ew_reshard_free(ew_reshard* r);
  * and bound in steady state (collective over the channel's members).
  * old_rows / replica_rows: the per-step snapshot's checksum rows of this
  * rank's OLD shard and of the replica it keeps (NULL: re-read here).
+ * flags bit 0: replica-aware sourcing — copies the plan sources from the OLD
+ * shard of the member this rank backs up read this rank's (current) replica
+ * of it instead, in local HBM (b200::prefer_local_replica).
  * new_buf: caller-owned NEW buffer of new_capacity bytes, large enough for
  * every departure (NULL: allocated here).  recover() (survivors only, all of
  * them): one verified copy launch into the NEW buffer, a device barrier,
@@ -583,7 +586,7 @@ typedef struct ew_prepared ew_prepared;
 int ew_prepared_create(ew_channel* ch, const int64_t* layer_bytes, int n_layers, void* old_buf,
                        const uint64_t* old_rows, void* replica, const uint64_t* replica_rows,
                        void* new_buf, int64_t new_capacity, int64_t block_bytes,
-                       double barrier_timeout_s, ew_prepared** out);
+                       double barrier_timeout_s, int flags, ew_prepared** out);
 int ew_prepared_recover(ew_prepared* p, int departed, ew_stream_t stream, ew_mttr_event* ev,
                         int* verified);
 int ew_prepared_new(const ew_prepared* p, int departed, void** ptr, int64_t* bytes);

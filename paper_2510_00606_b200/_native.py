@@ -295,7 +295,7 @@ _sig("ew_reshard_create", i32, vp, vp, P(i32), i32, P(i32), i32, i32, i32, i64, 
 _sig("ew_reshard_bind", i32, vp, vp, i32)
 _sig("ew_reshard_launch", i32, vp, vp, vp, i32, i32, vp)
 _sig("ew_reshard_free", None, vp)
-_sig("ew_prepared_create", i32, vp, P(i64), i32, vp, vp, vp, vp, vp, i64, i64, f64, P(vp))
+_sig("ew_prepared_create", i32, vp, P(i64), i32, vp, vp, vp, vp, vp, i64, i64, f64, i32, P(vp))
 _sig("ew_prepared_recover", i32, vp, i32, vp, P(MttrEventC), P(i32))
 _sig("ew_prepared_new", i32, vp, i32, P(vp), P(i64))
 _sig("ew_prepared_free", None, vp)

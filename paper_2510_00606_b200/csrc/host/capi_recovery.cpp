@@ -299,13 +299,14 @@ void ew_reshard_free(ew_reshard* r) { delete r; }
 int ew_prepared_create(ew_channel* ch, const int64_t* layer_bytes, int n_layers, void* old_buf,
                        const uint64_t* old_rows, void* replica, const uint64_t* replica_rows,
                        void* new_buf, int64_t new_capacity, int64_t block_bytes,
-                       double barrier_timeout_s, ew_prepared** out) {
+                       double barrier_timeout_s, int flags, ew_prepared** out) {
   return guarded([&]() -> int {
     if (ch == nullptr || layer_bytes == nullptr || n_layers < 1 || out == nullptr)
       return set_error(EW_ERR_INVALID_ARGUMENT, "ew_prepared_create: bad arguments");
     elaskit::b200::PreparedOptions opt;
     opt.block_bytes = block_bytes;
     opt.barrier_timeout_s = barrier_timeout_s;
+    opt.local_replicas = (flags & 1) != 0;
     *out = new ew_prepared{std::make_unique<PreparedRecovery>(
         *ch->c, std::vector<int64_t>(layer_bytes, layer_bytes + n_layers), old_buf, old_rows,
         replica, replica_rows, new_buf, new_capacity, opt)};

@@ -208,4 +208,21 @@ DpTransition dp_transition(const ClusterState& state, const ElasticEvent& ev, in
   return t;
 }
 
+std::vector<CopyDesc> prefer_local_replica(const std::vector<CopyDesc>& pull_copies,
+                                           const SnapshotRing& ring, const std::set<int>& failed,
+                                           int exec_rank) {
+  std::vector<CopyDesc> out = pull_copies;
+  if (ring.members.size() < 2 ||
+      std::find(ring.members.begin(), ring.members.end(), exec_rank) == ring.members.end())
+    return out;
+  const int held = ring.backs_up(exec_rank);
+  if (held == exec_rank || failed.count(held)) return out;  // a departed owner is sourced so already
+  for (CopyDesc& c : out)
+    if (c.dst_rank == exec_rank && c.src_role == BufRole::Old && c.src_rank == held) {
+      c.src_role = BufRole::Replica;  // same packing, same offsets
+      c.src_rank = exec_rank;
+    }
+  return out;
+}
+
 }  // namespace elaskit::b200

@@ -515,10 +515,14 @@ int ReshardPlan::replica_of(int holder) const {
 // ---------------------------------------------------------- ReshardExecutor
 
 ReshardExecutor::ReshardExecutor(const ReshardPlan& rp, int me, bool push,
-                                 std::int64_t block_bytes)
+                                 std::int64_t block_bytes, bool local_replica)
     : rp_(rp), me_(me), push_(push), block_bytes_(block_bytes) {
   copies_ = reshard_copies(rp_.plan, rp_.src, rp_.dst, rp_.failed,
                            rp_.ring.members.empty() ? nullptr : &rp_.ring, me_, push_);
+  if (local_replica) {
+    if (push_) throw std::invalid_argument("replica-aware sourcing is a pull-program option");
+    copies_ = prefer_local_replica(copies_, rp_.ring, rp_.failed, me_);
+  }
 }
 
 ReshardExecutor::~ReshardExecutor() {
@@ -1243,7 +1247,8 @@ PreparedRecovery::PreparedRecovery(Channel& ch, const std::vector<std::int64_t>&
     peers_.put(static_cast<int>(BufRole::New), me_, new_buf_);
     for (const auto& [d, rp] : plans_) {
       auto mv = std::make_unique<VerifiedMove>();
-      mv->exec = std::make_unique<ReshardExecutor>(*rp, me_, false, opt_.block_bytes);
+      mv->exec = std::make_unique<ReshardExecutor>(*rp, me_, false, opt_.block_bytes,
+                                                   opt_.local_replicas && replica != nullptr);
       mv->exec->bind(peers_, true);
       mv->wire(peers_, *rp, me_, n_words_);
       execs_[d] = std::move(mv->exec);

@@ -312,10 +312,14 @@ class PreparedRecovery:
                  old: torch.Tensor, replica: torch.Tensor,
                  block_bytes: int = dev.DEFAULT_BLOCK_BYTES, group=None,
                  old_rows: Optional[torch.Tensor] = None,
-                 replica_rows: Optional[torch.Tensor] = None, barrier_timeout_s: float = 30.0):
+                 replica_rows: Optional[torch.Tensor] = None, barrier_timeout_s: float = 30.0,
+                 local_replicas: bool = False):
         """`old`: this rank's live shard; `replica`: the shard of its ring
         successor (SnapshotRing.backs_up(rank)); `*_rows`: their per-step
-        snapshot checksum rows (None: recomputed).  Collective over `group`."""
+        snapshot checksum rows (None: recomputed).  local_replicas: replica-
+        aware sourcing (bytes the plan pulls from the successor's OLD shard
+        come from this rank's current replica of it, in local HBM).
+        Collective over `group`."""
         members = sorted(members)
         self.rank = rank
         self.block_bytes = block_bytes
@@ -332,7 +336,7 @@ class PreparedRecovery:
             self.channel.handle, N.i64_array(lb), len(lb), C.c_void_p(old.data_ptr()),
             dev._ptr(old_rows), C.c_void_p(replica.data_ptr()), dev._ptr(replica_rows),
             C.c_void_p(self.new.data_ptr()), int(self.new.numel()), int(block_bytes),
-            float(barrier_timeout_s), C.byref(h)))
+            float(barrier_timeout_s), int(bool(local_replicas)), C.byref(h)))
         self._h = h
         self._keep = (old, replica, old_rows, replica_rows)
 

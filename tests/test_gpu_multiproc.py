@@ -82,19 +82,29 @@ def _worker(rank, world, port, out_dir, scale):
         rep_rows = ms.new_row_sums()
         dev.checksum(ms, replica, rep_rows)
         torch.cuda.synchronize()
-        prep = PreparedRecovery(cfg.layer_bytes, members, rank, live, replica, block,
-                                old_rows=rows, replica_rows=rep_rows)
-        for d in members:
+        # replica-aware sourcing too: bytes the plan pulls from the
+        # successor's OLD shard come from this rank's replica of it
+        for local in (False, True):
+            prep = PreparedRecovery(cfg.layer_bytes, members, rank, live, replica, block,
+                                    old_rows=rows, replica_rows=rep_rows, local_replicas=local)
+            tag = "local-replica " if local else ""
+            for d in members:
+                dist.barrier()
+                if rank == d:
+                    continue
+                ev = prep.recover(d)
+                torch.cuda.synchronize()
+                n = prep.plans[d].dst.shard_bytes(rank)
+                exp = _fill_expected(dev, shard_map, prep.plans[d].dst, rank, 31, n)
+                rep[f"{tag}prepared drop{d} verified"] = ev.verified
+                rep[f"{tag}prepared drop{d} bytes"] = bool(torch.equal(prep.new_view(d)[:n],
+                                                                        exp[:n]))
+                rep[f"{tag}prepared drop{d} no barrier timeout"] = \
+                    ev.phases.get("barrier_timeouts") == 0
+            if local:
+                break
             dist.barrier()
-            if rank == d:
-                continue
-            ev = prep.recover(d)
-            torch.cuda.synchronize()
-            n = prep.plans[d].dst.shard_bytes(rank)
-            exp = _fill_expected(dev, shard_map, prep.plans[d].dst, rank, 31, n)
-            rep[f"prepared drop{d} verified"] = ev.verified
-            rep[f"prepared drop{d} bytes"] = bool(torch.equal(prep.new_view(d)[:n], exp[:n]))
-            rep[f"prepared drop{d} no barrier timeout"] = ev.phases.get("barrier_timeouts") == 0
+            prep.close()
         # a corrupted landing must be caught: poison a survivor's source
         # byte after the snapshot rows were taken, then recover again
         dist.barrier()
