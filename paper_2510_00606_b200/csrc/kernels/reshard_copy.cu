@@ -226,24 +226,25 @@ __device__ void checksum_piece(const uint8_t* stage, const Piece& pc, int warp_c
   }
 }
 
-__device__ __forceinline__ uint32_t pick(const uint32_t (&x)[8], int i) {
-  uint32_t r = x[0];  // i is uniform per piece; the select chain stays in registers
-#pragma unroll
-  for (int k = 1; k < 8; ++k) r = (i == k) ? x[k] : r;
-  return r;
-}
-
-// 16 bytes starting at byte `off` (1..15) of the 32-byte pair (a, b).
-__device__ __forceinline__ uint4 realign(const uint4& a, const uint4& b, int off) {
-  const uint32_t x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
-  const int ws = off >> 2;
-  const int bs = (off & 3) * 8;
-  uint4 o;
-  o.x = __funnelshift_r(pick(x, ws + 0), pick(x, ws + 1), bs);
-  o.y = __funnelshift_r(pick(x, ws + 1), pick(x, ws + 2), bs);
-  o.z = __funnelshift_r(pick(x, ws + 2), pick(x, ws + 3), bs);
-  o.w = __funnelshift_r(pick(x, ws + 3), pick(x, ws + 4), bs);
-  return o;
+// The piece's vectors realigned by a compile-time byte offset OFF (1..15):
+// four funnel shifts with constant word indices per 16-byte vector (the
+// select chain of realign() costs ~60 instructions per vector; all-local
+// programs — replica-aware recoveries, config D's 2->1 — are bound by it).
+template <int OFF>
+__device__ __forceinline__ void copy_realigned(uint8_t* db, const uint8_t* sb, int nv, int ctid) {
+  constexpr int kC = 32 * kConsumerWarps;
+  constexpr int ws = OFF >> 2, bs = (OFF & 3) * 8;
+#pragma unroll 4
+  for (int j = ctid; j < nv; j += kC) {
+    const uint4 a = lds128(sb + 16 * j), b = lds128(sb + 16 * j + 16);
+    const uint32_t x[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint4 o;
+    o.x = __funnelshift_r(x[ws + 0], x[ws + 1], bs);
+    o.y = __funnelshift_r(x[ws + 1], x[ws + 2], bs);
+    o.z = __funnelshift_r(x[ws + 2], x[ws + 3], bs);
+    o.w = __funnelshift_r(x[ws + 3], x[ws + 4], bs);
+    st_plain(db + 16 * j, o);
+  }
 }
 
 // Consumers write one staged piece.  `stage` holds the source window that
@@ -266,13 +267,27 @@ __device__ __forceinline__ void write_piece(const uint8_t* stage, const Piece& p
 #pragma unroll 4
     for (int j = ctid; j < nv; j += kC) st_plain(db + 16 * j, lds128(sb + 16 * j));
   } else {
-#pragma unroll 4
-    for (int j = ctid; j < nv; j += kC)
-      st_plain(db + 16 * j, realign(lds128(sb + 16 * j), lds128(sb + 16 * j + 16), off));
+    switch (off) {  // uniform per piece
+      case 1: copy_realigned<1>(db, sb, nv, ctid); break;
+      case 2: copy_realigned<2>(db, sb, nv, ctid); break;
+      case 3: copy_realigned<3>(db, sb, nv, ctid); break;
+      case 4: copy_realigned<4>(db, sb, nv, ctid); break;
+      case 5: copy_realigned<5>(db, sb, nv, ctid); break;
+      case 6: copy_realigned<6>(db, sb, nv, ctid); break;
+      case 7: copy_realigned<7>(db, sb, nv, ctid); break;
+      case 8: copy_realigned<8>(db, sb, nv, ctid); break;
+      case 9: copy_realigned<9>(db, sb, nv, ctid); break;
+      case 10: copy_realigned<10>(db, sb, nv, ctid); break;
+      case 11: copy_realigned<11>(db, sb, nv, ctid); break;
+      case 12: copy_realigned<12>(db, sb, nv, ctid); break;
+      case 13: copy_realigned<13>(db, sb, nv, ctid); break;
+      case 14: copy_realigned<14>(db, sb, nv, ctid); break;
+      default: copy_realigned<15>(db, sb, nv, ctid); break;
+    }
   }
 }
 
-__global__ void __launch_bounds__(kThreads) staged_copy_kernel(const CopyItem* __restrict__ items,
+__global__ void __launch_bounds__(kThreads, 2) staged_copy_kernel(const CopyItem* __restrict__ items,
                                                                int64_t n_remote,
                                                                int64_t remote_pieces,
                                                                int64_t n_local,
@@ -552,14 +567,19 @@ static int launch_program(const ew_copy_program* prog, int n_ctas, int remote_ct
   if (prog == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL program");
   if (prog->remote_pieces + prog->local_pieces == 0) return EW_OK;
   const int sms = num_sms();
-  if (n_ctas <= 0) n_ctas = 2 * sms;  // two 96 KiB rings per SM
+  const bool mixed = prog->remote_pieces > 0 && prog->local_pieces > 0;
+  // two 96 KiB rings per SM; a mixed program runs its local class one CTA
+  // per SM: with the constant-shift realign the local copies would otherwise
+  // finish early and press on the HBM the peers are still pulling from
+  // (r01 A/B at 4->3: 148 local CTAs 10.95 ms vs 222 local CTAs 11.32 ms)
+  if (n_ctas <= 0) n_ctas = mixed ? sms + std::max(1, sms / 2) : 2 * sms;
   if (prog->remote_pieces == 0) remote_ctas = 0;
   else if (prog->local_pieces == 0) remote_ctas = n_ctas;
   else if (remote_ctas <= 0 || remote_ctas >= n_ctas)
-    // NVLink class: a quarter of the CTAs, verified or not (N=4 sweep,
-    // tools/verify_dbg.sh: 74 CTAs 11.07 ms verified vs 11.11 ms plain;
-    // 98 CTAs 11.2 ms); callers sweep through the remote_ctas argument
-    remote_ctas = std::max(1, n_ctas / 4);
+    // NVLink class: half an SM's worth of CTAs per SM pair, verified or not
+    // (N=4 sweep: 74 CTAs 11.07 ms verified vs 11.11 ms plain; 98 CTAs
+    // 11.2 ms); callers sweep through the remote_ctas argument
+    remote_ctas = std::max(1, std::min(n_ctas - 1, sms / 2));
   staged_copy_kernel<<<n_ctas, kThreads, kSmem, (cudaStream_t)stream>>>(
       prog->d_items, prog->n_remote, prog->remote_pieces, prog->n_local, prog->local_pieces,
       remote_ctas, reinterpret_cast<unsigned long long*>(block_sums), prog->word_shift,
