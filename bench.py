@@ -638,7 +638,35 @@ def run_reshard(args, rank, world, out):
                               "bottleneck_nvlink_bytes": nvl,
                               "planner_exact_copy_ms": per_drop[f"r{d}"]["copy_ms"]}
     res["per_departure_local_replicas"] = per_local
+    # the same FailStop through DpGroup.recover with the replica-aware
+    # programs attached: the measured MTTR of this option
     barrier(world)
+    uid = [dev.Communicator.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm3 = dev.Communicator.init(uid[0], world, rank)
+    comm3.allreduce_i64(warm)
+    grp3 = DpGroup(lb, old, rank, comm3, prepare_comms=True, block_bytes=block)
+    grp3.attach(prep2)
+    torch.cuda.synchronize()
+    barrier(world)
+    if rank != drop:
+        ev = grp3.recover([drop], step=1)
+        vals = [ev.comm_repair_s, ev.other_s, ev.remap_s, ev.total_s()]
+        ok = ev.verified
+    else:
+        vals, ok = [0.0] * 4, True
+    vals = max_over_ranks(vals, world)
+    res["mttr_local_replicas"] = {
+        "what": "the measured FailStop of rank {} through DpGroup.recover with replica-aware "
+                "programs (max over survivors)".format(drop),
+        "comm_repair_ms": round(vals[0] * 1e3, 3), "reshape_ms": round(vals[1] * 1e3, 3),
+        "remap_ms": round(vals[2] * 1e3, 3), "total_ms": round(vals[3] * 1e3, 3),
+        "verified": all_ranks_true(ok, world)}
+    if world in (2, 4, 6) and args.reshard_state_gb <= 0:
+        res["projection_8to7_local_replicas"] = project_8to7_local(base, world, per_drop,
+                                                                  per_local, res["mttr"])
+    barrier(world)
+    grp3.close()
     prep2.close()
     del bufs, rep
     torch.cuda.empty_cache()
@@ -808,6 +836,38 @@ def project_8to7(base, world, per_drop, prepared):
         copy_ms = b / (gbs * 1e9) * 1e3
         res[f"drop_r{d}"] = {"bottleneck_gpu_bytes": b, "rate_gbs": gbs,
                              "copy_ms": round(copy_ms, 2), "mttr_ms": round(copy_ms + overhead_ms, 2)}
+    return res
+
+
+def project_8to7_local(base, world, per_drop, per_local, mttr):
+    """Config B's 8->7 MTTR with replica-aware programs, for pools with fewer
+    than 8 GPUs (a projection): the larger of the NVLink lane time (the
+    8->7 plan's replica-aware bottleneck bytes at the bottleneck-link rate
+    measured here for the same kind of departure) and the local-copy time
+    (NEW bytes per GPU at the all-local rate measured here), plus the
+    measured non-copy MTTR."""
+    from paper_2510_00606_b200.reshard import ReshardPlan
+
+    rate = {k: v["bottleneck_nvlink_gbs"] for k, v in per_drop.items()}
+    interior = [rate[f"r{d}"] for d in range(1, world - 1) if rate.get(f"r{d}")]
+    kinds = {0: rate.get("r0"), 7: rate.get(f"r{world - 1}"),
+             3: min(interior) if interior else rate.get(f"r{world - 1}")}
+    lb_here = base.layer_bytes if world == 8 else [x * world // 8 for x in base.layer_bytes]
+    here = ReshardPlan.build(lb_here, list(range(world)), [r for r in range(world) if r != world - 1])
+    local_gbs = max(here.dst.shard_bytes(r) for r in here.new_ranks) / \
+        (per_local[f"r{world - 1}"]["copy_ms"] / 1e3) / 1e9     # all-local at N -> N-1, last rank
+    overhead_ms = mttr["total_ms"] - mttr["phases_ms"]["copy"]
+    res = {"what": "projection, not a measurement: max(replica-aware NVLink bottleneck bytes / "
+                   f"measured link rate, NEW bytes / measured all-local rate {local_gbs:.0f} "
+                   "GB/s) + measured non-copy MTTR", "overhead_ms": round(overhead_ms, 3)}
+    for d, gbs in kinds.items():
+        rp = ReshardPlan.build(base.layer_bytes, list(range(8)), [r for r in range(8) if r != d])
+        nvl = local_replica_traffic(rp)
+        new_max = max(rp.dst.shard_bytes(r) for r in rp.new_ranks)
+        t_nvl = nvl / (gbs * 1e9) * 1e3 if nvl and gbs else 0.0
+        t_loc = new_max / (local_gbs * 1e9) * 1e3
+        res[f"drop_r{d}"] = {"nvlink_bottleneck_bytes": nvl, "copy_ms": round(max(t_nvl, t_loc), 2),
+                             "mttr_ms": round(max(t_nvl, t_loc) + overhead_ms, 2)}
     return res
 
 
