@@ -58,6 +58,8 @@ class Store {
   virtual ~Store() = default;
   virtual void set(const std::string& key, const std::string& value) = 0;
   virtual std::string get(const std::string& key) = 0;
+  // drop a key nobody will read again (default: keep it)
+  virtual void erase(const std::string& key) { (void)key; }
 };
 
 // TCP store: rank `is_server` hosts it on host:port (a listening thread), every
@@ -65,13 +67,18 @@ class Store {
 std::unique_ptr<Store> tcp_store(const std::string& host, int port, bool is_server,
                                  double timeout_s = 300.0);
 
-// Store over two caller callbacks (the C ABI's ew_store_callbacks).
+// Store over caller callbacks (the C ABI's ew_store_callbacks); `erase` may
+// be empty.
 std::unique_ptr<Store> callback_store(std::function<void(const std::string&, const std::string&)> set,
-                                      std::function<std::string(const std::string&)> get);
+                                      std::function<std::string(const std::string&)> get,
+                                      std::function<void(const std::string&)> erase = {});
 
 // Collective operations among an ordered member list over a Store.  Every
 // member issues the same sequence of calls; a per-channel counter names the
-// keys, so channels with distinct `name`s never collide.
+// keys, so channels with distinct `name`s never collide.  A member erases
+// its key of round k-1 once it has completed round k (every member has then
+// set its round-k key, so nobody still reads round k-1): the store holds at
+// most two rounds per channel.
 class Channel {
  public:
   Channel(Store& store, std::string name, std::vector<int> members, int me);

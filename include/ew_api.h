@@ -518,7 +518,11 @@ typedef int (*ew_store_set_fn)(void* ctx, const char* key, int64_t key_len, cons
                                int64_t len);
 typedef int (*ew_store_get_fn)(void* ctx, const char* key, int64_t key_len, char* buf,
                                int64_t cap, int64_t* len);
-int ew_store_callbacks(ew_store_set_fn set, ew_store_get_fn get, void* ctx, ew_store** out);
+/* erase (may be NULL): drop a key no member will read again; channels erase
+ * their keys two rounds behind, so a store holds O(channels x members). */
+typedef int (*ew_store_erase_fn)(void* ctx, const char* key, int64_t key_len);
+int ew_store_callbacks(ew_store_set_fn set, ew_store_get_fn get, ew_store_erase_fn erase,
+                       void* ctx, ew_store** out);
 int ew_store_set(ew_store* store, const char* key, const void* val, int64_t len);
 int ew_store_get(ew_store* store, const char* key, void* buf, int64_t cap, int64_t* len);
 void ew_store_free(ew_store* store);

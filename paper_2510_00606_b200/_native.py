@@ -274,9 +274,10 @@ class MttrEventC(C.Structure):
 
 STORE_SET_FN = C.CFUNCTYPE(i32, vp, C.POINTER(C.c_char), i64, C.POINTER(C.c_char), i64)
 STORE_GET_FN = C.CFUNCTYPE(i32, vp, C.POINTER(C.c_char), i64, C.POINTER(C.c_char), i64, P(i64))
+STORE_ERASE_FN = C.CFUNCTYPE(i32, vp, C.POINTER(C.c_char), i64)
 
 _sig("ew_store_tcp", i32, C.c_char_p, i32, i32, f64, P(vp))
-_sig("ew_store_callbacks", i32, STORE_SET_FN, STORE_GET_FN, vp, P(vp))
+_sig("ew_store_callbacks", i32, STORE_SET_FN, STORE_GET_FN, STORE_ERASE_FN, vp, P(vp))
 _sig("ew_store_set", i32, vp, C.c_char_p, vp, i64)
 _sig("ew_store_get", i32, vp, C.c_char_p, vp, i64, P(i64))
 _sig("ew_store_free", None, vp)

@@ -132,7 +132,8 @@ int ew_store_tcp(const char* host, int port, int is_server, double timeout_s, ew
   });
 }
 
-int ew_store_callbacks(ew_store_set_fn set, ew_store_get_fn get, void* ctx, ew_store** out) {
+int ew_store_callbacks(ew_store_set_fn set, ew_store_get_fn get, ew_store_erase_fn erase,
+                       void* ctx, ew_store** out) {
   return guarded([&]() -> int {
     if (set == nullptr || get == nullptr || out == nullptr)
       return set_error(EW_ERR_INVALID_ARGUMENT, "ew_store_callbacks: bad arguments");
@@ -157,7 +158,13 @@ int ew_store_callbacks(ew_store_set_fn set, ew_store_get_fn get, void* ctx, ew_s
       }
       throw std::runtime_error("store get callback: size changed between calls for " + k);
     };
-    *out = new ew_store{elaskit::b200::callback_store(s, g)};
+    std::function<void(const std::string&)> e;
+    if (erase != nullptr)
+      e = [erase, ctx](const std::string& k) {
+        if (erase(ctx, k.data(), static_cast<int64_t>(k.size())) != 0)
+          throw std::runtime_error("store erase callback failed for key " + k);
+      };
+    *out = new ew_store{elaskit::b200::callback_store(s, g, e)};
     return EW_OK;
   });
 }

@@ -167,6 +167,13 @@ class TcpServer {
         cv_.notify_all();
         const char ack = 1;
         if (!send_all(c, &ack, 1)) break;
+      } else if (op == 'D') {
+        {
+          std::lock_guard<std::mutex> lk(mu_);
+          data_.erase(key);
+        }
+        const char ack = 1;
+        if (!send_all(c, &ack, 1)) break;
       } else if (op == 'G') {
         std::string v;
         {
@@ -238,6 +245,15 @@ class TcpStore final : public Store {
         !send_all(fd_, &vl, 8) || !send_all(fd_, value.data(), vl) || !recv_all(fd_, &ack, 1))
       throw std::runtime_error("tcp store: set(" + key + ") failed");
   }
+  void erase(const std::string& key) override {
+    std::lock_guard<std::mutex> lk(mu_);
+    const char op = 'D';
+    const uint32_t kl = static_cast<uint32_t>(key.size());
+    char ack = 0;
+    if (!send_all(fd_, &op, 1) || !send_all(fd_, &kl, 4) || !send_all(fd_, key.data(), kl) ||
+        !recv_all(fd_, &ack, 1))
+      throw std::runtime_error("tcp store: erase(" + key + ") failed");
+  }
   std::string get(const std::string& key) override {
     std::lock_guard<std::mutex> lk(mu_);
     const char op = 'G';
@@ -260,14 +276,19 @@ class TcpStore final : public Store {
 class CallbackStore final : public Store {
  public:
   CallbackStore(std::function<void(const std::string&, const std::string&)> s,
-                std::function<std::string(const std::string&)> g)
-      : set_(std::move(s)), get_(std::move(g)) {}
+                std::function<std::string(const std::string&)> g,
+                std::function<void(const std::string&)> e)
+      : set_(std::move(s)), get_(std::move(g)), erase_(std::move(e)) {}
   void set(const std::string& k, const std::string& v) override { set_(k, v); }
   std::string get(const std::string& k) override { return get_(k); }
+  void erase(const std::string& k) override {
+    if (erase_) erase_(k);
+  }
 
  private:
   std::function<void(const std::string&, const std::string&)> set_;
   std::function<std::string(const std::string&)> get_;
+  std::function<void(const std::string&)> erase_;
 };
 
 // ------------------------------------------------------------ small helpers
@@ -372,8 +393,9 @@ std::unique_ptr<Store> tcp_store(const std::string& host, int port, bool is_serv
 
 std::unique_ptr<Store> callback_store(
     std::function<void(const std::string&, const std::string&)> set,
-    std::function<std::string(const std::string&)> get) {
-  return std::make_unique<CallbackStore>(std::move(set), std::move(get));
+    std::function<std::string(const std::string&)> get,
+    std::function<void(const std::string&)> erase) {
+  return std::make_unique<CallbackStore>(std::move(set), std::move(get), std::move(erase));
 }
 
 // ------------------------------------------------------------------ Channel
@@ -388,11 +410,15 @@ Channel::Channel(Store& store, std::string name, std::vector<int> members, int m
 }
 
 std::vector<std::string> Channel::allgather(const std::string& mine) {
-  const std::string base = name_ + "/" + std::to_string(seq_++) + "/";
+  const std::uint64_t round = seq_++;
+  const std::string base = name_ + "/" + std::to_string(round) + "/";
   store_.set(base + std::to_string(me_), mine);
   std::vector<std::string> out;
   out.reserve(members_.size());
   for (int m : members_) out.push_back(m == me_ ? mine : store_.get(base + std::to_string(m)));
+  // every member has set its key of this round, so it finished reading the
+  // previous one: that round's key of ours can go
+  if (round > 0) store_.erase(name_ + "/" + std::to_string(round - 1) + "/" + std::to_string(me_));
   return out;
 }
 

@@ -3,7 +3,7 @@ Channel through the C ABI).
 
 A Store is the key-value channel the ranks of a DP group meet on: the
 library's own TCP store (`Store.tcp`), or torch.distributed's c10d store
-plugged in through two callbacks (`Store.from_torch`, the default when a
+plugged in through callbacks (`Store.from_torch`, the default when a
 process group exists).  A Channel is an ordered member list on a store; its
 collectives (allgather, barrier, sum) are what the C++ executors use to
 exchange CUDA IPC handles and verdicts.  Plumbing only: no model byte or
@@ -66,10 +66,18 @@ class Store:
             except Exception:  # noqa: BLE001
                 return 12
 
+        def erase_cb(_ctx, key, klen):
+            try:
+                store.delete_key(C.string_at(key, klen).decode())
+                return 0
+            except Exception:  # noqa: BLE001
+                return 12
+
         s_fn, g_fn = N.STORE_SET_FN(set_cb), N.STORE_GET_FN(get_cb)
+        e_fn = N.STORE_ERASE_FN(erase_cb)
         h = C.c_void_p()
-        check(lib.ew_store_callbacks(s_fn, g_fn, None, C.byref(h)))
-        return cls(h, keep=(s_fn, g_fn, store))
+        check(lib.ew_store_callbacks(s_fn, g_fn, e_fn, None, C.byref(h)))
+        return cls(h, keep=(s_fn, g_fn, e_fn, store))
 
     def set(self, key: str, value: bytes) -> None:
         check(lib.ew_store_set(self._h, key.encode(), value, len(value)))
