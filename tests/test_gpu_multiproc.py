@@ -356,3 +356,49 @@ def test_multiprocess_recovery_on_one_gpu(world, tmp_path):
             assert v is True, (r, k, v)
             checks += 1
     assert checks > 20 * world
+
+
+def _timeout_worker(rank, world, port, out_dir):
+    """Rank 1 never arrives at the device barrier: rank 0's barrier times out
+    (no hang), and the copy gated on the barrier's error flag writes nothing
+    (a timed-out barrier must veto the in-place writes that would
+    overwrite bytes a lagging peer has not read)."""
+    import json
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    import torch.distributed as dist
+    from paper_2510_00606_b200 import device as dev
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rep = {}
+    try:
+        bar = dev.PeerBarrier(timeout_s=0.5)
+        src = dev.empty_bytes(1 << 20)
+        src.fill_(0x5A)
+        dst = torch.zeros_like(src)
+        prog = dev.CopyProgram.from_pointers([src.data_ptr()], [dst.data_ptr()], [1 << 20], [False])
+        if rank == 0:
+            bar.wait()
+            prog.launch(abort_flag=bar.error_flag)
+            torch.cuda.synchronize()
+            rep["barrier timed out"] = bar.timed_out()
+            rep["vetoed copy wrote nothing"] = int(dst.count_nonzero()) == 0
+        dist.barrier()
+        bar.close()
+    except Exception as e:  # noqa: BLE001
+        rep["error"] = repr(e)
+    Path(out_dir, f"t{rank}.json").write_text(json.dumps(rep))
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_barrier_timeout_vetoes_gated_writes(tmp_path):
+    import json
+    import torch.multiprocessing as mp
+    mp.spawn(_timeout_worker, args=(2, _port(), str(tmp_path)), nprocs=2, join=True)
+    rep = json.loads((tmp_path / "t0.json").read_text())
+    assert "error" not in rep, rep
+    assert rep == {"barrier timed out": True, "vetoed copy wrote nothing": True}
