@@ -366,6 +366,19 @@ int ew_fixed_point_bits(double global_absmax, int64_t total_units, int* frac_bit
 int ew_weighted_fold(const float* const* units, const double* weights, int n_units,
                      int64_t n_elems, int frac_bits, int64_t* acc, int accumulate,
                      ew_stream_t stream);
+/* The same steps with the scale in device memory (no host round trip: the
+ * whole (d) step is stream-ordered and CUDA-graph capturable).
+ * ew_fixed_point_bits_async writes ew_fixed_point_bits(*global_absmax,
+ * total_units) to *frac_bits (device int), INT_MIN for a non-finite or
+ * negative absmax (the _dev fold and dequant then produce zeros; check the
+ * bits after the step). */
+int ew_fixed_point_bits_async(const double* global_absmax, int64_t total_units, int* frac_bits,
+                              ew_stream_t stream);
+int ew_weighted_fold_dev(const float* const* units, const double* weights, int n_units,
+                         int64_t n_elems, const int* frac_bits, int64_t* acc, int accumulate,
+                         const int64_t* addend, ew_stream_t stream);
+int ew_fixed_to_float_dev(const int64_t* acc, int64_t n, const int* frac_bits, float* out,
+                          ew_stream_t stream);
 /* Shadow-gradient payback of a non-blocking layer migration: acc[i] +=
  * payback[i] (int64 fixed point, so the split of micro-batches between the
  * source's shadow instance and the target is bit-exactly invisible).
@@ -413,6 +426,11 @@ int ew_allreduce_max_f64(ew_comm* comm, double* buf, int64_t n, ew_stream_t stre
 int ew_weighted_reduce(ew_comm* comm, const float* const* units, const double* weights,
                        int n_units, int64_t total_units, int64_t n_elems, int64_t* ws_acc,
                        double* ws_max, float* out, int* frac_bits_out, ew_stream_t stream);
+/* Same, fully asynchronous: the scale lives in *ws_bits (device int); no host
+ * synchronisation, so the step can be captured in a CUDA graph. */
+int ew_weighted_reduce_async(ew_comm* comm, const float* const* units, const double* weights,
+                             int n_units, int64_t total_units, int64_t n_elems, int64_t* ws_acc,
+                             double* ws_max, int* ws_bits, float* out, ew_stream_t stream);
 
 /* (d) fused with its collective over NVLink peer memory (no NCCL): the same
  * quantised int64 sums, bit-identical to ew_weighted_reduce.  unit_ptrs lists

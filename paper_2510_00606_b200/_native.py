@@ -225,6 +225,10 @@ _sig("ew_weighted_fold", i32, P(vp), P(f64), i32, i64, i32, vp, i32, vp)
 _sig("ew_weighted_fold_addend", i32, P(vp), P(f64), i32, i64, i32, vp, i32, vp, vp)
 _sig("ew_fixed_to_float", i32, vp, i64, i32, vp, vp)
 _sig("ew_fixed_to_double", i32, vp, i64, i32, vp, vp)
+_sig("ew_fixed_point_bits_async", i32, vp, i64, vp, vp)
+_sig("ew_weighted_fold_dev", i32, P(vp), P(f64), i32, i64, vp, vp, i32, vp, vp)
+_sig("ew_fixed_to_float_dev", i32, vp, i64, vp, vp, vp)
+_sig("ew_weighted_reduce_async", i32, vp, P(vp), P(f64), i32, i64, i64, vp, vp, vp, vp, vp)
 
 _sig("ew_comm_unique_id", i32, C.c_char_p)
 _sig("ew_comm_init", i32, C.c_char_p, i32, i32, P(vp))

@@ -81,10 +81,41 @@ __global__ void __launch_bounds__(256) absmax_kernel(Units u, int64_t n,
   }
 }
 
+// Fixed-point bits computed on the device (ew_fixed_point_bits_async): the
+// whole (d) step can then run without a host round trip (CUDA-graph
+// capturable).  kBadBits marks a non-finite or negative absmax.
+constexpr int kBadBits = -2147483647 - 1;
+
+__device__ __forceinline__ double device_scale(const int* bits, double host_scale) {
+  if (bits == nullptr) return host_scale;
+  const int f = *bits;
+  return f == kBadBits ? 0.0 : ldexp(1.0, f);  // a bad scale folds to zeros
+}
+
+__global__ void scale_kernel(const double* __restrict__ gmax, int64_t total_units,
+                             int* __restrict__ bits) {
+  const double m = *gmax;
+  if (!isfinite(m) || m < 0) {
+    *bits = kBadBits;
+    return;
+  }
+  if (m == 0.0) {
+    *bits = 0;
+    return;
+  }
+  int e = 0;
+  frexp(m, &e);  // m < 2^e
+  int cu = 0;
+  while ((int64_t{1} << cu) < total_units) ++cu;
+  *bits = min(1000, 62 - e - cu);  // total_units * m * 2^F < 2^62, as ew_fixed_point_bits
+}
+
 template <bool kAccumulate>
-__global__ void __launch_bounds__(256) fold_kernel(Units u, int64_t n, double scale,
+__global__ void __launch_bounds__(256) fold_kernel(Units u, int64_t n, double host_scale,
                                                    long long* __restrict__ acc,
-                                                   const long long* __restrict__ addend) {
+                                                   const long long* __restrict__ addend,
+                                                   const int* __restrict__ dev_bits) {
+  const double scale = device_scale(dev_bits, host_scale);
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t n8 = n / 8;
   // 256-bit path: 8 elements per group, one 32-byte load per unit, two
@@ -180,7 +211,10 @@ __device__ __forceinline__ void store8<double>(double* out, int64_t g, const dou
 
 template <typename T>
 __global__ void __launch_bounds__(256) dequant_kernel(const long long* __restrict__ acc, int64_t n,
-                                                      double inv_scale, T* __restrict__ out) {
+                                                      double host_inv_scale, T* __restrict__ out,
+                                                      const int* __restrict__ dev_bits) {
+  const double inv_scale = dev_bits == nullptr ? host_inv_scale
+                           : (*dev_bits == kBadBits ? 0.0 : ldexp(1.0, -*dev_bits));
   constexpr int kDepth = 2;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   const int64_t t0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -292,16 +326,22 @@ int ew_weighted_fold(const float* const* units, const double* weights, int n_uni
                                  nullptr, stream);
 }
 
-int ew_weighted_fold_addend(const float* const* units, const double* weights, int n_units,
-                            int64_t n_elems, int frac_bits, int64_t* acc, int accumulate,
-                            const int64_t* addend, ew_stream_t stream) {
+}  // extern "C"
+
+namespace ew {
+namespace {
+
+// fold with the scale 2^frac_bits, or 2^(*dev_bits) when dev_bits != NULL
+int fold_impl(const float* const* units, const double* weights, int n_units, int64_t n_elems,
+              int frac_bits, const int* dev_bits, int64_t* acc, int accumulate,
+              const int64_t* addend, ew_stream_t stream) {
   if ((n_elems > 0 && acc == nullptr) || n_units < 0 || n_elems < 0 ||
       (n_units > 0 && (!units || !weights)))
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_weighted_fold: bad arguments");
-  if (frac_bits > 1000 || frac_bits < -1000)
+  if (dev_bits == nullptr && (frac_bits > 1000 || frac_bits < -1000))
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_weighted_fold: frac_bits out of range");
   if (n_elems == 0) return EW_OK;
-  const double scale = std::ldexp(1.0, frac_bits);
+  const double scale = dev_bits == nullptr ? std::ldexp(1.0, frac_bits) : 0.0;
   if (n_units == 0) {
     if (!accumulate)
       EW_CUDA_TRY(cudaMemsetAsync(acc, 0, n_elems * sizeof(int64_t), (cudaStream_t)stream));
@@ -317,36 +357,72 @@ int ew_weighted_fold_addend(const float* const* units, const double* weights, in
     long long* a = reinterpret_cast<long long*>(acc);
     const long long* add = off == 0 ? reinterpret_cast<const long long*>(addend) : nullptr;
     if (accumulate || off > 0)
-      fold_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a, add);
+      fold_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a, add,
+                                                                dev_bits);
     else
-      fold_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a, add);
+      fold_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a, add,
+                                                                 dev_bits);
     EW_CUDA_TRY(cudaGetLastError());
   }
   return EW_OK;
 }
 
-int ew_fixed_to_float(const int64_t* acc, int64_t n, int frac_bits, float* out,
-                      ew_stream_t stream) {
+template <typename T>
+int dequant_impl(const int64_t* acc, int64_t n, int frac_bits, const int* dev_bits, T* out,
+                 ew_stream_t stream) {
   if ((n > 0 && (!acc || !out)) || n < 0)
-    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fixed_to_float: bad arguments");
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fixed_to_float/double: bad arguments");
   if (n == 0) return EW_OK;
-  dequant_kernel<float><<<resident_grid((const void*)dequant_kernel<float>, (n + 7) / 8), 256, 0,
-                          (cudaStream_t)stream>>>(
-      reinterpret_cast<const long long*>(acc), n, std::ldexp(1.0, -frac_bits), out);
+  dequant_kernel<T><<<resident_grid((const void*)dequant_kernel<T>, (n + 7) / 8), 256, 0,
+                      (cudaStream_t)stream>>>(reinterpret_cast<const long long*>(acc), n,
+                                              std::ldexp(1.0, -frac_bits), out, dev_bits);
   EW_CUDA_TRY(cudaGetLastError());
   return EW_OK;
 }
 
-int ew_fixed_to_double(const int64_t* acc, int64_t n, int frac_bits, double* out,
-                       ew_stream_t stream) {
-  if ((n > 0 && (!acc || !out)) || n < 0)
-    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fixed_to_double: bad arguments");
-  if (n == 0) return EW_OK;
-  dequant_kernel<double><<<resident_grid((const void*)dequant_kernel<double>, (n + 7) / 8), 256,
-                           0, (cudaStream_t)stream>>>(
-      reinterpret_cast<const long long*>(acc), n, std::ldexp(1.0, -frac_bits), out);
+}  // namespace
+}  // namespace ew
+
+extern "C" {
+
+int ew_weighted_fold_addend(const float* const* units, const double* weights, int n_units,
+                            int64_t n_elems, int frac_bits, int64_t* acc, int accumulate,
+                            const int64_t* addend, ew_stream_t stream) {
+  return fold_impl(units, weights, n_units, n_elems, frac_bits, nullptr, acc, accumulate, addend,
+                   stream);
+}
+
+int ew_fixed_point_bits_async(const double* global_absmax, int64_t total_units, int* frac_bits,
+                              ew_stream_t stream) {
+  if (global_absmax == nullptr || frac_bits == nullptr || total_units < 1)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fixed_point_bits_async: bad arguments");
+  scale_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(global_absmax, total_units, frac_bits);
   EW_CUDA_TRY(cudaGetLastError());
   return EW_OK;
+}
+
+int ew_weighted_fold_dev(const float* const* units, const double* weights, int n_units,
+                         int64_t n_elems, const int* frac_bits, int64_t* acc, int accumulate,
+                         const int64_t* addend, ew_stream_t stream) {
+  if (frac_bits == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL frac_bits");
+  return fold_impl(units, weights, n_units, n_elems, 0, frac_bits, acc, accumulate, addend,
+                   stream);
+}
+
+int ew_fixed_to_float_dev(const int64_t* acc, int64_t n, const int* frac_bits, float* out,
+                          ew_stream_t stream) {
+  if (frac_bits == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL frac_bits");
+  return dequant_impl<float>(acc, n, 0, frac_bits, out, stream);
+}
+
+int ew_fixed_to_float(const int64_t* acc, int64_t n, int frac_bits, float* out,
+                      ew_stream_t stream) {
+  return dequant_impl<float>(acc, n, frac_bits, nullptr, out, stream);
+}
+
+int ew_fixed_to_double(const int64_t* acc, int64_t n, int frac_bits, double* out,
+                       ew_stream_t stream) {
+  return dequant_impl<double>(acc, n, frac_bits, nullptr, out, stream);
 }
 
 }  // extern "C"

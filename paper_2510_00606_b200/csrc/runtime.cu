@@ -391,4 +391,22 @@ int ew_weighted_reduce(ew_comm* comm, const float* const* units, const double* w
   return EW_OK;
 }
 
+int ew_weighted_reduce_async(ew_comm* comm, const float* const* units, const double* weights,
+                             int n_units, int64_t total_units, int64_t n_elems, int64_t* ws_acc,
+                             double* ws_max, int* ws_bits, float* out, ew_stream_t stream) {
+  if (comm == nullptr || ws_acc == nullptr || ws_max == nullptr || ws_bits == nullptr ||
+      out == nullptr)
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_weighted_reduce_async: NULL argument");
+  // every step stream-ordered on the device: no host round trip, capturable
+  // in a CUDA graph together with the collectives
+  if (int st = ew_weighted_absmax(units, weights, n_units, n_elems, ws_max, stream)) return st;
+  if (int st = ew_allreduce_max_f64(comm, ws_max, 1, stream)) return st;
+  if (int st = ew_fixed_point_bits_async(ws_max, total_units, ws_bits, stream)) return st;
+  if (int st = ew_weighted_fold_dev(units, weights, n_units, n_elems, ws_bits, ws_acc, 0, nullptr,
+                                    stream))
+    return st;
+  if (int st = ew_allreduce_i64(comm, ws_acc, n_elems, stream)) return st;
+  return ew_fixed_to_float_dev(ws_acc, n_elems, ws_bits, out, stream);
+}
+
 }  // extern "C"

@@ -323,6 +323,36 @@ def fixed_to_float(acc: torch.Tensor, frac_bits: int, out: Optional[torch.Tensor
     return out
 
 
+def fixed_point_bits_async(global_absmax: torch.Tensor, total_units: int,
+                           bits: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """ew_fixed_point_bits_async: the scale computed on the device (int32)."""
+    if bits is None:
+        bits = torch.empty(1, dtype=torch.int32, device="cuda")
+    check(lib.ew_fixed_point_bits_async(_ptr(global_absmax), int(total_units), _ptr(bits),
+                                        _stream(stream)))
+    return bits
+
+
+def weighted_fold_dev(units, weights, bits: torch.Tensor, acc: torch.Tensor,
+                      accumulate: bool = False, stream=None) -> torch.Tensor:
+    """ew_weighted_fold_dev: the fold with the scale read from device memory."""
+    ptrs, w, n = _units(units, weights)
+    if acc.dtype != torch.int64 or acc.numel() < n:
+        raise ValueError("acc must be int64 with one slot per element")
+    check(lib.ew_weighted_fold_dev(ptrs, w, len(units), n, _ptr(bits), _ptr(acc),
+                                   int(accumulate), None, _stream(stream)))
+    return acc
+
+
+def fixed_to_float_dev(acc: torch.Tensor, bits: torch.Tensor, out: Optional[torch.Tensor] = None,
+                       stream=None) -> torch.Tensor:
+    if out is None:
+        out = torch.empty(acc.numel(), dtype=torch.float32, device=acc.device)
+    check(lib.ew_fixed_to_float_dev(_ptr(acc), acc.numel(), _ptr(bits), _ptr(out),
+                                    _stream(stream)))
+    return out
+
+
 def fixed_to_double(acc: torch.Tensor, frac_bits: int, out: Optional[torch.Tensor] = None,
                     stream=None) -> torch.Tensor:
     if out is None:
@@ -555,6 +585,16 @@ class Communicator:
                                      _ptr(ws_acc), _ptr(ws_max), _ptr(out), C.byref(f),
                                      _stream(stream)))
         return f.value
+
+    def weighted_reduce_async(self, units, weights, total_units: int, out: torch.Tensor,
+                              ws_acc: torch.Tensor, ws_max: torch.Tensor, ws_bits: torch.Tensor,
+                              stream=None) -> None:
+        """Full (d) path with the scale in device memory (`ws_bits`, int32):
+        no host synchronisation, capturable in a CUDA graph."""
+        ptrs, w, n = _units(units, weights)
+        check(lib.ew_weighted_reduce_async(self._h, ptrs, w, len(units), int(total_units), n,
+                                           _ptr(ws_acc), _ptr(ws_max), _ptr(ws_bits), _ptr(out),
+                                           _stream(stream)))
 
 
 # ------------------------------------- ring replica by optimizer replay ---

@@ -348,6 +348,13 @@ def _worker(rank, world, port, result_dir):
             dev.weighted_fold(all_units, w, f, acc1)
             single = dev.fixed_to_float(acc1, f)
             report["reduce bit-identical to 1-GPU fold"] = bool(torch.equal(out, single))
+            # the same reduce with the scale kept on the device (no host sync)
+            out2 = torch.full_like(out, -1.0)
+            bits = torch.empty(1, dtype=torch.int32, device="cuda")
+            shrunk.weighted_reduce_async(units, [w[u] for u in mine], n_units, out2, acc, mx, bits)
+            torch.cuda.synchronize()
+            report["async reduce identical"] = bool(torch.equal(out2, out)) and \
+                int(bits.item()) == f
             report["shrunk size"] = shrunk.size
         dist.barrier()
         group.close()   # the group owns the communicators (parent and splits)

@@ -131,3 +131,40 @@ def test_dequant_vectorised_tails(dim):
         host = a.cpu().numpy().astype(np.float64) * 2.0 ** -40
         assert np.array_equal(dev.fixed_to_float(a, 40).cpu().numpy(), host.astype(np.float32))
         assert np.array_equal(dev.fixed_to_double(a, 40).cpu().numpy(), host)
+
+
+def test_device_scale_path_in_a_cuda_graph(oracle):
+    """The (d) step with the scale in device memory — absmax, scale,
+    fold, dequant — captured once in a CUDA graph and replayed: no host
+    round trip, bit-identical to the host-scale path; a non-finite absmax
+    yields the sentinel bits and zeros instead of a wrong scale."""
+    dim, U = 100_003, 6
+    g = make_units(23, U, dim)
+    w = np.linspace(0.05, 0.3, U)
+    units = [torch.from_numpy(x).cuda() for x in g]
+    f_host = dev.fixed_point_bits(dev.weighted_absmax(units, w).item(), U)
+    acc_h = torch.empty(dim, dtype=torch.int64, device="cuda")
+    dev.weighted_fold(units, w, f_host, acc_h)
+    want = dev.fixed_to_float(acc_h, f_host)
+    amax = torch.empty(1, dtype=torch.float64, device="cuda")
+    bits = torch.empty(1, dtype=torch.int32, device="cuda")
+    acc = torch.empty(dim, dtype=torch.int64, device="cuda")
+    out = torch.empty(dim, dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        dev.weighted_absmax(units, w, out=amax, stream=s)
+        dev.fixed_point_bits_async(amax, U, bits, stream=s)
+        dev.weighted_fold_dev(units, w, bits, acc, stream=s)
+        dev.fixed_to_float_dev(acc, bits, out, stream=s)
+    for _ in range(2):
+        out.fill_(-1.0)
+        graph.replay()
+    torch.cuda.synchronize()
+    assert int(bits.item()) == f_host
+    assert torch.equal(acc, acc_h) and torch.equal(out, want)
+    units[2][7] = float("nan")
+    graph.replay()
+    torch.cuda.synchronize()
+    assert int(bits.item()) == -2 ** 31 and int(out.count_nonzero()) == 0
