@@ -1675,6 +1675,40 @@ def run_reduce(args, rank, world, out):
                      "dequant_ms": round(t_deq * 1e3, 3),
                      "dequant_gbs": round(12 * n / t_deq / 1e9, 1),
                      "nccl_path_ms": round(t_all * 1e3, 3)}
+    # the same step with the scale kept in device memory: no host round trip
+    # between the global max and the fold (ew_fixed_point_bits_async ->
+    # ew_weighted_fold_dev -> ew_fixed_to_float_dev), same bits
+    amax_d = torch.empty(1, dtype=torch.float64, device="cuda")
+    bits_d = torch.empty(1, dtype=torch.int32, device="cuda")
+    res_d = torch.empty(n, dtype=torch.float32, device="cuda")
+
+    def reduce_step_dev():
+        dev.weighted_absmax(units, w, out=amax_d)
+        if world > 1:
+            dist.all_reduce(amax_d, op=dist.ReduceOp.MAX)
+        dev.fixed_point_bits_async(amax_d, REDUCE_UNITS, bits_d)
+        dev.weighted_fold_dev(units, w, bits_d, acc)
+        if world > 1:
+            dist.all_reduce(acc)
+        dev.fixed_to_float_dev(acc, bits_d, res_d)
+
+    reduce_step_dev()
+    torch.cuda.synchronize()
+    barrier(world)
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    reduce_step_dev()
+    e.record()
+    torch.cuda.synchronize()
+    barrier(world)
+    t_dev = max_over_ranks([s.elapsed_time(e) / 1e3], world)[0]
+    same = torch.tensor([1 if (torch.equal(res_d, res) and int(bits_d.item()) == f) else 0],
+                        device="cuda")
+    if world > 1:
+        dist.all_reduce(same, op=dist.ReduceOp.MIN)
+    out["reduce"].update({"device_scale_path_ms": round(t_dev * 1e3, 3),
+                          "device_scale_bit_identical": bool(same.item())})
+    del res_d
     del acc
     torch.cuda.empty_cache()
     if world > 1:

@@ -94,6 +94,22 @@ __device__ __forceinline__ Vec32 ld_stream32(const void* p) {
   return v;
 }
 
+// Read-only 256-bit load without the L2 evict-first hint: for streams that
+// may alias another stream of the same kernel (a unit buffer listed twice),
+// whose second read should hit L2.
+__device__ __forceinline__ Vec32 ld_nc32(const void* p) {
+  uint32_t r[8];
+  asm volatile(
+      "ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7])
+      : "l"(p));
+  Vec32 v;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v.w[k] = (static_cast<uint64_t>(r[2 * k + 1]) << 32) | r[2 * k];
+  return v;
+}
+
 // 32-byte load of data this kernel also writes (no .nc): read-modify-write
 // of an accumulator
 __device__ __forceinline__ Vec32 ld_plain32(const void* p) {

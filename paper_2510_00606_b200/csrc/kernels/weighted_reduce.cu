@@ -110,8 +110,18 @@ __global__ void scale_kernel(const double* __restrict__ gmax, int64_t total_unit
   *bits = min(1000, 62 - e - cu);  // total_units * m * 2^F < 2^62, as ew_fixed_point_bits
 }
 
-template <bool kAccumulate>
-__global__ void __launch_bounds__(256) fold_kernel(Units u, int64_t n, double host_scale,
+// kPipe (3+ units per element): one group per thread, unit k+1's load
+// issued before unit k's math.  There the fold is bound by the conversion
+// pipe (F2F.F64.F32 + F2I.S64.F64, ~15/clk/SM measured) rather than HBM, and
+// overlapping the next unit's latency with this unit's conversions is worth
+// ~11 % at 4 and 8 units (tools/microbench/fold_variants.cu); at 1-2 units
+// the two-deep unpipelined form streams faster.  Bounded to 4 CTAs/SM (64
+// registers; the pipelined forms keep 8-16 B on the stack, measured faster
+// than 80 registers at 3 CTAs/SM: tools/fold_sweep.py).  Unit loads carry no
+// L2 evict-first hint: a unit buffer listed twice (config E's N = 1 leg)
+// then re-reads from L2.
+template <bool kAccumulate, bool kPipe>
+__global__ void __launch_bounds__(256, 4) fold_kernel(Units u, int64_t n, double host_scale,
                                                    long long* __restrict__ acc,
                                                    const long long* __restrict__ addend,
                                                    const int* __restrict__ dev_bits) {
@@ -123,23 +133,35 @@ __global__ void __launch_bounds__(256) fold_kernel(Units u, int64_t n, double ho
   bool vec_ok = ((reinterpret_cast<uintptr_t>(acc) | reinterpret_cast<uintptr_t>(addend)) & 31) == 0;
   for (int k = 0; k < u.n; ++k) vec_ok = vec_ok && ((reinterpret_cast<uintptr_t>(u.p[k]) & 31) == 0);
   if (vec_ok) {
-    constexpr int kDepth = 2;  // independent 32-byte groups per thread
+    constexpr int kDepth = kPipe ? 1 : 2;  // independent 32-byte groups per thread
     for (int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i0 < n8;
          i0 += kDepth * stride) {
-      long long s[kDepth][8] = {};
-      for (int k = 0; k < u.n; ++k) {
-        const double w = u.w[k];
-        Vec32 g[kDepth];
+      auto load = [&](const float* p, Vec32 (&g)[kDepth]) {
 #pragma unroll
         for (int d = 0; d < kDepth; ++d) {
           const int64_t i = i0 + d * stride;
-          g[d] = i < n8 ? ld_stream32(u.p[k] + 8 * i) : Vec32{{0, 0, 0, 0}};
+          g[d] = i < n8 ? ld_nc32(p + 8 * i) : Vec32{{0, 0, 0, 0}};
         }
+      };
+      long long s[kDepth][8] = {};
+      Vec32 g[kDepth];
+      if (kPipe) load(u.p[0], g);
+      for (int k = 0; k < u.n; ++k) {
+        Vec32 next[kDepth];
+        if (!kPipe)
+          load(u.p[k], g);
+        else if (k + 1 < u.n)
+          load(u.p[k + 1], next);
+        const double w = u.w[k];
 #pragma unroll
         for (int d = 0; d < kDepth; ++d)
 #pragma unroll
           for (int e = 0; e < 8; ++e)
             s[d][e] += __double2ll_rn((w * static_cast<double>(f32_of(g[d], e))) * scale);
+        if (kPipe) {
+#pragma unroll
+          for (int d = 0; d < kDepth; ++d) g[d] = next[d];
+        }
       }
 #pragma unroll
       for (int d = 0; d < kDepth; ++d) {
@@ -257,10 +279,10 @@ int grid_for(int64_t work) {
 
 // Persistent grid for the 256-thread streaming kernels: every CTA resident
 // (SMs x occupancy), so the grid-stride loops run in one wave.
-int resident_grid(const void* kernel, int64_t work) {
+int resident_grid(const void* kernel, int64_t work, int waves = 1) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
-  const int64_t cap = static_cast<int64_t>(num_sms()) * std::max(1, per_sm);
+  const int64_t cap = static_cast<int64_t>(num_sms()) * std::max(1, per_sm) * waves;
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, cap)));
 }
 
@@ -350,18 +372,20 @@ int fold_impl(const float* const* units, const double* weights, int n_units, int
   for (int off = 0; off < n_units; off += kMaxUnits) {
     Units u;
     if (int st = pack_units(units, weights, n_units, off, u)) return st;
-    // one resident wave: 62 registers x 256 threads allow 4 CTAs per SM
-    const int grid = resident_grid(accumulate || off > 0 ? (const void*)fold_kernel<true>
-                                                         : (const void*)fold_kernel<false>,
-                                   (n_elems + 7) / 8);
     long long* a = reinterpret_cast<long long*>(acc);
     const long long* add = off == 0 ? reinterpret_cast<const long long*>(addend) : nullptr;
-    if (accumulate || off > 0)
-      fold_kernel<true><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a, add,
-                                                                dev_bits);
-    else
-      fold_kernel<false><<<grid, 256, 0, (cudaStream_t)stream>>>(u, n_elems, scale, a, add,
-                                                                 dev_bits);
+    const bool accum = accumulate || off > 0;
+    const bool pipe = u.n >= 3;
+    const void* kern = accum ? (pipe ? (const void*)fold_kernel<true, true>
+                                     : (const void*)fold_kernel<true, false>)
+                             : (pipe ? (const void*)fold_kernel<false, true>
+                                     : (const void*)fold_kernel<false, false>);
+    // unpipelined: one resident wave (62 registers x 256 threads: 4 CTAs/SM);
+    // pipelined: two waves' worth of CTAs (measured best)
+    const int grid = resident_grid(kern, (n_elems + 7) / 8, pipe ? 2 : 1);
+    void* args[] = {&u, &n_elems, const_cast<double*>(&scale), &a, &add,
+                    &dev_bits};
+    EW_CUDA_TRY(cudaLaunchKernel(kern, grid, 256, args, 0, (cudaStream_t)stream));
     EW_CUDA_TRY(cudaGetLastError());
   }
   return EW_OK;
