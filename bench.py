@@ -720,11 +720,17 @@ def run_host_replica(args, rank, world, out):
     members = list(range(world))
     drop = min(3, world - 1)
     rp = ReshardPlan.build(lb, members, [r for r in members if r != drop])
-    room = torch.tensor([shutil.disk_usage("/dev/shm").free], dtype=torch.float64, device="cuda")
+    # the images are double-buffered (2 x the state in /dev/shm, all of it
+    # touched by the three publishes below) and tmpfs pages are host RAM:
+    # require room in both, with margin, before creating them
+    import psutil
+    room = torch.tensor([shutil.disk_usage("/dev/shm").free, psutil.virtual_memory().available],
+                        dtype=torch.float64, device="cuda")
     dist.all_reduce(room, op=dist.ReduceOp.MIN)
-    if room.item() < 1.3 * sum(lb):
+    if room[0].item() < 2.2 * sum(lb) or room[1].item() < 2.5 * sum(lb):
         if rank == 0:
-            out["host_replica"] = {"skipped": "/dev/shm smaller than 1.3x the state"}
+            out["host_replica"] = {"skipped": "/dev/shm or host RAM below 2.2x / 2.5x the state "
+                                              "(double-buffered images)"}
         return
     S = rp.src.shard_bytes(rank)
     stream = torch.cuda.current_stream()
