@@ -84,6 +84,9 @@ def parse_args():
                    help="comma list of: e2e,cpu,inplace,reshard,host_replica,replica,replay,"
                         "migration,config_c,stage,philox,reduce")
     p.add_argument("--json-out", default="")
+    p.add_argument("--deadline-s", type=float, default=1500.0,
+                   help="wall-clock budget of the whole run: past it (a leg hung) rank 0 "
+                        "prints the line gathered so far, marked incomplete, and all ranks exit")
     p.add_argument("--trace", action="store_true",
                    help="log each leg's start to stderr on every rank (locates a hang)")
     return p.parse_args()
@@ -1796,12 +1799,94 @@ def run_reduce(args, rank, world, out):
 
 # ------------------------------------------------------------------- arms ---
 
+class LegGuard:
+    """Keeps one failing or hung secondary leg from costing the whole line.
+
+    The headline (snapshot + verify) is measured first; every later leg runs
+    through `run`.  A leg that raises on any rank posts the error in the c10d
+    store and that rank exits; a watchdog thread on every rank polls the store
+    and the --deadline-s budget, and on either rank 0 prints the JSON gathered
+    so far with an "incomplete" record (which leg, why) and every rank exits 0.
+    Ranks blocked inside a collective of the broken leg are released by the
+    exit rather than left to hang."""
+
+    KEY = "ew_bench_abort"
+
+    def __init__(self, args, rank, world, out, t_start):
+        import threading
+        self.rank, self.out, self.leg, self.done = rank, out, "snapshot", []
+        self.emitted = False
+        self.deadline = t_start + args.deadline_s
+        self.json_out = args.json_out
+        self.lock = threading.Lock()
+        self.store = None
+        if world > 1:
+            from torch.distributed import distributed_c10d as c10d
+            self.store = c10d._get_default_store()
+        threading.Thread(target=self._watch, daemon=True).start()
+
+    def _watch(self):
+        while True:
+            time.sleep(1.0)
+            reason = None
+            if time.time() > self.deadline:
+                reason = f"deadline passed during leg {self.leg!r}"
+            elif self.store is not None:
+                try:
+                    if self.store.check([self.KEY]):
+                        reason = self.store.get(self.KEY).decode(errors="replace")
+                except Exception:  # noqa: BLE001 - the store went away: peers are gone
+                    reason = f"rendezvous store lost during leg {self.leg!r}"
+            if reason:
+                self.finish(reason)
+
+    def finish(self, reason):
+        with self.lock:
+            if self.rank == 0 and not self.emitted:
+                line = None
+                for _ in range(5):  # the main thread may be writing `out`
+                    try:
+                        rec = dict(self.out)
+                        rec["incomplete"] = {"reason": reason, "legs_done": list(self.done)}
+                        line = json.dumps(rec)
+                        break
+                    except Exception:  # noqa: BLE001
+                        time.sleep(0.05)
+                if line is not None:
+                    emit(line)
+                    if self.json_out:
+                        Path(self.json_out).write_text(line + "\n")
+            sys.stdout.flush()
+            sys.stderr.flush()
+            os._exit(0)
+
+    def run(self, name, fn, *a):
+        self.leg = name
+        try:
+            fn(*a)
+        except Exception as e:  # noqa: BLE001
+            import traceback
+            traceback.print_exc()
+            msg = f"rank {self.rank} raised in leg {name!r}: {e!r}"[:600]
+            if self.store is not None:
+                try:  # a peer's failure may be the cause: report the first one
+                    if self.store.check([self.KEY]):
+                        msg = self.store.get(self.KEY).decode(errors="replace")
+                    else:
+                        self.store.set(self.KEY, msg)
+                except Exception:  # noqa: BLE001
+                    pass
+            self.finish(msg)
+        self.done.append(name)
+
+
 def bench_b200(args):
     import torch
     rank, world, local = dist_setup(args)
     skip = set(filter(None, args.skip.split(",")))
     out = {}
     t_start = time.time()
+    guard = LegGuard(args, rank, world, out, t_start)
 
     def trace(leg):
         if args.trace:
@@ -1815,54 +1900,57 @@ def bench_b200(args):
                  "philox", "reduce"}
     if "e2e" not in skip:
         trace("e2e")
-        run_e2e(args, rank, world, out, m, live, snap, rows, bad, S)
+        guard.run("e2e", run_e2e, args, rank, world, out, m, live, snap, rows, bad, S)
     del live, snap
     torch.cuda.empty_cache()
     if world > 1 and (args.inplace_state_gb > 0 or "inplace" not in skip):
         trace("inplace")
-        run_inplace(args, rank, world, out)
+        guard.run("inplace", run_inplace, args, rank, world, out)
     if world == 1 and rank == 0 and "cpu" not in skip:
         trace("cpu_baseline")
-        run_cpu_baseline(args, out, segs, S)
+        guard.run("cpu_baseline", run_cpu_baseline, args, out, segs, S)
     if world > 1 and "reshard" not in skip:
         trace("reshard")
-        run_reshard(args, rank, world, out)
+        guard.run("reshard", run_reshard, args, rank, world, out)
     if world > 1 and "host_replica" not in skip:
         trace("host_replica")
-        run_host_replica(args, rank, world, out)
+        guard.run("host_replica", run_host_replica, args, rank, world, out)
     if world > 1 and "replica" not in skip:
         trace("replica")
-        run_replica(args, rank, world, out)
+        guard.run("replica", run_replica, args, rank, world, out)
     if "replay" not in skip:
         trace("replay")
-        run_replay(args, rank, world, out)
+        guard.run("replay", run_replay, args, rank, world, out)
     if world > 1 and "migration" not in skip:
         trace("layer_migration")
-        run_layer_migration(args, rank, world, out)
+        guard.run("layer_migration", run_layer_migration, args, rank, world, out)
     if world >= 4 and "config_c" not in skip:
         trace("config_c")
-        run_config_c(args, rank, world, out)
+        guard.run("config_c", run_config_c, args, rank, world, out)
     if world > 1 and world % 2 == 0 and "stage" not in skip:
         trace("stage_move")
-        run_stage_move(args, rank, world, out)
+        guard.run("stage_move", run_stage_move, args, rank, world, out)
     if "philox" not in skip:
         trace("philox")
-        run_philox(args, rank, world, out)
+        guard.run("philox", run_philox, args, rank, world, out)
     if "reduce" not in skip:
         trace("reduce")
-        run_reduce(args, rank, world, out)
+        guard.run("reduce", run_reduce, args, rank, world, out)
     if world == 1 and "config_a" not in skip:
         trace("config_a")
-        run_config_a(args, rank, world, out)
+        guard.run("config_a", run_config_a, args, rank, world, out)
     if world == 1 and "config_d" not in skip:
         trace("config_d_snapshot")
-        run_config_d_snapshot(args, rank, world, out)
+        guard.run("config_d_snapshot", run_config_d_snapshot, args, rank, world, out)
     if world == 1 and rank == 0 and "cpu" not in skip:
         trace("cpu_beside")
-        run_cpu_beside(args, out)  # cpu_baseline leg, continued
+        guard.run("cpu_beside", run_cpu_beside, args, out)  # cpu_baseline leg, continued
+    guard.leg = "emit"
     if rank == 0:
         line = json.dumps(out)
-        emit(line)
+        with guard.lock:
+            emit(line)
+            guard.emitted = True
         if args.json_out:
             Path(args.json_out).write_text(line + "\n")
     if world > 1:
