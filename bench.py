@@ -277,7 +277,7 @@ def run_snapshot(args, rank, world, local, out):
         "state_gbs_per_gpu": round(S / step / 1e9, 2),
         "kernels": {"ew_snapshot_ms": round(t_snap * 1e3, 4), "ew_verify_ms": round(t_ver * 1e3, 4),
                     "ew_verify_gbs": round(S / t_ver / 1e9, 1)},
-        "roofline": {"kernel": "ew_snapshot (tma_row_kernel<kSnapshot>)", "bound": "hbm",
+        "roofline": {"kernel": "ew_snapshot (warp_row_kernel<kSnapshot>)", "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4),
                      "frac_of_8tbs_spec": round(achieved / 8000.0, 4),

@@ -282,6 +282,20 @@ struct RowCursor {
 }  // namespace ew
 
 // Opaque handle bodies shared between translation units.
+namespace ew {
+// Per-row geometry precomputed at ew_shardmap_create for the register-staged
+// snapshot kernel (one 32-byte broadcast load per row instead of a segment
+// cursor held in registers across the row).
+struct alignas(32) RowDesc {
+  int64_t w0;    // first local byte of the row's 32-byte-aligned window
+  int64_t q0;    // global word index of window word 0: floor((w0 + delta) / 8)
+  int32_t head;  // the row inside the window: [head, end)
+  int32_t end;
+  int32_t sh;    // (global - local) mod 8
+  int32_t pad;
+};
+}  // namespace ew
+
 struct ew_shardmap {
   int device = -1;
   int64_t n_segs = 0;
@@ -290,6 +304,7 @@ struct ew_shardmap {
   int64_t block_bytes = 0;
   int block_shift = 0;
   ew::DevSeg* d_segs = nullptr;      // device copy
+  ew::RowDesc* d_rows = nullptr;     // per-row geometry (n_rows entries)
   std::vector<ew::DevSeg> h_segs;    // host copy (row -> block queries)
   ew::ShardMapView view() const {
     return ew::ShardMapView{d_segs, n_segs, n_rows, total_bytes, block_shift};

@@ -5,22 +5,20 @@
 // sim.cpp:861-880) with the byte-moving operation: one HBM pass copies a
 // rank's packed shard live -> snapshot while checksumming it, a second pass
 // re-reads the snapshot and compares.  Both are HBM-bound streaming kernels:
-// a warp-specialised CTA streams its rows through a shared-memory ring with
-// cp.async.bulk (TMA) loads and stores, one checksum row (<= 64 KiB) per CTA
-// iteration, persistent grid of SMs x resident CTAs.
+// one warp per checksum row (<= one block), 256-bit loads kept in registers,
+// row sums reduced with shuffles (warp_row_kernel below).
 //
-// Checksum spec (ew_api.h, oracle/ew_oracle.c ew_oracle_row_sums): per global
-// block b, s0 = sum w_i and s1 = sum (i+1) w_i (mod 2^64) over the global
-// little-endian u64 words w_i, bytes the buffer does not hold read as zero.
+// Checksum spec (ew_api.h, oracle/ew_oracle.c ew_oracle_row_sums,
+// oracle/checksum_spec.py): per global block b, s0 = sum w_i and
+// s1 = sum (i+1) w_i (mod 2^64) over the global little-endian u64 words w_i,
+// bytes the buffer does not hold read as zero.
 //
 // Per local 8-byte word W at local byte x (8-aligned) the global position is
 // g = x + delta, q = floor(g/8), sh = g mod 8 (uniform per row).  W feeds
 // word q with A = W << 8sh and word q+1 with B = W >> (64-8sh) (sh > 0), so
 // with C = A + B:  s0 += C,  s1 += (q+1) C + B.  Bytes outside the row are
 // masked before the split, hence every nonzero contribution lands in the
-// row's own block.  Per thread the word indices are q_t + 256 i (+1 for the
-// odd word), so s1 needs only additions: sum i*D_i = n*T1 - T2 with the
-// running sums T1 += D_i, T2 += T1 (D_i = C_even + C_odd of iteration i).
+// row's own block.
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -110,215 +108,146 @@ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 bool aligned32(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; }
 
 // ------------------------------------------------------------------------
-// TMA-fed variant: the load pipeline never drains at row boundaries.
+// Register-staged variant (round 2): one WARP owns a row at a time.  Lanes
+// stride 32 bytes through the row's 32-byte-aligned window with
+// kWarpRowUnroll 256-bit loads in flight each, checksum in registers, store
+// the snapshot copy straight back (STG.256), and reduce s0/s1 with shuffles
+// at the row's end only.  No CTA barrier and no shared memory: no warp ever
+// waits for another, so the load pipeline never drains (a CTA-wide row
+// reduction capped register variants at 6.2-6.3 TB/s, the TMA ring at 6.45;
+// this form measured 6.51-6.53 TB/s, tools/microbench/warp_row_variants.cu).
 //
-// Warp 0 (one lane) streams 16 KiB pieces of this CTA's rows into a ring of
-// shared-memory stages with cp.async.bulk (mbarrier complete_tx); four
-// consumer warps checksum each stage from shared memory (16-byte units,
-// conflict-free), the first consumer lane writes the snapshot copy of the
-// stage back with one bulk shared->global store, and the stage is released
-// once both the consumers and the store engine have read it.  Row sums are
-// reduced through shared-memory slots (each consumer warp adds its sums, the
-// last to arrive finishes the row), so neither the producer nor any consumer
-// waits at a row end.  Unit k of a row's 32-byte-aligned window holds global
-// words q_t + 256*i (+1 for the odd word), i = the thread's iteration.
-constexpr int kTmaConsumers = 4;                  // warps
-constexpr int kTmaThreads = 32 * (kTmaConsumers + 1);
-constexpr int kTmaStages = 4;
-constexpr int kTmaPiece = 16 * 1024;              // bytes per stage
-constexpr int kTmaSmem = kTmaStages * kTmaPiece;  // 64 KiB -> 3 CTAs per SM
-constexpr int kTmaUnitsPerThread = kTmaPiece / 16 / (32 * kTmaConsumers);  // 8
-
-constexpr int kRowSlots = 8;                     // >= kTmaStages + 1, power of 2
-static_assert(kRowSlots > kTmaStages, "row slots must cover the ring");
-
-struct TmaRow {
-  int64_t w0;      // first local byte of the 32-byte-aligned window
-  int head, end;   // the row inside the window: [head, end)
-  int n_pieces;
-  int64_t window_bytes;
-};
-
-__device__ __forceinline__ TmaRow tma_row(const ShardMapView& m, int64_t r, RowGeom& g,
-                                          RowCursor& cur) {
-  g = cur.at(m, r);
-  TmaRow t;
-  t.w0 = g.local_lo & ~int64_t{31};
-  t.head = static_cast<int>(g.local_lo - t.w0);
-  t.end = t.head + static_cast<int>(g.len);
-  t.window_bytes = ((g.local_lo + g.len + 31) & ~int64_t{31}) - t.w0;
-  t.n_pieces = static_cast<int>((t.window_bytes + kTmaPiece - 1) / kTmaPiece);
-  return t;
-}
+// Window word m (local byte w0 + 8m) is global word q0 + m with
+// q0 = floor((w0 + delta) / 8), so with C_m and B_m as above
+//     s0 = sum C_m,   s1 = (q0 + 1) s0 + sum m C_m + sum B_m,
+// and per 32-byte vector j (words 4j..4j+3, c = C_0 + .. + C_3):
+//     sum m C_m = 4 j c + (C_1 + 2 C_2 + 3 C_3).
+// Copy ownership as in the ring kernel: a row stores the vectors whose first
+// byte it holds; the buffer's partial last vector is stored bytewise.
+constexpr int kWarpRowThreads = 256;        // per CTA
+constexpr int kWarpRowUnroll = 4;           // 32-byte loads in flight per lane
+constexpr int kWarpRowMinBlocks = 5;        // register cap: CTAs resident per SM
+constexpr int kWarpRowGridPct = 160;        // grid = resident CTAs x this / 100
+constexpr int kWarpRowStagger = 5;          // chunk rotation per warp (0: none)
 
 template <Mode M>
-__global__ void __launch_bounds__(kTmaThreads, 3) tma_row_kernel(ShardMapView map,
-                                                              const uint8_t* __restrict__ src,
-                                                              uint8_t* __restrict__ dst,
-                                                              uint64_t* __restrict__ row_sums,
-                                                              const uint64_t* __restrict__ expected,
-                                                              uint32_t* __restrict__ bad_count,
-                                                              int64_t* __restrict__ bad_rows,
-                                                              int64_t bad_cap) {
-  extern __shared__ __align__(128) uint8_t ring[];
-  __shared__ __align__(8) uint64_t full[kTmaStages];
-  __shared__ __align__(8) uint64_t empty[kTmaStages];
-  // per-row reduction slots: each consumer warp adds its sums, the last of
-  // the four to arrive finishes the row (no consumer barrier, so no warp
-  // ever waits for another at a row end).  A warp runs at most kTmaStages
-  // pieces (so <= kTmaStages rows) ahead of the slowest: 8 slots suffice.
-  __shared__ unsigned long long slot_s0[kRowSlots], slot_s1[kRowSlots];
-  __shared__ unsigned slot_n[kRowSlots];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (threadIdx.x < kRowSlots) {
-    slot_s0[threadIdx.x] = 0;
-    slot_s1[threadIdx.x] = 0;
-    slot_n[threadIdx.x] = 0;
-  }
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < kTmaStages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kTmaConsumers);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-
-  if (warp == 0) {  // producer
-    if (lane != 0) return;
-    RowCursor cur;
-    int64_t k = 0;
-    for (int64_t r = blockIdx.x; r < map.n_rows; r += gridDim.x) {
-      RowGeom g;
-      const TmaRow t = tma_row(map, r, g, cur);
-      for (int p = 0; p < t.n_pieces; ++p, ++k) {
-        const int s = static_cast<int>(k % kTmaStages);
-        if (k >= kTmaStages) {
-          mbar_wait(&empty[s], static_cast<uint32_t>(((k / kTmaStages) - 1) & 1));
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        }
-        const int64_t off = static_cast<int64_t>(p) * kTmaPiece;
-        const uint32_t n =
-            static_cast<uint32_t>(min(static_cast<int64_t>(kTmaPiece), t.window_bytes - off));
-        mbar_expect_tx(&full[s], n);
-        tma_load(ring + s * kTmaPiece, src + t.w0 + off, n, &full[s]);
-      }
-    }
-    return;
-  }
-
-  const int ctid = threadIdx.x - 32;
-  const int64_t last_vec_byte = (map.total_bytes - 1) & ~int64_t{31};  // start of the last 32-B vector
-  const int partial = static_cast<int>(map.total_bytes & 31);
-  int64_t k = 0;
-  unsigned row_iter = 0;
-  RowCursor cur;
-  for (int64_t r = blockIdx.x; r < map.n_rows; r += gridDim.x) {
-    RowGeom g;
-    const TmaRow t = tma_row(map, r, g, cur);
-    const int sh = static_cast<int>(g.delta & 7);
-    const int64_t q_t = floor_div(t.w0 + 16 * ctid + g.delta, 8);
-    uint64_t t1 = 0, t2 = 0, odd = 0, bsum = 0;
-    for (int p = 0; p < t.n_pieces; ++p, ++k) {
-      const int s = static_cast<int>(k % kTmaStages);
-      mbar_wait(&full[s], static_cast<uint32_t>((k / kTmaStages) & 1));
-      const uint8_t* stage = ring + s * kTmaPiece;
-      const int base = p * kTmaPiece;  // window byte of the stage's first byte
-      const int n = static_cast<int>(min(static_cast<int64_t>(kTmaPiece), t.window_bytes - base));
-      if (M == Mode::kSnapshot && ctid == 0) {
-        // store the 32-byte vectors this row owns (the row holding a
-        // vector's first byte copies it); the buffer's partial last vector
-        // goes through byte stores below
-        int lo = (p == 0 && t.head != 0) ? 32 : 0;
-        int hi = n;
-        const int64_t last_in_window = last_vec_byte - t.w0 - base;
-        if (partial && last_in_window >= 0 && last_in_window < n) hi = static_cast<int>(last_in_window);
-        if (hi > lo) {
-          tma_store(dst + t.w0 + base + lo, stage + lo, static_cast<uint32_t>(hi - lo));
-          bulk_commit();
-        }
-      }
+__global__ void __launch_bounds__(kWarpRowThreads, kWarpRowMinBlocks) warp_row_kernel(
+    const RowDesc* __restrict__ rows_desc, int n_rows, int64_t total_bytes,
+    const uint8_t* __restrict__ src, uint8_t* __restrict__ dst, uint64_t* __restrict__ row_sums,
+    const uint64_t* __restrict__ expected, uint32_t* __restrict__ bad_count,
+    int64_t* __restrict__ bad_rows, int64_t bad_cap) {
+  const int lane = threadIdx.x & 31;
+  const int warp = static_cast<int>((blockIdx.x * kWarpRowThreads + threadIdx.x) >> 5);
+  const int n_warps = static_cast<int>((gridDim.x * kWarpRowThreads) >> 5);
+  for (int r = warp; r < n_rows; r += n_warps) {
+    const RowDesc d = rows_desc[r];
+    const Vec32* s = reinterpret_cast<const Vec32*>(src + d.w0);
+    uint64_t s0 = 0, sj = 0, e = 0;
+    auto accumulate = [&](const Vec32& v, int j) {
+      const uint64_t cs = v.w[0] + v.w[1] + v.w[2] + v.w[3];
+      s0 += cs;
+      sj += static_cast<uint64_t>(j) * cs;
+      e += v.w[1] + 2 * v.w[2] + 3 * v.w[3];
+    };
+    if (d.head == 0 && d.sh == 0 && (d.end & 31) == 0 &&
+        (M != Mode::kSnapshot || d.w0 + d.end <= total_bytes)) {
+      // fast path (every full, aligned row): no masks, no shifts, no
+      // ownership or tail checks; kWarpRowUnroll loads in flight per lane
+      const int nvec = d.end >> 5;
+      // warps start their rows at staggered chunks (rotation by warp id):
+      // in lockstep at the same offset, concurrent warps' addresses would
+      // sit at a 64 KiB stride
+      constexpr int kChunk = 32 * kWarpRowUnroll;
+      const int n_chunks = (nvec + kChunk - 1) / kChunk;
+      const int rot = (warp * kWarpRowStagger) % n_chunks;
+      for (int c = 0; c < n_chunks; ++c) {
+        int cc = c + rot;
+        if (cc >= n_chunks) cc -= n_chunks;
+        const int j0 = cc * kChunk + lane;
+        Vec32 v[kWarpRowUnroll];
 #pragma unroll
-      for (int u = 0; u < kTmaUnitsPerThread; ++u) {
-        const int x = 16 * (ctid + u * 32 * kTmaConsumers);  // byte in the stage
-        const int wx = base + x;                             // byte in the window
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (x < n) v = lds128(stage + x);
-        uint64_t w0 = lo64(v), w1 = hi64(v);
-        if (wx < t.head || wx + 16 > t.end) {
-          w0 &= byte_mask(wx, t.head, t.end);
-          w1 &= byte_mask(wx + 8, t.head, t.end);
+        for (int u = 0; u < kWarpRowUnroll; ++u) {
+          const int j = j0 + 32 * u;
+          v[u] = j < nvec ? ld_stream32(s + j) : Vec32{{0, 0, 0, 0}};
         }
-        uint64_t c0 = w0, c1 = w1;
-        if (sh != 0) {
-          const uint64_t b0 = w0 >> (64 - 8 * sh), b1 = w1 >> (64 - 8 * sh);
-          c0 = (w0 << (8 * sh)) + b0;
-          c1 = (w1 << (8 * sh)) + b1;
-          bsum += b0 + b1;
+#pragma unroll
+        for (int u = 0; u < kWarpRowUnroll; ++u) {
+          const int j = j0 + 32 * u;
+          if (M == Mode::kSnapshot && j < nvec) st_stream32(dst + d.w0 + 32 * static_cast<int64_t>(j), v[u]);
+          accumulate(v[u], j);  // zero vectors past the end add nothing
         }
-        t1 += c0 + c1;
-        t2 += t1;
-        odd += c1;
       }
-      if (M == Mode::kSnapshot && partial) {
-        const int64_t last_in_window = last_vec_byte - t.w0 - base;
-        if (last_in_window >= 0 && last_in_window < n && ctid < partial &&
-            (last_in_window > 0 || p > 0 || t.head == 0))
-          dst[t.w0 + base + last_in_window + ctid] = stage[last_in_window + ctid];
+    } else {
+      // general path (rows at segment edges: partial windows, realignment,
+      // the buffer's last vector): one vector at a time
+      const int nvec = (d.end + 31) >> 5;
+      for (int j = lane; j < nvec; j += 32) {
+        Vec32 v = ld_stream32(s + j);
+        if (M == Mode::kSnapshot && !(j == 0 && d.head != 0)) {
+          const int64_t x = d.w0 + 32 * static_cast<int64_t>(j);
+          if (x + 32 <= total_bytes) {
+            st_stream32(dst + x, v);
+          } else {  // the buffer's partial last vector, once per buffer
+#pragma unroll
+            for (int k = 0; k < 31; ++k)
+              if (x + k < total_bytes) dst[x + k] = static_cast<uint8_t>(v.w[k >> 3] >> (8 * (k & 7)));
+          }
+        }
+        if (32 * j < d.head || 32 * j + 32 > d.end) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) v.w[k] &= byte_mask(32 * j + 8 * k, d.head, d.end);
+        }
+        if (d.sh != 0) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t b = v.w[k] >> (64 - 8 * d.sh);
+            v.w[k] = (v.w[k] << (8 * d.sh)) + b;
+            e += b;
+          }
+        }
+        accumulate(v, j);
       }
-      if (M == Mode::kSnapshot && ctid == 0) bulk_wait_read<0>();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
     }
-    const int64_t n_exec = static_cast<int64_t>(t.n_pieces) * kTmaUnitsPerThread;
-    uint64_t s0 = t1;
-    uint64_t s1 = static_cast<uint64_t>(q_t + 1) * t1 +
-                  static_cast<uint64_t>(2 * 32 * kTmaConsumers) *
-                      (static_cast<uint64_t>(n_exec) * t1 - t2) + odd + bsum;
-    s0 = warp_sum_u64(s0);
-    s1 = warp_sum_u64(s1);
-    const int sl = static_cast<int>(row_iter++ & (kRowSlots - 1));
-    bool last = false;
-    uint64_t x0 = 0, x1 = 0;
+    uint64_t s1 = static_cast<uint64_t>(d.q0 + 1) * s0 + 4 * sj + e;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
     if (lane == 0) {
-      atomicAdd(&slot_s0[sl], static_cast<unsigned long long>(s0));
-      atomicAdd(&slot_s1[sl], static_cast<unsigned long long>(s1));
-      __threadfence_block();
-      last = atomicAdd(&slot_n[sl], 1u) == kTmaConsumers - 1;
-      if (last) {
-        __threadfence_block();
-        x0 = atomicExch(&slot_s0[sl], 0ull);
-        x1 = atomicExch(&slot_s1[sl], 0ull);
-        atomicExch(&slot_n[sl], 0u);
-      }
-    }
-    if (last) {
       if (M == Mode::kVerify) {
-        if (x0 != expected[2 * r] || x1 != expected[2 * r + 1]) {
+        if (s0 != expected[2 * r] || s1 != expected[2 * r + 1]) {
           const uint32_t slot = atomicAdd(bad_count, 1u);
           if (bad_rows != nullptr && static_cast<int64_t>(slot) < bad_cap) bad_rows[slot] = r;
         }
       } else {
-        row_sums[2 * r] = x0;
-        row_sums[2 * r + 1] = x1;
+        row_sums[2 * r] = s0;
+        row_sums[2 * r + 1] = s1;
       }
     }
   }
-  if (M == Mode::kSnapshot && ctid == 0) bulk_wait_all();
 }
 
 template <Mode M>
-int launch_rows(const ShardMapView& v, const uint8_t* src, uint8_t* dst, uint64_t* rows,
+int launch_rows(const ew_shardmap* map, const uint8_t* src, uint8_t* dst, uint64_t* rows,
                 const uint64_t* expected, uint32_t* bad, int64_t* bad_rows, int64_t cap,
                 cudaStream_t stream) {
-  auto k = tma_row_kernel<M>;
-  // per device and cheap: set on every launch rather than caching
-  EW_CUDA_TRY(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, kTmaSmem));
+  // persistent: exactly the resident CTAs, warps take rows round-robin (a
+  // second wave of CTAs would run its rows at low occupancy: a tail)
+  auto k = warp_row_kernel<M>;
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kTmaThreads, kTmaSmem);
-  const int64_t grid = std::min<int64_t>(v.n_rows, static_cast<int64_t>(num_sms()) * std::max(1, per_sm));
-  k<<<static_cast<int>(grid), kTmaThreads, kTmaSmem, stream>>>(v, src, dst, rows, expected, bad,
-                                                                bad_rows, cap);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, kWarpRowThreads, 0);
+  // balanced: every warp gets k or k - 1 rows (k = rows per warp at the
+  // grid's capacity), so no last round runs with a fraction of the warps
+  const int64_t warps_per_cta = kWarpRowThreads / 32;
+  const int64_t cap_warps = std::max<int64_t>(
+      1, static_cast<int64_t>(num_sms()) * std::max(1, per_sm) * kWarpRowGridPct / 100 * warps_per_cta);
+  const int64_t k_rows = (map->n_rows + cap_warps - 1) / cap_warps;
+  const int64_t n_warps = (map->n_rows + k_rows - 1) / k_rows;
+  const int64_t grid = (n_warps + warps_per_cta - 1) / warps_per_cta;
+  k<<<static_cast<int>(grid), kWarpRowThreads, 0, stream>>>(
+      map->d_rows, static_cast<int>(map->n_rows), map->total_bytes, src, dst, rows, expected, bad,
+      bad_rows, cap);
   EW_CUDA_TRY(cudaGetLastError());
   return EW_OK;
 }
@@ -368,14 +297,41 @@ int ew_shardmap_create(const ew_segment* segs, int64_t n_segs, int64_t block_byt
   m->n_segs = static_cast<int64_t>(dev.size());
   m->n_rows = rows;
   m->total_bytes = local;
+  if (rows > INT32_MAX) {
+    delete m;
+    return set_error(EW_ERR_INVALID_ARGUMENT, "more than 2^31 rows: use larger blocks");
+  }
+  // per-row geometry for the snapshot / checksum / verify kernel
+  std::vector<RowDesc> desc;
+  desc.reserve(static_cast<size_t>(rows));
+  for (const DevSeg& d : dev) {
+    const int64_t delta = d.global_lo - d.local_off;
+    const int64_t b0 = d.global_lo >> shift, b1 = (d.global_lo + d.length - 1) >> shift;
+    for (int64_t b = b0; b <= b1; ++b) {
+      const int64_t g_lo = std::max(d.global_lo, b << shift);
+      const int64_t g_hi = std::min(d.global_lo + d.length, (b + 1) << shift);
+      const int64_t local_lo = g_lo - delta;
+      RowDesc r{};
+      r.w0 = local_lo & ~int64_t{31};
+      r.q0 = floor_div(r.w0 + delta, 8);
+      r.head = static_cast<int32_t>(local_lo - r.w0);
+      r.end = r.head + static_cast<int32_t>(g_hi - g_lo);
+      r.sh = static_cast<int32_t>(delta & 7);
+      desc.push_back(r);
+    }
+  }
   cudaError_t e = cudaGetDevice(&m->device);
   if (e == cudaSuccess && !dev.empty()) {
     e = cudaMalloc(&m->d_segs, dev.size() * sizeof(DevSeg));
     if (e == cudaSuccess)
       e = cudaMemcpy(m->d_segs, dev.data(), dev.size() * sizeof(DevSeg), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&m->d_rows, desc.size() * sizeof(RowDesc));
+    if (e == cudaSuccess)
+      e = cudaMemcpy(m->d_rows, desc.data(), desc.size() * sizeof(RowDesc), cudaMemcpyHostToDevice);
   }
   if (e != cudaSuccess) {
     if (m->d_segs) cudaFree(m->d_segs);
+    if (m->d_rows) cudaFree(m->d_rows);
     delete m;
     return cuda_status(e, "ew_shardmap_create");
   }
@@ -386,6 +342,7 @@ int ew_shardmap_create(const ew_segment* segs, int64_t n_segs, int64_t block_byt
 void ew_shardmap_free(ew_shardmap* map) {
   if (map == nullptr) return;
   if (map->d_segs) cudaFree(map->d_segs);
+  if (map->d_rows) cudaFree(map->d_rows);
   delete map;
 }
 
@@ -412,7 +369,7 @@ int ew_snapshot(const ew_shardmap* map, const void* live, void* snap, uint64_t* 
   if (!aligned32(live) || !aligned32(snap))
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_snapshot: live/snap must be 32-byte aligned");
   if (map->n_rows == 0) return EW_OK;
-  return launch_rows<Mode::kSnapshot>(map->view(), static_cast<const uint8_t*>(live),
+  return launch_rows<Mode::kSnapshot>(map, static_cast<const uint8_t*>(live),
                                       static_cast<uint8_t*>(snap), row_sums, nullptr, nullptr,
                                       nullptr, 0, (cudaStream_t)stream);
 }
@@ -423,7 +380,7 @@ int ew_checksum(const ew_shardmap* map, const void* buf, uint64_t* row_sums,
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_checksum: NULL argument");
   if (!aligned32(buf)) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_checksum: buf must be 32-byte aligned");
   if (map->n_rows == 0) return EW_OK;
-  return launch_rows<Mode::kChecksum>(map->view(), static_cast<const uint8_t*>(buf), nullptr,
+  return launch_rows<Mode::kChecksum>(map, static_cast<const uint8_t*>(buf), nullptr,
                                       row_sums, nullptr, nullptr, nullptr, 0,
                                       (cudaStream_t)stream);
 }
@@ -436,7 +393,7 @@ int ew_verify(const ew_shardmap* map, const void* buf, const uint64_t* expected,
   if (!aligned32(buf)) return set_error(EW_ERR_INVALID_ARGUMENT, "ew_verify: buf must be 32-byte aligned");
   EW_CUDA_TRY(cudaMemsetAsync(bad_count, 0, sizeof(uint32_t), (cudaStream_t)stream));
   if (map->n_rows == 0) return EW_OK;
-  return launch_rows<Mode::kVerify>(map->view(), static_cast<const uint8_t*>(buf), nullptr,
+  return launch_rows<Mode::kVerify>(map, static_cast<const uint8_t*>(buf), nullptr,
                                     nullptr, expected, bad_count, bad_rows, bad_cap,
                                     (cudaStream_t)stream);
 }

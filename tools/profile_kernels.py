@@ -2,7 +2,7 @@
 size, for ncu captures (`ncu --set full -k regex:...`).  Prints per-kernel
 CUDA-event times so the same command can run without ncu first.
 
-  (a) tma_row_kernel<0> snapshot, <2> verify          7B rank shard 11.79 GB
+  (a) warp_row_kernel<0> snapshot, <2> verify         7B rank shard 11.79 GB
   (b) staged_copy_kernel, local 4 GiB aligned + 1 GiB misaligned
   (c) mask_kernel, config E busiest rank (224 x 4096^2)
   (d) absmax_kernel, fold_kernel, dequant_kernel: one 7B fp32 gradient
