@@ -84,7 +84,7 @@ def parse_args():
                    help="comma list of: e2e,cpu,inplace,reshard,host_replica,replica,replay,"
                         "migration,config_c,stage,philox,reduce")
     p.add_argument("--json-out", default="")
-    p.add_argument("--deadline-s", type=float, default=1500.0,
+    p.add_argument("--deadline-s", type=float, default=900.0,
                    help="wall-clock budget of the whole run: past it (a leg hung) rank 0 "
                         "prints the line gathered so far, marked incomplete, and all ranks exit")
     p.add_argument("--trace", action="store_true",
