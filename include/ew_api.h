@@ -259,7 +259,7 @@ int ew_write_u64_async(void* dev_ptr, uint64_t value, ew_stream_t stream);
 typedef struct ew_shardmap ew_shardmap;
 
 /* segs: ascending global order, local_off tiling [0, total) back to back.
- * The map keeps a device row table (32 B per row: e.g. 2.9 MB for a 7B rank
+ * The map keeps a device row table (32 B per row: e.g. 5.8 MB for a 7B rank
  * shard at 64 KiB blocks) for the snapshot / checksum / verify kernel. */
 int ew_shardmap_create(const ew_segment* segs, int64_t n_segs, int64_t block_bytes,
                        ew_shardmap** out);
