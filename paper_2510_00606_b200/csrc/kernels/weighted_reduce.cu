@@ -120,6 +120,13 @@ __global__ void scale_kernel(const double* __restrict__ gmax, int64_t total_unit
 // than 80 registers at 3 CTAs/SM: tools/fold_sweep.py).  Unit loads carry no
 // L2 evict-first hint: a unit buffer listed twice (config E's N = 1 leg)
 // then re-reads from L2.
+// fold grids, % of the resident CTAs (tools/fold_grid_sweep.sh): one unit
+// per element streams best oversubscribed (12.7 vs 13.5 ms for a 7B
+// gradient), two units at one wave, the pipelined form at three waves
+constexpr int kFoldGrid1Pct = 160;     // 1 unit
+constexpr int kFoldGridPct = 100;      // 2 units
+constexpr int kFoldPipeGridPct = 300;  // 3+ units (pipelined)
+
 template <bool kAccumulate, bool kPipe>
 __global__ void __launch_bounds__(256, 4) fold_kernel(Units u, int64_t n, double host_scale,
                                                    long long* __restrict__ acc,
@@ -279,10 +286,11 @@ int grid_for(int64_t work) {
 
 // Persistent grid for the 256-thread streaming kernels: every CTA resident
 // (SMs x occupancy), so the grid-stride loops run in one wave.
-int resident_grid(const void* kernel, int64_t work, int waves = 1) {
+int resident_grid(const void* kernel, int64_t work, int pct = 100) {
   int per_sm = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, 0);
-  const int64_t cap = static_cast<int64_t>(num_sms()) * std::max(1, per_sm) * waves;
+  const int64_t cap = std::max<int64_t>(
+      1, static_cast<int64_t>(num_sms()) * std::max(1, per_sm) * pct / 100);
   return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, cap)));
 }
 
@@ -380,9 +388,9 @@ int fold_impl(const float* const* units, const double* weights, int n_units, int
                                      : (const void*)fold_kernel<true, false>)
                              : (pipe ? (const void*)fold_kernel<false, true>
                                      : (const void*)fold_kernel<false, false>);
-    // unpipelined: one resident wave (62 registers x 256 threads: 4 CTAs/SM);
-    // pipelined: two waves' worth of CTAs (measured best)
-    const int grid = resident_grid(kern, (n_elems + 7) / 8, pipe ? 2 : 1);
+    // 64 registers x 256 threads: 4 resident CTAs/SM
+    const int grid = resident_grid(kern, (n_elems + 7) / 8,
+                                   pipe ? kFoldPipeGridPct : u.n == 1 ? kFoldGrid1Pct : kFoldGridPct);
     void* args[] = {&u, &n_elems, const_cast<double*>(&scale), &a, &add,
                     &dev_bits};
     EW_CUDA_TRY(cudaLaunchKernel(kern, grid, 256, args, 0, (cudaStream_t)stream));

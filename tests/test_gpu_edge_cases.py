@@ -54,6 +54,30 @@ def test_fold_addend_matches_separate_add(oracle):
         assert np.array_equal(acc.cpu().numpy(), want)
 
 
+def test_pipelined_fold_addend_accumulate_and_device_scale(oracle):
+    """3+ units take the software-pipelined fold (kPipe): with an addend,
+    with accumulate, with the scale read from device memory, on ragged sizes
+    (scalar tails) — all bit-exact against the oracle."""
+    rng = np.random.default_rng(9)
+    for n in (1, 7, 8, 4099, 100_003):
+        g = rng.normal(0, 1e-2, (5, n)).astype(np.float32)
+        w = np.array([0.1, 0.15, 0.2, 0.25, 0.3])
+        add = torch.from_numpy(rng.integers(-2 ** 40, 2 ** 40, n)).cuda()
+        units = [torch.from_numpy(x).cuda() for x in g]
+        want = oracle.weighted_fixed(w, g, 30)
+        acc = torch.empty(n, dtype=torch.int64, device="cuda")
+        dev.weighted_fold(units, w, 30, acc, addend=add)
+        torch.cuda.synchronize()
+        assert np.array_equal(acc.cpu().numpy(), want + add.cpu().numpy()), n
+        dev.weighted_fold(units, w, 30, acc, accumulate=True)
+        torch.cuda.synchronize()
+        assert np.array_equal(acc.cpu().numpy(), 2 * want + add.cpu().numpy()), n
+        bits = torch.tensor([30], dtype=torch.int32, device="cuda")
+        dev.weighted_fold_dev(units, w, bits, acc)
+        torch.cuda.synchronize()
+        assert np.array_equal(acc.cpu().numpy(), want), n
+
+
 def test_copy_program_without_items_and_adam_payback_zero():
     p = dev.CopyProgram.from_pointers([], [], [], [])
     p.launch()
