@@ -120,12 +120,16 @@ __global__ void scale_kernel(const double* __restrict__ gmax, int64_t total_unit
 // than 80 registers at 3 CTAs/SM: tools/fold_sweep.py).  Unit loads carry no
 // L2 evict-first hint: a unit buffer listed twice (config E's N = 1 leg)
 // then re-reads from L2.
-// fold grids, % of the resident CTAs (tools/fold_grid_sweep.sh): one unit
-// per element streams best oversubscribed (12.7 vs 13.5 ms for a 7B
-// gradient), two units at one wave, the pipelined form at three waves
+//
+// Grids, % of the resident CTAs (tools/fold_grid_sweep.sh, 7B gradient): the
+// write-heavy streams run best oversubscribed 1.6x (fold of one unit 12.7 vs
+// 13.5 ms, dequant 12.5 vs 13.2 ms), the fold of two units and the
+// read-only absmax at one wave, the pipelined fold at three waves.
 constexpr int kFoldGrid1Pct = 160;     // 1 unit
 constexpr int kFoldGridPct = 100;      // 2 units
 constexpr int kFoldPipeGridPct = 300;  // 3+ units (pipelined)
+constexpr int kAbsmaxGridPct = 100;
+constexpr int kDequantGridPct = 160;
 
 template <bool kAccumulate, bool kPipe>
 __global__ void __launch_bounds__(256, 4) fold_kernel(Units u, int64_t n, double host_scale,
@@ -324,7 +328,7 @@ int ew_weighted_absmax(const float* const* units, const double* weights, int n_u
   for (int off = 0; off < n_units && n_elems > 0; off += kMaxUnits) {
     Units u;
     if (int st = pack_units(units, weights, n_units, off, u)) return st;
-    absmax_kernel<<<resident_grid((const void*)absmax_kernel, (n_elems + 7) / 8), 256, 0,
+    absmax_kernel<<<resident_grid((const void*)absmax_kernel, (n_elems + 7) / 8, kAbsmaxGridPct), 256, 0,
                     (cudaStream_t)stream>>>(
         u, n_elems, reinterpret_cast<unsigned long long*>(out_max));
     EW_CUDA_TRY(cudaGetLastError());
@@ -405,7 +409,7 @@ int dequant_impl(const int64_t* acc, int64_t n, int frac_bits, const int* dev_bi
   if ((n > 0 && (!acc || !out)) || n < 0)
     return set_error(EW_ERR_INVALID_ARGUMENT, "ew_fixed_to_float/double: bad arguments");
   if (n == 0) return EW_OK;
-  dequant_kernel<T><<<resident_grid((const void*)dequant_kernel<T>, (n + 7) / 8), 256, 0,
+  dequant_kernel<T><<<resident_grid((const void*)dequant_kernel<T>, (n + 7) / 8, kDequantGridPct), 256, 0,
                       (cudaStream_t)stream>>>(reinterpret_cast<const long long*>(acc), n,
                                               std::ldexp(1.0, -frac_bits), out, dev_bits);
   EW_CUDA_TRY(cudaGetLastError());

@@ -40,6 +40,20 @@ def main():
         dram = (4 * min(nu, 2) + 8) * n
         res[nu] = {"ms": round(best, 3), "dram_gbs": round(dram / best / 1e6, 1),
                    "unit_elems_g_per_s": round(nu * n / best / 1e6, 1)}
+    # the pre-pass and the dequant on one unit
+    f = dev.fixed_point_bits(dev.weighted_absmax(bufs[:1], [1.0]).item(), 1)
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    for name, fn, moved in (("absmax", lambda: dev.weighted_absmax(bufs[:1], [1.0]), 4 * n),
+                            ("dequant", lambda: dev.fixed_to_float(acc, f, out), 12 * n)):
+        best = 1e9
+        for _ in range(args.reps):
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            fn()
+            e.record()
+            torch.cuda.synchronize()
+            best = min(best, s.elapsed_time(e))
+        res[name] = {"ms": round(best, 3), "gbs": round(moved / best / 1e6, 1)}
     print(json.dumps(res))
 
 
