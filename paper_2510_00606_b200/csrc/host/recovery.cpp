@@ -304,6 +304,16 @@ void dfree(void* p) {
   if (p != nullptr) ew_free(p);
 }
 
+// owning device allocation (freed on every exit path)
+template <typename T>
+struct DevArray {
+  T* p;
+  explicit DevArray(std::int64_t count) : p(dalloc<T>(count)) {}
+  ~DevArray() { dfree(p); }
+  DevArray(const DevArray&) = delete;
+  DevArray& operator=(const DevArray&) = delete;
+};
+
 std::vector<ew_segment> to_ew(const std::vector<Segment>& segs) {
   std::vector<ew_segment> out;
   out.reserve(segs.size());
@@ -1371,13 +1381,12 @@ void DpGroup::prepare() {
   // time across the group (host barrier between them): siblings that share
   // resources must never run concurrently, and the members of different
   // siblings would otherwise start them in different orders
-  std::int64_t* one = dalloc<std::int64_t>(1);
+  const DevArray<std::int64_t> one(1);
   for (int d : members_) {
-    if (d != me) check(ew_allreduce_i64(prepared_comms_.at(d), one, 1, nullptr));
+    if (d != me) check(ew_allreduce_i64(prepared_comms_.at(d), one.p, 1, nullptr));
     check(ew_device_sync());
     ch_.barrier();
   }
-  dfree(one);
 }
 
 MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
@@ -1420,10 +1429,9 @@ MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
       ev.phases["comm_prepared"] = 0.0;
     }
     const auto t_c = Clock::now();
-    std::int64_t* one = dalloc<std::int64_t>(1);
-    check(ew_allreduce_i64(new_comm, one, 1, stream));
+    const DevArray<std::int64_t> one(1);
+    check(ew_allreduce_i64(new_comm, one.p, 1, stream));
     check(ew_stream_sync(stream));
-    dfree(one);
     ev.phases["comm_acquire_s"] = seconds(t_edit, t_c);
     ev.phases["first_collective_s"] = seconds(t_c, Clock::now());
   }
@@ -1454,11 +1462,13 @@ MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
                ch_.me());
     const ReshardPlan rp = ReshardPlan::build(layer_bytes_, members_, survivors);
     const std::int64_t n_words = 2 * rp.n_blocks(opt_.block_bytes);
-    std::uint64_t* landed = dalloc<std::uint64_t>(n_words);
-    std::uint64_t* old_blocks = dalloc<std::uint64_t>(n_words);
-    std::uint64_t* rep_blocks = dalloc<std::uint64_t>(n_words);
-    std::uint32_t* bad = dalloc<std::uint32_t>(4);
-    try {
+    const DevArray<std::uint64_t> landed_buf(n_words), old_buf(n_words), rep_buf(n_words);
+    const DevArray<std::uint32_t> bad_buf(4);
+    std::uint64_t* landed = landed_buf.p;
+    std::uint64_t* old_blocks = old_buf.p;
+    std::uint64_t* rep_blocks = rep_buf.p;
+    std::uint32_t* bad = bad_buf.p;
+    {
       const auto tp = Clock::now();
       check(ew_memset_async(old_blocks, 0, n_words * 8, stream));
       check(ew_memset_async(rep_blocks, 0, n_words * 8, stream));
@@ -1489,15 +1499,7 @@ MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
                              stream, &ev);
       mv.exec.reset();
       peers.close();
-    } catch (...) {
-      for (void* p : {static_cast<void*>(landed), static_cast<void*>(old_blocks),
-                      static_cast<void*>(rep_blocks), static_cast<void*>(bad)})
-        dfree(p);
-      throw;
     }
-    for (void* p : {static_cast<void*>(landed), static_cast<void*>(old_blocks),
-                    static_cast<void*>(rep_blocks), static_cast<void*>(bad)})
-      dfree(p);
   }
   ++events_;
   ev.remap_s = seconds(t2, Clock::now());
