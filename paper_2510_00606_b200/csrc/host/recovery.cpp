@@ -24,6 +24,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cerrno>
 #include <chrono>
 #include <condition_variable>
 #include <cstdio>
@@ -176,10 +177,21 @@ class TcpServer {
         if (!send_all(c, &ack, 1)) break;
       } else if (op == 'G') {
         std::string v;
+        bool gone = false;
         {
           std::unique_lock<std::mutex> lk(mu_);
-          cv_.wait(lk, [&] { return stop_.load() || data_.count(key) > 0; });
-          if (stop_) break;
+          // a client that gave up (its get timed out) and closed the
+          // connection must not keep this worker waiting for the key
+          while (!cv_.wait_for(lk, std::chrono::milliseconds(200),
+                               [&] { return stop_.load() || data_.count(key) > 0; })) {
+            char b;
+            const ssize_t k = ::recv(c, &b, 1, MSG_PEEK | MSG_DONTWAIT);
+            if (k == 0 || (k < 0 && errno != EAGAIN && errno != EWOULDBLOCK)) {
+              gone = true;
+              break;
+            }
+          }
+          if (stop_ || gone) break;
           v = data_[key];
         }
         const uint64_t vl = v.size();
@@ -237,39 +249,53 @@ class TcpStore final : public Store {
   }
   void set(const std::string& key, const std::string& value) override {
     std::lock_guard<std::mutex> lk(mu_);
+    usable();
     const char op = 'S';
     const uint32_t kl = static_cast<uint32_t>(key.size());
     const uint64_t vl = value.size();
     char ack = 0;
     if (!send_all(fd_, &op, 1) || !send_all(fd_, &kl, 4) || !send_all(fd_, key.data(), kl) ||
         !send_all(fd_, &vl, 8) || !send_all(fd_, value.data(), vl) || !recv_all(fd_, &ack, 1))
-      throw std::runtime_error("tcp store: set(" + key + ") failed");
+      fail("set(" + key + ") failed");
   }
   void erase(const std::string& key) override {
     std::lock_guard<std::mutex> lk(mu_);
+    usable();
     const char op = 'D';
     const uint32_t kl = static_cast<uint32_t>(key.size());
     char ack = 0;
     if (!send_all(fd_, &op, 1) || !send_all(fd_, &kl, 4) || !send_all(fd_, key.data(), kl) ||
         !recv_all(fd_, &ack, 1))
-      throw std::runtime_error("tcp store: erase(" + key + ") failed");
+      fail("erase(" + key + ") failed");
   }
   std::string get(const std::string& key) override {
     std::lock_guard<std::mutex> lk(mu_);
+    usable();
     const char op = 'G';
     const uint32_t kl = static_cast<uint32_t>(key.size());
     uint64_t vl = 0;
     if (!send_all(fd_, &op, 1) || !send_all(fd_, &kl, 4) || !send_all(fd_, key.data(), kl) ||
         !recv_all(fd_, &vl, 8))
-      throw std::runtime_error("tcp store: get(" + key + ") failed or timed out");
+      fail("get(" + key + ") failed or timed out");
     std::string v(vl, '\0');
-    if (!recv_all(fd_, v.data(), vl)) throw std::runtime_error("tcp store: get(" + key + ") cut");
+    if (!recv_all(fd_, v.data(), vl)) fail("get(" + key + ") cut");
     return v;
   }
 
  private:
+  // a failed or timed-out exchange leaves the stream mid-frame (the server may
+  // still answer a timed-out get): the connection is unusable from then on
+  void usable() const {
+    if (broken_) throw std::runtime_error("tcp store: connection broken by an earlier failure");
+  }
+  [[noreturn]] void fail(const std::string& what) {
+    broken_ = true;
+    throw std::runtime_error("tcp store: " + what);
+  }
+
   std::unique_ptr<TcpServer> server_;
   int fd_ = -1;
+  bool broken_ = false;
   std::mutex mu_;
 };
 

@@ -88,3 +88,23 @@ def test_mttr_csv_from_cpp():
     ev = MttrEvent(step=7, t_event_s=1.5, kind="scale_in", comm_repair_s=0.000163,
                    remap_s=0.0118, other_s=1e-6, lost_work_s=0.25)
     assert ev.csv_row(2) == "2,7,1.5,scale_in,0,0.000163,0.0118,0,1e-06,0.25,0.011964"
+
+
+def test_tcp_store_timeout_breaks_the_connection():
+    """A get that times out leaves the stream mid-frame (the server may
+    answer later): the store reports it and refuses further use instead of
+    reading a stale answer as the next reply."""
+    import sys
+    from pathlib import Path
+    sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+    from paper_2510_00606_b200._native import ElaskitError
+    from paper_2510_00606_b200.rendezvous import Store
+
+    st = Store.tcp("127.0.0.1", _port(), True, 0.5)
+    st.set("a", b"1")
+    assert st.get("a") == b"1"
+    with pytest.raises(ElaskitError, match="timed out"):
+        st.get("never-set")
+    with pytest.raises(ElaskitError, match="broken"):
+        st.set("b", b"2")
+    st.close()
