@@ -81,8 +81,8 @@ def parse_args():
     p.add_argument("--only-inplace", action="store_true",
                    help="run only the snapshot leg and the in-place reshard leg")
     p.add_argument("--skip", default="",
-                   help="comma list of: e2e,cpu,inplace,reshard,host_replica,replica,replay,"
-                        "migration,config_c,stage,philox,reduce")
+                   help="comma list of: e2e,cpu,inplace,config_d,reshard,host_replica,replica,"
+                        "replay,migration,config_c,stage,philox,reduce,config_a")
     p.add_argument("--json-out", default="")
     p.add_argument("--deadline-s", type=float, default=900.0,
                    help="wall-clock budget of the whole run: past it (a leg hung) rank 0 "
@@ -959,7 +959,23 @@ def run_config_c(args, rank, world, out):
     out["config_c"] = res
 
 
-def run_inplace(args, rank, world, out):
+def config_d_state_gb(world: int) -> float:
+    """Per-GPU state of the default config D reshard leg: as large as the
+    staged in-place footprint allows on the busiest rank — the ring holder of
+    the departed rank keeps max(OLD, NEW) = S·N/(N−1) plus the departed
+    rank's replica S plus the staging buffers — within ~150 GB of HBM, and at
+    most config D's 70 GB (2 -> 1: 50 GB, 4 -> 3: 64 GB, 8 -> 7: 70 GB)."""
+    return round(min(70.0, 150.0 / (world / (world - 1) + 1.0)), 1)
+
+
+def run_config_d_reshard(args, rank, world, out):
+    """Config D's reshard half in the default N > 1 run: fill-HBM geometry
+    (80 equal layers, config_d_state_gb per GPU), N -> N-1 staged in place."""
+    run_inplace(args, rank, world, out, state_gb=config_d_state_gb(world),
+                key="config_d_reshard")
+
+
+def run_inplace(args, rank, world, out, state_gb=None, key="inplace"):
     """Config D reshard at fill-HBM sizes, staged in place (inplace.py): a
     rank's OLD and NEW shards share one buffer, the move runs in phases over
     the global byte space through two staging buffers, verified on arrival.
@@ -973,8 +989,10 @@ def run_inplace(args, rank, world, out):
 
     torch.cuda.empty_cache()
     torch.cuda.reset_peak_memory_stats()
-    if args.inplace_state_gb > 0:   # config D geometry, S bytes per GPU
-        lb = configs.fill_hbm(world, int(args.inplace_state_gb * 1e9)).layer_bytes
+    if state_gb is None:
+        state_gb = args.inplace_state_gb
+    if state_gb > 0:                # config D geometry, S bytes per GPU
+        lb = configs.fill_hbm(world, int(state_gb * 1e9)).layer_bytes
         geometry = "config D fill-HBM"
     else:                           # the reshard leg's 7B-per-GPU state, for comparison
         base = configs.llama2_7b()
@@ -1042,7 +1060,7 @@ def run_inplace(args, rank, world, out):
     traffic = rp.traffic()
     bott = traffic["bottleneck_bytes"]
     sched = ex.sched
-    out["inplace"] = {
+    out[key] = {
         "workload": f"{geometry} {world}->{world - 1} (drop rank {drop}), staged in place",
         "per_gpu_state_bytes": rp.src.shard_bytes(0), "state_bytes": int(sum(lb)),
         "total_bytes_moved": traffic["total_bytes_moved"], "bottleneck_gpu_bytes": bott,
@@ -1906,6 +1924,9 @@ def bench_b200(args):
     if world > 1 and (args.inplace_state_gb > 0 or "inplace" not in skip):
         trace("inplace")
         guard.run("inplace", run_inplace, args, rank, world, out)
+    if world > 1 and "config_d" not in skip and not args.only_inplace:
+        trace("config_d_reshard")
+        guard.run("config_d_reshard", run_config_d_reshard, args, rank, world, out)
     if world == 1 and rank == 0 and "cpu" not in skip:
         trace("cpu_baseline")
         guard.run("cpu_baseline", run_cpu_baseline, args, out, segs, S)
