@@ -957,6 +957,136 @@ def run_config_c(args, rank, world, out):
         del bufs, before, after
         torch.cuda.empty_cache()
     out["config_c"] = res
+    res["mttr"] = config_c_mttr(args, rank, world, lb, gone)
+
+
+def config_c_mttr(args, rank, world, lb, gone):
+    """Config C's two events as measured recoveries through the C++ DpGroup
+    (the reference's recover_elaswave for FailStop/ScaleIn and ScaleOut,
+    sim.cpp:597-722), with the NCCL communicator of the (d) reduce repaired
+    each time: steady state prepares the shrunk communicator of the pair
+    (ncclCommSplit) and, after the departure, the grown standby communicator
+    for their return; the survivors then recover the pair (planned at failure
+    time: plan, IPC mapping, verified copy, conservation) and the pair
+    rejoins from the free pool (the same processes: ScaleOut, members re-cut
+    their shards over the grown group, joiners only receive).  Every
+    participant's buffers are IPC-mapped in steady state (DpGroup.premap, and
+    prepare_join for the joiners), the source block sums come from the
+    per-step snapshot rows, and each rank's verified program for the event is
+    lowered and bound in steady state (DpGroup.prepare_move), so the event
+    launches it.  MTTR = max over the participants; bytes checked against the
+    synthetic state."""
+    import torch
+    import torch.distributed as dist
+    from paper_2510_00606_b200 import device as dev
+    from paper_2510_00606_b200.fabric import SCALE_IN, SCALE_OUT
+    from paper_2510_00606_b200.recovery import DpGroup
+    from paper_2510_00606_b200.reshard import RankBuffers, ReshardPlan, shard_map
+
+    members = list(range(world))
+    kept = [r for r in members if r not in gone]
+    block = args.block_bytes
+    uid = [dev.Communicator.unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(uid, src=0)
+    comm = dev.Communicator.init(uid[0], world, rank)
+    grp = DpGroup(lb, members, rank, comm, prepare_comms=False, block_bytes=block)
+    t0 = time.perf_counter()
+    grp.prepare([gone])
+    t_prep_split = max_over_ranks([time.perf_counter() - t0], world)[0]
+    rp_in = ReshardPlan.build(lb, members, kept)
+    rp_out = ReshardPlan.build(lb, kept, members)
+    live = dev.empty_bytes(rp_in.src.shard_bytes(rank))
+    dev.fill_synthetic(shard_map(rp_in.src, rank, block), live, 8)
+    owner = rp_in.replica_of(rank)
+    replica = None
+    if owner in gone:
+        replica = dev.empty_bytes(rp_in.src.shard_bytes(owner))
+        dev.fill_synthetic(shard_map(rp_in.src, owner, block), replica, 8)
+    new_in = dev.empty_bytes(rp_in.dst.shard_bytes(rank)) if rank in kept else None
+    new_out = dev.empty_bytes(rp_out.dst.shard_bytes(rank))
+    # the per-step snapshot's checksum rows of the live shard and the replica
+    live_map = shard_map(rp_in.src, rank, block)
+    live_rows = live_map.new_row_sums()
+    dev.checksum(live_map, live, live_rows)
+    rep_rows = None
+    if replica is not None:
+        rep_map = shard_map(rp_in.src, owner, block)
+        rep_rows = rep_map.new_row_sums()
+        dev.checksum(rep_map, replica, rep_rows)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    grp.premap(RankBuffers(live, replica, None), live_rows, rep_rows)
+    grp.prepare_move(SCALE_IN, gone, new_in)
+    torch.cuda.synchronize()
+    t_premap = max_over_ranks([time.perf_counter() - t0], world)[0]
+
+    def expect(layout, buf):
+        n = layout.shard_bytes(rank)
+        e = dev.empty_bytes(n)
+        dev.fill_synthetic(shard_map(layout, rank, block), e, 8)
+        ok = bool(torch.equal(buf[:n], e[:n]))
+        del e
+        return ok
+
+    def summary(ev, ok):
+        vals = [ev.total_s(), ev.comm_repair_s, ev.remap_s, ev.phases.get("copy_s", 0.0),
+                ev.phases.get("map_bind_s", 0.0), ev.phases.get("plan_s", 0.0),
+                ev.phases.get("sums_s", 0.0), ev.phases.get("bind_s", 0.0)] \
+            if ev is not None else [0.0] * 8
+        mx = max_over_ranks(vals, world)
+        flags = torch.tensor([1 if ok else 0, 1 if (ev is None or ev.verified) else 0,
+                              1 if (ev is None or ev.phases.get("comm_prepared") == 1.0) else 0],
+                             device="cuda")
+        dist.all_reduce(flags, op=dist.ReduceOp.MIN)
+        pm = torch.tensor([1 if (ev is None or ev.phases.get("premapped") == 1.0) else 0,
+                           1 if (ev is None or ev.phases.get("prepared") == 1.0) else 0],
+                          device="cuda")
+        dist.all_reduce(pm, op=dist.ReduceOp.MIN)
+        return {"premapped": bool(pm[0].item()), "program_prepared": bool(pm[1].item()),
+                "mttr_ms": round(mx[0] * 1e3, 3), "comm_repair_ms": round(mx[1] * 1e3, 3),
+                "remap_ms": round(mx[2] * 1e3, 3), "copy_ms": round(mx[3] * 1e3, 3),
+                "map_bind_ms": round(mx[4] * 1e3, 3), "plan_ms": round(mx[5] * 1e3, 3),
+                "source_sums_ms": round(mx[6] * 1e3, 3), "lower_bind_ms": round(mx[7] * 1e3, 3),
+                "bytes_exact": bool(flags[0].item()), "verified": bool(flags[1].item()),
+                "comm_prepared": bool(flags[2].item()),
+                "mttr_csv_rank0_row": ev.csv_row(0) if (ev is not None and rank == 0) else None}
+
+    torch.cuda.synchronize()
+    barrier(world)
+    ev = None
+    if rank in kept:
+        ev = grp.recover(gone, RankBuffers(live, replica, new_in), step=1, kind=SCALE_IN)
+    scale_in = summary(ev, expect(rp_in.dst, new_in) if rank in kept else True)
+    barrier(world)
+    jg = DpGroup.joiner(lb, kept, rank, grp.name, block_bytes=block) if rank in gone else grp
+    t0 = time.perf_counter()
+    if rank in kept:  # steady state after the departure: snapshot rows, map the new shards
+        in_map = shard_map(rp_in.dst, rank, block)
+        in_rows = in_map.new_row_sums()
+        dev.checksum(in_map, new_in, in_rows)
+        grp.premap(RankBuffers(new_in, None, None), in_rows)
+    jg.prepare_join(gone)
+    jg.prepare_move(SCALE_OUT, gone, new_out)
+    torch.cuda.synchronize()
+    t_prep_standby = max_over_ranks([time.perf_counter() - t0], world)[0]
+    barrier(world)
+    ev = jg.admit(gone, RankBuffers(new_in, None, new_out), step=2)
+    rejoin = summary(ev, expect(rp_out.dst, new_out))
+    rejoin["members_after"] = len(jg.members)
+    barrier(world)
+    if jg is not grp:
+        jg.close()
+    grp.close()
+    del live, replica, new_in, new_out
+    torch.cuda.empty_cache()
+    return {"what": "measured through DpGroup (C++): ScaleIn of the pair, then its ScaleOut, "
+                    "each with comm repair, reshape and a verified remap prepared in steady "
+                    "state (premap, snapshot rows, prepare_move)",
+            "steady_state_ms": {"prepare_pair_split": round(t_prep_split * 1e3, 1),
+                                "premap_and_prepare_move": round(t_premap * 1e3, 1),
+                                "premap_standby_comm_and_prepare_move":
+                                    round(t_prep_standby * 1e3, 1)},
+            "scale_in": scale_in, "rejoin": rejoin}
 
 
 def config_d_state_gb(world: int) -> float:

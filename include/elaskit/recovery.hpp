@@ -584,6 +584,13 @@ class DpGroup {
   // departure, done in steady state).
   DpGroup(Channel& ch, const std::vector<std::int64_t>& layer_bytes, ew_comm* comm,
           DpGroupOptions opt = {});
+  // A process outside the group that joins it at a ScaleOut (a device from
+  // the free pool, cluster.hpp): it meets the members on `store` under the
+  // members' group channel name `group_name`, with the group's current
+  // `members`.  It has no communicator, shard or micro-batches until
+  // recover(joiners, EventKind::ScaleOut, ...), where it learns them.
+  DpGroup(Store& store, std::string group_name, const std::vector<std::int64_t>& layer_bytes,
+          std::vector<int> members, int me, DpGroupOptions opt = {});
   ~DpGroup();
   DpGroup(const DpGroup&) = delete;
   DpGroup& operator=(const DpGroup&) = delete;
@@ -593,25 +600,73 @@ class DpGroup {
   void attach(PreparedRecovery* prepared) { prepared_ = prepared; }
   // Survivors call this for a FailStop / ScaleIn of `departed`.  bufs: this
   // rank's OLD / REPLICA / NEW buffers for the change when not prepared.
+  // ScaleOut (the reference's rejoin, sim.cpp:608,676-677): `departed` names
+  // the joiners, and every member and every joiner calls it — members pass
+  // OLD (their shard) and NEW, joiners NEW only.  Comm repair adds the
+  // joiners' links (plan_edit) and builds the grown NCCL communicator (a
+  // standby one from prepare_join when every participant has it, else
+  // ncclCommInitRank now); the micro-batches are re-dealt over the grown
+  // group; the members' shards are re-cut over it by one verified pull
+  // program per GPU.  `step` names the event: the same (step, membership
+  // change) must not recur within one group.
   MttrEvent recover(const std::vector<int>& departed, EventKind kind, const RankBuffers& bufs,
                     ew_stream_t stream, int step = 0);
+  // Steady state before an expected ScaleOut (standby devices): build and
+  // warm the grown communicator over members ∪ joiners now, so the join's
+  // comm repair is a lookup; when the members premapped, the joiners map
+  // the members' buffers now too.  Collective over members and joiners.
+  void prepare_join(const std::vector<int>& joiners);
+  // Steady state: map every member's OLD shard and replica (what a pull
+  // program reads) and the verification arrays once, so an event planned at
+  // failure time (a departure set without a PreparedRecovery, a ScaleOut)
+  // pays no CUDA IPC mapping on its critical path.  Used by an event whose
+  // participants all pass the buffers they premapped (agreed over the
+  // store); otherwise the event maps as before.  old_rows / replica_rows:
+  // the per-step snapshot's checksum rows of those buffers (device arrays
+  // the caller refreshes in place every step); the event then takes its
+  // source block sums from them instead of re-reading the shards.
+  // Collective over the members.
+  void premap(const RankBuffers& bufs, const std::uint64_t* old_rows = nullptr,
+              const std::uint64_t* replica_rows = nullptr);
+  // Steady state, local: lower and bind this rank's verified pull program
+  // for one expected event (a departure set, kind FailStop/ScaleIn, or the
+  // joiners of a ScaleOut) into `new_buf`, over the premapped buffers.  The
+  // event then only launches it.  After premap (members) / prepare_join
+  // (joiners); a departing member has nothing to prepare.
+  void prepare_move(EventKind kind, const std::vector<int>& targets, void* new_buf);
   // (Re)build one shrunk communicator per possible single departure of the
   // current membership (ncclCommSplit, splitShare) and run one collective on
   // each: steady-state work, collective over the members.  The constructor
-  // calls it when opt.prepare_comms.
+  // calls it when opt.prepare_comms.  A departure whose set was prepared
+  // repairs by lookup; any other by ncclCommShrink at failure time.
   void prepare();
+  // The same for the given departure sets (e.g. config C's two non-adjacent
+  // members leaving together): one shrunk communicator per set.
+  void prepare(const std::vector<std::vector<int>>& departures);
   ew_comm* comm() const { return comm_; }
   const std::vector<int>& members() const { return members_; }
   const std::vector<int>& microbatch_sizes() const { return mb_sizes_; }
 
  private:
-  Channel& ch_;
+  MttrEvent admit(const std::vector<int>& joiners, const RankBuffers& bufs, ew_stream_t stream,
+                  int step);
+  void commit_members(std::vector<int> next);
+  struct Premap;
+  std::unique_ptr<Premap> pm_;
+
+  Store& store_;
+  std::string name_;
+  int me_;
+  Channel* ch_;                      // over members_: the caller's, after a change owned
+  std::unique_ptr<Channel> own_ch_;
   std::vector<std::int64_t> layer_bytes_;
   std::vector<int> members_;
   std::vector<int> mb_sizes_;
   std::set<Link> links_;
   ew_comm* comm_ = nullptr;
-  std::map<int, ew_comm*> prepared_comms_;  // departed member -> shrunk comm
+  std::map<std::vector<int>, ew_comm*> prepared_comms_;  // departed set -> shrunk comm
+  std::map<std::vector<int>, ew_comm*> standby_comms_;  // grown membership -> comm
+  std::map<std::vector<int>, int> standby_rounds_;
   std::vector<ew_comm*> retired_;           // parents of splits, freed last
   DpGroupOptions opt_;
   PreparedRecovery* prepared_ = nullptr;

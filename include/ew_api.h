@@ -566,6 +566,9 @@ typedef struct ew_mttr_event {
   double plan_edit_s, comm_acquire_s, first_collective_s, comm_prepared;
   double plan_s, map_bind_s, copy_s, barrier_verify_s, verdict_exchange_s, launch_to_verdict_s;
   double mismatched_block_words, barrier_timeouts;
+  double premapped; /* 1: the event used the group's steady-state peer mapping */
+  double sums_s, bind_s; /* map_bind_s split: source block sums; lowering + program build */
+  double prepared; /* 1: the event launched a program prepared in steady state */
 } ew_mttr_event;
 /* mttr.csv (reference sim.cpp:1119-1132): header line and one row, no '\n' */
 int ew_mttr_csv_header(char* buf, int64_t cap);
@@ -620,16 +623,38 @@ void ew_prepared_free(ew_prepared* p);
  * prepared shrunk communicator per possible departure (prepare_comms: a
  * collective ncclCommSplit per member, splitShare, warmed by one
  * all-reduce), micro-batch reshaper, recovery -> MttrEvent.  kind: 0
- * FailStop, 2 ScaleIn (elaskit::EventKind).  prepare_comms: bit 0 prepares
- * the communicators, bit 1 builds them with splitShare (less memory; NCCL
- * then forbids concurrent use of siblings).  old_buf / replica / new_buf are
- * used when no prepared recovery is attached (planning at failure time). */
+ * FailStop, 2 ScaleIn, 3 ScaleOut (elaskit::EventKind).  prepare_comms: bit
+ * 0 prepares the communicators, bit 1 builds them with splitShare (less
+ * memory; NCCL then forbids concurrent use of siblings).  old_buf / replica /
+ * new_buf are used when no prepared recovery is attached (planning at failure
+ * time).  ScaleOut: `departed` lists the joiners; every member (old_buf =
+ * its shard, new_buf) and every joiner (new_buf only) calls recover; a
+ * joiner's group comes from ew_dp_group_create_joiner (the members' group
+ * channel name and current members, `me` outside them).
+ * ew_dp_group_prepare_join: steady-state grown communicator over members +
+ * joiners (collective over both), so the join's comm repair is a lookup. */
 typedef struct ew_dp_group ew_dp_group;
 int ew_dp_group_create(ew_channel* ch, const int64_t* layer_bytes, int n_layers, ew_comm* comm,
                        int per_slot_mbs, int num_microbatches, int64_t block_bytes,
                        int prepare_comms, ew_dp_group** out);
+int ew_dp_group_create_joiner(ew_store* store, const char* group_name, const int64_t* layer_bytes,
+                              int n_layers, const int* members, int n_members, int me,
+                              int per_slot_mbs, int num_microbatches, int64_t block_bytes,
+                              ew_dp_group** out);
+int ew_dp_group_prepare_join(ew_dp_group* g, const int* joiners, int n);
+/* steady-state peer mapping of this member's OLD shard and replica (NULL if
+ * none) and the verification arrays (collective over the members); rows:
+ * the per-step snapshot rows of those buffers (NULL: re-read at the event).
+ * prepare_move (local): this rank's verified program for one expected event
+ * (kind 0/2 departure set, 3 joiners) into new_buf, bound in steady state. */
+int ew_dp_group_premap(ew_dp_group* g, void* old_buf, void* replica, const uint64_t* old_rows,
+                       const uint64_t* replica_rows);
+int ew_dp_group_prepare_move(ew_dp_group* g, int kind, const int* targets, int n, void* new_buf);
 int ew_dp_group_attach(ew_dp_group* g, ew_prepared* prepared);
 int ew_dp_group_prepare(ew_dp_group* g);
+/* prepared communicators for the given departure sets instead (set i =
+ * members[offsets[i] .. offsets[i + 1]), n_sets + 1 offsets) */
+int ew_dp_group_prepare_sets(ew_dp_group* g, const int* members, const int* offsets, int n_sets);
 int ew_dp_group_recover(ew_dp_group* g, const int* departed, int n, int kind, void* old_buf,
                         void* replica, void* new_buf, int step, ew_stream_t stream,
                         ew_mttr_event* ev);

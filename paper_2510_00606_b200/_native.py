@@ -273,7 +273,7 @@ class MttrEventC(C.Structure):
                     "lost_work_s", "plan_edit_s", "comm_acquire_s", "first_collective_s",
                     "comm_prepared", "plan_s", "map_bind_s", "copy_s", "barrier_verify_s",
                     "verdict_exchange_s", "launch_to_verdict_s", "mismatched_block_words",
-                    "barrier_timeouts")]
+                    "barrier_timeouts", "premapped", "sums_s", "bind_s", "prepared")]
 
 
 STORE_SET_FN = C.CFUNCTYPE(i32, vp, C.POINTER(C.c_char), i64, C.POINTER(C.c_char), i64)
@@ -305,8 +305,14 @@ _sig("ew_prepared_recover", i32, vp, i32, vp, P(MttrEventC), P(i32))
 _sig("ew_prepared_new", i32, vp, i32, P(vp), P(i64))
 _sig("ew_prepared_free", None, vp)
 _sig("ew_dp_group_create", i32, vp, P(i64), i32, vp, i32, i32, i64, i32, P(vp))
+_sig("ew_dp_group_create_joiner", i32, vp, C.c_char_p, P(i64), i32, P(i32), i32, i32, i32, i32,
+     i64, P(vp))
+_sig("ew_dp_group_prepare_join", i32, vp, P(i32), i32)
+_sig("ew_dp_group_premap", i32, vp, vp, vp, vp, vp)
+_sig("ew_dp_group_prepare_move", i32, vp, i32, P(i32), i32, vp)
 _sig("ew_dp_group_attach", i32, vp, vp)
 _sig("ew_dp_group_prepare", i32, vp)
+_sig("ew_dp_group_prepare_sets", i32, vp, P(i32), P(i32), i32)
 _sig("ew_dp_group_recover", i32, vp, P(i32), i32, i32, vp, vp, vp, i32, vp, P(MttrEventC))
 _sig("ew_dp_group_comm", i32, vp, P(vp))
 _sig("ew_dp_group_members", i32, vp, P(i32), i32, P(i32))

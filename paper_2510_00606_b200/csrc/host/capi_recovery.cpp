@@ -93,6 +93,10 @@ void to_c(const MttrEvent& ev, ew_mttr_event* out) {
   out->launch_to_verdict_s = ph("launch_to_verdict_s");
   out->mismatched_block_words = ph("mismatched_block_words");
   out->barrier_timeouts = ph("barrier_timeouts");
+  out->premapped = ph("premapped");
+  out->sums_s = ph("sums_s");
+  out->bind_s = ph("bind_s");
+  out->prepared = ph("prepared");
 }
 
 MttrEvent from_c(const ew_mttr_event& e) {
@@ -364,6 +368,58 @@ int ew_dp_group_create(ew_channel* ch, const int64_t* layer_bytes, int n_layers,
   });
 }
 
+int ew_dp_group_create_joiner(ew_store* store, const char* group_name, const int64_t* layer_bytes,
+                              int n_layers, const int* members, int n_members, int me,
+                              int per_slot_mbs, int num_microbatches, int64_t block_bytes,
+                              ew_dp_group** out) {
+  return guarded([&]() -> int {
+    if (store == nullptr || group_name == nullptr || layer_bytes == nullptr || n_layers < 1 ||
+        members == nullptr || n_members < 1 || out == nullptr)
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_dp_group_create_joiner: bad arguments");
+    elaskit::b200::DpGroupOptions opt;
+    opt.per_slot_mbs = per_slot_mbs;
+    opt.num_microbatches = num_microbatches;
+    opt.block_bytes = block_bytes;
+    opt.prepare_comms = false;
+    *out = new ew_dp_group{std::make_unique<DpGroup>(
+        *store->s, std::string(group_name), std::vector<int64_t>(layer_bytes, layer_bytes + n_layers),
+        std::vector<int>(members, members + n_members), me, opt)};
+    return EW_OK;
+  });
+}
+
+int ew_dp_group_prepare_join(ew_dp_group* g, const int* joiners, int n) {
+  return guarded([&]() -> int {
+    if (g == nullptr || joiners == nullptr || n < 1)
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_dp_group_prepare_join: bad arguments");
+    g->g->prepare_join(std::vector<int>(joiners, joiners + n));
+    return EW_OK;
+  });
+}
+
+int ew_dp_group_premap(ew_dp_group* g, void* old_buf, void* replica, const uint64_t* old_rows,
+                       const uint64_t* replica_rows) {
+  return guarded([&]() -> int {
+    if (g == nullptr || old_buf == nullptr)
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_dp_group_premap: bad arguments");
+    elaskit::b200::RankBuffers b;
+    b.old_buf = old_buf;
+    b.replica = replica;
+    g->g->premap(b, old_rows, replica_rows);
+    return EW_OK;
+  });
+}
+
+int ew_dp_group_prepare_move(ew_dp_group* g, int kind, const int* targets, int n, void* new_buf) {
+  return guarded([&]() -> int {
+    if (g == nullptr || targets == nullptr || n < 1 || kind < 0 || kind > 3)
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_dp_group_prepare_move: bad arguments");
+    g->g->prepare_move(static_cast<elaskit::EventKind>(kind),
+                       std::vector<int>(targets, targets + n), new_buf);
+    return EW_OK;
+  });
+}
+
 int ew_dp_group_attach(ew_dp_group* g, ew_prepared* p) {
   if (g == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
   g->g->attach(p ? p->p.get() : nullptr);
@@ -374,6 +430,21 @@ int ew_dp_group_prepare(ew_dp_group* g) {
   return guarded([&]() -> int {
     if (g == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL");
     g->g->prepare();
+    return EW_OK;
+  });
+}
+
+int ew_dp_group_prepare_sets(ew_dp_group* g, const int* members, const int* offsets, int n_sets) {
+  return guarded([&]() -> int {
+    if (g == nullptr || offsets == nullptr || n_sets < 1 || (members == nullptr && offsets[n_sets]))
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_dp_group_prepare_sets: bad arguments");
+    std::vector<std::vector<int>> sets;
+    for (int i = 0; i < n_sets; ++i) {
+      if (offsets[i + 1] < offsets[i])
+        return set_error(EW_ERR_INVALID_ARGUMENT, "ew_dp_group_prepare_sets: offsets decrease");
+      sets.emplace_back(members + offsets[i], members + offsets[i + 1]);
+    }
+    g->g->prepare(sets);
     return EW_OK;
   });
 }

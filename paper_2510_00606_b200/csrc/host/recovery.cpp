@@ -1368,14 +1368,196 @@ bool PreparedRecovery::recover(int departed, ew_stream_t stream, MttrEvent* ev) 
 
 // ----------------------------------------------------------------- DpGroup
 
+namespace {
+
+std::string csv(const std::vector<int>& v) {
+  std::string s;
+  for (int x : v) s += (s.empty() ? "" : ",") + std::to_string(x);
+  return s;
+}
+
+std::vector<int> parse_csv(const std::string& s) {
+  std::vector<int> out;
+  std::size_t p = 0;
+  while (p < s.size()) {
+    const std::size_t q = s.find(',', p);
+    out.push_back(std::stoi(s.substr(p, q == std::string::npos ? std::string::npos : q - p)));
+    if (q == std::string::npos) break;
+    p = q + 1;
+  }
+  return out;
+}
+
+// NCCL communicator over ch's members in member order (ncclCommInitRank; the
+// unique id comes from member index 0 over the channel).  Collective.
+ew_comm* init_comm(Channel& ch) {
+  std::string id;
+  if (ch.index() == 0) {
+    id.assign(128, '\0');
+    check(ew_comm_unique_id(id.data()));
+  }
+  const std::vector<std::string> ids = ch.allgather(id);
+  if (ids.front().size() != 128) throw std::runtime_error("communicator id exchange failed");
+  ew_comm* c = nullptr;
+  check(ew_comm_init(ids.front().data(), static_cast<int>(ch.members().size()), ch.index(), &c));
+  return c;
+}
+
+}  // namespace
+
+// Steady-state peer mapping of the group (DpGroup::premap / prepare_join):
+// the buffers a pull program reads on every participant, plus this rank's
+// verification arrays, mapped once.
+// A move lowered and bound ahead of its event (DpGroup::prepare_move).
+struct PreparedMove {
+  std::unique_ptr<ReshardPlan> rp;
+  VerifiedMove mv;
+  void* new_buf = nullptr;
+};
+
+// Steady-state peer mapping of the group (DpGroup::premap / prepare_join):
+// the buffers a pull program reads on every participant, plus this rank's
+// verification arrays, mapped once; the maps that turn the per-step
+// snapshot rows into source block sums; moves prepared ahead of events.
+struct DpGroup::Premap {
+  PeerBuffers peers;
+  void* old_buf = nullptr;
+  void* replica = nullptr;
+  const std::uint64_t* old_rows = nullptr;      // per-step snapshot rows (refreshed in place)
+  const std::uint64_t* replica_rows = nullptr;
+  std::vector<int> layout_members;  // the membership OLD and the replica are laid out over
+  ew_shardmap* old_map = nullptr;
+  ew_shardmap* rep_map = nullptr;
+  std::set<int> covers;  // ranks whose entries are in the table
+  std::int64_t n_words = 0;
+  std::unique_ptr<DevArray<std::uint64_t>> landed, old_blocks, rep_blocks;
+  std::unique_ptr<DevArray<std::uint32_t>> bad;
+  std::map<std::pair<int, std::vector<int>>, std::unique_ptr<PreparedMove>> moves;
+
+  explicit Premap(std::int64_t words) : n_words(words) {
+    landed = std::make_unique<DevArray<std::uint64_t>>(words);
+    old_blocks = std::make_unique<DevArray<std::uint64_t>>(words);
+    rep_blocks = std::make_unique<DevArray<std::uint64_t>>(words);
+    bad = std::make_unique<DevArray<std::uint32_t>>(4);
+  }
+  ~Premap() {
+    moves.clear();
+    peers.close();
+    ew_shardmap_free(old_map);
+    ew_shardmap_free(rep_map);
+  }
+  std::map<int, void*> mine() const {
+    return {{static_cast<int>(BufRole::Old), old_buf},
+            {static_cast<int>(BufRole::Replica), replica},
+            {kLanded, landed->p},
+            {kOldBlocks, old_blocks->p},
+            {kReplicaBlocks, rep_blocks->p}};
+  }
+  bool covers_all(const std::vector<int>& ranks) const {
+    for (int r : ranks)
+      if (!covers.count(r)) return false;
+    return true;
+  }
+  // this rank's source block sums of a move out of rp.src: from the
+  // snapshot rows when they describe these buffers and this layout, else a
+  // re-read of the buffers (stream-ordered either way)
+  void source_sums(const ReshardPlan& rp, int me, const RankBuffers& bufs, int owner,
+                   bool holder, std::int64_t block, ew_stream_t stream) const {
+    const std::int64_t nb = n_words / 2;
+    const bool same = layout_members == rp.old_members;
+    if (same && old_rows && old_map && old_buf == bufs.old_buf)
+      check(ew_rows_to_blocks(old_map, old_rows, old_blocks->p, nb, stream));
+    else
+      add_blocks(rp.src, me, bufs.old_buf, nullptr, old_blocks->p, nb, block, stream);
+    if (!holder) return;
+    if (same && replica_rows && rep_map && replica == bufs.replica)
+      check(ew_rows_to_blocks(rep_map, replica_rows, rep_blocks->p, nb, stream));
+    else
+      add_blocks(rp.src, owner, bufs.replica, nullptr, rep_blocks->p, nb, block, stream);
+  }
+};
+
+namespace {
+std::int64_t group_words(const std::vector<std::int64_t>& layer_bytes, std::int64_t block) {
+  std::int64_t total = 0;
+  for (std::int64_t b : layer_bytes) total += b;
+  return 2 * ((total + block - 1) / block);
+}
+}  // namespace
+
+void DpGroup::premap(const RankBuffers& bufs, const std::uint64_t* old_rows,
+                     const std::uint64_t* replica_rows) {
+  if (ch_ == nullptr) throw std::invalid_argument("premap: a joiner is mapped by prepare_join");
+  NvtxRange range("ew.premap");
+  auto pm = std::make_unique<Premap>(group_words(layer_bytes_, opt_.block_bytes));
+  pm->old_buf = bufs.old_buf;
+  pm->replica = bufs.replica;
+  pm->old_rows = old_rows;
+  pm->replica_rows = replica_rows;
+  pm->layout_members = members_;
+  const ReshardPlan self = ReshardPlan::build(layer_bytes_, members_, members_);
+  if (old_rows != nullptr) pm->old_map = make_map(shard_segments(self.src, me_), opt_.block_bytes);
+  if (replica_rows != nullptr && bufs.replica != nullptr && members_.size() > 1)
+    pm->rep_map = make_map(shard_segments(self.src, self.replica_of(me_)), opt_.block_bytes);
+  pm->peers.exchange(*ch_, pm->mine());
+  pm->covers.insert(members_.begin(), members_.end());
+  pm_ = std::move(pm);
+}
+
+void DpGroup::prepare_move(EventKind kind, const std::vector<int>& targets, void* new_buf) {
+  if (!pm_) throw std::logic_error("prepare_move: premap (members) / prepare_join (joiners) first");
+  if (kind == EventKind::FailSlow) throw std::invalid_argument("prepare_move: no move for FailSlow");
+  const bool join = kind == EventKind::ScaleOut;
+  std::vector<int> t(targets.begin(), targets.end());
+  std::sort(t.begin(), t.end());
+  t.erase(std::unique(t.begin(), t.end()), t.end());
+  std::vector<int> next;
+  if (join) {
+    next = members_;
+    next.insert(next.end(), t.begin(), t.end());
+    std::sort(next.begin(), next.end());
+  } else {
+    next = without(members_, std::set<int>(t.begin(), t.end()));
+    if (std::binary_search(t.begin(), t.end(), me_)) return;  // a departing member has no part
+  }
+  if (!pm_->covers_all(next) || !pm_->covers_all(members_))
+    throw std::invalid_argument("prepare_move: the participants are not mapped");
+  if (new_buf == nullptr) throw std::invalid_argument("prepare_move: NEW buffer required");
+  NvtxRange range("ew.prepare_move");
+  auto mv = std::make_unique<PreparedMove>();
+  mv->rp = std::make_unique<ReshardPlan>(ReshardPlan::build(layer_bytes_, members_, next));
+  mv->new_buf = new_buf;
+  pm_->peers.put(static_cast<int>(BufRole::New), me_, new_buf);
+  mv->mv.exec = std::make_unique<ReshardExecutor>(*mv->rp, me_, false, opt_.block_bytes);
+  mv->mv.exec->bind(pm_->peers, true);
+  mv->mv.wire(pm_->peers, *mv->rp, me_, pm_->n_words);
+  pm_->moves[{join ? 1 : 0, t}] = std::move(mv);
+}
+
 DpGroup::DpGroup(Channel& ch, const std::vector<std::int64_t>& layer_bytes, ew_comm* comm,
                  DpGroupOptions opt)
-    : ch_(ch), layer_bytes_(layer_bytes), members_(ch.members()), comm_(comm), opt_(opt) {
+    : store_(ch.store()), name_(ch.name()), me_(ch.me()), ch_(&ch), layer_bytes_(layer_bytes),
+      members_(ch.members()), comm_(comm), opt_(opt) {
   mb_sizes_.assign(members_.size(), opt_.per_slot_mbs);
   for (std::size_t i = 0; i < members_.size(); ++i)
     for (std::size_t j = i + 1; j < members_.size(); ++j)
       links_.insert(make_link(members_[i], members_[j]));
   if (opt_.prepare_comms && comm_ != nullptr) prepare();
+}
+
+DpGroup::DpGroup(Store& store, std::string group_name, const std::vector<std::int64_t>& layer_bytes,
+                 std::vector<int> members, int me, DpGroupOptions opt)
+    : store_(store), name_(std::move(group_name)), me_(me), ch_(nullptr),
+      layer_bytes_(layer_bytes), members_(std::move(members)), opt_(opt) {
+  std::sort(members_.begin(), members_.end());
+  if (members_.empty()) throw std::invalid_argument("a joiner needs the group's members");
+  if (index_of(members_, me_) >= 0)
+    throw std::invalid_argument("rank " + std::to_string(me_) + " is already a member");
+  // the members' link pool: the mesh over the current members (the DP mesh
+  // after any departures, communicator.cpp:74-81)
+  for (std::size_t i = 0; i < members_.size(); ++i)
+    for (std::size_t j = i + 1; j < members_.size(); ++j)
+      links_.insert(make_link(members_[i], members_[j]));
 }
 
 DpGroup::~DpGroup() {
@@ -1384,22 +1566,41 @@ DpGroup::~DpGroup() {
   // may be torn down on any subset of its members
   for (auto& [d, c] : prepared_comms_) ew_comm_abort(c);
   prepared_comms_.clear();
+  for (auto& [m, c] : standby_comms_) ew_comm_abort(c);
+  standby_comms_.clear();
   ew_comm_abort(comm_);
   for (auto it = retired_.rbegin(); it != retired_.rend(); ++it) ew_comm_abort(*it);
 }
 
 void DpGroup::prepare() {
-  if (comm_ == nullptr || members_.size() < 2) return;
+  std::vector<std::vector<int>> singles;
+  for (int d : members_) singles.push_back({d});
+  prepare(singles);
+}
+
+void DpGroup::prepare(const std::vector<std::vector<int>>& departures) {
+  if (comm_ == nullptr || members_.size() < 2 || ch_ == nullptr) return;
   NvtxRange range("ew.prepare_comms");
+  std::vector<std::vector<int>> sets;
+  for (std::vector<int> d : departures) {
+    std::sort(d.begin(), d.end());
+    d.erase(std::unique(d.begin(), d.end()), d.end());
+    if (d.empty() || d.size() >= members_.size())
+      throw std::invalid_argument("prepare: a departure set must leave survivors");
+    for (int x : d)
+      if (index_of(members_, x) < 0)
+        throw std::invalid_argument("prepare: member " + std::to_string(x) + " not in the group");
+    if (std::find(sets.begin(), sets.end(), d) == sets.end()) sets.push_back(d);
+  }
   for (auto& [d, c] : prepared_comms_) retired_.push_back(c);
   prepared_comms_.clear();
   for (auto it = retired_.rbegin(); it != retired_.rend(); ++it) ew_comm_abort(*it);
   retired_.clear();
-  const int me = ch_.me();
-  const int key = index_of(members_, me);
-  for (int d : members_) {
+  const int key = index_of(members_, me_);
+  for (const std::vector<int>& d : sets) {
+    const bool out = std::binary_search(d.begin(), d.end(), me_);
     ew_comm* c = nullptr;
-    check(ew_comm_split(comm_, me == d ? -1 : 0, key, opt_.share_comm_resources ? 1 : 0, &c));
+    check(ew_comm_split(comm_, out ? -1 : 0, key, opt_.share_comm_resources ? 1 : 0, &c));
     if (c != nullptr) prepared_comms_[d] = c;
   }
   // one collective on each (NCCL connects lazily): the repair at failure
@@ -1408,22 +1609,71 @@ void DpGroup::prepare() {
   // resources must never run concurrently, and the members of different
   // siblings would otherwise start them in different orders
   const DevArray<std::int64_t> one(1);
-  for (int d : members_) {
-    if (d != me) check(ew_allreduce_i64(prepared_comms_.at(d), one.p, 1, nullptr));
+  for (const std::vector<int>& d : sets) {
+    if (prepared_comms_.count(d)) check(ew_allreduce_i64(prepared_comms_.at(d), one.p, 1, nullptr));
     check(ew_device_sync());
-    ch_.barrier();
+    ch_->barrier();
   }
+}
+
+void DpGroup::prepare_join(const std::vector<int>& joiners) {
+  std::set<int> add(joiners.begin(), joiners.end());
+  if (add.empty()) throw std::invalid_argument("prepare_join: no joiners");
+  for (int j : add)
+    if (index_of(members_, j) >= 0)
+      throw std::invalid_argument("joining member " + std::to_string(j) + " is already in the group");
+  std::vector<int> next = members_;
+  next.insert(next.end(), add.begin(), add.end());
+  std::sort(next.begin(), next.end());
+  NvtxRange range("ew.prepare_join");
+  const int round = standby_rounds_[next]++;
+  Channel all(store_, name_ + "/standby" + std::to_string(round) + ":" + csv(members_) + ">" +
+                          csv(next), next, me_);
+  ew_comm* c = init_comm(all);
+  try {
+    const DevArray<std::int64_t> one(1);
+    check(ew_allreduce_i64(c, one.p, 1, nullptr));
+    check(ew_device_sync());
+  } catch (...) {
+    ew_comm_abort(c);
+    throw;
+  }
+  // the members' steady-state mapping grows to the joiners (when every
+  // member premapped): joiners map the members' buffers now
+  const bool joiner = add.count(me_) > 0;
+  const std::vector<std::string> flags = all.allgather(joiner ? "j" : (pm_ ? "p" : "-"));
+  bool members_mapped = true;
+  for (const std::string& f : flags) members_mapped = members_mapped && f != "-";
+  if (members_mapped) {
+    if (joiner) pm_ = std::make_unique<Premap>(group_words(layer_bytes_, opt_.block_bytes));
+    pm_->peers.exchange(all, pm_->mine());
+    pm_->covers.insert(next.begin(), next.end());
+  }
+  all.barrier();
+  const auto it = standby_comms_.find(next);
+  if (it != standby_comms_.end()) retired_.push_back(it->second);
+  standby_comms_[next] = c;
+}
+
+void DpGroup::commit_members(std::vector<int> next) {
+  members_ = std::move(next);
+  // later collectives of the group (prepare()) run over the new membership
+  own_ch_ = std::make_unique<Channel>(store_, name_ + "/members" + std::to_string(events_) + ":" +
+                                                  csv(members_), members_, me_);
+  ch_ = own_ch_.get();
 }
 
 MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
                            const RankBuffers& bufs, ew_stream_t stream, int step) {
-  if (kind == EventKind::ScaleOut || kind == EventKind::FailSlow)
-    throw std::invalid_argument("DpGroup::recover handles departures (FailStop / ScaleIn)");
+  if (kind == EventKind::ScaleOut) return admit(departed, bufs, stream, step);
+  if (kind == EventKind::FailSlow)
+    throw std::invalid_argument("DpGroup::recover handles FailStop / ScaleIn / ScaleOut");
+  if (ch_ == nullptr) throw std::invalid_argument("a joiner takes part in its ScaleOut first");
   std::set<int> gone(departed.begin(), departed.end());
   for (int d : gone)
     if (index_of(members_, d) < 0)
       throw std::invalid_argument("departed member " + std::to_string(d) + " is not in the group");
-  if (gone.count(ch_.me())) throw std::invalid_argument("a departed member does not recover");
+  if (gone.count(me_)) throw std::invalid_argument("a departed member does not recover");
   const std::vector<int> survivors = without(members_, gone);
   MttrEvent ev;
   ev.step = step;
@@ -1444,9 +1694,10 @@ MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
   const auto t_edit = Clock::now();
   ew_comm* new_comm = nullptr;
   if (comm_ != nullptr) {
-    if (gone.size() == 1 && prepared_comms_.count(*gone.begin())) {
-      new_comm = prepared_comms_.at(*gone.begin());
-      prepared_comms_.erase(*gone.begin());
+    const std::vector<int> key(gone.begin(), gone.end());
+    if (prepared_comms_.count(key)) {
+      new_comm = prepared_comms_.at(key);
+      prepared_comms_.erase(key);
       ev.phases["comm_prepared"] = 1.0;
     } else {
       std::vector<int> ranks;
@@ -1484,62 +1735,224 @@ MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
   if (prepared_ != nullptr && gone.size() == 1 && prepared_->members() == members_) {
     ev.verified = prepared_->recover(*gone.begin(), stream, &ev);
   } else {
-    Channel sc(ch_.store(), ch_.name() + "/event" + std::to_string(events_), survivors,
-               ch_.me());
+    Channel sc(store_, name_ + "/event" + std::to_string(events_), survivors, me_);
     const ReshardPlan rp = ReshardPlan::build(layer_bytes_, members_, survivors);
     const std::int64_t n_words = 2 * rp.n_blocks(opt_.block_bytes);
-    const DevArray<std::uint64_t> landed_buf(n_words), old_buf(n_words), rep_buf(n_words);
-    const DevArray<std::uint32_t> bad_buf(4);
-    std::uint64_t* landed = landed_buf.p;
-    std::uint64_t* old_blocks = old_buf.p;
-    std::uint64_t* rep_blocks = rep_buf.p;
-    std::uint32_t* bad = bad_buf.p;
-    {
-      const auto tp = Clock::now();
-      check(ew_memset_async(old_blocks, 0, n_words * 8, stream));
-      check(ew_memset_async(rep_blocks, 0, n_words * 8, stream));
-      add_blocks(rp.src, ch_.me(), bufs.old_buf, nullptr, old_blocks, n_words / 2,
-                 opt_.block_bytes, stream);
-      const int owner = rp.replica_of(ch_.me());
-      if (owner >= 0 && rp.failed.count(owner)) {
-        if (bufs.replica == nullptr)
-          throw std::invalid_argument("this rank holds the departed member's replica: pass it");
-        add_blocks(rp.src, owner, bufs.replica, nullptr, rep_blocks, n_words / 2,
-                   opt_.block_bytes, stream);
-      }
-      PeerBuffers peers;
-      std::map<int, void*> mine = {{static_cast<int>(BufRole::Old), bufs.old_buf},
-                                   {kLanded, landed}, {kOldBlocks, old_blocks},
-                                   {kReplicaBlocks, rep_blocks}};
-      if (owner >= 0 && rp.failed.count(owner)) mine[static_cast<int>(BufRole::Replica)] = bufs.replica;
-      peers.exchange(sc, mine);
-      peers.put(static_cast<int>(BufRole::New), ch_.me(), bufs.new_buf);
-      VerifiedMove mv;
-      mv.exec = std::make_unique<ReshardExecutor>(rp, ch_.me(), false, opt_.block_bytes);
-      mv.exec->bind(peers, true);
-      mv.wire(peers, rp, ch_.me(), n_words);
-      ev.phases["plan_s"] = rp.plan_seconds;
-      ev.phases["map_bind_s"] = seconds(tp, Clock::now());
-      sc.barrier();  // every survivor bound and its source sums ready
-      ev.verified = run_move(*mv.exec, *mv.verifier, landed, n_words, bad, nullptr, 0.0, sc,
-                             stream, &ev);
-      mv.exec.reset();
-      peers.close();
+    const int owner = rp.replica_of(me_);
+    const bool holder = owner >= 0 && rp.failed.count(owner) > 0;
+    if (holder && bufs.replica == nullptr)
+      throw std::invalid_argument("this rank holds the departed member's replica: pass it");
+    const auto tp = Clock::now();
+    // the steady-state mapping serves when every survivor passes the buffers
+    // it premapped (one store round)
+    const bool mine_mapped = pm_ && pm_->covers_all(survivors) && pm_->n_words == n_words &&
+                             pm_->old_buf == bufs.old_buf &&
+                             (!holder || pm_->replica == bufs.replica);
+    const bool mapped = sc.sum(mine_mapped ? 0 : 1) == 0;
+    std::unique_ptr<Premap> fresh;
+    if (!mapped) fresh = std::make_unique<Premap>(n_words);
+    Premap& pm = mapped ? *pm_ : *fresh;
+    check(ew_memset_async(pm.old_blocks->p, 0, n_words * 8, stream));
+    check(ew_memset_async(pm.rep_blocks->p, 0, n_words * 8, stream));
+    pm.source_sums(rp, me_, bufs, owner, holder, opt_.block_bytes, stream);
+    const auto ts = Clock::now();
+    ev.phases["sums_s"] = seconds(tp, ts);
+    if (!mapped) {
+      fresh->old_buf = bufs.old_buf;
+      fresh->replica = holder ? bufs.replica : nullptr;
+      fresh->peers.exchange(sc, fresh->mine());
     }
+    // a move prepared for exactly this departure set and NEW buffer skips
+    // the lowering and the program build
+    PreparedMove* ready = nullptr;
+    if (mapped) {
+      const auto it = pm_->moves.find({0, std::vector<int>(gone.begin(), gone.end())});
+      if (it != pm_->moves.end() && it->second->new_buf == bufs.new_buf) ready = it->second.get();
+    }
+    VerifiedMove local;
+    VerifiedMove& mv = ready ? ready->mv : local;
+    if (!ready) {
+      pm.peers.put(static_cast<int>(BufRole::New), me_, bufs.new_buf);
+      mv.exec = std::make_unique<ReshardExecutor>(rp, me_, false, opt_.block_bytes);
+      mv.exec->bind(pm.peers, true);
+      mv.wire(pm.peers, rp, me_, n_words);
+    }
+    ev.phases["plan_s"] = ready ? 0.0 : rp.plan_seconds;
+    ev.phases["map_bind_s"] = seconds(tp, Clock::now());
+    ev.phases["bind_s"] = seconds(ts, Clock::now());
+    ev.phases["premapped"] = mapped ? 1.0 : 0.0;
+    ev.phases["prepared"] = ready ? 1.0 : 0.0;
+    sc.barrier();  // every survivor bound and its source sums ready
+    ev.verified = run_move(*mv.exec, *mv.verifier, pm.landed->p, n_words, pm.bad->p, nullptr, 0.0,
+                           sc, stream, &ev);
   }
   ++events_;
   ev.remap_s = seconds(t2, Clock::now());
 
   // commit the new membership; the communicators of other departures were
   // built over the old membership
-  members_ = survivors;
   mb_sizes_ = next.per_slot_mbs;
+  commit_members(survivors);
   if (comm_ != nullptr) {
     // the parent and the other departures' communicators include the
     // departed member: retired (aborted later, never destroyed collectively)
     for (auto& [d, c] : prepared_comms_) retired_.push_back(c);
     prepared_comms_.clear();
+    for (auto& [m, c] : standby_comms_) retired_.push_back(c);
+    standby_comms_.clear();
     retired_.push_back(comm_);
+    comm_ = new_comm;
+  }
+  return ev;
+}
+
+MttrEvent DpGroup::admit(const std::vector<int>& joined, const RankBuffers& bufs,
+                         ew_stream_t stream, int step) {
+  std::set<int> add(joined.begin(), joined.end());
+  if (add.empty()) throw std::invalid_argument("ScaleOut without joiners");
+  for (int j : add)
+    if (index_of(members_, j) >= 0)
+      throw std::invalid_argument("joining member " + std::to_string(j) + " is already in the group");
+  const bool joiner = add.count(me_) > 0;
+  if (!joiner && index_of(members_, me_) < 0)
+    throw std::invalid_argument("rank " + std::to_string(me_) + " is neither a member nor a joiner");
+  if (bufs.new_buf == nullptr) throw std::invalid_argument("ScaleOut: pass the NEW buffer");
+  if (!joiner && bufs.old_buf == nullptr)
+    throw std::invalid_argument("ScaleOut: a member passes its OLD shard");
+  std::vector<int> next = members_;
+  next.insert(next.end(), add.begin(), add.end());
+  std::sort(next.begin(), next.end());
+  MttrEvent ev;
+  ev.step = step;
+  ev.kind = to_string(EventKind::ScaleOut);
+  NvtxRange range("ew.admit");
+  const auto t0 = Clock::now();
+  nvtxRangePushA("ew.comm_repair");
+
+  // comm repair: the groups after the event hold the joiners
+  // (comm_edit_time, sim.cpp:436-450); plan_edit adds the links incident to
+  // them that the pool lacks (communicator.cpp:65-70)
+  ElasticEvent e;
+  e.kind = EventKind::ScaleOut;
+  e.targets = std::vector<DeviceId>(add.begin(), add.end());
+  const EditPlan edit = plan_edit({CommGroup{"dp", next, GroupTopology::Mesh}}, e, links_);
+  for (const Link& l : edit.links_to_remove) links_.erase(l);
+  links_.insert(edit.links_to_add.begin(), edit.links_to_add.end());
+  const auto t_edit = Clock::now();
+  // rendezvous of members and joiners; the members hand the joiners the
+  // group's state: NCCL in use, event count, micro-batch sizes.  Everyone
+  // says whether it holds the standby communicator of this membership.
+  Channel all(store_, name_ + "/join" + std::to_string(step) + ":" + csv(members_) + ">" +
+                          csv(next), next, me_);
+  const bool has_standby = standby_comms_.count(next) > 0;
+  const std::string mine = std::string(has_standby ? "s" : "-") + ";" +
+                           (joiner ? std::string("j") : std::string(comm_ ? "1" : "0") + ";" +
+                                                            std::to_string(events_) + ";" +
+                                                            csv(mb_sizes_));
+  const std::vector<std::string> blobs = all.allgather(mine);
+  bool all_standby = true;
+  for (const std::string& b : blobs) all_standby = all_standby && !b.empty() && b[0] == 's';
+  const std::string& head = blobs[static_cast<std::size_t>(index_of(next, members_.front()))];
+  // head = "<s|->;<nccl>;<events>;<mb sizes>"
+  const std::size_t p1 = head.find(';', 2), p2 = head.find(';', p1 + 1);
+  if (head.size() < 4 || p1 == std::string::npos || p2 == std::string::npos)
+    throw std::runtime_error("ScaleOut: malformed group state from the members");
+  const bool nccl = head[2] == '1';
+  if (joiner) {
+    events_ = std::stoi(head.substr(p1 + 1, p2 - p1 - 1));
+    mb_sizes_ = parse_csv(head.substr(p2 + 1));
+  }
+  ew_comm* new_comm = nullptr;
+  if (nccl) {
+    if (all_standby) {
+      new_comm = standby_comms_.at(next);
+      standby_comms_.erase(next);
+      ev.phases["comm_prepared"] = 1.0;
+    } else {
+      new_comm = init_comm(all);
+      ev.phases["comm_prepared"] = 0.0;
+    }
+    const auto t_c = Clock::now();
+    const DevArray<std::int64_t> one(1);
+    check(ew_allreduce_i64(new_comm, one.p, 1, stream));
+    check(ew_stream_sync(stream));
+    ev.phases["comm_acquire_s"] = seconds(t_edit, t_c);  // rendezvous + communicator
+    ev.phases["first_collective_s"] = seconds(t_c, Clock::now());
+  }
+  ev.phases["plan_edit_s"] = seconds(t0, t_edit);
+  const auto t1 = Clock::now();
+  ev.comm_repair_s = seconds(t0, t1);
+  nvtxRangePop();
+  nvtxRangePushA("ew.reshape");
+
+  // dataflow: the global batch re-dealt over the grown group (dataflow.cpp:52-69)
+  MicrobatchAssignment mb;
+  for (std::size_t i = 0; i < members_.size(); ++i) mb.slots.push_back(static_cast<int>(i));
+  mb.per_slot_mbs = mb_sizes_;
+  mb.num_microbatches = opt_.num_microbatches;
+  std::vector<int> idx(next.size());
+  for (std::size_t i = 0; i < next.size(); ++i) idx[i] = static_cast<int>(i);
+  const MicrobatchAssignment nmb = reshard_microbatches(mb, idx);
+  const auto t2 = Clock::now();
+  ev.other_s = seconds(t1, t2);
+  nvtxRangePop();
+
+  // remap: the members' shards re-cut over the grown group; joiners only
+  // receive.  Conservation: the landed sums of every new member equal the
+  // source sums of every old member.
+  {
+    NvtxRange remap("ew.remap");
+    const auto tp = Clock::now();
+    const ReshardPlan rp = ReshardPlan::build(layer_bytes_, members_, next);
+    const std::int64_t n_words = 2 * rp.n_blocks(opt_.block_bytes);
+    const bool mine_mapped = pm_ && pm_->covers_all(next) && pm_->n_words == n_words &&
+                             (joiner || pm_->old_buf == bufs.old_buf);
+    const bool mapped = all.sum(mine_mapped ? 0 : 1) == 0;
+    std::unique_ptr<Premap> fresh;
+    if (!mapped) fresh = std::make_unique<Premap>(n_words);
+    Premap& pm = mapped ? *pm_ : *fresh;
+    check(ew_memset_async(pm.old_blocks->p, 0, n_words * 8, stream));
+    check(ew_memset_async(pm.rep_blocks->p, 0, n_words * 8, stream));
+    if (!joiner) pm.source_sums(rp, me_, bufs, -1, false, opt_.block_bytes, stream);
+    const auto ts = Clock::now();
+    ev.phases["sums_s"] = seconds(tp, ts);
+    if (!mapped) {
+      fresh->old_buf = joiner ? nullptr : bufs.old_buf;
+      fresh->peers.exchange(all, fresh->mine());
+    }
+    PreparedMove* ready = nullptr;
+    if (mapped) {
+      const auto it = pm_->moves.find({1, std::vector<int>(add.begin(), add.end())});
+      if (it != pm_->moves.end() && it->second->new_buf == bufs.new_buf) ready = it->second.get();
+    }
+    VerifiedMove local;
+    VerifiedMove& mv = ready ? ready->mv : local;
+    if (!ready) {
+      pm.peers.put(static_cast<int>(BufRole::New), me_, bufs.new_buf);
+      mv.exec = std::make_unique<ReshardExecutor>(rp, me_, false, opt_.block_bytes);
+      mv.exec->bind(pm.peers, true);
+      mv.wire(pm.peers, rp, me_, n_words);
+    }
+    ev.phases["plan_s"] = ready ? 0.0 : rp.plan_seconds;
+    ev.phases["map_bind_s"] = seconds(tp, Clock::now());
+    ev.phases["bind_s"] = seconds(ts, Clock::now());
+    ev.phases["premapped"] = mapped ? 1.0 : 0.0;
+    ev.phases["prepared"] = ready ? 1.0 : 0.0;
+    all.barrier();  // every participant bound and its source sums ready
+    ev.verified = run_move(*mv.exec, *mv.verifier, pm.landed->p, n_words, pm.bad->p, nullptr, 0.0,
+                           all, stream, &ev);
+  }
+  ++events_;
+  ev.remap_s = seconds(t2, Clock::now());
+
+  mb_sizes_ = nmb.per_slot_mbs;
+  commit_members(next);
+  if (nccl) {
+    // every communicator of the old membership is retired (the departure
+    // splits were built over it); the grown one serves the (d) reduce
+    for (auto& [d, c] : prepared_comms_) retired_.push_back(c);
+    prepared_comms_.clear();
+    if (comm_ != nullptr) retired_.push_back(comm_);
     comm_ = new_comm;
   }
   return ev;

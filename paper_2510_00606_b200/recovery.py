@@ -6,7 +6,9 @@ the C ABI); this module is its Python binding plus the ring-replica helpers.
 Per step the group keeps a same-GPU snapshot of every rank's ZeRO shard with
 checksum rows (kernel (a)) and a ring replica on the holder.  On a membership
 change (FailStop / ScaleIn) each surviving rank runs, in the reference's
-order:
+order (a ScaleOut — joiners from the free pool — runs the same three steps
+over members and joiners: grown communicator, micro-batches re-dealt, the
+members' shards re-cut over the grown group, DpGroup.admit):
 
   comm repair   plan_edit on the DP mesh (communicator.cpp:54-105), then the
                 NCCL communicator: a shrunk communicator prepared in steady
@@ -44,7 +46,8 @@ KIND_NAMES = {FAIL_STOP: "fail_stop", SCALE_IN: "scale_in", SCALE_OUT: "scale_ou
 
 _PHASES = ("plan_edit_s", "comm_acquire_s", "first_collective_s", "comm_prepared", "plan_s",
            "map_bind_s", "copy_s", "barrier_verify_s", "verdict_exchange_s",
-           "launch_to_verdict_s", "mismatched_block_words", "barrier_timeouts")
+           "launch_to_verdict_s", "mismatched_block_words", "barrier_timeouts", "premapped",
+           "sums_s", "bind_s", "prepared")
 
 
 @dataclass
@@ -394,17 +397,86 @@ class DpGroup:
         self._h = h
         self._prepared: Optional[PreparedRecovery] = None
 
+    @classmethod
+    def joiner(cls, layer_bytes: Sequence[int], members: Sequence[int], rank: int,
+               group_name: str, per_slot_mbs: int = 4, num_microbatches: int = 32,
+               block_bytes: int = dev.DEFAULT_BLOCK_BYTES, store=None) -> "DpGroup":
+        """A rank outside the group (a device from the free pool) that joins
+        it at a ScaleOut: `members` are the group's current members,
+        `group_name` the members' group channel name (`DpGroup.name`).  It
+        learns the communicator, micro-batches and its shard in recover()."""
+        from .rendezvous import default_store
+        self = cls.__new__(cls)
+        self.layer_bytes = list(layer_bytes)
+        self.rank = rank
+        self.channel = None
+        self._store = store or default_store()
+        h = C.c_void_p()
+        m = sorted(int(x) for x in members)
+        check(lib.ew_dp_group_create_joiner(self._store.handle, group_name.encode(),
+                                            N.i64_array(self.layer_bytes), len(self.layer_bytes),
+                                            N.int_array(m), len(m), int(rank), int(per_slot_mbs),
+                                            int(num_microbatches), int(block_bytes), C.byref(h)))
+        self._h = h
+        self._prepared = None
+        return self
+
+    @property
+    def name(self) -> str:
+        """The group channel's name (what a joiner passes to DpGroup.joiner)."""
+        return self.channel.name
+
+    def prepare_join(self, joiners: Sequence[int]) -> None:
+        """Steady state before an expected ScaleOut: the grown communicator
+        over members + joiners, built and warmed now (members and joiners)."""
+        j = list(joiners)
+        check(lib.ew_dp_group_prepare_join(self._h, N.int_array(j), len(j)))
+
+    def premap(self, bufs, old_rows=None, replica_rows=None) -> None:
+        """Steady state: map every member's OLD shard and replica once, so an
+        event planned at failure time (a departure set, a ScaleOut) maps
+        nothing on its critical path (members; joiners in prepare_join).
+        old_rows / replica_rows: the per-step snapshot rows of those buffers
+        (refreshed in place), the event's source block sums."""
+        p = lambda t: C.c_void_p(t.data_ptr() if t is not None else None)  # noqa: E731
+        check(lib.ew_dp_group_premap(self._h, p(bufs.old), p(bufs.replica), p(old_rows),
+                                     p(replica_rows)))
+
+    def prepare_move(self, kind: int, targets: Sequence[int], new: torch.Tensor) -> None:
+        """Steady state, local: this rank's verified program for one expected
+        event (departure set, or the joiners of a ScaleOut) into `new`."""
+        t = list(targets)
+        check(lib.ew_dp_group_prepare_move(self._h, int(kind), N.int_array(t), len(t),
+                                           C.c_void_p(new.data_ptr() if new is not None
+                                                      else None)))
+
+    def admit(self, joiners: Sequence[int], bufs, step: int = 0, stream=None) -> MttrEvent:
+        """ScaleOut: members (bufs.old = shard, bufs.new) and joiners (bufs.new)
+        all call it; returns this rank's measured MttrEvent."""
+        return self.recover(joiners, bufs, step=step, kind=SCALE_OUT, stream=stream)
+
     def attach(self, prepared: Optional[PreparedRecovery]) -> None:
         self._prepared = prepared
         check(lib.ew_dp_group_attach(self._h, prepared._h if prepared is not None else None))
 
-    def prepare(self) -> None:
-        """Steady state after a change: rebuild the per-departure communicators."""
-        check(lib.ew_dp_group_prepare(self._h))
+    def prepare(self, departures: Optional[Sequence[Sequence[int]]] = None) -> None:
+        """Steady state after a change: rebuild the per-departure
+        communicators — one per single departure, or one per given set of
+        members leaving together (collective over the members)."""
+        if departures is None:
+            check(lib.ew_dp_group_prepare(self._h))
+            return
+        flat, offs = [], [0]
+        for d in departures:
+            flat += [int(x) for x in d]
+            offs.append(len(flat))
+        check(lib.ew_dp_group_prepare_sets(self._h, N.int_array(flat or [0]), N.int_array(offs),
+                                           len(departures)))
 
     def recover(self, departed: Sequence[int], bufs=None, step: int = 0,
                 kind: int = FAIL_STOP, stream=None) -> MttrEvent:
-        """Run the DP recovery for `departed` on this (surviving) rank.
+        """Run the DP recovery for `departed` on this (surviving) rank
+        (kind SCALE_OUT: `departed` are the joiners, see admit()).
         `bufs` (reshard.RankBuffers: old / replica / new) are used when no
         prepared recovery is attached (planning at failure time)."""
         p = lambda t: C.c_void_p(t.data_ptr() if t is not None else None)  # noqa: E731

@@ -357,6 +357,85 @@ def _worker(rank, world, port, result_dir):
                 int(bits.item()) == f
             report["shrunk size"] = shrunk.size
         dist.barrier()
+        mark("rejoin")
+        # the departed device rejoins (ScaleOut, sim.cpp:608,676-677): a
+        # standby communicator over members + joiner prepared in steady
+        # state, then the join (grown communicator looked up, micro-batches
+        # re-dealt, shards re-cut, verified); re-prepare the departure splits
+        # over the grown group; the same device leaves again (prepared split)
+        # and rejoins without a standby (ncclCommInitRank at the event)
+        from paper_2510_00606_b200.fabric import FAIL_STOP
+        from paper_2510_00606_b200.reshard import RankBuffers
+        everyone = list(range(world))
+        rpj = ReshardPlan.build(cfg.layer_bytes, survivors, everyone)
+        jg = DpGroup.joiner(cfg.layer_bytes, survivors, rank, group.name) if rank == drop \
+            else group
+        jg.prepare_join([drop])
+        new_j = dev.empty_bytes(rpj.dst.shard_bytes(rank))
+        ev = jg.admit([drop], RankBuffers(bufs.new if rank != drop else None, None, new_j), step=2)
+        n = rpj.dst.shard_bytes(rank)
+        exp = dev.empty_bytes(n)
+        dev.fill_synthetic(shard_map(rpj.dst, rank), exp, 5)
+        report["rejoin verified"] = ev.verified
+        report["rejoin bytes"] = bool(torch.equal(new_j[:n], exp[:n]))
+        report["rejoin by the standby communicator"] = ev.phases.get("comm_prepared") == 1.0
+        report["rejoin members"] = jg.members == everyone
+        report["rejoin comm size"] = jg.comm is not None and jg.comm.size == world
+        jg.prepare()
+        holder = everyone[everyone.index(drop) - 1]
+        rep_d = None
+        if rank == holder:
+            rep_d = dev.empty_bytes(rpj.dst.shard_bytes(drop))
+            dev.fill_synthetic(shard_map(rpj.dst, drop), rep_d, 5)
+        # steady state: map, snapshot rows as the source sums, the program
+        # for this departure bound ahead
+        jm = shard_map(rpj.dst, rank)
+        j_rows = jm.new_row_sums()
+        dev.checksum(jm, new_j, j_rows)
+        d_rows = None
+        if rep_d is not None:
+            dm = shard_map(rpj.dst, drop)
+            d_rows = dm.new_row_sums()
+            dev.checksum(dm, rep_d, d_rows)
+        new2 = dev.empty_bytes(rp.dst.shard_bytes(rank)) if rank != drop else None
+        jg.premap(RankBuffers(new_j, rep_d, None), j_rows, d_rows)
+        jg.prepare_move(FAIL_STOP, [drop], new2)
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank != drop:
+            ev = jg.recover([drop], RankBuffers(new_j, rep_d, new2), step=3)
+            report["second departure premapped"] = ev.phases.get("premapped") == 1.0
+            report["second departure program prepared"] = ev.phases.get("prepared") == 1.0
+            n = rp.dst.shard_bytes(rank)
+            exp = dev.empty_bytes(n)
+            dev.fill_synthetic(shard_map(rp.dst, rank), exp, 5)
+            report["second departure verified"] = ev.verified
+            report["second departure by a prepared split"] = ev.phases.get("comm_prepared") == 1.0
+            report["second departure bytes"] = bool(torch.equal(new2[:n], exp[:n]))
+            old4 = new2
+        else:
+            old4 = None
+        dist.barrier()
+        jg2 = DpGroup.joiner(cfg.layer_bytes, survivors, rank, group.name) if rank == drop \
+            else jg
+        new4 = dev.empty_bytes(rpj.dst.shard_bytes(rank))
+        ev = jg2.admit([drop], RankBuffers(old4, None, new4), step=4)
+        n = rpj.dst.shard_bytes(rank)
+        exp = dev.empty_bytes(n)
+        dev.fill_synthetic(shard_map(rpj.dst, rank), exp, 5)
+        report["rejoin without standby verified"] = ev.verified
+        report["rejoin without standby bytes"] = bool(torch.equal(new4[:n], exp[:n]))
+        report["rejoin without standby: fresh communicator"] = \
+            ev.phases.get("comm_prepared") == 0.0 and jg2.comm is not None and \
+            jg2.comm.size == world
+        t = torch.ones(4, dtype=torch.int64, device="cuda")
+        jg2.comm.allreduce_i64(t)
+        torch.cuda.synchronize()
+        report["grown communicator sums over all"] = int(t[0].item()) == world
+        dist.barrier()
+        if rank == drop:
+            jg.close()
+            jg2.close()
         group.close()   # the group owns the communicators (parent and splits)
         mark("peer reduce")
         # the same reduce fused with its collective over peer memory (no NCCL)

@@ -156,20 +156,61 @@ def _worker(rank, world, port, out_dir, scale):
         holds = rp.replica_of(rank) in gone
         bufs = RankBuffers(live, replica if holds else None,
                            dev.empty_bytes(rp.dst.shard_bytes(rank)) if rank in survivors else None)
+        grp.premap(RankBuffers(live, replica, None))  # steady state: no IPC at the event
         dist.barrier()
         if rank in survivors:
             try:
-                grp.recover([1], bufs, kind=SCALE_OUT)
-                rep["scale-out rejected"] = False
+                grp.recover([survivors[0]], bufs, kind=SCALE_OUT)
+                rep["scale-out of a member rejected"] = False
             except ValueError:
-                rep["scale-out rejected"] = True
+                rep["scale-out of a member rejected"] = True
             ev = grp.recover(gone, bufs, step=9, kind=SCALE_IN)
             n = rp.dst.shard_bytes(rank)
             exp = _fill_expected(dev, shard_map, rp.dst, rank, 31, n)
             rep["two departures verified"] = ev.verified
             rep["two departures bytes"] = bool(torch.equal(bufs.new[:n], exp[:n]))
             rep["two departures kind"] = ev.kind == "scale_in"
+            rep["two departures used the steady-state mapping"] = ev.phases.get("premapped") == 1.0
         dist.barrier()
+
+        # ---- ...and rejoin (ScaleOut, config C's 6 -> 8): the departed
+        # processes come back as joiners from the free pool; members re-cut
+        # their shards over the grown group, joiners only receive
+        rpj = ReshardPlan.build(cfg.layer_bytes, survivors, members)
+        new_j = dev.empty_bytes(rpj.dst.shard_bytes(rank))
+        if rank in gone:
+            g2 = DpGroup.joiner(cfg.layer_bytes, survivors, rank, grp.name)
+            ev = g2.admit(gone, RankBuffers(None, None, new_j), step=10)
+        else:
+            g2 = grp
+            ev = g2.admit(gone, RankBuffers(bufs.new, None, new_j), step=10)
+        n = rpj.dst.shard_bytes(rank)
+        exp = _fill_expected(dev, shard_map, rpj.dst, rank, 31, n)
+        rep["rejoin verified"] = ev.verified
+        rep["rejoin bytes"] = bool(torch.equal(new_j[:n], exp[:n]))
+        rep["rejoin kind"] = ev.csv_row(0).startswith("0,10,0,scale_out,")
+        rep["rejoin members"] = g2.members == members
+        rep["rejoin mapped at the event"] = ev.phases.get("premapped") == 0.0
+        rep["rejoin microbatches conserve the batch"] = sum(g2.mb_sizes) == 4 * world
+        # the grown group recovers a later departure (channels of the new
+        # membership, event counters agreed with the joiners)
+        d3 = members[-1]
+        rp3 = ReshardPlan.build(cfg.layer_bytes, members, [m for m in members if m != d3])
+        holder3 = members[members.index(d3) - 1]  # SnapshotRing::backed_up_by
+        rep3 = None
+        if rank == holder3:
+            rep3 = _fill_expected(dev, shard_map, rpj.dst, d3, 31, rpj.dst.shard_bytes(d3))
+        dist.barrier()
+        if rank != d3:
+            new3 = dev.empty_bytes(rp3.dst.shard_bytes(rank))
+            ev = g2.recover([d3], RankBuffers(new_j, rep3, new3), step=11, kind=FAIL_STOP)
+            n = rp3.dst.shard_bytes(rank)
+            exp = _fill_expected(dev, shard_map, rp3.dst, rank, 31, n)
+            rep["departure after rejoin verified"] = ev.verified
+            rep["departure after rejoin bytes"] = bool(torch.equal(new3[:n], exp[:n]))
+        dist.barrier()
+        if g2 is not grp:
+            g2.close()
         grp.close()
 
         # ---- staged in-place reshard (C++ InPlaceExecutor): departures and a rejoin
