@@ -1629,30 +1629,40 @@ void DpGroup::prepare_join(const std::vector<int>& joiners) {
   const int round = standby_rounds_[next]++;
   Channel all(store_, name_ + "/standby" + std::to_string(round) + ":" + csv(members_) + ">" +
                           csv(next), next, me_);
-  ew_comm* c = init_comm(all);
-  try {
-    const DevArray<std::int64_t> one(1);
-    check(ew_allreduce_i64(c, one.p, 1, nullptr));
-    check(ew_device_sync());
-  } catch (...) {
-    ew_comm_abort(c);
-    throw;
-  }
-  // the members' steady-state mapping grows to the joiners (when every
-  // member premapped): joiners map the members' buffers now
+  // what the members run: a NCCL communicator (then the joiners need the
+  // grown one) and a steady-state mapping (then the joiners join it)
   const bool joiner = add.count(me_) > 0;
-  const std::vector<std::string> flags = all.allgather(joiner ? "j" : (pm_ ? "p" : "-"));
-  bool members_mapped = true;
-  for (const std::string& f : flags) members_mapped = members_mapped && f != "-";
+  const std::vector<std::string> flags =
+      all.allgather(joiner ? "j" : std::string(comm_ ? "n" : "-") + (pm_ ? "p" : "-"));
+  bool nccl = true, members_mapped = true;
+  for (const std::string& f : flags) {
+    if (f == "j") continue;
+    nccl = nccl && f[0] == 'n';
+    members_mapped = members_mapped && f[1] == 'p';
+  }
+  ew_comm* c = nullptr;
+  if (nccl) {
+    c = init_comm(all);
+    try {
+      const DevArray<std::int64_t> one(1);
+      check(ew_allreduce_i64(c, one.p, 1, nullptr));
+      check(ew_device_sync());
+    } catch (...) {
+      ew_comm_abort(c);
+      throw;
+    }
+  }
   if (members_mapped) {
     if (joiner) pm_ = std::make_unique<Premap>(group_words(layer_bytes_, opt_.block_bytes));
     pm_->peers.exchange(all, pm_->mine());
     pm_->covers.insert(next.begin(), next.end());
   }
   all.barrier();
-  const auto it = standby_comms_.find(next);
-  if (it != standby_comms_.end()) retired_.push_back(it->second);
-  standby_comms_[next] = c;
+  if (c != nullptr) {
+    const auto it = standby_comms_.find(next);
+    if (it != standby_comms_.end()) retired_.push_back(it->second);
+    standby_comms_[next] = c;
+  }
 }
 
 void DpGroup::commit_members(std::vector<int> next) {

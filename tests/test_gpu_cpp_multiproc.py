@@ -38,7 +38,7 @@ def driver():
     return BIN
 
 
-def _run(driver, world, drop, devices, nccl=False, scale="0.004"):
+def _run(driver, world, drop, devices, nccl=False, scale="0.004", rejoin=False):
     port = _port()
     procs = []
     for r in range(world):
@@ -46,6 +46,8 @@ def _run(driver, world, drop, devices, nccl=False, scale="0.004"):
                "--drop", str(drop), "--device", str(devices[r]), "--scale", scale]
         if nccl:
             cmd.append("--nccl")
+        if rejoin:
+            cmd.append("--rejoin")
         procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
                                       text=True))
     outs = []
@@ -63,12 +65,15 @@ def _run(driver, world, drop, devices, nccl=False, scale="0.004"):
 @pytest.mark.timeout(600)
 @pytest.mark.parametrize("drop", [0, 3])
 def test_cpp_driver_four_processes_one_gpu(driver, drop):
-    outs = _run(driver, 4, drop, [0, 0, 0, 0])
+    outs = _run(driver, 4, drop, [0, 0, 0, 0], rejoin=drop == 3)
     for r, (rc, o, e) in enumerate(outs):
         assert rc == 0, (r, o, e)
         if r != drop:
             assert "verified=1 bytes=1" in o, o
             assert f"rank {r} 0,1,0,fail_stop," in o, o
+        if drop == 3:  # ...and the departed process rejoins (ScaleOut), C++ only
+            assert f"rank {r} rejoin 1,2,0,scale_out," in o, o
+            assert "verified=1 bytes=1 members=1 prepared=1" in o, o
 
 
 @pytest.mark.timeout(600)
@@ -76,8 +81,11 @@ def test_cpp_driver_one_process_per_gpu_nccl(driver):
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs (one NCCL rank per GPU)")
-    outs = _run(driver, n, n - 1, list(range(n)), nccl=True, scale="0.01")
+    outs = _run(driver, n, n - 1, list(range(n)), nccl=True, scale="0.01", rejoin=True)
     for r, (rc, o, e) in enumerate(outs):
         assert rc == 0, (r, o, e)
         if r != n - 1:
             assert "verified=1 bytes=1" in o, o
+        # the rejoin over the standby grown NCCL communicator
+        assert f"rank {r} rejoin 1,2,0,scale_out," in o, o
+        assert "verified=1 bytes=1 members=1 prepared=1" in o, o

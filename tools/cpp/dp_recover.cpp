@@ -14,16 +14,23 @@
 //      communicator lookup + first collective, micro-batch reshape, the
 //      verified copy, device barrier, conservation over peer memory;
 //   4. each survivor checks its NEW bytes against the regenerated target
-//      layout and prints its mttr.csv row.
+//      layout and prints its mttr.csv row;
+//   5. with --rejoin, the departed process comes back from the free pool
+//      (ScaleOut): it builds a joiner-side DpGroup on the same store; in
+//      steady state the survivors premap their new shards, everyone
+//      prepares the grown communicator (NCCL) and its verified program; the
+//      join re-cuts the shards over the grown group; every rank checks its
+//      bytes and prints its scale_out mttr.csv row.
 //
 //   dp_recover --rank R --world N [--port P] [--host H] [--device D]
-//              [--scale S] [--drop d] [--nccl]
+//              [--scale S] [--drop d] [--nccl] [--rejoin]
 // Exit code 0 iff verified and the bytes match on this rank.
 #include <cuda_runtime.h>
 
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -84,6 +91,7 @@ int main(int argc, char** argv) {
   const double scale = std::atof(arg(argc, argv, "--scale", "0.01"));
   const int drop = std::atoi(arg(argc, argv, "--drop", "1"));
   const bool use_nccl = flag(argc, argv, "--nccl");
+  const bool rejoin = flag(argc, argv, "--rejoin");
   if (rank < 0 || world < 2 || rank >= world || drop < 0 || drop >= world) {
     std::fprintf(stderr, "usage: dp_recover --rank R --world N [--drop d] [--nccl] ...\n");
     return 2;
@@ -159,6 +167,44 @@ int main(int argc, char** argv) {
         cuda(cudaDeviceSynchronize(), "sync");
         cudaFree(one);
       }
+    }
+    if (rejoin) {
+      // the departed device returns from the free pool (ScaleOut)
+      std::vector<int> survivors;
+      for (int m : members)
+        if (m != drop) survivors.push_back(m);
+      const b200::ReshardPlan back = b200::ReshardPlan::build(layer_bytes, survivors, members);
+      const std::int64_t n_back = b200::shard_bytes(back.dst, rank);
+      DeviceBuffer grown(n_back);
+      std::unique_ptr<b200::DpGroup> joiner;
+      b200::DpGroup* g = &group;
+      b200::RankBuffers bufs;
+      bufs.new_buf = grown.p;
+      if (rank == drop) {
+        joiner = std::make_unique<b200::DpGroup>(*store, "dp", layer_bytes, survivors, rank, gopt);
+        g = joiner.get();
+      } else {
+        bufs.old_buf = prepared.new_buf();  // the shard recovered above
+        g->premap(bufs);                    // steady state after the departure
+      }
+      g->prepare_join({drop});
+      g->prepare_move(EventKind::ScaleOut, {drop}, grown.p);
+      const b200::MttrEvent ev = g->recover({drop}, EventKind::ScaleOut, bufs, nullptr, 2);
+      DeviceBuffer expect(n_back);
+      fill(back.dst, rank, expect.p, seed, nullptr, nullptr);
+      std::vector<unsigned char> a(static_cast<std::size_t>(n_back)), b(a.size());
+      cuda(cudaMemcpy(a.data(), grown.p, a.size(), cudaMemcpyDeviceToHost), "D2H");
+      cuda(cudaMemcpy(b.data(), expect.p, b.size(), cudaMemcpyDeviceToHost), "D2H");
+      const bool bytes_ok = a == b;
+      const bool grown_ok = g->members() == members;
+      std::printf("rank %d rejoin %s verified=%d bytes=%d members=%d prepared=%d copy_ms=%.3f\n",
+                  rank, b200::mttr_csv_row(1, ev).c_str(), ev.verified ? 1 : 0, bytes_ok ? 1 : 0,
+                  grown_ok ? 1 : 0,
+                  ev.phases.count("prepared") ? static_cast<int>(ev.phases.at("prepared")) : -1,
+                  ev.phases.count("copy_s") ? ev.phases.at("copy_s") * 1e3 : -1.0);
+      if (!(ev.verified && bytes_ok && grown_ok)) status = 1;
+      b200::Channel done(*store, "dp-rejoined", members, rank);
+      done.barrier();  // the joiner's mappings outlive every peer's reads
     }
     std::fflush(stdout);
     b200::Channel all(*store, "dp-exit", members, rank);
