@@ -624,8 +624,11 @@ class DpGroup {
   // store); otherwise the event maps as before.  old_rows / replica_rows:
   // the per-step snapshot's checksum rows of those buffers (device arrays
   // the caller refreshes in place every step); the event then takes its
-  // source block sums from them instead of re-reading the shards.
-  // Collective over the members.
+  // source block sums from them instead of re-reading the shards.  The
+  // buffers must stay allocated until the next premap or the group's end
+  // (peers hold IPC mappings of them; a buffer freed and reallocated at the
+  // same address would be read stale — verification on arrival then fails
+  // the event rather than passing wrong bytes).  Collective over the members.
   void premap(const RankBuffers& bufs, const std::uint64_t* old_rows = nullptr,
               const std::uint64_t* replica_rows = nullptr);
   // Steady state, local: lower and bind this rank's verified pull program
