@@ -81,12 +81,22 @@ __global__ void __launch_bounds__(256) mask_kernel(uint64_t seed, uint64_t sampl
                                                    int64_t n_elems, int64_t words_per_row,
                                                    uint64_t threshold, uint32_t* __restrict__ bits) {
   const int64_t total = n_samples * words_per_row;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < total;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = w / words_per_row;
-    const int64_t col = w - row * words_per_row;
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t w = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (w >= total) return;
+  // (row, col) advanced by the grid stride: one 64-bit division per thread,
+  // not one per word (a 64-bit divide is ~5 % of a word's 160-product budget)
+  int64_t row = w / words_per_row, col = w - row * words_per_row;
+  const int64_t srow = stride / words_per_row, scol = stride - srow * words_per_row;
+  // the lane product of round 0 is the same for every word of the launch
+  Stream s = make_stream(seed, sample_lo, lane);
+  for (; w < total; w += stride, row += srow, col += scol) {
+    if (col >= words_per_row) {
+      col -= words_per_row;
+      ++row;
+    }
     // sample ids wrap mod 2^64 like the reference's uint64 RngKey::sample_id
-    const Stream s = make_stream(seed, sample_lo + static_cast<uint64_t>(row), lane);
+    s.sample = sample_lo + static_cast<uint64_t>(row);
     const int64_t e0 = col * 32;
     const int nvalid = static_cast<int>(min((int64_t)32, n_elems - e0));
     uint32_t word = 0;
