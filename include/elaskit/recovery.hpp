@@ -614,7 +614,9 @@ class DpGroup {
   // Steady state before an expected ScaleOut (standby devices): build and
   // warm the grown communicator over members ∪ joiners now, so the join's
   // comm repair is a lookup; when the members premapped, the joiners map
-  // the members' buffers now too.  Collective over members and joiners.
+  // the members' buffers now too.  Collective over members and joiners;
+  // calls pair up in order per grown membership (the n-th call of a member
+  // meets the n-th call of the joiners' group objects for that membership).
   void prepare_join(const std::vector<int>& joiners);
   // Steady state: map every member's OLD shard and replica (what a pull
   // program reads) and the verification arrays once, so an event planned at

@@ -410,6 +410,7 @@ class DpGroup:
         self.layer_bytes = list(layer_bytes)
         self.rank = rank
         self.channel = None
+        self._name = group_name
         self._store = store or default_store()
         h = C.c_void_p()
         m = sorted(int(x) for x in members)
@@ -424,7 +425,7 @@ class DpGroup:
     @property
     def name(self) -> str:
         """The group channel's name (what a joiner passes to DpGroup.joiner)."""
-        return self.channel.name
+        return self.channel.name if self.channel is not None else self._name
 
     def prepare_join(self, joiners: Sequence[int]) -> None:
         """Steady state before an expected ScaleOut: the grown communicator
