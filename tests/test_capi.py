@@ -73,3 +73,29 @@ def test_shardmap_rejects_bad_segments_without_gpu():
         N.check(N.lib.ew_shardmap_create(bad, 2, 65536, C.byref(h)))
     with pytest.raises(N.InvalidArgument):
         N.check(N.lib.ew_shardmap_create(bad, 1, 1000, C.byref(h)))  # not a power of two
+
+
+def test_dp_group_membership_entry_points_validate_without_gpu():
+    """ScaleOut / departure-set entry points reject bad arguments before any
+    device or store call (joiner groups, prepared sets, premap, prepared
+    moves, the event kinds recover accepts)."""
+    h = C.c_void_p()
+    lb = (C.c_int64 * 2)(1 << 20, 1 << 20)
+    members = (C.c_int * 2)(0, 1)
+    with pytest.raises(N.InvalidArgument):  # no store
+        N.check(N.lib.ew_dp_group_create_joiner(None, b"dp", lb, 2, members, 2, 2, 4, 32, 65536,
+                                                C.byref(h)))
+    one = (C.c_int * 1)(3)
+    offs = (C.c_int * 2)(0, 1)
+    with pytest.raises(N.InvalidArgument):
+        N.check(N.lib.ew_dp_group_prepare_join(None, one, 1))
+    with pytest.raises(N.InvalidArgument):
+        N.check(N.lib.ew_dp_group_prepare_sets(None, one, offs, 1))
+    with pytest.raises(N.InvalidArgument):
+        N.check(N.lib.ew_dp_group_premap(None, None, None, None, None))
+    with pytest.raises(N.InvalidArgument):
+        N.check(N.lib.ew_dp_group_prepare_move(None, 3, one, 1, None))
+    ev = N.MttrEventC()
+    with pytest.raises(N.InvalidArgument):  # NULL group (a ScaleOut, kind 3)
+        N.check(N.lib.ew_dp_group_recover(None, one, 1, 3, None, None, None, 0, None,
+                                          C.byref(ev)))
