@@ -364,7 +364,7 @@ def _worker(rank, world, port, result_dir):
         # re-dealt, shards re-cut, verified); re-prepare the departure splits
         # over the grown group; the same device leaves again (prepared split)
         # and rejoins without a standby (ncclCommInitRank at the event)
-        from paper_2510_00606_b200.fabric import FAIL_STOP
+        from paper_2510_00606_b200.fabric import FAIL_STOP, SCALE_IN
         from paper_2510_00606_b200.reshard import RankBuffers
         everyone = list(range(world))
         rpj = ReshardPlan.build(cfg.layer_bytes, survivors, everyone)
@@ -433,6 +433,30 @@ def _worker(rank, world, port, result_dir):
         torch.cuda.synchronize()
         report["grown communicator sums over all"] = int(t[0].item()) == world
         dist.barrier()
+        if world >= 4:
+            # two non-adjacent members leave together: their shrunk
+            # communicator was prepared as a set (ncclCommSplit in steady state)
+            pair = [1, 3]
+            keep = [r for r in everyone if r not in pair]
+            rp5 = ReshardPlan.build(cfg.layer_bytes, everyone, keep)
+            jg2.prepare([pair])
+            owner5 = rp5.replica_of(rank)
+            rep5 = None
+            if owner5 in pair:  # this rank holds a departing member's replica
+                rep5 = dev.empty_bytes(rpj.dst.shard_bytes(owner5))
+                dev.fill_synthetic(shard_map(rpj.dst, owner5), rep5, 5)
+            dist.barrier()
+            if rank in keep:
+                new5 = dev.empty_bytes(rp5.dst.shard_bytes(rank))
+                ev = jg2.recover(pair, RankBuffers(new4, rep5, new5), step=5, kind=SCALE_IN)
+                n = rp5.dst.shard_bytes(rank)
+                exp = dev.empty_bytes(n)
+                dev.fill_synthetic(shard_map(rp5.dst, rank), exp, 5)
+                report["pair departure verified"] = ev.verified
+                report["pair departure bytes"] = bool(torch.equal(new5[:n], exp[:n]))
+                report["pair departure by a prepared set split"] = \
+                    ev.phases.get("comm_prepared") == 1.0 and jg2.comm.size == len(keep)
+            dist.barrier()
         if rank == drop:
             jg.close()
             jg2.close()
@@ -517,3 +541,7 @@ def test_multi_gpu_reshard_comm_reduce(world, tmp_path):
         if r != world - 1:
             assert rep["shrunk size"] == world - 1
             assert rep["recovery verified by checksums"] is True
+        # the rejoin / second departure / rejoin sequence ran on every rank
+        assert rep.get("rejoin verified") is True and rep.get("rejoin without standby verified")
+        if world >= 4 and r in (0, 2):
+            assert rep.get("pair departure by a prepared set split") is True

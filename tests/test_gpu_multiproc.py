@@ -156,7 +156,10 @@ def _worker(rank, world, port, out_dir, scale):
         holds = rp.replica_of(rank) in gone
         bufs = RankBuffers(live, replica if holds else None,
                            dev.empty_bytes(rp.dst.shard_bytes(rank)) if rank in survivors else None)
-        grp.premap(RankBuffers(live, replica, None))  # steady state: no IPC at the event
+        # steady state: IPC mapping, the per-step snapshot rows as the source
+        # sums, and this rank's program for the expected pair bound ahead
+        grp.premap(RankBuffers(live, replica, None), rows, rep_rows)
+        grp.prepare_move(SCALE_IN, gone, bufs.new)
         dist.barrier()
         if rank in survivors:
             try:
@@ -171,6 +174,7 @@ def _worker(rank, world, port, out_dir, scale):
             rep["two departures bytes"] = bool(torch.equal(bufs.new[:n], exp[:n]))
             rep["two departures kind"] = ev.kind == "scale_in"
             rep["two departures used the steady-state mapping"] = ev.phases.get("premapped") == 1.0
+            rep["two departures launched the prepared program"] = ev.phases.get("prepared") == 1.0
         dist.barrier()
 
         # ---- ...and rejoin (ScaleOut, config C's 6 -> 8): the departed
