@@ -403,7 +403,7 @@ def run_reshard(args, rank, world, out):
     import torch
     import torch.distributed as dist
     from paper_2510_00606_b200 import configs, device as dev
-    from paper_2510_00606_b200.recovery import DpGroup, PreparedRecovery
+    from paper_2510_00606_b200.recovery import DpGroup, FailureDetector, PreparedRecovery
     from paper_2510_00606_b200.reshard import ReshardExecutor, ReshardPlan, shard_map
 
     # start from a clean caching allocator: a cudaFree forced by an earlier
@@ -528,15 +528,28 @@ def run_reshard(args, rank, world, out):
     t_prep = time.perf_counter() - t0
     grp.attach(prep)
     t_prep_comm, t_prep = max_over_ranks([t_prep_comm, t_prep], world)
+    # failure detection (the reference charges a constant detect_s of 50 ms,
+    # presets.hpp:63): heartbeats every 1 ms, 20 ms of silence fails a member;
+    # the departing rank goes silent and the survivors' verdict starts the
+    # recovery
+    det = FailureDetector(f"bench{world}", 1e-3, 0.02)
     torch.cuda.synchronize()
     barrier(world)
+    time.sleep(0.05)
+    detect_s, detected = 0.0, True
+    if rank == drop:
+        det.stop_beating()
+    else:
+        dead, detect_s = det.wait(30.0)
+        detected = dead == [drop]
     fields = ("comm_repair_s", "other_s", "remap_s")
     phases = ("plan_edit_s", "comm_acquire_s", "first_collective_s", "copy_s",
               "barrier_verify_s", "verdict_exchange_s")
     if rank != drop:
         ev = grp.recover([drop], step=1)
+        ev.detect_s = detect_s
         vals = [getattr(ev, k) for k in fields] + [ev.phases.get(k, 0.0) for k in phases] + \
-               [ev.total_s()]
+               [ev.total_s() - ev.detect_s, ev.detect_s, ev.total_s()]
         verified = ev.verified
         n = prep.plans[drop].dst.shard_bytes(rank)
         exp = dev.empty_bytes(n)
@@ -545,9 +558,9 @@ def run_reshard(args, rank, world, out):
         del exp
         csv = ev.csv_row(0)
     else:
-        vals, verified, csv = [0.0] * (len(fields) + len(phases) + 1), True, ""
+        vals, verified, csv = [0.0] * (len(fields) + len(phases) + 3), True, ""
     vals = max_over_ranks(vals, world)
-    mt = dict(zip(fields + phases + ("total_s",), vals))
+    mt = dict(zip(fields + phases + ("total_s", "detect_s", "with_detect_s"), vals))
     res["mttr"] = {
         "what": "measured critical path of one FailStop of rank "
                 f"{drop}: DpGroup.recover (C++), max over survivors",
@@ -555,6 +568,13 @@ def run_reshard(args, rank, world, out):
         "reshape_ms": round(mt["other_s"] * 1e3, 3),
         "remap_ms": round(mt["remap_s"] * 1e3, 3),
         "total_ms": round(mt["total_s"] * 1e3, 3),
+        "detect_ms": round(mt["detect_s"] * 1e3, 3),
+        "total_with_detection_ms": round(mt["with_detect_s"] * 1e3, 3),
+        "detection": {"heartbeat_period_ms": 1.0, "timeout_ms": 20.0,
+                      "departed_rank_detected_by_all": all_ranks_true(detected, world),
+                      "note": "detect = time from the silent rank's last heartbeat to the "
+                              "survivors' verdict (FailureDetector, C++); total_ms excludes it, "
+                              "as the reference's 50 ms detect_s constant is separate"},
         "phases_ms": {k[:-2]: round(mt[k] * 1e3, 3) for k in phases},
         "verified_by_checksums_and_bytes": all_ranks_true(verified, world),
         "comm_repair_path": "prepared shrunk communicator (ncclCommSplit in steady state) "
@@ -565,6 +585,7 @@ def run_reshard(args, rank, world, out):
     if rank == 0:
         res["mttr"]["mttr_csv_rank0_row"] = csv
     barrier(world)
+    det.close()
     grp.close()
 
     # baseline: the NCCL communicator repaired at failure time (ncclCommShrink

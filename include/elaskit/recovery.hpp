@@ -31,12 +31,14 @@
 //                        one buffer, phases behind device-side barriers
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <functional>
 #include <map>
 #include <memory>
 #include <set>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "elaskit/b200.hpp"
@@ -422,6 +424,56 @@ class HostImages {
   std::map<int, std::int64_t> bytes_, slot_;
   std::map<int, Segment> segs_;
   std::int64_t next_epoch_ = -1;
+};
+
+// ------------------------------------------------------ failure detection
+
+// Heartbeat failure detector for the processes of one node's DP group (the
+// reference's detection is the constant detect_s, presets.hpp:63, used at
+// sim.cpp:601; the paper omits its agent).  Each member's beat thread proves
+// its device still executes work — a 4-byte H2D copy on a private stream
+// (a copy engine: the job's long kernels do not delay it), then a stream
+// synchronise — and only then publishes (beat count, CLOCK_MONOTONIC time)
+// in its slot of a node-shared POSIX shm segment; a member whose slot stops
+// advancing for timeout_s is failed (a dead process, or a live one whose
+// device no longer completes work).  Watching reads host memory only: no
+// CUDA call touches a failed peer.  detect_s of a verdict = time from the
+// failed member's last heartbeat to the verdict (an upper bound on the time
+// since it failed).
+struct DetectorOptions {
+  double period_s = 0.001;   // beat interval
+  double timeout_s = 0.02;   // silence that fails a member
+};
+
+class FailureDetector {
+ public:
+  // Collective over `ch` (segment creation and attach); starts beating.
+  FailureDetector(Channel& ch, const std::string& tag, DetectorOptions opt = {});
+  ~FailureDetector();
+  FailureDetector(const FailureDetector&) = delete;
+  FailureDetector& operator=(const FailureDetector&) = delete;
+
+  // Members silent for more than timeout_s now (ascending), with the age of
+  // each one's last heartbeat.
+  std::vector<int> failed(std::vector<double>* silence_s = nullptr) const;
+  // Block until at least one member fails or max_wait_s passes; returns the
+  // failed members and *detect_s (seconds from the first failed member's
+  // last heartbeat to this verdict).
+  std::vector<int> wait_for_failure(double max_wait_s, double* detect_s) const;
+  // Stop this member's beats (fault injection: a silent member).
+  void stop_beating();
+
+ private:
+  void beat_loop();
+  std::vector<int> members_;
+  int me_;
+  std::string name_;
+  DetectorOptions opt_;
+  void* shm_ = nullptr;
+  std::size_t shm_bytes_ = 0;
+  bool owner_ = false;
+  std::atomic<bool> stop_{false};
+  std::thread beater_;
 };
 
 // ------------------------------------------------- (d) over peer memory

@@ -663,6 +663,21 @@ int ew_dp_group_members(const ew_dp_group* g, int* out, int cap, int* n);
 int ew_dp_group_microbatches(const ew_dp_group* g, int* out, int cap, int* n);
 void ew_dp_group_free(ew_dp_group* g);
 
+/* Heartbeat failure detector of a node's DP group (recovery.hpp
+ * FailureDetector): collective create over the channel; each member beats
+ * every period_s once its GPU completed a tiny piece of work; a member
+ * silent for timeout_s is failed.  wait: up to max_wait_s for a failure;
+ * *n = 0 if none; *detect_s = seconds from the failed member's last beat to
+ * the verdict.  stop: this member stops beating (fault injection). */
+typedef struct ew_detector ew_detector;
+int ew_detector_create(ew_channel* ch, const char* tag, double period_s, double timeout_s,
+                       ew_detector** out);
+int ew_detector_failed(const ew_detector* d, int* out, int cap, int* n);
+int ew_detector_wait(const ew_detector* d, double max_wait_s, int* out, int cap, int* n,
+                     double* detect_s);
+int ew_detector_stop(ew_detector* d);
+void ew_detector_free(ew_detector* d);
+
 /* Staged in-place reshard executor (config D): collective over a channel of
  * old + new members; buf holds OLD on entry and NEW on exit. */
 typedef struct ew_inplace_exec ew_inplace_exec;

@@ -318,6 +318,11 @@ _sig("ew_dp_group_comm", i32, vp, P(vp))
 _sig("ew_dp_group_members", i32, vp, P(i32), i32, P(i32))
 _sig("ew_dp_group_microbatches", i32, vp, P(i32), i32, P(i32))
 _sig("ew_dp_group_free", None, vp)
+_sig("ew_detector_create", i32, vp, C.c_char_p, f64, f64, P(vp))
+_sig("ew_detector_failed", i32, vp, P(i32), i32, P(i32))
+_sig("ew_detector_wait", i32, vp, f64, P(i32), i32, P(i32), P(f64))
+_sig("ew_detector_stop", i32, vp)
+_sig("ew_detector_free", None, vp)
 _sig("ew_inplace_exec_create", i32, vp, P(i64), i32, P(i32), i32, P(i32), i32, vp, vp, i64, i64,
      i32, i32, i32, i64, f64, P(vp))
 _sig("ew_inplace_exec_launch", i32, vp, vp, vp)

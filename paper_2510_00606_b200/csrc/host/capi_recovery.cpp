@@ -43,6 +43,9 @@ struct ew_prepared {
 struct ew_dp_group {
   std::unique_ptr<DpGroup> g;
 };
+struct ew_detector {
+  std::unique_ptr<elaskit::b200::FailureDetector> d;
+};
 struct ew_inplace_exec {
   std::unique_ptr<InPlaceExecutor> x;
 };
@@ -492,6 +495,54 @@ int ew_dp_group_microbatches(const ew_dp_group* g, int* out, int cap, int* n) {
 }
 
 void ew_dp_group_free(ew_dp_group* g) { delete g; }
+
+// -------------------------------------------------------- failure detector
+
+int ew_detector_create(ew_channel* ch, const char* tag, double period_s, double timeout_s,
+                       ew_detector** out) {
+  return guarded([&]() -> int {
+    if (ch == nullptr || tag == nullptr || out == nullptr)
+      return set_error(EW_ERR_INVALID_ARGUMENT, "ew_detector_create: bad arguments");
+    elaskit::b200::DetectorOptions opt;
+    opt.period_s = period_s;
+    opt.timeout_s = timeout_s;
+    *out = new ew_detector{std::make_unique<elaskit::b200::FailureDetector>(*ch->c, tag, opt)};
+    return EW_OK;
+  });
+}
+
+static int copy_members(const std::vector<int>& f, int* out, int cap, int* n) {
+  *n = static_cast<int>(f.size());
+  if (*n > cap) return set_error(EW_ERR_CAPACITY, "member buffer too small");
+  std::copy(f.begin(), f.end(), out);
+  return EW_OK;
+}
+
+int ew_detector_failed(const ew_detector* d, int* out, int cap, int* n) {
+  if (d == nullptr || n == nullptr || (cap > 0 && out == nullptr))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_detector_failed: bad arguments");
+  return copy_members(d->d->failed(), out, cap, n);
+}
+
+int ew_detector_wait(const ew_detector* d, double max_wait_s, int* out, int cap, int* n,
+                     double* detect_s) {
+  if (d == nullptr || n == nullptr || (cap > 0 && out == nullptr))
+    return set_error(EW_ERR_INVALID_ARGUMENT, "ew_detector_wait: bad arguments");
+  return guarded([&]() -> int {
+    double t = 0.0;
+    const std::vector<int> f = d->d->wait_for_failure(max_wait_s, &t);
+    if (detect_s) *detect_s = t;
+    return copy_members(f, out, cap, n);
+  });
+}
+
+int ew_detector_stop(ew_detector* d) {
+  if (d == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL detector");
+  d->d->stop_beating();
+  return EW_OK;
+}
+
+void ew_detector_free(ew_detector* d) { delete d; }
 
 // ------------------------------------------------------- in-place executor
 

@@ -23,6 +23,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cctype>
 #include <atomic>
 #include <cerrno>
 #include <chrono>
@@ -1155,6 +1156,149 @@ bool PeerReduce::timed_out() const {
   int t = 0;
   check(ew_peer_barrier_timed_out(barrier_, &t));
   return t != 0;
+}
+
+// -------------------------------------------------------- FailureDetector
+
+namespace {
+
+struct alignas(64) BeatSlot {
+  std::uint64_t beats;
+  std::int64_t t_ns;  // steady_clock (CLOCK_MONOTONIC) of the last beat
+};
+
+std::int64_t now_ns() {
+  return std::chrono::duration_cast<std::chrono::nanoseconds>(
+             Clock::now().time_since_epoch()).count();
+}
+
+std::string shm_safe(const std::string& s) {
+  std::string out;
+  for (char c : s) out += (std::isalnum(static_cast<unsigned char>(c)) ? c : '_');
+  return out;
+}
+
+}  // namespace
+
+FailureDetector::FailureDetector(Channel& ch, const std::string& tag, DetectorOptions opt)
+    : members_(ch.members()), me_(ch.me()), opt_(opt) {
+  if (opt_.period_s <= 0 || opt_.timeout_s <= opt_.period_s)
+    throw std::invalid_argument("FailureDetector: need 0 < period_s < timeout_s");
+  name_ = "/ew_hb_" + shm_safe(tag) + "_" + shm_safe(ch.name());
+  shm_bytes_ = sizeof(BeatSlot) * members_.size();
+  owner_ = ch.index() == 0;
+  if (owner_) {
+    ::shm_unlink(name_.c_str());  // a stale segment of an earlier run
+    const int fd = ::shm_open(name_.c_str(), O_CREAT | O_EXCL | O_RDWR, 0600);
+    if (fd < 0) throw std::runtime_error("shm_open(" + name_ + ") failed");
+    if (::ftruncate(fd, static_cast<off_t>(shm_bytes_)) != 0) {
+      ::close(fd);
+      ::shm_unlink(name_.c_str());
+      throw std::runtime_error("ftruncate(" + name_ + ") failed");
+    }
+    shm_ = ::mmap(nullptr, shm_bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    ::close(fd);
+    if (shm_ == MAP_FAILED) {
+      shm_ = nullptr;
+      ::shm_unlink(name_.c_str());
+      throw std::runtime_error("mmap(" + name_ + ") failed");
+    }
+    std::memset(shm_, 0, shm_bytes_);
+  }
+  ch.barrier();  // the segment exists
+  if (!owner_) {
+    const int fd = ::shm_open(name_.c_str(), O_RDWR, 0600);
+    if (fd < 0) throw std::runtime_error("shm_open(" + name_ + ") failed");
+    shm_ = ::mmap(nullptr, shm_bytes_, PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
+    ::close(fd);
+    if (shm_ == MAP_FAILED) {
+      shm_ = nullptr;
+      throw std::runtime_error("mmap(" + name_ + ") failed");
+    }
+  }
+  BeatSlot* slot = static_cast<BeatSlot*>(shm_) + ch.index();
+  __atomic_store_n(&slot->t_ns, now_ns(), __ATOMIC_RELEASE);
+  __atomic_store_n(&slot->beats, std::uint64_t{1}, __ATOMIC_RELEASE);
+  ch.barrier();  // every member has a first beat before anyone watches
+  int device = 0;
+  cuda_check(cudaGetDevice(&device), "cudaGetDevice");
+  beater_ = std::thread([this, device] {
+    cudaSetDevice(device);
+    beat_loop();
+  });
+}
+
+FailureDetector::~FailureDetector() {
+  stop_beating();
+  if (shm_ != nullptr) ::munmap(shm_, shm_bytes_);
+  if (owner_) ::shm_unlink(name_.c_str());
+}
+
+void FailureDetector::stop_beating() {
+  stop_ = true;
+  if (beater_.joinable()) beater_.join();
+}
+
+void FailureDetector::beat_loop() {
+  // a beat is published only after the device completed a 4-byte H2D copy
+  // issued for it (a copy engine, not an SM: a long kernel of the job does
+  // not delay beats; a device that stops executing work stops them)
+  cudaStream_t s = nullptr;
+  void* word = nullptr;
+  std::uint32_t* host = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMalloc(&word, 4) != cudaSuccess ||
+      cudaHostAlloc(reinterpret_cast<void**>(&host), 4, cudaHostAllocDefault) != cudaSuccess)
+    return;  // no beats: peers will fail this member, which cannot use its GPU
+  BeatSlot* slot = static_cast<BeatSlot*>(shm_) + index_of(members_, me_);
+  std::uint64_t n = 1;
+  const auto period = std::chrono::duration<double>(opt_.period_s);
+  while (!stop_) {
+    *host = static_cast<std::uint32_t>(n);
+    if (cudaMemcpyAsync(word, host, 4, cudaMemcpyHostToDevice, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      break;  // a failed device: stop beating
+    __atomic_store_n(&slot->t_ns, now_ns(), __ATOMIC_RELEASE);
+    __atomic_store_n(&slot->beats, ++n, __ATOMIC_RELEASE);
+    std::this_thread::sleep_for(period);
+  }
+  cudaFreeHost(host);
+  cudaFree(word);
+  cudaStreamDestroy(s);
+}
+
+std::vector<int> FailureDetector::failed(std::vector<double>* silence_s) const {
+  std::vector<int> out;
+  if (silence_s) silence_s->clear();
+  const std::int64_t now = now_ns();
+  const BeatSlot* slots = static_cast<const BeatSlot*>(shm_);
+  for (std::size_t i = 0; i < members_.size(); ++i) {
+    if (members_[i] == me_) continue;
+    const double age = static_cast<double>(now - __atomic_load_n(&slots[i].t_ns, __ATOMIC_ACQUIRE)) * 1e-9;
+    if (age > opt_.timeout_s) {
+      out.push_back(members_[i]);
+      if (silence_s) silence_s->push_back(age);
+    }
+  }
+  return out;
+}
+
+std::vector<int> FailureDetector::wait_for_failure(double max_wait_s, double* detect_s) const {
+  const auto t0 = Clock::now();
+  const auto poll = std::chrono::duration<double>(opt_.period_s / 4);
+  for (;;) {
+    std::vector<double> age;
+    const std::vector<int> f = failed(&age);
+    if (!f.empty()) {
+      if (detect_s) *detect_s = *std::max_element(age.begin(), age.end());
+      return f;
+    }
+    if (seconds(t0, Clock::now()) > max_wait_s) {
+      if (detect_s) *detect_s = 0.0;
+      return {};
+    }
+    std::this_thread::sleep_for(poll);
+  }
 }
 
 // ------------------------------------------------------------------ MTTR

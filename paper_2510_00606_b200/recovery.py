@@ -526,3 +526,53 @@ class DpGroup:
             self.close()
         except Exception:  # noqa: BLE001
             pass
+
+
+class FailureDetector:
+    """Heartbeat failure detector of a node's DP group — a binding of the C++
+    elaskit::b200::FailureDetector (ew_detector).  Each member beats every
+    `period_s` once its GPU completed a tiny piece of work, into a node-shared
+    shm slot; a member silent for `timeout_s` is failed.  The reference only
+    charges a constant detect_s (presets.hpp:63, sim.cpp:601); wait() returns
+    the measured one.  Collective over `group` (all members)."""
+
+    def __init__(self, tag: str = "dp", period_s: float = 1e-3, timeout_s: float = 0.02,
+                 group=None, channel: Optional[Channel] = None):
+        self.channel = channel or Channel.from_group(group, "hb")
+        h = C.c_void_p()
+        check(lib.ew_detector_create(self.channel.handle, tag.encode(), float(period_s),
+                                     float(timeout_s), C.byref(h)))
+        self._h = h
+
+    def failed(self):
+        out = N.int_array([0] * 1024)
+        n = C.c_int()
+        check(lib.ew_detector_failed(self._h, out, 1024, C.byref(n)))
+        return list(out[:n.value])
+
+    def wait(self, max_wait_s: float):
+        """(failed members, detect_s): blocks until a member fails or
+        max_wait_s passes ([] then)."""
+        out = N.int_array([0] * 1024)
+        n = C.c_int()
+        t = C.c_double()
+        check(lib.ew_detector_wait(self._h, float(max_wait_s), out, 1024, C.byref(n),
+                                   C.byref(t)))
+        return list(out[:n.value]), t.value
+
+    def stop_beating(self) -> None:
+        check(lib.ew_detector_stop(self._h))
+
+    def close(self) -> None:
+        if getattr(self, "_h", None) is not None and self._h.value and lib is not None:
+            lib.ew_detector_free(self._h)
+            self._h = None
+        if getattr(self, "channel", None) is not None:
+            self.channel.close()
+            self.channel = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
