@@ -38,7 +38,7 @@ def driver():
     return BIN
 
 
-def _run(driver, world, drop, devices, nccl=False, scale="0.004", rejoin=False):
+def _run(driver, world, drop, devices, nccl=False, scale="0.004", rejoin=False, kill=False):
     port = _port()
     procs = []
     for r in range(world):
@@ -48,6 +48,8 @@ def _run(driver, world, drop, devices, nccl=False, scale="0.004", rejoin=False):
             cmd.append("--nccl")
         if rejoin:
             cmd.append("--rejoin")
+        if kill:
+            cmd.append("--kill")
         procs.append(subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE,
                                       text=True))
     outs = []
@@ -89,3 +91,26 @@ def test_cpp_driver_one_process_per_gpu_nccl(driver):
         # the rejoin over the standby grown NCCL communicator
         assert f"rank {r} rejoin 1,2,0,scale_out," in o, o
         assert "verified=1 bytes=1 members=1 prepared=1" in o, o
+
+
+@pytest.mark.timeout(600)
+def test_cpp_driver_killed_rank(driver):
+    """The departing process is SIGKILLed: the survivors' heartbeat detector
+    finds it and they recover without it (one GPU, and with NCCL one
+    process per GPU when there are >= 2 GPUs)."""
+    n = torch.cuda.device_count()
+    cases = [(4, [0, 0, 0, 0], False)]
+    if n >= 2:
+        cases.append((n, list(range(n)), True))
+    for world, devices, nccl in cases:
+        drop = world - 1
+        outs = _run(driver, world, drop, devices, nccl=nccl, kill=True)
+        for r, (rc, o, e) in enumerate(outs):
+            if r == drop:
+                assert rc == -9, (r, rc, e)
+                continue
+            assert rc == 0, (r, o, e)
+            assert "verified=1 bytes=1" in o, o
+            row = o.split(f"rank {r} ")[1].split()[0].split(",")
+            assert row[3] == "fail_stop" and 0.015 < float(row[4]) < 0.5, row  # detect_s
+

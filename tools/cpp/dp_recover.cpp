@@ -22,10 +22,17 @@
 //      join re-cuts the shards over the grown group; every rank checks its
 //      bytes and prints its scale_out mttr.csv row.
 //
+//   6. with --kill, the departing process is SIGKILLed instead of just
+//      leaving: the survivors' heartbeat FailureDetector finds it, and the
+//      recovery (no help from the dead process) records the measured
+//      detect_s in its mttr.csv row.
+//
 //   dp_recover --rank R --world N [--port P] [--host H] [--device D]
-//              [--scale S] [--drop d] [--nccl] [--rejoin]
+//              [--scale S] [--drop d] [--nccl] [--rejoin | --kill]
 // Exit code 0 iff verified and the bytes match on this rank.
 #include <cuda_runtime.h>
+#include <signal.h>
+#include <unistd.h>
 
 #include <cstdio>
 #include <cstdlib>
@@ -92,7 +99,9 @@ int main(int argc, char** argv) {
   const int drop = std::atoi(arg(argc, argv, "--drop", "1"));
   const bool use_nccl = flag(argc, argv, "--nccl");
   const bool rejoin = flag(argc, argv, "--rejoin");
-  if (rank < 0 || world < 2 || rank >= world || drop < 0 || drop >= world) {
+  const bool kill_drop = flag(argc, argv, "--kill");
+  if (rank < 0 || world < 2 || rank >= world || drop < 0 || drop >= world ||
+      (kill_drop && (drop == 0 || rejoin))) {  // rank 0 hosts the store
     std::fprintf(stderr, "usage: dp_recover --rank R --world N [--drop d] [--nccl] ...\n");
     return 2;
   }
@@ -140,11 +149,24 @@ int main(int argc, char** argv) {
     b200::PreparedRecovery prepared(ch, layer_bytes, live.p, static_cast<std::uint64_t*>(rows.p),
                                     replica.p, static_cast<std::uint64_t*>(rep_rows.p));
     group.attach(&prepared);
+    std::unique_ptr<b200::FailureDetector> detector;
+    if (kill_drop)
+      detector = std::make_unique<b200::FailureDetector>(ch, "dpr" + std::to_string(port));
     ch.barrier();
 
     int status = 0;
+    double detect_s = 0.0;
+    if (kill_drop) {
+      if (rank == drop) ::kill(::getpid(), SIGKILL);
+      const std::vector<int> dead = detector->wait_for_failure(60.0, &detect_s);
+      if (dead != std::vector<int>{drop}) {
+        std::fprintf(stderr, "rank %d: detector reported %zu failed members\n", rank, dead.size());
+        return 4;
+      }
+    }
     if (rank != drop) {
-      const b200::MttrEvent ev = group.recover({drop}, EventKind::FailStop, {}, nullptr, 1);
+      b200::MttrEvent ev = group.recover({drop}, EventKind::FailStop, {}, nullptr, 1);
+      ev.detect_s = detect_s;
       // bytes: NEW == the target layout's bytes of the synthetic state
       const b200::ReshardPlan& rp = prepared.plan(drop);
       const std::int64_t n_new = b200::shard_bytes(rp.dst, rank);
@@ -207,8 +229,12 @@ int main(int argc, char** argv) {
       done.barrier();  // the joiner's mappings outlive every peer's reads
     }
     std::fflush(stdout);
-    b200::Channel all(*store, "dp-exit", members, rank);
+    std::vector<int> alive;
+    for (int m : members)
+      if (!(kill_drop && m == drop)) alive.push_back(m);
+    b200::Channel all(*store, "dp-exit", alive, rank);
     all.barrier();  // nobody tears down mappings a peer may still read
+    if (kill_drop) std::_Exit(status);  // communicators with a dead member: no teardown
     return status;
   } catch (const std::exception& e) {
     std::fprintf(stderr, "rank %d: %s\n", rank, e.what());
