@@ -88,6 +88,7 @@ def _worker(rank, world, port, out_dir):
         # survivors only from here: nobody tears down mappings a peer reads
         Channel(default_store(), f"fi-exit{port}", [r for r in members if r != VICTIM],
                 rank).barrier()
+        det.close()  # stop beating; the segment's owner unlinks it
     except Exception as e:  # noqa: BLE001 - report, do not hang the survivors
         import traceback
         rep["error"] = repr(e) + "\n" + traceback.format_exc()[-2000:]

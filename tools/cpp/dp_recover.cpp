@@ -234,6 +234,7 @@ int main(int argc, char** argv) {
       if (!(kill_drop && m == drop)) alive.push_back(m);
     b200::Channel all(*store, "dp-exit", alive, rank);
     all.barrier();  // nobody tears down mappings a peer may still read
+    detector.reset();  // stop beating; the segment's owner unlinks it
     if (kill_drop) std::_Exit(status);  // communicators with a dead member: no teardown
     return status;
   } catch (const std::exception& e) {
