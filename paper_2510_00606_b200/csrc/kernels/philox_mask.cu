@@ -133,11 +133,19 @@ __global__ void uniform_kernel(uint64_t seed, uint64_t sample_lo, int64_t n_samp
                                int64_t n_elems, double* __restrict__ out) {
   const int64_t blocks_per_row = (n_elems + 3) / 4;
   const int64_t total = n_samples * blocks_per_row;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = t / blocks_per_row;
-    const int64_t blk = t - row * blocks_per_row;
-    const Stream s = make_stream(seed, sample_lo + static_cast<uint64_t>(row), lane);
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  int64_t t = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (t >= total) return;
+  // (row, blk) advanced by the grid stride, as in mask_kernel
+  int64_t row = t / blocks_per_row, blk = t - row * blocks_per_row;
+  const int64_t srow = stride / blocks_per_row, sblk = stride - srow * blocks_per_row;
+  Stream s = make_stream(seed, sample_lo, lane);
+  for (; t < total; t += stride, row += srow, blk += sblk) {
+    if (blk >= blocks_per_row) {
+      blk -= blocks_per_row;
+      ++row;
+    }
+    s.sample = sample_lo + static_cast<uint64_t>(row);
     uint64_t w[4];
     philox_block(s, static_cast<uint64_t>(blk + 1), w);
     for (int i = 0; i < 4; ++i) {
