@@ -2023,6 +2023,10 @@ MttrEvent DpGroup::admit(const std::vector<int>& joined, const RankBuffers& bufs
       standby_comms_.erase(next);
       ev.phases["comm_prepared"] = 1.0;
     } else {
+      if (has_standby) {  // not every participant built it: unusable
+        retired_.push_back(standby_comms_.at(next));
+        standby_comms_.erase(next);
+      }
       new_comm = init_comm(all);
       ev.phases["comm_prepared"] = 0.0;
     }
