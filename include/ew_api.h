@@ -627,8 +627,10 @@ void ew_prepared_free(ew_prepared* p);
  * 0 prepares the communicators, bit 1 builds them with splitShare (less
  * memory; NCCL then forbids concurrent use of siblings).  old_buf / replica /
  * new_buf are used when no prepared recovery is attached (planning at failure
- * time).  ScaleOut: `departed` lists the joiners; every member (old_buf =
- * its shard, new_buf) and every joiner (new_buf only) calls recover; a
+ * time).  ScaleOut (the reference's rejoin, sim.cpp:608,676-677 with
+ * comm_edit_time sim.cpp:436-450): `departed` lists the joiners; every
+ * member (old_buf = its shard, new_buf) and every joiner (new_buf only)
+ * calls recover; a
  * joiner's group comes from ew_dp_group_create_joiner (the members' group
  * channel name and current members, `me` outside them).
  * ew_dp_group_prepare_join: steady-state grown communicator over members +
@@ -664,7 +666,8 @@ int ew_dp_group_microbatches(const ew_dp_group* g, int* out, int cap, int* n);
 void ew_dp_group_free(ew_dp_group* g);
 
 /* Heartbeat failure detector of a node's DP group (recovery.hpp
- * FailureDetector): collective create over the channel; each member beats
+ * FailureDetector; replaces the reference's constant detect_s,
+ * presets.hpp:63 as charged at sim.cpp:601): collective create over the channel; each member beats
  * every period_s once its GPU completed a tiny piece of work; a member
  * silent for timeout_s is failed.  wait: up to max_wait_s for a failure;
  * *n = 0 if none; *detect_s = seconds from the failed member's last beat to
