@@ -586,7 +586,10 @@ class PreparedRecovery {
 
   // Survivors only, all of them: copy the departed member's share into NEW,
   // verify by conservation.  Returns the verdict; phases (seconds) in `ev`.
-  bool recover(int departed, ew_stream_t stream, MttrEvent* ev = nullptr);
+  // stale_snapshot: this rank's state is not of the event's step (counted
+  // into the verdict, which then fails)
+  bool recover(int departed, ew_stream_t stream, MttrEvent* ev = nullptr,
+               bool stale_snapshot = false);
   void* new_buf() const { return new_buf_; }
   std::int64_t new_bytes(int departed) const;
   const ReshardPlan& plan(int departed) const { return *plans_.at(departed); }
@@ -700,6 +703,12 @@ class DpGroup {
   // The same for the given departure sets (e.g. config C's two non-adjacent
   // members leaving together): one shrunk communicator per set.
   void prepare(const std::vector<std::vector<int>>& departures);
+  // The step whose state this member's OLD shard and replica hold — the
+  // snapshot ring's step_tag (param_fabric.hpp:42), documented to equal the
+  // current step but never checked by the reference.  Once set
+  // (>= 0), an event at another `step` counts this member as stale in the
+  // verdict: MttrEvent.verified is false, phases["stale_snapshots"] > 0.
+  void set_snapshot_step(std::int64_t step) { snapshot_step_ = step; }
   ew_comm* comm() const { return comm_; }
   const std::vector<int>& members() const { return members_; }
   const std::vector<int>& microbatch_sizes() const { return mb_sizes_; }
@@ -728,6 +737,7 @@ class DpGroup {
   DpGroupOptions opt_;
   PreparedRecovery* prepared_ = nullptr;
   int events_ = 0;
+  std::int64_t snapshot_step_ = -1;
 };
 
 // --------------------------------------------------------- in place (D)

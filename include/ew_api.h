@@ -569,6 +569,7 @@ typedef struct ew_mttr_event {
   double premapped; /* 1: the event used the group's steady-state peer mapping */
   double sums_s, bind_s; /* map_bind_s split: source block sums; lowering + program build */
   double prepared; /* 1: the event launched a program prepared in steady state */
+  double stale_snapshots; /* participants whose snapshot step differs from the event's */
 } ew_mttr_event;
 /* mttr.csv (reference sim.cpp:1119-1132): header line and one row, no '\n' */
 int ew_mttr_csv_header(char* buf, int64_t cap);
@@ -653,6 +654,9 @@ int ew_dp_group_premap(ew_dp_group* g, void* old_buf, void* replica, const uint6
                        const uint64_t* replica_rows);
 int ew_dp_group_prepare_move(ew_dp_group* g, int kind, const int* targets, int n, void* new_buf);
 int ew_dp_group_attach(ew_dp_group* g, ew_prepared* prepared);
+/* the step this member's OLD shard and replica hold (SnapshotRing step_tag,
+ * param_fabric.hpp:42); an event at another step fails the verdict */
+int ew_dp_group_set_snapshot_step(ew_dp_group* g, int64_t step);
 int ew_dp_group_prepare(ew_dp_group* g);
 /* prepared communicators for the given departure sets instead (set i =
  * members[offsets[i] .. offsets[i + 1]), n_sets + 1 offsets) */

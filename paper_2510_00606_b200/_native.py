@@ -273,7 +273,8 @@ class MttrEventC(C.Structure):
                     "lost_work_s", "plan_edit_s", "comm_acquire_s", "first_collective_s",
                     "comm_prepared", "plan_s", "map_bind_s", "copy_s", "barrier_verify_s",
                     "verdict_exchange_s", "launch_to_verdict_s", "mismatched_block_words",
-                    "barrier_timeouts", "premapped", "sums_s", "bind_s", "prepared")]
+                    "barrier_timeouts", "premapped", "sums_s", "bind_s", "prepared",
+                    "stale_snapshots")]
 
 
 STORE_SET_FN = C.CFUNCTYPE(i32, vp, C.POINTER(C.c_char), i64, C.POINTER(C.c_char), i64)
@@ -311,6 +312,7 @@ _sig("ew_dp_group_prepare_join", i32, vp, P(i32), i32)
 _sig("ew_dp_group_premap", i32, vp, vp, vp, vp, vp)
 _sig("ew_dp_group_prepare_move", i32, vp, i32, P(i32), i32, vp)
 _sig("ew_dp_group_attach", i32, vp, vp)
+_sig("ew_dp_group_set_snapshot_step", i32, vp, i64)
 _sig("ew_dp_group_prepare", i32, vp)
 _sig("ew_dp_group_prepare_sets", i32, vp, P(i32), P(i32), i32)
 _sig("ew_dp_group_recover", i32, vp, P(i32), i32, i32, vp, vp, vp, i32, vp, P(MttrEventC))

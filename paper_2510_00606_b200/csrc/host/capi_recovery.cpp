@@ -100,6 +100,7 @@ void to_c(const MttrEvent& ev, ew_mttr_event* out) {
   out->sums_s = ph("sums_s");
   out->bind_s = ph("bind_s");
   out->prepared = ph("prepared");
+  out->stale_snapshots = ph("stale_snapshots");
 }
 
 MttrEvent from_c(const ew_mttr_event& e) {
@@ -421,6 +422,12 @@ int ew_dp_group_prepare_move(ew_dp_group* g, int kind, const int* targets, int n
                        std::vector<int>(targets, targets + n), new_buf);
     return EW_OK;
   });
+}
+
+int ew_dp_group_set_snapshot_step(ew_dp_group* g, int64_t step) {
+  if (g == nullptr) return set_error(EW_ERR_INVALID_ARGUMENT, "NULL group");
+  g->g->set_snapshot_step(step);
+  return EW_OK;
 }
 
 int ew_dp_group_attach(ew_dp_group* g, ew_prepared* p) {

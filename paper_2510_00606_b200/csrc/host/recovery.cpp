@@ -1352,7 +1352,7 @@ struct VerifiedMove {
 bool run_move(const ReshardExecutor& exec, const BlockVerifier& verifier, std::uint64_t* landed,
               std::int64_t n_words,
               std::uint32_t* bad, ew_peer_barrier* barrier, double timeout_s, Channel& survivors,
-              ew_stream_t stream, MttrEvent* ev) {
+              ew_stream_t stream, MttrEvent* ev, bool stale_snapshot = false) {
   NvtxRange range("ew.remap.copy_verify");
   cudaEvent_t e[3];
   for (cudaEvent_t& x : e) cuda_check(cudaEventCreate(&x), "cudaEventCreate");
@@ -1376,8 +1376,11 @@ bool run_move(const ReshardExecutor& exec, const BlockVerifier& verifier, std::u
   if (barrier != nullptr) check(ew_peer_barrier_timed_out(barrier, &timed_out));
   const auto t1 = Clock::now();
   nvtxRangePushA("ew.remap.verdict");
+  // one verdict round: mismatched words, barrier timeouts, and members whose
+  // snapshot is not of the event's step (SnapshotRing::step_tag)
   const std::int64_t total = survivors.sum(static_cast<std::int64_t>(bad_host) +
-                                           (timed_out ? (std::int64_t{1} << 40) : 0));
+                                           (timed_out ? (std::int64_t{1} << 40) : 0) +
+                                           (stale_snapshot ? (std::int64_t{1} << 50) : 0));
   nvtxRangePop();
   const auto t2 = Clock::now();
   float copy_ms = 0.f, verify_ms = 0.f;
@@ -1390,7 +1393,8 @@ bool run_move(const ReshardExecutor& exec, const BlockVerifier& verifier, std::u
     ev->phases["verdict_exchange_s"] = seconds(t1, t2);
     ev->phases["launch_to_verdict_s"] = seconds(t0, t2);
     ev->phases["mismatched_block_words"] = static_cast<double>(total % (std::int64_t{1} << 40));
-    ev->phases["barrier_timeouts"] = static_cast<double>(total >> 40);
+    ev->phases["barrier_timeouts"] = static_cast<double>((total >> 40) & 1023);
+    ev->phases["stale_snapshots"] = static_cast<double>(total >> 50);
   }
   return total == 0;
 }
@@ -1495,13 +1499,14 @@ std::int64_t PreparedRecovery::new_bytes(int departed) const {
   return shard_bytes(plans_.at(departed)->dst, me_);
 }
 
-bool PreparedRecovery::recover(int departed, ew_stream_t stream, MttrEvent* ev) {
+bool PreparedRecovery::recover(int departed, ew_stream_t stream, MttrEvent* ev,
+                               bool stale_snapshot) {
   if (departed == me_) throw std::invalid_argument("the departed member does not recover itself");
   if (!plans_.count(departed))
     throw std::invalid_argument("member " + std::to_string(departed) + " is not in the group");
   const bool ok = run_move(*execs_.at(departed), *verifiers_.at(departed), landed_, n_words_,
                            bad_, barriers_.at(departed), opt_.barrier_timeout_s,
-                           *survivors_.at(departed), stream, ev);
+                           *survivors_.at(departed), stream, ev, stale_snapshot);
   if (ev != nullptr) {
     ev->phases["plan_s"] = 0.0;  // planned in steady state
     ev->phases["prepared"] = 1.0;
@@ -1886,8 +1891,11 @@ MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
   NvtxRange remap("ew.remap");
 
   // remap
+  // SnapshotRing::step_tag (param_fabric.hpp:42): the state a survivor moves
+  // must be the event's step; a mismatch fails the verdict
+  const bool stale = snapshot_step_ >= 0 && snapshot_step_ != step;
   if (prepared_ != nullptr && gone.size() == 1 && prepared_->members() == members_) {
-    ev.verified = prepared_->recover(*gone.begin(), stream, &ev);
+    ev.verified = prepared_->recover(*gone.begin(), stream, &ev, stale);
   } else {
     Channel sc(store_, name_ + "/event" + std::to_string(events_), survivors, me_);
     const ReshardPlan rp = ReshardPlan::build(layer_bytes_, members_, survivors);
@@ -1938,7 +1946,7 @@ MttrEvent DpGroup::recover(const std::vector<int>& departed, EventKind kind,
     ev.phases["prepared"] = ready ? 1.0 : 0.0;
     sc.barrier();  // every survivor bound and its source sums ready
     ev.verified = run_move(*mv.exec, *mv.verifier, pm.landed->p, n_words, pm.bad->p, nullptr, 0.0,
-                           sc, stream, &ev);
+                           sc, stream, &ev, stale);
   }
   ++events_;
   ev.remap_s = seconds(t2, Clock::now());
@@ -2097,8 +2105,9 @@ MttrEvent DpGroup::admit(const std::vector<int>& joined, const RankBuffers& bufs
     ev.phases["premapped"] = mapped ? 1.0 : 0.0;
     ev.phases["prepared"] = ready ? 1.0 : 0.0;
     all.barrier();  // every participant bound and its source sums ready
+    const bool stale = !joiner && snapshot_step_ >= 0 && snapshot_step_ != step;
     ev.verified = run_move(*mv.exec, *mv.verifier, pm.landed->p, n_words, pm.bad->p, nullptr, 0.0,
-                           all, stream, &ev);
+                           all, stream, &ev, stale);
   }
   ++events_;
   ev.remap_s = seconds(t2, Clock::now());

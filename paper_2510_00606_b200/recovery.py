@@ -47,7 +47,7 @@ KIND_NAMES = {FAIL_STOP: "fail_stop", SCALE_IN: "scale_in", SCALE_OUT: "scale_ou
 _PHASES = ("plan_edit_s", "comm_acquire_s", "first_collective_s", "comm_prepared", "plan_s",
            "map_bind_s", "copy_s", "barrier_verify_s", "verdict_exchange_s",
            "launch_to_verdict_s", "mismatched_block_words", "barrier_timeouts", "premapped",
-           "sums_s", "bind_s", "prepared")
+           "sums_s", "bind_s", "prepared", "stale_snapshots")
 
 
 @dataclass
@@ -455,6 +455,12 @@ class DpGroup:
         """ScaleOut: members (bufs.old = shard, bufs.new) and joiners (bufs.new)
         all call it; returns this rank's measured MttrEvent."""
         return self.recover(joiners, bufs, step=step, kind=SCALE_OUT, stream=stream)
+
+    def set_snapshot_step(self, step: int) -> None:
+        """The step this member's OLD shard and replica hold (the snapshot
+        ring's step_tag, param_fabric.hpp:42): an event at another step fails
+        its verdict (phases["stale_snapshots"])."""
+        check(lib.ew_dp_group_set_snapshot_step(self._h, int(step)))
 
     def attach(self, prepared: Optional[PreparedRecovery]) -> None:
         self._prepared = prepared

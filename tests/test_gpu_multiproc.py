@@ -145,6 +145,20 @@ def _worker(rank, world, port, out_dir, scale):
         dist.barrier()
         grp.close()
 
+        # ---- the snapshot ring's step tag is enforced: one survivor's state
+        # is of step 7 while the event is at step 8 -> every verdict fails
+        grp = DpGroup(cfg.layer_bytes, members, rank, None)
+        grp.set_snapshot_step(7 if rank == 0 else 8)
+        bufs = RankBuffers(live, replica if succ == drop else None,
+                           dev.empty_bytes(rp.dst.shard_bytes(rank)) if rank != drop else None)
+        dist.barrier()
+        if rank != drop:
+            ev = grp.recover([drop], bufs, step=8, kind=FAIL_STOP)
+            rep["stale snapshot fails the verdict"] = not ev.verified
+            rep["stale snapshot counted once"] = ev.phases.get("stale_snapshots") == 1.0
+        dist.barrier()
+        grp.close()
+
         # ---- two non-adjacent members leave at once (ScaleIn), planned at
         # failure time: integrity_check passes (their holders survive), the
         # copy sources both departed shards from their ring holders
